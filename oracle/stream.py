@@ -1,0 +1,405 @@
+"""Oracle Part 1 (bytes) — per-stage instruction streams and byte-exact replay.
+
+TEST INFRASTRUCTURE ONLY (see ``oracle/__init__.py``).
+
+Expands the compute orders of ``oracle.schedule`` into the instruction streams
+that ``tpipe_plan`` must emit (DESIGN.md §3 "instruction stream"), attaching
+to every instruction the buffers it allocates (at its start) and frees (at its
+end). Replaying a stage's stream in order gives the live bytes after every
+instruction boundary; its maximum is the stage's peak HBM bytes, which is
+order-determined (independent of durations, SURVEY D-16). The byte model
+ is the reading of N-2 for this build's kernels.
+
+Everything here is integer arithmetic, written out long-hand.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from collections import defaultdict
+
+from . import schedule as S
+
+FP32, BF16 = 0, 1
+
+
+@dataclass(frozen=True)
+class ModelDesc:
+    n_layers: int
+    hidden: int
+    n_heads: int
+    ffn_hidden: int
+    vocab: int
+    seq_len: int
+    micro_batch: int
+    dtype: int = BF16
+    layers_chunk: tuple = (0, 0)  # per-stage (chunk1, chunk2) layers; 0 = auto
+
+    @property
+    def es(self) -> int:
+        return 2 if self.dtype == BF16 else 4
+
+    @property
+    def tokens(self) -> int:
+        return self.seq_len * self.micro_batch
+
+
+def layers_per_chunk(d: ModelDesc, p: int, v: int):
+    """n = L/p layers per stage (p | L required). v=2: the extra layer of an odd
+    n goes to chunk 1. Override via d.layers_chunk."""
+    if d.n_layers % p:
+        raise ValueError("n_layers")
+    n = d.n_layers // p
+    if v == 1:
+        return (n,)
+    if d.layers_chunk[0] or d.layers_chunk[1]:
+        if sum(d.layers_chunk) != n or min(d.layers_chunk) < 1:
+            raise ValueError("layers_chunk")
+        return tuple(d.layers_chunk)
+    if n < 2:
+        raise ValueError("n_layers")
+    return ((n + 1) // 2, n // 2)
+
+
+def layer_params(d: ModelDesc) -> int:
+    h, f = d.hidden, d.ffn_hidden
+    ln = 2 * h
+    qkv = 3 * h * h + 3 * h
+    proj = h * h + h
+    fc1 = f * h + f
+    fc2 = h * f + h
+    return ln + qkv + proj + ln + fc1 + fc2
+
+
+def chunk_params(d: ModelDesc, p: int, v: int, s: int, c: int) -> int:
+    n = layers_per_chunk(d, p, v)[c - 1]
+    P = n * layer_params(d)
+    if s == 0 and c == 1:
+        P += d.vocab * d.hidden + d.seq_len * d.hidden          # wte, wpe
+    if s == p - 1 and c == v:
+        P += 2 * d.hidden + d.vocab * d.hidden                  # ln_f, lm head
+    return P
+
+
+def model_state_bytes(d: ModelDesc, P: int, offloaded: bool) -> int:
+    """bf16: weight 2 + fp32 grad 4 + fp32 master 4 + Adam m,v 8 = 18 B/param;
+    fp32: weight(=master) 4 + grad 4 + m,v 8 = 16 B/param.
+    T-Offload keeps only weight + grad on the device."""
+    if offloaded:
+        return P * (d.es + 4)
+    master = 4 if d.dtype == BF16 else 0
+    return P * (d.es + 4 + master + 8)
+
+
+def n_partials(M: int) -> int:
+    """Row blocks of 64 for deterministic column reductions."""
+    return -(-M // 64)
+
+
+def sizes(d: ModelDesc, p: int, v: int, s: int, c: int, full_recomp: bool = False):
+    """Byte model per (stage, chunk), DESIGN.md §4."""
+    M, h, a, f, V, es = d.tokens, d.hidden, d.n_heads, d.ffn_hidden, d.vocab, d.es
+    n = layers_per_chunk(d, p, v)[c - 1]
+    act = M * h * es
+    emb = (s == 0 and c == 1)
+    head = (s == p - 1 and c == v)
+    # per-layer stash: x_in, ln1 mean/rstd, qkv, attn out, lse, x_mid, ln2 stats, u
+    LS = M * h * es + 8 * M + 3 * M * h * es + M * h * es + 4 * a * M \
+        + M * h * es + 8 * M + M * f * es
+    head_stash = M * h * es + 8 * M + 4 * M       # x_f, ln_f stats, CE lse
+    if full_recomp:
+        stash = n * M * h * es                   # layer inputs only
+    else:
+        stash = n * LS
+    if not emb:
+        stash -= act                             # layer-0 input is the IN buffer
+    if head:
+        stash += head_stash
+    nb = n_partials(M)
+    ws_f = M * (h + f) * es
+    if head:
+        ws_f += M * h * es + 4 * M * V + 4 * M
+    ws_b = M * (2 * f + 8 * h) * es + 4 * a * M + 4 * nb * max(f, 3 * h)
+    if full_recomp:
+        ws_b += LS - M * h * es                  # one-layer recompute buffer
+    if head:
+        ws_b += 2 * M * h * es + 4 * M * V + M * V * es
+    if emb:
+        ws_b += 8 * M
+    return {
+        "act": act, "stash": stash, "ws_f": ws_f, "ws_b": ws_b,
+        "input_is_act": not emb, "has_output": not head,
+    }
+
+
+# --------------------------------------------------------------------------
+# instruction streams
+# --------------------------------------------------------------------------
+
+@dataclass
+class Instr:
+    kind: str                      # F B R RECV_ACT RECV_GRAD SEND_ACT SEND_GRAD SEND_WAIT
+                                   # OPT GRAD_D2H HOST_OPT W_H2D W_WAIT
+    chunk: int = 0
+    mb: int = 0
+    peer: int = -1
+    channel: tuple = ()
+    msg: int = -1                  # message index on channel
+    allocs: list = field(default_factory=list)   # (name, category, bytes)
+    frees: list = field(default_factory=list)    # names
+
+    def key(self):
+        return (self.kind, self.chunk, self.mb, self.peer, self.msg)
+
+
+STRATS = {
+    # name: (order strategy, v, recompute chunk-1 block-wise, layer-grouped full)
+    "tpipe": ("tpipe", 2, False, False),
+    "tpipe_trecomp": ("tpipe_trecomp", 2, True, False),
+    "1f1b": ("1f1b", 1, False, False),
+    "1f1b_full_recomp": ("1f1b_full_recomp", 1, False, True),
+}
+
+
+def build_streams(d: ModelDesc, p: int, m: int, strategy: str, k=None,
+                  window: int = 2, offload_model_state: bool = False):
+    """Per-stage instruction streams. Returns (streams, static)
+    where static[s] = list of (name, category, bytes) live for the whole step."""
+    ostrat, v, trecomp, full = STRATS[strategy]
+    if offload_model_state and v != 2:
+        raise ValueError("offload requires v=2")
+    orders = S.strategy_orders(ostrat, p, m, k=k)[0]
+    sz = {(s, c): sizes(d, p, v, s, c, full_recomp=full)
+          for s in range(p) for c in range(1, v + 1)}
+
+    static = []
+    for s in range(p):
+        st = []
+        for c in range(1, v + 1):
+            P = chunk_params(d, p, v, s, c)
+            off = offload_model_state and c == v
+            st.append((f"MS{c}", "model_state", model_state_bytes(d, P, off)))
+        if s == 0:
+            st.append(("TOKENS", "io", 4 * m * d.tokens))
+        if s == p - 1:
+            st.append(("TARGETS", "io", 4 * m * d.tokens + 4 * m))
+        static.append(st)
+
+    # message indices per channel on the sender side
+    streams = []
+    for s in range(p):
+        out = []
+        sent = defaultdict(int)          # channel -> messages produced so far
+        waited = defaultdict(int)        # channel -> messages waited
+        last_b = {c: max(op[2] for op in orders[s] if op[0] == "B" and op[1] == c)
+                  for c in range(1, v + 1)}
+        first_f = {c: min(op[2] for op in orders[s] if op[0] == "F" and op[1] == c)
+                   for c in range(1, v + 1)}
+        first_op_done = False
+        for op in orders[s]:
+            kind, c, i = op
+            z = sz[(s, c)]
+            msg = S.message_of(s, op, p, v)
+            # 1. send-window wait before the op producing message j+W
+            if msg is not None:
+                ch = msg[0]
+                j = sent[ch]
+                while waited[ch] <= j - window:
+                    jj = waited[ch]
+                    out.append(Instr("SEND_WAIT", channel=ch, peer=ch[2], msg=jj,
+                                     frees=[_msgbuf(ch, jj)]))
+                    waited[ch] += 1
+            # 2. receive before the consuming op
+            if offload_model_state and kind == "F" and c == v and i == first_f[v]:
+                out.append(Instr("W_WAIT", chunk=v))
+            if kind == "F" and z["input_is_act"]:
+                src = _src_stage(s, c, p, "F")
+                if src is not None and src != s:
+                    ch = ("A", src, s)
+                    out.append(Instr("RECV_ACT", c, i, peer=src, channel=ch,
+                                     allocs=[(("IN", c, i), "act", z["act"])]))
+            if kind == "B" and z["has_output"]:
+                src = _src_stage(s, c, p, "B", v)
+                if src is not None and src != s:
+                    ch = ("G", src, s)
+                    out.append(Instr("RECV_GRAD", c, i, peer=src, channel=ch,
+                                     allocs=[(("GIN", c, i), "comm", z["act"])]))
+            # 3. the compute op
+            ins = Instr(kind, c, i)
+            if kind == "F":
+                if trecomp and c == 1:
+                    ins.allocs.append((("TSTASH", c, i), "act", z["stash"]))
+                    ins.frees.append(("TSTASH", c, i))
+                else:
+                    ins.allocs.append((("STASH", c, i), "act", z["stash"]))
+                if msg is not None:
+                    ins.allocs.append((_msgbuf(msg[0], sent[msg[0]]), "comm", z["act"]))
+                elif z["has_output"]:
+                    # p == 1 local hand-off: output is the next chunk's input
+                    ins.allocs.append((("IN", c + 1, i), "act", z["act"]))
+                ins.allocs.append((("WSF", c, i), "workspace", z["ws_f"]))
+                ins.frees.append(("WSF", c, i))
+            elif kind == "R":
+                ins.allocs.append((("RBUF", c, i), "recomp_buf", z["stash"]))
+                ins.allocs.append((("WSR", c, i), "workspace", z["ws_f"]))
+                ins.frees.append(("WSR", c, i))
+            else:  # B
+                if msg is not None:
+                    ins.allocs.append((_msgbuf(msg[0], sent[msg[0]]), "comm", z["act"]))
+                elif not (s == 0 and c == 1):
+                    ins.allocs.append((("GIN", c - 1, i), "comm", z["act"]))
+                ins.allocs.append((("WSB", c, i), "workspace", z["ws_b"]))
+                ins.frees.append(("WSB", c, i))
+                ins.frees.append(("RBUF", c, i) if (trecomp and c == 1) else ("STASH", c, i))
+                if z["input_is_act"]:
+                    ins.frees.append(("IN", c, i))
+                if z["has_output"]:
+                    ins.frees.append(("GIN", c, i))
+            out.append(ins)
+            # 4. send after the producing op
+            if msg is not None:
+                ch = msg[0]
+                out.append(Instr("SEND_ACT" if kind == "F" else "SEND_GRAD", c, i,
+                                 peer=ch[2], channel=ch, msg=sent[ch]))
+                sent[ch] += 1
+            # 5. optimizer / offload after the chunk's last backward
+            if kind == "B" and i == last_b[c]:
+                if offload_model_state and c == v:
+                    out.append(Instr("GRAD_D2H", chunk=c))
+                    out.append(Instr("HOST_OPT", chunk=c))
+                else:
+                    out.append(Instr("OPT", chunk=c))
+            # weight upload right after the stage's first forward
+            if offload_model_state and not first_op_done and kind == "F":
+                out.append(Instr("W_H2D", chunk=v))
+            first_op_done = first_op_done or kind == "F"
+        # 6. flush outstanding sends (channels sorted, then message order)
+        for ch in sorted(sent):
+            while waited[ch] < sent[ch]:
+                jj = waited[ch]
+                out.append(Instr("SEND_WAIT", channel=ch, peer=ch[2], msg=jj,
+                                 frees=[_msgbuf(ch, jj)]))
+                waited[ch] += 1
+        streams.append(out)
+    return streams, static
+
+
+def _msgbuf(ch, j):
+    return ("MSG", ch, j)
+
+
+def _src_stage(s, c, p, kind, v=2):
+    """Stage producing the input (F) or output-grad (B) of chunk op (s, c)."""
+    if kind == "F":
+        if s > 0:
+            return s - 1
+        if c > 1:
+            return p - 1
+        return None
+    if s < p - 1:
+        return s + 1
+    if c < v:
+        return 0
+    return None
+
+
+def replay(stream, static):
+    """Live-byte replay: allocs at instruction start, frees at its end.
+    Returns {'total_peak', per-category peaks, 'final'}; 'final' must equal the
+    static bytes (everything transient released at step end)."""
+    live = {}
+    cat_live = defaultdict(int)
+    cat_peak = defaultdict(int)
+    base = sum(b for _n, _c, b in static)
+    for _n, cat, b in static:
+        cat_live[cat] += b
+        cat_peak[cat] = max(cat_peak[cat], cat_live[cat])
+    cur = base
+    peak = cur
+    for ins in stream:
+        for name, cat, b in ins.allocs:
+            assert name not in live, f"double alloc {name}"
+            live[name] = (cat, b)
+            cur += b
+            cat_live[cat] += b
+            cat_peak[cat] = max(cat_peak[cat], cat_live[cat])
+        peak = max(peak, cur)
+        for name in ins.frees:
+            cat, b = live.pop(name)
+            cur -= b
+            cat_live[cat] -= b
+    assert not live, f"leaked {list(live)[:4]}"
+    out = dict(cat_peak)
+    out["total_peak"] = peak
+    out["final"] = cur
+    return out
+
+
+def deadlock_free(streams) -> bool:
+    """Static deadlock test: nodes are instructions;
+    edges are program order, SEND(j) -> RECV(j) and RECV(j) -> SEND_WAIT(j)
+    (a send completes only once its receive is posted). Acyclic <=> no
+    deadlock for any durations. Kahn's algorithm."""
+    nodes = []
+    idx = {}
+    for s, st in enumerate(streams):
+        for n, ins in enumerate(st):
+            idx[(s, n)] = len(nodes)
+            nodes.append((s, n, ins))
+    succ = defaultdict(list)
+    indeg = [0] * len(nodes)
+
+    def edge(a, b):
+        succ[a].append(b)
+        indeg[b] += 1
+
+    sends, recvs, waits = {}, {}, {}
+    recv_count = defaultdict(int)
+    for s, st in enumerate(streams):
+        for n, ins in enumerate(st):
+            if n:
+                edge(idx[(s, n - 1)], idx[(s, n)])
+            if ins.kind in ("SEND_ACT", "SEND_GRAD"):
+                sends[(ins.channel, ins.msg)] = idx[(s, n)]
+            elif ins.kind in ("RECV_ACT", "RECV_GRAD"):
+                j = recv_count[ins.channel]
+                recv_count[ins.channel] += 1
+                recvs[(ins.channel, j)] = idx[(s, n)]
+            elif ins.kind == "SEND_WAIT":
+                waits[(ins.channel, ins.msg)] = idx[(s, n)]
+    for key, a in sends.items():
+        edge(a, recvs[key])
+    for key, w in waits.items():
+        edge(recvs[key], w)
+    q = [x for x in range(len(nodes)) if indeg[x] == 0]
+    seen = 0
+    while q:
+        x = q.pop()
+        seen += 1
+        for y in succ[x]:
+            indeg[y] -= 1
+            if indeg[y] == 0:
+                q.append(y)
+    return seen == len(nodes)
+
+
+def fifo_consistent(streams) -> bool:
+    """Receiver consume order equals sender production order on every channel
+    (SURVEY D-14): the j-th RECV on a channel must receive the (chunk, mb) the
+    j-th SEND produced for it."""
+    sent = defaultdict(list)
+    got = defaultdict(list)
+    p = len(streams)
+    for s, st in enumerate(streams):
+        for ins in st:
+            if ins.kind == "SEND_ACT":
+                # consumer (chunk, mb): wrap edge p-1 -> 0 advances the chunk
+                c = ins.chunk + 1 if (s == p - 1 and ins.channel[2] == 0 and p > 1
+                                      and s != 0) else ins.chunk
+                sent[ins.channel].append((c, ins.mb))
+            elif ins.kind == "SEND_GRAD":
+                c = ins.chunk - 1 if (s == 0 and ins.channel[2] == p - 1 and p > 1) else ins.chunk
+                sent[ins.channel].append((c, ins.mb))
+            elif ins.kind in ("RECV_ACT", "RECV_GRAD"):
+                got[ins.channel].append((ins.chunk, ins.mb))
+    return all(sent[ch] == got[ch] for ch in set(sent) | set(got))

@@ -1,0 +1,71 @@
+"""Pins for the oracle's byte-level instruction streams (oracle/stream.py)."""
+
+import pytest
+
+from oracle import schedule as S
+from oracle import stream as T
+
+C1 = T.ModelDesc(8, 64, 4, 256, 256, 32, 2, T.BF16)
+
+
+def desc(L, dtype=T.BF16):
+    return T.ModelDesc(L, 64, 4, 256, 256, 32, 2, dtype)
+
+
+@pytest.mark.parametrize("strategy", ["tpipe", "tpipe_trecomp", "1f1b", "1f1b_full_recomp"])
+@pytest.mark.parametrize("p", [1, 2, 4, 8])
+def test_stream_invariants(strategy, p):
+    """Deadlock-free with W=2 (static acyclicity, D-14), channel FIFO
+    consistency, every transient byte released at step end."""
+    d = desc(2 * p if p > 4 else 8)
+    st, static = T.build_streams(d, p, 8, strategy)
+    assert T.deadlock_free(st)
+    assert T.fifo_consistent(st)
+    for s in range(p):
+        r = T.replay(st[s], static[s])
+        assert r["final"] == sum(b for _n, _c, b in static[s])
+
+
+def test_send_window_one_deadlocks_trecomp_p8():
+    """SURVEY D-14: W=1 deadlocks T-Recomp at p=8 (k=1); W=2 does not."""
+    d = desc(16)
+    st, _ = T.build_streams(d, 8, 32, "tpipe_trecomp", window=1)
+    assert not T.deadlock_free(st)
+    st, _ = T.build_streams(d, 8, 32, "tpipe_trecomp", window=2)
+    assert T.deadlock_free(st)
+
+
+@pytest.mark.parametrize("p", [4, 8])
+def test_bytes_match_blocks(p):
+    """The byte replay of a middle stage's activations (stash + chunk input)
+    equals the block replay (P:611 blocks) times the per-chunk stash bytes."""
+    d = desc(2 * p)                       # one layer per chunk
+    m = 4 * p
+    st, static = T.build_streams(d, p, m, "tpipe")
+    z = T.sizes(d, p, 2, 1, 1)
+    block_bytes = z["stash"] + z["act"]
+    orders = S.tpipe_orders(p, m)
+    for s in range(1, p - 1):
+        r = T.replay(st[s], static[s])
+        _pk, tot = S.block_replay(orders[s], "tpipe")
+        assert r["act"] == tot * block_bytes
+
+
+def test_model_state_offload_one_third():
+    """T-Offload of chunk 2 (of 2) cuts model-state memory by 33.33%:
+    12 of 18 B/param move to host for half the params (SURVEY D-8)."""
+    d = desc(16)
+    P1 = T.chunk_params(d, 8, 2, 3, 1)
+    P2 = T.chunk_params(d, 8, 2, 3, 2)
+    assert P1 == P2
+    full = T.model_state_bytes(d, P1, False) + T.model_state_bytes(d, P2, False)
+    off = T.model_state_bytes(d, P1, False) + T.model_state_bytes(d, P2, True)
+    assert (full - off) * 3 == full
+
+
+def test_trecomp_bytes_below_tpipe():
+    """T-Recomp's stage-0 peak bytes are below T-Pipe's."""
+    d = desc(16)
+    a = T.replay(*[x[0] for x in T.build_streams(d, 8, 32, "tpipe")])
+    b = T.replay(*[x[0] for x in T.build_streams(d, 8, 32, "tpipe_trecomp")])
+    assert b["total_peak"] < a["total_peak"]
