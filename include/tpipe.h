@@ -1,0 +1,215 @@
+/*
+ * tpipe.h — C-ABI of libtpipe.so: the B200-native TPipe training hot path.
+ *
+ * Problem statement: given a model,
+ * P pipeline stages, m micro-batches and a fixed HBM capacity, choose a
+ * pipeline schedule plus recompute / offload decisions that fit HBM with
+ * minimal throughput loss. Two calls follow it:
+ *
+ *   tpipe_plan_create(model, n_stages, n_microbatches, hbm_budget, opts)
+ *       -> per-stage instruction streams (T-Pipe order P:303-310 / App. A
+ *          P:611-636; T-Recomp P:324-367 / App. B-C; T-Offload
+ *          P:376-420 / App. D), byte-exact per-stage peak HBM.
+ *   tpipe_step(runtime, tokens, targets, ...)
+ *       -> one training step executed from those streams with sm_100a
+ *          kernels, an exact-accounting HBM pool, copy-engine offload and
+ *          stage-to-stage transport.
+ *
+ * Conventions
+ *   - All functions return 0 on success or a negative TPIPE_E_* code; the
+ *     thread-local message of the last failure is tpipe_last_error().
+ *   - Pointers are HOST pointers unless documented as device pointers.
+ *   - Structs passed in are copied; nothing caller-owned is retained.
+ *   - Objects returned through `**out` are owned by the library and released
+ *     by the matching *_destroy. Pointers borrowed from a plan
+ *     (tpipe_plan_stage_ops/bufs/events) stay valid until tpipe_plan_destroy.
+ *   - A plan is immutable and may be read concurrently; a runtime is not
+ *     thread-safe (one per process / rank).
+ *
+ * Readings of the paper used here are listed in DESIGN.md (R1..R22); the
+ * instruction-stream and byte model are DESIGN.md §3-§4.
+ */
+#ifndef TPIPE_H
+#define TPIPE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ codes */
+#define TPIPE_OK            0
+#define TPIPE_E_INVALID    -1   /* invalid argument / config field (message names it) */
+#define TPIPE_E_INCOMPAT   -2   /* strategy incompatible with config (e.g. v) */
+#define TPIPE_E_DOMAIN     -3   /* outside a formula's domain */
+#define TPIPE_E_CONFLICT   -4   /* schedule dependency conflict */
+#define TPIPE_E_DEADLOCK   -5   /* instruction streams can deadlock */
+#define TPIPE_E_BUDGET     -6   /* no escalation fits the HBM budget */
+#define TPIPE_E_CUDA       -7
+#define TPIPE_E_NCCL       -8
+#define TPIPE_E_OOM        -9   /* runtime pool cap hit (a ledger bug) */
+#define TPIPE_E_STATE     -10   /* call not valid in the current state */
+
+#define TPIPE_FP32 0
+#define TPIPE_BF16 1
+
+/* ------------------------------------------------------------------ plan */
+typedef struct {
+    int32_t n_layers;        /* L, transformer blocks; must be divisible by n_stages */
+    int32_t hidden;          /* h, multiple of 64 */
+    int32_t n_heads;         /* a, h % a == 0, head_dim <= 128 */
+    int32_t ffn_hidden;      /* multiple of 64 */
+    int32_t vocab;           /* V, multiple of 64 */
+    int32_t seq_len;         /* s */
+    int32_t micro_batch;     /* b; tokens per micro-batch M = b*s */
+    int32_t dtype;           /* TPIPE_FP32 | TPIPE_BF16 */
+    int32_t layers_chunk[2]; /* per-stage layers of chunk 1 / chunk 2; {0,0} = auto (R14) */
+} tpipe_model_desc;
+
+enum {
+    TPIPE_S_1F1B = 0,             /* DAPPLE 1F1B, P:202 (baseline) */
+    TPIPE_S_1F1B_FULL_RECOMP = 1, /* 1F1B + full layer-grouped recompute */
+    TPIPE_S_TPIPE = 2,            /* T-Pipe, v = 2 */
+    TPIPE_S_TPIPE_TRECOMP = 3     /* T-Pipe + block-wise T-Recomp of chunk 1 */
+};
+
+#define TPIPE_OFFLOAD_MODEL_STATE 1   /* T-Offload of chunk-2 grads/optimizer/weights */
+
+typedef struct {
+    int32_t strategy;      /* TPIPE_S_*, or -1 = auto: escalate TPIPE -> TPIPE_TRECOMP ->
+                              TPIPE_TRECOMP + model-state offload until hbm_budget fits */
+    int32_t delay_rounds;  /* T-Recomp k; -1 = App. B constraint as printed */
+    int32_t send_window;   /* W, max in-flight sends per channel; 0 = default 2 (DESIGN R12) */
+    int32_t offload;       /* TPIPE_OFFLOAD_* bitmask (explicit strategies); -1 = auto */
+} tpipe_plan_opts;
+
+enum {
+    TPIPE_OP_F = 0, TPIPE_OP_B = 1, TPIPE_OP_R = 2,
+    TPIPE_OP_RECV_ACT = 3, TPIPE_OP_RECV_GRAD = 4,
+    TPIPE_OP_SEND_ACT = 5, TPIPE_OP_SEND_GRAD = 6, TPIPE_OP_SEND_WAIT = 7,
+    TPIPE_OP_OPT = 8, TPIPE_OP_GRAD_D2H = 9, TPIPE_OP_HOST_OPT = 10,
+    TPIPE_OP_W_H2D = 11, TPIPE_OP_W_WAIT = 12
+};
+
+/* One instruction of a stage's stream. Buffers listed in
+ * events[alloc_first .. +n_alloc) are allocated when the instruction starts,
+ * events[free_first .. +n_free) are released when it ends. */
+typedef struct {
+    int32_t kind;        /* TPIPE_OP_* */
+    int32_t chunk;       /* 1 or 2 (0 if not applicable) */
+    int32_t mb;          /* micro-batch 1..m (0 if not applicable) */
+    int32_t peer;        /* peer stage for SEND/RECV/SEND_WAIT, else -1 */
+    int32_t channel;     /* channel id (tpipe_plan_channel), else -1 */
+    int32_t msg;         /* message index on the channel (sender side), else -1 */
+    int32_t alloc_first, n_alloc, free_first, n_free;
+} tpipe_op;
+
+enum {
+    TPIPE_CAT_MODEL_STATE = 0, TPIPE_CAT_IO = 1, TPIPE_CAT_ACT = 2, TPIPE_CAT_RECOMP_BUF = 3,
+    TPIPE_CAT_COMM = 4, TPIPE_CAT_WORKSPACE = 5, TPIPE_CAT_COUNT = 6
+};
+
+enum {  /* buffer roles */
+    TPIPE_BUF_STASH = 0, TPIPE_BUF_TSTASH = 1, TPIPE_BUF_IN = 2, TPIPE_BUF_MSG = 3,
+    TPIPE_BUF_GIN = 4, TPIPE_BUF_RBUF = 5, TPIPE_BUF_WS = 6, TPIPE_BUF_STATIC = 7
+};
+
+typedef struct {
+    int32_t role;        /* TPIPE_BUF_* */
+    int32_t category;    /* TPIPE_CAT_* */
+    int32_t chunk, mb;   /* owner (chunk, micro-batch); for MSG: channel, msg index */
+    uint64_t bytes;      /* requested bytes (the ledger counts exactly these) */
+} tpipe_buf;
+
+typedef struct {
+    uint64_t peak[TPIPE_CAT_COUNT];  /* per-category maxima */
+    uint64_t total_peak;             /* maximum simultaneous live bytes */
+    uint64_t static_bytes;           /* model state + io, live the whole step */
+} tpipe_mem_report;
+
+typedef struct {
+    int32_t n_stages, n_microbatches, v, strategy, delay_rounds, send_window, offload;
+    int32_t layers_chunk[2];
+    int32_t n_channels;
+    uint64_t params_total;
+} tpipe_plan_info;
+
+typedef struct {
+    int64_t makespan;      /* unit-time model: F=1, B=2, R=1 (v=2); F=2, B=4(+recompute) (v=1) */
+    int64_t busy[64];      /* per-stage busy units (first 64 stages) */
+} tpipe_sim_report;
+
+typedef struct tpipe_plan tpipe_plan;
+
+int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, int32_t n_microbatches,
+                      uint64_t hbm_budget_bytes, const tpipe_plan_opts* opts, tpipe_plan** out);
+void tpipe_plan_destroy(tpipe_plan* plan);
+int tpipe_plan_get_info(const tpipe_plan* plan, tpipe_plan_info* out);
+int tpipe_plan_stage_ops(const tpipe_plan* plan, int32_t stage, const tpipe_op** ops, size_t* n);
+int tpipe_plan_stage_bufs(const tpipe_plan* plan, int32_t stage, const tpipe_buf** bufs, size_t* n);
+int tpipe_plan_stage_events(const tpipe_plan* plan, int32_t stage, const int32_t** ids, size_t* n);
+int tpipe_plan_stage_peak(const tpipe_plan* plan, int32_t stage, tpipe_mem_report* out);
+/* channel c: kind (0 = activations, 1 = activation grads), src stage, dst stage */
+int tpipe_plan_channel(const tpipe_plan* plan, int32_t c, int32_t* kind, int32_t* src, int32_t* dst);
+/* unit-time ASAP replay of the compute order (mirror of the oracle simulator) */
+int tpipe_plan_simulate(const tpipe_plan* plan, tpipe_sim_report* out);
+/* parameters of (stage, chunk) in the packed order of DESIGN.md §2.3 */
+int tpipe_plan_chunk_params(const tpipe_plan* plan, int32_t stage, int32_t chunk, uint64_t* n);
+
+/* ------------------------------------------------------------------ runtime */
+typedef struct {
+    int32_t stage;          /* stage executed by this process; -1 = all stages in-process
+                               (virtual pipeline on one GPU, device-local transport) */
+    int32_t device;         /* CUDA device ordinal */
+    const void* nccl_ids;   /* n_channels x 128-byte ncclUniqueId (stage >= 0, n_stages > 1) */
+    uint64_t pool_cap;      /* hard cap of the HBM pool in bytes; 0 = plan peak of owned stages */
+    float lr, beta1, beta2, eps, weight_decay;   /* AdamW (DESIGN R16); 0 -> defaults */
+} tpipe_runtime_opts;
+
+typedef struct {
+    uint64_t pool_high_water[64];   /* ledger high-water per stage (bytes, exact) */
+    uint64_t pool_reserved;         /* physical bytes reserved by the pool */
+    int64_t  kernel_launches;       /* kernels launched by the last step */
+    int64_t  step;                  /* completed steps */
+    double   offload_d2h_bytes, offload_h2d_bytes;   /* last step */
+    double   host_opt_ms;           /* last host optimizer duration */
+} tpipe_runtime_stats;
+
+typedef struct tpipe_runtime tpipe_runtime;
+
+#define TPIPE_STEP_NO_OPT 1u        /* skip optimizer ops: gradients stay accumulated */
+
+int tpipe_runtime_create(const tpipe_plan* plan, const tpipe_runtime_opts* opts,
+                         tpipe_runtime** out);
+void tpipe_runtime_destroy(tpipe_runtime* rt);
+/* fp32 parameters of (stage, chunk), packed order, n values */
+int tpipe_runtime_set_params(tpipe_runtime* rt, int32_t stage, int32_t chunk, const float* src,
+                             uint64_t n);
+int tpipe_runtime_get_params(tpipe_runtime* rt, int32_t stage, int32_t chunk, float* dst,
+                             uint64_t n);
+int tpipe_runtime_get_grads(tpipe_runtime* rt, int32_t stage, int32_t chunk, float* dst,
+                            uint64_t n);
+/* One training step. tokens/targets: int32 [m, b, s]; HOST pointers for
+ * tpipe_step (copied in by the runtime), DEVICE pointers for tpipe_step_device.
+ * loss_out (host) receives the mean token cross-entropy of the step (read on
+ * the last stage; 0 elsewhere). Synchronous. */
+int tpipe_step(tpipe_runtime* rt, const int32_t* tokens, const int32_t* targets, uint32_t flags,
+               float* loss_out);
+int tpipe_step_device(tpipe_runtime* rt, const int32_t* tokens_dev, const int32_t* targets_dev,
+                      uint32_t flags, float* loss_out);
+int tpipe_runtime_get_stats(const tpipe_runtime* rt, tpipe_runtime_stats* out);
+/* CUDA stream the runtime launches compute on (cudaStream_t), for event timing */
+void* tpipe_runtime_stream(const tpipe_runtime* rt);
+
+/* 128-byte ncclUniqueId (for stage >= 0 runtimes); TPIPE_E_NCCL if NCCL absent */
+int tpipe_nccl_unique_id(void* out128);
+
+const char* tpipe_last_error(void);
+int tpipe_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TPIPE_H */

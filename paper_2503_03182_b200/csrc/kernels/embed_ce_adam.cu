@@ -1,0 +1,250 @@
+// Embedding (K7), cross-entropy (K8 softmax part), AdamW (K9) and small
+// helpers. All deterministic: no floating-point atomics anywhere.
+#include <cstring>
+
+#include "adam_math.h"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace tpipe {
+
+// ============================================================== embedding
+template <typename T>
+__global__ void embed_fwd_kernel(const int* __restrict__ tok, const T* __restrict__ wte,
+                                 const T* __restrict__ wpe, T* __restrict__ x, int rows, int s,
+                                 int h) {
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long)rows * h) return;
+    const int r = (int)(i / h), c = (int)(i % h);
+    const float v = to_f<T>(wte[(long)tok[r] * h + c]) + to_f<T>(wpe[(long)(r % s) * h + c]);
+    x[i] = from_f<T>(v);
+}
+
+int embed_fwd(int dtype, const int* tok, const void* wte, const void* wpe, void* x, int rows,
+              int s, int h, cudaStream_t st) {
+    if (rows <= 0) return 0;
+    const long n = (long)rows * h;
+    const int blocks = (int)((n + 255) / 256);
+    if (dtype == DT_BF16)
+        embed_fwd_kernel<bf16><<<blocks, 256, 0, st>>>(tok, (const bf16*)wte, (const bf16*)wpe,
+                                                       (bf16*)x, rows, s, h);
+    else
+        embed_fwd_kernel<float><<<blocks, 256, 0, st>>>(tok, (const float*)wte, (const float*)wpe,
+                                                        (float*)x, rows, s, h);
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+// Single-CTA bitonic sort of keys (tok << 15 | row) in shared memory.
+__global__ void embed_sort_kernel(const int* __restrict__ tok, int* __restrict__ keys_out, int rows,
+                                  int n_pow2) {
+    extern __shared__ unsigned int sk[];
+    for (int i = threadIdx.x; i < n_pow2; i += blockDim.x)
+        sk[i] = i < rows ? ((unsigned)tok[i] << 15) | (unsigned)i : 0xFFFFFFFFu;
+    __syncthreads();
+    for (int k = 2; k <= n_pow2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n_pow2; i += blockDim.x) {
+                int ixj = i ^ j;
+                if (ixj > i) {
+                    unsigned a = sk[i], b = sk[ixj];
+                    bool up = (i & k) == 0;
+                    if ((a > b) == up) {
+                        sk[i] = b;
+                        sk[ixj] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < rows; i += blockDim.x) keys_out[i] = (int)sk[i];
+}
+
+// One CTA per sorted position; run-start CTAs sum their run in row order.
+template <typename T>
+__global__ void embed_wte_bwd_kernel(const int* __restrict__ keys, const T* __restrict__ dx,
+                                     float* __restrict__ dwte, int rows, int h) {
+    const int i = blockIdx.x;
+    const unsigned k = (unsigned)keys[i];
+    const unsigned t = k >> 15;
+    if (i > 0 && ((unsigned)keys[i - 1] >> 15) == t) return;
+    int end = i + 1;
+    while (end < rows && ((unsigned)keys[end] >> 15) == t) ++end;
+    for (int c = threadIdx.x; c < h; c += blockDim.x) {
+        float s = 0.f;
+        for (int j = i; j < end; ++j) {
+            const int r = (int)((unsigned)keys[j] & 0x7FFFu);
+            s += to_f<T>(dx[(long)r * h + c]);
+        }
+        dwte[(long)t * h + c] += s;
+    }
+}
+
+template <typename T>
+__global__ void embed_wpe_bwd_kernel(const T* __restrict__ dx, float* __restrict__ dwpe, int rows,
+                                     int s, int h) {
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long)s * h) return;
+    const int t = (int)(i / h), c = (int)(i % h);
+    float acc = 0.f;
+    for (int r = t; r < rows; r += s) acc += to_f<T>(dx[(long)r * h + c]);
+    dwpe[i] += acc;
+}
+
+int embed_bwd(int dtype, const int* tok, const void* dx, float* dwte, float* dwpe, int* ws,
+              int rows, int s, int h, cudaStream_t st) {
+    if (rows <= 0) return 0;
+    if (rows > 32768) return -1;
+    int n2 = 1;
+    while (n2 < rows) n2 <<= 1;
+    const size_t smem = (size_t)n2 * 4;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(embed_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             32768 * 4);
+        attr = true;
+    }
+    embed_sort_kernel<<<1, 1024, smem, st>>>(tok, ws, rows, n2);
+    const int wpe_blocks = (int)(((long)s * h + 255) / 256);
+    if (dtype == DT_BF16) {
+        embed_wte_bwd_kernel<bf16><<<rows, 256, 0, st>>>(ws, (const bf16*)dx, dwte, rows, h);
+        embed_wpe_bwd_kernel<bf16><<<wpe_blocks, 256, 0, st>>>((const bf16*)dx, dwpe, rows, s, h);
+    } else {
+        embed_wte_bwd_kernel<float><<<rows, 256, 0, st>>>(ws, (const float*)dx, dwte, rows, h);
+        embed_wpe_bwd_kernel<float><<<wpe_blocks, 256, 0, st>>>((const float*)dx, dwpe, rows, s, h);
+    }
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+// ============================================================== cross entropy
+__global__ void ce_lse_kernel(const float* __restrict__ logits, float* __restrict__ lse, int V) {
+    const int r = blockIdx.x;
+    const float* l = logits + (long)r * V;
+    __shared__ float red[32];
+    float mx = -INFINITY;
+    for (int c = threadIdx.x; c < V; c += blockDim.x) mx = fmaxf(mx, l[c]);
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : -INFINITY;
+        v = warp_max(v);
+        if (threadIdx.x == 0) red[0] = v;
+    }
+    __syncthreads();
+    mx = red[0];
+    __syncthreads();
+    float s = 0.f;
+    for (int c = threadIdx.x; c < V; c += blockDim.x) s += expf(l[c] - mx);
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+        v = warp_sum(v);
+        if (threadIdx.x == 0) lse[r] = mx + logf(v);
+    }
+}
+
+// one block: loss_out[0] += scale * sum_r (lse_r - logit[r, tgt_r]); fixed tree order
+__global__ void ce_loss_kernel(const float* __restrict__ logits, const int* __restrict__ tgt,
+                               const float* __restrict__ lse, float* __restrict__ loss_out,
+                               float scale, int rows, int V) {
+    __shared__ float red[32];
+    float s = 0.f;
+    for (int r = threadIdx.x; r < rows; r += blockDim.x)
+        s += lse[r] - logits[(long)r * V + tgt[r]];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+        v = warp_sum(v);
+        if (threadIdx.x == 0) loss_out[0] += v * scale;
+    }
+}
+
+int ce_fwd(const float* logits, const int* tgt, float* lse, float* loss_out, float scale, int rows,
+           int V, cudaStream_t st) {
+    if (rows <= 0) return 0;
+    ce_lse_kernel<<<rows, 512, 0, st>>>(logits, lse, V);
+    ce_loss_kernel<<<1, 1024, 0, st>>>(logits, tgt, lse, loss_out, scale, rows, V);
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+template <typename T>
+__global__ void ce_bwd_kernel(const float* __restrict__ logits, const int* __restrict__ tgt,
+                              const float* __restrict__ lse, T* __restrict__ d, float scale,
+                              int rows, int V) {
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long)rows * V) return;
+    const int r = (int)(i / V), c = (int)(i % V);
+    float p = expf(logits[i] - lse[r]);
+    if (c == tgt[r]) p -= 1.0f;
+    d[i] = from_f<T>(p * scale);
+}
+
+int ce_bwd(int dtype, const float* logits, const int* tgt, const float* lse, void* dlogits,
+           float scale, int rows, int V, cudaStream_t st) {
+    if (rows <= 0) return 0;
+    const long n = (long)rows * V;
+    const int blocks = (int)((n + 255) / 256);
+    if (dtype == DT_BF16)
+        ce_bwd_kernel<bf16><<<blocks, 256, 0, st>>>(logits, tgt, lse, (bf16*)dlogits, scale, rows, V);
+    else
+        ce_bwd_kernel<float><<<blocks, 256, 0, st>>>(logits, tgt, lse, (float*)dlogits, scale, rows, V);
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+// ============================================================== AdamW
+// The arithmetic below is written with explicit round-to-nearest intrinsics
+// (no FMA contraction) so that adamw_host (compiled with -ffp-contract=off)
+// produces bit-identical results (T-Offload on/off bit-exactness).
+template <typename T>
+__global__ void adamw_kernel(float* __restrict__ master, float* __restrict__ m,
+                             float* __restrict__ v, float* __restrict__ grad, T* __restrict__ w,
+                             long n, int decay, AdamHyper hp) {
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    AdamOut o = adam_elem(master[i], m[i], v[i], grad[i], decay, hp);
+    master[i] = o.w;
+    m[i] = o.m;
+    v[i] = o.v;
+    grad[i] = 0.f;
+    if (w) w[i] = from_f<T>(o.w);
+}
+
+int adamw(int dtype, float* master, float* m, float* v, float* grad, void* w, long n, int decay,
+          const AdamHyper& hp, cudaStream_t st) {
+    if (n <= 0) return 0;
+    const int blocks = (int)((n + 255) / 256);
+    if (dtype == DT_BF16)
+        adamw_kernel<bf16><<<blocks, 256, 0, st>>>(master, m, v, grad, (bf16*)w, n, decay, hp);
+    else  // fp32: the weight IS the master
+        adamw_kernel<float><<<blocks, 256, 0, st>>>(master, m, v, grad,
+                                                    (float*)(w == master ? nullptr : w), n, decay, hp);
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+// ============================================================== misc
+int fill_zero(void* p, size_t bytes, cudaStream_t st) {
+    return cudaMemsetAsync(p, 0, bytes, st) == cudaSuccess ? 0 : -3;
+}
+
+template <typename T>
+__global__ void cast_kernel(const float* __restrict__ s, T* __restrict__ d, long n) {
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) d[i] = from_f<T>(s[i]);
+}
+
+int cast_f32_to(int dtype, const float* src, void* dst, long n, cudaStream_t st) {
+    if (n <= 0) return 0;
+    const int blocks = (int)((n + 255) / 256);
+    if (dtype == DT_BF16)
+        cast_kernel<bf16><<<blocks, 256, 0, st>>>(src, (bf16*)dst, n);
+    else
+        cast_kernel<float><<<blocks, 256, 0, st>>>(src, (float*)dst, n);
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+}  // namespace tpipe

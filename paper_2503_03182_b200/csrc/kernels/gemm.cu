@@ -1,0 +1,475 @@
+// Dense GEMMs for the stage executor.
+//
+//   C = A * B^T   A logical [M,K], B logical [N,K], fp32 accumulation,
+//   fused epilogues (bias, residual, GELU, dGELU, fp32 main-grad accumulate).
+//
+// bf16: tcgen05.mma (kind::f16, M=128, N=BN, K=16) issued by one thread, A/B
+// staged by TMA (128B swizzle) into a 4-6 stage mbarrier ring, fp32
+// accumulators double-buffered in TMEM, 4 epilogue warps read TMEM with
+// tcgen05.ld and apply the epilogue in registers. Persistent grid (<= #SMs).
+// Both operands may be K-major or MN-major (fprop: K/K, dgrad: K/MN,
+// wgrad: MN/MN), so no transposes are materialised.
+//
+// fp32: exact-fp32 SIMT tiled kernel (parity mode).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace tpipe {
+
+// ============================================================== epilogue
+template <typename T>
+__device__ __forceinline__ void load32(const T* p, float (&o)[32]);
+template <>
+__device__ __forceinline__ void load32<bf16>(const bf16* p, float (&o)[32]) {
+    const uint4* q = reinterpret_cast<const uint4*>(p);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        uint4 u = q[i];
+        const bf16* h = reinterpret_cast<const bf16*>(&u);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[i * 8 + j] = __bfloat162float(h[j]);
+    }
+}
+template <>
+__device__ __forceinline__ void load32<float>(const float* p, float (&o)[32]) {
+    const float4* q = reinterpret_cast<const float4*>(p);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        float4 u = q[i];
+        o[4 * i] = u.x; o[4 * i + 1] = u.y; o[4 * i + 2] = u.z; o[4 * i + 3] = u.w;
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void store32(T* p, const float (&v)[32]);
+template <>
+__device__ __forceinline__ void store32<bf16>(bf16* p, const float (&v)[32]) {
+    uint4* q = reinterpret_cast<uint4*>(p);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        uint4 u;
+        bf16* h = reinterpret_cast<bf16*>(&u);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) h[j] = __float2bfloat16_rn(v[i * 8 + j]);
+        q[i] = u;
+    }
+}
+template <>
+__device__ __forceinline__ void store32<float>(float* p, const float (&v)[32]) {
+    float4* q = reinterpret_cast<float4*>(p);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) q[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+}
+
+// Apply the epilogue to 32 consecutive columns n0..n0+31 of row m (all in range).
+template <typename T>
+__device__ __forceinline__ void epi_chunk32(const GemmDesc& g, long m, long n0, float (&v)[32]) {
+    const int epi = g.epi;
+    if (epi == EPI_ACC_F32 || epi == EPI_STORE_F32) {
+        float* C = reinterpret_cast<float*>(g.C) + m * g.ldc + n0;
+        if (epi == EPI_ACC_F32) {
+            float c[32];
+            load32<float>(C, c);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = c[j] + v[j];
+        }
+        store32<float>(C, v);
+        return;
+    }
+    if (epi == EPI_BIAS || epi == EPI_BIAS_RES || epi == EPI_BIAS_GELU) {
+        float b[32];
+        load32<T>(reinterpret_cast<const T*>(g.bias) + n0, b);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = v[j] + b[j];
+    }
+    if (epi == EPI_BIAS_RES) {
+        float r[32];
+        load32<T>(reinterpret_cast<const T*>(g.res) + m * g.ldr + n0, r);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = v[j] + r[j];
+    }
+    if (epi == EPI_BIAS_GELU) {
+        float gg[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) gg[j] = gelu_tanh(rnd<T>(v[j]));
+        store32<T>(reinterpret_cast<T*>(g.C2) + m * g.ldc2 + n0, gg);
+    }
+    if (epi == EPI_DGELU) {
+        float u[32], gg[32];
+        load32<T>(reinterpret_cast<const T*>(g.aux) + m * g.ldaux + n0, u);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            gg[j] = gelu_tanh(u[j]);
+            v[j] = v[j] * gelu_tanh_grad(u[j]);
+        }
+        store32<T>(reinterpret_cast<T*>(g.C2) + m * g.ldc2 + n0, gg);
+    }
+    store32<T>(reinterpret_cast<T*>(g.C) + m * g.ldc + n0, v);
+}
+
+// ============================================================== SIMT (fp32 parity mode)
+constexpr int SB_M = 64, SB_N = 64, SB_K = 16;
+
+template <typename T>
+__device__ __forceinline__ float ldA(const GemmDesc& g, long m, long k) {
+    const T* A = reinterpret_cast<const T*>(g.A);
+    return to_f<T>(g.a_kmajor ? A[m * g.lda + k] : A[k * g.lda + m]);
+}
+template <typename T>
+__device__ __forceinline__ float ldB(const GemmDesc& g, long n, long k) {
+    const T* B = reinterpret_cast<const T*>(g.B);
+    return to_f<T>(g.b_kmajor ? B[n * g.ldb + k] : B[k * g.ldb + n]);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) gemm_simt_kernel(GemmDesc g) {
+    __shared__ float As[SB_K][SB_M + 4];
+    __shared__ float Bs[SB_K][SB_N + 4];
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    const long m0 = (long)blockIdx.y * SB_M, n0 = (long)blockIdx.x * SB_N;
+    float acc[4][4] = {};
+    for (long k0 = 0; k0 < g.K; k0 += SB_K) {
+        for (int e = threadIdx.x; e < SB_M * SB_K; e += 256) {
+            // coalesce along the contiguous dimension of each operand
+            int mm, kk;
+            if (g.a_kmajor) { kk = e % SB_K; mm = e / SB_K; } else { mm = e % SB_M; kk = e / SB_M; }
+            long gm = m0 + mm, gk = k0 + kk;
+            As[kk][mm] = (gm < g.M && gk < g.K) ? ldA<T>(g, gm, gk) : 0.f;
+            int nn, kb;
+            if (g.b_kmajor) { kb = e % SB_K; nn = e / SB_K; } else { nn = e % SB_N; kb = e / SB_N; }
+            long gn = n0 + nn, gk2 = k0 + kb;
+            Bs[kb][nn] = (gn < g.N && gk2 < g.K) ? ldB<T>(g, gn, gk2) : 0.f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < SB_K; ++kk) {
+            float a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+    // scalar epilogue
+    for (int i = 0; i < 4; ++i) {
+        long m = m0 + ty * 4 + i;
+        if (m >= g.M) continue;
+        for (int j = 0; j < 4; ++j) {
+            long n = n0 + tx * 4 + j;
+            if (n >= g.N) continue;
+            float v = acc[i][j];
+            switch (g.epi) {
+                case EPI_ACC_F32: {
+                    float* C = reinterpret_cast<float*>(g.C) + m * g.ldc + n;
+                    *C = *C + v;
+                    continue;
+                }
+                case EPI_STORE_F32:
+                    reinterpret_cast<float*>(g.C)[m * g.ldc + n] = v;
+                    continue;
+                case EPI_BIAS:
+                case EPI_BIAS_RES:
+                case EPI_BIAS_GELU:
+                    v = v + to_f<T>(reinterpret_cast<const T*>(g.bias)[n]);
+                    if (g.epi == EPI_BIAS_RES)
+                        v = v + to_f<T>(reinterpret_cast<const T*>(g.res)[m * g.ldr + n]);
+                    if (g.epi == EPI_BIAS_GELU)
+                        reinterpret_cast<T*>(g.C2)[m * g.ldc2 + n] = from_f<T>(gelu_tanh(rnd<T>(v)));
+                    break;
+                case EPI_DGELU: {
+                    float u = to_f<T>(reinterpret_cast<const T*>(g.aux)[m * g.ldaux + n]);
+                    reinterpret_cast<T*>(g.C2)[m * g.ldc2 + n] = from_f<T>(gelu_tanh(u));
+                    v = v * gelu_tanh_grad(u);
+                    break;
+                }
+                default:
+                    break;
+            }
+            reinterpret_cast<T*>(g.C)[m * g.ldc + n] = from_f<T>(v);
+        }
+    }
+}
+
+int gemm_simt(int dtype, const GemmDesc& g, cudaStream_t st) {
+    if (g.M <= 0 || g.N <= 0) return 0;
+    dim3 grid((g.N + SB_N - 1) / SB_N, (g.M + SB_M - 1) / SB_M);
+    if (dtype == DT_BF16)
+        gemm_simt_kernel<bf16><<<grid, 256, 0, st>>>(g);
+    else
+        gemm_simt_kernel<float><<<grid, 256, 0, st>>>(g);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+// ============================================================== tcgen05 (bf16)
+constexpr int TC_BM = 128, TC_BK = 64;
+
+template <int BN>
+struct TcCfg {
+    static constexpr int STAGES = BN == 256 ? 4 : 6;
+    static constexpr int A_BYTES = TC_BM * TC_BK * 2;
+    static constexpr int B_BYTES = BN * TC_BK * 2;
+    static constexpr int TMEM_COLS = 2 * BN;
+    static constexpr int SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
+};
+
+// instruction descriptor: bf16 x bf16 -> f32, M=128, N=BN, majors
+template <int BN, bool A_MN, bool B_MN>
+__device__ __forceinline__ uint32_t tc_idesc() {
+    return (1u << 4)                     // D format f32
+           | (1u << 7)                   // A bf16
+           | (1u << 10)                  // B bf16
+           | ((A_MN ? 1u : 0u) << 15)    // A major
+           | ((B_MN ? 1u : 0u) << 16)    // B major
+           | ((uint32_t)(BN >> 3) << 17) // N
+           | ((uint32_t)(TC_BM >> 4) << 24);  // M
+}
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(256, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const GemmDesc g, int num_m, int num_n, int num_kb) {
+    using Cfg = TcCfg<BN>;
+    constexpr int STAGES = Cfg::STAGES;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::B_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int num_tiles = num_m * num_n;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+    }
+    if (warp == 1 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int e = 0; e < 2; ++e) {
+            mbar_init(&tfull[e], 1);
+            mbar_init(&tempty[e], 128);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- TMA producer
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                const int mb = tile % num_m, nb = tile / num_m;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* a = sA + stage * Cfg::A_BYTES;
+                    uint8_t* b = sB + stage * Cfg::B_BYTES;
+                    if (!A_MN) {
+                        tma_load_2d(a, &tmA, &full[stage], kb * TC_BK, mb * TC_BM);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < TC_BM / 64; ++i)
+                            tma_load_2d(a + i * 64 * TC_BK * 2, &tmA, &full[stage], mb * TC_BM + i * 64,
+                                        kb * TC_BK);
+                    }
+                    if (!B_MN) {
+                        tma_load_2d(b, &tmB, &full[stage], kb * TC_BK, nb * BN);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < BN / 64; ++i)
+                            tma_load_2d(b + i * 64 * TC_BK * 2, &tmB, &full[stage], nb * BN + i * 64,
+                                        kb * TC_BK);
+                    }
+                    mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---------------- MMA issuer (single thread)
+            const uint32_t idesc = tc_idesc<BN, A_MN, B_MN>();
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+                const int acc = it & 1;
+                const uint32_t aph = (it >> 1) & 1;
+                mbar_wait(&tempty[acc], aph ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem_base + acc * BN;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a_addr = smem_u32(sA + stage * Cfg::A_BYTES);
+                    const uint32_t b_addr = smem_u32(sB + stage * Cfg::B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < TC_BK / 16; ++k) {
+                        // K-major: 16 elements = 32 bytes inside the 128B swizzle atom row;
+                        // MN-major: 16 K-rows of 128 B = 2048 bytes; MN atoms 8192 B apart.
+                        const uint64_t da = A_MN ? umma_desc_sw128(a_addr + k * 2048, TC_BK * 128, 1024)
+                                                 : umma_desc_sw128(a_addr + k * 32, 0, 1024);
+                        const uint64_t db = B_MN ? umma_desc_sw128(b_addr + k * 2048, TC_BK * 128, 1024)
+                                                 : umma_desc_sw128(b_addr + k * 32, 0, 1024);
+                        umma_bf16(d, da, db, idesc, (kb | k) != 0 ? 1u : 0u);
+                    }
+                    umma_commit(&empty[stage]);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                umma_commit(&tfull[acc]);
+            }
+        }
+    } else if (warp >= 4) {
+        // ---------------- epilogue: TMEM -> registers -> fused epilogue -> global
+        const int ew = warp - 4;
+        int it = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+            const int mb = tile % num_m, nb = tile / num_m;
+            const int acc = it & 1;
+            const uint32_t aph = (it >> 1) & 1;
+            mbar_wait(&tfull[acc], aph);
+            tc_fence_after();
+            const long m = (long)mb * TC_BM + ew * 32 + lane;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t r[32];
+                tmem_ld32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + c * 32, r);
+                tmem_wait_ld();
+                const long n0 = (long)nb * BN + c * 32;
+                if (m < g.M && n0 < g.N) {
+                    float v[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                    epi_chunk32<bf16>(g, m, n0, v);
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+        }
+    }
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    }
+}
+
+// ---------------------------------------------------------------- host side
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
+                                             &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// 2-D bf16 tensor map over a row-major [rows, cols] array with row stride ld
+// (elements); box = {box_inner (cols), box_outer (rows)}, 128B swizzle.
+static int make_map(CUtensorMap* map, const void* base, long cols, long rows, long ld, int box_inner,
+                    int box_outer) {
+    auto enc = get_encode();
+    if (!enc) return -1;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+    cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : -2;
+}
+
+static int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return n;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+static int launch_tc(const GemmDesc& g, cudaStream_t st) {
+    using Cfg = TcCfg<BN>;
+    CUtensorMap ta, tb;
+    int rc;
+    if (!A_MN)
+        rc = make_map(&ta, g.A, g.K, g.M, g.lda, TC_BK, TC_BM);
+    else
+        rc = make_map(&ta, g.A, g.M, g.K, g.lda, 64, TC_BK);
+    if (rc) return rc;
+    if (!B_MN)
+        rc = make_map(&tb, g.B, g.K, g.N, g.ldb, TC_BK, BN);
+    else
+        rc = make_map(&tb, g.B, g.N, g.K, g.ldb, 64, TC_BK);
+    if (rc) return rc;
+    const int num_m = (g.M + TC_BM - 1) / TC_BM;
+    const int num_n = (g.N + BN - 1) / BN;
+    const int num_kb = (g.K + TC_BK - 1) / TC_BK;
+    const int tiles = num_m * num_n;
+    const int grid = tiles < num_sms() ? tiles : num_sms();
+    auto kern = gemm_tc_kernel<BN, A_MN, B_MN>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+        attr_set = true;
+    }
+    kern<<<grid, 256, Cfg::SMEM, st>>>(ta, tb, g, num_m, num_n, num_kb);
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+int gemm_tc(const GemmDesc& g, cudaStream_t st) {
+    if (g.M <= 0 || g.N <= 0) return 0;
+    if (g.K <= 0) return -4;
+    // TMA: 16-byte aligned bases and row strides; 32-column epilogue chunks
+    if ((g.N % 32) || (g.lda % 8) || (g.ldb % 8)) return -5;
+    const int num_m = (g.M + TC_BM - 1) / TC_BM;
+    const bool wide = (long)num_m * ((g.N + 255) / 256) >= num_sms() && g.N % 256 == 0;
+    const bool amn = !g.a_kmajor, bmn = !g.b_kmajor;
+    if (wide) {
+        if (!amn && !bmn) return launch_tc<256, false, false>(g, st);
+        if (!amn && bmn) return launch_tc<256, false, true>(g, st);
+        if (amn && bmn) return launch_tc<256, true, true>(g, st);
+        return launch_tc<256, true, false>(g, st);
+    }
+    if (!amn && !bmn) return launch_tc<128, false, false>(g, st);
+    if (!amn && bmn) return launch_tc<128, false, true>(g, st);
+    if (amn && bmn) return launch_tc<128, true, true>(g, st);
+    return launch_tc<128, true, false>(g, st);
+}
+
+int gemm(int dtype, const GemmDesc& g, cudaStream_t st) {
+    if (dtype == DT_BF16) return gemm_tc(g, st);
+    return gemm_simt(DT_FP32, g, st);
+}
+
+}  // namespace tpipe

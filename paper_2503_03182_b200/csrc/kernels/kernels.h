@@ -1,0 +1,102 @@
+// Internal kernel launchers (not part of the C-ABI; see include/tpipe.h).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tpipe {
+
+enum DType : int { DT_FP32 = 0, DT_BF16 = 1 };
+
+// GEMM epilogues. C = A * B^T with A logical [M,K], B logical [N,K], fp32 accumulate.
+enum Epi : int {
+    EPI_STORE = 0,      // C(es)  = acc
+    EPI_BIAS = 1,       // C(es)  = acc + bias[n]
+    EPI_BIAS_RES = 2,   // C(es)  = acc + bias[n] + R[m,n]
+    EPI_BIAS_GELU = 3,  // C(es)  = u = acc + bias[n];  C2(es) = gelu(rnd(u))
+    EPI_DGELU = 4,      // C(es)  = acc * gelu'(U[m,n]); C2(es) = gelu(U[m,n])
+    EPI_ACC_F32 = 5,    // Cf32  += acc
+    EPI_STORE_F32 = 6,  // Cf32   = acc
+};
+
+struct GemmDesc {
+    int M = 0, N = 0, K = 0;
+    const void* A = nullptr; long lda = 0; int a_kmajor = 1;  // A[m,k] = kmajor ? A[m*lda+k] : A[k*lda+m]
+    const void* B = nullptr; long ldb = 0; int b_kmajor = 1;  // B[n,k] = kmajor ? B[n*ldb+k] : B[k*ldb+n]
+    int epi = EPI_STORE;
+    void* C = nullptr; long ldc = 0;
+    const void* bias = nullptr;
+    const void* res = nullptr; long ldr = 0;
+    void* C2 = nullptr; long ldc2 = 0;
+    const void* aux = nullptr; long ldaux = 0;
+};
+
+// dtype DT_BF16 -> tcgen05/TMA tensor-core kernel; DT_FP32 -> exact fp32 SIMT kernel.
+int gemm(int dtype, const GemmDesc& g, cudaStream_t st);
+// Plain SIMT kernel for either dtype (fp32 arithmetic); used for fp32 mode.
+int gemm_simt(int dtype, const GemmDesc& g, cudaStream_t st);
+// tcgen05 kernel (bf16 only).
+int gemm_tc(const GemmDesc& g, cudaStream_t st);
+
+// ---------------------------------------------------------------- layernorm
+// y = (x - mean) * rstd * gamma + beta over rows of length h; saves mean/rstd (fp32).
+int ln_fwd(int dtype, const void* x, const void* gamma, const void* beta, void* y, float* mean,
+           float* rstd, int rows, int h, cudaStream_t st);
+// y from saved stats (operator-level recompute); bit-identical to ln_fwd's y.
+int ln_apply(int dtype, const void* x, const void* gamma, const void* beta, const float* mean,
+             const float* rstd, void* y, int rows, int h, cudaStream_t st);
+// dx = resid + LN_bwd(dy); dgamma/dbeta partials per 64-row block into ws (fp32
+// [2][nblk][h]), then reduced in block order and ADDED to dgamma/dbeta (fp32).
+int ln_bwd(int dtype, const void* dy, const void* x, const void* gamma, const float* mean,
+           const float* rstd, const void* resid, void* dx, float* dgamma, float* dbeta, float* ws,
+           int rows, int h, cudaStream_t st);
+
+// ---------------------------------------------------------------- attention
+// qkv: [b*s, 3h] (q | k | v, head j = cols j*d..), o: [b*s, h], lse: [b, a, s] fp32.
+int attn_fwd(int dtype, const void* qkv, void* o, float* lse, int b, int s, int a, int d,
+             cudaStream_t st);
+// dqkv: [b*s, 3h]; ws: fp32 [b, a, s] for D = rowsum(dO * O).
+int attn_bwd(int dtype, const void* qkv, const void* o, const void* dout, const float* lse,
+             void* dqkv, float* ws, int b, int s, int a, int d, cudaStream_t st);
+
+// ---------------------------------------------------------------- embedding
+// x[r] = wte[tok[r]] + wpe[r % s]
+int embed_fwd(int dtype, const int* tok, const void* wte, const void* wpe, void* x, int rows,
+              int s, int h, cudaStream_t st);
+// dwte[tok] += dx rows (deterministic: sort by (token, row)); dwpe[t] += sum_b dx[b*s+t].
+// ws: int32 [2*rows].
+int embed_bwd(int dtype, const int* tok, const void* dx, float* dwte, float* dwpe, int* ws,
+              int rows, int s, int h, cudaStream_t st);
+
+// ---------------------------------------------------------------- cross entropy
+// logits fp32 [rows, V]; loss_out[0] += sum_r (lse_r - logit[r, tgt_r]) * scale (fixed order);
+// lse fp32 [rows].
+int ce_fwd(const float* logits, const int* tgt, float* lse, float* loss_out, float scale, int rows,
+           int V, cudaStream_t st);
+// dlogits(es) [rows, V] = (exp(logit - lse) - onehot) * scale
+int ce_bwd(int dtype, const float* logits, const int* tgt, const float* lse, void* dlogits,
+           float scale, int rows, int V, cudaStream_t st);
+
+// ---------------------------------------------------------------- reductions
+// out[n] += sum_r X[r, n] (deterministic, 64-row partials into ws fp32 [nblk, n]).
+int colsum_acc(int dtype, const void* X, float* out, float* ws, int rows, int n, cudaStream_t st);
+
+// ---------------------------------------------------------------- optimizer
+struct AdamHyper {
+    float lr, b1, b2, eps, wd;
+    float bc1, bc2;  // 1 - b1^t, 1 - b2^t (computed on the host in double, rounded once)
+};
+// master/m/v/grad fp32 [n]; w (es) [n] = master rounded (bf16) or master itself (fp32: w==master).
+// decay_mask: per-element? No: ranges [dec_lo, dec_hi) list handled by caller -> one call per range.
+int adamw(int dtype, float* master, float* m, float* v, float* grad, void* w, long n, int decay,
+          const AdamHyper& hp, cudaStream_t st);
+// host reference of the same arithmetic, bit-identical (T-Offload host optimizer)
+void adamw_host(float* master, float* m, float* v, const float* grad, uint16_t* w_bf16, long n,
+                int decay, const AdamHyper& hp);
+
+// ---------------------------------------------------------------- misc
+int fill_zero(void* p, size_t bytes, cudaStream_t st);
+int cast_f32_to(int dtype, const float* src, void* dst, long n, cudaStream_t st);
+
+}  // namespace tpipe

@@ -1,0 +1,728 @@
+// tpipe_plan: schedule generator (SURVEY §8(a) a1, §8(b) boundary).
+//
+// Turns (model, p, m, HBM budget) into per-stage instruction streams:
+//   1. compute order per stage —
+//        T-Pipe  (App. A): closed-form slot table
+//                 (R1) sorted per stage, executed ASAP;
+//        T-Recomp (App. B/C P:641-670): R(s,1,i) immediately before
+//                 B(s,1,i), chunk-1 forwards advanced k rounds with k
+//                 from the App. B constraint as printed (R3);
+//        1F1B and 1F1B + full layer-grouped recompute;
+//   2. SEND/RECV on FIFO channels per (kind, src, dst) with a send window W
+//      (SEND_WAIT placement);
+//   3. T-Offload: GRAD_D2H + HOST_OPT after the deep chunk's last
+//      backward, W_H2D after the first forward, W_WAIT before the first deep
+//      forward (windows Eq. 5 P:680 / Eq. 7);
+//   4. byte-exact live-set replay at instruction granularity.
+//
+// Written independently of oracle/stream.py; tests/test_plan_parity.py
+// checks the two element by element.
+#include "plan/plan.h"
+
+#include <algorithm>
+#include <cstdarg>
+#include <map>
+#include <new>
+#include <string>
+#include <tuple>
+
+#include "runtime/errors.h"
+
+namespace tpipe {
+
+static int cdiv(int n, int d) {  // ceiling division, n may be negative
+    return n >= 0 ? (n + d - 1) / d : -((-n) / d);
+}
+
+int delay_rounds_appB(int p) {
+    if (p < 3) return 0;
+    const int a = cdiv(p - 3, 6);
+    const int fwd_interval = 3 + 6 * a - p;
+    const int delta = cdiv(p - 1, 2) - a - 1;
+    int k = 0;
+    while (fwd_interval - delta + 7 * k < 0) ++k;
+    return k;
+}
+
+uint64_t layer_params(const tpipe_model_desc& d) {
+    const uint64_t h = d.hidden, f = d.ffn_hidden;
+    return 2 * h + (3 * h * h + 3 * h) + (h * h + h) + 2 * h + (f * h + f) + (h * f + h);
+}
+
+uint64_t chunk_params(const tpipe_model_desc& d, int p, int v, const int layers[2], int s, int c) {
+    uint64_t P = (uint64_t)layers[c - 1] * layer_params(d);
+    if (s == 0 && c == 1) P += (uint64_t)d.vocab * d.hidden + (uint64_t)d.seq_len * d.hidden;
+    if (s == p - 1 && c == v) P += 2ull * d.hidden + (uint64_t)d.vocab * d.hidden;
+    return P;
+}
+
+static ChunkSizes chunk_sizes(const tpipe_model_desc& d, int p, int v, const int layers[2], int s,
+                              int c, bool full_recomp) {
+    const uint64_t M = (uint64_t)d.micro_batch * d.seq_len, h = d.hidden, a = d.n_heads,
+                   f = d.ffn_hidden, V = d.vocab, es = d.dtype == TPIPE_BF16 ? 2 : 4;
+    const uint64_t n = layers[c - 1];
+    const bool emb = (s == 0 && c == 1), head = (s == p - 1 && c == v);
+    ChunkSizes z;
+    z.act = M * h * es;
+    z.input_is_act = !emb;
+    z.has_output = !head;
+    // per-layer stash: x_in, ln1 stats, qkv, attn out, lse, x_mid, ln2 stats, u (fc1 pre-act)
+    const uint64_t LS = M * h * es + 8 * M + 3 * M * h * es + M * h * es + 4 * a * M +
+                        M * h * es + 8 * M + M * f * es;
+    const uint64_t head_stash = M * h * es + 8 * M + 4 * M;   // x_f, ln_f stats, CE lse
+    uint64_t stash = full_recomp ? n * M * h * es : n * LS;
+    if (!emb) stash -= z.act;
+    if (head) stash += head_stash;
+    z.stash = stash;
+    const uint64_t nb = (M + 63) / 64;
+    uint64_t ws_f = M * (h + f) * es;
+    if (head) ws_f += M * h * es + 4 * M * V + 4 * M;
+    uint64_t ws_b = M * (2 * f + 8 * h) * es + 4 * a * M + 4 * nb * std::max(f, 3 * h);
+    if (full_recomp) ws_b += LS - M * h * es;
+    if (head) ws_b += 2 * M * h * es + 4 * M * V + M * V * es;
+    if (emb) ws_b += 8 * M;
+    z.ws_f = ws_f;
+    z.ws_b = ws_b;
+    return z;
+}
+
+// ---------------------------------------------------------------- compute orders
+using COp = std::array<int, 3>;  // {kind, chunk, mb}; kind: 0 F, 1 B, 2 R
+enum { KF = 0, KB = 1, KR = 2 };
+
+static std::vector<std::vector<COp>> tpipe_order(int p, int m, bool recomp, int k) {
+    const int a = cdiv(p - 3, 6), b = cdiv(2 * p - 3, 6);
+    std::vector<std::vector<COp>> out(p);
+    for (int s = 0; s < p; ++s) {
+        std::vector<std::pair<long, COp>> slots;
+        for (int i = 1; i <= m; ++i) {
+            const long f1 = 6L * (i - 1) + s;
+            const long f2 = 6L * (i - 1) + 3 + 6L * a + s;
+            const long f2last = 6L * (i - 1) + 3 + 6L * a + (p - 1);
+            const long b2 = f2last + 1 + 2L * (p - 1 - s);
+            const long b2first = f2last + 1 + 2L * (p - 1);
+            const long b1 = b2first + 3 + 6L * b - 2L * s;
+            slots.push_back({f1, {KF, 1, i}});
+            slots.push_back({f2, {KF, 2, i}});
+            slots.push_back({b2, {KB, 2, i}});
+            slots.push_back({b1, {KB, 1, i}});
+        }
+        std::sort(slots.begin(), slots.end(),
+                  [](const auto& x, const auto& y) { return x.first < y.first; });
+        std::vector<COp> lst;
+        for (auto& x : slots) lst.push_back(x.second);
+        if (recomp && k > 0) {
+            std::vector<COp> rel;
+            for (int i = 1; i <= std::min(k, m); ++i) rel.push_back({KF, 1, i});
+            int n = 0;
+            for (auto& op : lst) {
+                if (op[0] == KF && op[1] == 1) {
+                    ++n;
+                    if (n + k <= m) rel.push_back({KF, 1, n + k});
+                } else {
+                    rel.push_back(op);
+                }
+            }
+            lst.swap(rel);
+        }
+        if (recomp) {
+            std::vector<COp> withr;
+            for (auto& op : lst) {
+                if (op[0] == KB && op[1] == 1) withr.push_back({KR, 1, op[2]});
+                withr.push_back(op);
+            }
+            lst.swap(withr);
+        }
+        out[s] = lst;
+    }
+    return out;
+}
+
+static std::vector<std::vector<COp>> onef1b_order(int p, int m) {
+    std::vector<std::vector<COp>> out(p);
+    for (int s = 0; s < p; ++s) {
+        const int w = std::min(p - s - 1, m);
+        auto& lst = out[s];
+        for (int i = 1; i <= w; ++i) lst.push_back({KF, 1, i});
+        for (int i = 1; i <= m - w; ++i) {
+            lst.push_back({KF, 1, w + i});
+            lst.push_back({KB, 1, i});
+        }
+        for (int i = m - w + 1; i <= m; ++i) lst.push_back({KB, 1, i});
+    }
+    return out;
+}
+
+// destination of a compute op's output message; returns false if none / local
+struct Msg {
+    int kind, src, dst;  // kind 0 = act, 1 = grad
+};
+static bool message_of(int s, const COp& op, int p, int v, Msg* out) {
+    const int kind = op[0], c = op[1];
+    int dst;
+    if (kind == KF) {
+        if (s < p - 1) dst = s + 1;
+        else if (c < v) dst = 0;
+        else return false;
+        *out = {0, s, dst};
+    } else if (kind == KB) {
+        if (s > 0) dst = s - 1;
+        else if (c > 1) dst = p - 1;
+        else return false;
+        *out = {1, s, dst};
+    } else {
+        return false;
+    }
+    return dst != s;
+}
+
+// stage producing the input (F) / output grad (B) of (s, c); -1 if none
+static int src_stage(int s, int c, int p, int v, int kind) {
+    if (kind == KF) {
+        if (s > 0) return s - 1;
+        if (c > 1) return p - 1;
+        return -1;
+    }
+    if (s < p - 1) return s + 1;
+    if (c < v) return 0;
+    return -1;
+}
+
+// ---------------------------------------------------------------- plan builder
+struct Builder {
+    tpipe_plan* P;
+    int s;
+    std::vector<tpipe_op>& ops;
+    std::vector<tpipe_buf>& bufs;
+    std::vector<int32_t>& ev;
+    std::map<std::tuple<int, int, int, int>, int> live;  // (role, chunk, mb, extra) -> buf id
+
+    Builder(tpipe_plan* P_, int s_)
+        : P(P_), s(s_), ops(P_->ops[s_]), bufs(P_->bufs[s_]), ev(P_->events[s_]) {}
+
+    int newbuf(int role, int cat, int chunk, int mb, uint64_t bytes, int extra = 0) {
+        bufs.push_back({role, cat, chunk, mb, bytes});
+        const int id = (int)bufs.size() - 1;
+        live[{role, chunk, mb, extra}] = id;
+        return id;
+    }
+    int take(int role, int chunk, int mb, int extra = 0) {
+        auto it = live.find({role, chunk, mb, extra});
+        if (it == live.end()) return -1;
+        int id = it->second;
+        live.erase(it);
+        return id;
+    }
+    struct Pending {
+        std::vector<int> allocs, frees;
+    };
+    void emit(int kind, int chunk, int mb, int peer, int channel, int msg, const Pending& pe) {
+        tpipe_op op{};
+        op.kind = kind;
+        op.chunk = chunk;
+        op.mb = mb;
+        op.peer = peer;
+        op.channel = channel;
+        op.msg = msg;
+        op.alloc_first = (int)ev.size();
+        op.n_alloc = (int)pe.allocs.size();
+        for (int id : pe.allocs) ev.push_back(id);
+        op.free_first = (int)ev.size();
+        op.n_free = (int)pe.frees.size();
+        for (int id : pe.frees) ev.push_back(id);
+        ops.push_back(op);
+    }
+};
+
+static int build(tpipe_plan* P, bool trecomp, bool full_recomp) {
+    const tpipe_model_desc& d = P->model;
+    const int p = P->p, m = P->m, v = P->v;
+    P->ops.assign(p, {});
+    P->bufs.assign(p, {});
+    P->events.assign(p, {});
+    P->peak.assign(p, {});
+    P->chunk_params.assign(p, {0, 0});
+
+    // channel table sorted by (kind, src, dst)
+    std::map<std::tuple<int, int, int>, int> chan_id;
+    for (int s = 0; s < p; ++s)
+        for (auto& op : P->order[s]) {
+            Msg mg;
+            if (message_of(s, op, p, v, &mg)) chan_id[{mg.kind, mg.src, mg.dst}] = 0;
+        }
+    P->channels.clear();
+    for (auto& kv : chan_id) {
+        kv.second = (int)P->channels.size();
+        P->channels.push_back({std::get<0>(kv.first), std::get<1>(kv.first), std::get<2>(kv.first)});
+    }
+
+    const bool off = (P->offload & TPIPE_OFFLOAD_MODEL_STATE) != 0;
+    const uint64_t es = d.dtype == TPIPE_BF16 ? 2 : 4;
+    const uint64_t M = (uint64_t)d.micro_batch * d.seq_len;
+    P->params_total = 0;
+
+    for (int s = 0; s < p; ++s) {
+        Builder B(P, s);
+        // static buffers: model state per chunk, io
+        for (int c = 1; c <= v; ++c) {
+            const uint64_t np = chunk_params(d, p, v, P->layers, s, c);
+            P->chunk_params[s][c - 1] = np;
+            P->params_total += np;
+            const bool o = off && c == v;
+            const uint64_t per = o ? (es + 4) : (es + 4 + (d.dtype == TPIPE_BF16 ? 4 : 0) + 8);
+            B.bufs.push_back({TPIPE_BUF_STATIC, TPIPE_CAT_MODEL_STATE, c, 0, np * per});
+        }
+        if (s == 0) B.bufs.push_back({TPIPE_BUF_STATIC, TPIPE_CAT_IO, 0, 0, 4ull * m * M});
+        if (s == p - 1) B.bufs.push_back({TPIPE_BUF_STATIC, TPIPE_CAT_IO, 0, 1, 4ull * m * M + 4ull * m});
+
+        ChunkSizes z[3];
+        for (int c = 1; c <= v; ++c) z[c] = chunk_sizes(d, p, v, P->layers, s, c, full_recomp);
+
+        const auto& order = P->order[s];
+        std::map<int, int> sent, waited;  // channel -> count
+        int last_b[3] = {0, 0, 0}, first_f[3] = {1 << 30, 1 << 30, 1 << 30};
+        for (auto& op : order) {
+            if (op[0] == KB) last_b[op[1]] = std::max(last_b[op[1]], op[2]);
+            if (op[0] == KF) first_f[op[1]] = std::min(first_f[op[1]], op[2]);
+        }
+        bool first_f_done = false;
+        for (auto& op : order) {
+            const int kind = op[0], c = op[1], i = op[2];
+            const ChunkSizes& zz = z[c];
+            Msg mg;
+            const bool has_msg = message_of(s, op, p, v, &mg);
+            const int ch = has_msg ? chan_id[{mg.kind, mg.src, mg.dst}] : -1;
+            // 1. send-window waits
+            if (has_msg) {
+                const int j = sent[ch];
+                while (waited[ch] <= j - P->W) {
+                    const int jj = waited[ch];
+                    Builder::Pending pe;
+                    pe.frees.push_back(B.take(TPIPE_BUF_MSG, ch, jj));
+                    B.emit(TPIPE_OP_SEND_WAIT, 0, 0, mg.dst, ch, jj, pe);
+                    waited[ch] += 1;
+                }
+            }
+            // 2. weight-upload wait and receives
+            if (off && kind == KF && c == v && i == first_f[v]) B.emit(TPIPE_OP_W_WAIT, v, 0, -1, -1, -1, {});
+            if (kind == KF && zz.input_is_act) {
+                const int src = src_stage(s, c, p, v, KF);
+                if (src >= 0 && src != s) {
+                    Builder::Pending pe;
+                    pe.allocs.push_back(B.newbuf(TPIPE_BUF_IN, TPIPE_CAT_ACT, c, i, zz.act));
+                    B.emit(TPIPE_OP_RECV_ACT, c, i, src, chan_id[{0, src, s}], -1, pe);
+                }
+            }
+            if (kind == KB && zz.has_output) {
+                const int src = src_stage(s, c, p, v, KB);
+                if (src >= 0 && src != s) {
+                    Builder::Pending pe;
+                    pe.allocs.push_back(B.newbuf(TPIPE_BUF_GIN, TPIPE_CAT_COMM, c, i, zz.act));
+                    B.emit(TPIPE_OP_RECV_GRAD, c, i, src, chan_id[{1, src, s}], -1, pe);
+                }
+            }
+            // 3. the compute op
+            Builder::Pending pe;
+            if (kind == KF) {
+                if (trecomp && c == 1) {
+                    int id = B.newbuf(TPIPE_BUF_TSTASH, TPIPE_CAT_ACT, c, i, zz.stash);
+                    pe.allocs.push_back(id);
+                    pe.frees.push_back(B.take(TPIPE_BUF_TSTASH, c, i));
+                } else {
+                    pe.allocs.push_back(B.newbuf(TPIPE_BUF_STASH, TPIPE_CAT_ACT, c, i, zz.stash));
+                }
+                if (has_msg) {
+                    pe.allocs.push_back(B.newbuf(TPIPE_BUF_MSG, TPIPE_CAT_COMM, ch, sent[ch], zz.act));
+                } else if (zz.has_output) {
+                    pe.allocs.push_back(B.newbuf(TPIPE_BUF_IN, TPIPE_CAT_ACT, c + 1, i, zz.act));
+                }
+                int ws = B.newbuf(TPIPE_BUF_WS, TPIPE_CAT_WORKSPACE, c, i, zz.ws_f, 1);
+                pe.allocs.push_back(ws);
+                pe.frees.push_back(B.take(TPIPE_BUF_WS, c, i, 1));
+            } else if (kind == KR) {
+                pe.allocs.push_back(B.newbuf(TPIPE_BUF_RBUF, TPIPE_CAT_RECOMP_BUF, c, i, zz.stash));
+                pe.allocs.push_back(B.newbuf(TPIPE_BUF_WS, TPIPE_CAT_WORKSPACE, c, i, zz.ws_f, 2));
+                pe.frees.push_back(B.take(TPIPE_BUF_WS, c, i, 2));
+            } else {
+                if (has_msg) {
+                    pe.allocs.push_back(B.newbuf(TPIPE_BUF_MSG, TPIPE_CAT_COMM, ch, sent[ch], zz.act));
+                } else if (!(s == 0 && c == 1)) {
+                    pe.allocs.push_back(B.newbuf(TPIPE_BUF_GIN, TPIPE_CAT_COMM, c - 1, i, zz.act));
+                }
+                pe.allocs.push_back(B.newbuf(TPIPE_BUF_WS, TPIPE_CAT_WORKSPACE, c, i, zz.ws_b, 3));
+                pe.frees.push_back(B.take(TPIPE_BUF_WS, c, i, 3));
+                if (trecomp && c == 1)
+                    pe.frees.push_back(B.take(TPIPE_BUF_RBUF, c, i));
+                else
+                    pe.frees.push_back(B.take(TPIPE_BUF_STASH, c, i));
+                if (zz.input_is_act) pe.frees.push_back(B.take(TPIPE_BUF_IN, c, i));
+                if (zz.has_output) pe.frees.push_back(B.take(TPIPE_BUF_GIN, c, i));
+            }
+            for (int id : pe.frees)
+                if (id < 0) return set_error(TPIPE_E_CONFLICT, "stage %d: free of a buffer never allocated", s);
+            B.emit(kind == KF ? TPIPE_OP_F : kind == KB ? TPIPE_OP_B : TPIPE_OP_R, c, i, -1, -1, -1, pe);
+            // 4. send
+            if (has_msg) {
+                B.emit(kind == KF ? TPIPE_OP_SEND_ACT : TPIPE_OP_SEND_GRAD, c, i, mg.dst, ch, sent[ch], {});
+                sent[ch] += 1;
+            }
+            // 5. optimizer after the chunk's last backward
+            if (kind == KB && i == last_b[c]) {
+                if (off && c == v) {
+                    B.emit(TPIPE_OP_GRAD_D2H, c, 0, -1, -1, -1, {});
+                    B.emit(TPIPE_OP_HOST_OPT, c, 0, -1, -1, -1, {});
+                } else {
+                    B.emit(TPIPE_OP_OPT, c, 0, -1, -1, -1, {});
+                }
+            }
+            // 6. weight upload after the first forward
+            if (off && !first_f_done && kind == KF) B.emit(TPIPE_OP_W_H2D, v, 0, -1, -1, -1, {});
+            first_f_done = first_f_done || kind == KF;
+        }
+        // flush outstanding sends, channels in id order (= sorted (kind, src, dst))
+        for (auto& kv : sent) {
+            const int ch = kv.first;
+            while (waited[ch] < kv.second) {
+                const int jj = waited[ch];
+                Builder::Pending pe;
+                pe.frees.push_back(B.take(TPIPE_BUF_MSG, ch, jj));
+                B.emit(TPIPE_OP_SEND_WAIT, 0, 0, P->channels[ch][2], ch, jj, pe);
+                waited[ch] += 1;
+            }
+        }
+        if (!B.live.empty()) return set_error(TPIPE_E_CONFLICT, "stage %d: %zu buffers leak", s, B.live.size());
+
+        // live-byte replay
+        tpipe_mem_report r{};
+        uint64_t cur = 0, cat_live[TPIPE_CAT_COUNT] = {};
+        for (auto& b : B.bufs)
+            if (b.role == TPIPE_BUF_STATIC) {
+                cur += b.bytes;
+                cat_live[b.category] += b.bytes;
+                r.peak[b.category] = std::max(r.peak[b.category], cat_live[b.category]);
+            }
+        r.static_bytes = cur;
+        uint64_t peak = cur;
+        for (auto& op : B.ops) {
+            for (int e = 0; e < op.n_alloc; ++e) {
+                const tpipe_buf& b = B.bufs[B.ev[op.alloc_first + e]];
+                cur += b.bytes;
+                cat_live[b.category] += b.bytes;
+                r.peak[b.category] = std::max(r.peak[b.category], cat_live[b.category]);
+            }
+            peak = std::max(peak, cur);
+            for (int e = 0; e < op.n_free; ++e) {
+                const tpipe_buf& b = B.bufs[B.ev[op.free_first + e]];
+                cur -= b.bytes;
+                cat_live[b.category] -= b.bytes;
+            }
+        }
+        r.total_peak = peak;
+        P->peak[s] = r;
+    }
+    (void)M;
+    return 0;
+}
+
+// static deadlock check: program order + SEND(j)->RECV(j) + RECV(j)->SEND_WAIT(j)
+static bool deadlock_free(const tpipe_plan* P) {
+    const int p = P->p;
+    std::vector<int> base(p + 1, 0);
+    for (int s = 0; s < p; ++s) base[s + 1] = base[s] + (int)P->ops[s].size();
+    const int N = base[p];
+    std::vector<std::vector<int>> succ(N);
+    std::vector<int> indeg(N, 0);
+    auto edge = [&](int a, int b) {
+        succ[a].push_back(b);
+        indeg[b]++;
+    };
+    std::map<std::pair<int, int>, int> sends, recvs, waits;
+    std::map<int, int> rcount;
+    for (int s = 0; s < p; ++s)
+        for (int n = 0; n < (int)P->ops[s].size(); ++n) {
+            const tpipe_op& op = P->ops[s][n];
+            const int id = base[s] + n;
+            if (n) edge(id - 1, id);
+            if (op.kind == TPIPE_OP_SEND_ACT || op.kind == TPIPE_OP_SEND_GRAD) sends[{op.channel, op.msg}] = id;
+            if (op.kind == TPIPE_OP_RECV_ACT || op.kind == TPIPE_OP_RECV_GRAD) recvs[{op.channel, rcount[op.channel]++}] = id;
+            if (op.kind == TPIPE_OP_SEND_WAIT) waits[{op.channel, op.msg}] = id;
+        }
+    for (auto& kv : sends) {
+        auto it = recvs.find(kv.first);
+        if (it == recvs.end()) return false;
+        edge(kv.second, it->second);
+    }
+    for (auto& kv : waits) {
+        auto it = recvs.find(kv.first);
+        if (it == recvs.end()) return false;
+        edge(it->second, kv.second);
+    }
+    std::vector<int> q;
+    for (int i = 0; i < N; ++i)
+        if (!indeg[i]) q.push_back(i);
+    int seen = 0;
+    while (!q.empty()) {
+        int x = q.back();
+        q.pop_back();
+        ++seen;
+        for (int y : succ[x])
+            if (--indeg[y] == 0) q.push_back(y);
+    }
+    return seen == N;
+}
+
+static int validate(const tpipe_model_desc* d, int p, int m) {
+    if (!d) return set_error(TPIPE_E_INVALID, "model is NULL");
+    if (p < 1 || p > 64) return set_error(TPIPE_E_INVALID, "n_stages must be in [1, 64]");
+    if (m < 1) return set_error(TPIPE_E_INVALID, "n_microbatches must be >= 1");
+    if (d->dtype != TPIPE_FP32 && d->dtype != TPIPE_BF16) return set_error(TPIPE_E_INVALID, "dtype");
+    if (d->n_layers < 1 || d->n_layers % p) return set_error(TPIPE_E_INVALID, "n_layers must be a positive multiple of n_stages");
+    if (d->hidden < 64 || d->hidden % 64) return set_error(TPIPE_E_INVALID, "hidden must be a multiple of 64");
+    if (d->ffn_hidden < 64 || d->ffn_hidden % 64) return set_error(TPIPE_E_INVALID, "ffn_hidden must be a multiple of 64");
+    if (d->vocab < 64 || d->vocab % 64 || d->vocab >= (1 << 17)) return set_error(TPIPE_E_INVALID, "vocab must be a multiple of 64 below 131072");
+    if (d->n_heads < 1 || d->hidden % d->n_heads) return set_error(TPIPE_E_INVALID, "n_heads must divide hidden");
+    const int hd = d->hidden / d->n_heads;
+    if (hd > 128 || hd % 8) return set_error(TPIPE_E_INVALID, "head_dim must be a multiple of 8, <= 128");
+    if (d->seq_len < 1 || d->micro_batch < 1) return set_error(TPIPE_E_INVALID, "seq_len / micro_batch");
+    if ((long)d->seq_len * d->micro_batch > 32768) return set_error(TPIPE_E_INVALID, "micro_batch*seq_len must be <= 32768");
+    return 0;
+}
+
+}  // namespace tpipe
+
+using namespace tpipe;
+
+#define TP_API extern "C" __attribute__((visibility("default")))
+
+static int make_plan(const tpipe_model_desc* model, int p, int m, int strategy, int k, int W,
+                     int offload, tpipe_plan** out) {
+    tpipe_plan* P = new (std::nothrow) tpipe_plan();
+    if (!P) return set_error(TPIPE_E_INVALID, "out of host memory");
+    P->model = *model;
+    P->p = p;
+    P->m = m;
+    P->strategy = strategy;
+    P->W = W;
+    P->offload = offload;
+    const bool is_tp = strategy == TPIPE_S_TPIPE || strategy == TPIPE_S_TPIPE_TRECOMP;
+    P->v = is_tp ? 2 : 1;
+    const int n = model->n_layers / p;
+    if (P->v == 2) {
+        if (model->layers_chunk[0] || model->layers_chunk[1]) {
+            if (model->layers_chunk[0] < 1 || model->layers_chunk[1] < 1 ||
+                model->layers_chunk[0] + model->layers_chunk[1] != n) {
+                delete P;
+                return set_error(TPIPE_E_INVALID, "layers_chunk must be >= 1 and sum to n_layers/n_stages");
+            }
+            P->layers[0] = model->layers_chunk[0];
+            P->layers[1] = model->layers_chunk[1];
+        } else {
+            if (n < 2) {
+                delete P;
+                return set_error(TPIPE_E_INCOMPAT, "T-Pipe needs >= 2 layers per stage (2 chunks)");
+            }
+            P->layers[0] = (n + 1) / 2;  // extra layer to the shallow chunk (DESIGN R14)
+            P->layers[1] = n / 2;
+        }
+    } else {
+        if (offload) {
+            delete P;
+            return set_error(TPIPE_E_INCOMPAT, "model-state offload requires T-Pipe (v = 2)");
+        }
+        P->layers[0] = n;
+    }
+    const bool trecomp = strategy == TPIPE_S_TPIPE_TRECOMP;
+    P->k = trecomp ? (k < 0 ? delay_rounds_appB(p) : k) : 0;
+    if (is_tp) {
+        auto ord = tpipe_order(p, m, trecomp, P->k);
+        P->order.assign(p, {});
+        for (int s = 0; s < p; ++s) P->order[s] = ord[s];
+    } else {
+        auto ord = onef1b_order(p, m);
+        P->order.assign(p, {});
+        for (int s = 0; s < p; ++s) P->order[s] = ord[s];
+    }
+    int rc = build(P, trecomp, strategy == TPIPE_S_1F1B_FULL_RECOMP);
+    if (rc) {
+        delete P;
+        return rc;
+    }
+    if (!deadlock_free(P)) {
+        delete P;
+        return set_error(TPIPE_E_DEADLOCK, "instruction streams can deadlock (send window %d)", W);
+    }
+    *out = P;
+    return 0;
+}
+
+static uint64_t max_peak(const tpipe_plan* P) {
+    uint64_t x = 0;
+    for (auto& r : P->peak) x = std::max(x, r.total_peak);
+    return x;
+}
+
+TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, int32_t n_microbatches,
+                             uint64_t hbm_budget_bytes, const tpipe_plan_opts* opts,
+                             tpipe_plan** out) {
+    if (!out) return set_error(TPIPE_E_INVALID, "out is NULL");
+    *out = nullptr;
+    if (int rc = validate(model, n_stages, n_microbatches)) return rc;
+    tpipe_plan_opts o{-1, -1, 0, -1};
+    if (opts) o = *opts;
+    const int W = o.send_window > 0 ? o.send_window : 2;
+    if (o.strategy < -1 || o.strategy > TPIPE_S_TPIPE_TRECOMP) return set_error(TPIPE_E_INVALID, "strategy");
+    if (o.delay_rounds < -1) return set_error(TPIPE_E_INVALID, "delay_rounds");
+    if (o.strategy >= 0) {
+        const int off = o.offload < 0 ? 0 : o.offload;
+        tpipe_plan* P = nullptr;
+        int rc = make_plan(model, n_stages, n_microbatches, o.strategy, o.delay_rounds, W, off, &P);
+        if (rc) return rc;
+        if (hbm_budget_bytes && max_peak(P) > hbm_budget_bytes) {
+            const uint64_t pk = max_peak(P);
+            delete P;
+            return set_error(TPIPE_E_BUDGET, "peak %llu bytes exceeds budget %llu",
+                             (unsigned long long)pk, (unsigned long long)hbm_budget_bytes);
+        }
+        *out = P;
+        return 0;
+    }
+    // auto escalation: T-Pipe -> + T-Recomp -> + model-state T-Offload
+    const int ladder[3][2] = {{TPIPE_S_TPIPE, 0},
+                              {TPIPE_S_TPIPE_TRECOMP, 0},
+                              {TPIPE_S_TPIPE_TRECOMP, TPIPE_OFFLOAD_MODEL_STATE}};
+    uint64_t best = 0;
+    for (auto& rung : ladder) {
+        if (o.offload >= 0 && rung[1] && !(o.offload & TPIPE_OFFLOAD_MODEL_STATE)) continue;
+        tpipe_plan* P = nullptr;
+        int rc = make_plan(model, n_stages, n_microbatches, rung[0], o.delay_rounds, W, rung[1], &P);
+        if (rc) return rc;
+        best = max_peak(P);
+        if (!hbm_budget_bytes || best <= hbm_budget_bytes) {
+            *out = P;
+            return 0;
+        }
+        delete P;
+    }
+    return set_error(TPIPE_E_BUDGET, "no escalation fits: best peak %llu > budget %llu",
+                     (unsigned long long)best, (unsigned long long)hbm_budget_bytes);
+}
+
+TP_API void tpipe_plan_destroy(tpipe_plan* plan) { delete plan; }
+
+TP_API int tpipe_plan_get_info(const tpipe_plan* P, tpipe_plan_info* out) {
+    if (!P || !out) return set_error(TPIPE_E_INVALID, "NULL argument");
+    out->n_stages = P->p;
+    out->n_microbatches = P->m;
+    out->v = P->v;
+    out->strategy = P->strategy;
+    out->delay_rounds = P->k;
+    out->send_window = P->W;
+    out->offload = P->offload;
+    out->layers_chunk[0] = P->layers[0];
+    out->layers_chunk[1] = P->layers[1];
+    out->n_channels = (int32_t)P->channels.size();
+    out->params_total = P->params_total;
+    return 0;
+}
+
+TP_API int tpipe_plan_stage_ops(const tpipe_plan* P, int32_t s, const tpipe_op** ops, size_t* n) {
+    if (!P || !ops || !n || s < 0 || s >= P->p) return set_error(TPIPE_E_INVALID, "stage");
+    *ops = P->ops[s].data();
+    *n = P->ops[s].size();
+    return 0;
+}
+
+TP_API int tpipe_plan_stage_bufs(const tpipe_plan* P, int32_t s, const tpipe_buf** b, size_t* n) {
+    if (!P || !b || !n || s < 0 || s >= P->p) return set_error(TPIPE_E_INVALID, "stage");
+    *b = P->bufs[s].data();
+    *n = P->bufs[s].size();
+    return 0;
+}
+
+TP_API int tpipe_plan_stage_events(const tpipe_plan* P, int32_t s, const int32_t** ids, size_t* n) {
+    if (!P || !ids || !n || s < 0 || s >= P->p) return set_error(TPIPE_E_INVALID, "stage");
+    *ids = P->events[s].data();
+    *n = P->events[s].size();
+    return 0;
+}
+
+TP_API int tpipe_plan_stage_peak(const tpipe_plan* P, int32_t s, tpipe_mem_report* out) {
+    if (!P || !out || s < 0 || s >= P->p) return set_error(TPIPE_E_INVALID, "stage");
+    *out = P->peak[s];
+    return 0;
+}
+
+TP_API int tpipe_plan_channel(const tpipe_plan* P, int32_t c, int32_t* kind, int32_t* src,
+                              int32_t* dst) {
+    if (!P || c < 0 || c >= (int)P->channels.size()) return set_error(TPIPE_E_INVALID, "channel");
+    if (kind) *kind = P->channels[c][0];
+    if (src) *src = P->channels[c][1];
+    if (dst) *dst = P->channels[c][2];
+    return 0;
+}
+
+TP_API int tpipe_plan_chunk_params(const tpipe_plan* P, int32_t s, int32_t c, uint64_t* n) {
+    if (!P || !n || s < 0 || s >= P->p || c < 1 || c > P->v) return set_error(TPIPE_E_INVALID, "stage/chunk");
+    *n = P->chunk_params[s][c - 1];
+    return 0;
+}
+
+// unit-time ASAP replay of the compute order (F=1,B=2,R=1 at v=2; F=2,B=4(+2) at v=1)
+TP_API int tpipe_plan_simulate(const tpipe_plan* P, tpipe_sim_report* out) {
+    if (!P || !out) return set_error(TPIPE_E_INVALID, "NULL argument");
+    const int p = P->p, v = P->v;
+    const bool rec = P->strategy == TPIPE_S_TPIPE_TRECOMP;
+    auto dur = [&](int kind) -> long {
+        if (v == 2) return kind == KB ? 2 : 1;
+        if (kind == KF) return 2;
+        return P->strategy == TPIPE_S_1F1B_FULL_RECOMP ? 6 : 4;
+    };
+    std::map<std::tuple<int, int, int, int>, long> endt;  // (stage, kind, chunk, mb)
+    std::vector<size_t> pos(p, 0);
+    std::vector<long> freet(p, 0), busy(p, 0);
+    size_t total = 0, done = 0;
+    for (auto& o : P->order) total += o.size();
+    while (done < total) {
+        bool prog = false;
+        for (int s = 0; s < p; ++s) {
+            while (pos[s] < P->order[s].size()) {
+                const COp& op = P->order[s][pos[s]];
+                const int kind = op[0], c = op[1], i = op[2];
+                std::vector<std::tuple<int, int, int, int>> deps;
+                if (kind == KF) {
+                    if (s > 0) deps.push_back({s - 1, KF, c, i});
+                    else if (c > 1) deps.push_back({p - 1, KF, c - 1, i});
+                } else if (kind == KR) {
+                    deps.push_back({s, KF, c, i});
+                } else {
+                    deps.push_back({s, KF, c, i});
+                    if (rec && c == 1) deps.push_back({s, KR, c, i});
+                    if (s < p - 1) deps.push_back({s + 1, KB, c, i});
+                    else if (c < v) deps.push_back({0, KB, c + 1, i});
+                }
+                long t0 = freet[s];
+                bool ready = true;
+                for (auto& dd : deps) {
+                    auto it = endt.find(dd);
+                    if (it == endt.end()) { ready = false; break; }
+                    t0 = std::max(t0, it->second);
+                }
+                if (!ready) break;
+                const long t1 = t0 + dur(kind);
+                endt[{s, kind, c, i}] = t1;
+                freet[s] = t1;
+                busy[s] += t1 - t0;
+                ++pos[s];
+                ++done;
+                prog = true;
+            }
+        }
+        if (!prog) return set_error(TPIPE_E_DEADLOCK, "compute order deadlocks");
+    }
+    out->makespan = 0;
+    for (int s = 0; s < p; ++s) out->makespan = std::max<int64_t>(out->makespan, freet[s]);
+    for (int s = 0; s < 64; ++s) out->busy[s] = s < p ? busy[s] : 0;
+    return 0;
+}
+
+TP_API int tpipe_version(void) { return 1; }

@@ -1,0 +1,40 @@
+// Internal representation of an immutable TPipe plan (see include/tpipe.h).
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <vector>
+
+#include "tpipe.h"
+
+struct tpipe_plan {
+    tpipe_model_desc model{};
+    int p = 0, m = 0, v = 0;
+    int strategy = 0, k = 0, W = 2, offload = 0;
+    int layers[2] = {0, 0};
+    uint64_t params_total = 0;
+    // per stage
+    std::vector<std::vector<tpipe_op>> ops;
+    std::vector<std::vector<tpipe_buf>> bufs;
+    std::vector<std::vector<int32_t>> events;
+    std::vector<tpipe_mem_report> peak;
+    std::vector<std::array<uint64_t, 2>> chunk_params;
+    // compute order (F/B/R only) per stage: {kind, chunk, mb}
+    std::vector<std::vector<std::array<int, 3>>> order;
+    // channels: {kind (0 act, 1 grad), src, dst}
+    std::vector<std::array<int, 3>> channels;
+};
+
+namespace tpipe {
+
+// byte model of one (stage, chunk)
+struct ChunkSizes {
+    uint64_t act = 0, stash = 0, ws_f = 0, ws_b = 0;
+    bool input_is_act = true, has_output = true;
+};
+
+int delay_rounds_appB(int p);
+uint64_t layer_params(const tpipe_model_desc& d);
+uint64_t chunk_params(const tpipe_model_desc& d, int p, int v, const int layers[2], int s, int c);
+
+}  // namespace tpipe

@@ -1,0 +1,53 @@
+// Host AdamW for T-Offload ("performing its optimizer
+// updates" on the CPU in the cooldown bubble). Same element arithmetic as the
+// device kernel (adam_math.h), compiled with -ffp-contract=off, so the result
+// is bit-identical to tpipe::adamw on the GPU. Multithreaded over contiguous
+// slices (order of elements is irrelevant: the update is elementwise).
+#include <cstring>
+#include <thread>
+#include <vector>
+
+#include "kernels/adam_math.h"
+
+namespace tpipe {
+
+static inline uint16_t f32_to_bf16_rne(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7fffffffu) > 0x7f800000u) return (uint16_t)((u >> 16) | 0x40);  // quiet NaN
+    u += 0x7fffu + ((u >> 16) & 1u);
+    return (uint16_t)(u >> 16);
+}
+
+static void adamw_host_range(float* master, float* m, float* v, const float* grad,
+                             uint16_t* w_bf16, long lo, long hi, int decay, const AdamHyper& hp) {
+    for (long i = lo; i < hi; ++i) {
+        AdamOut o = adam_elem(master[i], m[i], v[i], grad[i], decay, hp);
+        master[i] = o.w;
+        m[i] = o.m;
+        v[i] = o.v;
+        if (w_bf16) w_bf16[i] = f32_to_bf16_rne(o.w);
+    }
+}
+
+void adamw_host(float* master, float* m, float* v, const float* grad, uint16_t* w_bf16, long n,
+                int decay, const AdamHyper& hp) {
+    unsigned nt = std::thread::hardware_concurrency();
+    if (nt == 0) nt = 1;
+    if (nt > 32) nt = 32;
+    if (n < (1L << 16)) nt = 1;
+    if (nt == 1) {
+        adamw_host_range(master, m, v, grad, w_bf16, 0, n, decay, hp);
+        return;
+    }
+    std::vector<std::thread> th;
+    const long chunk = (n + nt - 1) / nt;
+    for (unsigned t = 0; t < nt; ++t) {
+        const long lo = t * chunk, hi = lo + chunk < n ? lo + chunk : n;
+        if (lo >= hi) break;
+        th.emplace_back(adamw_host_range, master, m, v, grad, w_bf16, lo, hi, decay, std::cref(hp));
+    }
+    for (auto& x : th) x.join();
+}
+
+}  // namespace tpipe

@@ -1,0 +1,304 @@
+"""Kernel-level parity: each sm_100a kernel (called through the C-ABI of
+include/tpipe_kernels.h) vs the fp64 oracle / definition, element by element.
+
+Tolerances: fp32 mode <= 1e-4 max-relative (per tensor, vs the
+tensor's max magnitude); bf16 outputs <= 2e-2 relative L2; fp32-accumulator
+outputs of bf16 GEMMs <= 1e-4 (inputs are exact bf16 values).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from oracle import model as R  # noqa: E402
+
+dev = "cuda"
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    from paper_2503_03182_b200 import lib
+    assert torch.cuda.is_available(), "gpu tests need a GPU"
+    lib()
+
+
+def K():
+    from paper_2503_03182_b200 import kernels
+    return kernels
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / (np.linalg.norm(b) + 1e-30))
+
+
+def max_rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.abs(a - b).max() / (np.abs(b).max() + 1e-30))
+
+
+def t(x, dtype):
+    tt = torch.tensor(np.asarray(x, np.float32), device=dev)
+    return tt.to(torch.bfloat16) if dtype == "bf16" else tt
+
+
+def h(x):
+    return x.float().cpu().numpy().astype(np.float64)
+
+
+# ------------------------------------------------------------------ GEMM
+GEMM_SHAPES = [(256, 512, 256), (300, 192, 320), (64, 64, 64), (2048, 6144, 2048), (130, 96, 200)]
+
+
+@pytest.mark.parametrize("M,N,Kd", GEMM_SHAPES)
+@pytest.mark.parametrize("majors", [(1, 1), (1, 0), (0, 0)])
+def test_gemm_bf16_tcgen05(M, N, Kd, majors):
+    """tcgen05 GEMM, all operand majors (fprop K/K, dgrad K/MN, wgrad MN/MN),
+    fp32-output epilogue: near-exact vs fp64 of the same bf16 inputs."""
+    ak, bk = majors
+    rng = np.random.default_rng(M + N + Kd)
+    A = rng.standard_normal((M, Kd)).astype(np.float32)
+    B = rng.standard_normal((N, Kd)).astype(np.float32)
+    At = t(A if ak else A.T.copy(), "bf16")
+    Bt = t(B if bk else B.T.copy(), "bf16")
+    ref = h(At if ak else At.T) @ h(Bt if bk else Bt.T).T
+    C = torch.zeros((M, N), device=dev, dtype=torch.float32)
+    K().tpipe_k_gemm(1, M, N, Kd, At, Kd if ak else M, ak, Bt, Kd if bk else N, bk,
+                     K().EPI_STORE_F32, C, N)
+    torch.cuda.synchronize()
+    assert max_rel(h(C), ref) < 1e-4
+    # accumulate epilogue: C += A B^T
+    K().tpipe_k_gemm(1, M, N, Kd, At, Kd if ak else M, ak, Bt, Kd if bk else N, bk,
+                     K().EPI_ACC_F32, C, N)
+    torch.cuda.synchronize()
+    assert max_rel(h(C), 2 * ref) < 1e-4
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_gemm_epilogues(dtype):
+    """bias / residual / GELU / dGELU epilogues vs fp64 definitions."""
+    dt = 1 if dtype == "bf16" else 0
+    M, N, Kd = 192, 320, 128
+    rng = np.random.default_rng(7)
+    A = t(rng.standard_normal((M, Kd)), dtype)
+    B = t(rng.standard_normal((N, Kd)) * 0.1, dtype)
+    bias = t(rng.standard_normal(N), dtype)
+    Rm = t(rng.standard_normal((M, N)), dtype)
+    U = t(rng.standard_normal((M, N)), dtype)
+    acc = h(A) @ h(B).T
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    tol = 2e-2 if dtype == "bf16" else 1e-4
+    metric = rel_l2 if dtype == "bf16" else max_rel
+    C = torch.empty((M, N), device=dev, dtype=tdt)
+    C2 = torch.empty((M, N), device=dev, dtype=tdt)
+    k = K()
+    k.tpipe_k_gemm(dt, M, N, Kd, A, Kd, 1, B, Kd, 1, k.EPI_STORE, C, N)
+    torch.cuda.synchronize()
+    assert metric(h(C), acc) < tol
+    k.tpipe_k_gemm(dt, M, N, Kd, A, Kd, 1, B, Kd, 1, k.EPI_BIAS, C, N, bias=bias)
+    torch.cuda.synchronize()
+    assert metric(h(C), acc + h(bias)) < tol
+    k.tpipe_k_gemm(dt, M, N, Kd, A, Kd, 1, B, Kd, 1, k.EPI_BIAS_RES, C, N, bias=bias, R=Rm, ldr=N)
+    torch.cuda.synchronize()
+    assert metric(h(C), acc + h(bias) + h(Rm)) < tol
+    k.tpipe_k_gemm(dt, M, N, Kd, A, Kd, 1, B, Kd, 1, k.EPI_BIAS_GELU, C, N, bias=bias, C2=C2, ldc2=N)
+    torch.cuda.synchronize()
+    u = acc + h(bias)
+    assert metric(h(C), u) < tol
+    assert metric(h(C2), R.gelu(h(C))) < tol
+    k.tpipe_k_gemm(dt, M, N, Kd, A, Kd, 1, B, Kd, 1, k.EPI_DGELU, C, N, C2=C2, ldc2=N, aux=U,
+                   ldaux=N)
+    torch.cuda.synchronize()
+    assert metric(h(C), acc * R.gelu_grad(h(U))) < tol
+    assert metric(h(C2), R.gelu(h(U))) < tol
+
+
+@pytest.mark.parametrize("majors", [(1, 1), (1, 0), (0, 0)])
+def test_gemm_fp32_simt(majors):
+    ak, bk = majors
+    M, N, Kd = 130, 96, 200
+    rng = np.random.default_rng(3)
+    A = rng.standard_normal((M, Kd))
+    B = rng.standard_normal((N, Kd))
+    At = t(A if ak else A.T.copy(), "fp32")
+    Bt = t(B if bk else B.T.copy(), "fp32")
+    C = torch.zeros((M, N), device=dev)
+    K().tpipe_k_gemm(0, M, N, Kd, At, Kd if ak else M, ak, Bt, Kd if bk else N, bk,
+                     K().EPI_STORE_F32, C, N)
+    torch.cuda.synchronize()
+    assert max_rel(h(C), A.astype(np.float32).astype(np.float64) @ B.astype(np.float32).T) < 1e-5
+
+
+# ------------------------------------------------------------------ LayerNorm
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("rows,hd", [(64, 64), (130, 2048), (5, 5120)])
+def test_layernorm(dtype, rows, hd):
+    dt = 1 if dtype == "bf16" else 0
+    rng = np.random.default_rng(rows)
+    x = t(rng.standard_normal((rows, hd)) * 2 + 0.5, dtype)
+    g = t(1 + 0.1 * rng.standard_normal(hd), dtype)
+    b = t(0.1 * rng.standard_normal(hd), dtype)
+    dy = t(rng.standard_normal((rows, hd)), dtype)
+    res = t(rng.standard_normal((rows, hd)), dtype)
+    y = torch.empty_like(x)
+    mean = torch.empty(rows, device=dev)
+    rstd = torch.empty(rows, device=dev)
+    k = K()
+    k.tpipe_k_ln_fwd(dt, x, g, b, y, mean, rstd, rows, hd)
+    yr, cache = R.ln_fwd(h(x), h(g), h(b))
+    dx = torch.empty_like(x)
+    dg = torch.zeros(hd, device=dev)
+    db = torch.zeros(hd, device=dev)
+    ws = torch.empty(2 * ((rows + 63) // 64) * hd, device=dev)
+    k.tpipe_k_ln_bwd(dt, dy, x, g, mean, rstd, res, dx, dg, db, ws, rows, hd)
+    torch.cuda.synchronize()
+    dxr, dgr, dbr = R.ln_bwd(h(dy), cache)
+    tol, metric = (2e-2, rel_l2) if dtype == "bf16" else (1e-4, max_rel)
+    assert metric(h(y), yr) < tol
+    assert max_rel(h(mean), h(x).mean(-1)) < 1e-5
+    assert metric(h(dx), dxr + h(res)) < tol
+    assert max_rel(h(dg), dgr) < (1e-2 if dtype == "bf16" else 1e-4)
+    assert max_rel(h(db), dbr) < 1e-4
+
+
+# ------------------------------------------------------------------ attention
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("b,s,a,d", [(2, 32, 4, 16), (1, 100, 2, 64), (1, 257, 2, 128)])
+def test_attention(dtype, b, s, a, d):
+    dt = 1 if dtype == "bf16" else 0
+    hdim = a * d
+    rng = np.random.default_rng(s + d)
+    qkv = t(rng.standard_normal((b * s, 3 * hdim)), dtype)
+    dout = t(rng.standard_normal((b * s, hdim)), dtype)
+    o = torch.empty((b * s, hdim), device=dev, dtype=qkv.dtype)
+    lse = torch.empty((b, a, s), device=dev)
+    k = K()
+    k.tpipe_k_attn_fwd(dt, qkv, o, lse, b, s, a, d)
+    Q = h(qkv).reshape(b, s, 3 * hdim)
+    q = R.split_heads(Q[..., :hdim], a)
+    kk = R.split_heads(Q[..., hdim:2 * hdim], a)
+    v = R.split_heads(Q[..., 2 * hdim:], a)
+    Oref, cache, lref = R.attn_fwd(q, kk, v)
+    dqkv = torch.empty_like(qkv)
+    ws = torch.empty((b, a, s), device=dev)
+    k.tpipe_k_attn_bwd(dt, qkv, o, dout, lse, dqkv, ws, b, s, a, d)
+    torch.cuda.synchronize()
+    dQ, dK, dV = R.attn_bwd(R.split_heads(h(dout).reshape(b, s, hdim), a), cache)
+    tol, metric = (2e-2, rel_l2) if dtype == "bf16" else (1e-4, max_rel)
+    assert metric(h(o).reshape(b, s, hdim), R.merge_heads(Oref)) < tol
+    assert max_rel(h(lse), lref) < 1e-4
+    got = h(dqkv).reshape(b, s, 3 * hdim)
+    assert metric(got[..., :hdim], R.merge_heads(dQ)) < tol
+    assert metric(got[..., hdim:2 * hdim], R.merge_heads(dK)) < tol
+    assert metric(got[..., 2 * hdim:], R.merge_heads(dV)) < tol
+
+
+# ------------------------------------------------------------------ embedding / CE / colsum
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_embedding(dtype):
+    dt = 1 if dtype == "bf16" else 0
+    V, s, bsz, hd = 97, 32, 3, 64
+    rows = s * bsz
+    rng = np.random.default_rng(11)
+    tok = torch.tensor(rng.integers(0, V, rows), dtype=torch.int32, device=dev)
+    wte = t(rng.standard_normal((V, hd)), dtype)
+    wpe = t(rng.standard_normal((s, hd)), dtype)
+    x = torch.empty((rows, hd), device=dev, dtype=wte.dtype)
+    k = K()
+    k.tpipe_k_embed_fwd(dt, tok, wte, wpe, x, rows, s, hd)
+    dx = t(rng.standard_normal((rows, hd)), dtype)
+    dwte = torch.zeros((V, hd), device=dev)
+    dwpe = torch.zeros((s, hd), device=dev)
+    ws = torch.empty(2 * rows, dtype=torch.int32, device=dev)
+    k.tpipe_k_embed_bwd(dt, tok, dx, dwte, dwpe, ws, rows, s, hd)
+    torch.cuda.synchronize()
+    tk = tok.cpu().numpy()
+    ref = h(wte)[tk] + h(wpe)[np.arange(rows) % s]
+    assert max_rel(h(x), ref) < (1e-2 if dtype == "bf16" else 1e-6)
+    dref = np.zeros((V, hd))
+    for r in range(rows):
+        dref[tk[r]] += h(dx)[r]
+    assert max_rel(h(dwte), dref) < 1e-5
+    assert max_rel(h(dwpe), h(dx).reshape(bsz, s, hd).sum(0)) < 1e-5
+    # determinism: a second run gives identical bits
+    dwte2 = torch.zeros_like(dwte)
+    k.tpipe_k_embed_bwd(dt, tok, dx, dwte2, dwpe, ws, rows, s, hd)
+    torch.cuda.synchronize()
+    assert torch.equal(dwte, dwte2)
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_cross_entropy(dtype):
+    dt = 1 if dtype == "bf16" else 0
+    rows, V = 70, 50304
+    rng = np.random.default_rng(5)
+    logits = torch.tensor(rng.standard_normal((rows, V)).astype(np.float32) * 3, device=dev)
+    tgt = torch.tensor(rng.integers(0, V, rows), dtype=torch.int32, device=dev)
+    lse = torch.empty(rows, device=dev)
+    loss = torch.zeros(1, device=dev)
+    k = K()
+    k.tpipe_k_ce_fwd(logits, tgt, lse, loss, 1.0 / rows, rows, V)
+    d = torch.empty((rows, V), device=dev, dtype=torch.bfloat16 if dt else torch.float32)
+    k.tpipe_k_ce_bwd(dt, logits, tgt, lse, d, 1.0 / rows, rows, V)
+    torch.cuda.synchronize()
+    L = h(logits)
+    mx = L.max(-1, keepdims=True)
+    lref = (mx + np.log(np.exp(L - mx).sum(-1, keepdims=True)))[:, 0]
+    tk = tgt.cpu().numpy()
+    assert max_rel(h(lse), lref) < 1e-6
+    assert abs(h(loss)[0] - (lref - L[np.arange(rows), tk]).mean()) < 1e-5
+    P = np.exp(L - lref[:, None])
+    P[np.arange(rows), tk] -= 1
+    tol = 2e-2 if dt else 1e-4
+    assert (rel_l2 if dt else max_rel)(h(d), P / rows) < tol
+
+
+def test_colsum():
+    rows, n = 300, 192
+    rng = np.random.default_rng(2)
+    X = t(rng.standard_normal((rows, n)), "fp32")
+    out = torch.ones(n, device=dev)
+    ws = torch.empty(((rows + 63) // 64) * n, device=dev)
+    K().tpipe_k_colsum(0, X, out, ws, rows, n)
+    torch.cuda.synchronize()
+    assert max_rel(h(out), 1 + h(X).sum(0)) < 1e-5
+
+
+# ------------------------------------------------------------------ AdamW
+@pytest.mark.parametrize("decay", [0, 1])
+def test_adamw_device_host_bitexact(decay):
+    """Device AdamW == host AdamW bit for bit (T-Offload on/off),
+    and both match the fp64 oracle step."""
+    n = 100_003
+    rng = np.random.default_rng(9)
+    w0 = rng.standard_normal(n).astype(np.float32)
+    m0 = (rng.standard_normal(n) * 1e-3).astype(np.float32)
+    v0 = (rng.random(n) * 1e-6).astype(np.float32)
+    g0 = (rng.standard_normal(n) * 1e-2).astype(np.float32)
+    hp = dict(lr=3e-3, b1=0.9, b2=0.95, eps=1e-8, wd=0.1)
+    step = 3
+    bc1, bc2 = 1 - 0.9 ** step, 1 - 0.95 ** step
+    Wm, Mm, Vm, Gm = (torch.tensor(x, device=dev) for x in (w0, m0, v0, g0))
+    wb = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    K().tpipe_k_adamw(1, Wm, Mm, Vm, Gm, wb, n, decay, hp["lr"], hp["b1"], hp["b2"], hp["eps"],
+                      hp["wd"], bc1, bc2)
+    torch.cuda.synchronize()
+    hw, hm, hv = w0.copy(), m0.copy(), v0.copy()
+    hb = np.empty(n, np.uint16)
+    K().tpipe_host_adamw(hw, hm, hv, g0, hb, n, decay, hp["lr"], hp["b1"], hp["b2"], hp["eps"],
+                         hp["wd"], bc1, bc2)
+    assert np.array_equal(Wm.cpu().numpy().view(np.uint32), hw.view(np.uint32))
+    assert np.array_equal(Mm.cpu().numpy().view(np.uint32), hm.view(np.uint32))
+    assert np.array_equal(Vm.cpu().numpy().view(np.uint32), hv.view(np.uint32))
+    assert np.array_equal(wb.cpu().view(torch.int16).numpy().view(np.uint16), hb)
+    assert float(Gm.abs().max()) == 0.0            # grad zeroed
+    rw, rm, rv = R.adamw(w0, g0.astype(np.float64), m0.astype(np.float64),
+                         v0.astype(np.float64), step, hp["lr"], bool(decay))
+    assert max_rel(hw, rw) < 1e-6

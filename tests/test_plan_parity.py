@@ -1,0 +1,158 @@
+"""Plan parity (CPU): the C++ planner behind tpipe_plan_create must emit the
+same per-stage instruction streams and the same byte-exact per-stage peaks
+as the independent oracle (oracle/stream.py), for every strategy, several
+stage counts and micro-batch counts. Also: the C-ABI library loads and
+exports every symbol include/*.h declares."""
+
+import os
+import re
+
+import pytest
+
+from oracle import schedule as S
+from oracle import stream as T
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _plan_mod():
+    from paper_2503_03182_b200 import plan
+    return plan
+
+
+def declared_symbols():
+    names = []
+    for hdr in ("tpipe.h", "tpipe_kernels.h"):
+        src = open(os.path.join(ROOT, "include", hdr)).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        names += re.findall(r"\b(tpipe_\w+)\s*\(", src)
+    return sorted(set(names))
+
+
+def test_library_exports_every_declared_symbol():
+    import ctypes
+    from paper_2503_03182_b200 import LIB_PATH
+    L = ctypes.CDLL(LIB_PATH)
+    missing = [n for n in declared_symbols() if not hasattr(L, n)]
+    assert not missing, missing
+    assert len(declared_symbols()) >= 30
+
+
+def oracle_ops(st):
+    return [dict(kind=i.kind, chunk=i.chunk, mb=i.mb, peer=i.peer, channel=tuple(i.channel),
+                 msg=i.msg) for i in st]
+
+
+def live_trace(ops, size_of):
+    """cumulative live bytes after each instruction's allocs (before frees)."""
+    cur, out = 0, []
+    for o in ops:
+        for a in o["allocs"]:
+            cur += size_of(a)
+        out.append(cur)
+        for f in o["frees"]:
+            cur -= size_of(f)
+    return out
+
+
+CASES = []
+for strat in ("tpipe", "tpipe_trecomp", "1f1b", "1f1b_full_recomp"):
+    for p in (1, 2, 3, 4, 8):
+        for m in (1, 3, 8, 32):
+            CASES.append((strat, p, m))
+
+
+@pytest.mark.parametrize("strategy,p,m", CASES)
+@pytest.mark.parametrize("dtype", [T.BF16, T.FP32])
+def test_streams_and_peaks_match_oracle(strategy, p, m, dtype):
+    P = _plan_mod()
+    L = 2 * p if p > 2 else 4
+    od = T.ModelDesc(L, 64, 4, 256, 128, 32, 2, dtype)
+    pd = P.Model(L, 64, 4, 256, 128, 32, 2, dtype)
+    plan = P.Plan(pd, p, m, strategy=strategy)
+    st, static = T.build_streams(od, p, m, strategy)
+    for s in range(p):
+        got, bufs = plan.ops(s)
+        want = oracle_ops(st[s])
+        strip = [{k: o[k] for k in ("kind", "chunk", "mb", "peer", "channel", "msg")} for o in got]
+        assert strip == want, f"stage {s}"
+        # allocations: same categories and bytes in the same order
+        for g, w in zip(got, st[s]):
+            assert [(bufs[a][1], bufs[a][4]) for a in g["allocs"]] == [(c, b) for _n, c, b in w.allocs]
+            assert len(g["frees"]) == len(w.frees)
+        # identical live-byte trace and peaks
+        sizes = {n: b for ins in st[s] for n, _c, b in ins.allocs}
+        w_trace = live_trace([dict(allocs=[n for n, _c, _b in i.allocs], frees=i.frees)
+                              for i in st[s]], lambda n: sizes[n])
+        g_trace = live_trace(got, lambda a: bufs[a][4])
+        assert g_trace == w_trace
+        r = T.replay(st[s], static[s])
+        pk = plan.peak(s)
+        assert pk["total_peak"] == r["total_peak"]
+        for cat in ("model_state", "io", "act", "recomp_buf", "comm", "workspace"):
+            assert pk[cat] == r.get(cat, 0), cat
+
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+def test_offload_streams_match_oracle(p):
+    P = _plan_mod()
+    od = T.ModelDesc(2 * p, 64, 4, 256, 128, 32, 2, T.BF16)
+    pd = P.Model(2 * p, 64, 4, 256, 128, 32, 2, T.BF16)
+    plan = P.Plan(pd, p, 16, strategy="tpipe_trecomp", offload=P.OFFLOAD_MODEL_STATE)
+    st, static = T.build_streams(od, p, 16, "tpipe_trecomp", offload_model_state=True)
+    for s in range(p):
+        got, _ = plan.ops(s)
+        strip = [{k: o[k] for k in ("kind", "chunk", "mb", "peer", "channel", "msg")} for o in got]
+        assert strip == oracle_ops(st[s])
+        assert plan.peak(s)["total_peak"] == T.replay(st[s], static[s])["total_peak"]
+
+
+@pytest.mark.parametrize("strategy", ["tpipe", "tpipe_trecomp", "1f1b", "1f1b_full_recomp"])
+@pytest.mark.parametrize("p", [1, 2, 4, 5, 8, 16])
+def test_simulate_matches_oracle(strategy, p):
+    """C++ unit-time replay == oracle simulator (makespan and busy time)."""
+    P = _plan_mod()
+    m = 2 * p + 3
+    plan = P.Plan(P.Model(2 * p if p > 1 else 2, 64, 4, 256, 128, 32, 2), p, m, strategy=strategy)
+    orders, v, rec, dur = S.strategy_orders(strategy, p, m)
+    sim = S.simulate(orders, p, v, dur, rec)
+    mk, busy = plan.simulate()
+    assert mk == sim["makespan"]
+    for s in range(p):
+        assert busy[s] == sum(sim["end"][(s, o)] - sim["start"][(s, o)] for o in orders[s])
+
+
+def test_delay_rounds_and_params():
+    P = _plan_mod()
+    for p, k in [(3, 0), (8, 1), (10, 0), (16, 0)]:
+        plan = P.Plan(P.Model(2 * p, 64, 4, 256, 128, 32, 2), p, 2 * p, strategy="tpipe_trecomp")
+        assert plan.k == k == S.delay_rounds(p)
+    od = T.ModelDesc(8, 64, 4, 256, 128, 32, 2)
+    plan = P.Plan(P.Model(8, 64, 4, 256, 128, 32, 2), 4, 8, strategy="tpipe")
+    for s in range(4):
+        for c in (1, 2):
+            assert plan.chunk_params(s, c) == T.chunk_params(od, 4, 2, s, c)
+
+
+def test_budget_escalation_and_errors():
+    P = _plan_mod()
+    from paper_2503_03182_b200._lib import TPipeError
+    md = P.Model(16, 64, 4, 256, 128, 32, 2)
+    a = P.Plan(md, 8, 32, strategy="tpipe")
+    b = P.Plan(md, 8, 32, strategy="tpipe_trecomp")
+    c = P.Plan(md, 8, 32, strategy="tpipe_trecomp", offload=P.OFFLOAD_MODEL_STATE)
+    pa, pb, pc = (max(x.peak(s)["total_peak"] for s in range(8)) for x in (a, b, c))
+    assert pa > pb > pc
+    assert P.Plan(md, 8, 32, hbm_budget=pa, strategy="auto").strategy == P.S_TPIPE
+    auto = P.Plan(md, 8, 32, hbm_budget=pb, strategy="auto")
+    assert (auto.strategy, auto.offload) == (P.S_TPIPE_TRECOMP, 0)
+    auto = P.Plan(md, 8, 32, hbm_budget=pc, strategy="auto")
+    assert (auto.strategy, auto.offload) == (P.S_TPIPE_TRECOMP, 1)
+    with pytest.raises(TPipeError, match="budget"):
+        P.Plan(md, 8, 32, hbm_budget=pc - 1, strategy="auto")
+    with pytest.raises(TPipeError, match="n_layers"):
+        P.Plan(P.Model(15, 64, 4, 256, 128, 32, 2), 8, 32)
+    with pytest.raises(TPipeError, match="hidden"):
+        P.Plan(P.Model(16, 60, 4, 256, 128, 32, 2), 8, 32)
+    with pytest.raises(TPipeError, match="deadlock"):
+        P.Plan(md, 8, 32, strategy="tpipe_trecomp", send_window=1)
