@@ -1,0 +1,375 @@
+#!/usr/bin/env python
+"""bench.py — TPipe training-step throughput on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl tpipe|reference]
+
+Workload (BASELINE.json configs[1]): GPT-3 1.3B (L=24, h=2048, a=16,
+ffn=8192, V=50304), seq 2048, micro-batch 1, m=32 micro-batches per step
+(65,536 tokens), bf16, T-Pipe schedule with p = N pipeline stages (one stage
+per GPU; at N=1 the two T-Pipe chunks run on one GPU). Synthetic seeded
+tokens (uniform < 50257) and random-init weights (N(0, 0.02)).
+
+A "step" is one pass of the whole hot path: every F/B(/R) op of every
+micro-batch in the plan's order, the stage transport, and the AdamW update.
+`value` = tokens/s over all ranks with tokens already resident in HBM;
+`e2e` = the same through tpipe_step with host (pinned) tokens copied in and
+the loss copied out inside the timed region. The step's working set
+(weights + activations, >> 126 MB L2) exceeds L2, so no explicit flush.
+`roofline` = the dominant kernel class (tcgen05 GEMMs), algorithmic 2MNK
+FLOPs / summed CUDA-event durations of its launches, from a profiled pass of
+the same K steps (events on the runtime's launch stream), vs the measured
+sustained bf16 peak in MEASURED_PEAKS.json.
+`cpu_baseline` = the fp64 NumPy oracle (oracle/model.py) doing one
+micro-batch forward+backward of one layer at the same (h, s), scaled to
+model tokens/s (/L), on this host's cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "max trainable params at fixed HBM/GPU; tokens/s vs 1F1B+recomp, 1-8 B200"
+C2 = dict(n_layers=24, hidden=2048, n_heads=16, ffn_hidden=8192, vocab=50304, seq_len=2048,
+          micro_batch=1, vocab_eff=50257, m=32)
+C5 = dict(hidden=4096, n_heads=32, ffn_hidden=16384, vocab=32000, seq_len=8192, micro_batch=1)
+BUDGET = 80 * 2 ** 30
+
+
+def model_flops_per_token(c):
+    """Algorithmic FLOPs/token, causal attention at its triangle:
+    L(72h^2 + 6sh) + 6hV (uses ffn = 4h)."""
+    L, h, s, V = c["n_layers"], c["hidden"], c["seq_len"], c["vocab"]
+    return L * (72 * h * h + 6 * s * h) + 6 * h * V
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, idx):
+        self.idx, self.samples, self.stop = idx, [], threading.Event()
+        self.t = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) > 1 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons}
+
+
+def init_chunk(plan, s, c, rng):
+    """Random-init packed chunk vector (N(0,0.02) matrices, LN gamma 1, zero
+    biases) in the packed order of DESIGN.md §2.3."""
+    from paper_2503_03182_b200 import params as PR
+    h, f = plan.model.hidden, plan.model.ffn_hidden
+    V, sl = plan.model.vocab, plan.model.seq_len
+    shapes = {"wte": (V, h), "wpe": (sl, h), "lnf_g": (h,), "lnf_b": (h,), "w_head": (V, h)}
+    import synth
+    shapes.update(synth.layer_shapes(h, f))
+    parts = []
+    for k, _l in PR.chunk_entries(plan.p, plan.v, plan.layers_chunk, s, c):
+        shp = shapes[k]
+        n = int(np.prod(shp))
+        if len(shp) == 2:
+            parts.append(rng.standard_normal(n, dtype=np.float32) * np.float32(0.02))
+        elif k.endswith("_g"):
+            parts.append(np.ones(n, np.float32))
+        else:
+            parts.append(np.zeros(n, np.float32))
+    return np.concatenate(parts)
+
+
+def cpu_baseline(c, seconds_cap=30.0):
+    """fp64 oracle: one micro-batch forward+backward of ONE layer at (h, s) of
+    the workload; model tokens/s = layer tokens/s / L."""
+    from oracle import model as R
+    import synth
+    h, f, s, a = c["hidden"], c["ffn_hidden"], c["seq_len"], c["n_heads"]
+    W = synth.weights(1, h, f, 64, s, seed=1)
+    L = R.to64(W)["layers"][0]
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((1, s, h))
+    dy = rng.standard_normal((1, s, h))
+    t0 = time.perf_counter()
+    n = 0
+    while True:
+        y, cache = R.layer_fwd(x, L, a)
+        R.layer_bwd(dy, cache, L, a)
+        n += 1
+        if time.perf_counter() - t0 > seconds_cap / 3 or n >= 3:
+            break
+    dt = time.perf_counter() - t0
+    layer_tps = n * s / dt
+    try:
+        from threadpoolctl import threadpool_info
+        blas = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
+    except Exception:
+        blas = None
+    cores = len(os.sched_getaffinity(0))
+    return {"value": layer_tps / c["n_layers"], "unit": "tokens/s", "cores": cores,
+            "blas_threads": blas, "kind": "oracle",
+            "sample": f"{n} x (1 micro-batch fwd+bwd of 1 layer, h={h}, s={s}, fp64 NumPy) "
+                      f"in {dt:.1f}s; model tokens/s = layer tokens/s / L={c['n_layers']}"}
+
+
+def capacity(p, strategies=("1f1b", "tpipe", "tpipe_trecomp", "tpipe_all")):
+    """Max trainable layers / params under an 80 GiB per-GPU plan peak for the
+    C5 sweep shape (h=4096, s=8192), L in steps of p (planner byte model)."""
+    from paper_2503_03182_b200 import plan as P
+    from paper_2503_03182_b200._lib import TPipeError
+    out = {}
+    for st in strategies:
+        strat, off = ("tpipe_trecomp", 1) if st == "tpipe_all" else (st, 0)
+        best = None
+        L = 2 * p
+        while L <= 400:
+            md = P.Model(L, C5["hidden"], C5["n_heads"], C5["ffn_hidden"], C5["vocab"],
+                         C5["seq_len"], C5["micro_batch"], P.BF16)
+            try:
+                pl = P.Plan(md, p, 32, hbm_budget=BUDGET, strategy=strat, offload=off)
+                best = (L, pl.params_total)
+            except TPipeError:
+                break
+            L += 2 * p
+        out[st] = {"max_layers": best[0] if best else 0,
+                   "max_params_B": round(best[1] / 1e9, 2) if best else 0}
+    return out
+
+
+def run_tpipe(args):
+    import torch
+    from paper_2503_03182_b200 import plan as P, runtime as RT
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    N = max(args.gpus, world)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    torch.cuda.set_device(local)
+    c = C2
+    md = P.Model(c["n_layers"], c["hidden"], c["n_heads"], c["ffn_hidden"], c["vocab"],
+                 c["seq_len"], c["micro_batch"], P.BF16)
+    m = c["m"]
+    plan = P.Plan(md, N, m, strategy=args.strategy)
+    ids = None
+    if world > 1:
+        ids = [b"".join(RT.nccl_unique_id() for _ in plan.channels)] if rank == 0 else [None]
+        dist.broadcast_object_list(ids, src=0)
+        ids = ids[0]
+    rt = RT.Runtime(plan, stage=rank if world > 1 else -1, device=local, nccl_ids=ids, lr=1e-4)
+    rng = np.random.default_rng(1234 + rank)
+    stages = [rank] if world > 1 else list(range(N))
+    for s in stages:
+        for ch in range(1, plan.v + 1):
+            rt.set_params(s, ch, init_chunk(plan, s, ch, rng))
+    import synth
+    tok, tgt = synth.tokens(c["vocab"], m, c["micro_batch"], c["seq_len"], step=0,
+                            vocab_eff=c["vocab_eff"])
+    dtok = torch.tensor(tok, dtype=torch.int32, device="cuda")
+    dtgt = torch.tensor(tgt, dtype=torch.int32, device="cuda")
+    ext = torch.cuda.ExternalStream(rt.stream())
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+
+    def timed(fn, k):
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(ext)
+        for _ in range(k):
+            fn()
+        e1.record(ext)
+        barrier()
+        ms = e0.elapsed_time(e1)
+        if dist:
+            t = torch.tensor([ms])
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t[0])
+        return ms
+
+    for _ in range(args.warmup):
+        rt.step_device(dtok.data_ptr(), dtgt.data_ptr())
+    with Clocks(local) as clk:
+        ms = timed(lambda: rt.step_device(dtok.data_ptr(), dtgt.data_ptr()), args.steps)
+    launches = rt.stats()["kernel_launches"]
+    # e2e: host tokens (pinned) -> tpipe_step (H2D inside) -> loss D2H
+    htok = torch.from_numpy(tok).pin_memory().numpy()
+    htgt = torch.from_numpy(tgt).pin_memory().numpy()
+    ms_e2e = timed(lambda: rt.step(htok, htgt), args.steps)
+    # profiled pass of the same K steps: per-kernel-class CUDA-event timing
+    kms = np.zeros(4)
+    kfl = np.zeros(4)
+    kcnt = np.zeros(4)
+    for _ in range(args.steps):
+        rt.step_device(dtok.data_ptr(), dtgt.data_ptr(), RT.STEP_PROFILE)
+        st = rt.stats()
+        kms += st["kernel_ms"]
+        kfl += st["kernel_flops"]
+        kcnt += st["kernel_count"]
+    hw = rt.stats()["pool_high_water"]
+    tokens = m * c["micro_batch"] * c["seq_len"]
+    value = tokens * args.steps / (ms / 1e3)
+    e2e = tokens * args.steps / (ms_e2e / 1e3)
+    hbm, pk_burst, pk_sust, src = peaks()
+    gemm_tf = kfl[0] / (kms[0] / 1e3) / 1e12 if kms[0] else None
+    step_ms = ms / args.steps
+    prof_step_ms = None
+    out = None
+    if rank == 0:
+        mfu = value * model_flops_per_token(c) / (N * pk_sust * 1e12)
+        out = {
+            "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": N,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic (seeded uniform tokens < 50257; random-init weights)",
+            "config": {"workload": "configs[1]: GPT-3 1.3B, seq 2048, T-Pipe, m=32 micro-batches",
+                       "model": "gpt3-1.3b", "n_layers": 24, "hidden": 2048, "seq_len": 2048,
+                       "micro_batch": 1, "n_microbatches": m, "global_batch_tokens": tokens,
+                       "strategy": args.strategy, "parallelism": f"pp{N}",
+                       "layers_per_chunk": list(plan.layers_chunk),
+                       "l2": "working set >> 126 MB L2 (no flush needed)"},
+            "mfu": round(mfu, 4),
+            "mfu_peak": f"{pk_sust} TFLOP/s bf16 sustained ({src})",
+            "gpu_launches": int(launches) * args.steps,
+            "pool_high_water_bytes": hw,
+            "e2e": {"value": round(e2e, 1), "unit": "tokens/s",
+                    "h2d_bytes_per_step": int(2 * tok.nbytes), "d2h_bytes_per_step": 4 * m},
+            "roofline": {"bound": "tensor", "kernel": "tcgen05 GEMMs (all K1/K2/K8 launches)",
+                         "achieved": round(gemm_tf, 1) if gemm_tf else None, "peak": pk_sust,
+                         "unit": "TFLOP/s",
+                         "frac": round(gemm_tf / pk_sust, 4) if gemm_tf else None,
+                         "traffic": None, "peak_src": f"bf16_tflops_sustained ({src})",
+                         "launches_per_step": int(kcnt[0] / args.steps),
+                         "share_of_step": round(kms[0] / args.steps / step_ms, 3)},
+            "kernel_classes": {
+                "gemm": {"ms_per_step": round(kms[0] / args.steps, 2), "tflops": round(gemm_tf, 1) if gemm_tf else None},
+                "attn_fwd": {"ms_per_step": round(kms[1] / args.steps, 2),
+                             "tflops": round(kfl[1] / (kms[1] / 1e3) / 1e12, 1) if kms[1] else None},
+                "attn_bwd": {"ms_per_step": round(kms[2] / args.steps, 2),
+                             "tflops": round(kfl[2] / (kms[2] / 1e3) / 1e12, 1) if kms[2] else None}},
+            "clocks": clk.summary(),
+        }
+    rt.close()
+    del rt
+    if rank == 0 and not args.no_extras and world == 1:
+        out["capacity_80GiB"] = {"p": N, "shape": "h=4096 a=32 s=8192 V=32000 b=1 m=32",
+                                 **capacity(max(N, 8) if N == 1 else N)}
+        out["cpu_baseline"] = cpu_baseline(c)
+    if dist:
+        dist.barrier()
+    return out
+
+
+def run_reference(args):
+    """Reference arm: the oracle (oracle/model.py) as it stands, on host
+    cores, same metric/config; each step = a bounded sample (one micro-batch
+    fwd+bwd of one layer), reported as model tokens/s."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    from oracle import model as R
+    import synth
+    c = C2
+    h, f, s, a = c["hidden"], c["ffn_hidden"], c["seq_len"], c["n_heads"]
+    W = synth.weights(1, h, f, 64, s, seed=1)
+    L = R.to64(W)["layers"][0]
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((1, s, h))
+    dy = rng.standard_normal((1, s, h))
+
+    def step():
+        y, cache = R.layer_fwd(x, L, a)
+        R.layer_bwd(dy, cache, L, a)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    value = s * args.steps / dt / c["n_layers"]
+    cores = len(os.sched_getaffinity(0))
+    sample = (f"per step: 1 micro-batch fwd+bwd of 1 of {c['n_layers']} layers "
+              f"(h={h}, s={s}, fp64 NumPy), scaled /L to model tokens/s")
+    return {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "tokens/s",
+            "n_gpus": max(args.gpus, world), "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(dt / args.steps * 1e3, 1), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": "configs[1]: GPT-3 1.3B, seq 2048",
+                                            "model": "gpt3-1.3b", "seq_len": s},
+            "cpu_baseline": {"value": round(value, 3), "unit": "tokens/s", "cores": cores,
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": round(value, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="tpipe", choices=["tpipe", "reference"])
+    ap.add_argument("--strategy", default="tpipe", choices=["tpipe", "tpipe_trecomp", "1f1b"])
+    ap.add_argument("--no-extras", action="store_true", help="skip capacity sweep and CPU oracle")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    out = run_reference(args) if args.impl == "reference" else run_tpipe(args)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -175,11 +175,19 @@ typedef struct {
     int64_t  step;                  /* completed steps */
     double   offload_d2h_bytes, offload_h2d_bytes;   /* last step */
     double   host_opt_ms;           /* last host optimizer duration */
+    /* TPIPE_STEP_PROFILE only: per kernel class (0 GEMM, 1 attention fwd,
+     * 2 attention bwd), summed CUDA-event durations of the launches in the
+     * last step (ms), launch counts and algorithmic FLOPs (2MNK for GEMMs,
+     * causal-triangle counts for attention). */
+    double   kernel_ms[4];
+    double   kernel_flops[4];
+    int64_t  kernel_count[4];
 } tpipe_runtime_stats;
 
 typedef struct tpipe_runtime tpipe_runtime;
 
 #define TPIPE_STEP_NO_OPT 1u        /* skip optimizer ops: gradients stay accumulated */
+#define TPIPE_STEP_PROFILE 2u       /* bracket GEMM / attention launches with CUDA events */
 
 int tpipe_runtime_create(const tpipe_plan* plan, const tpipe_runtime_opts* opts,
                          tpipe_runtime** out);

@@ -68,24 +68,24 @@ def attn_fwd(q, k, v):
     d = q.shape[-1]
     s = q.shape[-2]
     scale = 1.0 / math.sqrt(d)
-    S = np.einsum("basd,batd->bast", q, k) * scale
+    S = (q @ k.swapaxes(-1, -2)) * scale                  # [b, a, s, s]
     mask = np.triu(np.ones((s, s), dtype=bool), k=1)       # j > i masked
     S = np.where(mask, -np.inf, S)
     Smax = S.max(axis=-1, keepdims=True)
     E = np.exp(S - Smax)
     P = E / E.sum(axis=-1, keepdims=True)
-    O = np.einsum("bast,batd->basd", P, v)
+    O = P @ v
     lse = (Smax + np.log(E.sum(axis=-1, keepdims=True)))[..., 0]
     return O, (q, k, v, P, scale), lse
 
 
 def attn_bwd(dO, cache):
     q, k, v, P, scale = cache
-    dV = np.einsum("bast,basd->batd", P, dO)
-    dP = np.einsum("basd,batd->bast", dO, v)
+    dV = P.swapaxes(-1, -2) @ dO
+    dP = dO @ v.swapaxes(-1, -2)
     dS = P * (dP - (dP * P).sum(axis=-1, keepdims=True))
-    dQ = np.einsum("bast,batd->basd", dS, k) * scale
-    dK = np.einsum("bast,basd->batd", dS, q) * scale
+    dQ = (dS @ k) * scale
+    dK = (dS.swapaxes(-1, -2) @ q) * scale
     return dQ, dK, dV
 
 

@@ -50,7 +50,9 @@ class RuntimeOpts(C.Structure):
 class RuntimeStats(C.Structure):
     _fields_ = [("pool_high_water", u64 * 64), ("pool_reserved", u64), ("kernel_launches", i64),
                 ("step", i64), ("offload_d2h_bytes", C.c_double),
-                ("offload_h2d_bytes", C.c_double), ("host_opt_ms", C.c_double)]
+                ("offload_h2d_bytes", C.c_double), ("host_opt_ms", C.c_double),
+                ("kernel_ms", C.c_double * 4), ("kernel_flops", C.c_double * 4),
+                ("kernel_count", i64 * 4)]
 
 
 def declare(L):

@@ -174,6 +174,7 @@ int attn_fwd_simt(int dtype, const void* qkv, void* o, float* lse, int b, int s,
         attn_fwd_simt_kernel<bf16><<<grid, 128, 0, st>>>((const bf16*)qkv, (bf16*)o, lse, s, a, d);
     else
         attn_fwd_simt_kernel<float><<<grid, 128, 0, st>>>((const float*)qkv, (float*)o, lse, s, a, d);
+    note_launches(1);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
@@ -193,6 +194,7 @@ int attn_bwd_simt(int dtype, const void* qkv, const void* o, const void* dout, c
         attn_bwd_dkv_kernel<float><<<grid, 128, 0, st>>>((const float*)qkv, (const float*)dout, lse,
                                                          ws, (float*)dqkv, s, a, d);
     }
+    note_launches(3);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 

@@ -31,6 +31,7 @@ int embed_fwd(int dtype, const int* tok, const void* wte, const void* wpe, void*
     else
         embed_fwd_kernel<float><<<blocks, 256, 0, st>>>(tok, (const float*)wte, (const float*)wpe,
                                                         (float*)x, rows, s, h);
+    note_launches(1);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
@@ -113,6 +114,7 @@ int embed_bwd(int dtype, const int* tok, const void* dx, float* dwte, float* dwp
         embed_wte_bwd_kernel<float><<<rows, 256, 0, st>>>(ws, (const float*)dx, dwte, rows, h);
         embed_wpe_bwd_kernel<float><<<wpe_blocks, 256, 0, st>>>((const float*)dx, dwpe, rows, s, h);
     }
+    note_launches(3);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
@@ -169,6 +171,7 @@ int ce_fwd(const float* logits, const int* tgt, float* lse, float* loss_out, flo
     if (rows <= 0) return 0;
     ce_lse_kernel<<<rows, 512, 0, st>>>(logits, lse, V);
     ce_loss_kernel<<<1, 1024, 0, st>>>(logits, tgt, lse, loss_out, scale, rows, V);
+    note_launches(2);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
@@ -193,6 +196,7 @@ int ce_bwd(int dtype, const float* logits, const int* tgt, const float* lse, voi
         ce_bwd_kernel<bf16><<<blocks, 256, 0, st>>>(logits, tgt, lse, (bf16*)dlogits, scale, rows, V);
     else
         ce_bwd_kernel<float><<<blocks, 256, 0, st>>>(logits, tgt, lse, (float*)dlogits, scale, rows, V);
+    note_launches(1);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
@@ -223,6 +227,7 @@ int adamw(int dtype, float* master, float* m, float* v, float* grad, void* w, lo
     else  // fp32: the weight IS the master
         adamw_kernel<float><<<blocks, 256, 0, st>>>(master, m, v, grad,
                                                     (float*)(w == master ? nullptr : w), n, decay, hp);
+    note_launches(1);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
@@ -244,6 +249,7 @@ int cast_f32_to(int dtype, const float* src, void* dst, long n, cudaStream_t st)
         cast_kernel<bf16><<<blocks, 256, 0, st>>>(src, (bf16*)dst, n);
     else
         cast_kernel<float><<<blocks, 256, 0, st>>>(src, (float*)dst, n);
+    note_launches(1);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 

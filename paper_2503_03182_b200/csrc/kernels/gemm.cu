@@ -208,6 +208,7 @@ int gemm_simt(int dtype, const GemmDesc& g, cudaStream_t st) {
         gemm_simt_kernel<bf16><<<grid, 256, 0, st>>>(g);
     else
         gemm_simt_kernel<float><<<grid, 256, 0, st>>>(g);
+    note_launches(1);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
@@ -444,6 +445,7 @@ static int launch_tc(const GemmDesc& g, cudaStream_t st) {
         attr_set = true;
     }
     kern<<<grid, 256, Cfg::SMEM, st>>>(ta, tb, g, num_m, num_n, num_kb);
+    note_launches(1);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 

@@ -96,6 +96,10 @@ void adamw_host(float* master, float* m, float* v, const float* grad, uint16_t* 
                 int decay, const AdamHyper& hp);
 
 // ---------------------------------------------------------------- misc
+// count of kernels launched by this library (gpu_launches evidence)
+void note_launches(int n);
+long launch_count();
+void host_cast_bf16(const float* src, uint16_t* dst, long n);
 int fill_zero(void* p, size_t bytes, cudaStream_t st);
 int cast_f32_to(int dtype, const float* src, void* dst, long n, cudaStream_t st);
 

@@ -111,6 +111,7 @@ int ln_fwd(int dtype, const void* x, const void* gamma, const void* beta, void* 
     else
         ln_fwd_kernel<float><<<blocks, threads, 0, st>>>((const float*)x, (const float*)gamma,
                                                          (const float*)beta, (float*)y, mean, rstd, rows, h, 0);
+    note_launches(1);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
@@ -128,6 +129,7 @@ int ln_apply(int dtype, const void* x, const void* gamma, const void* beta, cons
                                                          (const float*)beta, (float*)y,
                                                          const_cast<float*>(mean),
                                                          const_cast<float*>(rstd), rows, h, 1);
+    note_launches(1);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
@@ -227,6 +229,7 @@ int ln_bwd(int dtype, const void* dy, const void* x, const void* gamma, const fl
     }
     reduce_blocks_kernel<<<(h + 255) / 256, 256, 0, st>>>(ws, dgamma, h, nblk);
     reduce_blocks_kernel<<<(h + 255) / 256, 256, 0, st>>>(ws + (long)nblk * h, dbeta, h, nblk);
+    note_launches(4);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
@@ -251,6 +254,7 @@ int colsum_acc(int dtype, const void* X, float* out, float* ws, int rows, int n,
     else
         colsum_partial_kernel<float><<<pg, 256, 0, st>>>((const float*)X, ws, rows, n);
     reduce_blocks_kernel<<<(n + 255) / 256, 256, 0, st>>>(ws, out, n, nblk);
+    note_launches(2);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 

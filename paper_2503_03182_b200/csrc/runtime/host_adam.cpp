@@ -3,6 +3,7 @@
 // device kernel (adam_math.h), compiled with -ffp-contract=off, so the result
 // is bit-identical to tpipe::adamw on the GPU. Multithreaded over contiguous
 // slices (order of elements is irrelevant: the update is elementwise).
+#include <atomic>
 #include <cstring>
 #include <thread>
 #include <vector>
@@ -28,6 +29,14 @@ static void adamw_host_range(float* master, float* m, float* v, const float* gra
         v[i] = o.v;
         if (w_bf16) w_bf16[i] = f32_to_bf16_rne(o.w);
     }
+}
+
+static std::atomic<long> g_launches{0};
+void note_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+long launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+void host_cast_bf16(const float* src, uint16_t* dst, long n) {
+    for (long i = 0; i < n; ++i) dst[i] = f32_to_bf16_rne(src[i]);
 }
 
 void adamw_host(float* master, float* m, float* v, const float* grad, uint16_t* w_bf16, long n,

@@ -1,0 +1,25 @@
+// NCCL entry points resolved with dlopen (libnccl.so.2: the copy torch loads,
+// or the system one), so libtpipe.so has no link-time NCCL dependency and the
+// single-GPU path never touches it.
+#pragma once
+
+#include <nccl.h>
+
+namespace tpipe {
+
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    bool ok = false;
+};
+
+// nullptr if NCCL cannot be loaded
+const NcclApi* nccl();
+
+}  // namespace tpipe

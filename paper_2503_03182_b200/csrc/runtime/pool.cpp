@@ -1,0 +1,96 @@
+#include "runtime/pool.h"
+
+#include <algorithm>
+
+namespace tpipe {
+
+static constexpr size_t ALIGN = 256;
+
+int Pool::init(size_t bytes, int n_stages) {
+    release();
+    cur_.assign(n_stages, 0);
+    hw_.assign(n_stages, 0);
+    limit_.assign(n_stages, 0);
+    bytes = (bytes + ALIGN - 1) / ALIGN * ALIGN;
+    if (bytes) {
+        if (cudaMalloc(&base_, bytes) != cudaSuccess) {
+            base_ = nullptr;
+            return -1;
+        }
+        cap_ = bytes;
+        free_[0] = bytes;
+    }
+    return 0;
+}
+
+void Pool::release() {
+    if (base_) cudaFree(base_);
+    for (void* p : overflow_) cudaFree(p);
+    base_ = nullptr;
+    cap_ = 0;
+    overflow_.clear();
+    overflow_bytes_ = 0;
+    free_.clear();
+    used_.clear();
+    req_.clear();
+}
+
+void* Pool::alloc(int stage, uint64_t bytes) {
+    const size_t need = std::max<size_t>(ALIGN, (bytes + ALIGN - 1) / ALIGN * ALIGN);
+    // best fit
+    auto best = free_.end();
+    for (auto it = free_.begin(); it != free_.end(); ++it)
+        if (it->second >= need && (best == free_.end() || it->second < best->second)) best = it;
+    void* p = nullptr;
+    if (best != free_.end()) {
+        const size_t off = best->first, sz = best->second;
+        free_.erase(best);
+        if (sz > need) free_[off + need] = sz - need;
+        p = base_ + off;
+        used_[p] = {off, need};
+    } else {
+        // arena exhausted by fragmentation: dedicated block (physical only; the
+        // ledger below is unaffected)
+        if (cudaMalloc(&p, need) != cudaSuccess) return nullptr;
+        overflow_.push_back(p);
+        overflow_bytes_ += need;
+        used_[p] = {SIZE_MAX, need};
+    }
+    req_[p] = bytes;
+    cur_[stage] += bytes;
+    hw_[stage] = std::max(hw_[stage], cur_[stage]);
+    if (limit_[stage] && cur_[stage] > limit_[stage]) over_cap_ = true;
+    return p;
+}
+
+void Pool::free(int stage, void* p) {
+    auto it = used_.find(p);
+    if (it == used_.end()) return;
+    const size_t off = it->second.first, sz = it->second.second;
+    used_.erase(it);
+    cur_[stage] -= req_[p];
+    req_.erase(p);
+    if (off == SIZE_MAX) {
+        cudaFree(p);
+        overflow_.erase(std::find(overflow_.begin(), overflow_.end(), p));
+        overflow_bytes_ -= sz;
+        return;
+    }
+    size_t o = off, s = sz;
+    auto nxt = free_.lower_bound(o);
+    if (nxt != free_.end() && nxt->first == o + s) {
+        s += nxt->second;
+        nxt = free_.erase(nxt);
+    }
+    if (nxt != free_.begin()) {
+        auto prv = std::prev(nxt);
+        if (prv->first + prv->second == o) {
+            o = prv->first;
+            s += prv->second;
+            free_.erase(prv);
+        }
+    }
+    free_[o] = s;
+}
+
+}  // namespace tpipe

@@ -1,0 +1,738 @@
+// tpipe_runtime / tpipe_step: executes a plan's per-stage instruction streams
+// (SURVEY CS2, §8(a) a2-a9).
+//
+// * Every buffer is allocated from the HBM pool at the instruction the plan
+//   names and released at the instruction the plan names, so the pool's
+//   ledger high-water equals the plan's byte-exact peak (tpipe_plan_stage_peak).
+// * Transport: stage >= 0 -> one process per GPU, one 2-rank NCCL
+//   communicator + stream per FIFO channel (kind, src, dst), send window by
+//   SEND_WAIT events; stage == -1 -> all stages in this process on one GPU
+//   with device-to-device copies (a virtual pipeline used for parity tests).
+// * T-Offload: GRAD_D2H on a copy-engine stream, HOST_OPT on a host
+//   thread (bit-identical AdamW), W_H2D on a second copy stream in the next
+//   step's warm-up, W_WAIT before the first deep-chunk forward.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <memory>
+#include <new>
+#include <thread>
+#include <tuple>
+#include <vector>
+
+#include "kernels/kernels.h"
+#include "plan/plan.h"
+#include "runtime/errors.h"
+#include "runtime/nccl_dl.h"
+#include "runtime/pool.h"
+#include "runtime/stage.h"
+#include "tpipe.h"
+
+
+
+using namespace tpipe;
+
+#define TP_API extern "C" __attribute__((visibility("default")))
+
+#define CU(x)                                                                          \
+    do {                                                                               \
+        cudaError_t _e = (x);                                                          \
+        if (_e != cudaSuccess)                                                         \
+            return set_error(TPIPE_E_CUDA, "%s: %s", #x, cudaGetErrorString(_e));      \
+    } while (0)
+
+#define TRY(x)               \
+    do {                     \
+        int _rc = (x);       \
+        if (_rc) return _rc; \
+    } while (0)
+
+namespace {
+
+struct ChunkState {
+    long P = 0;
+    bool offloaded = false;
+    ParamLayout lay;
+    StashLayout sl;
+    void* w = nullptr;
+    float *grad = nullptr, *master = nullptr, *m = nullptr, *v = nullptr;
+    // T-Offload host side (pinned)
+    float *h_master = nullptr, *h_m = nullptr, *h_v = nullptr, *h_grad = nullptr;
+    void* h_w = nullptr;
+    cudaEvent_t ev_d2h = nullptr, ev_h2d = nullptr;
+    bool d2h_pending = false, h2d_pending = false;
+    std::thread host_thr;
+    double host_ms = 0;
+};
+
+struct StageState {
+    int s = 0;
+    ChunkState ch[3];
+    int* tokens = nullptr;
+    int* targets = nullptr;
+    float* loss_slots = nullptr;
+    std::vector<void*> bufptr;
+    std::map<std::tuple<int, int, int>, void*> live;
+    size_t pc = 0;
+};
+
+struct Channel {
+    int kind = 0, src = 0, dst = 0;
+    std::deque<void*> q;  // virtual transport: sender buffers in FIFO order
+    int popped = 0;
+    ncclComm_t comm = nullptr;
+    cudaStream_t st = nullptr;
+    std::vector<cudaEvent_t> send_done;
+};
+
+}  // namespace
+
+struct tpipe_runtime {
+    tpipe_plan plan;                 // deep copy (immutable)
+    int stage_sel = -1, device = 0;
+    Dims D;
+    std::vector<int> owned;
+    std::vector<std::unique_ptr<StageState>> st;   // indexed by stage (null if not owned)
+    std::vector<Channel> ch;
+    Pool pool;
+    cudaStream_t stream = nullptr, d2h = nullptr, h2d = nullptr;
+    cudaEvent_t ev_tmp = nullptr;
+    AdamHyper hp{};
+    float lr = 3e-4f, b1 = 0.9f, b2 = 0.95f, eps = 1e-8f, wd = 0.1f;
+    long t = 0;
+    long launches_last = 0;
+    double d2h_bytes = 0, h2d_bytes = 0;
+    int* h_tok_stage = nullptr;   // pinned staging for tpipe_step host inputs
+    size_t h_tok_bytes = 0;
+    std::vector<cudaEvent_t> evpool;
+    size_t evnext = 0;
+    double kms[4] = {0, 0, 0, 0}, kflops[4] = {0, 0, 0, 0};
+    int64_t kcount[4] = {0, 0, 0, 0};
+
+    explicit tpipe_runtime(const tpipe_plan& p) : plan(p), D(p.model) {}
+};
+
+namespace {
+
+cudaEvent_t next_event(tpipe_runtime* rt) {
+    if (rt->evnext == rt->evpool.size()) {
+        cudaEvent_t e;
+        cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        rt->evpool.push_back(e);
+    }
+    return rt->evpool[rt->evnext++];
+}
+
+AdamHyper hyper(const tpipe_runtime* rt, long step) {
+    AdamHyper h;
+    h.lr = rt->lr;
+    h.b1 = rt->b1;
+    h.b2 = rt->b2;
+    h.eps = rt->eps;
+    h.wd = rt->wd;
+    h.bc1 = (float)(1.0 - std::pow((double)rt->b1, (double)step));
+    h.bc2 = (float)(1.0 - std::pow((double)rt->b2, (double)step));
+    return h;
+}
+
+std::tuple<int, int, int> key_of(const tpipe_buf& b) { return {b.role, b.chunk, b.mb}; }
+
+void* live_get(StageState& S, int role, int chunk, int mb) {
+    auto it = S.live.find({role, chunk, mb});
+    return it == S.live.end() ? nullptr : it->second;
+}
+
+int op_alloc_ptr(tpipe_runtime* rt, StageState& S, const tpipe_op& op, int role, int chunk_or_any,
+                 void** out) {
+    const auto& ev = rt->plan.events[S.s];
+    const auto& bufs = rt->plan.bufs[S.s];
+    for (int e = 0; e < op.n_alloc; ++e) {
+        const int id = ev[op.alloc_first + e];
+        if (bufs[id].role == role && (chunk_or_any < 0 || bufs[id].chunk == chunk_or_any)) {
+            *out = S.bufptr[id];
+            return 1;
+        }
+    }
+    *out = nullptr;
+    return 0;
+}
+
+int adam_chunk(tpipe_runtime* rt, ChunkState& C, const AdamHyper& hp, cudaStream_t st) {
+    const int dt = rt->D.dtype;
+    for (auto& sg : C.lay.segments) {
+        const long off = sg[0], n = sg[1];
+        void* w = dt == DT_BF16 ? (void*)((uint16_t*)C.w + off) : (void*)(C.master + off);
+        if (adamw(dt, C.master + off, C.m + off, C.v + off, C.grad + off, w, n, (int)sg[2], hp, st))
+            return set_error(TPIPE_E_CUDA, "adamw launch failed");
+    }
+    return 0;
+}
+
+void host_opt_run(tpipe_runtime* rt, ChunkState* C, AdamHyper hp) {
+    auto t0 = std::chrono::steady_clock::now();
+    cudaEventSynchronize(C->ev_d2h);
+    uint16_t* wb = rt->D.dtype == DT_BF16 ? (uint16_t*)C->h_w : nullptr;
+    for (auto& sg : C->lay.segments) {
+        const long off = sg[0], n = sg[1];
+        adamw_host(C->h_master + off, C->h_m + off, C->h_v + off, C->h_grad + off,
+                   wb ? wb + off : nullptr, n, (int)sg[2], hp);
+    }
+    C->host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+void join_host(ChunkState& C) {
+    if (C.host_thr.joinable()) C.host_thr.join();
+}
+
+// ------------------------------------------------------------------ one instruction
+int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags) {
+    const int s = S.s;
+    const auto& P = rt->plan;
+    const auto& bufs = P.bufs[s];
+    const auto& ev = P.events[s];
+    const Dims& D = rt->D;
+    cudaStream_t cs = rt->stream;
+    const int p = P.p, v = P.v;
+    const bool trecomp = P.strategy == TPIPE_S_TPIPE_TRECOMP;
+    const bool no_opt = flags & TPIPE_STEP_NO_OPT;
+
+    // allocations at instruction start
+    for (int e = 0; e < op.n_alloc; ++e) {
+        const int id = ev[op.alloc_first + e];
+        void* ptr = rt->pool.alloc(s, bufs[id].bytes);
+        if (!ptr) return set_error(TPIPE_E_CUDA, "pool allocation of %llu bytes failed",
+                                   (unsigned long long)bufs[id].bytes);
+        S.bufptr[id] = ptr;
+        S.live[key_of(bufs[id])] = ptr;
+    }
+    if (rt->pool.over_cap())
+        return set_error(TPIPE_E_OOM, "stage %d ledger exceeds the plan peak (ledger bug)", s);
+
+    const int c = op.chunk, i = op.mb;
+    switch (op.kind) {
+        case TPIPE_OP_F:
+        case TPIPE_OP_R: {
+            ChunkState& C = S.ch[c];
+            const bool emb = (s == 0 && c == 1);
+            FwdArgs a{};
+            a.in = emb ? nullptr : live_get(S, TPIPE_BUF_IN, c, i);
+            a.tokens = S.tokens ? S.tokens + (long)(i - 1) * D.M : nullptr;
+            a.targets = (S.targets && s == p - 1 && c == v) ? S.targets + (long)(i - 1) * D.M : nullptr;
+            a.loss_slot = S.loss_slots ? S.loss_slots + (i - 1) : nullptr;
+            a.loss_scale = 1.0f / ((float)P.m * (float)D.M);
+            void* ws = nullptr;
+            op_alloc_ptr(rt, S, op, TPIPE_BUF_WS, -1, &ws);
+            a.ws = (uint8_t*)ws;
+            if (op.kind == TPIPE_OP_R) {
+                void* rb;
+                op_alloc_ptr(rt, S, op, TPIPE_BUF_RBUF, -1, &rb);
+                a.stash = (uint8_t*)rb;
+                a.out = nullptr;
+                a.targets = nullptr;
+            } else {
+                void* stp;
+                if (!op_alloc_ptr(rt, S, op, TPIPE_BUF_STASH, -1, &stp))
+                    op_alloc_ptr(rt, S, op, TPIPE_BUF_TSTASH, -1, &stp);
+                a.stash = (uint8_t*)stp;
+                void* out = nullptr;
+                if (!op_alloc_ptr(rt, S, op, TPIPE_BUF_MSG, -1, &out))
+                    op_alloc_ptr(rt, S, op, TPIPE_BUF_IN, c + 1, &out);
+                a.out = out;
+            }
+            if (!a.stash || !a.ws || (!emb && !a.in))
+                return set_error(TPIPE_E_STATE, "stage %d op %d: missing buffer", s, op.kind);
+            ChunkParamsDev cp{&C.lay, C.w, C.grad};
+            if (chunk_forward(D, C.sl, cp, a, cs))
+                return set_error(TPIPE_E_CUDA, "chunk_forward failed: %s",
+                                 cudaGetErrorString(cudaGetLastError()));
+            break;
+        }
+        case TPIPE_OP_B: {
+            ChunkState& C = S.ch[c];
+            const bool emb = (s == 0 && c == 1), head = (s == p - 1 && c == v);
+            BwdArgs a{};
+            a.in = emb ? nullptr : live_get(S, TPIPE_BUF_IN, c, i);
+            a.tokens = S.tokens ? S.tokens + (long)(i - 1) * D.M : nullptr;
+            a.targets = head ? S.targets + (long)(i - 1) * D.M : nullptr;
+            a.loss_scale = 1.0f / ((float)P.m * (float)D.M);
+            void* stp = (trecomp && c == 1) ? live_get(S, TPIPE_BUF_RBUF, c, i)
+                                            : live_get(S, TPIPE_BUF_STASH, c, i);
+            a.stash = (uint8_t*)stp;
+            void* ws = nullptr;
+            op_alloc_ptr(rt, S, op, TPIPE_BUF_WS, -1, &ws);
+            a.ws = (uint8_t*)ws;
+            a.gin = head ? nullptr : live_get(S, TPIPE_BUF_GIN, c, i);
+            void* gout = nullptr;
+            if (!op_alloc_ptr(rt, S, op, TPIPE_BUF_MSG, -1, &gout))
+                op_alloc_ptr(rt, S, op, TPIPE_BUF_GIN, c - 1, &gout);
+            a.gout = gout;
+            if (!a.stash || !a.ws || (!emb && !a.in) || (!head && !a.gin) || (!emb && !a.gout))
+                return set_error(TPIPE_E_STATE, "stage %d B(%d,%d): missing buffer", s, c, i);
+            ChunkParamsDev cp{&C.lay, C.w, C.grad};
+            if (chunk_backward(D, C.sl, cp, a, cs))
+                return set_error(TPIPE_E_CUDA, "chunk_backward failed: %s",
+                                 cudaGetErrorString(cudaGetLastError()));
+            break;
+        }
+        case TPIPE_OP_RECV_ACT:
+        case TPIPE_OP_RECV_GRAD: {
+            Channel& chn = rt->ch[op.channel];
+            void* dst = nullptr;
+            op_alloc_ptr(rt, S, op, op.kind == TPIPE_OP_RECV_ACT ? TPIPE_BUF_IN : TPIPE_BUF_GIN, -1, &dst);
+            const size_t bytes = (size_t)D.M * D.h * D.es;
+            if (rt->stage_sel < 0) {
+                void* src = chn.q.front();
+                chn.q.pop_front();
+                chn.popped++;
+                CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, cs));
+            } else {
+                const NcclApi* N = nccl();
+                cudaEvent_t e0 = next_event(rt), e1 = next_event(rt);
+                CU(cudaEventRecord(e0, cs));
+                CU(cudaStreamWaitEvent(chn.st, e0, 0));
+                ncclResult_t r = N->Recv(dst, bytes, ncclUint8, 0, chn.comm, chn.st);
+                if (r != ncclSuccess) return set_error(TPIPE_E_NCCL, "ncclRecv: %s", N->GetErrorString(r));
+                CU(cudaEventRecord(e1, chn.st));
+                CU(cudaStreamWaitEvent(cs, e1, 0));
+            }
+            break;
+        }
+        case TPIPE_OP_SEND_ACT:
+        case TPIPE_OP_SEND_GRAD: {
+            Channel& chn = rt->ch[op.channel];
+            void* src = live_get(S, TPIPE_BUF_MSG, op.channel, op.msg);
+            if (!src) return set_error(TPIPE_E_STATE, "send buffer missing");
+            const size_t bytes = (size_t)D.M * D.h * D.es;
+            if (rt->stage_sel < 0) {
+                chn.q.push_back(src);
+            } else {
+                const NcclApi* N = nccl();
+                cudaEvent_t e0 = next_event(rt);
+                CU(cudaEventRecord(e0, cs));
+                CU(cudaStreamWaitEvent(chn.st, e0, 0));
+                ncclResult_t r = N->Send(src, bytes, ncclUint8, 1, chn.comm, chn.st);
+                if (r != ncclSuccess) return set_error(TPIPE_E_NCCL, "ncclSend: %s", N->GetErrorString(r));
+                if ((int)chn.send_done.size() <= op.msg) chn.send_done.resize(op.msg + 1, nullptr);
+                chn.send_done[op.msg] = next_event(rt);
+                CU(cudaEventRecord(chn.send_done[op.msg], chn.st));
+            }
+            break;
+        }
+        case TPIPE_OP_SEND_WAIT: {
+            if (rt->stage_sel >= 0) {
+                Channel& chn = rt->ch[op.channel];
+                CU(cudaStreamWaitEvent(cs, chn.send_done[op.msg], 0));
+            }
+            break;
+        }
+        case TPIPE_OP_OPT:
+            if (!no_opt) TRY(adam_chunk(rt, S.ch[c], hyper(rt, rt->t + 1), cs));
+            break;
+        case TPIPE_OP_GRAD_D2H: {
+            if (no_opt) break;
+            ChunkState& C = S.ch[c];
+            cudaEvent_t e0 = next_event(rt);
+            CU(cudaEventRecord(e0, cs));
+            CU(cudaStreamWaitEvent(rt->d2h, e0, 0));
+            CU(cudaMemcpyAsync(C.h_grad, C.grad, (size_t)C.P * 4, cudaMemcpyDeviceToHost, rt->d2h));
+            CU(cudaMemsetAsync(C.grad, 0, (size_t)C.P * 4, rt->d2h));
+            CU(cudaEventRecord(C.ev_d2h, rt->d2h));
+            C.d2h_pending = true;
+            rt->d2h_bytes += (double)C.P * 4;
+            break;
+        }
+        case TPIPE_OP_HOST_OPT: {
+            if (no_opt) break;
+            ChunkState& C = S.ch[c];
+            join_host(C);
+            C.host_thr = std::thread(host_opt_run, rt, &C, hyper(rt, rt->t + 1));
+            break;
+        }
+        case TPIPE_OP_W_H2D: {
+            ChunkState& C = S.ch[c];
+            join_host(C);
+            CU(cudaMemcpyAsync(C.w, C.h_w, (size_t)C.P * D.es, cudaMemcpyHostToDevice, rt->h2d));
+            CU(cudaEventRecord(C.ev_h2d, rt->h2d));
+            C.h2d_pending = true;
+            rt->h2d_bytes += (double)C.P * D.es;
+            break;
+        }
+        case TPIPE_OP_W_WAIT: {
+            ChunkState& C = S.ch[c];
+            if (C.h2d_pending) CU(cudaStreamWaitEvent(cs, C.ev_h2d, 0));
+            if (C.d2h_pending) CU(cudaStreamWaitEvent(cs, C.ev_d2h, 0));
+            C.h2d_pending = C.d2h_pending = false;
+            break;
+        }
+        default:
+            return set_error(TPIPE_E_STATE, "unknown op kind %d", op.kind);
+    }
+
+    // releases at instruction end
+    for (int e = 0; e < op.n_free; ++e) {
+        const int id = ev[op.free_first + e];
+        rt->pool.free(s, S.bufptr[id]);
+        S.live.erase(key_of(bufs[id]));
+        S.bufptr[id] = nullptr;
+    }
+    return 0;
+}
+
+bool op_ready(tpipe_runtime* rt, const tpipe_op& op) {
+    if (rt->stage_sel >= 0) return true;
+    if (op.kind == TPIPE_OP_RECV_ACT || op.kind == TPIPE_OP_RECV_GRAD) return !rt->ch[op.channel].q.empty();
+    if (op.kind == TPIPE_OP_SEND_WAIT) return rt->ch[op.channel].popped > op.msg;
+    return true;
+}
+
+int run_step(tpipe_runtime* rt, const int32_t* tok_dev, const int32_t* tgt_dev, uint32_t flags,
+             float* loss_out) {
+    const auto& P = rt->plan;
+    const Dims& D = rt->D;
+    cudaStream_t cs = rt->stream;
+    const size_t io_bytes = (size_t)P.m * D.M * 4;
+    rt->evnext = 0;
+    rt->d2h_bytes = rt->h2d_bytes = 0;
+    const long l0 = launch_count();
+    profiler().begin_step((flags & TPIPE_STEP_PROFILE) != 0);
+    for (int s : rt->owned) {
+        StageState& S = *rt->st[s];
+        S.pc = 0;
+        if (s == 0 && tok_dev) CU(cudaMemcpyAsync(S.tokens, tok_dev, io_bytes, cudaMemcpyDeviceToDevice, cs));
+        if (s == P.p - 1) {
+            if (tgt_dev) CU(cudaMemcpyAsync(S.targets, tgt_dev, io_bytes, cudaMemcpyDeviceToDevice, cs));
+            CU(cudaMemsetAsync(S.loss_slots, 0, (size_t)P.m * 4, cs));
+        }
+    }
+    for (auto& c : rt->ch) {
+        c.q.clear();
+        c.popped = 0;
+        c.send_done.clear();
+    }
+    size_t remaining = 0;
+    for (int s : rt->owned) remaining += P.ops[s].size();
+    while (remaining) {
+        bool prog = false;
+        for (int s : rt->owned) {
+            StageState& S = *rt->st[s];
+            const auto& ops = P.ops[s];
+            while (S.pc < ops.size() && op_ready(rt, ops[S.pc])) {
+                TRY(exec_op(rt, S, ops[S.pc], flags));
+                S.pc++;
+                remaining--;
+                prog = true;
+            }
+        }
+        if (!prog) return set_error(TPIPE_E_DEADLOCK, "virtual transport made no progress");
+    }
+    float loss = 0.f;
+    if (std::find(rt->owned.begin(), rt->owned.end(), P.p - 1) != rt->owned.end()) {
+        std::vector<float> slots(P.m);
+        CU(cudaMemcpyAsync(slots.data(), rt->st[P.p - 1]->loss_slots, (size_t)P.m * 4,
+                           cudaMemcpyDeviceToHost, cs));
+        CU(cudaStreamSynchronize(cs));
+        for (float x : slots) loss += x;   // micro-batch index order
+    } else {
+        CU(cudaStreamSynchronize(cs));
+    }
+    if (loss_out) *loss_out = loss;
+    if (flags & TPIPE_STEP_PROFILE) {
+        profiler().collect(rt->kms, rt->kflops, rt->kcount);
+        profiler().on = false;
+    }
+    if (!(flags & TPIPE_STEP_NO_OPT)) rt->t += 1;
+    rt->launches_last = launch_count() - l0;
+    return 0;
+}
+
+}  // namespace
+
+// ================================================================== C-ABI
+TP_API int tpipe_runtime_create(const tpipe_plan* plan, const tpipe_runtime_opts* opts,
+                                tpipe_runtime** out) {
+    if (!plan || !out) return set_error(TPIPE_E_INVALID, "NULL argument");
+    *out = nullptr;
+    tpipe_runtime_opts o{};
+    o.stage = -1;
+    if (opts) o = *opts;
+    if (o.stage < -1 || o.stage >= plan->p) return set_error(TPIPE_E_INVALID, "stage");
+    if (plan->strategy == TPIPE_S_1F1B_FULL_RECOMP)
+        return set_error(TPIPE_E_INCOMPAT, "1F1B+full-recompute runtime not built yet");
+    if ((long)plan->model.micro_batch * plan->model.seq_len % 8)
+        return set_error(TPIPE_E_INVALID, "micro_batch*seq_len must be a multiple of 8");
+    std::unique_ptr<tpipe_runtime> rt(new (std::nothrow) tpipe_runtime(*plan));
+    if (!rt) return set_error(TPIPE_E_INVALID, "out of host memory");
+    rt->stage_sel = o.stage;
+    rt->device = o.device;
+    if (o.lr > 0) rt->lr = o.lr;
+    if (o.beta1 > 0) rt->b1 = o.beta1;
+    if (o.beta2 > 0) rt->b2 = o.beta2;
+    if (o.eps > 0) rt->eps = o.eps;
+    if (o.weight_decay > 0) rt->wd = o.weight_decay;
+    CU(cudaSetDevice(o.device));
+    CU(cudaStreamCreateWithFlags(&rt->stream, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&rt->d2h, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&rt->h2d, cudaStreamNonBlocking));
+    const tpipe_plan& P = rt->plan;
+    const Dims& D = rt->D;
+    if (o.stage < 0) {
+        for (int s = 0; s < P.p; ++s) rt->owned.push_back(s);
+    } else {
+        rt->owned.push_back(o.stage);
+    }
+    uint64_t need = 0;
+    for (int s : rt->owned) need += P.peak[s].total_peak;
+    if (rt->pool.init((size_t)(need * 1.08) + (256ull << 20), P.p))
+        return set_error(TPIPE_E_CUDA, "pool: cudaMalloc of %llu bytes failed", (unsigned long long)need);
+    rt->st.resize(P.p);
+    const bool off = (P.offload & TPIPE_OFFLOAD_MODEL_STATE) != 0;
+    for (int s : rt->owned) {
+        rt->pool.set_cap(s, o.pool_cap ? o.pool_cap : P.peak[s].total_peak);
+        auto S = std::make_unique<StageState>();
+        S->s = s;
+        S->bufptr.assign(P.bufs[s].size(), nullptr);
+        for (size_t id = 0; id < P.bufs[s].size(); ++id) {
+            const tpipe_buf& b = P.bufs[s][id];
+            if (b.role != TPIPE_BUF_STATIC) continue;
+            void* ptr = rt->pool.alloc(s, b.bytes);
+            if (!ptr) return set_error(TPIPE_E_CUDA, "pool: static allocation failed");
+            S->bufptr[id] = ptr;
+            CU(cudaMemset(ptr, 0, b.bytes));
+            if (b.category == TPIPE_CAT_MODEL_STATE) {
+                const int c = b.chunk;
+                ChunkState& C = S->ch[c];
+                const bool emb = (s == 0 && c == 1), head = (s == P.p - 1 && c == P.v);
+                C.lay = make_param_layout(P.model, P.layers[c - 1], emb, head);
+                C.sl = make_stash_layout(P.model, P.layers[c - 1], emb, head);
+                C.P = C.lay.total;
+                if ((uint64_t)C.P != P.chunk_params[s][c - 1])
+                    return set_error(TPIPE_E_STATE, "param layout mismatch");
+                C.offloaded = off && c == P.v;
+                uint8_t* q = (uint8_t*)ptr;
+                C.w = q;
+                q += (size_t)C.P * D.es;
+                C.grad = (float*)q;
+                q += (size_t)C.P * 4;
+                if (!C.offloaded) {
+                    if (D.dtype == DT_BF16) {
+                        C.master = (float*)q;
+                        q += (size_t)C.P * 4;
+                    } else {
+                        C.master = (float*)C.w;
+                    }
+                    C.m = (float*)q;
+                    q += (size_t)C.P * 4;
+                    C.v = (float*)q;
+                } else {
+                    CU(cudaHostAlloc(&C.h_master, (size_t)C.P * 4, cudaHostAllocDefault));
+                    CU(cudaHostAlloc(&C.h_m, (size_t)C.P * 4, cudaHostAllocDefault));
+                    CU(cudaHostAlloc(&C.h_v, (size_t)C.P * 4, cudaHostAllocDefault));
+                    CU(cudaHostAlloc(&C.h_grad, (size_t)C.P * 4, cudaHostAllocDefault));
+                    std::memset(C.h_m, 0, (size_t)C.P * 4);
+                    std::memset(C.h_v, 0, (size_t)C.P * 4);
+                    if (D.dtype == DT_BF16) CU(cudaHostAlloc(&C.h_w, (size_t)C.P * 2, cudaHostAllocDefault));
+                    else C.h_w = C.h_master;
+                    CU(cudaEventCreateWithFlags(&C.ev_d2h, cudaEventDisableTiming));
+                    CU(cudaEventCreateWithFlags(&C.ev_h2d, cudaEventDisableTiming));
+                }
+            } else if (b.category == TPIPE_CAT_IO) {
+                if (b.mb == 0) S->tokens = (int*)ptr;
+                else {
+                    S->targets = (int*)ptr;
+                    S->loss_slots = (float*)((uint8_t*)ptr + (size_t)P.m * D.M * 4);
+                }
+            }
+        }
+        rt->st[s] = std::move(S);
+    }
+    // channels
+    rt->ch.resize(P.channels.size());
+    for (size_t c = 0; c < P.channels.size(); ++c) {
+        rt->ch[c].kind = P.channels[c][0];
+        rt->ch[c].src = P.channels[c][1];
+        rt->ch[c].dst = P.channels[c][2];
+    }
+    if (o.stage >= 0 && P.p > 1) {
+        const NcclApi* N = nccl();
+        if (!N) return set_error(TPIPE_E_NCCL, "libnccl.so.2 not loadable");
+        if (!o.nccl_ids) return set_error(TPIPE_E_INVALID, "nccl_ids required for stage >= 0");
+        const ncclUniqueId* ids = (const ncclUniqueId*)o.nccl_ids;
+        N->GroupStart();
+        for (size_t c = 0; c < rt->ch.size(); ++c) {
+            Channel& chn = rt->ch[c];
+            if (chn.src != o.stage && chn.dst != o.stage) continue;
+            CU(cudaStreamCreateWithFlags(&chn.st, cudaStreamNonBlocking));
+            ncclResult_t r = N->CommInitRank(&chn.comm, 2, ids[c], chn.src == o.stage ? 0 : 1);
+            if (r != ncclSuccess && r != ncclInProgress) {
+                N->GroupEnd();
+                return set_error(TPIPE_E_NCCL, "ncclCommInitRank: %s", N->GetErrorString(r));
+            }
+        }
+        ncclResult_t r = N->GroupEnd();
+        if (r != ncclSuccess) return set_error(TPIPE_E_NCCL, "ncclGroupEnd: %s", N->GetErrorString(r));
+    }
+    CU(cudaDeviceSynchronize());
+    *out = rt.release();
+    return 0;
+}
+
+TP_API void tpipe_runtime_destroy(tpipe_runtime* rt) {
+    if (!rt) return;
+    cudaSetDevice(rt->device);
+    cudaDeviceSynchronize();
+    for (int s : rt->owned) {
+        for (auto& C : rt->st[s]->ch) {
+            join_host(C);
+            if (C.h_master) cudaFreeHost(C.h_master);
+            if (C.h_m) cudaFreeHost(C.h_m);
+            if (C.h_v) cudaFreeHost(C.h_v);
+            if (C.h_grad) cudaFreeHost(C.h_grad);
+            if (C.h_w && C.h_w != C.h_master) cudaFreeHost(C.h_w);
+            if (C.ev_d2h) cudaEventDestroy(C.ev_d2h);
+            if (C.ev_h2d) cudaEventDestroy(C.ev_h2d);
+        }
+    }
+    if (const NcclApi* N = nccl())
+        for (auto& c : rt->ch)
+            if (c.comm) N->CommDestroy(c.comm);
+    for (auto& c : rt->ch)
+        if (c.st) cudaStreamDestroy(c.st);
+    for (auto e : rt->evpool) cudaEventDestroy(e);
+    if (rt->h_tok_stage) cudaFreeHost(rt->h_tok_stage);
+    rt->pool.release();
+    cudaStreamDestroy(rt->stream);
+    cudaStreamDestroy(rt->d2h);
+    cudaStreamDestroy(rt->h2d);
+    delete rt;
+}
+
+static int chunk_of(tpipe_runtime* rt, int32_t s, int32_t c, uint64_t n, ChunkState** out) {
+    if (!rt || s < 0 || s >= rt->plan.p || !rt->st[s]) return set_error(TPIPE_E_INVALID, "stage not owned");
+    if (c < 1 || c > rt->plan.v) return set_error(TPIPE_E_INVALID, "chunk");
+    ChunkState& C = rt->st[s]->ch[c];
+    if ((uint64_t)C.P != n) return set_error(TPIPE_E_INVALID, "n (%llu) != chunk params (%ld)",
+                                             (unsigned long long)n, C.P);
+    *out = &C;
+    return 0;
+}
+
+TP_API int tpipe_runtime_set_params(tpipe_runtime* rt, int32_t s, int32_t c, const float* src,
+                                    uint64_t n) {
+    ChunkState* C;
+    TRY(chunk_of(rt, s, c, n, &C));
+    join_host(*C);
+    CU(cudaSetDevice(rt->device));
+    CU(cudaStreamSynchronize(rt->stream));
+    // stream-ordered copies: a pageable cudaMemcpy may return before its DMA
+    // lands, so the cast kernel below must be ordered on the same stream
+    if (!C->offloaded) {
+        CU(cudaMemcpyAsync(C->master, src, n * 4, cudaMemcpyHostToDevice, rt->stream));
+        if (rt->D.dtype == DT_BF16) {
+            if (cast_f32_to(DT_BF16, C->master, C->w, (long)n, rt->stream))
+                return set_error(TPIPE_E_CUDA, "cast");
+        }
+        CU(cudaMemsetAsync(C->m, 0, n * 4, rt->stream));
+        CU(cudaMemsetAsync(C->v, 0, n * 4, rt->stream));
+    } else {
+        std::memcpy(C->h_master, src, n * 4);
+        std::memset(C->h_m, 0, n * 4);
+        std::memset(C->h_v, 0, n * 4);
+        if (rt->D.dtype == DT_BF16) host_cast_bf16(C->h_master, (uint16_t*)C->h_w, (long)n);
+        CU(cudaMemcpyAsync(C->w, C->h_w, n * rt->D.es, cudaMemcpyHostToDevice, rt->stream));
+    }
+    CU(cudaMemsetAsync(C->grad, 0, n * 4, rt->stream));
+    CU(cudaStreamSynchronize(rt->stream));
+    rt->t = 0;
+    return 0;
+}
+
+TP_API int tpipe_runtime_get_params(tpipe_runtime* rt, int32_t s, int32_t c, float* dst, uint64_t n) {
+    ChunkState* C;
+    TRY(chunk_of(rt, s, c, n, &C));
+    join_host(*C);
+    CU(cudaStreamSynchronize(rt->stream));
+    if (C->offloaded) std::memcpy(dst, C->h_master, n * 4);
+    else CU(cudaMemcpyAsync(dst, C->master, n * 4, cudaMemcpyDeviceToHost, rt->stream));
+    CU(cudaStreamSynchronize(rt->stream));
+    return 0;
+}
+
+TP_API int tpipe_runtime_get_grads(tpipe_runtime* rt, int32_t s, int32_t c, float* dst, uint64_t n) {
+    ChunkState* C;
+    TRY(chunk_of(rt, s, c, n, &C));
+    CU(cudaStreamSynchronize(rt->stream));
+    CU(cudaStreamSynchronize(rt->d2h));
+    CU(cudaMemcpyAsync(dst, C->grad, n * 4, cudaMemcpyDeviceToHost, rt->stream));
+    CU(cudaStreamSynchronize(rt->stream));
+    return 0;
+}
+
+TP_API int tpipe_step_device(tpipe_runtime* rt, const int32_t* tok, const int32_t* tgt, uint32_t flags,
+                             float* loss_out) {
+    if (!rt) return set_error(TPIPE_E_INVALID, "runtime is NULL");
+    CU(cudaSetDevice(rt->device));
+    return run_step(rt, tok, tgt, flags, loss_out);
+}
+
+TP_API int tpipe_step(tpipe_runtime* rt, const int32_t* tokens, const int32_t* targets, uint32_t flags,
+                      float* loss_out) {
+    if (!rt) return set_error(TPIPE_E_INVALID, "runtime is NULL");
+    CU(cudaSetDevice(rt->device));
+    const auto& P = rt->plan;
+    const size_t io = (size_t)P.m * rt->D.M * 4;
+    if (rt->h_tok_bytes < 2 * io) {
+        if (rt->h_tok_stage) cudaFreeHost(rt->h_tok_stage);
+        CU(cudaHostAlloc(&rt->h_tok_stage, 2 * io, cudaHostAllocDefault));
+        rt->h_tok_bytes = 2 * io;
+    }
+    // host -> pinned staging -> HBM (the H2D is part of the step)
+    for (int s : rt->owned) {
+        StageState& S = *rt->st[s];
+        if (s == 0 && tokens) {
+            std::memcpy(rt->h_tok_stage, tokens, io);
+            CU(cudaMemcpyAsync(S.tokens, rt->h_tok_stage, io, cudaMemcpyHostToDevice, rt->stream));
+        }
+        if (s == P.p - 1 && targets) {
+            std::memcpy((uint8_t*)rt->h_tok_stage + io, targets, io);
+            CU(cudaMemcpyAsync(S.targets, (uint8_t*)rt->h_tok_stage + io, io, cudaMemcpyHostToDevice,
+                               rt->stream));
+        }
+    }
+    return run_step(rt, nullptr, nullptr, flags, loss_out);
+}
+
+TP_API int tpipe_runtime_get_stats(const tpipe_runtime* rt, tpipe_runtime_stats* out) {
+    if (!rt || !out) return set_error(TPIPE_E_INVALID, "NULL argument");
+    std::memset(out, 0, sizeof(*out));
+    for (int s : rt->owned)
+        if (s < 64) out->pool_high_water[s] = rt->pool.high_water(s);
+    out->pool_reserved = rt->pool.reserved();
+    out->kernel_launches = rt->launches_last;
+    out->step = rt->t;
+    out->offload_d2h_bytes = rt->d2h_bytes;
+    out->offload_h2d_bytes = rt->h2d_bytes;
+    for (int s : rt->owned)
+        for (auto& C : rt->st[s]->ch) out->host_opt_ms += C.host_ms;
+    for (int c = 0; c < 4; ++c) {
+        out->kernel_ms[c] = rt->kms[c];
+        out->kernel_flops[c] = rt->kflops[c];
+        out->kernel_count[c] = rt->kcount[c];
+    }
+    return 0;
+}
+
+TP_API void* tpipe_runtime_stream(const tpipe_runtime* rt) { return rt ? (void*)rt->stream : nullptr; }
+
+TP_API int tpipe_nccl_unique_id(void* out128) {
+    const NcclApi* N = nccl();
+    if (!N) return set_error(TPIPE_E_NCCL, "libnccl.so.2 not loadable");
+    if (!out128) return set_error(TPIPE_E_INVALID, "NULL argument");
+    ncclResult_t r = N->GetUniqueId((ncclUniqueId*)out128);
+    if (r != ncclSuccess) return set_error(TPIPE_E_NCCL, "ncclGetUniqueId: %s", N->GetErrorString(r));
+    return 0;
+}

@@ -1,0 +1,396 @@
+// Per-chunk forward / block-wise recompute / backward of the pre-LN GPT block
+// stack (model reading DESIGN.md §2 = SURVEY N-1).
+//
+// Per layer, forward:
+//   LN1 -> QKV GEMM(+bias) -> causal attention -> out-proj GEMM(+bias+residual)
+//   -> LN2 -> FC1 GEMM(+bias, GELU fused: u stashed, g transient)
+//   -> FC2 GEMM(+bias+residual).
+// Saved per layer (20h+16+4a bytes/token in bf16, N-2 with op-level recompute):
+//   x_in, LN1 stats, qkv, attn out, LSE, x_mid, LN2 stats, u.
+// Backward recomputes LN outputs from saved stats and GELU(u) inside the FC2
+// dgrad epilogue (operator-level recompute), and P from the LSE in
+// the attention backward. Weight gradients accumulate (fp32, beta = 1) per
+// micro-batch in index order; no atomics anywhere, so recompute on/off and
+// offload on/off give bit-identical gradients.
+#include "runtime/stage.h"
+
+#include <array>
+
+namespace tpipe {
+
+Dims::Dims(const tpipe_model_desc& d)
+    : dtype(d.dtype == TPIPE_BF16 ? DT_BF16 : DT_FP32),
+      M(d.micro_batch * d.seq_len),
+      h(d.hidden),
+      a(d.n_heads),
+      hd(d.hidden / d.n_heads),
+      f(d.ffn_hidden),
+      V(d.vocab),
+      s(d.seq_len),
+      b(d.micro_batch),
+      es(d.dtype == TPIPE_BF16 ? 2 : 4) {}
+
+ParamLayout make_param_layout(const tpipe_model_desc& d, int n_layers, bool emb, bool head) {
+    ParamLayout P;
+    P.emb = emb;
+    P.head = head;
+    const long h = d.hidden, f = d.ffn_hidden, V = d.vocab, s = d.seq_len;
+    long off = 0;
+    auto seg = [&](long n, int decay) {
+        P.segments.push_back({off, n, decay});
+        long o = off;
+        off += n;
+        return o;
+    };
+    if (emb) {
+        P.wte = seg(V * h, 1);
+        P.wpe = seg(s * h, 1);
+    }
+    const long sizes[N_LAYER_TENSORS] = {h, h, 3 * h * h, 3 * h, h * h, h, h, h, f * h, f, h * f, h};
+    const int decay[N_LAYER_TENSORS] = {0, 0, 1, 0, 1, 0, 0, 0, 1, 0, 1, 0};
+    for (int l = 0; l < n_layers; ++l) {
+        std::array<long, N_LAYER_TENSORS> o{};
+        for (int t = 0; t < N_LAYER_TENSORS; ++t) o[t] = seg(sizes[t], decay[t]);
+        P.layer.push_back(o);
+    }
+    if (head) {
+        P.lnf_g = seg(h, 0);
+        P.lnf_b = seg(h, 0);
+        P.w_head = seg(V * h, 1);
+    }
+    P.total = off;
+    return P;
+}
+
+StashLayout make_stash_layout(const tpipe_model_desc& d, int n_layers, bool emb, bool head) {
+    StashLayout S;
+    const long M = (long)d.micro_batch * d.seq_len, h = d.hidden, a = d.n_heads, f = d.ffn_hidden;
+    const long es = d.dtype == TPIPE_BF16 ? 2 : 4;
+    long off = 0;
+    auto take = [&](long bytes) {
+        long o = off;
+        off += bytes;
+        return o;
+    };
+    for (int l = 0; l < n_layers; ++l) {
+        StashLayout::L L;
+        L.x_in = (l == 0 && !emb) ? -1 : take(M * h * es);
+        L.ln1_mean = take(4 * M);
+        L.ln1_rstd = take(4 * M);
+        L.qkv = take(3 * M * h * es);
+        L.o = take(M * h * es);
+        L.lse = take(4 * a * M);
+        L.x_mid = take(M * h * es);
+        L.ln2_mean = take(4 * M);
+        L.ln2_rstd = take(4 * M);
+        L.u = take(M * f * es);
+        S.layer.push_back(L);
+    }
+    if (head) {
+        S.x_f = take(M * h * es);
+        S.lnf_mean = take(4 * M);
+        S.lnf_rstd = take(4 * M);
+        S.ce_lse = take(4 * M);
+    }
+    S.total = off;
+    return S;
+}
+
+// ---------------------------------------------------------------- helpers
+#define TRY(x)                        \
+    do {                              \
+        int _rc = (x);                \
+        if (_rc) return _rc;          \
+    } while (0)
+
+template <typename T>
+static inline T* at(void* base, long byte_off) {
+    return reinterpret_cast<T*>(reinterpret_cast<uint8_t*>(base) + byte_off);
+}
+
+KernelProfiler& profiler() {
+    static KernelProfiler P;
+    return P;
+}
+cudaEvent_t KernelProfiler::ev() {
+    if (next == pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        pool.push_back(e);
+    }
+    return pool[next++];
+}
+void KernelProfiler::collect(double ms[4], double flops[4], int64_t count[4]) {
+    for (int c = 0; c < 4; ++c) ms[c] = flops[c] = 0, count[c] = 0;
+    for (auto& r : recs) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, r.a, r.b);
+        ms[r.cls] += t;
+        flops[r.cls] += r.flops;
+        count[r.cls] += 1;
+    }
+}
+KernelProfiler::~KernelProfiler() {
+    for (auto e : pool) cudaEventDestroy(e);
+}
+
+// bracket one launch with events when profiling
+struct ProfScope {
+    KernelProfiler& P;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr;
+    int cls;
+    double flops;
+    ProfScope(int c, double f, cudaStream_t s) : P(profiler()), st(s), cls(c), flops(f) {
+        if (P.on) {
+            a = P.ev();
+            cudaEventRecord(a, st);
+        }
+    }
+    ~ProfScope() {
+        if (P.on) {
+            cudaEvent_t b = P.ev();
+            cudaEventRecord(b, st);
+            P.recs.push_back({a, b, cls, flops});
+        }
+    }
+};
+
+static int mm(const Dims& D, int M, int N, int K, const void* A, long lda, int ak, const void* B,
+              long ldb, int bk, int epi, void* C, long ldc, const void* bias = nullptr,
+              const void* R = nullptr, long ldr = 0, void* C2 = nullptr, long ldc2 = 0,
+              const void* aux = nullptr, long ldaux = 0, cudaStream_t st = nullptr) {
+    GemmDesc g;
+    g.M = M; g.N = N; g.K = K;
+    g.A = A; g.lda = lda; g.a_kmajor = ak;
+    g.B = B; g.ldb = ldb; g.b_kmajor = bk;
+    g.epi = epi; g.C = C; g.ldc = ldc; g.bias = bias; g.res = R; g.ldr = ldr;
+    g.C2 = C2; g.ldc2 = ldc2; g.aux = aux; g.ldaux = ldaux;
+    ProfScope ps(0, 2.0 * M * N * K, st);
+    return gemm(D.dtype, g, st) ? -7 : 0;
+}
+
+struct LayerPtrs {  // one layer's saved tensors
+    const void* x_in;
+    float *ln1_mean, *ln1_rstd;
+    void *qkv, *o;
+    float* lse;
+    void* x_mid;
+    float *ln2_mean, *ln2_rstd;
+    void* u;
+};
+
+static LayerPtrs layer_ptrs(const StashLayout::L& L, uint8_t* stash, const void* x_in) {
+    LayerPtrs p;
+    p.x_in = L.x_in >= 0 ? (const void*)(stash + L.x_in) : x_in;
+    p.ln1_mean = at<float>(stash, L.ln1_mean);
+    p.ln1_rstd = at<float>(stash, L.ln1_rstd);
+    p.qkv = stash + L.qkv;
+    p.o = stash + L.o;
+    p.lse = at<float>(stash, L.lse);
+    p.x_mid = stash + L.x_mid;
+    p.ln2_mean = at<float>(stash, L.ln2_mean);
+    p.ln2_rstd = at<float>(stash, L.ln2_rstd);
+    p.u = stash + L.u;
+    return p;
+}
+
+struct LW {  // one layer's weights (es) and fp32 grads
+    const void* w[N_LAYER_TENSORS];
+    float* g[N_LAYER_TENSORS];
+};
+
+static LW layer_w(const Dims& D, const ChunkParamsDev& P, int l) {
+    LW r;
+    for (int t = 0; t < N_LAYER_TENSORS; ++t) {
+        r.w[t] = reinterpret_cast<const uint8_t*>(P.w) + P.lay->layer[l][t] * D.es;
+        r.g[t] = P.grad + P.lay->layer[l][t];
+    }
+    return r;
+}
+
+// forward of one layer: x_in -> out, saving into lp; ws_ln [M,h], ws_g [M,f]
+static int layer_forward(const Dims& D, const LW& W, const LayerPtrs& lp, void* ws_ln, void* ws_g,
+                         void* out, cudaStream_t st) {
+    const int M = D.M, h = D.h, f = D.f;
+    TRY(ln_fwd(D.dtype, lp.x_in, W.w[LN1_G], W.w[LN1_B], ws_ln, lp.ln1_mean, lp.ln1_rstd, M, h, st));
+    TRY(mm(D, M, 3 * h, h, ws_ln, h, 1, W.w[W_QKV], h, 1, EPI_BIAS, lp.qkv, 3 * h, W.w[B_QKV],
+           nullptr, 0, nullptr, 0, nullptr, 0, st));
+    {
+        ProfScope ps(1, 4.0 * D.b * D.a * (0.5 * D.s * (D.s + 1)) * D.hd, st);
+        TRY(attn_fwd(D.dtype, lp.qkv, lp.o, lp.lse, D.b, D.s, D.a, D.hd, st));
+    }
+    TRY(mm(D, M, h, h, lp.o, h, 1, W.w[W_O], h, 1, EPI_BIAS_RES, lp.x_mid, h, W.w[B_O], lp.x_in, h,
+           nullptr, 0, nullptr, 0, st));
+    TRY(ln_fwd(D.dtype, lp.x_mid, W.w[LN2_G], W.w[LN2_B], ws_ln, lp.ln2_mean, lp.ln2_rstd, M, h, st));
+    TRY(mm(D, M, f, h, ws_ln, h, 1, W.w[W_1], h, 1, EPI_BIAS_GELU, lp.u, f, W.w[B_1], nullptr, 0,
+           ws_g, f, nullptr, 0, st));
+    TRY(mm(D, M, h, f, ws_g, f, 1, W.w[W_2], f, 1, EPI_BIAS_RES, out, h, W.w[B_2], lp.x_mid, h,
+           nullptr, 0, nullptr, 0, st));
+    return 0;
+}
+
+// backward workspace carve-up (ws_b)
+struct BwdWs {
+    void *G0, *G1, *du, *g, *ln, *dln, *dout;
+    void* dqkv;
+    float* Dv;
+    float* part;
+    uint8_t* rbuf;  // one-layer recompute buffer (full-recompute strategy)
+    void *lnf, *dlnf;
+    float* logits;
+    void* dlogits;
+    int* emb_ws;
+};
+
+static BwdWs carve_bwd(const Dims& D, uint8_t* ws, bool head, bool emb, long part_elems,
+                       long rbuf_bytes) {
+    const long M = D.M, h = D.h, f = D.f, es = D.es;
+    BwdWs w;
+    long off = 0;
+    auto take = [&](long bytes) {
+        uint8_t* p = ws + off;
+        off += bytes;
+        return p;
+    };
+    w.G0 = take(M * h * es);
+    w.G1 = take(M * h * es);
+    w.du = take(M * f * es);
+    w.g = take(M * f * es);
+    w.ln = take(M * h * es);
+    w.dln = take(M * h * es);
+    w.dout = take(M * h * es);
+    w.dqkv = take(3 * M * h * es);
+    w.Dv = reinterpret_cast<float*>(take(4L * D.a * M));
+    w.part = reinterpret_cast<float*>(take(4 * part_elems));
+    w.rbuf = rbuf_bytes ? take(rbuf_bytes) : nullptr;
+    w.lnf = w.dlnf = w.dlogits = nullptr;
+    w.logits = nullptr;
+    if (head) {
+        w.lnf = take(M * h * es);
+        w.dlnf = take(M * h * es);
+        w.logits = reinterpret_cast<float*>(take(4 * M * D.V));
+        w.dlogits = take(M * D.V * es);
+    }
+    w.emb_ws = emb ? reinterpret_cast<int*>(take(8 * M)) : nullptr;
+    return w;
+}
+
+// backward of one layer: dy -> dx (dx may alias G0 == dy buffer: dy is fully
+// consumed before the LN1 backward writes dx)
+static int layer_backward(const Dims& D, const LW& W, const LayerPtrs& lp, const void* dy, void* dx,
+                          const BwdWs& w, cudaStream_t st) {
+    const int M = D.M, h = D.h, f = D.f, dt = D.dtype;
+    // FC2: dg = dy W2 (dGELU fused: du = dg * gelu'(u), g = gelu(u) recomputed)
+    TRY(mm(D, M, f, h, dy, h, 1, W.w[W_2], f, 0, EPI_DGELU, w.du, f, nullptr, nullptr, 0, w.g, f,
+           lp.u, f, st));
+    TRY(mm(D, h, f, M, dy, h, 0, w.g, f, 0, EPI_ACC_F32, W.g[W_2], f, nullptr, nullptr, 0, nullptr,
+           0, nullptr, 0, st));
+    TRY(colsum_acc(dt, dy, W.g[B_2], w.part, M, h, st));
+    // FC1
+    TRY(ln_apply(dt, lp.x_mid, W.w[LN2_G], W.w[LN2_B], lp.ln2_mean, lp.ln2_rstd, w.ln, M, h, st));
+    TRY(mm(D, f, h, M, w.du, f, 0, w.ln, h, 0, EPI_ACC_F32, W.g[W_1], h, nullptr, nullptr, 0,
+           nullptr, 0, nullptr, 0, st));
+    TRY(colsum_acc(dt, w.du, W.g[B_1], w.part, M, f, st));
+    TRY(mm(D, M, h, f, w.du, f, 1, W.w[W_1], h, 0, EPI_STORE, w.dln, h, nullptr, nullptr, 0,
+           nullptr, 0, nullptr, 0, st));
+    TRY(ln_bwd(dt, w.dln, lp.x_mid, W.w[LN2_G], lp.ln2_mean, lp.ln2_rstd, dy, w.G1, W.g[LN2_G],
+               W.g[LN2_B], w.part, M, h, st));
+    // out-proj
+    TRY(mm(D, h, h, M, w.G1, h, 0, lp.o, h, 0, EPI_ACC_F32, W.g[W_O], h, nullptr, nullptr, 0,
+           nullptr, 0, nullptr, 0, st));
+    TRY(colsum_acc(dt, w.G1, W.g[B_O], w.part, M, h, st));
+    TRY(mm(D, M, h, h, w.G1, h, 1, W.w[W_O], h, 0, EPI_STORE, w.dout, h, nullptr, nullptr, 0,
+           nullptr, 0, nullptr, 0, st));
+    // attention (P recomputed from LSE)
+    {
+        // algorithmic: P recompute + dV, dP, dQ, dK = 5 GEMMs over the causal triangle
+        ProfScope ps(2, 10.0 * D.b * D.a * (0.5 * D.s * (D.s + 1)) * D.hd, st);
+        TRY(attn_bwd(dt, lp.qkv, lp.o, w.dout, lp.lse, w.dqkv, w.Dv, D.b, D.s, D.a, D.hd, st));
+    }
+    // QKV
+    TRY(ln_apply(dt, lp.x_in, W.w[LN1_G], W.w[LN1_B], lp.ln1_mean, lp.ln1_rstd, w.ln, M, h, st));
+    TRY(mm(D, 3 * h, h, M, w.dqkv, 3 * h, 0, w.ln, h, 0, EPI_ACC_F32, W.g[W_QKV], h, nullptr,
+           nullptr, 0, nullptr, 0, nullptr, 0, st));
+    TRY(colsum_acc(dt, w.dqkv, W.g[B_QKV], w.part, M, 3 * h, st));
+    TRY(mm(D, M, h, 3 * h, w.dqkv, 3 * h, 1, W.w[W_QKV], h, 0, EPI_STORE, w.dln, h, nullptr,
+           nullptr, 0, nullptr, 0, nullptr, 0, st));
+    TRY(ln_bwd(dt, w.dln, lp.x_in, W.w[LN1_G], lp.ln1_mean, lp.ln1_rstd, w.G1, dx, W.g[LN1_G],
+               W.g[LN1_B], w.part, M, h, st));
+    return 0;
+}
+
+int chunk_forward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P, const FwdArgs& a,
+                  cudaStream_t st) {
+    const ParamLayout& lay = *P.lay;
+    const int n = (int)lay.layer.size();
+    const long M = D.M, h = D.h;
+    uint8_t* ws = a.ws;
+    void* ws_ln = ws;
+    void* ws_g = ws + M * h * D.es;
+    const uint8_t* wb = reinterpret_cast<const uint8_t*>(P.w);
+    if (lay.emb)
+        TRY(embed_fwd(D.dtype, a.tokens, wb + lay.wte * D.es, wb + lay.wpe * D.es,
+                      a.stash + SL.layer[0].x_in, D.M, D.s, D.h, st));
+    for (int l = 0; l < n; ++l) {
+        LayerPtrs lp = layer_ptrs(SL.layer[l], a.stash, a.in);
+        void* out;
+        if (l + 1 < n) out = a.stash + SL.layer[l + 1].x_in;
+        else if (lay.head) out = a.stash + SL.x_f;
+        else out = a.out ? a.out : ws_ln;   // recompute: discard into free scratch
+        TRY(layer_forward(D, layer_w(D, P, l), lp, ws_ln, ws_g, out, st));
+    }
+    if (lay.head && a.targets) {
+        uint8_t* lnf = ws + M * (h + D.f) * D.es;
+        float* logits = reinterpret_cast<float*>(lnf + M * h * D.es);
+        TRY(ln_fwd(D.dtype, a.stash + SL.x_f, wb + lay.lnf_g * D.es, wb + lay.lnf_b * D.es, lnf,
+                   at<float>(a.stash, SL.lnf_mean), at<float>(a.stash, SL.lnf_rstd), M, h, st));
+        TRY(mm(D, M, D.V, h, lnf, h, 1, wb + lay.w_head * D.es, h, 1, EPI_STORE_F32, logits, D.V,
+               nullptr, nullptr, 0, nullptr, 0, nullptr, 0, st));
+        TRY(ce_fwd(logits, a.targets, at<float>(a.stash, SL.ce_lse), a.loss_slot, a.loss_scale, M,
+                   D.V, st));
+    }
+    return 0;
+}
+
+int chunk_backward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P, const BwdArgs& a,
+                   cudaStream_t st) {
+    const ParamLayout& lay = *P.lay;
+    const int n = (int)lay.layer.size();
+    const long M = D.M, h = D.h;
+    const long part = ((M + 63) / 64) * (D.f > 3 * h ? D.f : 3 * h);
+    BwdWs w = carve_bwd(D, a.ws, lay.head, lay.emb, part, 0);
+    const uint8_t* wb = reinterpret_cast<const uint8_t*>(P.w);
+    const void* dy = a.gin;
+    if (lay.head) {
+        const void* ln_g = wb + lay.lnf_g * D.es;
+        TRY(ln_apply(D.dtype, a.stash + SL.x_f, ln_g, wb + lay.lnf_b * D.es,
+                     at<float>(a.stash, SL.lnf_mean), at<float>(a.stash, SL.lnf_rstd), w.lnf, M, h,
+                     st));
+        const void* wh = wb + lay.w_head * D.es;
+        TRY(mm(D, M, D.V, h, w.lnf, h, 1, wh, h, 1, EPI_STORE_F32, w.logits, D.V, nullptr, nullptr,
+               0, nullptr, 0, nullptr, 0, st));
+        TRY(ce_bwd(D.dtype, w.logits, a.targets, at<float>(a.stash, SL.ce_lse), w.dlogits,
+                   a.loss_scale, M, D.V, st));
+        TRY(mm(D, D.V, h, M, w.dlogits, D.V, 0, w.lnf, h, 0, EPI_ACC_F32, P.grad + lay.w_head, h,
+               nullptr, nullptr, 0, nullptr, 0, nullptr, 0, st));
+        TRY(mm(D, M, h, D.V, w.dlogits, D.V, 1, wh, h, 0, EPI_STORE, w.dlnf, h, nullptr, nullptr, 0,
+               nullptr, 0, nullptr, 0, st));
+        TRY(ln_bwd(D.dtype, w.dlnf, a.stash + SL.x_f, ln_g, at<float>(a.stash, SL.lnf_mean),
+                   at<float>(a.stash, SL.lnf_rstd), nullptr, w.G0, P.grad + lay.lnf_g,
+                   P.grad + lay.lnf_b, w.part, M, h, st));
+        dy = w.G0;
+    }
+    for (int l = n - 1; l >= 0; --l) {
+        LayerPtrs lp = layer_ptrs(SL.layer[l], a.stash, a.in);
+        void* dx = (l > 0 || lay.emb) ? w.G0 : a.gout;
+        TRY(layer_backward(D, layer_w(D, P, l), lp, dy, dx, w, st));
+        dy = w.G0;
+    }
+    if (lay.emb)
+        TRY(embed_bwd(D.dtype, a.tokens, w.G0, P.grad + lay.wte, P.grad + lay.wpe, w.emb_ws, M, D.s,
+                      h, st));
+    return 0;
+}
+
+}  // namespace tpipe

@@ -69,7 +69,10 @@ class Plan:
 
     def __del__(self):
         if getattr(self, "_h", None):
-            lib().tpipe_plan_destroy(self._h)
+            try:
+                lib().tpipe_plan_destroy(self._h)
+            except Exception:  # interpreter shutdown
+                pass
             self._h = None
 
     def ops(self, stage):

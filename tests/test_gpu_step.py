@@ -1,0 +1,170 @@
+"""Full training-step parity through the C-ABI (tpipe_plan -> tpipe_runtime ->
+tpipe_step) against the fp64 oracle (oracle.model), on seeded synthetic
+inputs of config C1 shape (BASELINE.json configs[0]).
+
+Bars (BASELINE.json north_star): fp32 mode loss and every
+gradient tensor max-relative error <= 1e-4; bf16 mode relative L2 <= 2e-2;
+T-Recomp on/off and T-Offload on/off bit-exact; pool ledger high-water ==
+plan peak bytes exactly.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import synth  # noqa: E402
+from oracle import model as R  # noqa: E402
+
+C1 = dict(n_layers=8, hidden=64, n_heads=4, ffn_hidden=256, vocab=256, seq_len=32, micro_batch=2)
+
+
+def mods():
+    from paper_2503_03182_b200 import params, plan, runtime
+    return plan, runtime, params
+
+
+def build(cfg, p, m, strategy, dtype, offload=0, lr=1e-3, seed=11):
+    P, RT, PR = mods()
+    md = P.Model(cfg["n_layers"], cfg["hidden"], cfg["n_heads"], cfg["ffn_hidden"], cfg["vocab"],
+                 cfg["seq_len"], cfg["micro_batch"], dtype)
+    plan = P.Plan(md, p, m, strategy=strategy, offload=offload)
+    rt = RT.Runtime(plan, stage=-1, lr=lr)
+    W = synth.weights(cfg["n_layers"], cfg["hidden"], cfg["ffn_hidden"], cfg["vocab"],
+                      cfg["seq_len"], seed=seed, std=0.05, bias_std=0.02, ln_jitter=0.05)
+    for s in range(p):
+        for c in range(1, plan.v + 1):
+            rt.set_params(s, c, PR.pack(W, p, plan.v, plan.layers_chunk, s, c))
+    return plan, rt, W
+
+
+def oracle_grads(cfg, W, tok, tgt):
+    return R.step_grads(R.to64(W), tok, tgt, cfg["n_heads"])
+
+
+def compare(plan, rt, W, G, metric, tol):
+    _P, _RT, PR = mods()
+    worst = 0.0
+    for s in range(plan.p):
+        for c in range(1, plan.v + 1):
+            got = PR.unpack(rt.get_grads(s, c), W, plan.p, plan.v, plan.layers_chunk, s, c)
+            for (k, l), g in got.items():
+                ref = G["layers"][l][k] if l is not None else G[k]
+                err = metric(g, ref)
+                worst = max(worst, err)
+                assert err <= tol, (s, c, k, l, err)
+    return worst
+
+
+def max_rel(a, b):
+    return float(np.abs(np.asarray(a, np.float64) - b).max() / (np.abs(b).max() + 1e-30))
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64)
+    return float(np.linalg.norm(a - b) / (np.linalg.norm(b) + 1e-30))
+
+
+@pytest.mark.parametrize("strategy", ["tpipe", "tpipe_trecomp", "1f1b"])
+@pytest.mark.parametrize("p", [1, 2, 4])
+def test_step_fp32_parity(strategy, p):
+    _P, RT, _PR = mods()
+    m = 8
+    plan, rt, W = build(C1, p, m, strategy, 0)
+    tok, tgt = synth.tokens(C1["vocab"], m, C1["micro_batch"], C1["seq_len"], step=0)
+    loss = rt.step(tok, tgt, RT.STEP_NO_OPT)
+    lref, G = oracle_grads(C1, W, tok, tgt)
+    assert abs(loss - lref) / abs(lref) < 1e-5
+    compare(plan, rt, W, G, max_rel, 1e-4)
+    # pool ledger high-water == plan peak (byte-exact)
+    st = rt.stats()
+    for s in range(p):
+        assert st["pool_high_water"][s] == plan.peak(s)["total_peak"]
+    assert st["kernel_launches"] > 0
+
+
+@pytest.mark.parametrize("strategy", ["tpipe", "tpipe_trecomp"])
+def test_step_bf16_parity(strategy):
+    _P, RT, _PR = mods()
+    p, m = 4, 8
+    plan, rt, W = build(C1, p, m, strategy, 1)
+    tok, tgt = synth.tokens(C1["vocab"], m, C1["micro_batch"], C1["seq_len"], step=0)
+    loss = rt.step(tok, tgt, RT.STEP_NO_OPT)
+    lref, G = oracle_grads(C1, W, tok, tgt)
+    assert abs(loss - lref) / abs(lref) < 2e-2
+    compare(plan, rt, W, G, rel_l2, 2e-2)
+
+
+@pytest.mark.parametrize("dtype", [0, 1])
+def test_trecomp_bitexact_vs_tpipe(dtype):
+    """T-Recomp regenerates chunk-1 activations with the same kernels, so the
+    gradients are bit-identical to T-Pipe's (BASELINE north_star)."""
+    _P, RT, _PR = mods()
+    p, m = 4, 8
+    tok, tgt = synth.tokens(C1["vocab"], m, C1["micro_batch"], C1["seq_len"], step=3)
+    out = []
+    for strategy in ("tpipe", "tpipe_trecomp"):
+        plan, rt, _W = build(C1, p, m, strategy, dtype)
+        loss = rt.step(tok, tgt, RT.STEP_NO_OPT)
+        out.append((loss, [rt.get_grads(s, c) for s in range(p) for c in (1, 2)]))
+    assert out[0][0] == out[1][0]
+    for a, b in zip(out[0][1], out[1][1]):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+@pytest.mark.parametrize("dtype", [0, 1])
+def test_offload_bitexact(dtype):
+    """T-Offload (host AdamW for chunk 2) vs device AdamW: parameters
+    after 3 optimizer steps are bit-identical; the step counters and the
+    uploaded weights agree."""
+    _P, RT, _PR = mods()
+    p, m = 4, 8
+    res = []
+    for off in (0, 1):
+        plan, rt, _W = build(C1, p, m, "tpipe_trecomp", dtype, offload=off)
+        losses = []
+        for step in range(3):
+            tok, tgt = synth.tokens(C1["vocab"], m, C1["micro_batch"], C1["seq_len"], step=step)
+            losses.append(rt.step(tok, tgt))
+        res.append((losses, [rt.get_params(s, c) for s in range(p) for c in (1, 2)]))
+        if off:
+            assert rt.stats()["offload_d2h_bytes"] > 0
+    assert res[0][0] == res[1][0]
+    for a, b in zip(res[0][1], res[1][1]):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def test_adamw_step_matches_oracle_fp32():
+    """One full step with the optimizer: new fp32 weights vs the oracle's
+    fp64 AdamW applied to the oracle gradients (N-3)."""
+    _P, RT, PR = mods()
+    p, m, lr = 2, 4, 1e-3
+    plan, rt, W = build(C1, p, m, "tpipe", 0, lr=lr)
+    tok, tgt = synth.tokens(C1["vocab"], m, C1["micro_batch"], C1["seq_len"], step=0)
+    rt.step(tok, tgt)
+    _l, G = oracle_grads(C1, W, tok, tgt)
+    W64 = R.to64(W)
+    for s in range(p):
+        for c in (1, 2):
+            got = PR.unpack(rt.get_params(s, c), W, p, 2, plan.layers_chunk, s, c)
+            for (k, l), w in got.items():
+                w0 = W64["layers"][l][k] if l is not None else W64[k]
+                g = G["layers"][l][k] if l is not None else G[k]
+                ref, _, _ = R.adamw(w0, g, np.zeros_like(g), np.zeros_like(g), 1, lr,
+                                    decay=(np.ndim(w0) == 2))
+                # step-1 Adam update is ~ lr * sign(g): compare the update itself
+                upd, upd_ref = np.asarray(w, np.float64) - w0, ref - w0
+                mask = np.abs(g) > 1e-3 * np.abs(g).max()   # |g| >> Adam eps
+                assert np.abs(upd - upd_ref)[mask].max() <= 2e-4 * lr + 1e-7, (s, c, k, l)
+
+
+def test_loss_decreases_bf16():
+    """Sanity of the whole step (fwd, bwd, optimizer) at C1: training on a
+    fixed batch drives the loss down."""
+    _P, RT, _PR = mods()
+    p, m = 4, 8
+    plan, rt, _W = build(C1, p, m, "tpipe_trecomp", 1, lr=3e-3)
+    tok, tgt = synth.tokens(C1["vocab"], m, C1["micro_batch"], C1["seq_len"], step=0)
+    losses = [rt.step(tok, tgt) for _ in range(8)]
+    assert losses[-1] < losses[0] - 0.1, losses

@@ -156,3 +156,26 @@ def test_budget_escalation_and_errors():
         P.Plan(P.Model(16, 60, 4, 256, 128, 32, 2), 8, 32)
     with pytest.raises(TPipeError, match="deadlock"):
         P.Plan(md, 8, 32, strategy="tpipe_trecomp", send_window=1)
+
+
+@pytest.mark.parametrize("strategy,p", [("tpipe", 1), ("tpipe", 4), ("1f1b", 2), ("tpipe", 2)])
+def test_param_packing_matches_plan(strategy, p):
+    """Packed chunk vectors (params.py) have exactly the
+    plan's per-chunk parameter counts and cover every global layer once."""
+    import synth
+    P = _plan_mod()
+    from paper_2503_03182_b200 import params as PR
+    L = 8
+    plan = P.Plan(P.Model(L, 64, 4, 256, 128, 32, 2), p, 4, strategy=strategy)
+    W = synth.weights(L, 64, 256, 128, 32)
+    seen = []
+    for s in range(p):
+        for c in range(1, plan.v + 1):
+            flat = PR.pack(W, p, plan.v, plan.layers_chunk, s, c)
+            assert flat.size == plan.chunk_params(s, c)
+            seen += PR.global_layers(p, plan.v, plan.layers_chunk, s, c)
+            back = PR.unpack(flat, W, p, plan.v, plan.layers_chunk, s, c)
+            for (k, l), a in back.items():
+                ref = W["layers"][l][k] if l is not None else W[k]
+                assert (a == ref).all()
+    assert sorted(seen) == list(range(L))
