@@ -303,7 +303,7 @@ def run_tpipe(args):
     rt.close()
     del rt
     if rank == 0 and not args.no_extras and world == 1:
-        out["capacity_80GiB"] = {"p": N, "shape": "h=4096 a=32 s=8192 V=32000 b=1 m=32",
+        out["capacity_80GiB"] = {"p": max(N, 8) if N == 1 else N, "shape": "h=4096 a=32 s=8192 V=32000 b=1 m=32",
                                  **capacity(max(N, 8) if N == 1 else N)}
         out["cpu_baseline"] = cpu_baseline(c)
     if dist:
