@@ -183,6 +183,39 @@ def capacity(p, strategies=("1f1b", "tpipe", "tpipe_trecomp", "tpipe_all")):
     return out
 
 
+def quick_measure(strategy, N, m, dtok, dtgt, args):
+    """tokens/s of another schedule on the same kernels/workload (N=1)."""
+    import torch
+    from paper_2503_03182_b200 import plan as P, runtime as RT
+    c = C2
+    md = P.Model(c["n_layers"], c["hidden"], c["n_heads"], c["ffn_hidden"], c["vocab"],
+                 c["seq_len"], c["micro_batch"], P.BF16)
+    plan = P.Plan(md, N, m, strategy=strategy)
+    rt = RT.Runtime(plan, stage=-1, lr=1e-4)
+    rng = np.random.default_rng(99)
+    for s in range(N):
+        for ch in range(1, plan.v + 1):
+            rt.set_params(s, ch, init_chunk(plan, s, ch, rng))
+    ext = torch.cuda.ExternalStream(rt.stream())
+    for _ in range(2):
+        rt.step_device(dtok.data_ptr(), dtgt.data_ptr())
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k = max(2, args.steps // 2)
+    e0.record(ext)
+    for _ in range(k):
+        rt.step_device(dtok.data_ptr(), dtgt.data_ptr())
+    e1.record(ext)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / k
+    tokens = m * c["micro_batch"] * c["seq_len"]
+    res = {"tokens_s": round(tokens / (ms / 1e3), 1), "ms_per_step": round(ms, 2),
+           "steps": k, "plan_peak_GiB": round(plan.peak(0)["total_peak"] / 2 ** 30, 2),
+           "pool_high_water_GiB": round(rt.stats()["pool_high_water"][0] / 2 ** 30, 2)}
+    rt.close()
+    return res
+
+
 def run_tpipe(args):
     import torch
     from paper_2503_03182_b200 import plan as P, runtime as RT
@@ -303,6 +336,15 @@ def run_tpipe(args):
     rt.close()
     del rt
     if rank == 0 and not args.no_extras and world == 1:
+        # in-build baselines on the same kernels (north star): same model,
+        # tokens and step; plan peak HBM per stage from the byte model
+        comp = {args.strategy: {"tokens_s": round(value, 1),
+                                "plan_peak_GiB": round(plan.peak(0)["total_peak"] / 2 ** 30, 2)}}
+        for st in ("1f1b", "1f1b_full_recomp", "tpipe_trecomp", "tpipe"):
+            if st in comp:
+                continue
+            comp[st] = quick_measure(st, N, m, dtok, dtgt, args)
+        out["compare"] = comp
         out["capacity_80GiB"] = {"p": max(N, 8) if N == 1 else N, "shape": "h=4096 a=32 s=8192 V=32000 b=1 m=32",
                                  **capacity(max(N, 8) if N == 1 else N)}
         out["cpu_baseline"] = cpu_baseline(c)

@@ -76,6 +76,7 @@ enum {
 };
 
 #define TPIPE_OFFLOAD_MODEL_STATE 1   /* T-Offload of chunk-2 grads/optimizer/weights */
+#define TPIPE_OFFLOAD_ACTIVATIONS 2   /* chunk-1 stash to pinned host and back (R23) */
 
 typedef struct {
     int32_t strategy;      /* TPIPE_S_*, or -1 = auto: escalate TPIPE -> TPIPE_TRECOMP ->
@@ -83,6 +84,8 @@ typedef struct {
     int32_t delay_rounds;  /* T-Recomp k; -1 = App. B constraint as printed */
     int32_t send_window;   /* W, max in-flight sends per channel; 0 = default 2 (DESIGN R12) */
     int32_t offload;       /* TPIPE_OFFLOAD_* bitmask (explicit strategies); -1 = auto */
+    int32_t act_distance;  /* activation offload: release / prefetch distance in compute
+                              ops (0 = default 2); blocks with F->B distance <= 2x are kept */
 } tpipe_plan_opts;
 
 enum {
@@ -90,7 +93,11 @@ enum {
     TPIPE_OP_RECV_ACT = 3, TPIPE_OP_RECV_GRAD = 4,
     TPIPE_OP_SEND_ACT = 5, TPIPE_OP_SEND_GRAD = 6, TPIPE_OP_SEND_WAIT = 7,
     TPIPE_OP_OPT = 8, TPIPE_OP_GRAD_D2H = 9, TPIPE_OP_HOST_OPT = 10,
-    TPIPE_OP_W_H2D = 11, TPIPE_OP_W_WAIT = 12
+    TPIPE_OP_W_H2D = 11, TPIPE_OP_W_WAIT = 12,
+    TPIPE_OP_ACT_D2H = 13,       /* copy STASH(1,i) to pinned host (after F) */
+    TPIPE_OP_ACT_D2H_WAIT = 14,  /* copy done -> release STASH(1,i) on the device */
+    TPIPE_OP_ACT_H2D = 15,       /* re-allocate STASH(1,i), start the prefetch */
+    TPIPE_OP_ACT_H2D_WAIT = 16   /* prefetch landed (before B(1,i)) */
 };
 
 /* One instruction of a stage's stream. Buffers listed in
@@ -131,6 +138,7 @@ typedef struct {
 
 typedef struct {
     int32_t n_stages, n_microbatches, v, strategy, delay_rounds, send_window, offload;
+    int32_t act_distance;
     int32_t layers_chunk[2];
     int32_t n_channels;
     uint64_t params_total;

@@ -117,6 +117,8 @@ def sizes(d: ModelDesc, p: int, v: int, s: int, c: int, full_recomp: bool = Fals
         stash += head_stash
     nb = n_partials(M)
     ws_f = M * (h + f) * es
+    if full_recomp:
+        ws_f += LS - M * h * es                  # one layer's transient internals
     if head:
         ws_f += M * h * es + 4 * M * V + 4 * M
     ws_b = M * (2 * f + 8 * h) * es + 4 * a * M + 4 * nb * max(f, 3 * h)
@@ -140,6 +142,7 @@ def sizes(d: ModelDesc, p: int, v: int, s: int, c: int, full_recomp: bool = Fals
 class Instr:
     kind: str                      # F B R RECV_ACT RECV_GRAD SEND_ACT SEND_GRAD SEND_WAIT
                                    # OPT GRAD_D2H HOST_OPT W_H2D W_WAIT
+                                   # ACT_D2H ACT_D2H_WAIT ACT_H2D ACT_H2D_WAIT
     chunk: int = 0
     mb: int = 0
     peer: int = -1
@@ -161,13 +164,34 @@ STRATS = {
 }
 
 
+def act_offload_sets(order, d_release: int, d_prefetch: int):
+    """Activation offload (R23; north-star extension of
+    P:416): chunk-1 stash blocks whose compute-op distance F(1,i) -> B(1,i)
+    exceeds d_release + d_prefetch are copied to host after F, released
+    d_release compute ops after F, and prefetched d_prefetch ops before B.
+    Returns (offloaded mbs, release_at[op index], fetch_at[op index])."""
+    pos = {op: n for n, op in enumerate(order)}
+    off, rel, fet = [], defaultdict(list), defaultdict(list)
+    for op, n in pos.items():
+        if op[0] == "F" and op[1] == 1:
+            nb = pos[("B", 1, op[2])]
+            if nb - n > d_release + d_prefetch:
+                off.append(op[2])
+                rel[n + d_release].append(op[2])
+                fet[nb - d_prefetch].append(op[2])
+    return set(off), rel, fet
+
+
 def build_streams(d: ModelDesc, p: int, m: int, strategy: str, k=None,
-                  window: int = 2, offload_model_state: bool = False):
+                  window: int = 2, offload_model_state: bool = False,
+                  offload_activations: bool = False, act_distance: int = 2):
     """Per-stage instruction streams. Returns (streams, static)
     where static[s] = list of (name, category, bytes) live for the whole step."""
     ostrat, v, trecomp, full = STRATS[strategy]
     if offload_model_state and v != 2:
         raise ValueError("offload requires v=2")
+    if offload_activations and (v != 2 or trecomp):
+        raise ValueError("activation offload applies to T-Pipe chunk 1 (no T-Recomp)")
     orders = S.strategy_orders(ostrat, p, m, k=k)[0]
     sz = {(s, c): sizes(d, p, v, s, c, full_recomp=full)
           for s in range(p) for c in range(1, v + 1)}
@@ -196,10 +220,20 @@ def build_streams(d: ModelDesc, p: int, m: int, strategy: str, k=None,
         first_f = {c: min(op[2] for op in orders[s] if op[0] == "F" and op[1] == c)
                    for c in range(1, v + 1)}
         first_op_done = False
-        for op in orders[s]:
+        if offload_activations:
+            aoff, arel, afet = act_offload_sets(orders[s], act_distance, act_distance)
+        else:
+            aoff, arel, afet = set(), {}, {}
+        for n_op, op in enumerate(orders[s]):
             kind, c, i = op
             z = sz[(s, c)]
             msg = S.message_of(s, op, p, v)
+            # 0. activation offload: release copied blocks, start prefetches
+            for mb in sorted(arel.get(n_op, [])):
+                out.append(Instr("ACT_D2H_WAIT", 1, mb, frees=[("STASH", 1, mb)]))
+            for mb in sorted(afet.get(n_op, [])):
+                out.append(Instr("ACT_H2D", 1, mb,
+                                 allocs=[(("STASH", 1, mb), "act", sz[(s, 1)]["stash"])]))
             # 1. send-window wait before the op producing message j+W
             if msg is not None:
                 ch = msg[0]
@@ -224,6 +258,8 @@ def build_streams(d: ModelDesc, p: int, m: int, strategy: str, k=None,
                     ch = ("G", src, s)
                     out.append(Instr("RECV_GRAD", c, i, peer=src, channel=ch,
                                      allocs=[(("GIN", c, i), "comm", z["act"])]))
+            if kind == "B" and c == 1 and i in aoff:
+                out.append(Instr("ACT_H2D_WAIT", 1, i))
             # 3. the compute op
             ins = Instr(kind, c, i)
             if kind == "F":
@@ -262,6 +298,8 @@ def build_streams(d: ModelDesc, p: int, m: int, strategy: str, k=None,
                 out.append(Instr("SEND_ACT" if kind == "F" else "SEND_GRAD", c, i,
                                  peer=ch[2], channel=ch, msg=sent[ch]))
                 sent[ch] += 1
+            if kind == "F" and c == 1 and i in aoff:
+                out.append(Instr("ACT_D2H", 1, i))
             # 5. optimizer / offload after the chunk's last backward
             if kind == "B" and i == last_b[c]:
                 if offload_model_state and c == v:

@@ -23,6 +23,7 @@
 #include <cstdarg>
 #include <map>
 #include <new>
+#include <set>
 #include <string>
 #include <tuple>
 
@@ -76,6 +77,7 @@ static ChunkSizes chunk_sizes(const tpipe_model_desc& d, int p, int v, const int
     z.stash = stash;
     const uint64_t nb = (M + 63) / 64;
     uint64_t ws_f = M * (h + f) * es;
+    if (full_recomp) ws_f += LS - M * h * es;  // one layer's transient internals
     if (head) ws_f += M * h * es + 4 * M * V + 4 * M;
     uint64_t ws_b = M * (2 * f + 8 * h) * es + 4 * a * M + 4 * nb * std::max(f, 3 * h);
     if (full_recomp) ws_b += LS - M * h * es;
@@ -257,6 +259,7 @@ static int build(tpipe_plan* P, bool trecomp, bool full_recomp) {
     }
 
     const bool off = (P->offload & TPIPE_OFFLOAD_MODEL_STATE) != 0;
+    const bool aoff_on = (P->offload & TPIPE_OFFLOAD_ACTIVATIONS) != 0 && v == 2 && !trecomp;
     const uint64_t es = d.dtype == TPIPE_BF16 ? 2 : 4;
     const uint64_t M = (uint64_t)d.micro_batch * d.seq_len;
     P->params_total = 0;
@@ -286,12 +289,46 @@ static int build(tpipe_plan* P, bool trecomp, bool full_recomp) {
             if (op[0] == KF) first_f[op[1]] = std::min(first_f[op[1]], op[2]);
         }
         bool first_f_done = false;
-        for (auto& op : order) {
+        // activation offload of chunk-1 stash blocks (R23): blocks whose
+        // F(1,i) -> B(1,i) distance exceeds 2d compute ops go to pinned host
+        std::set<int> aoff;
+        std::map<int, std::vector<int>> arel, afet;
+        const int dd = P->act_distance;
+        if (aoff_on) {
+            for (size_t n = 0; n < order.size(); ++n) {
+                if (order[n][0] != KF || order[n][1] != 1) continue;
+                const int mb = order[n][2];
+                size_t nb = n;
+                while (nb < order.size() && !(order[nb][0] == KB && order[nb][1] == 1 && order[nb][2] == mb)) ++nb;
+                if ((long)nb - (long)n > 2L * dd) {
+                    aoff.insert(mb);
+                    arel[(int)n + dd].push_back(mb);
+                    afet[(int)nb - dd].push_back(mb);
+                }
+            }
+            for (auto& kv : arel) std::sort(kv.second.begin(), kv.second.end());
+            for (auto& kv : afet) std::sort(kv.second.begin(), kv.second.end());
+        }
+        for (size_t n_op = 0; n_op < order.size(); ++n_op) {
+            const auto& op = order[n_op];
             const int kind = op[0], c = op[1], i = op[2];
             const ChunkSizes& zz = z[c];
             Msg mg;
             const bool has_msg = message_of(s, op, p, v, &mg);
             const int ch = has_msg ? chan_id[{mg.kind, mg.src, mg.dst}] : -1;
+            // 0. activation offload: release copied blocks, start prefetches
+            if (arel.count((int)n_op))
+                for (int mb : arel[(int)n_op]) {
+                    Builder::Pending pe;
+                    pe.frees.push_back(B.take(TPIPE_BUF_STASH, 1, mb));
+                    B.emit(TPIPE_OP_ACT_D2H_WAIT, 1, mb, -1, -1, -1, pe);
+                }
+            if (afet.count((int)n_op))
+                for (int mb : afet[(int)n_op]) {
+                    Builder::Pending pe;
+                    pe.allocs.push_back(B.newbuf(TPIPE_BUF_STASH, TPIPE_CAT_ACT, 1, mb, z[1].stash));
+                    B.emit(TPIPE_OP_ACT_H2D, 1, mb, -1, -1, -1, pe);
+                }
             // 1. send-window waits
             if (has_msg) {
                 const int j = sent[ch];
@@ -321,6 +358,7 @@ static int build(tpipe_plan* P, bool trecomp, bool full_recomp) {
                     B.emit(TPIPE_OP_RECV_GRAD, c, i, src, chan_id[{1, src, s}], -1, pe);
                 }
             }
+            if (kind == KB && c == 1 && aoff.count(i)) B.emit(TPIPE_OP_ACT_H2D_WAIT, 1, i, -1, -1, -1, {});
             // 3. the compute op
             Builder::Pending pe;
             if (kind == KF) {
@@ -366,6 +404,7 @@ static int build(tpipe_plan* P, bool trecomp, bool full_recomp) {
                 B.emit(kind == KF ? TPIPE_OP_SEND_ACT : TPIPE_OP_SEND_GRAD, c, i, mg.dst, ch, sent[ch], {});
                 sent[ch] += 1;
             }
+            if (kind == KF && c == 1 && aoff.count(i)) B.emit(TPIPE_OP_ACT_D2H, 1, i, -1, -1, -1, {});
             // 5. optimizer after the chunk's last backward
             if (kind == KB && i == last_b[c]) {
                 if (off && c == v) {
@@ -495,7 +534,9 @@ using namespace tpipe;
 #define TP_API extern "C" __attribute__((visibility("default")))
 
 static int make_plan(const tpipe_model_desc* model, int p, int m, int strategy, int k, int W,
-                     int offload, tpipe_plan** out) {
+                     int offload, int act_distance, tpipe_plan** out) {
+    if ((offload & TPIPE_OFFLOAD_ACTIVATIONS) && strategy != TPIPE_S_TPIPE)
+        return set_error(TPIPE_E_INCOMPAT, "activation offload applies to T-Pipe without T-Recomp");
     tpipe_plan* P = new (std::nothrow) tpipe_plan();
     if (!P) return set_error(TPIPE_E_INVALID, "out of host memory");
     P->model = *model;
@@ -504,6 +545,7 @@ static int make_plan(const tpipe_model_desc* model, int p, int m, int strategy, 
     P->strategy = strategy;
     P->W = W;
     P->offload = offload;
+    P->act_distance = act_distance > 0 ? act_distance : 2;
     const bool is_tp = strategy == TPIPE_S_TPIPE || strategy == TPIPE_S_TPIPE_TRECOMP;
     P->v = is_tp ? 2 : 1;
     const int n = model->n_layers / p;
@@ -567,7 +609,7 @@ TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, in
     if (!out) return set_error(TPIPE_E_INVALID, "out is NULL");
     *out = nullptr;
     if (int rc = validate(model, n_stages, n_microbatches)) return rc;
-    tpipe_plan_opts o{-1, -1, 0, -1};
+    tpipe_plan_opts o{-1, -1, 0, -1, 0};
     if (opts) o = *opts;
     const int W = o.send_window > 0 ? o.send_window : 2;
     if (o.strategy < -1 || o.strategy > TPIPE_S_TPIPE_TRECOMP) return set_error(TPIPE_E_INVALID, "strategy");
@@ -575,7 +617,8 @@ TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, in
     if (o.strategy >= 0) {
         const int off = o.offload < 0 ? 0 : o.offload;
         tpipe_plan* P = nullptr;
-        int rc = make_plan(model, n_stages, n_microbatches, o.strategy, o.delay_rounds, W, off, &P);
+        int rc = make_plan(model, n_stages, n_microbatches, o.strategy, o.delay_rounds, W, off,
+                           o.act_distance, &P);
         if (rc) return rc;
         if (hbm_budget_bytes && max_peak(P) > hbm_budget_bytes) {
             const uint64_t pk = max_peak(P);
@@ -594,7 +637,8 @@ TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, in
     for (auto& rung : ladder) {
         if (o.offload >= 0 && rung[1] && !(o.offload & TPIPE_OFFLOAD_MODEL_STATE)) continue;
         tpipe_plan* P = nullptr;
-        int rc = make_plan(model, n_stages, n_microbatches, rung[0], o.delay_rounds, W, rung[1], &P);
+        int rc = make_plan(model, n_stages, n_microbatches, rung[0], o.delay_rounds, W, rung[1],
+                           o.act_distance, &P);
         if (rc) return rc;
         best = max_peak(P);
         if (!hbm_budget_bytes || best <= hbm_budget_bytes) {
@@ -618,6 +662,7 @@ TP_API int tpipe_plan_get_info(const tpipe_plan* P, tpipe_plan_info* out) {
     out->delay_rounds = P->k;
     out->send_window = P->W;
     out->offload = P->offload;
+    out->act_distance = P->act_distance;
     out->layers_chunk[0] = P->layers[0];
     out->layers_chunk[1] = P->layers[1];
     out->n_channels = (int32_t)P->channels.size();

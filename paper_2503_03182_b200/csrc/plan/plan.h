@@ -10,7 +10,7 @@
 struct tpipe_plan {
     tpipe_model_desc model{};
     int p = 0, m = 0, v = 0;
-    int strategy = 0, k = 0, W = 2, offload = 0;
+    int strategy = 0, k = 0, W = 2, offload = 0, act_distance = 2;
     int layers[2] = {0, 0};
     uint64_t params_total = 0;
     // per stage

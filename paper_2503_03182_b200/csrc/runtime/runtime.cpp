@@ -79,6 +79,10 @@ struct StageState {
     std::vector<void*> bufptr;
     std::map<std::tuple<int, int, int>, void*> live;
     size_t pc = 0;
+    // activation offload (R23): pinned host slots per micro-batch, free list
+    std::map<int, void*> act_host;
+    std::vector<void*> act_free;
+    std::map<int, cudaEvent_t> act_ev_d2h, act_ev_h2d;
 };
 
 struct Channel {
@@ -369,6 +373,50 @@ int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags
             C.h2d_pending = C.d2h_pending = false;
             break;
         }
+        case TPIPE_OP_ACT_D2H: {
+            ChunkState& C = S.ch[1];
+            void* dev = live_get(S, TPIPE_BUF_STASH, 1, i);
+            if (!dev) return set_error(TPIPE_E_STATE, "ACT_D2H: stash (1,%d) not live", i);
+            const size_t bytes = (size_t)C.sl.total;
+            void* host;
+            if (!S.act_free.empty()) {
+                host = S.act_free.back();
+                S.act_free.pop_back();
+            } else {
+                CU(cudaHostAlloc(&host, bytes, cudaHostAllocDefault));
+            }
+            S.act_host[i] = host;
+            cudaEvent_t e0 = next_event(rt), e1 = next_event(rt);
+            CU(cudaEventRecord(e0, cs));
+            CU(cudaStreamWaitEvent(rt->d2h, e0, 0));
+            CU(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, rt->d2h));
+            CU(cudaEventRecord(e1, rt->d2h));
+            S.act_ev_d2h[i] = e1;
+            rt->d2h_bytes += (double)bytes;
+            break;
+        }
+        case TPIPE_OP_ACT_D2H_WAIT:
+            // device copy may be released only once the copy engine has read it
+            CU(cudaStreamWaitEvent(cs, S.act_ev_d2h.at(i), 0));
+            break;
+        case TPIPE_OP_ACT_H2D: {
+            ChunkState& C = S.ch[1];
+            void* dev = live_get(S, TPIPE_BUF_STASH, 1, i);
+            void* host = S.act_host.at(i);
+            cudaEvent_t e0 = next_event(rt), e1 = next_event(rt);
+            CU(cudaEventRecord(e0, cs));   // previous users of `dev` are done
+            CU(cudaStreamWaitEvent(rt->h2d, e0, 0));
+            CU(cudaMemcpyAsync(dev, host, (size_t)C.sl.total, cudaMemcpyHostToDevice, rt->h2d));
+            CU(cudaEventRecord(e1, rt->h2d));
+            S.act_ev_h2d[i] = e1;
+            rt->h2d_bytes += (double)C.sl.total;
+            break;
+        }
+        case TPIPE_OP_ACT_H2D_WAIT:
+            CU(cudaStreamWaitEvent(cs, S.act_ev_h2d.at(i), 0));
+            S.act_free.push_back(S.act_host.at(i));
+            S.act_host.erase(i);
+            break;
         default:
             return set_error(TPIPE_E_STATE, "unknown op kind %d", op.kind);
     }
@@ -461,8 +509,6 @@ TP_API int tpipe_runtime_create(const tpipe_plan* plan, const tpipe_runtime_opts
     o.stage = -1;
     if (opts) o = *opts;
     if (o.stage < -1 || o.stage >= plan->p) return set_error(TPIPE_E_INVALID, "stage");
-    if (plan->strategy == TPIPE_S_1F1B_FULL_RECOMP)
-        return set_error(TPIPE_E_INCOMPAT, "1F1B+full-recompute runtime not built yet");
     if ((long)plan->model.micro_batch * plan->model.seq_len % 8)
         return set_error(TPIPE_E_INVALID, "micro_batch*seq_len must be a multiple of 8");
     std::unique_ptr<tpipe_runtime> rt(new (std::nothrow) tpipe_runtime(*plan));
@@ -508,7 +554,8 @@ TP_API int tpipe_runtime_create(const tpipe_plan* plan, const tpipe_runtime_opts
                 ChunkState& C = S->ch[c];
                 const bool emb = (s == 0 && c == 1), head = (s == P.p - 1 && c == P.v);
                 C.lay = make_param_layout(P.model, P.layers[c - 1], emb, head);
-                C.sl = make_stash_layout(P.model, P.layers[c - 1], emb, head);
+                C.sl = make_stash_layout(P.model, P.layers[c - 1], emb, head,
+                                         P.strategy == TPIPE_S_1F1B_FULL_RECOMP);
                 C.P = C.lay.total;
                 if ((uint64_t)C.P != P.chunk_params[s][c - 1])
                     return set_error(TPIPE_E_STATE, "param layout mismatch");
@@ -586,6 +633,8 @@ TP_API void tpipe_runtime_destroy(tpipe_runtime* rt) {
     cudaSetDevice(rt->device);
     cudaDeviceSynchronize();
     for (int s : rt->owned) {
+        for (void* hp : rt->st[s]->act_free) cudaFreeHost(hp);
+        for (auto& kv : rt->st[s]->act_host) cudaFreeHost(kv.second);
         for (auto& C : rt->st[s]->ch) {
             join_host(C);
             if (C.h_master) cudaFreeHost(C.h_master);

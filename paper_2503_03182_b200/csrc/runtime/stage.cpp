@@ -62,8 +62,10 @@ ParamLayout make_param_layout(const tpipe_model_desc& d, int n_layers, bool emb,
     return P;
 }
 
-StashLayout make_stash_layout(const tpipe_model_desc& d, int n_layers, bool emb, bool head) {
+StashLayout make_stash_layout(const tpipe_model_desc& d, int n_layers, bool emb, bool head,
+                              bool ckpt_only) {
     StashLayout S;
+    S.ckpt_only = ckpt_only;
     const long M = (long)d.micro_batch * d.seq_len, h = d.hidden, a = d.n_heads, f = d.ffn_hidden;
     const long es = d.dtype == TPIPE_BF16 ? 2 : 4;
     long off = 0;
@@ -72,6 +74,36 @@ StashLayout make_stash_layout(const tpipe_model_desc& d, int n_layers, bool emb,
         off += bytes;
         return o;
     };
+    auto internals = [&](StashLayout::L& L) {
+        L.ln1_mean = take(4 * M);
+        L.ln1_rstd = take(4 * M);
+        L.qkv = take(3 * M * h * es);
+        L.o = take(M * h * es);
+        L.lse = take(4 * a * M);
+        L.x_mid = take(M * h * es);
+        L.ln2_mean = take(4 * M);
+        L.ln2_rstd = take(4 * M);
+        L.u = take(M * f * es);
+    };
+    if (ckpt_only) {
+        for (int l = 0; l < n_layers; ++l) {
+            StashLayout::L L{};
+            L.x_in = (l == 0 && !emb) ? -1 : take(M * h * es);
+            S.layer.push_back(L);
+        }
+        if (head) {
+            S.x_f = take(M * h * es);
+            S.lnf_mean = take(4 * M);
+            S.lnf_rstd = take(4 * M);
+            S.ce_lse = take(4 * M);
+        }
+        S.total = off;
+        off = 0;
+        S.scratch.x_in = -1;
+        internals(S.scratch);
+        S.scratch_bytes = off;
+        return S;
+    }
     for (int l = 0; l < n_layers; ++l) {
         StashLayout::L L;
         L.x_in = (l == 0 && !emb) ? -1 : take(M * h * es);
@@ -192,6 +224,14 @@ static LayerPtrs layer_ptrs(const StashLayout::L& L, uint8_t* stash, const void*
     p.ln2_mean = at<float>(stash, L.ln2_mean);
     p.ln2_rstd = at<float>(stash, L.ln2_rstd);
     p.u = stash + L.u;
+    return p;
+}
+
+// full recompute: layer input from the checkpoint stash, internals in `scratch`
+static LayerPtrs scratch_ptrs(const StashLayout& SL, int l, uint8_t* stash, const void* x_in,
+                              uint8_t* scratch) {
+    LayerPtrs p = layer_ptrs(SL.scratch, scratch, nullptr);
+    p.x_in = SL.layer[l].x_in >= 0 ? (const void*)(stash + SL.layer[l].x_in) : x_in;
     return p;
 }
 
@@ -329,11 +369,13 @@ int chunk_forward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P,
     void* ws_ln = ws;
     void* ws_g = ws + M * h * D.es;
     const uint8_t* wb = reinterpret_cast<const uint8_t*>(P.w);
+    uint8_t* scratch = ws + M * (h + D.f) * D.es;   // full-recompute: one layer's internals
     if (lay.emb)
         TRY(embed_fwd(D.dtype, a.tokens, wb + lay.wte * D.es, wb + lay.wpe * D.es,
                       a.stash + SL.layer[0].x_in, D.M, D.s, D.h, st));
     for (int l = 0; l < n; ++l) {
-        LayerPtrs lp = layer_ptrs(SL.layer[l], a.stash, a.in);
+        LayerPtrs lp = SL.ckpt_only ? scratch_ptrs(SL, l, a.stash, a.in, scratch)
+                                    : layer_ptrs(SL.layer[l], a.stash, a.in);
         void* out;
         if (l + 1 < n) out = a.stash + SL.layer[l + 1].x_in;
         else if (lay.head) out = a.stash + SL.x_f;
@@ -341,7 +383,7 @@ int chunk_forward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P,
         TRY(layer_forward(D, layer_w(D, P, l), lp, ws_ln, ws_g, out, st));
     }
     if (lay.head && a.targets) {
-        uint8_t* lnf = ws + M * (h + D.f) * D.es;
+        uint8_t* lnf = scratch + SL.scratch_bytes;
         float* logits = reinterpret_cast<float*>(lnf + M * h * D.es);
         TRY(ln_fwd(D.dtype, a.stash + SL.x_f, wb + lay.lnf_g * D.es, wb + lay.lnf_b * D.es, lnf,
                    at<float>(a.stash, SL.lnf_mean), at<float>(a.stash, SL.lnf_rstd), M, h, st));
@@ -359,7 +401,7 @@ int chunk_backward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P
     const int n = (int)lay.layer.size();
     const long M = D.M, h = D.h;
     const long part = ((M + 63) / 64) * (D.f > 3 * h ? D.f : 3 * h);
-    BwdWs w = carve_bwd(D, a.ws, lay.head, lay.emb, part, 0);
+    BwdWs w = carve_bwd(D, a.ws, lay.head, lay.emb, part, SL.ckpt_only ? SL.scratch_bytes : 0);
     const uint8_t* wb = reinterpret_cast<const uint8_t*>(P.w);
     const void* dy = a.gin;
     if (lay.head) {
@@ -382,7 +424,15 @@ int chunk_backward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P
         dy = w.G0;
     }
     for (int l = n - 1; l >= 0; --l) {
-        LayerPtrs lp = layer_ptrs(SL.layer[l], a.stash, a.in);
+        LayerPtrs lp;
+        if (SL.ckpt_only) {
+            // layer-grouped just-in-time recompute (1F1B + full recompute):
+            // regenerate this layer's internals from its checkpoint, output discarded
+            lp = scratch_ptrs(SL, l, a.stash, a.in, w.rbuf);
+            TRY(layer_forward(D, layer_w(D, P, l), lp, w.ln, w.g, w.dout, st));
+        } else {
+            lp = layer_ptrs(SL.layer[l], a.stash, a.in);
+        }
         void* dx = (l > 0 || lay.emb) ? w.G0 : a.gout;
         TRY(layer_backward(D, layer_w(D, P, l), lp, dy, dx, w, st));
         dy = w.G0;

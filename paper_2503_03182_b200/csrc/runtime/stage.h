@@ -35,9 +35,15 @@ struct StashLayout {
     std::vector<L> layer;   // x_in == -1 for layer 0 when the chunk input is the IN buffer
     long x_f = -1, lnf_mean = -1, lnf_rstd = -1, ce_lse = -1;
     long total = 0;
+    // 1F1B + full recompute: the stash keeps only layer inputs (checkpoints);
+    // one layer's internals live in a scratch (offsets relative to its base)
+    bool ckpt_only = false;
+    L scratch{};
+    long scratch_bytes = 0;
 };
 
-StashLayout make_stash_layout(const tpipe_model_desc& d, int n_layers, bool emb, bool head);
+StashLayout make_stash_layout(const tpipe_model_desc& d, int n_layers, bool emb, bool head,
+                              bool ckpt_only = false);
 
 struct Dims {
     int dtype, M, h, a, hd, f, V, s, b, es;

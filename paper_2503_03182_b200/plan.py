@@ -14,8 +14,10 @@ S_1F1B, S_1F1B_FULL_RECOMP, S_TPIPE, S_TPIPE_TRECOMP = 0, 1, 2, 3
 STRATEGY = {"1f1b": S_1F1B, "1f1b_full_recomp": S_1F1B_FULL_RECOMP, "tpipe": S_TPIPE,
             "tpipe_trecomp": S_TPIPE_TRECOMP}
 OFFLOAD_MODEL_STATE = 1
+OFFLOAD_ACTIVATIONS = 2
 OP_NAMES = ["F", "B", "R", "RECV_ACT", "RECV_GRAD", "SEND_ACT", "SEND_GRAD", "SEND_WAIT", "OPT",
-            "GRAD_D2H", "HOST_OPT", "W_H2D", "W_WAIT"]
+            "GRAD_D2H", "HOST_OPT", "W_H2D", "W_WAIT", "ACT_D2H", "ACT_D2H_WAIT", "ACT_H2D",
+            "ACT_H2D_WAIT"]
 CATS = ["model_state", "io", "act", "recomp_buf", "comm", "workspace"]
 
 
@@ -42,10 +44,11 @@ class Plan:
     """tpipe_plan_create(model, n_stages, n_microbatches, hbm_budget, opts)."""
 
     def __init__(self, model: Model, n_stages: int, n_microbatches: int, hbm_budget: int = 0,
-                 strategy="tpipe", delay_rounds: int = -1, send_window: int = 0, offload: int = 0):
+                 strategy="tpipe", delay_rounds: int = -1, send_window: int = 0, offload: int = 0,
+                 act_distance: int = 0):
         L = lib()
         st = -1 if strategy in (None, "auto") else STRATEGY.get(strategy, strategy)
-        opts = D.PlanOpts(st, delay_rounds, send_window, offload if st >= 0 else -1)
+        opts = D.PlanOpts(st, delay_rounds, send_window, offload if st >= 0 else -1, act_distance)
         self._h = C.c_void_p()
         self.model = model
         check(L.tpipe_plan_create(C.byref(model.c()), n_stages, n_microbatches, hbm_budget,
@@ -55,6 +58,7 @@ class Plan:
         self.p, self.m, self.v = info.n_stages, info.n_microbatches, info.v
         self.strategy, self.k, self.W, self.offload = (info.strategy, info.delay_rounds,
                                                        info.send_window, info.offload)
+        self.act_distance = info.act_distance
         self.layers_chunk = (info.layers_chunk[0], info.layers_chunk[1])
         self.params_total = info.params_total
         self.channels = []

@@ -66,7 +66,7 @@ def rel_l2(a, b):
     return float(np.linalg.norm(a - b) / (np.linalg.norm(b) + 1e-30))
 
 
-@pytest.mark.parametrize("strategy", ["tpipe", "tpipe_trecomp", "1f1b"])
+@pytest.mark.parametrize("strategy", ["tpipe", "tpipe_trecomp", "1f1b", "1f1b_full_recomp"])
 @pytest.mark.parametrize("p", [1, 2, 4])
 def test_step_fp32_parity(strategy, p):
     _P, RT, _PR = mods()
@@ -168,3 +168,46 @@ def test_loss_decreases_bf16():
     tok, tgt = synth.tokens(C1["vocab"], m, C1["micro_batch"], C1["seq_len"], step=0)
     losses = [rt.step(tok, tgt) for _ in range(8)]
     assert losses[-1] < losses[0] - 0.1, losses
+
+
+@pytest.mark.parametrize("dtype", [0, 1])
+def test_full_recompute_bitexact_vs_1f1b(dtype):
+    """1F1B + full layer-grouped recompute (the in-build baseline)
+    regenerates every layer's internals with the same kernels: gradients are
+    bit-identical to plain 1F1B."""
+    _P, RT, _PR = mods()
+    p, m = 2, 4
+    tok, tgt = synth.tokens(C1["vocab"], m, C1["micro_batch"], C1["seq_len"], step=5)
+    out = []
+    for strategy in ("1f1b", "1f1b_full_recomp"):
+        plan, rt, _W = build(C1, p, m, strategy, dtype)
+        loss = rt.step(tok, tgt, RT.STEP_NO_OPT)
+        out.append((loss, [rt.get_grads(s, 1) for s in range(p)]))
+        st = rt.stats()
+        assert all(st["pool_high_water"][s] == plan.peak(s)["total_peak"] for s in range(p))
+    assert out[0][0] == out[1][0]
+    for a, b in zip(out[0][1], out[1][1]):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+@pytest.mark.parametrize("dtype", [0, 1])
+@pytest.mark.parametrize("p", [1, 2, 4])
+def test_activation_offload_bitexact(dtype, p):
+    """Activation offload (chunk-1 stash -> pinned host -> back, R23) moves
+    bytes only: loss and gradients are bit-identical to plain T-Pipe, the
+    pool ledger matches the (smaller) plan peak, and bytes actually moved."""
+    P, RT, _PR = mods()
+    m = 8
+    tok, tgt = synth.tokens(C1["vocab"], m, C1["micro_batch"], C1["seq_len"], step=7)
+    out = []
+    for off in (0, P.OFFLOAD_ACTIVATIONS):
+        plan, rt, _W = build(C1, p, m, "tpipe", dtype, offload=off)
+        loss = rt.step(tok, tgt, RT.STEP_NO_OPT)
+        out.append((loss, [rt.get_grads(s, c) for s in range(p) for c in (1, 2)]))
+        st = rt.stats()
+        assert all(st["pool_high_water"][s] == plan.peak(s)["total_peak"] for s in range(p))
+        if off:
+            assert st["offload_d2h_bytes"] > 0 and st["offload_h2d_bytes"] == st["offload_d2h_bytes"]
+    assert out[0][0] == out[1][0]
+    for a, b in zip(out[0][1], out[1][1]):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))

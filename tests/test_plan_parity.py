@@ -179,3 +179,28 @@ def test_param_packing_matches_plan(strategy, p):
                 ref = W["layers"][l][k] if l is not None else W[k]
                 assert (a == ref).all()
     assert sorted(seen) == list(range(L))
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("dist", [1, 2, 3])
+def test_activation_offload_streams_match_oracle(p, dist):
+    """Activation offload (R23): identical instruction streams and byte peaks;
+    the offloaded plan never needs more HBM than plain T-Pipe."""
+    P = _plan_mod()
+    L = 2 * p if p > 2 else 4
+    od = T.ModelDesc(L, 64, 4, 256, 128, 32, 2, T.BF16)
+    pd = P.Model(L, 64, 4, 256, 128, 32, 2, T.BF16)
+    plan = P.Plan(pd, p, 16, strategy="tpipe", offload=P.OFFLOAD_ACTIVATIONS, act_distance=dist)
+    base = P.Plan(pd, p, 16, strategy="tpipe")
+    st, static = T.build_streams(od, p, 16, "tpipe", offload_activations=True, act_distance=dist)
+    assert T.deadlock_free(st)
+    for s in range(p):
+        got, bufs = plan.ops(s)
+        strip = [{k: o[k] for k in ("kind", "chunk", "mb", "peer", "channel", "msg")} for o in got]
+        assert strip == oracle_ops(st[s])
+        r = T.replay(st[s], static[s])
+        assert plan.peak(s)["total_peak"] == r["total_peak"]
+        assert r["total_peak"] <= base.peak(s)["total_peak"]
+    from paper_2503_03182_b200._lib import TPipeError
+    with pytest.raises(TPipeError, match="activation offload"):
+        P.Plan(pd, p, 16, strategy="tpipe_trecomp", offload=P.OFFLOAD_ACTIVATIONS)
