@@ -455,7 +455,11 @@ int gemm_tc(const GemmDesc& g, cudaStream_t st) {
     // TMA: 16-byte aligned bases and row strides; 32-column epilogue chunks
     if ((g.N % 32) || (g.lda % 8) || (g.ldb % 8)) return -5;
     const int num_m = (g.M + TC_BM - 1) / TC_BM;
-    const bool wide = (long)num_m * ((g.N + 255) / 256) >= num_sms() && g.N % 256 == 0;
+    // N=128 tiles read 8 KB of operands per 64-cycle MMA (128 B/cycle, the
+    // shared-memory limit); N=256 tiles need 96 B/cycle. Prefer 256 whenever
+    // it still occupies >= ~65% of the SMs.
+    // (a ragged last N tile is fine: TMA zero-fills, the epilogue masks n >= N)
+    const bool wide = (long)num_m * ((g.N + 255) / 256) * 3 >= 2L * num_sms();
     const bool amn = !g.a_kmajor, bmn = !g.b_kmajor;
     if (wide) {
         if (!amn && !bmn) return launch_tc<256, false, false>(g, st);

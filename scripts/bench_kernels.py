@@ -46,6 +46,32 @@ gemm_case("fc1_dgrad", M, h, f, 1, 0, K.EPI_STORE)
 gemm_case("fc2_dgrad", M, f, h, 1, 0, K.EPI_STORE)
 gemm_case("fc1_wgrad", f, h, M, 0, 0, K.EPI_ACC_F32)
 gemm_case("qkv_wgrad", 3 * h, h, M, 0, 0, K.EPI_ACC_F32)
+gemm_case("o_fprop", M, h, h, 1, 1, K.EPI_BIAS)
+gemm_case("o_wgrad", h, h, M, 0, 0, K.EPI_ACC_F32)
+V = 50304 if h == 2048 else 32000
+gemm_case("head_fprop", M, V, h, 1, 1, K.EPI_STORE_F32)
+gemm_case("head_dgrad", M, h, V, 1, 0, K.EPI_STORE)
+gemm_case("head_wgrad", V, h, M, 0, 0, K.EPI_ACC_F32)
 gemm_case("sq8192", 8192, 8192, 8192, 1, 1, K.EPI_STORE)
 for o in out:
     print(json.dumps(o))
+
+# attention at the C2 / C3 shape: tcgen05 (default) vs legacy mma.sync
+b, a, d = 1, h // 128, 128
+qkv = (torch.randn((b * s, 3 * h), device=dev) * 0.5).to(torch.bfloat16)
+o = torch.empty((b * s, h), device=dev, dtype=torch.bfloat16)
+lse = torch.empty((b, a, s), device=dev)
+dout = torch.randn((b * s, h), device=dev).to(torch.bfloat16)
+dqkv = torch.empty_like(qkv)
+ws = torch.empty((b, a, s), device=dev)
+ffl = 4.0 * b * a * (s * (s + 1) / 2) * d
+for name, f_fwd, f_bwd in (("tcgen05", lambda: K.tpipe_k_attn_fwd(1, qkv, o, lse, b, s, a, d),
+                            lambda: K.tpipe_k_attn_bwd(1, qkv, o, dout, lse, dqkv, ws, b, s, a, d)),
+                           ("mma", lambda: K.tpipe_k_attn_fwd_mma(qkv, o, lse, b, s, a, d),
+                            lambda: K.tpipe_k_attn_bwd_mma(qkv, o, dout, lse, dqkv, ws, b, s, a, d))):
+    ms = timeit(f_fwd)
+    print(json.dumps(dict(kernel=f"attn_fwd_{name}", s=s, heads=a, d=d, ms=round(ms, 4),
+                          tflops=round(ffl / ms / 1e9, 1))))
+    ms = timeit(f_bwd)
+    print(json.dumps(dict(kernel=f"attn_bwd_{name}", s=s, heads=a, d=d, ms=round(ms, 4),
+                          tflops=round(2.5 * ffl / ms / 1e9, 1))))
