@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(256, 1)
 //   rows : S_j -> P_j (one pass, 128 scores in registers) -> wait PV_{j-1}
 //          -> O *= corr_j (skipped per warp when corr == 1) -> P_j ready
 template <int D>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     fwd2_kernel(const __grid_constant__ CUtensorMap tm_qkv, bf16* __restrict__ o,
                 float* __restrict__ lse, int s, int a) {
     constexpr int TB = Tile<D>::BYTES;
@@ -280,7 +280,9 @@ __global__ void __launch_bounds__(256, 1)
     uint8_t* sQ = sm;
     uint8_t* sK = sQ + TB;                   // STAGES
     uint8_t* sV = sK + STAGES * TB;          // STAGES
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sV + STAGES * TB);
+    float* sMax = reinterpret_cast<float*>(sV + STAGES * TB);   // [2 iters][2 groups][128]
+    float* sSum = sMax + 4 * BR;                                  // [2 groups][128]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sSum + 2 * BR);
     uint64_t* q_full = bar;
     uint64_t* kv_full = bar + 1;             // [STAGES]
     uint64_t* kv_empty = kv_full + STAGES;   // [STAGES]
@@ -307,7 +309,7 @@ __global__ void __launch_bounds__(256, 1)
         }
         mbar_init(&s_full[0], 1);
         mbar_init(&s_full[1], 1);
-        mbar_init(p_full, 128);
+        mbar_init(p_full, 256);
         mbar_init(pv_done, 1);
         fence_mbar_init();
     }
@@ -365,54 +367,60 @@ __global__ void __launch_bounds__(256, 1)
             }
         }
     } else if (warp >= 4) {
-        const int r = threadIdx.x - 128;
+        // 8 softmax warps: row r = TMEM lane (warp % 4 = lane quarter); column
+        // group cg owns scores [64cg, 64cg+64) and O columns [cg D/2, (cg+1) D/2)
+        const int et = threadIdx.x - 128;
+        const int r = et & 127, cg = et >> 7;
         const int q = q0 + r;
-        const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
         const float sc = rsqrtf((float)D) * LOG2E;
         float m = -INFINITY, l = 0.f;
         for (int j = 0; j < nkb; ++j) {
             const uint32_t tS = tmem + (j & 1) * 128 + lane_off;
             mbar_wait(&s_full[j & 1], (j >> 1) & 1);
             tc_fence_after();
-            float sv[BR];
-#pragma unroll
-            for (int c = 0; c < BR / 32; ++c) {
+            float sv[64];
+            {
                 uint32_t rr[32];
-                tmem_ld32(tS + c * 32, rr);
+                tmem_ld32(tS + cg * 64, rr);
 #pragma unroll
-                for (int e = 0; e < 32; ++e) sv[c * 32 + e] = __uint_as_float(rr[e]);
+                for (int e = 0; e < 32; ++e) sv[e] = __uint_as_float(rr[e]);
+                tmem_ld32(tS + cg * 64 + 32, rr);
+                tmem_wait_ld();
+#pragma unroll
+                for (int e = 0; e < 32; ++e) sv[32 + e] = __uint_as_float(rr[e]);
             }
-            tmem_wait_ld();
             const bool diag = (j == nkb - 1);
-            float mx = m;
+            float lmx = -INFINITY;
 #pragma unroll
-            for (int e = 0; e < BR; ++e) {
-                const float x = (diag && j * BR + e > q) ? -INFINITY : sv[e] * sc;
+            for (int e = 0; e < 64; ++e) {
+                const float x = (diag && j * BR + cg * 64 + e > q) ? -INFINITY : sv[e] * sc;
                 sv[e] = x;
-                mx = fmaxf(mx, x);
+                lmx = fmaxf(lmx, x);
             }
+            float* mb = sMax + (j & 1) * 2 * BR;
+            mb[cg * BR + r] = lmx;
+            named_bar_sync(1, 256);
+            const float mx = fmaxf(m, fmaxf(lmx, mb[(cg ^ 1) * BR + r]));
             float rs = 0.f;
-            uint32_t pk[BR / 2];
+            uint32_t pk[32];
 #pragma unroll
-            for (int e = 0; e < BR; e += 2) {
+            for (int e = 0; e < 64; e += 2) {
                 const float p0 = exp2f(sv[e] - mx), p1 = exp2f(sv[e + 1] - mx);
                 rs += p0 + p1;
                 __nv_bfloat162 v2 = __floats2bfloat162_rn(p0, p1);
                 pk[e / 2] = *reinterpret_cast<uint32_t*>(&v2);
             }
             const float corr = exp2f(m - mx);
-            l = l * corr + rs;
+            l = l * corr + rs;        // partial (this group's columns), same m history
             m = mx;
-            // P_j over S_j (64 columns of packed bf16)
-            tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
-            tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
-            // O (holding blocks < j) must be final before it is rescaled
+            tmem_st32(tS + cg * 32, pk);   // P_j over S_j: packed cols [32cg, 32cg+32)
             if (j > 0) {
                 mbar_wait(pv_done, (j - 1) & 1);
                 tc_fence_after();
                 if (__any_sync(0xffffffffu, corr != 1.0f)) {
 #pragma unroll
-                    for (int c = 0; c < D / 32; ++c) {
+                    for (int c = cg * (D / 64); c < (cg + 1) * (D / 64); ++c) {
                         uint32_t ov[32];
                         tmem_ld32(tO + lane_off + c * 32, ov);
                         tmem_wait_ld();
@@ -426,13 +434,16 @@ __global__ void __launch_bounds__(256, 1)
             tc_fence_before();
             mbar_arrive(p_full);
         }
+        sSum[cg * BR + r] = l;
+        named_bar_sync(1, 256);
+        l += sSum[(cg ^ 1) * BR + r];
         mbar_wait(pv_done, (nkb - 1) & 1);
         tc_fence_after();
         // tcgen05.ld is .sync.aligned: every lane loads; only valid rows store
         const float inv = 1.0f / l;
         bf16* orow = o + ((long)b * s + q) * h + head * D;
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
+        for (int c = cg * (D / 64); c < (cg + 1) * (D / 64); ++c) {
             float v[32];
             tmem_ld32f(tO + lane_off + c * 32, v);
             if (q < s) {
@@ -447,7 +458,7 @@ __global__ void __launch_bounds__(256, 1)
                 }
             }
         }
-        if (q < s) lse[((long)b * a + head) * s + q] = (m + log2f(l)) / LOG2E;
+        if (q < s && cg == 0) lse[((long)b * a + head) * s + q] = (m + log2f(l)) / LOG2E;
     }
     tc_fence_before();
     __syncthreads();
@@ -785,6 +796,395 @@ __global__ void __launch_bounds__(256, 1)
     }
 }
 
+// ============================================================== backward v2
+// 64-row halves so the MMA of half h+1 overlaps the elementwise work of half h.
+// Half tiles are [D/64 atoms][64 rows][128 B] (atom stride 8 KB).
+constexpr int HR = 64;
+__device__ __forceinline__ uint64_t desc_k_h(uint32_t base, int k) {   // 64-row tile, K-major
+    return umma_desc_sw128(base + (k >> 2) * (HR * 128) + (k & 3) * 32, 0, 1024);
+}
+__device__ __forceinline__ uint64_t desc_mn_h(uint32_t base, int k) {  // 64-row tile, MN-major
+    return umma_desc_sw128(base + k * 2048, HR * 128, 1024);
+}
+template <int D>
+__device__ __forceinline__ void tma_half(uint8_t* sm, const CUtensorMap* map, uint64_t* bar, int col,
+                                         int row) {
+#pragma unroll
+    for (int a = 0; a < D / 64; ++a) tma_load_2d(sm + a * (HR * 128), map, bar, col + a * 64, row);
+}
+// write 32 bf16 (cols col0..col0+31, col0 < 64) of row r of a one-atom [rows][64] tile
+__device__ __forceinline__ void st_row32_h(uint8_t* tile, int r, int col0, const float (&v)[32]) {
+    const int c0 = col0 >> 3;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        uint4 u;
+        __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) hh[j] = __floats2bfloat162_rn(v[q * 8 + 2 * j], v[q * 8 + 2 * j + 1]);
+        *reinterpret_cast<uint4*>(tile + swz(r, c0 + q)) = u;
+    }
+}
+
+// dK/dV: CTA owns 128 keys; loops over 64-query halves from the diagonal.
+template <int D>
+__global__ void __launch_bounds__(384, 1)
+    dkdv2_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_qkv64,
+                 const __grid_constant__ CUtensorMap tm_do64, const float* __restrict__ lse,
+                 const float* __restrict__ Dv, bf16* __restrict__ dqkv, int s, int a) {
+    constexpr int TB = Tile<D>::BYTES;          // 128-row tile
+    constexpr int HB = (D / 64) * HR * 128;      // 64-row tile
+    extern __shared__ uint8_t smraw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sK = sm;
+    uint8_t* sV = sK + TB;
+    uint8_t* sQ = sV + TB;                 // [2] half tiles
+    uint8_t* sO = sQ + 2 * HB;             // [2] dO half tiles
+    uint8_t* sP = sO + 2 * HB;             // [2] P^T  [128 keys][64 q] (one atom, 16 KB)
+    uint8_t* sS = sP + 2 * BR * 128;       // [2] dS^T
+    float* sL = reinterpret_cast<float*>(sS + 2 * BR * 128);   // [2][64]
+    float* sD = sL + 2 * HR;                                   // [2][64]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sD + 2 * HR);
+    uint64_t* kv_full = bar;
+    uint64_t* q_full = bar + 1;     // [2]
+    uint64_t* q_empty = bar + 3;    // [2]
+    uint64_t* s_full = bar + 5;     // [2]
+    uint64_t* p_full = bar + 7;     // 128 arrivals per half
+    uint64_t* g_done = bar + 8;     // [2] dV/dK MMAs of a half complete
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int kb = blockIdx.x;
+    const int head = blockIdx.y, b = blockIdx.z;
+    const int h = a * D;
+    const int k0 = kb * BR;
+    const int row0 = b * s;
+    const int hq0 = k0 / HR;                   // first 64-query half at the diagonal
+    const int nh = (s + HR - 1) / HR - hq0;    // halves to process
+    const float* lseb = lse + ((long)b * a + head) * s;
+    const float* Db = Dv + ((long)b * a + head) * s;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tm_qkv);
+        tma_prefetch_desc(&tm_qkv64);
+        tma_prefetch_desc(&tm_do64);
+        mbar_init(kv_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&q_full[i], 1);
+            mbar_init(&q_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&g_done[i], 1);
+        }
+        mbar_init(p_full, 256);
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tdV = tmem + 256, tdK = tmem + 256 + D;   // D <= 128
+
+    if (warp == 0) {
+        if (lane == 0) {
+            mbar_arrive_expect_tx(kv_full, 2 * TB);
+            tma_tile<D>(sK, &tm_qkv, kv_full, h + head * D, row0 + k0);
+            tma_tile<D>(sV, &tm_qkv, kv_full, 2 * h + head * D, row0 + k0);
+            for (int hh = 0; hh < nh; ++hh) {
+                const int sl = hh & 1;
+                mbar_wait(&q_empty[sl], ((hh >> 1) & 1) ^ 1);
+                mbar_arrive_expect_tx(&q_full[sl], 2 * HB);
+                const int qrow = row0 + (hq0 + hh) * HR;
+                tma_half<D>(sQ + sl * HB, &tm_qkv64, &q_full[sl], head * D, qrow);
+                tma_half<D>(sO + sl * HB, &tm_do64, &q_full[sl], head * D, qrow);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t iS = idesc(HR, false, false);   // M=128 keys, N=64 queries
+            const uint32_t iG = idesc(D, false, true);
+            const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
+            mbar_wait(kv_full, 0);
+            auto issue_s = [&](int hh) {
+                const int sl = hh & 1;
+                mbar_wait(&q_full[sl], (hh >> 1) & 1);
+                tc_fence_after();
+                const uint32_t aQ = smem_u32(sQ + sl * HB), aO = smem_u32(sO + sl * HB);
+                const uint32_t tS = tmem + sl * 128, tP = tS + 64;
+#pragma unroll
+                for (int k = 0; k < D / 16; ++k) {
+                    umma_bf16(tS, desc_k(aK, k), desc_k_h(aQ, k), iS, k > 0);   // S^T = K Q^T
+                    umma_bf16(tP, desc_k(aV, k), desc_k_h(aO, k), iS, k > 0);   // dP^T = V dO^T
+                }
+                umma_commit(&s_full[sl]);
+            };
+            issue_s(0);
+            for (int hh = 0; hh < nh; ++hh) {
+                const int sl = hh & 1;
+                if (hh + 1 < nh) issue_s(hh + 1);   // TMEM buffer (hh+1)&1 freed by p_full(hh-1)
+                mbar_wait(p_full, hh & 1);
+                tc_fence_after();
+                const uint32_t aQ = smem_u32(sQ + sl * HB), aO = smem_u32(sO + sl * HB);
+                const uint32_t aP = smem_u32(sP + sl * BR * 128), aS = smem_u32(sS + sl * BR * 128);
+#pragma unroll
+                for (int k = 0; k < HR / 16; ++k) {
+                    umma_bf16(tdV, desc_k(aP, k), desc_mn_h(aO, k), iG, (hh | k) > 0);  // dV += P^T dO
+                    umma_bf16(tdK, desc_k(aS, k), desc_mn_h(aQ, k), iG, (hh | k) > 0);  // dK += dS^T Q
+                }
+                umma_commit(&g_done[sl]);
+                umma_commit(&q_empty[sl]);
+            }
+        }
+    } else if (warp >= 4) {
+        // 8 elementwise warps: row r = TMEM lane (warp % 4 selects the lane quarter),
+        // column group cg = which 32 of the 64 half-columns this thread owns
+        const int et = threadIdx.x - 128;
+        const int r = et & 127, cg = et >> 7;
+        const int key = k0 + r;
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        const float sc = rsqrtf((float)D) * LOG2E;
+        for (int hh = 0; hh < nh; ++hh) {
+            const int sl = hh & 1;
+            const int q0 = (hq0 + hh) * HR;
+            // P/dS buffer and L/D slot `sl` were last read by the MMA of half hh-2
+            if (hh >= 2) mbar_wait(&g_done[sl], ((hh - 2) >> 1) & 1);
+            if (et < HR) {
+                const int qq = q0 + et;
+                sL[sl * HR + et] = qq < s ? lseb[qq] * LOG2E : 0.f;
+                sD[sl * HR + et] = qq < s ? Db[qq] : 0.f;
+            }
+            named_bar_sync(1, 256);
+            mbar_wait(&s_full[sl], (hh >> 1) & 1);
+            tc_fence_after();
+            const uint32_t tS = tmem + sl * 128 + lane_off, tP = tS + 64;
+            uint8_t* P = sP + sl * BR * 128;
+            uint8_t* Sd = sS + sl * BR * 128;
+            const float* L = sL + sl * HR;
+            const float* Dq = sD + sl * HR;
+            {
+                const int c = cg;
+                float sv[32], pv[32];
+                tmem_ld32f(tS + c * 32, sv);
+                tmem_ld32f(tP + c * 32, pv);
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    const int ql = c * 32 + e, qq = q0 + ql;
+                    const float p = (qq >= key && qq < s) ? exp2f(sv[e] * sc - L[ql]) : 0.f;
+                    sv[e] = p;
+                    pv[e] = p * (pv[e] - Dq[ql]);
+                }
+                st_row32_h(P, r, c * 32, sv);
+                st_row32_h(Sd, r, c * 32, pv);
+            }
+            fence_async_smem();
+            tc_fence_before();
+            mbar_arrive(p_full);
+        }
+        mbar_wait(&g_done[(nh - 1) & 1], ((nh - 1) >> 1) & 1);
+        tc_fence_after();
+        const float scale = rsqrtf((float)D);
+        bf16* dkr = dqkv + ((long)b * s + key) * (3L * h) + h + head * D;
+        bf16* dvr = dkr + h;
+#pragma unroll
+        for (int c = cg * (D / 64); c < (cg + 1) * (D / 64); ++c) {
+            float v[32];
+            tmem_ld32f(tdK + lane_off + c * 32, v);
+            if (key < s) {
+#pragma unroll
+                for (int q8 = 0; q8 < 4; ++q8) {
+                    uint4 u;
+                    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj)
+                        h2[jj] = __floats2bfloat162_rn(v[q8 * 8 + 2 * jj] * scale, v[q8 * 8 + 2 * jj + 1] * scale);
+                    *reinterpret_cast<uint4*>(dkr + c * 32 + q8 * 8) = u;
+                }
+            }
+            tmem_ld32f(tdV + lane_off + c * 32, v);
+            if (key < s) {
+#pragma unroll
+                for (int q8 = 0; q8 < 4; ++q8) {
+                    uint4 u;
+                    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj)
+                        h2[jj] = __floats2bfloat162_rn(v[q8 * 8 + 2 * jj], v[q8 * 8 + 2 * jj + 1]);
+                    *reinterpret_cast<uint4*>(dvr + c * 32 + q8 * 8) = u;
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+// dQ: CTA owns 128 queries; loops over 64-key halves up to the diagonal.
+template <int D>
+__global__ void __launch_bounds__(384, 1)
+    dq2_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+               const __grid_constant__ CUtensorMap tm_qkv64, const float* __restrict__ lse,
+               const float* __restrict__ Dv, bf16* __restrict__ dqkv, int s, int a) {
+    constexpr int TB = Tile<D>::BYTES;
+    constexpr int HB = (D / 64) * HR * 128;
+    extern __shared__ uint8_t smraw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = sm;
+    uint8_t* sO = sQ + TB;
+    uint8_t* sK = sO + TB;              // [2] half tiles
+    uint8_t* sV = sK + 2 * HB;          // [2]
+    uint8_t* sS = sV + 2 * HB;          // [2] dS [128 q][64 keys] (one atom)
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sS + 2 * BR * 128);
+    uint64_t* q_full = bar;
+    uint64_t* kv_full = bar + 1;        // [2]
+    uint64_t* kv_empty = bar + 3;       // [2]
+    uint64_t* s_full = bar + 5;         // [2]
+    uint64_t* p_full = bar + 7;
+    uint64_t* g_done = bar + 8;         // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nqb = (s + BR - 1) / BR;
+    const int qb = nqb - 1 - blockIdx.x;
+    const int head = blockIdx.y, b = blockIdx.z;
+    const int h = a * D;
+    const int q0 = qb * BR;
+    const int row0 = b * s;
+    const int last_q = min(q0 + BR, s) - 1;
+    const int nh = last_q / HR + 1;     // key halves 0 .. containing the last query
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tm_qkv);
+        tma_prefetch_desc(&tm_do);
+        tma_prefetch_desc(&tm_qkv64);
+        mbar_init(q_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&kv_full[i], 1);
+            mbar_init(&kv_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&g_done[i], 1);
+        }
+        mbar_init(p_full, 256);
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tdQ = tmem + 256;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            mbar_arrive_expect_tx(q_full, 2 * TB);
+            tma_tile<D>(sQ, &tm_qkv, q_full, head * D, row0 + q0);
+            tma_tile<D>(sO, &tm_do, q_full, head * D, row0 + q0);
+            for (int hh = 0; hh < nh; ++hh) {
+                const int sl = hh & 1;
+                mbar_wait(&kv_empty[sl], ((hh >> 1) & 1) ^ 1);
+                mbar_arrive_expect_tx(&kv_full[sl], 2 * HB);
+                tma_half<D>(sK + sl * HB, &tm_qkv64, &kv_full[sl], h + head * D, row0 + hh * HR);
+                tma_half<D>(sV + sl * HB, &tm_qkv64, &kv_full[sl], 2 * h + head * D, row0 + hh * HR);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t iS = idesc(HR, false, false);   // M=128 q, N=64 keys
+            const uint32_t iG = idesc(D, false, true);
+            const uint32_t aQ = smem_u32(sQ), aO = smem_u32(sO);
+            mbar_wait(q_full, 0);
+            auto issue_s = [&](int hh) {
+                const int sl = hh & 1;
+                mbar_wait(&kv_full[sl], (hh >> 1) & 1);
+                tc_fence_after();
+                const uint32_t aK = smem_u32(sK + sl * HB), aV = smem_u32(sV + sl * HB);
+                const uint32_t tS = tmem + sl * 128, tP = tS + 64;
+#pragma unroll
+                for (int k = 0; k < D / 16; ++k) {
+                    umma_bf16(tS, desc_k(aQ, k), desc_k_h(aK, k), iS, k > 0);   // S = Q K^T
+                    umma_bf16(tP, desc_k(aO, k), desc_k_h(aV, k), iS, k > 0);   // dP = dO V^T
+                }
+                umma_commit(&s_full[sl]);
+            };
+            issue_s(0);
+            for (int hh = 0; hh < nh; ++hh) {
+                const int sl = hh & 1;
+                if (hh + 1 < nh) issue_s(hh + 1);
+                mbar_wait(p_full, hh & 1);
+                tc_fence_after();
+                const uint32_t aK = smem_u32(sK + sl * HB), aS = smem_u32(sS + sl * BR * 128);
+#pragma unroll
+                for (int k = 0; k < HR / 16; ++k)
+                    umma_bf16(tdQ, desc_k(aS, k), desc_mn_h(aK, k), iG, (hh | k) > 0);   // dQ += dS K
+                umma_commit(&g_done[sl]);
+                umma_commit(&kv_empty[sl]);
+            }
+        }
+    } else if (warp >= 4) {
+        const int et = threadIdx.x - 128;
+        const int r = et & 127, cg = et >> 7;
+        const int q = q0 + r;
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        const float sc = rsqrtf((float)D) * LOG2E;
+        const float* lseb = lse + ((long)b * a + head) * s;
+        const float* Db = Dv + ((long)b * a + head) * s;
+        const float L = q < s ? lseb[q] * LOG2E : 0.f;
+        const float Dq = q < s ? Db[q] : 0.f;
+        for (int hh = 0; hh < nh; ++hh) {
+            const int sl = hh & 1;
+            if (hh >= 2) mbar_wait(&g_done[sl], ((hh - 2) >> 1) & 1);   // dS buffer reuse
+            mbar_wait(&s_full[sl], (hh >> 1) & 1);
+            tc_fence_after();
+            const uint32_t tS = tmem + sl * 128 + lane_off, tP = tS + 64;
+            uint8_t* Sd = sS + sl * BR * 128;
+            {
+                const int c = cg;
+                float sv[32], pv[32];
+                tmem_ld32f(tS + c * 32, sv);
+                tmem_ld32f(tP + c * 32, pv);
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    const int key = hh * HR + c * 32 + e;
+                    const float p = (key <= q) ? exp2f(sv[e] * sc - L) : 0.f;
+                    pv[e] = p * (pv[e] - Dq);
+                }
+                st_row32_h(Sd, r, c * 32, pv);
+            }
+            fence_async_smem();
+            tc_fence_before();
+            mbar_arrive(p_full);
+        }
+        mbar_wait(&g_done[(nh - 1) & 1], ((nh - 1) >> 1) & 1);
+        tc_fence_after();
+        const float scale = rsqrtf((float)D);
+        bf16* dqr = dqkv + ((long)b * s + q) * (3L * h) + head * D;
+#pragma unroll
+        for (int c = cg * (D / 64); c < (cg + 1) * (D / 64); ++c) {
+            float v[32];
+            tmem_ld32f(tdQ + lane_off + c * 32, v);
+            if (q < s) {
+#pragma unroll
+                for (int q8 = 0; q8 < 4; ++q8) {
+                    uint4 u;
+                    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj)
+                        h2[jj] = __floats2bfloat162_rn(v[q8 * 8 + 2 * jj] * scale, v[q8 * 8 + 2 * jj + 1] * scale);
+                    *reinterpret_cast<uint4*>(dqr + c * 32 + q8 * 8) = u;
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
 // D[b,head,i] = sum_e dO O (fp32), one warp per row
 __global__ void d_kernel(const bf16* __restrict__ o, const bf16* __restrict__ dout,
                          float* __restrict__ Dv, int s, int a, int d) {
@@ -820,13 +1220,13 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// 2-D bf16 map over [rows, cols] row-major (row stride ld elements), box {64, 128}
-static int map2d(CUtensorMap* m, const void* base, long cols, long rows, long ld) {
+// 2-D bf16 map over [rows, cols] row-major (row stride ld elements), box {64, box_rows}
+static int map2d(CUtensorMap* m, const void* base, long cols, long rows, long ld, int box_rows = 128) {
     auto enc = encode_fn();
     if (!enc) return -1;
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
-    cuuint32_t box[2] = {64, 128};
+    cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
     cuuint32_t es[2] = {1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -838,7 +1238,7 @@ static int map2d(CUtensorMap* m, const void* base, long cols, long rows, long ld
 template <int D>
 static int fwd5(const void* qkv, void* o, float* lse, int b, int s, int a, cudaStream_t st) {
     constexpr int TB = fa5::Tile<D>::BYTES;
-    constexpr int smem = 1024 + TB * 5 + 256;
+    constexpr int smem = 1024 + TB * 5 + 6 * 128 * 4 + 256;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(fa5::fwd2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -847,7 +1247,7 @@ static int fwd5(const void* qkv, void* o, float* lse, int b, int s, int a, cudaS
     CUtensorMap m;
     if (map2d(&m, qkv, 3L * a * D, (long)b * s, 3L * a * D)) return -2;
     dim3 grid((s + 127) / 128, a, b);
-    fa5::fwd2_kernel<D><<<grid, 256, smem, st>>>(m, (bf16*)o, lse, s, a);
+    fa5::fwd2_kernel<D><<<grid, 384, smem, st>>>(m, (bf16*)o, lse, s, a);
     note_launches(1);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
@@ -856,22 +1256,25 @@ template <int D>
 static int bwd5(const void* qkv, const void* o, const void* dout, const float* lse, void* dqkv,
                 float* ws, int b, int s, int a, cudaStream_t st) {
     constexpr int TB = fa5::Tile<D>::BYTES;
-    constexpr int smem_kv = 1024 + TB * 4 + 4 * 128 * 128 + 2 * 128 * 4 + 256;
-    constexpr int smem_q = 1024 + TB * 6 + 2 * 128 * 128 + 256;
+    constexpr int HB = (D / 64) * 64 * 128;
+    constexpr int smem_kv = 1024 + 2 * TB + 4 * HB + 4 * 128 * 128 + 4 * 64 * 4 + 256;
+    constexpr int smem_q = 1024 + 2 * TB + 4 * HB + 2 * 128 * 128 + 256;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(fa5::dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kv);
-        cudaFuncSetAttribute(fa5::dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_q);
+        cudaFuncSetAttribute(fa5::dkdv2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kv);
+        cudaFuncSetAttribute(fa5::dq2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_q);
         attr = true;
     }
-    CUtensorMap mq, md;
+    CUtensorMap mq, mq64, md, md64;
     if (map2d(&mq, qkv, 3L * a * D, (long)b * s, 3L * a * D)) return -2;
+    if (map2d(&mq64, qkv, 3L * a * D, (long)b * s, 3L * a * D, 64)) return -2;
     if (map2d(&md, dout, (long)a * D, (long)b * s, (long)a * D)) return -2;
+    if (map2d(&md64, dout, (long)a * D, (long)b * s, (long)a * D, 64)) return -2;
     dim3 gd((s + 3) / 4, a, b);
     fa5::d_kernel<<<gd, 128, 0, st>>>((const bf16*)o, (const bf16*)dout, ws, s, a, D);
     dim3 grid((s + 127) / 128, a, b);
-    fa5::dkdv_kernel<D><<<grid, 256, smem_kv, st>>>(mq, md, lse, ws, (bf16*)dqkv, s, a);
-    fa5::dq_kernel<D><<<grid, 256, smem_q, st>>>(mq, md, lse, ws, (bf16*)dqkv, s, a);
+    fa5::dkdv2_kernel<D><<<grid, 384, smem_kv, st>>>(mq, mq64, md64, lse, ws, (bf16*)dqkv, s, a);
+    fa5::dq2_kernel<D><<<grid, 384, smem_q, st>>>(mq, md, mq64, lse, ws, (bf16*)dqkv, s, a);
     note_launches(3);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
