@@ -221,8 +221,94 @@ struct TcCfg {
     static constexpr int A_BYTES = TC_BM * TC_BK * 2;
     static constexpr int B_BYTES = BN * TC_BK * 2;
     static constexpr int TMEM_COLS = 2 * BN;
-    static constexpr int SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
+    // epilogue staging: 4 warps x 2 buffers x (32 rows x 128 B)
+    static constexpr int STAGING = 4 * 2 * 4096;
+    static constexpr int SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + STAGING + 256;
 };
+
+// epilogue math on 32 columns n0.. of row m (no stores); out2 for GELU/dGELU.
+// Rows m >= M (TMA clips their stores) skip the residual / aux loads.
+__device__ __forceinline__ void epi_math(const GemmDesc& g, long m, long n0, bool row_ok,
+                                         float (&v)[32], float (&v2)[32]) {
+    const int epi = g.epi;
+    if (epi == EPI_BIAS || epi == EPI_BIAS_RES || epi == EPI_BIAS_GELU) {
+        float b[32];
+        load32<bf16>(reinterpret_cast<const bf16*>(g.bias) + n0, b);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = v[j] + b[j];
+    }
+    if (epi == EPI_BIAS_RES && row_ok) {
+        float r[32];
+        load32<bf16>(reinterpret_cast<const bf16*>(g.res) + m * g.ldr + n0, r);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = v[j] + r[j];
+    }
+    if (epi == EPI_BIAS_GELU) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v2[j] = gelu_tanh(rnd<bf16>(v[j]));
+    }
+    if (epi == EPI_DGELU) {
+        float u[32];
+        if (row_ok) {
+            load32<bf16>(reinterpret_cast<const bf16*>(g.aux) + m * g.ldaux + n0, u);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) u[j] = 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            v2[j] = gelu_tanh(u[j]);
+            v[j] = v[j] * gelu_tanh_grad(u[j]);
+        }
+    }
+}
+
+__device__ __forceinline__ void tma_store_2d(const void* map, const void* smem, int x, int y) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+                 "r"(smem_u32(smem)), "r"(x), "r"(y)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_2d(const void* map, const void* smem, int x, int y) {
+    asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     map),
+                 "r"(smem_u32(smem)), "r"(x), "r"(y)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() {
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// Stage one warp's 32 x 32 chunk (row = lane) in swizzled smem and issue one
+// TMA store (or fp32 reduce-add) of the box at (n0, m0).
+__device__ __forceinline__ void stage_store(uint8_t* buf, const float (&v)[32], bool f32, bool reduce,
+                                            const CUtensorMap* map, int n0, int m0, int lane) {
+    if (lane == 0) bulk_wait_read1();   // the store that last used `buf` has read it
+    __syncwarp();
+    if (f32) {   // 128 B rows, 128B swizzle: chunk q of row r at (q ^ (r & 7))
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            *reinterpret_cast<float4*>(buf + lane * 128 + ((q ^ (lane & 7)) << 4)) =
+                make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    } else {     // 64 B rows, 64B swizzle: chunk q of row r at (q ^ ((r >> 1) & 3))
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint4 u;
+            bf16* hh = reinterpret_cast<bf16*>(&u);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) hh[j] = __float2bfloat16_rn(v[q * 8 + j]);
+            *reinterpret_cast<uint4*>(buf + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) = u;
+        }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+        if (reduce) tma_reduce_add_2d(map, buf, n0, m0);
+        else tma_store_2d(map, buf, n0, m0);
+        bulk_commit();
+    }
+}
 
 // instruction descriptor: bf16 x bf16 -> f32, M=128, N=BN, majors
 template <int BN, bool A_MN, bool B_MN>
@@ -239,6 +325,7 @@ __device__ __forceinline__ uint32_t tc_idesc() {
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(256, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
                    const GemmDesc g, int num_m, int num_n, int num_kb) {
     using Cfg = TcCfg<BN>;
     constexpr int STAGES = Cfg::STAGES;
@@ -246,7 +333,8 @@ __global__ void __launch_bounds__(256, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::B_BYTES);
+    uint8_t* stg = sB + STAGES * Cfg::B_BYTES;          // epilogue staging (1 KB aligned)
+    uint64_t* full = reinterpret_cast<uint64_t*>(stg + Cfg::STAGING);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
@@ -258,6 +346,8 @@ __global__ void __launch_bounds__(256, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
+        tma_prefetch_desc(&tmC);
+        tma_prefetch_desc(&tmC2);
     }
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -343,8 +433,13 @@ __global__ void __launch_bounds__(256, 1)
             }
         }
     } else if (warp >= 4) {
-        // ---------------- epilogue: TMEM -> registers -> fused epilogue -> global
+        // ---------------- epilogue: TMEM -> registers -> fused math -> swizzled smem -> TMA
         const int ew = warp - 4;
+        uint8_t* mystg = stg + ew * 2 * 4096;
+        const bool f32out = (g.epi == EPI_ACC_F32 || g.epi == EPI_STORE_F32);
+        const bool reduce = (g.epi == EPI_ACC_F32);
+        const bool two = (g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU);
+        int sb = 0;
         int it = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
             const int mb = tile % num_m, nb = tile / num_m;
@@ -352,23 +447,31 @@ __global__ void __launch_bounds__(256, 1)
             const uint32_t aph = (it >> 1) & 1;
             mbar_wait(&tfull[acc], aph);
             tc_fence_after();
-            const long m = (long)mb * TC_BM + ew * 32 + lane;
+            const int m0 = mb * TC_BM + ew * 32;
+            const long m = m0 + lane;
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
                 uint32_t r[32];
                 tmem_ld32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + c * 32, r);
                 tmem_wait_ld();
-                const long n0 = (long)nb * BN + c * 32;
-                if (m < g.M && n0 < g.N) {
-                    float v[32];
+                const int n0 = nb * BN + c * 32;
+                if (n0 >= g.N) continue;      // warp-uniform; TMA clips partial rows
+                float v[32], v2[32];
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-                    epi_chunk32<bf16>(g, m, n0, v);
+                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                epi_math(g, m, n0, m < g.M, v, v2);
+                stage_store(mystg + sb * 4096, v, f32out, reduce, &tmC, n0, m0, lane);
+                sb ^= 1;
+                if (two) {
+                    stage_store(mystg + sb * 4096, v2, false, false, &tmC2, n0, m0, lane);
+                    sb ^= 1;
                 }
             }
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
         }
+        if (lane == 0) bulk_wait_all();
+        __syncwarp();
     }
     __syncthreads();
     if (warp == 2) {
@@ -392,18 +495,19 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-// 2-D bf16 tensor map over a row-major [rows, cols] array with row stride ld
-// (elements); box = {box_inner (cols), box_outer (rows)}, 128B swizzle.
+// 2-D tensor map over a row-major [rows, cols] array with row stride ld
+// (elements); box = {box_inner (cols), box_outer (rows)}.
 static int make_map(CUtensorMap* map, const void* base, long cols, long rows, long ld, int box_inner,
-                    int box_outer) {
+                    int box_outer, bool f32 = false,
+                    CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
     auto enc = get_encode();
     if (!enc) return -1;
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+    cuuint64_t strides[1] = {(cuuint64_t)(ld * (f32 ? 4 : 2))};
     cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
     cuuint32_t es[2] = {1, 1};
-    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
-                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+    CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                     const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? 0 : -2;
 }
@@ -433,6 +537,18 @@ static int launch_tc(const GemmDesc& g, cudaStream_t st) {
     else
         rc = make_map(&tb, g.B, g.N, g.K, g.ldb, 64, TC_BK);
     if (rc) return rc;
+    // output maps: 32 x 32 boxes (fp32: 128 B rows, 128B swizzle; bf16: 64 B rows, 64B swizzle)
+    CUtensorMap tc, tc2;
+    const bool f32out = (g.epi == EPI_ACC_F32 || g.epi == EPI_STORE_F32);
+    rc = make_map(&tc, g.C, g.N, g.M, g.ldc, 32, 32, f32out,
+                  f32out ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
+    if (rc) return rc;
+    if (g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU) {
+        rc = make_map(&tc2, g.C2, g.N, g.M, g.ldc2, 32, 32, false, CU_TENSOR_MAP_SWIZZLE_64B);
+        if (rc) return rc;
+    } else {
+        tc2 = tc;
+    }
     const int num_m = (g.M + TC_BM - 1) / TC_BM;
     const int num_n = (g.N + BN - 1) / BN;
     const int num_kb = (g.K + TC_BK - 1) / TC_BK;
@@ -444,7 +560,7 @@ static int launch_tc(const GemmDesc& g, cudaStream_t st) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
         attr_set = true;
     }
-    kern<<<grid, 256, Cfg::SMEM, st>>>(ta, tb, g, num_m, num_n, num_kb);
+    kern<<<grid, 256, Cfg::SMEM, st>>>(ta, tb, tc, tc2, g, num_m, num_n, num_kb);
     note_launches(1);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
@@ -453,7 +569,9 @@ int gemm_tc(const GemmDesc& g, cudaStream_t st) {
     if (g.M <= 0 || g.N <= 0) return 0;
     if (g.K <= 0) return -4;
     // TMA: 16-byte aligned bases and row strides; 32-column epilogue chunks
-    if ((g.N % 32) || (g.lda % 8) || (g.ldb % 8)) return -5;
+    if ((g.N % 32) || (g.lda % 8) || (g.ldb % 8) || (g.ldc % 8) ||
+        ((g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU) && (g.ldc2 % 8)))
+        return -5;
     const int num_m = (g.M + TC_BM - 1) / TC_BM;
     // N=128 tiles read 8 KB of operands per 64-cycle MMA (128 B/cycle, the
     // shared-memory limit); N=256 tiles need 96 B/cycle. Prefer 256 whenever

@@ -53,6 +53,10 @@ gemm_case("head_fprop", M, V, h, 1, 1, K.EPI_STORE_F32)
 gemm_case("head_dgrad", M, h, V, 1, 0, K.EPI_STORE)
 gemm_case("head_wgrad", V, h, M, 0, 0, K.EPI_ACC_F32)
 gemm_case("sq8192", 8192, 8192, 8192, 1, 1, K.EPI_STORE)
+for ak, bk in ((1, 1), (1, 0), (0, 0), (0, 1)):
+    gemm_case(f"sq4096_maj{ak}{bk}_f32", 4096, 4096, 4096, ak, bk, K.EPI_STORE_F32)
+    gemm_case(f"sq4096_maj{ak}{bk}_acc", 4096, 4096, 4096, ak, bk, K.EPI_ACC_F32)
+    gemm_case(f"sq4096_maj{ak}{bk}_bf16", 4096, 4096, 4096, ak, bk, K.EPI_STORE)
 for o in out:
     print(json.dumps(o))
 
