@@ -330,7 +330,10 @@ def run_tpipe(args):
                 "attn_fwd": {"ms_per_step": round(kms[1] / args.steps, 2),
                              "tflops": round(kfl[1] / (kms[1] / 1e3) / 1e12, 1) if kms[1] else None},
                 "attn_bwd": {"ms_per_step": round(kms[2] / args.steps, 2),
-                             "tflops": round(kfl[2] / (kms[2] / 1e3) / 1e12, 1) if kms[2] else None}},
+                             "tflops": round(kfl[2] / (kms[2] / 1e3) / 1e12, 1) if kms[2] else None},
+                "other": {"ms_per_step": round(kms[3] / args.steps, 2),
+                          "launches_per_step": int(kcnt[3] / args.steps)},
+                "idle_ms_per_step": round(step_ms - kms.sum() / args.steps, 2)},
             "clocks": clk.summary(),
         }
     rt.close()

@@ -184,9 +184,10 @@ typedef struct {
     double   offload_d2h_bytes, offload_h2d_bytes;   /* last step */
     double   host_opt_ms;           /* last host optimizer duration */
     /* TPIPE_STEP_PROFILE only: per kernel class (0 GEMM, 1 attention fwd,
-     * 2 attention bwd), summed CUDA-event durations of the launches in the
+     * 2 attention bwd, 3 other), summed CUDA-event durations of the launches in the
      * last step (ms), launch counts and algorithmic FLOPs (2MNK for GEMMs,
-     * causal-triangle counts for attention). */
+     * causal-triangle counts for attention); class 3 = all other stage
+     * kernels (LayerNorm, bias-grad sums, embedding, cross-entropy). */
     double   kernel_ms[4];
     double   kernel_flops[4];
     int64_t  kernel_count[4];

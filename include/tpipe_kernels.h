@@ -60,10 +60,20 @@ int tpipe_k_ln_fwd(int dtype, const void* x, const void* gamma, const void* beta
 
 /* LayerNorm backward: dx = resid + dLN(dy) (resid may be NULL);
  * dgamma/dbeta (fp32 [h]) are ACCUMULATED (+=) deterministically.
- * ws: fp32 scratch of 2*ceil(rows/64)*h elements. */
+ * ws: fp32 scratch of 2*ceil(rows/16)*h elements. */
 int tpipe_k_ln_bwd(int dtype, const void* dy, const void* x, const void* gamma,
                    const float* mean, const float* rstd, const void* resid, void* dx,
                    float* dgamma, float* dbeta, float* ws, int rows, int h, void* stream);
+
+/* tpipe_k_ln_bwd plus dresid_sum[h] += column sums of resid (required, with
+ * resid): in a pre-LN block the gradient entering LN's residual branch is also
+ * the output gradient of the preceding linear, so its bias gradient is fused
+ * here (one pass over resid instead of two). ws: fp32 scratch of
+ * 3*ceil(rows/16)*h elements. */
+int tpipe_k_ln_bwd_rsum(int dtype, const void* dy, const void* x, const void* gamma,
+                        const float* mean, const float* rstd, const void* resid, void* dx,
+                        float* dgamma, float* dbeta, float* dresid_sum, float* ws, int rows,
+                        int h, void* stream);
 
 /* Causal attention forward. qkv [b*s, 3h] (q|k|v, head j at columns j*d),
  * o [b*s, h], lse fp32 [b, a, s]; h = a*d, scale 1/sqrt(d). */
@@ -102,7 +112,7 @@ int tpipe_k_ce_fwd(const float* logits, const int* tgt, float* lse, float* loss_
 int tpipe_k_ce_bwd(int dtype, const float* logits, const int* tgt, const float* lse,
                    void* dlogits, float scale, int rows, int V, void* stream);
 
-/* out[n] += sum_r X[r, n] (fp32, deterministic). ws fp32 [ceil(rows/64)*n]. */
+/* out[n] += sum_r X[r, n] (fp32, deterministic). ws fp32 [ceil(rows/16)*n]. */
 int tpipe_k_colsum(int dtype, const void* X, float* out, float* ws, int rows, int n,
                    void* stream);
 

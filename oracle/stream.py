@@ -92,8 +92,8 @@ def model_state_bytes(d: ModelDesc, P: int, offloaded: bool) -> int:
 
 
 def n_partials(M: int) -> int:
-    """Row blocks of 64 for deterministic column reductions."""
-    return -(-M // 64)
+    """Row blocks of 16 for deterministic column reductions."""
+    return -(-M // 16)
 
 
 def sizes(d: ModelDesc, p: int, v: int, s: int, c: int, full_recomp: bool = False):

@@ -46,6 +46,7 @@ def _declare(L):
     L.tpipe_k_gemm_simt.argtypes = gemm_args
     L.tpipe_k_ln_fwd.argtypes = [i32, vp, vp, vp, vp, vp, vp, i32, i32, vp]
     L.tpipe_k_ln_bwd.argtypes = [i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp]
+    L.tpipe_k_ln_bwd_rsum.argtypes = [i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp]
     L.tpipe_k_attn_fwd.argtypes = [i32, vp, vp, vp, i32, i32, i32, i32, vp]
     L.tpipe_k_attn_bwd.argtypes = [i32, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, vp]
     L.tpipe_k_attn_fwd_mma.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp]

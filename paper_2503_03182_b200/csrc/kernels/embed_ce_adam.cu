@@ -166,9 +166,84 @@ __global__ void ce_loss_kernel(const float* __restrict__ logits, const int* __re
     }
 }
 
+// single pass: per-thread online (max, sum), float4 loads, block combine in a
+// fixed order (V % 4 == 0)
+__device__ __forceinline__ void lse_push(float& m, float& s, float x) {
+    if (x > m) {
+        s = s * expf(m - x) + 1.0f;
+        m = x;
+    } else {
+        s += expf(x - m);
+    }
+}
+
+__global__ void ce_lse1_kernel(const float* __restrict__ logits, float* __restrict__ lse, int V) {
+    const int r = blockIdx.x;
+    const float4* l4 = reinterpret_cast<const float4*>(logits + (long)r * V);
+    __shared__ float rm[32], rsum[32];
+    float m = -INFINITY, s = 0.f;
+    for (int c = threadIdx.x; c < V / 4; c += blockDim.x) {
+        const float4 v = l4[c];
+        lse_push(m, s, v.x);
+        lse_push(m, s, v.y);
+        lse_push(m, s, v.z);
+        lse_push(m, s, v.w);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {   // combine (m, s) pairs within the warp
+        const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+        const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+        const float mm = fmaxf(m, m2);
+        s = (m == -INFINITY ? 0.f : s * expf(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * expf(m2 - mm));
+        m = mm;
+    }
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        rm[w] = m;
+        rsum[w] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float M = -INFINITY;
+        for (int i = 0; i < nw; ++i) M = fmaxf(M, rm[i]);
+        float S = 0.f;
+        for (int i = 0; i < nw; ++i) S += rm[i] == -INFINITY ? 0.f : rsum[i] * expf(rm[i] - M);
+        lse[r] = M + logf(S);
+    }
+}
+
+__global__ void ce_bwd4_kernel(const float* __restrict__ logits, const int* __restrict__ tgt,
+                               const float* __restrict__ lse, bf16* __restrict__ d, float scale,
+                               int rows, int V) {
+    const long i4 = (long)blockIdx.x * blockDim.x + threadIdx.x;   // float4 index
+    if (i4 >= (long)rows * V / 4) return;
+    const long i = i4 * 4;
+    const int r = (int)(i / V), c = (int)(i % V);
+    const float4 v = reinterpret_cast<const float4*>(logits)[i4];
+    const float L = lse[r];
+    const int t = tgt[r];
+    float p0 = expf(v.x - L), p1 = expf(v.y - L), p2 = expf(v.z - L), p3 = expf(v.w - L);
+    if (t == c) p0 -= 1.f;
+    if (t == c + 1) p1 -= 1.f;
+    if (t == c + 2) p2 -= 1.f;
+    if (t == c + 3) p3 -= 1.f;
+    __nv_bfloat162 a = __floats2bfloat162_rn(p0 * scale, p1 * scale);
+    __nv_bfloat162 b = __floats2bfloat162_rn(p2 * scale, p3 * scale);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&a);
+    u.y = *reinterpret_cast<uint32_t*>(&b);
+    reinterpret_cast<uint2*>(d)[i4] = u;
+}
+
 int ce_fwd(const float* logits, const int* tgt, float* lse, float* loss_out, float scale, int rows,
            int V, cudaStream_t st) {
     if (rows <= 0) return 0;
+    if (V % 4 == 0) {
+        ce_lse1_kernel<<<rows, 512, 0, st>>>(logits, lse, V);
+        ce_loss_kernel<<<1, 1024, 0, st>>>(logits, tgt, lse, loss_out, scale, rows, V);
+        note_launches(2);
+        return cudaGetLastError() == cudaSuccess ? 0 : -3;
+    }
     ce_lse_kernel<<<rows, 512, 0, st>>>(logits, lse, V);
     ce_loss_kernel<<<1, 1024, 0, st>>>(logits, tgt, lse, loss_out, scale, rows, V);
     note_launches(2);
@@ -191,6 +266,12 @@ int ce_bwd(int dtype, const float* logits, const int* tgt, const float* lse, voi
            float scale, int rows, int V, cudaStream_t st) {
     if (rows <= 0) return 0;
     const long n = (long)rows * V;
+    if (dtype == DT_BF16 && V % 4 == 0) {
+        ce_bwd4_kernel<<<(int)((n / 4 + 255) / 256), 256, 0, st>>>(logits, tgt, lse, (bf16*)dlogits,
+                                                                   scale, rows, V);
+        note_launches(1);
+        return cudaGetLastError() == cudaSuccess ? 0 : -3;
+    }
     const int blocks = (int)((n + 255) / 256);
     if (dtype == DT_BF16)
         ce_bwd_kernel<bf16><<<blocks, 256, 0, st>>>(logits, tgt, lse, (bf16*)dlogits, scale, rows, V);

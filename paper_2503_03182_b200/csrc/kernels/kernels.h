@@ -46,11 +46,13 @@ int ln_fwd(int dtype, const void* x, const void* gamma, const void* beta, void* 
 // y from saved stats (operator-level recompute); bit-identical to ln_fwd's y.
 int ln_apply(int dtype, const void* x, const void* gamma, const void* beta, const float* mean,
              const float* rstd, void* y, int rows, int h, cudaStream_t st);
-// dx = resid + LN_bwd(dy); dgamma/dbeta partials per 64-row block into ws (fp32
-// [2][nblk][h]), then reduced in block order and ADDED to dgamma/dbeta (fp32).
+// dx = resid + LN_bwd(dy); dgamma/dbeta partials per 16-row block into ws (fp32
+// [2][nblk][h], [3][nblk][h] with dresid_sum), then reduced in a fixed order and
+// ADDED to dgamma/dbeta (fp32). dresid_sum (optional, needs resid): += column
+// sums of resid (the bias gradient of the linear whose output gradient resid is).
 int ln_bwd(int dtype, const void* dy, const void* x, const void* gamma, const float* mean,
            const float* rstd, const void* resid, void* dx, float* dgamma, float* dbeta, float* ws,
-           int rows, int h, cudaStream_t st);
+           int rows, int h, cudaStream_t st, float* dresid_sum = nullptr);
 
 // ---------------------------------------------------------------- attention
 // qkv: [b*s, 3h] (q | k | v, head j = cols j*d..), o: [b*s, h], lse: [b, a, s] fp32.
@@ -84,7 +86,7 @@ int ce_bwd(int dtype, const float* logits, const int* tgt, const float* lse, voi
            float scale, int rows, int V, cudaStream_t st);
 
 // ---------------------------------------------------------------- reductions
-// out[n] += sum_r X[r, n] (deterministic, 64-row partials into ws fp32 [nblk, n]).
+// out[n] += sum_r X[r, n] (deterministic; 16-row partials into ws fp32 [ceil(rows/16), n]).
 int colsum_acc(int dtype, const void* X, float* out, float* ws, int rows, int n, cudaStream_t st);
 
 // ---------------------------------------------------------------- optimizer

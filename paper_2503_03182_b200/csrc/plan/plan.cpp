@@ -75,7 +75,7 @@ static ChunkSizes chunk_sizes(const tpipe_model_desc& d, int p, int v, const int
     if (!emb) stash -= z.act;
     if (head) stash += head_stash;
     z.stash = stash;
-    const uint64_t nb = (M + 63) / 64;
+    const uint64_t nb = (M + 15) / 16;   // 16-row reduction blocks
     uint64_t ws_f = M * (h + f) * es;
     if (full_recomp) ws_f += LS - M * h * es;  // one layer's transient internals
     if (head) ws_f += M * h * es + 4 * M * V + 4 * M;

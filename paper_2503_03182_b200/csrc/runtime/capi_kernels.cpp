@@ -70,6 +70,17 @@ TP_API int tpipe_k_ln_bwd(int dtype, const void* dy, const void* x, const void* 
                      "ln_bwd");
 }
 
+TP_API int tpipe_k_ln_bwd_rsum(int dtype, const void* dy, const void* x, const void* gamma,
+                               const float* mean, const float* rstd, const void* resid, void* dx,
+                               float* dgamma, float* dbeta, float* dresid_sum, float* ws, int rows,
+                               int h, void* stream) {
+    if (int e = chk_dtype(dtype)) return e;
+    if (!resid || !dresid_sum) return set_error(TPIPE_E_INVALID, "ln_bwd_rsum: resid and dresid_sum are required");
+    return launch_rc(ln_bwd(dtype, dy, x, gamma, mean, rstd, resid, dx, dgamma, dbeta, ws, rows, h,
+                            S(stream), dresid_sum),
+                     "ln_bwd_rsum");
+}
+
 TP_API int tpipe_k_attn_fwd(int dtype, const void* qkv, void* o, float* lse, int b, int s, int a,
                             int d, void* stream) {
     if (int e = chk_dtype(dtype)) return e;

@@ -253,7 +253,10 @@ static LW layer_w(const Dims& D, const ChunkParamsDev& P, int l) {
 static int layer_forward(const Dims& D, const LW& W, const LayerPtrs& lp, void* ws_ln, void* ws_g,
                          void* out, cudaStream_t st) {
     const int M = D.M, h = D.h, f = D.f;
-    TRY(ln_fwd(D.dtype, lp.x_in, W.w[LN1_G], W.w[LN1_B], ws_ln, lp.ln1_mean, lp.ln1_rstd, M, h, st));
+    {
+        ProfScope _ps(3, 0.0, st);
+        TRY(ln_fwd(D.dtype, lp.x_in, W.w[LN1_G], W.w[LN1_B], ws_ln, lp.ln1_mean, lp.ln1_rstd, M, h, st));
+    }
     TRY(mm(D, M, 3 * h, h, ws_ln, h, 1, W.w[W_QKV], h, 1, EPI_BIAS, lp.qkv, 3 * h, W.w[B_QKV],
            nullptr, 0, nullptr, 0, nullptr, 0, st));
     {
@@ -262,7 +265,10 @@ static int layer_forward(const Dims& D, const LW& W, const LayerPtrs& lp, void* 
     }
     TRY(mm(D, M, h, h, lp.o, h, 1, W.w[W_O], h, 1, EPI_BIAS_RES, lp.x_mid, h, W.w[B_O], lp.x_in, h,
            nullptr, 0, nullptr, 0, st));
-    TRY(ln_fwd(D.dtype, lp.x_mid, W.w[LN2_G], W.w[LN2_B], ws_ln, lp.ln2_mean, lp.ln2_rstd, M, h, st));
+    {
+        ProfScope _ps(3, 0.0, st);
+        TRY(ln_fwd(D.dtype, lp.x_mid, W.w[LN2_G], W.w[LN2_B], ws_ln, lp.ln2_mean, lp.ln2_rstd, M, h, st));
+    }
     TRY(mm(D, M, f, h, ws_ln, h, 1, W.w[W_1], h, 1, EPI_BIAS_GELU, lp.u, f, W.w[B_1], nullptr, 0,
            ws_g, f, nullptr, 0, st));
     TRY(mm(D, M, h, f, ws_g, f, 1, W.w[W_2], f, 1, EPI_BIAS_RES, out, h, W.w[B_2], lp.x_mid, h,
@@ -326,20 +332,28 @@ static int layer_backward(const Dims& D, const LW& W, const LayerPtrs& lp, const
            lp.u, f, st));
     TRY(mm(D, h, f, M, dy, h, 0, w.g, f, 0, EPI_ACC_F32, W.g[W_2], f, nullptr, nullptr, 0, nullptr,
            0, nullptr, 0, st));
-    TRY(colsum_acc(dt, dy, W.g[B_2], w.part, M, h, st));
     // FC1
-    TRY(ln_apply(dt, lp.x_mid, W.w[LN2_G], W.w[LN2_B], lp.ln2_mean, lp.ln2_rstd, w.ln, M, h, st));
+    {
+        ProfScope _ps(3, 0.0, st);
+        TRY(ln_apply(dt, lp.x_mid, W.w[LN2_G], W.w[LN2_B], lp.ln2_mean, lp.ln2_rstd, w.ln, M, h, st));
+    }
     TRY(mm(D, f, h, M, w.du, f, 0, w.ln, h, 0, EPI_ACC_F32, W.g[W_1], h, nullptr, nullptr, 0,
            nullptr, 0, nullptr, 0, st));
-    TRY(colsum_acc(dt, w.du, W.g[B_1], w.part, M, f, st));
+    {
+        ProfScope _ps(3, 0.0, st);
+        TRY(colsum_acc(dt, w.du, W.g[B_1], w.part, M, f, st));
+    }
     TRY(mm(D, M, h, f, w.du, f, 1, W.w[W_1], h, 0, EPI_STORE, w.dln, h, nullptr, nullptr, 0,
            nullptr, 0, nullptr, 0, st));
-    TRY(ln_bwd(dt, w.dln, lp.x_mid, W.w[LN2_G], lp.ln2_mean, lp.ln2_rstd, dy, w.G1, W.g[LN2_G],
-               W.g[LN2_B], w.part, M, h, st));
+    {
+        ProfScope _ps(3, 0.0, st);
+        // + dB2 = colsum(dy), fused (dy is LN2's residual-branch gradient)
+        TRY(ln_bwd(dt, w.dln, lp.x_mid, W.w[LN2_G], lp.ln2_mean, lp.ln2_rstd, dy, w.G1, W.g[LN2_G],
+                   W.g[LN2_B], w.part, M, h, st, W.g[B_2]));
+    }
     // out-proj
     TRY(mm(D, h, h, M, w.G1, h, 0, lp.o, h, 0, EPI_ACC_F32, W.g[W_O], h, nullptr, nullptr, 0,
            nullptr, 0, nullptr, 0, st));
-    TRY(colsum_acc(dt, w.G1, W.g[B_O], w.part, M, h, st));
     TRY(mm(D, M, h, h, w.G1, h, 1, W.w[W_O], h, 0, EPI_STORE, w.dout, h, nullptr, nullptr, 0,
            nullptr, 0, nullptr, 0, st));
     // attention (P recomputed from LSE)
@@ -349,14 +363,24 @@ static int layer_backward(const Dims& D, const LW& W, const LayerPtrs& lp, const
         TRY(attn_bwd(dt, lp.qkv, lp.o, w.dout, lp.lse, w.dqkv, w.Dv, D.b, D.s, D.a, D.hd, st));
     }
     // QKV
-    TRY(ln_apply(dt, lp.x_in, W.w[LN1_G], W.w[LN1_B], lp.ln1_mean, lp.ln1_rstd, w.ln, M, h, st));
+    {
+        ProfScope _ps(3, 0.0, st);
+        TRY(ln_apply(dt, lp.x_in, W.w[LN1_G], W.w[LN1_B], lp.ln1_mean, lp.ln1_rstd, w.ln, M, h, st));
+    }
     TRY(mm(D, 3 * h, h, M, w.dqkv, 3 * h, 0, w.ln, h, 0, EPI_ACC_F32, W.g[W_QKV], h, nullptr,
            nullptr, 0, nullptr, 0, nullptr, 0, st));
-    TRY(colsum_acc(dt, w.dqkv, W.g[B_QKV], w.part, M, 3 * h, st));
+    {
+        ProfScope _ps(3, 0.0, st);
+        TRY(colsum_acc(dt, w.dqkv, W.g[B_QKV], w.part, M, 3 * h, st));
+    }
     TRY(mm(D, M, h, 3 * h, w.dqkv, 3 * h, 1, W.w[W_QKV], h, 0, EPI_STORE, w.dln, h, nullptr,
            nullptr, 0, nullptr, 0, nullptr, 0, st));
-    TRY(ln_bwd(dt, w.dln, lp.x_in, W.w[LN1_G], lp.ln1_mean, lp.ln1_rstd, w.G1, dx, W.g[LN1_G],
-               W.g[LN1_B], w.part, M, h, st));
+    {
+        ProfScope _ps(3, 0.0, st);
+        // + dBo = colsum(G1), fused (G1 is LN1's residual-branch gradient)
+        TRY(ln_bwd(dt, w.dln, lp.x_in, W.w[LN1_G], lp.ln1_mean, lp.ln1_rstd, w.G1, dx, W.g[LN1_G],
+                   W.g[LN1_B], w.part, M, h, st, W.g[B_O]));
+    }
     return 0;
 }
 
@@ -371,8 +395,11 @@ int chunk_forward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P,
     const uint8_t* wb = reinterpret_cast<const uint8_t*>(P.w);
     uint8_t* scratch = ws + M * (h + D.f) * D.es;   // full-recompute: one layer's internals
     if (lay.emb)
-        TRY(embed_fwd(D.dtype, a.tokens, wb + lay.wte * D.es, wb + lay.wpe * D.es,
+        {
+            ProfScope _ps(3, 0.0, st);
+            TRY(embed_fwd(D.dtype, a.tokens, wb + lay.wte * D.es, wb + lay.wpe * D.es,
                       a.stash + SL.layer[0].x_in, D.M, D.s, D.h, st));
+        }
     for (int l = 0; l < n; ++l) {
         LayerPtrs lp = SL.ckpt_only ? scratch_ptrs(SL, l, a.stash, a.in, scratch)
                                     : layer_ptrs(SL.layer[l], a.stash, a.in);
@@ -385,12 +412,18 @@ int chunk_forward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P,
     if (lay.head && a.targets) {
         uint8_t* lnf = scratch + SL.scratch_bytes;
         float* logits = reinterpret_cast<float*>(lnf + M * h * D.es);
-        TRY(ln_fwd(D.dtype, a.stash + SL.x_f, wb + lay.lnf_g * D.es, wb + lay.lnf_b * D.es, lnf,
+        {
+            ProfScope _ps(3, 0.0, st);
+            TRY(ln_fwd(D.dtype, a.stash + SL.x_f, wb + lay.lnf_g * D.es, wb + lay.lnf_b * D.es, lnf,
                    at<float>(a.stash, SL.lnf_mean), at<float>(a.stash, SL.lnf_rstd), M, h, st));
+        }
         TRY(mm(D, M, D.V, h, lnf, h, 1, wb + lay.w_head * D.es, h, 1, EPI_STORE_F32, logits, D.V,
                nullptr, nullptr, 0, nullptr, 0, nullptr, 0, st));
-        TRY(ce_fwd(logits, a.targets, at<float>(a.stash, SL.ce_lse), a.loss_slot, a.loss_scale, M,
+        {
+            ProfScope _ps(3, 0.0, st);
+            TRY(ce_fwd(logits, a.targets, at<float>(a.stash, SL.ce_lse), a.loss_slot, a.loss_scale, M,
                    D.V, st));
+        }
     }
     return 0;
 }
@@ -400,27 +433,36 @@ int chunk_backward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P
     const ParamLayout& lay = *P.lay;
     const int n = (int)lay.layer.size();
     const long M = D.M, h = D.h;
-    const long part = ((M + 63) / 64) * (D.f > 3 * h ? D.f : 3 * h);
+    const long part = ((M + 15) / 16) * (D.f > 3 * h ? D.f : 3 * h);
     BwdWs w = carve_bwd(D, a.ws, lay.head, lay.emb, part, SL.ckpt_only ? SL.scratch_bytes : 0);
     const uint8_t* wb = reinterpret_cast<const uint8_t*>(P.w);
     const void* dy = a.gin;
     if (lay.head) {
         const void* ln_g = wb + lay.lnf_g * D.es;
-        TRY(ln_apply(D.dtype, a.stash + SL.x_f, ln_g, wb + lay.lnf_b * D.es,
+        {
+            ProfScope _ps(3, 0.0, st);
+            TRY(ln_apply(D.dtype, a.stash + SL.x_f, ln_g, wb + lay.lnf_b * D.es,
                      at<float>(a.stash, SL.lnf_mean), at<float>(a.stash, SL.lnf_rstd), w.lnf, M, h,
                      st));
+        }
         const void* wh = wb + lay.w_head * D.es;
         TRY(mm(D, M, D.V, h, w.lnf, h, 1, wh, h, 1, EPI_STORE_F32, w.logits, D.V, nullptr, nullptr,
                0, nullptr, 0, nullptr, 0, st));
-        TRY(ce_bwd(D.dtype, w.logits, a.targets, at<float>(a.stash, SL.ce_lse), w.dlogits,
+        {
+            ProfScope _ps(3, 0.0, st);
+            TRY(ce_bwd(D.dtype, w.logits, a.targets, at<float>(a.stash, SL.ce_lse), w.dlogits,
                    a.loss_scale, M, D.V, st));
+        }
         TRY(mm(D, D.V, h, M, w.dlogits, D.V, 0, w.lnf, h, 0, EPI_ACC_F32, P.grad + lay.w_head, h,
                nullptr, nullptr, 0, nullptr, 0, nullptr, 0, st));
         TRY(mm(D, M, h, D.V, w.dlogits, D.V, 1, wh, h, 0, EPI_STORE, w.dlnf, h, nullptr, nullptr, 0,
                nullptr, 0, nullptr, 0, st));
-        TRY(ln_bwd(D.dtype, w.dlnf, a.stash + SL.x_f, ln_g, at<float>(a.stash, SL.lnf_mean),
+        {
+            ProfScope _ps(3, 0.0, st);
+            TRY(ln_bwd(D.dtype, w.dlnf, a.stash + SL.x_f, ln_g, at<float>(a.stash, SL.lnf_mean),
                    at<float>(a.stash, SL.lnf_rstd), nullptr, w.G0, P.grad + lay.lnf_g,
                    P.grad + lay.lnf_b, w.part, M, h, st));
+        }
         dy = w.G0;
     }
     for (int l = n - 1; l >= 0; --l) {
@@ -438,8 +480,11 @@ int chunk_backward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P
         dy = w.G0;
     }
     if (lay.emb)
-        TRY(embed_bwd(D.dtype, a.tokens, w.G0, P.grad + lay.wte, P.grad + lay.wpe, w.emb_ws, M, D.s,
+        {
+            ProfScope _ps(3, 0.0, st);
+            TRY(embed_bwd(D.dtype, a.tokens, w.G0, P.grad + lay.wte, P.grad + lay.wpe, w.emb_ws, M, D.s,
                       h, st));
+        }
     return 0;
 }
 

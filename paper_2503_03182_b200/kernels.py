@@ -39,6 +39,12 @@ def tpipe_k_ln_bwd(dtype, dy, x, g, mean, rstd, resid, dx, dg, db, ws, rows, h):
                                _p(dg), _p(db), _p(ws), rows, h, _stream()), "ln_bwd")
 
 
+def tpipe_k_ln_bwd_rsum(dtype, dy, x, g, mean, rstd, resid, dx, dg, db, drs, ws, rows, h):
+    check(lib().tpipe_k_ln_bwd_rsum(dtype, _p(dy), _p(x), _p(g), _p(mean), _p(rstd), _p(resid),
+                                    _p(dx), _p(dg), _p(db), _p(drs), _p(ws), rows, h, _stream()),
+          "ln_bwd_rsum")
+
+
 def tpipe_k_attn_fwd(dtype, qkv, o, lse, b, s, a, d):
     check(lib().tpipe_k_attn_fwd(dtype, _p(qkv), _p(o), _p(lse), b, s, a, d, _stream()), "attn_fwd")
 

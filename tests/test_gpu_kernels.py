@@ -138,7 +138,8 @@ def test_gemm_fp32_simt(majors):
 
 # ------------------------------------------------------------------ LayerNorm
 @pytest.mark.parametrize("dtype", ["fp32", "bf16"])
-@pytest.mark.parametrize("rows,hd", [(64, 64), (130, 2048), (5, 5120)])
+@pytest.mark.parametrize("rows,hd", [(64, 64), (130, 2048), (5, 5120), (45, 1024), (3, 4096),
+                                     (9, 256)])
 def test_layernorm(dtype, rows, hd):
     dt = 1 if dtype == "bf16" else 0
     rng = np.random.default_rng(rows)
@@ -156,7 +157,7 @@ def test_layernorm(dtype, rows, hd):
     dx = torch.empty_like(x)
     dg = torch.zeros(hd, device=dev)
     db = torch.zeros(hd, device=dev)
-    ws = torch.empty(2 * ((rows + 63) // 64) * hd, device=dev)
+    ws = torch.empty(2 * ((rows + 15) // 16) * hd, device=dev)
     k.tpipe_k_ln_bwd(dt, dy, x, g, mean, rstd, res, dx, dg, db, ws, rows, hd)
     torch.cuda.synchronize()
     dxr, dgr, dbr = R.ln_bwd(h(dy), cache)
@@ -166,6 +167,46 @@ def test_layernorm(dtype, rows, hd):
     assert metric(h(dx), dxr + h(res)) < tol
     assert max_rel(h(dg), dgr) < (1e-2 if dtype == "bf16" else 1e-4)
     assert max_rel(h(db), dbr) < 1e-4
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("rows,hd", [(64, 64), (130, 2048), (45, 1024), (33, 4096)])
+def test_layernorm_bwd_rsum(dtype, rows, hd):
+    """ln_bwd with the fused residual-gradient column sum (bias grad of the
+    preceding linear): equals ln_bwd + colsum(resid), accumulates (+=), and is
+    bit-reproducible run to run."""
+    dt = 1 if dtype == "bf16" else 0
+    rng = np.random.default_rng(rows + hd)
+    x = t(rng.standard_normal((rows, hd)) * 2 + 0.5, dtype)
+    g = t(1 + 0.1 * rng.standard_normal(hd), dtype)
+    b = t(0.1 * rng.standard_normal(hd), dtype)
+    dy = t(rng.standard_normal((rows, hd)), dtype)
+    res = t(rng.standard_normal((rows, hd)), dtype)
+    y = torch.empty_like(x)
+    mean = torch.empty(rows, device=dev)
+    rstd = torch.empty(rows, device=dev)
+    k = K()
+    k.tpipe_k_ln_fwd(dt, x, g, b, y, mean, rstd, rows, hd)
+    _, cache = R.ln_fwd(h(x), h(g), h(b))
+    dxr, dgr, dbr = R.ln_bwd(h(dy), cache)
+    ws = torch.empty(3 * ((rows + 15) // 16) * hd, device=dev)
+    outs = []
+    for _ in range(2):
+        dx = torch.empty_like(x)
+        dg = torch.zeros(hd, device=dev)
+        db = torch.zeros(hd, device=dev)
+        drs = torch.full((hd,), 0.25, device=dev)
+        k.tpipe_k_ln_bwd_rsum(dt, dy, x, g, mean, rstd, res, dx, dg, db, drs, ws, rows, hd)
+        torch.cuda.synchronize()
+        outs.append((dx.clone(), dg.clone(), db.clone(), drs.clone()))
+    dx, dg, db, drs = outs[0]
+    for u, v in zip(outs[0], outs[1]):
+        assert torch.equal(u, v)
+    tol, metric = (2e-2, rel_l2) if dtype == "bf16" else (1e-4, max_rel)
+    assert metric(h(dx), dxr + h(res)) < tol
+    assert max_rel(h(dg), dgr) < (1e-2 if dtype == "bf16" else 1e-4)
+    assert max_rel(h(db), dbr) < 1e-4
+    assert max_rel(h(drs), 0.25 + h(res).sum(0)) < 1e-4
 
 
 # ------------------------------------------------------------------ attention
@@ -270,15 +311,16 @@ def test_cross_entropy(dtype):
     assert (rel_l2 if dt else max_rel)(h(d), P / rows) < tol
 
 
-def test_colsum():
-    rows, n = 300, 192
+@pytest.mark.parametrize("rows,n", [(300, 192), (2048, 2048), (130, 8192), (37, 6144), (16, 2056)])
+def test_colsum(rows, n):
     rng = np.random.default_rng(2)
-    X = t(rng.standard_normal((rows, n)), "fp32")
-    out = torch.ones(n, device=dev)
-    ws = torch.empty(((rows + 63) // 64) * n, device=dev)
-    K().tpipe_k_colsum(0, X, out, ws, rows, n)
-    torch.cuda.synchronize()
-    assert max_rel(h(out), 1 + h(X).sum(0)) < 1e-5
+    for dtype in ("fp32", "bf16"):
+        X = t(rng.standard_normal((rows, n)), dtype)
+        out = torch.ones(n, device=dev)
+        ws = torch.empty(((rows + 15) // 16) * n, device=dev)
+        K().tpipe_k_colsum(1 if dtype == "bf16" else 0, X, out, ws, rows, n)
+        torch.cuda.synchronize()
+        assert max_rel(h(out), 1 + h(X).sum(0)) < 1e-5
 
 
 # ------------------------------------------------------------------ AdamW
