@@ -1,11 +1,13 @@
 // Causal flash attention on 5th-generation tensor cores (tcgen05 + TMEM + TMA),
 // bf16, head_dim 64 / 128 (FlashAttention is the paper's
-// default). One CTA = 128 query rows (fwd, dQ) or 128 keys (dK/dV) of
-// one (sequence, head).
+// default). Persistent kernels: one CTA per SM loops over work items of
+// 128 query rows (fwd, dQ) or 128 keys (dK/dV) of one (sequence, head), dealt
+// heaviest first (causal work) in zigzag rounds.
 //
-// Roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer (one
-// thread), warp 2 = TMEM allocator, warps 4..7 = 128 "row" threads (thread r
-// owns TMEM lane r = one query / key row) doing softmax / dS and epilogues.
+// Roles (384 threads): warp 0 = TMA producer, warp 1 = MMA issuer (one
+// thread), warp 2 = TMEM allocator, warps 4..11 = 256 elementwise threads
+// (two column groups; thread r of a group owns TMEM lane r = one query / key
+// row) doing softmax / dS and the epilogues.
 //
 // Shared-memory tiles are [64-element atom][rows][128 B] with the 128-byte
 // swizzle, so one tile serves as a K-major operand (rows = M/N, K = head dim)
@@ -94,221 +96,76 @@ __device__ __forceinline__ void tma_tile(uint8_t* sm, const CUtensorMap* map, ui
     for (int a = 0; a < D / 64; ++a) tma_load_2d(sm + a * (BR * 128), map, bar, col + a * 64, row);
 }
 
-// ============================================================== forward
-template <int D>
-__global__ void __launch_bounds__(256, 1)
-    fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, bf16* __restrict__ o,
-               float* __restrict__ lse, int s, int a) {
-    constexpr int TB = Tile<D>::BYTES;
-    constexpr int STAGES = 2;
-    extern __shared__ uint8_t smraw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sQ = sm;
-    uint8_t* sK = sQ + TB;                   // STAGES
-    uint8_t* sV = sK + STAGES * TB;          // STAGES
-    uint8_t* sP = sV + STAGES * TB;          // 128 x 128 bf16 (2 atoms)
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sP + 2 * BR * 128);
-    uint64_t* q_full = bar;
-    uint64_t* kv_full = bar + 1;             // [STAGES]
-    uint64_t* kv_empty = kv_full + STAGES;   // [STAGES]
-    uint64_t* s_full = kv_empty + STAGES;
-    uint64_t* p_full = s_full + 1;
-    uint64_t* o_full = p_full + 1;           // PV done (also frees P and S)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nqb = (s + BR - 1) / BR;
-    const int qb = nqb - 1 - blockIdx.x;  // heaviest first
-    const int head = blockIdx.y, b = blockIdx.z;
-    const int h = a * D;
-    const int q0 = qb * BR;
-    const int row0 = b * s;               // first row of this sequence in [b*s, 3h]
-    const int nkb = qb + 1;               // key blocks 0..qb (BR == BN)
-
-    if (warp == 0 && lane == 0) {
-        tma_prefetch_desc(&tm_qkv);
-        mbar_init(q_full, 1);
-        for (int i = 0; i < STAGES; ++i) {
-            mbar_init(&kv_full[i], 1);
-            mbar_init(&kv_empty[i], 1);
-        }
-        mbar_init(s_full, 1);
-        mbar_init(p_full, 128);
-        mbar_init(o_full, 1);
-        fence_mbar_init();
-    }
-    if (warp == 2) tmem_alloc(tmem_slot, 512);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    const uint32_t tS = tmem, tO = tmem + 256;
-
-    if (warp == 0) {
-        if (lane == 0) {
-            mbar_arrive_expect_tx(q_full, TB);
-            tma_tile<D>(sQ, &tm_qkv, q_full, head * D, row0 + q0);
-            for (int j = 0; j < nkb; ++j) {
-                const int st = j % STAGES;
-                mbar_wait(&kv_empty[st], ((j / STAGES) & 1) ^ 1);
-                mbar_arrive_expect_tx(&kv_full[st], 2 * TB);
-                tma_tile<D>(sK + st * TB, &tm_qkv, &kv_full[st], h + head * D, row0 + j * BR);
-                tma_tile<D>(sV + st * TB, &tm_qkv, &kv_full[st], 2 * h + head * D, row0 + j * BR);
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            const uint32_t iS = idesc(BR, false, false);
-            const uint32_t iO = idesc(D, false, true);
-            const uint32_t aQ = smem_u32(sQ), aP = smem_u32(sP);
-            mbar_wait(q_full, 0);
-            for (int j = 0; j < nkb; ++j) {
-                const int st = j % STAGES;
-                mbar_wait(&kv_full[st], (j / STAGES) & 1);
-                if (j > 0) mbar_wait(o_full, (j - 1) & 1);   // S/P of block j-1 consumed
-                tc_fence_after();
-                const uint32_t aK = smem_u32(sK + st * TB), aV = smem_u32(sV + st * TB);
-#pragma unroll
-                for (int k = 0; k < D / 16; ++k) umma_bf16(tS, desc_k(aQ, k), desc_k(aK, k), iS, k > 0);
-                umma_commit(s_full);
-                mbar_wait(p_full, j & 1);
-                tc_fence_after();
-#pragma unroll
-                for (int k = 0; k < BR / 16; ++k) umma_bf16(tO, desc_k(aP, k), desc_mn(aV, k), iO, k > 0);
-                umma_commit(o_full);
-                umma_commit(&kv_empty[st]);
-            }
-        }
-    } else if (warp >= 4) {
-        const int r = threadIdx.x - 128;           // query row within the tile == TMEM lane
-        const int q = q0 + r;
-        const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
-        const float sc = rsqrtf((float)D) * LOG2E;
-        float m = -INFINITY, l = 0.f;
-        float oacc[D];
-#pragma unroll
-        for (int i = 0; i < D; ++i) oacc[i] = 0.f;
-        for (int j = 0; j < nkb; ++j) {
-            mbar_wait(s_full, j & 1);
-            tc_fence_after();
-            const bool diag = (j == nkb - 1);
-            // pass 1: row max of the scaled, masked scores
-            float mx = m;
-#pragma unroll
-            for (int c = 0; c < BR / 32; ++c) {
-                float v[32];
-                tmem_ld32f(tS + lane_off + c * 32, v);
-#pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    const int key = j * BR + c * 32 + e;
-                    const float x = (diag && key > q) ? -INFINITY : v[e] * sc;
-                    mx = fmaxf(mx, x);
-                }
-            }
-            const float corr = exp2f(m - mx);
-            float rs = 0.f;
-            // pass 2: P = exp2(x - mx) -> smem (bf16), row sum
-#pragma unroll
-            for (int c = 0; c < BR / 32; ++c) {
-                float v[32];
-                tmem_ld32f(tS + lane_off + c * 32, v);
-#pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    const int key = j * BR + c * 32 + e;
-                    const float p = (diag && key > q) ? 0.f : exp2f(v[e] * sc - mx);
-                    v[e] = p;
-                    rs += p;
-                }
-                st_row32(sP, r, c * 32, v);
-            }
-            l = l * corr + rs;
-            m = mx;
-            fence_async_smem();
-            tc_fence_before();
-            mbar_arrive(p_full);
-            // O = O * corr + P V
-            mbar_wait(o_full, j & 1);
-            tc_fence_after();
-#pragma unroll
-            for (int c = 0; c < D / 32; ++c) {
-                float v[32];
-                tmem_ld32f(tO + lane_off + c * 32, v);
-#pragma unroll
-                for (int e = 0; e < 32; ++e) oacc[c * 32 + e] = oacc[c * 32 + e] * corr + v[e];
-            }
-            tc_fence_before();
-        }
-        if (q < s) {
-            const float inv = 1.0f / l;
-            bf16* orow = o + ((long)b * s + q) * h + head * D;
-#pragma unroll
-            for (int c = 0; c < D / 8; ++c) {
-                uint4 u;
-                __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-                for (int jj = 0; jj < 4; ++jj)
-                    hh[jj] = __floats2bfloat162_rn(oacc[c * 8 + 2 * jj] * inv, oacc[c * 8 + 2 * jj + 1] * inv);
-                *reinterpret_cast<uint4*>(orow + c * 8) = u;
-            }
-            lse[((long)b * a + head) * s + q] = (m + log2f(l)) / LOG2E;
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 2) {
-        tc_fence_after();
-        tmem_dealloc(tmem, 512);
-    }
+// ---------------------------------------------------------------- persistent schedule
+// grid = min(items, SMs); items are numbered heaviest first (causal work falls
+// with the item index) and dealt to CTAs in zigzag rounds: round r gives item
+// r*G + c (r even) or r*G + G-1-c (r odd) to CTA c — a static LPT-style
+// assignment, so every output row still has exactly one owner.
+__device__ __forceinline__ int sched_item(int k, int T) {
+    const int G = gridDim.x, c = blockIdx.x;
+    const int t = k * G + ((k & 1) ? (G - 1 - c) : c);
+    return t < T ? t : -1;
 }
 
-// ============================================================== forward v2
+// ============================================================== forward (persistent)
 // S double-buffered in TMEM (columns [0,128) and [128,256)); P_j is written
 // back over S_j as packed bf16 (64 columns) and consumed as the TMEM
 // A-operand of O += P_j V_j; O (D columns at 256) accumulates in TMEM and is
 // rescaled in place by the row threads when the running max moves.
-//   MMA  : S_0 | for j: [S_{j+1} once PV_{j-1} freed its buffer] [PV_j once P_j ready]
-//   rows : S_j -> P_j (one pass, 128 scores in registers) -> wait PV_{j-1}
-//          -> O *= corr_j (skipped per warp when corr == 1) -> P_j ready
+// All rings (K/V stages, S buffers, P/PV handshakes) run on a global tile
+// counter g that continues across this CTA's items, so the S MMA of an item's
+// first tile overlaps the previous item's last softmax and epilogue; Q is
+// double-buffered per item.
+//   MMA  : S_0 | for g: [S_{g+1} once PV_{g-1} freed its buffer] [PV_g once P_g ready]
+//   rows : S_g -> P_g (one pass, 64 scores per thread in registers) -> wait PV_{g-1}
+//          -> O *= corr_g (skipped per warp when corr == 1) -> P_g ready
+// Item t (heaviest first): qb = nqb-1 - t/(a*nb), head = t%a, batch = (t/a)%nb.
 template <int D>
 __global__ void __launch_bounds__(384, 1)
     fwd2_kernel(const __grid_constant__ CUtensorMap tm_qkv, bf16* __restrict__ o,
-                float* __restrict__ lse, int s, int a) {
+                float* __restrict__ lse, int s, int a, int nb) {
     constexpr int TB = Tile<D>::BYTES;
     constexpr int STAGES = 2;
     extern __shared__ uint8_t smraw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sQ = sm;
-    uint8_t* sK = sQ + TB;                   // STAGES
-    uint8_t* sV = sK + STAGES * TB;          // STAGES
+    uint8_t* sQ = sm;                        // [2]
+    uint8_t* sK = sQ + 2 * TB;               // [STAGES]
+    uint8_t* sV = sK + STAGES * TB;          // [STAGES]
     float* sMax = reinterpret_cast<float*>(sV + STAGES * TB);   // [2 iters][2 groups][128]
     float* sSum = sMax + 4 * BR;                                  // [2 groups][128]
     uint64_t* bar = reinterpret_cast<uint64_t*>(sSum + 2 * BR);
-    uint64_t* q_full = bar;
-    uint64_t* kv_full = bar + 1;             // [STAGES]
+    uint64_t* q_full = bar;                  // [2]
+    uint64_t* q_empty = bar + 2;             // [2]
+    uint64_t* kv_full = bar + 4;             // [STAGES]
     uint64_t* kv_empty = kv_full + STAGES;   // [STAGES]
     uint64_t* s_full = kv_empty + STAGES;    // [2] S buffer ready
-    uint64_t* p_full = s_full + 2;           // P_j in TMEM + O corrected (128 arrivals)
-    uint64_t* pv_done = p_full + 1;          // PV_j complete
+    uint64_t* p_full = s_full + 2;           // P_g in TMEM + O corrected (256 arrivals)
+    uint64_t* pv_done = p_full + 1;          // PV_g complete
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nqb = (s + BR - 1) / BR;
-    const int qb = nqb - 1 - blockIdx.x;  // heaviest first
-    const int head = blockIdx.y, b = blockIdx.z;
+    const int T = nqb * a * nb;
     const int h = a * D;
-    const int q0 = qb * BR;
-    const int row0 = b * s;
-    const int nkb = qb + 1;
+    auto decode = [&](int t, int& qb, int& head, int& b) {
+        qb = nqb - 1 - t / (a * nb);
+        const int rem = t % (a * nb);
+        head = rem % a;
+        b = rem / a;
+    };
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tm_qkv);
-        mbar_init(q_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&q_full[i], 1);
+            mbar_init(&q_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+        }
         for (int i = 0; i < STAGES; ++i) {
             mbar_init(&kv_full[i], 1);
             mbar_init(&kv_empty[i], 1);
         }
-        mbar_init(&s_full[0], 1);
-        mbar_init(&s_full[1], 1);
         mbar_init(p_full, 256);
         mbar_init(pv_done, 1);
         fence_mbar_init();
@@ -322,48 +179,80 @@ __global__ void __launch_bounds__(384, 1)
 
     if (warp == 0) {
         if (lane == 0) {
-            mbar_arrive_expect_tx(q_full, TB);
-            tma_tile<D>(sQ, &tm_qkv, q_full, head * D, row0 + q0);
-            for (int j = 0; j < nkb; ++j) {
-                const int st = j % STAGES;
-                mbar_wait(&kv_empty[st], ((j / STAGES) & 1) ^ 1);
-                mbar_arrive_expect_tx(&kv_full[st], 2 * TB);
-                tma_tile<D>(sK + st * TB, &tm_qkv, &kv_full[st], h + head * D, row0 + j * BR);
-                tma_tile<D>(sV + st * TB, &tm_qkv, &kv_full[st], 2 * h + head * D, row0 + j * BR);
+            int g = 0;
+            for (int k = 0;; ++k) {
+                const int t = sched_item(k, T);
+                if (t < 0) break;
+                int qb, head, b;
+                decode(t, qb, head, b);
+                const int sl = k & 1;
+                mbar_wait(&q_empty[sl], ((k >> 1) & 1) ^ 1);
+                mbar_arrive_expect_tx(&q_full[sl], TB);
+                tma_tile<D>(sQ + sl * TB, &tm_qkv, &q_full[sl], head * D, b * s + qb * BR);
+                for (int j = 0; j <= qb; ++j, ++g) {
+                    const int st = g % STAGES;
+                    mbar_wait(&kv_empty[st], ((g / STAGES) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&kv_full[st], 2 * TB);
+                    tma_tile<D>(sK + st * TB, &tm_qkv, &kv_full[st], h + head * D, b * s + j * BR);
+                    tma_tile<D>(sV + st * TB, &tm_qkv, &kv_full[st], 2 * h + head * D, b * s + j * BR);
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
             const uint32_t iS = idesc(BR, false, false);
             const uint32_t iO = idesc(D, false, true);
-            const uint32_t aQ = smem_u32(sQ);
-            mbar_wait(q_full, 0);
-            auto issue_s = [&](int j) {
-                const int st = j % STAGES;
-                mbar_wait(&kv_full[st], (j / STAGES) & 1);
+            // S-issue cursor: item k_s (tiles 0..qb_s), tile j_s, global index gs
+            int k_s = 0, j_s = 0, nkb_s = 0, gs = 0;
+            bool have_s;
+            {
+                const int t = sched_item(0, T);
+                have_s = t >= 0;
+                if (have_s) nkb_s = nqb - t / (a * nb);
+            }
+            auto issue_s = [&]() {
+                const int sl = k_s & 1;
+                if (j_s == 0) mbar_wait(&q_full[sl], (k_s >> 1) & 1);
+                const int st = gs % STAGES;
+                mbar_wait(&kv_full[st], (gs / STAGES) & 1);
                 tc_fence_after();
+                const uint32_t aQ = smem_u32(sQ + sl * TB);
                 const uint32_t aK = smem_u32(sK + st * TB);
-                const uint32_t tS = tmem + (j & 1) * 128;
+                const uint32_t tS = tmem + (gs & 1) * 128;
 #pragma unroll
-                for (int k = 0; k < D / 16; ++k) umma_bf16(tS, desc_k(aQ, k), desc_k(aK, k), iS, k > 0);
-                umma_commit(&s_full[j & 1]);
-            };
-            issue_s(0);
-            for (int j = 0; j < nkb; ++j) {
-                if (j + 1 < nkb) {
-                    if (j >= 1) mbar_wait(pv_done, (j - 1) & 1);  // buffer (j+1)&1 held P_{j-1}
-                    issue_s(j + 1);
+                for (int kk = 0; kk < D / 16; ++kk) umma_bf16(tS, desc_k(aQ, kk), desc_k(aK, kk), iS, kk > 0);
+                umma_commit(&s_full[gs & 1]);
+                if (j_s == nkb_s - 1) umma_commit(&q_empty[sl]);   // Q of this item fully consumed
+                ++gs;
+                if (++j_s == nkb_s) {
+                    j_s = 0;
+                    const int t = sched_item(++k_s, T);
+                    have_s = t >= 0;
+                    if (have_s) nkb_s = nqb - t / (a * nb);
                 }
-                mbar_wait(p_full, j & 1);
-                tc_fence_after();
-                const int st = j % STAGES;
-                const uint32_t aV = smem_u32(sV + st * TB);
-                const uint32_t tP = tmem + (j & 1) * 128;
+            };
+            if (have_s) issue_s();
+            int g = 0;
+            for (int k = 0;; ++k) {
+                const int t = sched_item(k, T);
+                if (t < 0) break;
+                const int nkb = nqb - t / (a * nb);
+                for (int j = 0; j < nkb; ++j, ++g) {
+                    if (have_s) {
+                        if (g >= 1) mbar_wait(pv_done, (g - 1) & 1);   // S buffer (g+1)&1 held P_{g-1}
+                        issue_s();
+                    }
+                    mbar_wait(p_full, g & 1);
+                    tc_fence_after();
+                    const int st = g % STAGES;
+                    const uint32_t aV = smem_u32(sV + st * TB);
+                    const uint32_t tP = tmem + (g & 1) * 128;
 #pragma unroll
-                for (int k = 0; k < BR / 16; ++k)
-                    umma_bf16_ts(tO, tP + k * 8, desc_mn(aV, k), iO, (j | k) > 0);
-                umma_commit(pv_done);
-                umma_commit(&kv_empty[st]);
+                    for (int kk = 0; kk < BR / 16; ++kk)
+                        umma_bf16_ts(tO, tP + kk * 8, desc_mn(aV, kk), iO, (j | kk) > 0);
+                    umma_commit(pv_done);
+                    umma_commit(&kv_empty[st]);
+                }
             }
         }
     } else if (warp >= 4) {
@@ -371,409 +260,88 @@ __global__ void __launch_bounds__(384, 1)
         // group cg owns scores [64cg, 64cg+64) and O columns [cg D/2, (cg+1) D/2)
         const int et = threadIdx.x - 128;
         const int r = et & 127, cg = et >> 7;
-        const int q = q0 + r;
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
         const float sc = rsqrtf((float)D) * LOG2E;
-        float m = -INFINITY, l = 0.f;
-        for (int j = 0; j < nkb; ++j) {
-            const uint32_t tS = tmem + (j & 1) * 128 + lane_off;
-            mbar_wait(&s_full[j & 1], (j >> 1) & 1);
-            tc_fence_after();
-            float sv[64];
-            {
-                uint32_t rr[32];
-                tmem_ld32(tS + cg * 64, rr);
+        int g = 0;
+        for (int k = 0;; ++k) {
+            const int t = sched_item(k, T);
+            if (t < 0) break;
+            int qb, head, b;
+            decode(t, qb, head, b);
+            const int nkb = qb + 1;
+            const int q = qb * BR + r;
+            float m = -INFINITY, l = 0.f;
+            for (int j = 0; j < nkb; ++j, ++g) {
+                const uint32_t tS = tmem + (g & 1) * 128 + lane_off;
+                mbar_wait(&s_full[g & 1], (g >> 1) & 1);
+                tc_fence_after();
+                float sv[64];
+                {
+                    uint32_t rr[32];
+                    tmem_ld32(tS + cg * 64, rr);
 #pragma unroll
-                for (int e = 0; e < 32; ++e) sv[e] = __uint_as_float(rr[e]);
-                tmem_ld32(tS + cg * 64 + 32, rr);
-                tmem_wait_ld();
+                    for (int e = 0; e < 32; ++e) sv[e] = __uint_as_float(rr[e]);
+                    tmem_ld32(tS + cg * 64 + 32, rr);
+                    tmem_wait_ld();
 #pragma unroll
-                for (int e = 0; e < 32; ++e) sv[32 + e] = __uint_as_float(rr[e]);
+                    for (int e = 0; e < 32; ++e) sv[32 + e] = __uint_as_float(rr[e]);
+                }
+                const bool diag = (j == nkb - 1);
+                float lmx = -INFINITY;
+#pragma unroll
+                for (int e = 0; e < 64; ++e) {
+                    const float x = (diag && j * BR + cg * 64 + e > q) ? -INFINITY : sv[e] * sc;
+                    sv[e] = x;
+                    lmx = fmaxf(lmx, x);
+                }
+                float* mb = sMax + (g & 1) * 2 * BR;
+                mb[cg * BR + r] = lmx;
+                named_bar_sync(1, 256);
+                const float mx = fmaxf(m, fmaxf(lmx, mb[(cg ^ 1) * BR + r]));
+                float rs = 0.f;
+                uint32_t pk[32];
+#pragma unroll
+                for (int e = 0; e < 64; e += 2) {
+                    const float p0 = exp2f(sv[e] - mx), p1 = exp2f(sv[e + 1] - mx);
+                    rs += p0 + p1;
+                    __nv_bfloat162 v2 = __floats2bfloat162_rn(p0, p1);
+                    pk[e / 2] = *reinterpret_cast<uint32_t*>(&v2);
+                }
+                const float corr = exp2f(m - mx);
+                l = l * corr + rs;        // partial (this group's columns), same m history
+                m = mx;
+                tmem_st32(tS + cg * 32, pk);   // P_g over S_g: packed cols [32cg, 32cg+32)
+                if (j > 0) {
+                    mbar_wait(pv_done, (g - 1) & 1);
+                    tc_fence_after();
+                    if (__any_sync(0xffffffffu, corr != 1.0f)) {
+#pragma unroll
+                        for (int c = cg * (D / 64); c < (cg + 1) * (D / 64); ++c) {
+                            uint32_t ov[32];
+                            tmem_ld32(tO + lane_off + c * 32, ov);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * corr);
+                            tmem_st32(tO + lane_off + c * 32, ov);
+                        }
+                    }
+                }
+                tmem_wait_st();
+                tc_fence_before();
+                mbar_arrive(p_full);
             }
-            const bool diag = (j == nkb - 1);
-            float lmx = -INFINITY;
-#pragma unroll
-            for (int e = 0; e < 64; ++e) {
-                const float x = (diag && j * BR + cg * 64 + e > q) ? -INFINITY : sv[e] * sc;
-                sv[e] = x;
-                lmx = fmaxf(lmx, x);
-            }
-            float* mb = sMax + (j & 1) * 2 * BR;
-            mb[cg * BR + r] = lmx;
+            sSum[cg * BR + r] = l;
             named_bar_sync(1, 256);
-            const float mx = fmaxf(m, fmaxf(lmx, mb[(cg ^ 1) * BR + r]));
-            float rs = 0.f;
-            uint32_t pk[32];
-#pragma unroll
-            for (int e = 0; e < 64; e += 2) {
-                const float p0 = exp2f(sv[e] - mx), p1 = exp2f(sv[e + 1] - mx);
-                rs += p0 + p1;
-                __nv_bfloat162 v2 = __floats2bfloat162_rn(p0, p1);
-                pk[e / 2] = *reinterpret_cast<uint32_t*>(&v2);
-            }
-            const float corr = exp2f(m - mx);
-            l = l * corr + rs;        // partial (this group's columns), same m history
-            m = mx;
-            tmem_st32(tS + cg * 32, pk);   // P_j over S_j: packed cols [32cg, 32cg+32)
-            if (j > 0) {
-                mbar_wait(pv_done, (j - 1) & 1);
-                tc_fence_after();
-                if (__any_sync(0xffffffffu, corr != 1.0f)) {
-#pragma unroll
-                    for (int c = cg * (D / 64); c < (cg + 1) * (D / 64); ++c) {
-                        uint32_t ov[32];
-                        tmem_ld32(tO + lane_off + c * 32, ov);
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * corr);
-                        tmem_st32(tO + lane_off + c * 32, ov);
-                    }
-                }
-            }
-            tmem_wait_st();
-            tc_fence_before();
-            mbar_arrive(p_full);
-        }
-        sSum[cg * BR + r] = l;
-        named_bar_sync(1, 256);
-        l += sSum[(cg ^ 1) * BR + r];
-        mbar_wait(pv_done, (nkb - 1) & 1);
-        tc_fence_after();
-        // tcgen05.ld is .sync.aligned: every lane loads; only valid rows store
-        const float inv = 1.0f / l;
-        bf16* orow = o + ((long)b * s + q) * h + head * D;
-#pragma unroll
-        for (int c = cg * (D / 64); c < (cg + 1) * (D / 64); ++c) {
-            float v[32];
-            tmem_ld32f(tO + lane_off + c * 32, v);
-            if (q < s) {
-#pragma unroll
-                for (int q8 = 0; q8 < 4; ++q8) {
-                    uint4 u;
-                    __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-                    for (int jj = 0; jj < 4; ++jj)
-                        hh[jj] = __floats2bfloat162_rn(v[q8 * 8 + 2 * jj] * inv, v[q8 * 8 + 2 * jj + 1] * inv);
-                    *reinterpret_cast<uint4*>(orow + c * 32 + q8 * 8) = u;
-                }
-            }
-        }
-        if (q < s && cg == 0) lse[((long)b * a + head) * s + q] = (m + log2f(l)) / LOG2E;
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 2) {
-        tc_fence_after();
-        tmem_dealloc(tmem, 512);
-    }
-}
-
-// ============================================================== backward dK, dV
-template <int D>
-__global__ void __launch_bounds__(256, 1)
-    dkdv_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-                const float* __restrict__ lse, const float* __restrict__ Dv,
-                bf16* __restrict__ dqkv, int s, int a) {
-    constexpr int TB = Tile<D>::BYTES;
-    extern __shared__ uint8_t smraw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sK = sm;
-    uint8_t* sV = sK + TB;
-    uint8_t* sQ = sV + TB;            // per query block
-    uint8_t* sO = sQ + TB;            // dO
-    uint8_t* sP = sO + TB;            // P^T  [keys][queries] (2 atoms)
-    uint8_t* sS = sP + 2 * BR * 128;  // dS^T
-    float* sL = reinterpret_cast<float*>(sS + 2 * BR * 128);   // LSE*log2e of the q block
-    float* sD = sL + BR;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sD + BR);
-    uint64_t* kv_full = bar;
-    uint64_t* q_full = bar + 1;
-    uint64_t* s_full = bar + 2;       // S^T, dP^T ready
-    uint64_t* p_full = bar + 3;       // P^T, dS^T written (128 arrivals)
-    uint64_t* g_done = bar + 4;       // dV/dK MMAs of this block done (frees Q, dO, P, dS, S)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 5);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nqb = (s + BR - 1) / BR;
-    const int kb = blockIdx.x;
-    const int head = blockIdx.y, b = blockIdx.z;
-    const int h = a * D;
-    const int k0 = kb * BR;
-    const int row0 = b * s;
-    const float* lseb = lse + ((long)b * a + head) * s;
-    const float* Db = Dv + ((long)b * a + head) * s;
-
-    if (warp == 0 && lane == 0) {
-        tma_prefetch_desc(&tm_qkv);
-        tma_prefetch_desc(&tm_do);
-        mbar_init(kv_full, 1);
-        mbar_init(q_full, 1);
-        mbar_init(s_full, 1);
-        mbar_init(p_full, 128);
-        mbar_init(g_done, 1);
-        fence_mbar_init();
-    }
-    if (warp == 2) tmem_alloc(tmem_slot, 512);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    const uint32_t tS = tmem, tP = tmem + 128, tdV = tmem + 256, tdK = tmem + 256 + D;
-
-    if (warp == 0) {
-        if (lane == 0) {
-            mbar_arrive_expect_tx(kv_full, 2 * TB);
-            tma_tile<D>(sK, &tm_qkv, kv_full, h + head * D, row0 + k0);
-            tma_tile<D>(sV, &tm_qkv, kv_full, 2 * h + head * D, row0 + k0);
-            for (int qb = kb, it = 0; qb < nqb; ++qb, ++it) {
-                if (it > 0) mbar_wait(g_done, (it - 1) & 1);
-                mbar_arrive_expect_tx(q_full, 2 * TB);
-                tma_tile<D>(sQ, &tm_qkv, q_full, head * D, row0 + qb * BR);
-                tma_tile<D>(sO, &tm_do, q_full, head * D, row0 + qb * BR);
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            const uint32_t iS = idesc(BR, false, false);
-            const uint32_t iG = idesc(D, false, true);
-            const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aQ = smem_u32(sQ),
-                           aO = smem_u32(sO), aP = smem_u32(sP), aS = smem_u32(sS);
-            mbar_wait(kv_full, 0);
-            for (int qb = kb, it = 0; qb < nqb; ++qb, ++it) {
-                mbar_wait(q_full, it & 1);
-                tc_fence_after();
-#pragma unroll
-                for (int k = 0; k < D / 16; ++k) {
-                    umma_bf16(tS, desc_k(aK, k), desc_k(aQ, k), iS, k > 0);   // S^T = K Q^T
-                    umma_bf16(tP, desc_k(aV, k), desc_k(aO, k), iS, k > 0);   // dP^T = V dO^T
-                }
-                umma_commit(s_full);
-                mbar_wait(p_full, it & 1);
-                tc_fence_after();
-#pragma unroll
-                for (int k = 0; k < BR / 16; ++k) {
-                    umma_bf16(tdV, desc_k(aP, k), desc_mn(aO, k), iG, (it | k) > 0);  // dV += P^T dO
-                    umma_bf16(tdK, desc_k(aS, k), desc_mn(aQ, k), iG, (it | k) > 0);  // dK += dS^T Q
-                }
-                umma_commit(g_done);
-            }
-        }
-    } else if (warp >= 4) {
-        const int r = threadIdx.x - 128;          // key row == TMEM lane
-        const int key = k0 + r;
-        const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
-        const float sc = rsqrtf((float)D) * LOG2E;
-        for (int qb = kb, it = 0; qb < nqb; ++qb, ++it) {
-            const int q0 = qb * BR;
-            // L, D of the query block -> smem (previous block's readers are done:
-            // they arrived on p_full, and the MMA reading sP/sS has completed
-            // before s_full of this block was committed)
-            if (it > 0) mbar_wait(g_done, (it - 1) & 1);
-            {
-                const int qq = q0 + r;
-                sL[r] = qq < s ? lseb[qq] * LOG2E : 0.f;
-                sD[r] = qq < s ? Db[qq] : 0.f;
-            }
-            named_bar_sync(1, 128);
-            mbar_wait(s_full, it & 1);
+            l += sSum[(cg ^ 1) * BR + r];
+            mbar_wait(pv_done, (g - 1) & 1);
             tc_fence_after();
+            // tcgen05.ld is .sync.aligned: every lane loads; only valid rows store
+            const float inv = 1.0f / l;
+            bf16* orow = o + ((long)b * s + q) * h + head * D;
 #pragma unroll
-            for (int c = 0; c < BR / 32; ++c) {
-                float sv[32], pv[32];
-                tmem_ld32f(tS + lane_off + c * 32, sv);
-                tmem_ld32f(tP + lane_off + c * 32, pv);
-#pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    const int ql = c * 32 + e, qq = q0 + ql;
-                    const float p = (qq >= key && qq < s) ? exp2f(sv[e] * sc - sL[ql]) : 0.f;
-                    sv[e] = p;
-                    pv[e] = p * (pv[e] - sD[ql]);
-                }
-                st_row32(sP, r, c * 32, sv);
-                st_row32(sS, r, c * 32, pv);
-            }
-            fence_async_smem();
-            tc_fence_before();
-            mbar_arrive(p_full);
-        }
-        // epilogue: dK (scaled), dV
-        mbar_wait(g_done, (nqb - kb - 1) & 1);
-        tc_fence_after();
-        {   // every lane loads (tcgen05.ld is .sync.aligned); only valid keys store
-            const float scale = rsqrtf((float)D);
-            bf16* dkr = dqkv + ((long)b * s + key) * (3L * h) + h + head * D;
-            bf16* dvr = dkr + h;
-#pragma unroll
-            for (int c = 0; c < D / 32; ++c) {
+            for (int c = cg * (D / 64); c < (cg + 1) * (D / 64); ++c) {
                 float v[32];
-                tmem_ld32f(tdK + lane_off + c * 32, v);
-                if (key < s) {
-#pragma unroll
-                    for (int q8 = 0; q8 < 4; ++q8) {
-                        uint4 u;
-                        __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-                        for (int jj = 0; jj < 4; ++jj)
-                            hh[jj] = __floats2bfloat162_rn(v[q8 * 8 + 2 * jj] * scale, v[q8 * 8 + 2 * jj + 1] * scale);
-                        *reinterpret_cast<uint4*>(dkr + c * 32 + q8 * 8) = u;
-                    }
-                }
-                tmem_ld32f(tdV + lane_off + c * 32, v);
-                if (key < s) {
-#pragma unroll
-                    for (int q8 = 0; q8 < 4; ++q8) {
-                        uint4 u;
-                        __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-                        for (int jj = 0; jj < 4; ++jj)
-                            hh[jj] = __floats2bfloat162_rn(v[q8 * 8 + 2 * jj], v[q8 * 8 + 2 * jj + 1]);
-                        *reinterpret_cast<uint4*>(dvr + c * 32 + q8 * 8) = u;
-                    }
-                }
-            }
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 2) {
-        tc_fence_after();
-        tmem_dealloc(tmem, 512);
-    }
-}
-
-// ============================================================== backward dQ
-template <int D>
-__global__ void __launch_bounds__(256, 1)
-    dq_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-              const float* __restrict__ lse, const float* __restrict__ Dv, bf16* __restrict__ dqkv,
-              int s, int a) {
-    constexpr int TB = Tile<D>::BYTES;
-    constexpr int STAGES = 2;
-    extern __shared__ uint8_t smraw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sQ = sm;
-    uint8_t* sO = sQ + TB;                  // dO
-    uint8_t* sK = sO + TB;                  // STAGES
-    uint8_t* sV = sK + STAGES * TB;         // STAGES
-    uint8_t* sS = sV + STAGES * TB;         // dS [queries][keys] (2 atoms)
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sS + 2 * BR * 128);
-    uint64_t* q_full = bar;
-    uint64_t* kv_full = bar + 1;            // [STAGES]
-    uint64_t* kv_empty = kv_full + STAGES;  // [STAGES]
-    uint64_t* s_full = kv_empty + STAGES;
-    uint64_t* p_full = s_full + 1;
-    uint64_t* g_done = p_full + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(g_done + 1);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nqb = (s + BR - 1) / BR;
-    const int qb = nqb - 1 - blockIdx.x;
-    const int head = blockIdx.y, b = blockIdx.z;
-    const int h = a * D;
-    const int q0 = qb * BR;
-    const int row0 = b * s;
-    const int nkb = qb + 1;
-
-    if (warp == 0 && lane == 0) {
-        tma_prefetch_desc(&tm_qkv);
-        tma_prefetch_desc(&tm_do);
-        mbar_init(q_full, 1);
-        for (int i = 0; i < STAGES; ++i) {
-            mbar_init(&kv_full[i], 1);
-            mbar_init(&kv_empty[i], 1);
-        }
-        mbar_init(s_full, 1);
-        mbar_init(p_full, 128);
-        mbar_init(g_done, 1);
-        fence_mbar_init();
-    }
-    if (warp == 2) tmem_alloc(tmem_slot, 512);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    const uint32_t tS = tmem, tP = tmem + 128, tdQ = tmem + 256;
-
-    if (warp == 0) {
-        if (lane == 0) {
-            mbar_arrive_expect_tx(q_full, 2 * TB);
-            tma_tile<D>(sQ, &tm_qkv, q_full, head * D, row0 + q0);
-            tma_tile<D>(sO, &tm_do, q_full, head * D, row0 + q0);
-            for (int j = 0; j < nkb; ++j) {
-                const int st = j % STAGES;
-                mbar_wait(&kv_empty[st], ((j / STAGES) & 1) ^ 1);
-                mbar_arrive_expect_tx(&kv_full[st], 2 * TB);
-                tma_tile<D>(sK + st * TB, &tm_qkv, &kv_full[st], h + head * D, row0 + j * BR);
-                tma_tile<D>(sV + st * TB, &tm_qkv, &kv_full[st], 2 * h + head * D, row0 + j * BR);
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            const uint32_t iS = idesc(BR, false, false);
-            const uint32_t iG = idesc(D, false, true);
-            const uint32_t aQ = smem_u32(sQ), aO = smem_u32(sO), aS = smem_u32(sS);
-            mbar_wait(q_full, 0);
-            for (int j = 0; j < nkb; ++j) {
-                const int st = j % STAGES;
-                mbar_wait(&kv_full[st], (j / STAGES) & 1);
-                if (j > 0) mbar_wait(g_done, (j - 1) & 1);
-                tc_fence_after();
-                const uint32_t aK = smem_u32(sK + st * TB), aV = smem_u32(sV + st * TB);
-#pragma unroll
-                for (int k = 0; k < D / 16; ++k) {
-                    umma_bf16(tS, desc_k(aQ, k), desc_k(aK, k), iS, k > 0);   // S = Q K^T
-                    umma_bf16(tP, desc_k(aO, k), desc_k(aV, k), iS, k > 0);   // dP = dO V^T
-                }
-                umma_commit(s_full);
-                mbar_wait(p_full, j & 1);
-                tc_fence_after();
-#pragma unroll
-                for (int k = 0; k < BR / 16; ++k)
-                    umma_bf16(tdQ, desc_k(aS, k), desc_mn(aK, k), iG, (j | k) > 0);   // dQ += dS K
-                umma_commit(g_done);
-                umma_commit(&kv_empty[st]);
-            }
-        }
-    } else if (warp >= 4) {
-        const int r = threadIdx.x - 128;
-        const int q = q0 + r;
-        const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
-        const float sc = rsqrtf((float)D) * LOG2E;
-        const float* lseb = lse + ((long)b * a + head) * s;
-        const float* Db = Dv + ((long)b * a + head) * s;
-        const float L = q < s ? lseb[q] * LOG2E : 0.f;
-        const float Dq = q < s ? Db[q] : 0.f;
-        for (int j = 0; j < nkb; ++j) {
-            mbar_wait(s_full, j & 1);
-            tc_fence_after();
-#pragma unroll
-            for (int c = 0; c < BR / 32; ++c) {
-                float sv[32], pv[32];
-                tmem_ld32f(tS + lane_off + c * 32, sv);
-                tmem_ld32f(tP + lane_off + c * 32, pv);
-#pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    const int key = j * BR + c * 32 + e;
-                    const float p = (key <= q) ? exp2f(sv[e] * sc - L) : 0.f;
-                    pv[e] = p * (pv[e] - Dq);
-                }
-                st_row32(sS, r, c * 32, pv);
-            }
-            fence_async_smem();
-            tc_fence_before();
-            mbar_arrive(p_full);
-            // dS smem is re-written next iteration only after g_done (the MMA that
-            // reads it) — wait for it before touching sS again
-            mbar_wait(g_done, j & 1);
-        }
-        tc_fence_after();
-        {   // every lane loads (tcgen05.ld is .sync.aligned); only valid rows store
-            const float scale = rsqrtf((float)D);
-            bf16* dqr = dqkv + ((long)b * s + q) * (3L * h) + head * D;
-#pragma unroll
-            for (int c = 0; c < D / 32; ++c) {
-                float v[32];
-                tmem_ld32f(tdQ + lane_off + c * 32, v);
+                tmem_ld32f(tO + lane_off + c * 32, v);
                 if (q < s) {
 #pragma unroll
                     for (int q8 = 0; q8 < 4; ++q8) {
@@ -781,11 +349,14 @@ __global__ void __launch_bounds__(256, 1)
                         __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
                         for (int jj = 0; jj < 4; ++jj)
-                            hh[jj] = __floats2bfloat162_rn(v[q8 * 8 + 2 * jj] * scale, v[q8 * 8 + 2 * jj + 1] * scale);
-                        *reinterpret_cast<uint4*>(dqr + c * 32 + q8 * 8) = u;
+                            hh[jj] = __floats2bfloat162_rn(v[q8 * 8 + 2 * jj] * inv, v[q8 * 8 + 2 * jj + 1] * inv);
+                        *reinterpret_cast<uint4*>(orow + c * 32 + q8 * 8) = u;
                     }
                 }
             }
+            if (q < s && cg == 0) lse[((long)b * a + head) * s + q] = (m + log2f(l)) / LOG2E;
+            // the next item's sSum write is ordered after the other group's read
+            // above by the named barrier of its first tile
         }
     }
     tc_fence_before();
@@ -825,12 +396,16 @@ __device__ __forceinline__ void st_row32_h(uint8_t* tile, int r, int col0, const
     }
 }
 
-// dK/dV: CTA owns 128 keys; loops over 64-query halves from the diagonal.
+// dK/dV (persistent): an item is 128 keys of one (sequence, head); it loops
+// over 64-query halves from the diagonal. Item t (heaviest first):
+// kb = t/(a*nb), head = t%a, batch = (t/a)%nb. Half rings (Q/dO halves, S/dP
+// TMEM buffers, P/dS smem) run on a global half counter across items; K/V are
+// single-buffered per item and released after the item's last S MMA.
 template <int D>
 __global__ void __launch_bounds__(384, 1)
     dkdv2_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_qkv64,
                  const __grid_constant__ CUtensorMap tm_do64, const float* __restrict__ lse,
-                 const float* __restrict__ Dv, bf16* __restrict__ dqkv, int s, int a) {
+                 const float* __restrict__ Dv, bf16* __restrict__ dqkv, int s, int a, int nb) {
     constexpr int TB = Tile<D>::BYTES;          // 128-row tile
     constexpr int HB = (D / 64) * HR * 128;      // 64-row tile
     extern __shared__ uint8_t smraw[];
@@ -845,29 +420,33 @@ __global__ void __launch_bounds__(384, 1)
     float* sD = sL + 2 * HR;                                   // [2][64]
     uint64_t* bar = reinterpret_cast<uint64_t*>(sD + 2 * HR);
     uint64_t* kv_full = bar;
-    uint64_t* q_full = bar + 1;     // [2]
-    uint64_t* q_empty = bar + 3;    // [2]
-    uint64_t* s_full = bar + 5;     // [2]
-    uint64_t* p_full = bar + 7;     // 128 arrivals per half
-    uint64_t* g_done = bar + 8;     // [2] dV/dK MMAs of a half complete
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
+    uint64_t* kv_empty = bar + 1;
+    uint64_t* q_full = bar + 2;     // [2]
+    uint64_t* q_empty = bar + 4;    // [2]
+    uint64_t* s_full = bar + 6;     // [2]
+    uint64_t* p_full = bar + 8;     // 256 arrivals per half
+    uint64_t* g_done = bar + 9;     // [2] dV/dK MMAs of a half complete
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 11);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int kb = blockIdx.x;
-    const int head = blockIdx.y, b = blockIdx.z;
+    const int nkb = (s + BR - 1) / BR;
+    const int nq64 = (s + HR - 1) / HR;
+    const int T = nkb * a * nb;
     const int h = a * D;
-    const int k0 = kb * BR;
-    const int row0 = b * s;
-    const int hq0 = k0 / HR;                   // first 64-query half at the diagonal
-    const int nh = (s + HR - 1) / HR - hq0;    // halves to process
-    const float* lseb = lse + ((long)b * a + head) * s;
-    const float* Db = Dv + ((long)b * a + head) * s;
+    auto decode = [&](int t, int& kb, int& head, int& b) {
+        kb = t / (a * nb);
+        const int rem = t % (a * nb);
+        head = rem % a;
+        b = rem / a;
+    };
+    auto halves = [&](int t) { return nq64 - 2 * (t / (a * nb)); };
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tm_qkv);
         tma_prefetch_desc(&tm_qkv64);
         tma_prefetch_desc(&tm_do64);
         mbar_init(kv_full, 1);
+        mbar_init(kv_empty, 1);
         for (int i = 0; i < 2; ++i) {
             mbar_init(&q_full[i], 1);
             mbar_init(&q_empty[i], 1);
@@ -886,16 +465,26 @@ __global__ void __launch_bounds__(384, 1)
 
     if (warp == 0) {
         if (lane == 0) {
-            mbar_arrive_expect_tx(kv_full, 2 * TB);
-            tma_tile<D>(sK, &tm_qkv, kv_full, h + head * D, row0 + k0);
-            tma_tile<D>(sV, &tm_qkv, kv_full, 2 * h + head * D, row0 + k0);
-            for (int hh = 0; hh < nh; ++hh) {
-                const int sl = hh & 1;
-                mbar_wait(&q_empty[sl], ((hh >> 1) & 1) ^ 1);
-                mbar_arrive_expect_tx(&q_full[sl], 2 * HB);
-                const int qrow = row0 + (hq0 + hh) * HR;
-                tma_half<D>(sQ + sl * HB, &tm_qkv64, &q_full[sl], head * D, qrow);
-                tma_half<D>(sO + sl * HB, &tm_do64, &q_full[sl], head * D, qrow);
+            int g = 0;
+            for (int k = 0;; ++k) {
+                const int t = sched_item(k, T);
+                if (t < 0) break;
+                int kb, head, b;
+                decode(t, kb, head, b);
+                const int row0 = b * s;
+                mbar_wait(kv_empty, (k & 1) ^ 1);
+                mbar_arrive_expect_tx(kv_full, 2 * TB);
+                tma_tile<D>(sK, &tm_qkv, kv_full, h + head * D, row0 + kb * BR);
+                tma_tile<D>(sV, &tm_qkv, kv_full, 2 * h + head * D, row0 + kb * BR);
+                const int nh = halves(t);
+                for (int hh = 0; hh < nh; ++hh, ++g) {
+                    const int sl = g & 1;
+                    mbar_wait(&q_empty[sl], ((g >> 1) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&q_full[sl], 2 * HB);
+                    const int qrow = row0 + (2 * kb + hh) * HR;
+                    tma_half<D>(sQ + sl * HB, &tm_qkv64, &q_full[sl], head * D, qrow);
+                    tma_half<D>(sO + sl * HB, &tm_do64, &q_full[sl], head * D, qrow);
+                }
             }
         }
     } else if (warp == 1) {
@@ -903,35 +492,56 @@ __global__ void __launch_bounds__(384, 1)
             const uint32_t iS = idesc(HR, false, false);   // M=128 keys, N=64 queries
             const uint32_t iG = idesc(D, false, true);
             const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
-            mbar_wait(kv_full, 0);
-            auto issue_s = [&](int hh) {
-                const int sl = hh & 1;
-                mbar_wait(&q_full[sl], (hh >> 1) & 1);
+            int k_s = 0, h_s = 0, nh_s = 0, gs = 0;
+            bool have_s;
+            {
+                const int t = sched_item(0, T);
+                have_s = t >= 0;
+                if (have_s) nh_s = halves(t);
+            }
+            auto issue_s = [&]() {
+                const int sl = gs & 1;
+                if (h_s == 0) mbar_wait(kv_full, k_s & 1);
+                mbar_wait(&q_full[sl], (gs >> 1) & 1);
                 tc_fence_after();
                 const uint32_t aQ = smem_u32(sQ + sl * HB), aO = smem_u32(sO + sl * HB);
                 const uint32_t tS = tmem + sl * 128, tP = tS + 64;
 #pragma unroll
-                for (int k = 0; k < D / 16; ++k) {
-                    umma_bf16(tS, desc_k(aK, k), desc_k_h(aQ, k), iS, k > 0);   // S^T = K Q^T
-                    umma_bf16(tP, desc_k(aV, k), desc_k_h(aO, k), iS, k > 0);   // dP^T = V dO^T
+                for (int kk = 0; kk < D / 16; ++kk) {
+                    umma_bf16(tS, desc_k(aK, kk), desc_k_h(aQ, kk), iS, kk > 0);   // S^T = K Q^T
+                    umma_bf16(tP, desc_k(aV, kk), desc_k_h(aO, kk), iS, kk > 0);   // dP^T = V dO^T
                 }
                 umma_commit(&s_full[sl]);
-            };
-            issue_s(0);
-            for (int hh = 0; hh < nh; ++hh) {
-                const int sl = hh & 1;
-                if (hh + 1 < nh) issue_s(hh + 1);   // TMEM buffer (hh+1)&1 freed by p_full(hh-1)
-                mbar_wait(p_full, hh & 1);
-                tc_fence_after();
-                const uint32_t aQ = smem_u32(sQ + sl * HB), aO = smem_u32(sO + sl * HB);
-                const uint32_t aP = smem_u32(sP + sl * BR * 128), aS = smem_u32(sS + sl * BR * 128);
-#pragma unroll
-                for (int k = 0; k < HR / 16; ++k) {
-                    umma_bf16(tdV, desc_k(aP, k), desc_mn_h(aO, k), iG, (hh | k) > 0);  // dV += P^T dO
-                    umma_bf16(tdK, desc_k(aS, k), desc_mn_h(aQ, k), iG, (hh | k) > 0);  // dK += dS^T Q
+                if (h_s == nh_s - 1) umma_commit(kv_empty);   // K, V of this item consumed
+                ++gs;
+                if (++h_s == nh_s) {
+                    h_s = 0;
+                    const int t = sched_item(++k_s, T);
+                    have_s = t >= 0;
+                    if (have_s) nh_s = halves(t);
                 }
-                umma_commit(&g_done[sl]);
-                umma_commit(&q_empty[sl]);
+            };
+            if (have_s) issue_s();
+            int g = 0;
+            for (int k = 0;; ++k) {
+                const int t = sched_item(k, T);
+                if (t < 0) break;
+                const int nh = halves(t);
+                for (int hh = 0; hh < nh; ++hh, ++g) {
+                    const int sl = g & 1;
+                    if (have_s) issue_s();   // TMEM buffer (g+1)&1 freed by p_full(g-1)
+                    mbar_wait(p_full, g & 1);
+                    tc_fence_after();
+                    const uint32_t aQ = smem_u32(sQ + sl * HB), aO = smem_u32(sO + sl * HB);
+                    const uint32_t aP = smem_u32(sP + sl * BR * 128), aS = smem_u32(sS + sl * BR * 128);
+#pragma unroll
+                    for (int kk = 0; kk < HR / 16; ++kk) {
+                        umma_bf16(tdV, desc_k(aP, kk), desc_mn_h(aO, kk), iG, (hh | kk) > 0);  // dV += P^T dO
+                        umma_bf16(tdK, desc_k(aS, kk), desc_mn_h(aQ, kk), iG, (hh | kk) > 0);  // dK += dS^T Q
+                    }
+                    umma_commit(&g_done[sl]);
+                    umma_commit(&q_empty[sl]);
+                }
             }
         }
     } else if (warp >= 4) {
@@ -939,76 +549,86 @@ __global__ void __launch_bounds__(384, 1)
         // column group cg = which 32 of the 64 half-columns this thread owns
         const int et = threadIdx.x - 128;
         const int r = et & 127, cg = et >> 7;
-        const int key = k0 + r;
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
         const float sc = rsqrtf((float)D) * LOG2E;
-        for (int hh = 0; hh < nh; ++hh) {
-            const int sl = hh & 1;
-            const int q0 = (hq0 + hh) * HR;
-            // P/dS buffer and L/D slot `sl` were last read by the MMA of half hh-2
-            if (hh >= 2) mbar_wait(&g_done[sl], ((hh - 2) >> 1) & 1);
-            if (et < HR) {
-                const int qq = q0 + et;
-                sL[sl * HR + et] = qq < s ? lseb[qq] * LOG2E : 0.f;
-                sD[sl * HR + et] = qq < s ? Db[qq] : 0.f;
-            }
-            named_bar_sync(1, 256);
-            mbar_wait(&s_full[sl], (hh >> 1) & 1);
-            tc_fence_after();
-            const uint32_t tS = tmem + sl * 128 + lane_off, tP = tS + 64;
-            uint8_t* P = sP + sl * BR * 128;
-            uint8_t* Sd = sS + sl * BR * 128;
-            const float* L = sL + sl * HR;
-            const float* Dq = sD + sl * HR;
-            {
-                const int c = cg;
-                float sv[32], pv[32];
-                tmem_ld32f(tS + c * 32, sv);
-                tmem_ld32f(tP + c * 32, pv);
-#pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    const int ql = c * 32 + e, qq = q0 + ql;
-                    const float p = (qq >= key && qq < s) ? exp2f(sv[e] * sc - L[ql]) : 0.f;
-                    sv[e] = p;
-                    pv[e] = p * (pv[e] - Dq[ql]);
-                }
-                st_row32_h(P, r, c * 32, sv);
-                st_row32_h(Sd, r, c * 32, pv);
-            }
-            fence_async_smem();
-            tc_fence_before();
-            mbar_arrive(p_full);
-        }
-        mbar_wait(&g_done[(nh - 1) & 1], ((nh - 1) >> 1) & 1);
-        tc_fence_after();
         const float scale = rsqrtf((float)D);
-        bf16* dkr = dqkv + ((long)b * s + key) * (3L * h) + h + head * D;
-        bf16* dvr = dkr + h;
-#pragma unroll
-        for (int c = cg * (D / 64); c < (cg + 1) * (D / 64); ++c) {
-            float v[32];
-            tmem_ld32f(tdK + lane_off + c * 32, v);
-            if (key < s) {
-#pragma unroll
-                for (int q8 = 0; q8 < 4; ++q8) {
-                    uint4 u;
-                    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-                    for (int jj = 0; jj < 4; ++jj)
-                        h2[jj] = __floats2bfloat162_rn(v[q8 * 8 + 2 * jj] * scale, v[q8 * 8 + 2 * jj + 1] * scale);
-                    *reinterpret_cast<uint4*>(dkr + c * 32 + q8 * 8) = u;
+        int g = 0;
+        for (int k = 0;; ++k) {
+            const int t = sched_item(k, T);
+            if (t < 0) break;
+            int kb, head, b;
+            decode(t, kb, head, b);
+            const int nh = halves(t);
+            const int key = kb * BR + r;
+            const float* lseb = lse + ((long)b * a + head) * s;
+            const float* Db = Dv + ((long)b * a + head) * s;
+            for (int hh = 0; hh < nh; ++hh, ++g) {
+                const int sl = g & 1;
+                const int q0 = (2 * kb + hh) * HR;
+                // P/dS buffer `sl` was last read by the MMAs of half g-2
+                if (g >= 2) mbar_wait(&g_done[sl], ((g - 2) >> 1) & 1);
+                if (et < HR) {
+                    const int qq = q0 + et;
+                    sL[sl * HR + et] = qq < s ? lseb[qq] * LOG2E : 0.f;
+                    sD[sl * HR + et] = qq < s ? Db[qq] : 0.f;
                 }
+                named_bar_sync(1, 256);
+                mbar_wait(&s_full[sl], (g >> 1) & 1);
+                tc_fence_after();
+                const uint32_t tS = tmem + sl * 128 + lane_off, tP = tS + 64;
+                uint8_t* P = sP + sl * BR * 128;
+                uint8_t* Sd = sS + sl * BR * 128;
+                const float* L = sL + sl * HR;
+                const float* Dq = sD + sl * HR;
+                {
+                    const int c = cg;
+                    float sv[32], pv[32];
+                    tmem_ld32f(tS + c * 32, sv);
+                    tmem_ld32f(tP + c * 32, pv);
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        const int ql = c * 32 + e, qq = q0 + ql;
+                        const float p = (qq >= key && qq < s) ? exp2f(sv[e] * sc - L[ql]) : 0.f;
+                        sv[e] = p;
+                        pv[e] = p * (pv[e] - Dq[ql]);
+                    }
+                    st_row32_h(P, r, c * 32, sv);
+                    st_row32_h(Sd, r, c * 32, pv);
+                }
+                fence_async_smem();
+                tc_fence_before();
+                mbar_arrive(p_full);
             }
-            tmem_ld32f(tdV + lane_off + c * 32, v);
-            if (key < s) {
+            mbar_wait(&g_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
+            tc_fence_after();
+            bf16* dkr = dqkv + ((long)b * s + key) * (3L * h) + h + head * D;
+            bf16* dvr = dkr + h;
 #pragma unroll
-                for (int q8 = 0; q8 < 4; ++q8) {
-                    uint4 u;
-                    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+            for (int c = cg * (D / 64); c < (cg + 1) * (D / 64); ++c) {
+                float v[32];
+                tmem_ld32f(tdK + lane_off + c * 32, v);
+                if (key < s) {
 #pragma unroll
-                    for (int jj = 0; jj < 4; ++jj)
-                        h2[jj] = __floats2bfloat162_rn(v[q8 * 8 + 2 * jj], v[q8 * 8 + 2 * jj + 1]);
-                    *reinterpret_cast<uint4*>(dvr + c * 32 + q8 * 8) = u;
+                    for (int q8 = 0; q8 < 4; ++q8) {
+                        uint4 u;
+                        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+                        for (int jj = 0; jj < 4; ++jj)
+                            h2[jj] = __floats2bfloat162_rn(v[q8 * 8 + 2 * jj] * scale, v[q8 * 8 + 2 * jj + 1] * scale);
+                        *reinterpret_cast<uint4*>(dkr + c * 32 + q8 * 8) = u;
+                    }
+                }
+                tmem_ld32f(tdV + lane_off + c * 32, v);
+                if (key < s) {
+#pragma unroll
+                    for (int q8 = 0; q8 < 4; ++q8) {
+                        uint4 u;
+                        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+                        for (int jj = 0; jj < 4; ++jj)
+                            h2[jj] = __floats2bfloat162_rn(v[q8 * 8 + 2 * jj], v[q8 * 8 + 2 * jj + 1]);
+                        *reinterpret_cast<uint4*>(dvr + c * 32 + q8 * 8) = u;
+                    }
                 }
             }
         }
@@ -1021,12 +641,15 @@ __global__ void __launch_bounds__(384, 1)
     }
 }
 
-// dQ: CTA owns 128 queries; loops over 64-key halves up to the diagonal.
+// dQ (persistent): an item is 128 queries of one (sequence, head); it loops
+// over 64-key halves up to the diagonal. Item t (heaviest first):
+// qb = nqb-1 - t/(a*nb). Q/dO single-buffered per item (released after the
+// item's last S MMA); K/V halves, S/dP buffers and dS smem on a global ring.
 template <int D>
 __global__ void __launch_bounds__(384, 1)
     dq2_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                const __grid_constant__ CUtensorMap tm_qkv64, const float* __restrict__ lse,
-               const float* __restrict__ Dv, bf16* __restrict__ dqkv, int s, int a) {
+               const float* __restrict__ Dv, bf16* __restrict__ dqkv, int s, int a, int nb) {
     constexpr int TB = Tile<D>::BYTES;
     constexpr int HB = (D / 64) * HR * 128;
     extern __shared__ uint8_t smraw[];
@@ -1038,28 +661,35 @@ __global__ void __launch_bounds__(384, 1)
     uint8_t* sS = sV + 2 * HB;          // [2] dS [128 q][64 keys] (one atom)
     uint64_t* bar = reinterpret_cast<uint64_t*>(sS + 2 * BR * 128);
     uint64_t* q_full = bar;
-    uint64_t* kv_full = bar + 1;        // [2]
-    uint64_t* kv_empty = bar + 3;       // [2]
-    uint64_t* s_full = bar + 5;         // [2]
-    uint64_t* p_full = bar + 7;
-    uint64_t* g_done = bar + 8;         // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
+    uint64_t* q_empty = bar + 1;
+    uint64_t* kv_full = bar + 2;        // [2]
+    uint64_t* kv_empty = bar + 4;       // [2]
+    uint64_t* s_full = bar + 6;         // [2]
+    uint64_t* p_full = bar + 8;
+    uint64_t* g_done = bar + 9;         // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 11);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nqb = (s + BR - 1) / BR;
-    const int qb = nqb - 1 - blockIdx.x;
-    const int head = blockIdx.y, b = blockIdx.z;
+    const int T = nqb * a * nb;
     const int h = a * D;
-    const int q0 = qb * BR;
-    const int row0 = b * s;
-    const int last_q = min(q0 + BR, s) - 1;
-    const int nh = last_q / HR + 1;     // key halves 0 .. containing the last query
+    auto decode = [&](int t, int& qb, int& head, int& b) {
+        qb = nqb - 1 - t / (a * nb);
+        const int rem = t % (a * nb);
+        head = rem % a;
+        b = rem / a;
+    };
+    auto halves = [&](int t) {   // key halves 0 .. the one holding the item's last query
+        const int qb = nqb - 1 - t / (a * nb);
+        return (min(qb * BR + BR, s) - 1) / HR + 1;
+    };
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tm_qkv);
         tma_prefetch_desc(&tm_do);
         tma_prefetch_desc(&tm_qkv64);
         mbar_init(q_full, 1);
+        mbar_init(q_empty, 1);
         for (int i = 0; i < 2; ++i) {
             mbar_init(&kv_full[i], 1);
             mbar_init(&kv_empty[i], 1);
@@ -1078,15 +708,25 @@ __global__ void __launch_bounds__(384, 1)
 
     if (warp == 0) {
         if (lane == 0) {
-            mbar_arrive_expect_tx(q_full, 2 * TB);
-            tma_tile<D>(sQ, &tm_qkv, q_full, head * D, row0 + q0);
-            tma_tile<D>(sO, &tm_do, q_full, head * D, row0 + q0);
-            for (int hh = 0; hh < nh; ++hh) {
-                const int sl = hh & 1;
-                mbar_wait(&kv_empty[sl], ((hh >> 1) & 1) ^ 1);
-                mbar_arrive_expect_tx(&kv_full[sl], 2 * HB);
-                tma_half<D>(sK + sl * HB, &tm_qkv64, &kv_full[sl], h + head * D, row0 + hh * HR);
-                tma_half<D>(sV + sl * HB, &tm_qkv64, &kv_full[sl], 2 * h + head * D, row0 + hh * HR);
+            int g = 0;
+            for (int k = 0;; ++k) {
+                const int t = sched_item(k, T);
+                if (t < 0) break;
+                int qb, head, b;
+                decode(t, qb, head, b);
+                const int row0 = b * s;
+                mbar_wait(q_empty, (k & 1) ^ 1);
+                mbar_arrive_expect_tx(q_full, 2 * TB);
+                tma_tile<D>(sQ, &tm_qkv, q_full, head * D, row0 + qb * BR);
+                tma_tile<D>(sO, &tm_do, q_full, head * D, row0 + qb * BR);
+                const int nh = halves(t);
+                for (int hh = 0; hh < nh; ++hh, ++g) {
+                    const int sl = g & 1;
+                    mbar_wait(&kv_empty[sl], ((g >> 1) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&kv_full[sl], 2 * HB);
+                    tma_half<D>(sK + sl * HB, &tm_qkv64, &kv_full[sl], h + head * D, row0 + hh * HR);
+                    tma_half<D>(sV + sl * HB, &tm_qkv64, &kv_full[sl], 2 * h + head * D, row0 + hh * HR);
+                }
             }
         }
     } else if (warp == 1) {
@@ -1094,85 +734,114 @@ __global__ void __launch_bounds__(384, 1)
             const uint32_t iS = idesc(HR, false, false);   // M=128 q, N=64 keys
             const uint32_t iG = idesc(D, false, true);
             const uint32_t aQ = smem_u32(sQ), aO = smem_u32(sO);
-            mbar_wait(q_full, 0);
-            auto issue_s = [&](int hh) {
-                const int sl = hh & 1;
-                mbar_wait(&kv_full[sl], (hh >> 1) & 1);
+            int k_s = 0, h_s = 0, nh_s = 0, gs = 0;
+            bool have_s;
+            {
+                const int t = sched_item(0, T);
+                have_s = t >= 0;
+                if (have_s) nh_s = halves(t);
+            }
+            auto issue_s = [&]() {
+                const int sl = gs & 1;
+                if (h_s == 0) mbar_wait(q_full, k_s & 1);
+                mbar_wait(&kv_full[sl], (gs >> 1) & 1);
                 tc_fence_after();
                 const uint32_t aK = smem_u32(sK + sl * HB), aV = smem_u32(sV + sl * HB);
                 const uint32_t tS = tmem + sl * 128, tP = tS + 64;
 #pragma unroll
-                for (int k = 0; k < D / 16; ++k) {
-                    umma_bf16(tS, desc_k(aQ, k), desc_k_h(aK, k), iS, k > 0);   // S = Q K^T
-                    umma_bf16(tP, desc_k(aO, k), desc_k_h(aV, k), iS, k > 0);   // dP = dO V^T
+                for (int kk = 0; kk < D / 16; ++kk) {
+                    umma_bf16(tS, desc_k(aQ, kk), desc_k_h(aK, kk), iS, kk > 0);   // S = Q K^T
+                    umma_bf16(tP, desc_k(aO, kk), desc_k_h(aV, kk), iS, kk > 0);   // dP = dO V^T
                 }
                 umma_commit(&s_full[sl]);
+                if (h_s == nh_s - 1) umma_commit(q_empty);   // Q, dO of this item consumed
+                ++gs;
+                if (++h_s == nh_s) {
+                    h_s = 0;
+                    const int t = sched_item(++k_s, T);
+                    have_s = t >= 0;
+                    if (have_s) nh_s = halves(t);
+                }
             };
-            issue_s(0);
-            for (int hh = 0; hh < nh; ++hh) {
-                const int sl = hh & 1;
-                if (hh + 1 < nh) issue_s(hh + 1);
-                mbar_wait(p_full, hh & 1);
-                tc_fence_after();
-                const uint32_t aK = smem_u32(sK + sl * HB), aS = smem_u32(sS + sl * BR * 128);
+            if (have_s) issue_s();
+            int g = 0;
+            for (int k = 0;; ++k) {
+                const int t = sched_item(k, T);
+                if (t < 0) break;
+                const int nh = halves(t);
+                for (int hh = 0; hh < nh; ++hh, ++g) {
+                    const int sl = g & 1;
+                    if (have_s) issue_s();
+                    mbar_wait(p_full, g & 1);
+                    tc_fence_after();
+                    const uint32_t aK = smem_u32(sK + sl * HB), aS = smem_u32(sS + sl * BR * 128);
 #pragma unroll
-                for (int k = 0; k < HR / 16; ++k)
-                    umma_bf16(tdQ, desc_k(aS, k), desc_mn_h(aK, k), iG, (hh | k) > 0);   // dQ += dS K
-                umma_commit(&g_done[sl]);
-                umma_commit(&kv_empty[sl]);
+                    for (int kk = 0; kk < HR / 16; ++kk)
+                        umma_bf16(tdQ, desc_k(aS, kk), desc_mn_h(aK, kk), iG, (hh | kk) > 0);   // dQ += dS K
+                    umma_commit(&g_done[sl]);
+                    umma_commit(&kv_empty[sl]);
+                }
             }
         }
     } else if (warp >= 4) {
         const int et = threadIdx.x - 128;
         const int r = et & 127, cg = et >> 7;
-        const int q = q0 + r;
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
         const float sc = rsqrtf((float)D) * LOG2E;
-        const float* lseb = lse + ((long)b * a + head) * s;
-        const float* Db = Dv + ((long)b * a + head) * s;
-        const float L = q < s ? lseb[q] * LOG2E : 0.f;
-        const float Dq = q < s ? Db[q] : 0.f;
-        for (int hh = 0; hh < nh; ++hh) {
-            const int sl = hh & 1;
-            if (hh >= 2) mbar_wait(&g_done[sl], ((hh - 2) >> 1) & 1);   // dS buffer reuse
-            mbar_wait(&s_full[sl], (hh >> 1) & 1);
-            tc_fence_after();
-            const uint32_t tS = tmem + sl * 128 + lane_off, tP = tS + 64;
-            uint8_t* Sd = sS + sl * BR * 128;
-            {
-                const int c = cg;
-                float sv[32], pv[32];
-                tmem_ld32f(tS + c * 32, sv);
-                tmem_ld32f(tP + c * 32, pv);
-#pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    const int key = hh * HR + c * 32 + e;
-                    const float p = (key <= q) ? exp2f(sv[e] * sc - L) : 0.f;
-                    pv[e] = p * (pv[e] - Dq);
-                }
-                st_row32_h(Sd, r, c * 32, pv);
-            }
-            fence_async_smem();
-            tc_fence_before();
-            mbar_arrive(p_full);
-        }
-        mbar_wait(&g_done[(nh - 1) & 1], ((nh - 1) >> 1) & 1);
-        tc_fence_after();
         const float scale = rsqrtf((float)D);
-        bf16* dqr = dqkv + ((long)b * s + q) * (3L * h) + head * D;
+        int g = 0;
+        for (int k = 0;; ++k) {
+            const int t = sched_item(k, T);
+            if (t < 0) break;
+            int qb, head, b;
+            decode(t, qb, head, b);
+            const int nh = halves(t);
+            const int q = qb * BR + r;
+            const float* lseb = lse + ((long)b * a + head) * s;
+            const float* Db = Dv + ((long)b * a + head) * s;
+            const float L = q < s ? lseb[q] * LOG2E : 0.f;
+            const float Dq = q < s ? Db[q] : 0.f;
+            for (int hh = 0; hh < nh; ++hh, ++g) {
+                const int sl = g & 1;
+                if (g >= 2) mbar_wait(&g_done[sl], ((g - 2) >> 1) & 1);   // dS buffer reuse
+                mbar_wait(&s_full[sl], (g >> 1) & 1);
+                tc_fence_after();
+                const uint32_t tS = tmem + sl * 128 + lane_off, tP = tS + 64;
+                uint8_t* Sd = sS + sl * BR * 128;
+                {
+                    const int c = cg;
+                    float sv[32], pv[32];
+                    tmem_ld32f(tS + c * 32, sv);
+                    tmem_ld32f(tP + c * 32, pv);
 #pragma unroll
-        for (int c = cg * (D / 64); c < (cg + 1) * (D / 64); ++c) {
-            float v[32];
-            tmem_ld32f(tdQ + lane_off + c * 32, v);
-            if (q < s) {
+                    for (int e = 0; e < 32; ++e) {
+                        const int key = hh * HR + c * 32 + e;
+                        const float p = (key <= q) ? exp2f(sv[e] * sc - L) : 0.f;
+                        pv[e] = p * (pv[e] - Dq);
+                    }
+                    st_row32_h(Sd, r, c * 32, pv);
+                }
+                fence_async_smem();
+                tc_fence_before();
+                mbar_arrive(p_full);
+            }
+            mbar_wait(&g_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
+            tc_fence_after();
+            bf16* dqr = dqkv + ((long)b * s + q) * (3L * h) + head * D;
 #pragma unroll
-                for (int q8 = 0; q8 < 4; ++q8) {
-                    uint4 u;
-                    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+            for (int c = cg * (D / 64); c < (cg + 1) * (D / 64); ++c) {
+                float v[32];
+                tmem_ld32f(tdQ + lane_off + c * 32, v);
+                if (q < s) {
 #pragma unroll
-                    for (int jj = 0; jj < 4; ++jj)
-                        h2[jj] = __floats2bfloat162_rn(v[q8 * 8 + 2 * jj] * scale, v[q8 * 8 + 2 * jj + 1] * scale);
-                    *reinterpret_cast<uint4*>(dqr + c * 32 + q8 * 8) = u;
+                    for (int q8 = 0; q8 < 4; ++q8) {
+                        uint4 u;
+                        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+                        for (int jj = 0; jj < 4; ++jj)
+                            h2[jj] = __floats2bfloat162_rn(v[q8 * 8 + 2 * jj] * scale, v[q8 * 8 + 2 * jj + 1] * scale);
+                        *reinterpret_cast<uint4*>(dqr + c * 32 + q8 * 8) = u;
+                    }
                 }
             }
         }
@@ -1235,10 +904,23 @@ static int map2d(CUtensorMap* m, const void* base, long cols, long rows, long ld
                : -2;
 }
 
+static int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+static int persistent_grid(int items) { return items < num_sms() ? items : num_sms(); }
+
 template <int D>
 static int fwd5(const void* qkv, void* o, float* lse, int b, int s, int a, cudaStream_t st) {
     constexpr int TB = fa5::Tile<D>::BYTES;
-    constexpr int smem = 1024 + TB * 5 + 6 * 128 * 4 + 256;
+    constexpr int smem = 1024 + TB * 6 + 6 * 128 * 4 + 256;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(fa5::fwd2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1246,8 +928,8 @@ static int fwd5(const void* qkv, void* o, float* lse, int b, int s, int a, cudaS
     }
     CUtensorMap m;
     if (map2d(&m, qkv, 3L * a * D, (long)b * s, 3L * a * D)) return -2;
-    dim3 grid((s + 127) / 128, a, b);
-    fa5::fwd2_kernel<D><<<grid, 384, smem, st>>>(m, (bf16*)o, lse, s, a);
+    const int grid = persistent_grid(((s + 127) / 128) * a * b);
+    fa5::fwd2_kernel<D><<<grid, 384, smem, st>>>(m, (bf16*)o, lse, s, a, b);
     note_launches(1);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
@@ -1272,9 +954,9 @@ static int bwd5(const void* qkv, const void* o, const void* dout, const float* l
     if (map2d(&md64, dout, (long)a * D, (long)b * s, (long)a * D, 64)) return -2;
     dim3 gd((s + 3) / 4, a, b);
     fa5::d_kernel<<<gd, 128, 0, st>>>((const bf16*)o, (const bf16*)dout, ws, s, a, D);
-    dim3 grid((s + 127) / 128, a, b);
-    fa5::dkdv2_kernel<D><<<grid, 384, smem_kv, st>>>(mq, mq64, md64, lse, ws, (bf16*)dqkv, s, a);
-    fa5::dq2_kernel<D><<<grid, 384, smem_q, st>>>(mq, md, mq64, lse, ws, (bf16*)dqkv, s, a);
+    const int grid = persistent_grid(((s + 127) / 128) * a * b);
+    fa5::dkdv2_kernel<D><<<grid, 384, smem_kv, st>>>(mq, mq64, md64, lse, ws, (bf16*)dqkv, s, a, b);
+    fa5::dq2_kernel<D><<<grid, 384, smem_q, st>>>(mq, md, mq64, lse, ws, (bf16*)dqkv, s, a, b);
     note_launches(3);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
