@@ -53,6 +53,19 @@ int tpipe_k_gemm_simt(int dtype, int M, int N, int K,
                       const void* R, long ldr, void* C2, long ldc2,
                       const void* aux, long ldaux, void* stream);
 
+/* Enable (1) or disable (0, default) stream-K scheduling in the tcgen05 GEMM
+ * (process-wide; for A/B measurement). Stream-K splits the concatenated K
+ * iterations of all output tiles evenly over the SMs; split tiles are summed
+ * in a fixed order, so results stay bit-reproducible for a given shape and
+ * SM count. Uses a lazily allocated per-stream workspace of #SMs x 128 KB. */
+void tpipe_k_gemm_set_stream_k(int on);
+
+/* Enable (1, default) or disable (0) CTA-pair tiles in the tcgen05 GEMM
+ * (process-wide; for A/B measurement): a cluster of two CTAs on one TPC
+ * computes a 256 x 256 tile with tcgen05.mma.cta_group::2, each CTA staging
+ * half of the A and B operands. Used when the shape yields >= 32 such tiles. */
+void tpipe_k_gemm_set_pair(int on);
+
 /* LayerNorm forward over rows of length h (eps 1e-5, biased variance):
  * y = (x-mean)*rstd*gamma + beta; mean/rstd fp32 [rows]. */
 int tpipe_k_ln_fwd(int dtype, const void* x, const void* gamma, const void* beta,

@@ -10,12 +10,28 @@
 // Both operands may be K-major or MN-major (fprop: K/K, dgrad: K/MN,
 // wgrad: MN/MN), so no transposes are materialised.
 //
+// Stream-K (off by default; tpipe_k_gemm_set_stream_k): when whole tiles
+// would leave SMs idle in the last wave (every 2048-multiple shape of the
+// model on 148 SMs caps at ~86%), the tiles' K iterations are laid end to end
+// and split evenly over the CTAs (or CTA pairs). Measured 20-50% SLOWER than
+// the data-parallel schedule on the model shapes (the owners' partial fix-up
+// sits on the critical path and concurrent CTAs no longer share L2 lines), so
+// it is kept for A/B runs only. A CTA whose
+// range starts inside a tile ("contributor") writes its fp32 partial to its
+// own workspace slot and publishes a flag; the CTA that holds the tile's k=0
+// part ("owner", which reaches it last) adds the partials in CTA order in its
+// epilogue. Fixed summation order => bit-reproducible results.
+//
 // fp32: exact-fp32 SIMT tiled kernel (parity mode).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
+#include <utility>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -214,12 +230,20 @@ int gemm_simt(int dtype, const GemmDesc& g, cudaStream_t st) {
 
 // ============================================================== tcgen05 (bf16)
 constexpr int TC_BM = 128, TC_BK = 64;
+static bool g_stream_k_enabled = false;   // measured slower on the model shapes
+static bool g_pair_enabled = true;
+void gemm_set_stream_k(int on) { g_stream_k_enabled = on != 0; }
+void gemm_set_pair(int on) { g_pair_enabled = on != 0; }
 
-template <int BN>
+// CG = 1: one CTA computes a 128 x BN tile. CG = 2: a CTA pair (cluster of 2
+// on one TPC) computes a 256 x BN tile with tcgen05.mma.cta_group::2; each CTA
+// stages 128 rows of A and BN/2 rows of B, so per-SM operand traffic (L2->smem
+// and smem->tensor core) is 2/3 of the CG = 1, BN = 256 tile's.
+template <int BN, int CG = 1>
 struct TcCfg {
-    static constexpr int STAGES = BN == 256 ? 4 : 6;
+    static constexpr int STAGES = CG == 2 ? 6 : (BN == 256 ? 4 : 6);
     static constexpr int A_BYTES = TC_BM * TC_BK * 2;
-    static constexpr int B_BYTES = BN * TC_BK * 2;
+    static constexpr int B_BYTES = (BN / CG) * TC_BK * 2;
     static constexpr int TMEM_COLS = 2 * BN;
     // epilogue staging: 4 warps x 2 buffers x (32 rows x 128 B)
     static constexpr int STAGING = 4 * 2 * 4096;
@@ -310,8 +334,8 @@ __device__ __forceinline__ void stage_store(uint8_t* buf, const float (&v)[32], 
     }
 }
 
-// instruction descriptor: bf16 x bf16 -> f32, M=128, N=BN, majors
-template <int BN, bool A_MN, bool B_MN>
+// instruction descriptor: bf16 x bf16 -> f32, M=128*CG, N=BN, majors
+template <int BN, bool A_MN, bool B_MN, int CG>
 __device__ __forceinline__ uint32_t tc_idesc() {
     return (1u << 4)                     // D format f32
            | (1u << 7)                   // A bf16
@@ -319,16 +343,72 @@ __device__ __forceinline__ uint32_t tc_idesc() {
            | ((A_MN ? 1u : 0u) << 15)    // A major
            | ((B_MN ? 1u : 0u) << 16)    // B major
            | ((uint32_t)(BN >> 3) << 17) // N
-           | ((uint32_t)(TC_BM >> 4) << 24);  // M
+           | ((uint32_t)((TC_BM * CG) >> 4) << 24);  // M
 }
 
-template <int BN, bool A_MN, bool B_MN>
+// Work of one CTA: whole tiles strided by the grid (data-parallel) or a
+// contiguous range of the concatenated K iterations (stream-K).
+struct TcSched {
+    int num_tiles, num_kb, sk, tile_dp, stride;
+    long it, it_end;
+    // CG = 2: both CTAs of a pair walk the same tiles (unit = cluster)
+    __device__ void init(int nt, int nkb, int sk_, int cg = 1) {
+        num_tiles = nt;
+        num_kb = nkb;
+        sk = sk_;
+        tile_dp = blockIdx.x / cg;
+        stride = gridDim.x / cg;
+        const long I = (long)nt * nkb;
+        it = (long)tile_dp * I / stride;
+        it_end = (long)(tile_dp + 1) * I / stride;
+    }
+    // next segment: tile, k blocks [kb0, kb1)
+    __device__ bool next(int& tile, int& kb0, int& kb1) {
+        if (!sk) {
+            if (tile_dp >= num_tiles) return false;
+            tile = tile_dp;
+            kb0 = 0;
+            kb1 = num_kb;
+            tile_dp += stride;
+            return true;
+        }
+        if (it >= it_end) return false;
+        tile = (int)(it / num_kb);
+        kb0 = (int)(it % num_kb);
+        const long left = it_end - it;
+        kb1 = left < (long)(num_kb - kb0) ? kb0 + (int)left : num_kb;
+        it += kb1 - kb0;
+        return true;
+    }
+};
+
+// unit (CTA, or CTA pair for CG = 2) whose stream-K range holds iteration x
+__device__ __forceinline__ int sk_unit_of(long x, long I, int G) {
+    int c = (int)(x * G / I);
+    while (c + 1 < G && (long)(c + 1) * I / G <= x) ++c;
+    while (c > 0 && (long)c * I / G > x) --c;
+    return c;
+}
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int BN, bool A_MN, bool B_MN, int CG>
 __global__ void __launch_bounds__(256, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
-                   const GemmDesc g, int num_m, int num_n, int num_kb) {
-    using Cfg = TcCfg<BN>;
+                   const GemmDesc g, int num_m, int num_n, int num_kb, int sk, float* __restrict__ sk_ws,
+                   unsigned* __restrict__ sk_flags, unsigned epoch) {
+    using Cfg = TcCfg<BN, CG>;
     constexpr int STAGES = Cfg::STAGES;
+    constexpr int TM = TC_BM * CG;        // tile rows
+    constexpr int BNC = BN / CG;          // B rows staged per CTA
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
@@ -342,6 +422,7 @@ __global__ void __launch_bounds__(256, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int num_tiles = num_m * num_n;
+    const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;   // 0 = pair leader (issues the MMAs)
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
@@ -350,19 +431,27 @@ __global__ void __launch_bounds__(256, 1)
         tma_prefetch_desc(&tmC2);
     }
     if (warp == 1 && lane == 0) {
+        // CG = 2: the leader's full[] gets both CTAs' arrivals and TMA bytes;
+        // empty[] / tfull[] of each CTA are signalled by the leader's multicast
+        // commits; the leader's tempty[] gets one arrival per epilogue warp of
+        // both CTAs.
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], CG);
             mbar_init(&empty[s], 1);
         }
         for (int e = 0; e < 2; ++e) {
             mbar_init(&tfull[e], 1);
-            mbar_init(&tempty[e], 128);
+            mbar_init(&tempty[e], CG == 2 ? 8 : 128);
         }
         fence_mbar_init();
     }
-    if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+    if (warp == 2) {
+        if (CG == 2) tmem_alloc_pair(tmem_slot, Cfg::TMEM_COLS);
+        else tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+    }
     tc_fence_before();
-    __syncthreads();
+    if (CG == 2) cluster_sync_all();
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -371,47 +460,73 @@ __global__ void __launch_bounds__(256, 1)
             // ---------------- TMA producer
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            TcSched sch;
+            sch.init(num_tiles, num_kb, sk, CG);
+            int tile, kb0, kb1;
+            while (sch.next(tile, kb0, kb1)) {
                 const int mb = tile % num_m, nb = tile / num_m;
-                for (int kb = 0; kb < num_kb; ++kb) {
+                const int am = mb * TM + rank * TC_BM;     // this CTA's A rows
+                const int bn = nb * BN + rank * BNC;       // this CTA's B rows
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* a = sA + stage * Cfg::A_BYTES;
                     uint8_t* b = sB + stage * Cfg::B_BYTES;
-                    if (!A_MN) {
-                        tma_load_2d(a, &tmA, &full[stage], kb * TC_BK, mb * TC_BM);
-                    } else {
+                    if (CG == 1) {
+                        if (!A_MN) {
+                            tma_load_2d(a, &tmA, &full[stage], kb * TC_BK, am);
+                        } else {
 #pragma unroll
-                        for (int i = 0; i < TC_BM / 64; ++i)
-                            tma_load_2d(a + i * 64 * TC_BK * 2, &tmA, &full[stage], mb * TC_BM + i * 64,
-                                        kb * TC_BK);
-                    }
-                    if (!B_MN) {
-                        tma_load_2d(b, &tmB, &full[stage], kb * TC_BK, nb * BN);
-                    } else {
+                            for (int i = 0; i < TC_BM / 64; ++i)
+                                tma_load_2d(a + i * 64 * TC_BK * 2, &tmA, &full[stage], am + i * 64, kb * TC_BK);
+                        }
+                        if (!B_MN) {
+                            tma_load_2d(b, &tmB, &full[stage], kb * TC_BK, bn);
+                        } else {
 #pragma unroll
-                        for (int i = 0; i < BN / 64; ++i)
-                            tma_load_2d(b + i * 64 * TC_BK * 2, &tmB, &full[stage], nb * BN + i * 64,
-                                        kb * TC_BK);
+                            for (int i = 0; i < BNC / 64; ++i)
+                                tma_load_2d(b + i * 64 * TC_BK * 2, &tmB, &full[stage], bn + i * 64, kb * TC_BK);
+                        }
+                        mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
+                    } else {
+                        const uint32_t fb = mapa_shared(&full[stage], 0);   // leader's barrier
+                        if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (Cfg::A_BYTES + Cfg::B_BYTES));
+                        if (!A_MN) {
+                            tma_load_2d_pair(a, &tmA, fb, kb * TC_BK, am);
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < TC_BM / 64; ++i)
+                                tma_load_2d_pair(a + i * 64 * TC_BK * 2, &tmA, fb, am + i * 64, kb * TC_BK);
+                        }
+                        if (!B_MN) {
+                            tma_load_2d_pair(b, &tmB, fb, kb * TC_BK, bn);
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < BNC / 64; ++i)
+                                tma_load_2d_pair(b + i * 64 * TC_BK * 2, &tmB, fb, bn + i * 64, kb * TC_BK);
+                        }
+                        if (rank != 0) mbar_arrive_cluster(fb);
                     }
-                    mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            // ---------------- MMA issuer (single thread)
-            const uint32_t idesc = tc_idesc<BN, A_MN, B_MN>();
+        if (lane == 0 && rank == 0) {
+            // ---------------- MMA issuer (single thread; the pair leader for CG = 2)
+            const uint32_t idesc = tc_idesc<BN, A_MN, B_MN, CG>();
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+            TcSched sch;
+            sch.init(num_tiles, num_kb, sk, CG);
+            int tile, kb0, kb1;
+            for (; sch.next(tile, kb0, kb1); ++it) {
                 const int acc = it & 1;
                 const uint32_t aph = (it >> 1) & 1;
                 mbar_wait(&tempty[acc], aph ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem_base + acc * BN;
-                for (int kb = 0; kb < num_kb; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t a_addr = smem_u32(sA + stage * Cfg::A_BYTES);
@@ -424,12 +539,16 @@ __global__ void __launch_bounds__(256, 1)
                                                  : umma_desc_sw128(a_addr + k * 32, 0, 1024);
                         const uint64_t db = B_MN ? umma_desc_sw128(b_addr + k * 2048, TC_BK * 128, 1024)
                                                  : umma_desc_sw128(b_addr + k * 32, 0, 1024);
-                        umma_bf16(d, da, db, idesc, (kb | k) != 0 ? 1u : 0u);
+                        const uint32_t accum = (kb != kb0 || k != 0) ? 1u : 0u;
+                        if (CG == 2) umma_bf16_pair(d, da, db, idesc, accum);
+                        else umma_bf16(d, da, db, idesc, accum);
                     }
-                    umma_commit(&empty[stage]);
+                    if (CG == 2) umma_commit_pair(&empty[stage], 3);
+                    else umma_commit(&empty[stage]);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                umma_commit(&tfull[acc]);
+                if (CG == 2) umma_commit_pair(&tfull[acc], 3);
+                else umma_commit(&tfull[acc]);
             }
         }
     } else if (warp >= 4) {
@@ -441,14 +560,57 @@ __global__ void __launch_bounds__(256, 1)
         const bool two = (g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU);
         int sb = 0;
         int it = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        TcSched sch;
+        sch.init(num_tiles, num_kb, sk, CG);
+        const long I = (long)num_tiles * num_kb;
+        const uint32_t tempty_leader = CG == 2 ? mapa_shared(&tempty[0], 0) : 0;
+        const int row = ew * 32 + lane;   // row of the tile this thread owns
+        int tile, kb0, kb1;
+        for (; sch.next(tile, kb0, kb1); ++it) {
             const int mb = tile % num_m, nb = tile / num_m;
             const int acc = it & 1;
             const uint32_t aph = (it >> 1) & 1;
             mbar_wait(&tfull[acc], aph);
             tc_fence_after();
-            const int m0 = mb * TC_BM + ew * 32;
+            const int m0 = mb * TM + rank * TC_BM + ew * 32;
             const long m = m0 + lane;
+            if (kb0 > 0) {
+                // ---- stream-K contributor: fp32 partial -> own slot (one per CTA;
+                // for a pair each CTA holds its 128 rows), then flag
+                float* slot = sk_ws + (size_t)blockIdx.x * TC_BM * BN;
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t r[32];
+                    tmem_ld32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + c * 32, r);
+                    tmem_wait_ld();
+                    float4* dst = reinterpret_cast<float4*>(slot + ((size_t)c * TC_BM + row) * 32);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        __stcg(dst + q, make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                                    __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3])));
+                }
+                __threadfence();
+                named_bar_sync(1, 128);
+                if (ew == 0 && lane == 0) st_release_u32(sk_flags + blockIdx.x, epoch);
+                tc_fence_before();
+                if (CG == 2) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
+                } else {
+                    mbar_arrive(&tempty[acc]);
+                }
+                continue;
+            }
+            // owner of a split tile: contributors are the CTAs after this one up
+            // to the one holding the tile's last iteration
+            const int unit = blockIdx.x / CG, nunits = gridDim.x / CG;
+            int c_last = unit;
+            if (kb1 < num_kb) {
+                c_last = sk_unit_of((long)tile * num_kb + num_kb - 1, I, nunits);
+                for (int cc = unit + 1; cc <= c_last; ++cc)
+                    while (ld_acquire_u32(sk_flags + cc * CG + rank) != epoch) {
+                    }
+            }
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
                 uint32_t r[32];
@@ -459,6 +621,18 @@ __global__ void __launch_bounds__(256, 1)
                 float v[32], v2[32];
 #pragma unroll
                 for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                for (int cc = unit + 1; cc <= c_last; ++cc) {   // fixed order: k ascending
+                    const float4* src = reinterpret_cast<const float4*>(
+                        sk_ws + (size_t)(cc * CG + rank) * TC_BM * BN + ((size_t)c * TC_BM + row) * 32);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const float4 p = __ldcg(src + q);
+                        v[4 * q] += p.x;
+                        v[4 * q + 1] += p.y;
+                        v[4 * q + 2] += p.z;
+                        v[4 * q + 3] += p.w;
+                    }
+                }
                 epi_math(g, m, n0, m < g.M, v, v2);
                 stage_store(mystg + sb * 4096, v, f32out, reduce, &tmC, n0, m0, lane);
                 sb ^= 1;
@@ -468,15 +642,23 @@ __global__ void __launch_bounds__(256, 1)
                 }
             }
             tc_fence_before();
-            mbar_arrive(&tempty[acc]);
+            if (CG == 2) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
+            } else {
+                mbar_arrive(&tempty[acc]);
+            }
         }
         if (lane == 0) bulk_wait_all();
         __syncwarp();
     }
-    __syncthreads();
+    tc_fence_before();
+    if (CG == 2) cluster_sync_all();
+    else __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+        if (CG == 2) tmem_dealloc_pair(tmem_base, Cfg::TMEM_COLS);
+        else tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
     }
 }
 
@@ -522,9 +704,56 @@ static int num_sms() {
     return n;
 }
 
-template <int BN, bool A_MN, bool B_MN>
+// Stream-K workspace, one per (device, stream): #SMs slots of a 128 x 256 fp32
+// partial tile (19.4 MB on 148 SMs) + one flag per slot. Flags carry a
+// per-launch epoch, so they never need resetting. Launches on one stream are
+// serialised, so a slot is never shared by two live kernels.
+struct SkWs {
+    float* ws = nullptr;
+    unsigned* flags = nullptr;
+};
+static int sk_workspace(cudaStream_t st, SkWs& out) {
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<int, cudaStream_t>, SkWs>> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& e : cache)
+        if (e.first.first == dev && e.first.second == st) {
+            out = e.second;
+            return 0;
+        }
+    SkWs w;
+    const size_t slots = (size_t)num_sms();
+    if (cudaMalloc(&w.ws, slots * TC_BM * 256 * sizeof(float)) != cudaSuccess) return -6;
+    if (cudaMalloc(&w.flags, slots * sizeof(unsigned)) != cudaSuccess) return -6;
+    if (cudaMemset(w.flags, 0, slots * sizeof(unsigned)) != cudaSuccess) return -6;
+    if (cudaDeviceSynchronize() != cudaSuccess) return -6;
+    cache.push_back({{dev, st}, w});
+    out = w;
+    return 0;
+}
+static unsigned next_epoch() {
+    static std::atomic<unsigned> e{0};
+    unsigned v = ++e;
+    if (v == 0) v = ++e;   // 0 is the flags' initial value
+    return v;
+}
+
+// Stream-K pays when whole tiles leave >= 8% of the SM-waves idle and each CTA
+// still gets >= 4 K blocks.
+static bool use_stream_k(int tiles, int num_kb, int G) {
+    if (tiles <= 0) return false;
+    const long waves = (tiles + G - 1) / G;
+    const double eff = (double)tiles / (double)(waves * G);
+    const long I = (long)tiles * num_kb;
+    return eff < 0.92 && I >= 4L * G;
+}
+
+template <int BN, bool A_MN, bool B_MN, int CG>
 static int launch_tc(const GemmDesc& g, cudaStream_t st) {
-    using Cfg = TcCfg<BN>;
+    using Cfg = TcCfg<BN, CG>;
+    constexpr int BNC = BN / CG;
     CUtensorMap ta, tb;
     int rc;
     if (!A_MN)
@@ -533,7 +762,7 @@ static int launch_tc(const GemmDesc& g, cudaStream_t st) {
         rc = make_map(&ta, g.A, g.M, g.K, g.lda, 64, TC_BK);
     if (rc) return rc;
     if (!B_MN)
-        rc = make_map(&tb, g.B, g.K, g.N, g.ldb, TC_BK, BN);
+        rc = make_map(&tb, g.B, g.K, g.N, g.ldb, TC_BK, BNC);
     else
         rc = make_map(&tb, g.B, g.N, g.K, g.ldb, 64, TC_BK);
     if (rc) return rc;
@@ -549,20 +778,63 @@ static int launch_tc(const GemmDesc& g, cudaStream_t st) {
     } else {
         tc2 = tc;
     }
-    const int num_m = (g.M + TC_BM - 1) / TC_BM;
+    const int num_m = (g.M + TC_BM * CG - 1) / (TC_BM * CG);
     const int num_n = (g.N + BN - 1) / BN;
     const int num_kb = (g.K + TC_BK - 1) / TC_BK;
     const int tiles = num_m * num_n;
-    const int grid = tiles < num_sms() ? tiles : num_sms();
-    auto kern = gemm_tc_kernel<BN, A_MN, B_MN>;
+    const int units = num_sms() / CG;
+    const int sk = g_stream_k_enabled && use_stream_k(tiles, num_kb, units) ? 1 : 0;
+    const int grid = CG * (sk ? units : (tiles < units ? tiles : units));
+    SkWs w;
+    unsigned epoch = 0;
+    if (sk) {
+        if (int e = sk_workspace(st, w)) return e;
+        epoch = next_epoch();
+    }
+    auto kern = gemm_tc_kernel<BN, A_MN, B_MN, CG>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
         attr_set = true;
     }
-    kern<<<grid, 256, Cfg::SMEM, st>>>(ta, tb, tc, tc2, g, num_m, num_n, num_kb);
+    if (CG == 1) {
+        kern<<<grid, 256, Cfg::SMEM, st>>>(ta, tb, tc, tc2, g, num_m, num_n, num_kb, sk, w.ws, w.flags, epoch);
+    } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = Cfg::SMEM;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        static bool dbg_once = false;
+        if (!dbg_once && getenv("TPIPE_GEMM_DEBUG")) {
+            dbg_once = true;
+            int ncl = -1;
+            cudaError_t e = cudaOccupancyMaxActiveClusters(&ncl, (void*)kern, &cfg);
+            fprintf(stderr, "[gemm] pair kernel: max active clusters %d (%s), grid %d, smem %d\n", ncl,
+                    cudaGetErrorString(e), grid, Cfg::SMEM);
+        }
+        if (cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tc2, g, num_m, num_n, num_kb, sk, w.ws, w.flags, epoch) !=
+            cudaSuccess)
+            return -3;
+    }
     note_launches(1);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+template <int BN, int CG>
+static int launch_majors(const GemmDesc& g, cudaStream_t st) {
+    const bool amn = !g.a_kmajor, bmn = !g.b_kmajor;
+    if (!amn && !bmn) return launch_tc<BN, false, false, CG>(g, st);
+    if (!amn && bmn) return launch_tc<BN, false, true, CG>(g, st);
+    if (amn && bmn) return launch_tc<BN, true, true, CG>(g, st);
+    return launch_tc<BN, true, false, CG>(g, st);
 }
 
 int gemm_tc(const GemmDesc& g, cudaStream_t st) {
@@ -572,23 +844,22 @@ int gemm_tc(const GemmDesc& g, cudaStream_t st) {
     if ((g.N % 32) || (g.lda % 8) || (g.ldb % 8) || (g.ldc % 8) ||
         ((g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU) && (g.ldc2 % 8)))
         return -5;
+    // CTA-pair 256 x 256 tiles: per SM they move 32 KB of operands per 64-deep
+    // K block instead of 48 KB. Measured on the model shapes (profiles/
+    // r1_gemm_modes.jsonl) they win once there are >= 96 pair tiles or the K
+    // loop is long (>= 4096); a 2048 x 2048 x 2048 GEMM (64 pair tiles on 74
+    // pairs) is faster as 128 single-CTA tiles.
+    const long pair_tiles = (long)((g.M + 255) / 256) * ((g.N + 255) / 256);
+    if (g_pair_enabled && (pair_tiles >= 96 || (pair_tiles >= 32 && g.K >= 4096)))
+        return launch_majors<256, 2>(g, st);
     const int num_m = (g.M + TC_BM - 1) / TC_BM;
     // N=128 tiles read 8 KB of operands per 64-cycle MMA (128 B/cycle, the
     // shared-memory limit); N=256 tiles need 96 B/cycle. Prefer 256 whenever
     // it still occupies >= ~65% of the SMs.
     // (a ragged last N tile is fine: TMA zero-fills, the epilogue masks n >= N)
     const bool wide = (long)num_m * ((g.N + 255) / 256) * 3 >= 2L * num_sms();
-    const bool amn = !g.a_kmajor, bmn = !g.b_kmajor;
-    if (wide) {
-        if (!amn && !bmn) return launch_tc<256, false, false>(g, st);
-        if (!amn && bmn) return launch_tc<256, false, true>(g, st);
-        if (amn && bmn) return launch_tc<256, true, true>(g, st);
-        return launch_tc<256, true, false>(g, st);
-    }
-    if (!amn && !bmn) return launch_tc<128, false, false>(g, st);
-    if (!amn && bmn) return launch_tc<128, false, true>(g, st);
-    if (amn && bmn) return launch_tc<128, true, true>(g, st);
-    return launch_tc<128, true, false>(g, st);
+    if (wide) return launch_majors<256, 1>(g, st);
+    return launch_majors<128, 1>(g, st);
 }
 
 int gemm(int dtype, const GemmDesc& g, cudaStream_t st) {

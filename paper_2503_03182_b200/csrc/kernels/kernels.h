@@ -38,6 +38,10 @@ int gemm(int dtype, const GemmDesc& g, cudaStream_t st);
 int gemm_simt(int dtype, const GemmDesc& g, cudaStream_t st);
 // tcgen05 kernel (bf16 only).
 int gemm_tc(const GemmDesc& g, cudaStream_t st);
+// stream-K scheduling on/off for the tcgen05 GEMM (default on)
+void gemm_set_stream_k(int on);
+// CTA-pair (cta_group::2) 256-row tiles on/off (default on)
+void gemm_set_pair(int on);
 
 // ---------------------------------------------------------------- layernorm
 // y = (x - mean) * rstd * gamma + beta over rows of length h; saves mean/rstd (fp32).

@@ -98,3 +98,11 @@ def tpipe_host_adamw(master, m, v, grad, w_bf16, n, decay, lr, b1, b2, eps, wd, 
     ptr = (lambda a: None if a is None else a.ctypes.data)
     lib().tpipe_host_adamw(ptr(master), ptr(m), ptr(v), ptr(grad), ptr(w_bf16), n, decay, lr, b1,
                            b2, eps, wd, bc1, bc2)
+
+
+def tpipe_k_gemm_set_stream_k(on):
+    lib().tpipe_k_gemm_set_stream_k(1 if on else 0)
+
+
+def tpipe_k_gemm_set_pair(on):
+    lib().tpipe_k_gemm_set_pair(1 if on else 0)

@@ -81,6 +81,97 @@ def test_gemm_bf16_tcgen05(M, N, Kd, majors):
     assert max_rel(h(C), 2 * ref) < 1e-4
 
 
+@pytest.mark.parametrize("M,N,Kd", [(512, 512, 4160), (296, 320, 4200), (2048, 2048, 2048)])
+@pytest.mark.parametrize("majors", [(1, 1), (1, 0), (0, 0)])
+def test_gemm_stream_k(M, N, Kd, majors):
+    """Shapes whose whole tiles under-fill the SMs take the stream-K schedule
+    (split tiles summed from per-CTA partials in a fixed order): matches fp64,
+    matches the data-parallel schedule to fp32 rounding, and is bit-identical
+    run to run (fp32 store, fp32 accumulate, bias and dGELU epilogues)."""
+    ak, bk = majors
+    k = K()
+    rng = np.random.default_rng(M * 7 + Kd)
+    A = rng.standard_normal((M, Kd)).astype(np.float32)
+    B = rng.standard_normal((N, Kd)).astype(np.float32)
+    At = t(A if ak else A.T.copy(), "bf16")
+    Bt = t(B if bk else B.T.copy(), "bf16")
+    ref = h(At if ak else At.T) @ h(Bt if bk else Bt.T).T
+    bias = t(rng.standard_normal(N), "bf16")
+    U = t(rng.standard_normal((M, N)), "bf16")
+    args = (M, N, Kd, At, Kd if ak else M, ak, Bt, Kd if bk else N, bk)
+
+    def run():
+        C = torch.zeros((M, N), device=dev, dtype=torch.float32)
+        k.tpipe_k_gemm(1, *args, k.EPI_STORE_F32, C, N)
+        Acc = torch.ones((M, N), device=dev, dtype=torch.float32)
+        k.tpipe_k_gemm(1, *args, k.EPI_ACC_F32, Acc, N)
+        Cb = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
+        k.tpipe_k_gemm(1, *args, k.EPI_BIAS, Cb, N, bias=bias)
+        Cd = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
+        Cg = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
+        k.tpipe_k_gemm(1, *args, k.EPI_DGELU, Cd, N, C2=Cg, ldc2=N, aux=U, ldaux=N)
+        torch.cuda.synchronize()
+        return C, Acc, Cb, Cd
+    try:
+        k.tpipe_k_gemm_set_stream_k(1)
+        r1 = run()
+        r2 = run()
+        k.tpipe_k_gemm_set_stream_k(0)
+        dp = run()
+    finally:
+        k.tpipe_k_gemm_set_stream_k(0)
+    for u, v in zip(r1, r2):
+        assert torch.equal(u, v)
+    C, Acc, Cb, Cd = r1
+    assert max_rel(h(C), ref) < 1e-4
+    assert max_rel(h(Acc), 1 + ref) < 1e-4
+    assert rel_l2(h(Cb), ref + h(bias)) < 1e-2
+    assert rel_l2(h(Cd), ref * R.gelu_grad(h(U))) < 1e-2
+    assert max_rel(h(C), h(dp[0])) < 1e-5
+
+
+@pytest.mark.parametrize("M,N,Kd", [(2048, 6144, 2048), (2000, 2080, 4200), (4096, 2816, 520)])
+@pytest.mark.parametrize("majors", [(1, 1), (1, 0), (0, 0)])
+def test_gemm_cta_pair(M, N, Kd, majors):
+    """CTA-pair (cta_group::2, 256 x 256) tiles incl. ragged M/N edges: matches
+    fp64 and the single-CTA kernel (pair off) for fp32 store,
+    fp32 accumulate and the bf16 dGELU epilogue."""
+    ak, bk = majors
+    k = K()
+    rng = np.random.default_rng(M + 3 * N + Kd)
+    A = rng.standard_normal((M, Kd)).astype(np.float32)
+    B = rng.standard_normal((N, Kd)).astype(np.float32)
+    At = t(A if ak else A.T.copy(), "bf16")
+    Bt = t(B if bk else B.T.copy(), "bf16")
+    ref = h(At if ak else At.T) @ h(Bt if bk else Bt.T).T
+    U = t(rng.standard_normal((M, N)), "bf16")
+    args = (M, N, Kd, At, Kd if ak else M, ak, Bt, Kd if bk else N, bk)
+
+    def run():
+        C = torch.zeros((M, N), device=dev, dtype=torch.float32)
+        k.tpipe_k_gemm(1, *args, k.EPI_STORE_F32, C, N)
+        Acc = torch.full((M, N), 2.0, device=dev, dtype=torch.float32)
+        k.tpipe_k_gemm(1, *args, k.EPI_ACC_F32, Acc, N)
+        Cd = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
+        Cg = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
+        k.tpipe_k_gemm(1, *args, k.EPI_DGELU, Cd, N, C2=Cg, ldc2=N, aux=U, ldaux=N)
+        torch.cuda.synchronize()
+        return C, Acc, Cd, Cg
+    pair = run()
+    try:
+        k.tpipe_k_gemm_set_pair(0)
+        single = run()
+    finally:
+        k.tpipe_k_gemm_set_pair(1)
+    C, Acc, Cd, Cg = pair
+    assert max_rel(h(C), ref) < 1e-4
+    assert max_rel(h(Acc), 2 + ref) < 1e-4
+    assert rel_l2(h(Cd), ref * R.gelu_grad(h(U))) < 1e-2
+    assert rel_l2(h(Cg), R.gelu(h(U))) < 1e-2
+    assert max_rel(h(C), h(single[0])) < 1e-5
+    assert max_rel(h(Acc), h(single[1])) < 1e-5
+
+
 @pytest.mark.parametrize("dtype", ["bf16", "fp32"])
 def test_gemm_epilogues(dtype):
     """bias / residual / GELU / dGELU epilogues vs fp64 definitions."""
