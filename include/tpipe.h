@@ -220,6 +220,14 @@ int tpipe_runtime_get_stats(const tpipe_runtime* rt, tpipe_runtime_stats* out);
 /* CUDA stream the runtime launches compute on (cudaStream_t), for event timing */
 void* tpipe_runtime_stream(const tpipe_runtime* rt);
 
+/* Run each layer backward's weight-gradient GEMMs (and the LayerNorm
+ * recomputes feeding them) on a side stream concurrent with the data-gradient
+ * chain (1, default) or everything on the compute stream (0). Process-wide;
+ * results are bit-identical either way (every output has one writer and the
+ * fp32 accumulations keep their order); forced off while TPIPE_STEP_PROFILE
+ * times kernel classes. */
+void tpipe_set_side_stream(int on);
+
 /* 128-byte ncclUniqueId (for stage >= 0 runtimes); TPIPE_E_NCCL if NCCL absent */
 int tpipe_nccl_unique_id(void* out128);
 

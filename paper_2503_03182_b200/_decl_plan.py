@@ -82,3 +82,5 @@ def declare(L):
         L.tpipe_runtime_stream.argtypes = [vp]
         L.tpipe_runtime_stream.restype = vp
         L.tpipe_nccl_unique_id.argtypes = [vp]
+        L.tpipe_set_side_stream.argtypes = [i32]
+        L.tpipe_set_side_stream.restype = None

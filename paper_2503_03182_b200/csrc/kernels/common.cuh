@@ -43,6 +43,31 @@ __device__ __forceinline__ float gelu_tanh_grad(float u) {
     return __fadd_rn(__fmul_rn(0.5f, __fadd_rn(1.0f, t)), __fmul_rn(__fmul_rn(0.5f, u), dt));
 }
 
+// bf16 tensor-core epilogues: GELU / GELU' with the hardware tanh
+// (tanh.approx.f32, rel. error ~2^-11, far below bf16's 2^-9 rounding), one
+// tanh shared by the value and the derivative. Forward (EPI_BIAS_GELU) and
+// backward recompute (EPI_DGELU) both call gelu_fast on the same bf16 u, so
+// the recomputed activation is bit-identical to the stored one.
+__device__ __forceinline__ float tanh_fast(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float gelu_fast(float u) {
+    const float c = 0.7978845608028654f;
+    const float t = tanh_fast(__fmul_rn(c, __fadd_rn(u, __fmul_rn(0.044715f, __fmul_rn(__fmul_rn(u, u), u)))));
+    return __fmul_rn(__fmul_rn(0.5f, u), __fadd_rn(1.0f, t));
+}
+__device__ __forceinline__ void gelu_fast_and_grad(float u, float& g, float& dg) {
+    const float c = 0.7978845608028654f;
+    const float u2 = __fmul_rn(u, u);
+    const float t = tanh_fast(__fmul_rn(c, __fadd_rn(u, __fmul_rn(0.044715f, __fmul_rn(u2, u)))));
+    g = __fmul_rn(__fmul_rn(0.5f, u), __fadd_rn(1.0f, t));
+    const float dt = __fmul_rn(__fmul_rn(__fsub_rn(1.0f, __fmul_rn(t, t)), c),
+                               __fadd_rn(1.0f, __fmul_rn(0.134145f, u2)));
+    dg = __fadd_rn(__fmul_rn(0.5f, __fadd_rn(1.0f, t)), __fmul_rn(__fmul_rn(0.5f, u), dt));
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

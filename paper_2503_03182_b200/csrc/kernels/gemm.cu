@@ -269,7 +269,7 @@ __device__ __forceinline__ void epi_math(const GemmDesc& g, long m, long n0, boo
     }
     if (epi == EPI_BIAS_GELU) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v2[j] = gelu_tanh(rnd<bf16>(v[j]));
+        for (int j = 0; j < 32; ++j) v2[j] = gelu_fast(rnd<bf16>(v[j]));
     }
     if (epi == EPI_DGELU) {
         float u[32];
@@ -281,8 +281,9 @@ __device__ __forceinline__ void epi_math(const GemmDesc& g, long m, long n0, boo
         }
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-            v2[j] = gelu_tanh(u[j]);
-            v[j] = v[j] * gelu_tanh_grad(u[j]);
+            float gd;
+            gelu_fast_and_grad(u[j], v2[j], gd);
+            v[j] = v[j] * gd;
         }
     }
 }

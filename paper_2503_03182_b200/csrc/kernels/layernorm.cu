@@ -103,12 +103,12 @@ __global__ void ln_fwd_kernel(const T* __restrict__ x, const T* __restrict__ gam
 }
 
 // ---------------------------------------------------------------- wide-row path
-// bf16, h % 256 == 0, h <= 4096: one thread per 16-byte vector of a row
-// (tpr = h/8 threads form a "row group"; a CTA holds G row groups working on
-// different rows at once, each prefetching its next row), reductions in a
-// fixed order (deterministic). Partial-block layout: RB rows per CTA.
+// bf16, h % 256 == 0, h <= 4096. Forward: a warp per register-resident row.
+// Backward: a CTA per RB-row block, rows staged in shared memory by bulk
+// copies; a "row group" of tpr = h/8 threads (one 16-byte vector each) works
+// on one row, G row groups per CTA; reductions in a fixed order
+// (deterministic). Partial-block layout: RB rows per CTA.
 constexpr int RB = 16;        // rows per CTA in the backward / column-sum kernels
-constexpr int FWD_RPC = 8;    // rows per CTA in the forward kernel
 constexpr int WIDE_THREADS = 512;
 
 // Sum of (a, b) over the tpr threads of row group `grp` (named barrier 1+grp).
@@ -137,150 +137,6 @@ __device__ __forceinline__ void unpack8(const uint4& u, float (&o)[8]) {
     const bf16* hp = reinterpret_cast<const bf16*>(&u);
 #pragma unroll
     for (int j = 0; j < 8; ++j) o[j] = __bfloat162float(hp[j]);
-}
-
-// y = LN(x): FWD_RPC rows per CTA, row group grp takes rows r0+grp, r0+grp+G, ...
-__global__ void __launch_bounds__(WIDE_THREADS)
-ln_fwd_wide_kernel(const bf16* __restrict__ x, const bf16* __restrict__ gamma,
-                   const bf16* __restrict__ beta, bf16* __restrict__ y, float* __restrict__ mean,
-                   float* __restrict__ rstd, int rows, int h, int apply_only) {
-    __shared__ float red[4][32][2];
-    const int tpr = h >> 3, G = blockDim.x / tpr, grp = threadIdx.x / tpr;
-    const int c = (threadIdx.x % tpr) * 8;
-    const int r0 = blockIdx.x * FWD_RPC, r1 = min(rows, r0 + FWD_RPC);
-    float g[8], b[8];
-    Vec<bf16>::load(gamma + c, g);
-    Vec<bf16>::load(beta + c, b);
-    int r = r0 + grp;
-    uint4 cur = make_uint4(0, 0, 0, 0);
-    if (r < r1) ld8(x + (long)r * h + c, cur);
-    for (; r < r1; r += G) {
-        uint4 nxt = make_uint4(0, 0, 0, 0);
-        if (r + G < r1) ld8(x + (long)(r + G) * h + c, nxt);
-        float v[8], o[8];
-        unpack8(cur, v);
-        float mu, rs;
-        if (!apply_only) {
-            float s = 0.f, dummy = 0.f;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) s += v[j];
-            group_sum2(s, dummy, red[grp], grp, tpr);
-            mu = s / (float)h;
-            float q = 0.f;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const float d = v[j] - mu;
-                q += d * d;
-            }
-            group_sum2(q, dummy, red[grp], grp, tpr);
-            rs = 1.0f / sqrtf(q / (float)h + LN_EPS);
-            if (threadIdx.x % tpr == 0) {
-                mean[r] = mu;
-                rstd[r] = rs;
-            }
-        } else {
-            mu = mean[r];
-            rs = rstd[r];
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) o[j] = ln_y(v[j], mu, rs, g[j], b[j]);
-        Vec<bf16>::store(y + (long)r * h + c, o);
-        cur = nxt;
-    }
-}
-
-// dx = resid + rstd (dxhat - mean(dxhat) - xhat mean(dxhat xhat)); per CTA (RB
-// rows) partials into ws[k][nblk][h]: k=0 dgamma, k=1 dbeta, k=2 (if
-// with_rsum) the column sum of resid — the bias gradient of the linear layer
-// whose output gradient resid is, fused here to save one pass over it.
-// Row groups combine their partials in group order through shared memory.
-__global__ void __launch_bounds__(WIDE_THREADS)
-ln_bwd_wide_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
-                   const bf16* __restrict__ gamma, const float* __restrict__ mean,
-                   const float* __restrict__ rstd, const bf16* __restrict__ resid,
-                   bf16* __restrict__ dx, float* __restrict__ ws, int rows, int h, int nblk,
-                   int with_rsum) {
-    __shared__ float red[4][32][2];
-    extern __shared__ float buf[];          // [3][h] when G > 1
-    const int tpr = h >> 3, G = blockDim.x / tpr, grp = threadIdx.x / tpr;
-    const int c = (threadIdx.x % tpr) * 8;
-    float g[8], pg[8] = {}, pb[8] = {}, pr[8] = {};
-    Vec<bf16>::load(gamma + c, g);
-    const int r0 = blockIdx.x * RB, r1 = min(rows, r0 + RB);
-    int r = r0 + grp;
-    uint4 cd = make_uint4(0, 0, 0, 0), cx = cd, cr = cd;
-    if (r < r1) {
-        ld8(dy + (long)r * h + c, cd);
-        ld8(x + (long)r * h + c, cx);
-        if (resid) ld8(resid + (long)r * h + c, cr);
-    }
-    for (; r < r1; r += G) {
-        uint4 nd = make_uint4(0, 0, 0, 0), nx = nd, nr = nd;
-        if (r + G < r1) {
-            const long o2 = (long)(r + G) * h + c;
-            ld8(dy + o2, nd);
-            ld8(x + o2, nx);
-            if (resid) ld8(resid + o2, nr);
-        }
-        float d[8], v[8], rr[8];
-        unpack8(cd, d);
-        unpack8(cx, v);
-        unpack8(cr, rr);
-        const float mu = mean[r], rs = rstd[r];
-        float xh[8], dxh[8], s1 = 0.f, s2 = 0.f;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            xh[j] = (v[j] - mu) * rs;
-            dxh[j] = d[j] * g[j];
-            s1 += dxh[j];
-            s2 += dxh[j] * xh[j];
-            pg[j] += d[j] * xh[j];
-            pb[j] += d[j];
-            pr[j] += rr[j];
-        }
-        group_sum2(s1, s2, red[grp], grp, tpr);
-        const float c1 = s1 / (float)h, c2 = s2 / (float)h;
-        float o[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) o[j] = rs * (dxh[j] - c1 - xh[j] * c2) + (resid ? rr[j] : 0.f);
-        Vec<bf16>::store(dx + (long)r * h + c, o);
-        cd = nd;
-        cx = nx;
-        cr = nr;
-    }
-    // combine row groups in fixed order: p_0 + (p_1 + (... + p_{G-1}))
-    for (int k = G - 1; k >= 1; --k) {
-        if (grp == k) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const bool first = (k == G - 1);
-                buf[c + j] = first ? pg[j] : pg[j] + buf[c + j];
-                buf[h + c + j] = first ? pb[j] : pb[j] + buf[h + c + j];
-                buf[2 * h + c + j] = first ? pr[j] : pr[j] + buf[2 * h + c + j];
-            }
-        }
-        __syncthreads();
-    }
-    if (grp != 0) return;
-    if (G > 1) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            pg[j] += buf[c + j];
-            pb[j] += buf[h + c + j];
-            pr[j] += buf[2 * h + c + j];
-        }
-    }
-    float* wg = ws + (long)blockIdx.x * h + c;
-    float* wb = ws + (long)(nblk + blockIdx.x) * h + c;
-    *reinterpret_cast<float4*>(wg) = make_float4(pg[0], pg[1], pg[2], pg[3]);
-    *reinterpret_cast<float4*>(wg + 4) = make_float4(pg[4], pg[5], pg[6], pg[7]);
-    *reinterpret_cast<float4*>(wb) = make_float4(pb[0], pb[1], pb[2], pb[3]);
-    *reinterpret_cast<float4*>(wb + 4) = make_float4(pb[4], pb[5], pb[6], pb[7]);
-    if (with_rsum) {
-        float* wr = ws + (long)(2 * nblk + blockIdx.x) * h + c;
-        *reinterpret_cast<float4*>(wr) = make_float4(pr[0], pr[1], pr[2], pr[3]);
-        *reinterpret_cast<float4*>(wr + 4) = make_float4(pr[4], pr[5], pr[6], pr[7]);
-    }
 }
 
 // per-CTA (RB rows) column partial sums of X[rows, n] into ws[nblk][n]; a CTA
@@ -364,6 +220,199 @@ reduce_parts_kernel(const float* __restrict__ ws, float* __restrict__ out0, floa
     }
 }
 
+// ---------------------------------------------------------------- warp-per-row forward
+// bf16, h = 256*NV: one warp per row, the whole row register-resident (NV
+// 16-byte vectors per lane, all loads issued before any use), warp-shuffle
+// reductions only (no block barriers), so every row of the launch is in
+// flight at once. mean first, then the centred second moment from registers.
+template <int NV>
+__global__ void __launch_bounds__(256)
+ln_fwd_warp_kernel(const bf16* __restrict__ x, const bf16* __restrict__ gamma,
+                   const bf16* __restrict__ beta, bf16* __restrict__ y, float* __restrict__ mean,
+                   float* __restrict__ rstd, int rows, int apply_only) {
+    constexpr int h = NV * 256;
+    const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const bf16* xr = x + (long)row * h;
+    uint4 u[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) ld8(xr + (i * 32 + lane) * 8, u[i]);
+    float mu, rs;
+    if (!apply_only) {
+        float s = 0.f;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            float v[8];
+            unpack8(u[i], v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) s += v[j];
+        }
+        mu = warp_sum(s) / (float)h;
+        float q = 0.f;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            float v[8];
+            unpack8(u[i], v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float d = v[j] - mu;
+                q += d * d;
+            }
+        }
+        rs = 1.0f / sqrtf(warp_sum(q) / (float)h + LN_EPS);
+        if (lane == 0) {
+            mean[row] = mu;
+            rstd[row] = rs;
+        }
+    } else {
+        mu = mean[row];
+        rs = rstd[row];
+    }
+    bf16* yr = y + (long)row * h;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        const int c = (i * 32 + lane) * 8;
+        float v[8], g[8], b[8], o[8];
+        unpack8(u[i], v);
+        Vec<bf16>::load(gamma + c, g);
+        Vec<bf16>::load(beta + c, b);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = ln_y(v[j], mu, rs, g[j], b[j]);
+        Vec<bf16>::store(yr + c, o);
+    }
+}
+
+template <int NV>
+static void launch_ln_fwd_warp(const bf16* x, const bf16* g, const bf16* b, bf16* y, float* mean, float* rstd,
+                               int rows, int apply_only, cudaStream_t st) {
+    ln_fwd_warp_kernel<NV><<<(rows + 7) / 8, 256, 0, st>>>(x, g, b, y, mean, rstd, rows, apply_only);
+}
+
+static int ln_fwd_warp(const bf16* x, const bf16* g, const bf16* b, bf16* y, float* mean, float* rstd, int rows,
+                       int h, int apply_only, cudaStream_t st) {
+    switch (h / 256) {
+#define TP_LNW(NV) \
+    case NV: launch_ln_fwd_warp<NV>(x, g, b, y, mean, rstd, rows, apply_only, st); return 0;
+        TP_LNW(1) TP_LNW(2) TP_LNW(3) TP_LNW(4) TP_LNW(5) TP_LNW(6) TP_LNW(7) TP_LNW(8)
+        TP_LNW(9) TP_LNW(10) TP_LNW(11) TP_LNW(12) TP_LNW(13) TP_LNW(14) TP_LNW(15) TP_LNW(16)
+#undef TP_LNW
+        default: return -1;
+    }
+}
+
+// ---------------------------------------------------------------- staged backward
+// One CTA per RB-row block; the block's dy / x / resid rows are fetched with
+// 16-byte cp.async into shared memory in chunks of RC rows, so all of a
+// chunk's bytes are in flight at once; the row groups then work from shared
+// memory.
+constexpr int LNB_SMEM_ROWS_BYTES = 192 * 1024;
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+__global__ void __launch_bounds__(WIDE_THREADS, 1)
+ln_bwd_stage_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
+                    const bf16* __restrict__ gamma, const float* __restrict__ mean,
+                    const float* __restrict__ rstd, const bf16* __restrict__ resid,
+                    bf16* __restrict__ dx, float* __restrict__ ws, int rows, int h, int nblk,
+                    int with_rsum, int RC) {
+    __shared__ float red[4][32][2];
+    __shared__ float smu[RB], srs[RB];
+    extern __shared__ __align__(128) uint8_t smraw[];
+    bf16* sdy = reinterpret_cast<bf16*>(smraw);          // [RC][h]
+    bf16* sx = sdy + (size_t)RC * h;                     // [RC][h]
+    bf16* sr = sx + (size_t)RC * h;                      // [RC][h]
+    float* buf = reinterpret_cast<float*>(smraw);        // [3][h] group combine (after the rows)
+    const int tpr = h >> 3, G = blockDim.x / tpr, grp = threadIdx.x / tpr;
+    const int c = (threadIdx.x % tpr) * 8;
+    const int r0 = blockIdx.x * RB, r1 = min(rows, r0 + RB);
+    if (threadIdx.x < RB && r0 + threadIdx.x < r1) {   // row statistics off the per-row critical path
+        smu[threadIdx.x] = mean[r0 + threadIdx.x];
+        srs[threadIdx.x] = rstd[r0 + threadIdx.x];
+    }
+    __syncthreads();
+    float g[8], pg[8] = {}, pb[8] = {}, pr[8] = {};
+    Vec<bf16>::load(gamma + c, g);
+    for (int q0 = r0; q0 < r1; q0 += RC) {
+        const int nr = min(RC, r1 - q0);
+        // each thread fetches only the 16-byte slices it will read itself
+        // (cp.async, no registers held), so no CTA barrier is needed before use
+        for (int i = grp; i < nr; i += G) {
+            const long off = (long)(q0 + i) * h + c;
+            cp_async16(sdy + (size_t)i * h + c, dy + off);
+            cp_async16(sx + (size_t)i * h + c, x + off);
+            if (resid) cp_async16(sr + (size_t)i * h + c, resid + off);
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        for (int i = grp; i < nr; i += G) {
+            const int r = q0 + i;
+            float d[8], v[8], rr[8];
+            Vec<bf16>::load(sdy + (size_t)i * h + c, d);
+            Vec<bf16>::load(sx + (size_t)i * h + c, v);
+            if (resid) {
+                Vec<bf16>::load(sr + (size_t)i * h + c, rr);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) rr[j] = 0.f;
+            }
+            const float mu = smu[r - r0], rs = srs[r - r0];
+            float xh[8], dxh[8], s1 = 0.f, s2 = 0.f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                xh[j] = (v[j] - mu) * rs;
+                dxh[j] = d[j] * g[j];
+                s1 += dxh[j];
+                s2 += dxh[j] * xh[j];
+                pg[j] += d[j] * xh[j];
+                pb[j] += d[j];
+                pr[j] += rr[j];
+            }
+            group_sum2(s1, s2, red[grp], grp, tpr);
+            const float c1 = s1 / (float)h, c2 = s2 / (float)h;
+            float o[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) o[j] = rs * (dxh[j] - c1 - xh[j] * c2) + (resid ? rr[j] : 0.f);
+            Vec<bf16>::store(dx + (long)r * h + c, o);
+        }
+        __syncthreads();   // chunk buffer free for the next chunk / the combine below
+    }
+    // combine row groups in fixed order: p_0 + (p_1 + (... + p_{G-1}))
+    for (int k = G - 1; k >= 1; --k) {
+        if (grp == k) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const bool first = (k == G - 1);
+                buf[c + j] = first ? pg[j] : pg[j] + buf[c + j];
+                buf[h + c + j] = first ? pb[j] : pb[j] + buf[h + c + j];
+                buf[2 * h + c + j] = first ? pr[j] : pr[j] + buf[2 * h + c + j];
+            }
+        }
+        __syncthreads();
+    }
+    if (grp != 0) return;
+    if (G > 1) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            pg[j] += buf[c + j];
+            pb[j] += buf[h + c + j];
+            pr[j] += buf[2 * h + c + j];
+        }
+    }
+    float* wg = ws + (long)blockIdx.x * h + c;
+    float* wb = ws + (long)(nblk + blockIdx.x) * h + c;
+    *reinterpret_cast<float4*>(wg) = make_float4(pg[0], pg[1], pg[2], pg[3]);
+    *reinterpret_cast<float4*>(wg + 4) = make_float4(pg[4], pg[5], pg[6], pg[7]);
+    *reinterpret_cast<float4*>(wb) = make_float4(pb[0], pb[1], pb[2], pb[3]);
+    *reinterpret_cast<float4*>(wb + 4) = make_float4(pb[4], pb[5], pb[6], pb[7]);
+    if (with_rsum) {
+        float* wr = ws + (long)(2 * nblk + blockIdx.x) * h + c;
+        *reinterpret_cast<float4*>(wr) = make_float4(pr[0], pr[1], pr[2], pr[3]);
+        *reinterpret_cast<float4*>(wr + 4) = make_float4(pr[4], pr[5], pr[6], pr[7]);
+    }
+}
+
 static int wide_groups(int h) {
     const int tpr = h / 8;
     int G = WIDE_THREADS / tpr;
@@ -377,9 +426,9 @@ int ln_fwd(int dtype, const void* x, const void* gamma, const void* beta, void* 
     if (rows <= 0) return 0;
     if (h % 8) return -1;
     if (wide_ok(dtype, h)) {
-        const int G = wide_groups(h);
-        ln_fwd_wide_kernel<<<(rows + FWD_RPC - 1) / FWD_RPC, G * (h / 8), 0, st>>>(
-            (const bf16*)x, (const bf16*)gamma, (const bf16*)beta, (bf16*)y, mean, rstd, rows, h, 0);
+        if (ln_fwd_warp((const bf16*)x, (const bf16*)gamma, (const bf16*)beta, (bf16*)y, mean, rstd, rows, h, 0,
+                        st))
+            return -1;
         note_launches(1);
         return cudaGetLastError() == cudaSuccess ? 0 : -3;
     }
@@ -398,10 +447,9 @@ int ln_apply(int dtype, const void* x, const void* gamma, const void* beta, cons
              const float* rstd, void* y, int rows, int h, cudaStream_t st) {
     if (rows <= 0) return 0;
     if (wide_ok(dtype, h)) {
-        const int G = wide_groups(h);
-        ln_fwd_wide_kernel<<<(rows + FWD_RPC - 1) / FWD_RPC, G * (h / 8), 0, st>>>(
-            (const bf16*)x, (const bf16*)gamma, (const bf16*)beta, (bf16*)y, const_cast<float*>(mean),
-            const_cast<float*>(rstd), rows, h, 1);
+        if (ln_fwd_warp((const bf16*)x, (const bf16*)gamma, (const bf16*)beta, (bf16*)y, const_cast<float*>(mean),
+                        const_cast<float*>(rstd), rows, h, 1, st))
+            return -1;
         note_launches(1);
         return cudaGetLastError() == cudaSuccess ? 0 : -3;
     }
@@ -503,9 +551,19 @@ int ln_bwd(int dtype, const void* dy, const void* x, const void* gamma, const fl
         const int nb = (rows + RB - 1) / RB;
         const int G = wide_groups(h);
         const int rs = dresid_sum ? 1 : 0;
-        ln_bwd_wide_kernel<<<nb, G * (h / 8), G > 1 ? 3 * h * sizeof(float) : 0, st>>>(
-            (const bf16*)dy, (const bf16*)x, (const bf16*)gamma, mean, rstd, (const bf16*)resid,
-            (bf16*)dx, ws, rows, h, nb, rs);
+        // rows staged per chunk: all RB rows of the three inputs when they fit
+        int RC = LNB_SMEM_ROWS_BYTES / (3 * h * 2);
+        if (RC > RB) RC = RB;
+        const size_t smem = (size_t)RC * 3 * h * 2;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(ln_bwd_stage_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 LNB_SMEM_ROWS_BYTES);
+            attr = true;
+        }
+        ln_bwd_stage_kernel<<<nb, G * (h / 8), smem, st>>>((const bf16*)dy, (const bf16*)x, (const bf16*)gamma,
+                                                           mean, rstd, (const bf16*)resid, (bf16*)dx, ws, rows,
+                                                           h, nb, rs, RC);
         reduce_parts_kernel<<<dim3((h + 31) / 32, 2 + rs), 256, 0, st>>>(ws, dgamma, dbeta, dresid_sum,
                                                                          h, nb);
         note_launches(2);

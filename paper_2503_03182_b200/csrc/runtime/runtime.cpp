@@ -777,6 +777,8 @@ TP_API int tpipe_runtime_get_stats(const tpipe_runtime* rt, tpipe_runtime_stats*
 
 TP_API void* tpipe_runtime_stream(const tpipe_runtime* rt) { return rt ? (void*)rt->stream : nullptr; }
 
+TP_API void tpipe_set_side_stream(int on) { stage_set_side_stream(on); }
+
 TP_API int tpipe_nccl_unique_id(void* out128) {
     const NcclApi* N = nccl();
     if (!N) return set_error(TPIPE_E_NCCL, "libnccl.so.2 not loadable");

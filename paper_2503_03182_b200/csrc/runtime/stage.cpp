@@ -14,6 +14,9 @@
 // offload on/off give bit-identical gradients.
 #include "runtime/stage.h"
 
+#include <mutex>
+#include <vector>
+
 #include <array>
 
 namespace tpipe {
@@ -322,23 +325,73 @@ static BwdWs carve_bwd(const Dims& D, uint8_t* ws, bool head, bool emb, long par
     return w;
 }
 
+// Side stream for the backward of a layer: weight-gradient GEMMs (and the LN
+// recomputes that feed them) are independent of the data-gradient chain, so
+// they run concurrently on a second stream and fill the SMs the other
+// chain's last GEMM wave leaves idle (each tcgen05 GEMM is a persistent grid
+// of <= #SMs CTAs; a 2048-multiple shape occupies ~86% of the SM-waves).
+// One side stream + events per compute stream, created on first use.
+struct SideStream {
+    cudaStream_t main = nullptr, aux = nullptr;
+    cudaEvent_t ev[5] = {};
+};
+static SideStream* side_stream(cudaStream_t main) {
+    static std::mutex mu;
+    static std::vector<SideStream*> all;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto* s : all)
+        if (s->main == main) return s;
+    auto* s = new SideStream;
+    s->main = main;
+    if (cudaStreamCreateWithFlags(&s->aux, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    for (auto& e : s->ev)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    all.push_back(s);
+    (void)dev;
+    return s;
+}
+static bool g_side_stream_enabled = true;
+void stage_set_side_stream(int on) { g_side_stream_enabled = on != 0; }
+
+// `b` waits for everything issued so far on `a`
+static int stream_dep(cudaStream_t a, cudaStream_t b, cudaEvent_t e) {
+    if (a == b) return 0;
+    if (cudaEventRecord(e, a) != cudaSuccess) return -3;
+    return cudaStreamWaitEvent(b, e, 0) == cudaSuccess ? 0 : -3;
+}
+
 // backward of one layer: dy -> dx (dx may alias G0 == dy buffer: dy is fully
 // consumed before the LN1 backward writes dx)
+//   main: fc2 dgrad | colsum b1, fc1 dgrad, LN2 bwd (+b2) | out dgrad, attn bwd
+//         | colsum bqkv, qkv dgrad, LN1 bwd (+bo) | join
+//   aux : (after fc2 dgrad) fc2 wgrad, LN2 apply, fc1 wgrad, LN1 apply
+//         | (after LN2 bwd) out wgrad | (after attn bwd) qkv wgrad
+// Every buffer is written and read on one stream or ordered by an event
+// (the partial-sum workspace is used on main only; dy is read by fc2 wgrad on
+// aux before LN1 bwd overwrites it on main: ev[2]).
 static int layer_backward(const Dims& D, const LW& W, const LayerPtrs& lp, const void* dy, void* dx,
                           const BwdWs& w, cudaStream_t st) {
     const int M = D.M, h = D.h, f = D.f, dt = D.dtype;
+    SideStream* ss = (g_side_stream_enabled && !profiler().on) ? side_stream(st) : nullptr;
+    const cudaStream_t ax = ss ? ss->aux : st;
+    cudaEvent_t* ev = ss ? ss->ev : nullptr;
     // FC2: dg = dy W2 (dGELU fused: du = dg * gelu'(u), g = gelu(u) recomputed)
     TRY(mm(D, M, f, h, dy, h, 1, W.w[W_2], f, 0, EPI_DGELU, w.du, f, nullptr, nullptr, 0, w.g, f,
            lp.u, f, st));
+    if (ss) TRY(stream_dep(st, ax, ev[0]));
+    // ---- aux: weight gradients of FC2 / FC1 and the LN recomputes
     TRY(mm(D, h, f, M, dy, h, 0, w.g, f, 0, EPI_ACC_F32, W.g[W_2], f, nullptr, nullptr, 0, nullptr,
-           0, nullptr, 0, st));
-    // FC1
+           0, nullptr, 0, ax));
+    if (ss && cudaEventRecord(ev[1], ax) != cudaSuccess) return -3;   // dy consumed on aux
     {
-        ProfScope _ps(3, 0.0, st);
-        TRY(ln_apply(dt, lp.x_mid, W.w[LN2_G], W.w[LN2_B], lp.ln2_mean, lp.ln2_rstd, w.ln, M, h, st));
+        ProfScope _ps(3, 0.0, ax);
+        TRY(ln_apply(dt, lp.x_mid, W.w[LN2_G], W.w[LN2_B], lp.ln2_mean, lp.ln2_rstd, w.ln, M, h, ax));
     }
     TRY(mm(D, f, h, M, w.du, f, 0, w.ln, h, 0, EPI_ACC_F32, W.g[W_1], h, nullptr, nullptr, 0,
-           nullptr, 0, nullptr, 0, st));
+           nullptr, 0, nullptr, 0, ax));
+    // ---- main: data-gradient chain
     {
         ProfScope _ps(3, 0.0, st);
         TRY(colsum_acc(dt, w.du, W.g[B_1], w.part, M, f, st));
@@ -351,36 +404,43 @@ static int layer_backward(const Dims& D, const LW& W, const LayerPtrs& lp, const
         TRY(ln_bwd(dt, w.dln, lp.x_mid, W.w[LN2_G], lp.ln2_mean, lp.ln2_rstd, dy, w.G1, W.g[LN2_G],
                    W.g[LN2_B], w.part, M, h, st, W.g[B_2]));
     }
-    // out-proj
+    // aux (in order after FC1 wgrad, so w.ln is free): LN1 recompute; then,
+    // once G1 exists, the out-proj weight gradient
+    {
+        ProfScope _ps(3, 0.0, ax);
+        TRY(ln_apply(dt, lp.x_in, W.w[LN1_G], W.w[LN1_B], lp.ln1_mean, lp.ln1_rstd, w.ln, M, h, ax));
+    }
+    if (ss) TRY(stream_dep(st, ax, ev[2]));
     TRY(mm(D, h, h, M, w.G1, h, 0, lp.o, h, 0, EPI_ACC_F32, W.g[W_O], h, nullptr, nullptr, 0,
-           nullptr, 0, nullptr, 0, st));
+           nullptr, 0, nullptr, 0, ax));
+    // main: out-proj dgrad, attention backward (P recomputed from LSE)
     TRY(mm(D, M, h, h, w.G1, h, 1, W.w[W_O], h, 0, EPI_STORE, w.dout, h, nullptr, nullptr, 0,
            nullptr, 0, nullptr, 0, st));
-    // attention (P recomputed from LSE)
     {
         // algorithmic: P recompute + dV, dP, dQ, dK = 5 GEMMs over the causal triangle
         ProfScope ps(2, 10.0 * D.b * D.a * (0.5 * D.s * (D.s + 1)) * D.hd, st);
         TRY(attn_bwd(dt, lp.qkv, lp.o, w.dout, lp.lse, w.dqkv, w.Dv, D.b, D.s, D.a, D.hd, st));
     }
-    // QKV
-    {
-        ProfScope _ps(3, 0.0, st);
-        TRY(ln_apply(dt, lp.x_in, W.w[LN1_G], W.w[LN1_B], lp.ln1_mean, lp.ln1_rstd, w.ln, M, h, st));
-    }
+    if (ss) TRY(stream_dep(st, ax, ev[3]));
+    // aux: QKV weight gradient
     TRY(mm(D, 3 * h, h, M, w.dqkv, 3 * h, 0, w.ln, h, 0, EPI_ACC_F32, W.g[W_QKV], h, nullptr,
-           nullptr, 0, nullptr, 0, nullptr, 0, st));
+           nullptr, 0, nullptr, 0, nullptr, 0, ax));
+    // main: QKV bias / dgrad, LN1 backward
     {
         ProfScope _ps(3, 0.0, st);
         TRY(colsum_acc(dt, w.dqkv, W.g[B_QKV], w.part, M, 3 * h, st));
     }
     TRY(mm(D, M, h, 3 * h, w.dqkv, 3 * h, 1, W.w[W_QKV], h, 0, EPI_STORE, w.dln, h, nullptr,
            nullptr, 0, nullptr, 0, nullptr, 0, st));
+    if (ss && cudaStreamWaitEvent(st, ev[1], 0) != cudaSuccess) return -3;   // dx may alias dy
     {
         ProfScope _ps(3, 0.0, st);
         // + dBo = colsum(G1), fused (G1 is LN1's residual-branch gradient)
         TRY(ln_bwd(dt, w.dln, lp.x_in, W.w[LN1_G], lp.ln1_mean, lp.ln1_rstd, w.G1, dx, W.g[LN1_G],
                    W.g[LN1_B], w.part, M, h, st, W.g[B_O]));
     }
+    // join: the layer's gradients are complete and w.* free for the next layer
+    if (ss) TRY(stream_dep(ax, st, ev[4]));
     return 0;
 }
 

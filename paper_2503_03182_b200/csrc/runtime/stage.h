@@ -101,6 +101,9 @@ KernelProfiler& profiler();
 
 int chunk_forward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P, const FwdArgs& a,
                   cudaStream_t st);
+// layer backward: run weight-gradient GEMMs on a side stream (default on;
+// always off while TPIPE_STEP_PROFILE is timing kernel classes)
+void stage_set_side_stream(int on);
 int chunk_backward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P, const BwdArgs& a,
                    cudaStream_t st);
 

@@ -113,6 +113,35 @@ def test_trecomp_bitexact_vs_tpipe(dtype):
         assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
 
 
+C_MID = dict(n_layers=4, hidden=256, n_heads=2, ffn_hidden=1024, vocab=512, seq_len=256, micro_batch=1)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C_MID"])
+@pytest.mark.parametrize("dtype", [0, 1])
+def test_side_stream_bitexact(cfg, dtype):
+    """Weight-gradient GEMMs on the side stream vs all on one stream: loss,
+    gradients and updated parameters bit-identical (C_MID exercises the
+    tcgen05 GEMM / attention kernels in bf16)."""
+    _P, RT, _PR = mods()
+    c = C1 if cfg == "C1" else C_MID
+    p, m = 2, 4
+    res = []
+    try:
+        for side in (1, 0):
+            RT.set_side_stream(side)
+            plan, rt, _W = build(c, p, m, "tpipe", dtype)
+            tok, tgt = synth.tokens(c["vocab"], m, c["micro_batch"], c["seq_len"], step=1)
+            loss = rt.step(tok, tgt, RT.STEP_NO_OPT)
+            grads = [rt.get_grads(s, ch) for s in range(p) for ch in (1, 2)]
+            loss2 = rt.step(tok, tgt)
+            res.append((loss, loss2, grads, [rt.get_params(s, ch) for s in range(p) for ch in (1, 2)]))
+    finally:
+        RT.set_side_stream(1)
+    assert res[0][0] == res[1][0] and res[0][1] == res[1][1]
+    for a, b in zip(res[0][2] + res[0][3], res[1][2] + res[1][3]):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
 @pytest.mark.parametrize("dtype", [0, 1])
 def test_offload_bitexact(dtype):
     """T-Offload (host AdamW for chunk 2) vs device AdamW: parameters
