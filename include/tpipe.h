@@ -228,6 +228,13 @@ void* tpipe_runtime_stream(const tpipe_runtime* rt);
  * times kernel classes. */
 void tpipe_set_side_stream(int on);
 
+/* Launch the bf16 hot-path kernels (tcgen05 GEMMs and attention, LayerNorm,
+ * column sums) with programmatic dependent launch (1, default; env TPIPE_PDL=0
+ * starts with 0): a kernel's prologue overlaps its predecessor's drain and it
+ * waits (griddepcontrol.wait) before touching global memory, so results are
+ * bit-identical either way. Process-wide. */
+void tpipe_set_pdl(int on);
+
 /* 128-byte ncclUniqueId (for stage >= 0 runtimes); TPIPE_E_NCCL if NCCL absent */
 int tpipe_nccl_unique_id(void* out128);
 

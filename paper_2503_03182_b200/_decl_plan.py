@@ -84,3 +84,5 @@ def declare(L):
         L.tpipe_nccl_unique_id.argtypes = [vp]
         L.tpipe_set_side_stream.argtypes = [i32]
         L.tpipe_set_side_stream.restype = None
+        L.tpipe_set_pdl.argtypes = [i32]
+        L.tpipe_set_pdl.restype = None

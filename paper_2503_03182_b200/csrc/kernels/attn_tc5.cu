@@ -175,6 +175,8 @@ __global__ void __launch_bounds__(384, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();
+    pdl_trigger();
     const uint32_t tO = tmem + 256;
 
     if (warp == 0) {
@@ -461,6 +463,8 @@ __global__ void __launch_bounds__(384, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();
+    pdl_trigger();
     const uint32_t tdV = tmem + 256, tdK = tmem + 256 + D;   // D <= 128
 
     if (warp == 0) {
@@ -704,6 +708,8 @@ __global__ void __launch_bounds__(384, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();
+    pdl_trigger();
     const uint32_t tdQ = tmem + 256;
 
     if (warp == 0) {
@@ -860,6 +866,8 @@ __global__ void d_kernel(const bf16* __restrict__ o, const bf16* __restrict__ do
     const int lane = threadIdx.x & 31;
     const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int head = blockIdx.y, b = blockIdx.z;
+    pdl_wait();
+    pdl_trigger();
     if (i >= s) return;
     const long off = ((long)b * s + i) * a * d + head * d;
     float part = 0.f;
@@ -929,7 +937,9 @@ static int fwd5(const void* qkv, void* o, float* lse, int b, int s, int a, cudaS
     CUtensorMap m;
     if (map2d(&m, qkv, 3L * a * D, (long)b * s, 3L * a * D)) return -2;
     const int grid = persistent_grid(((s + 127) / 128) * a * b);
-    fa5::fwd2_kernel<D><<<grid, 384, smem, st>>>(m, (bf16*)o, lse, s, a, b);
+    if (launch_k(fa5::fwd2_kernel<D>, dim3(grid), dim3(384), smem, st, 1, m, (bf16*)o, lse, s, a, b) !=
+        cudaSuccess)
+        return -3;
     note_launches(1);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
@@ -953,10 +963,16 @@ static int bwd5(const void* qkv, const void* o, const void* dout, const float* l
     if (map2d(&md, dout, (long)a * D, (long)b * s, (long)a * D)) return -2;
     if (map2d(&md64, dout, (long)a * D, (long)b * s, (long)a * D, 64)) return -2;
     dim3 gd((s + 3) / 4, a, b);
-    fa5::d_kernel<<<gd, 128, 0, st>>>((const bf16*)o, (const bf16*)dout, ws, s, a, D);
+    if (launch_k(fa5::d_kernel, gd, dim3(128), 0, st, 1, (const bf16*)o, (const bf16*)dout, ws, s, a, D) !=
+        cudaSuccess)
+        return -3;
     const int grid = persistent_grid(((s + 127) / 128) * a * b);
-    fa5::dkdv2_kernel<D><<<grid, 384, smem_kv, st>>>(mq, mq64, md64, lse, ws, (bf16*)dqkv, s, a, b);
-    fa5::dq2_kernel<D><<<grid, 384, smem_q, st>>>(mq, md, mq64, lse, ws, (bf16*)dqkv, s, a, b);
+    if (launch_k(fa5::dkdv2_kernel<D>, dim3(grid), dim3(384), smem_kv, st, 1, mq, mq64, md64, lse,
+                 (const float*)ws, (bf16*)dqkv, s, a, b) != cudaSuccess)
+        return -3;
+    if (launch_k(fa5::dq2_kernel<D>, dim3(grid), dim3(384), smem_q, st, 1, mq, md, mq64, lse, (const float*)ws,
+                 (bf16*)dqkv, s, a, b) != cudaSuccess)
+        return -3;
     note_launches(3);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }

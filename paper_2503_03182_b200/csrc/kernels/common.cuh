@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <utility>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 
@@ -20,6 +21,51 @@ template <> __device__ __forceinline__ bf16 from_f<bf16>(float x) { return __flo
 
 // round a float through the storage type T (identity for float)
 template <typename T> __device__ __forceinline__ float rnd(float x) { return to_f<T>(from_f<T>(x)); }
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// The hot-path kernels (tcgen05 GEMMs, tcgen05 attention, LayerNorm, column
+// sums) are launched with programmatic stream serialisation: a kernel may be
+// scheduled while its predecessor on the stream drains its last CTAs, runs its
+// prologue (barrier init, TMEM alloc, descriptor prefetch) and then blocks in
+// pdl_wait() until the predecessor has completed and its writes are visible.
+// Every such kernel calls pdl_wait() before its first global-memory access
+// (read or write), so stream order semantics are unchanged; pdl_trigger()
+// lets the successor be scheduled early. Without the launch attribute both are
+// no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();
+void set_pdl(int on);
+
+// cudaLaunchKernelEx with the PDL attribute (when enabled) and an optional
+// cluster dimension.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            int cluster, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    unsigned n = 0;
+    if (pdl_enabled()) {
+        at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
+    if (cluster > 1) {
+        at[n].id = cudaLaunchAttributeClusterDimension;
+        at[n].val.clusterDim.x = cluster;
+        at[n].val.clusterDim.y = 1;
+        at[n].val.clusterDim.z = 1;
+        ++n;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = n;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ---------------------------------------------------------------- math
 // GELU, tanh approximation (DESIGN.md §2 reading N-1). Written with explicit

@@ -38,6 +38,16 @@
 
 namespace tpipe {
 
+static int g_pdl = -1;   // -1: from TPIPE_PDL (default on)
+bool pdl_enabled() {
+    if (g_pdl < 0) {
+        const char* e = getenv("TPIPE_PDL");
+        g_pdl = (e && e[0] == '0') ? 0 : 1;
+    }
+    return g_pdl != 0;
+}
+void set_pdl(int on) { g_pdl = on != 0; }
+
 // ============================================================== epilogue
 template <typename T>
 __device__ __forceinline__ void load32(const T* p, float (&o)[32]);
@@ -230,6 +240,14 @@ int gemm_simt(int dtype, const GemmDesc& g, cudaStream_t st) {
 
 // ============================================================== tcgen05 (bf16)
 constexpr int TC_BM = 128, TC_BK = 64;
+// EW = 8 epilogue warps (two warpgroups, warps 4..11) for the math-heavy
+// epilogues (GELU, dGELU, residual): warp w reads TMEM lane quarter w % 4 and
+// column half (w - 4) / 4 of every tile, so the fused math runs on 2 warps per
+// scheduler and stays under the next tile's main loop (with 4 warps it was the
+// critical path of the dGELU GEMM: 775 -> 1029 TFLOP/s). The light epilogues
+// (store, bias, fp32 reduce-add) keep EW = 4 and the deeper operand ring that
+// the smaller staging area leaves room for.
+__host__ __device__ constexpr int tc_threads(int ew) { return 128 + 32 * ew; }
 static bool g_stream_k_enabled = false;   // measured slower on the model shapes
 static bool g_pair_enabled = true;
 void gemm_set_stream_k(int on) { g_stream_k_enabled = on != 0; }
@@ -239,14 +257,15 @@ void gemm_set_pair(int on) { g_pair_enabled = on != 0; }
 // on one TPC) computes a 256 x BN tile with tcgen05.mma.cta_group::2; each CTA
 // stages 128 rows of A and BN/2 rows of B, so per-SM operand traffic (L2->smem
 // and smem->tensor core) is 2/3 of the CG = 1, BN = 256 tile's.
-template <int BN, int CG = 1>
+template <int BN, int CG = 1, int EPI_WARPS = 4>
 struct TcCfg {
-    static constexpr int STAGES = CG == 2 ? 6 : (BN == 256 ? 4 : 6);
+    static constexpr int STAGES = EPI_WARPS == 8 ? (CG == 2 ? 5 : (BN == 256 ? 3 : 5))
+                                                 : (CG == 2 ? 6 : (BN == 256 ? 4 : 6));
     static constexpr int A_BYTES = TC_BM * TC_BK * 2;
     static constexpr int B_BYTES = (BN / CG) * TC_BK * 2;
     static constexpr int TMEM_COLS = 2 * BN;
-    // epilogue staging: 4 warps x 2 buffers x (32 rows x 128 B)
-    static constexpr int STAGING = 4 * 2 * 4096;
+    // epilogue staging: EPI_WARPS warps x 2 buffers x (32 rows x 128 B)
+    static constexpr int STAGING = EPI_WARPS * 2 * 4096;
     static constexpr int SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + STAGING + 256;
 };
 
@@ -400,13 +419,13 @@ __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <int BN, bool A_MN, bool B_MN, int CG>
-__global__ void __launch_bounds__(256, 1)
+template <int BN, bool A_MN, bool B_MN, int CG, int EPI_WARPS>
+__global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
                    const GemmDesc g, int num_m, int num_n, int num_kb, int sk, float* __restrict__ sk_ws,
                    unsigned* __restrict__ sk_flags, unsigned epoch) {
-    using Cfg = TcCfg<BN, CG>;
+    using Cfg = TcCfg<BN, CG, EPI_WARPS>;
     constexpr int STAGES = Cfg::STAGES;
     constexpr int TM = TC_BM * CG;        // tile rows
     constexpr int BNC = BN / CG;          // B rows staged per CTA
@@ -442,7 +461,7 @@ __global__ void __launch_bounds__(256, 1)
         }
         for (int e = 0; e < 2; ++e) {
             mbar_init(&tfull[e], 1);
-            mbar_init(&tempty[e], CG == 2 ? 8 : 128);
+            mbar_init(&tempty[e], CG == 2 ? 2 * EPI_WARPS : 32 * EPI_WARPS);
         }
         fence_mbar_init();
     }
@@ -455,6 +474,8 @@ __global__ void __launch_bounds__(256, 1)
     else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_wait();
+    pdl_trigger();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -554,8 +575,9 @@ __global__ void __launch_bounds__(256, 1)
         }
     } else if (warp >= 4) {
         // ---------------- epilogue: TMEM -> registers -> fused math -> swizzled smem -> TMA
-        const int ew = warp - 4;
-        uint8_t* mystg = stg + ew * 2 * 4096;
+        const int ew = warp & 3;             // TMEM lane quarter = tile rows [32ew, 32ew+32)
+        const int chalf = (warp - 4) >> 2;   // column half of the tile
+        uint8_t* mystg = stg + (warp - 4) * 2 * 4096;
         const bool f32out = (g.epi == EPI_ACC_F32 || g.epi == EPI_STORE_F32);
         const bool reduce = (g.epi == EPI_ACC_F32);
         const bool two = (g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU);
@@ -566,6 +588,8 @@ __global__ void __launch_bounds__(256, 1)
         const long I = (long)num_tiles * num_kb;
         const uint32_t tempty_leader = CG == 2 ? mapa_shared(&tempty[0], 0) : 0;
         const int row = ew * 32 + lane;   // row of the tile this thread owns
+        constexpr int NCH = BN / 32 / (EPI_WARPS / 4);   // 32-column chunks per column group
+        const int c_lo = chalf * NCH, c_hi = c_lo + NCH;
         int tile, kb0, kb1;
         for (; sch.next(tile, kb0, kb1); ++it) {
             const int mb = tile % num_m, nb = tile / num_m;
@@ -580,7 +604,7 @@ __global__ void __launch_bounds__(256, 1)
                 // for a pair each CTA holds its 128 rows), then flag
                 float* slot = sk_ws + (size_t)blockIdx.x * TC_BM * BN;
 #pragma unroll 1
-                for (int c = 0; c < BN / 32; ++c) {
+                for (int c = c_lo; c < c_hi; ++c) {
                     uint32_t r[32];
                     tmem_ld32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + c * 32, r);
                     tmem_wait_ld();
@@ -591,7 +615,7 @@ __global__ void __launch_bounds__(256, 1)
                                                     __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3])));
                 }
                 __threadfence();
-                named_bar_sync(1, 128);
+                named_bar_sync(1, 32 * EPI_WARPS);
                 if (ew == 0 && lane == 0) st_release_u32(sk_flags + blockIdx.x, epoch);
                 tc_fence_before();
                 if (CG == 2) {
@@ -613,7 +637,7 @@ __global__ void __launch_bounds__(256, 1)
                     }
             }
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int c = c_lo; c < c_hi; ++c) {
                 uint32_t r[32];
                 tmem_ld32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + c * 32, r);
                 tmem_wait_ld();
@@ -751,9 +775,10 @@ static bool use_stream_k(int tiles, int num_kb, int G) {
     return eff < 0.92 && I >= 4L * G;
 }
 
-template <int BN, bool A_MN, bool B_MN, int CG>
+template <int BN, bool A_MN, bool B_MN, int CG, int EPI_WARPS>
 static int launch_tc(const GemmDesc& g, cudaStream_t st) {
-    using Cfg = TcCfg<BN, CG>;
+    using Cfg = TcCfg<BN, CG, EPI_WARPS>;
+    constexpr int TC_THREADS = tc_threads(EPI_WARPS);
     constexpr int BNC = BN / CG;
     CUtensorMap ta, tb;
     int rc;
@@ -792,50 +817,31 @@ static int launch_tc(const GemmDesc& g, cudaStream_t st) {
         if (int e = sk_workspace(st, w)) return e;
         epoch = next_epoch();
     }
-    auto kern = gemm_tc_kernel<BN, A_MN, B_MN, CG>;
+    auto kern = gemm_tc_kernel<BN, A_MN, B_MN, CG, EPI_WARPS>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
         attr_set = true;
     }
-    if (CG == 1) {
-        kern<<<grid, 256, Cfg::SMEM, st>>>(ta, tb, tc, tc2, g, num_m, num_n, num_kb, sk, w.ws, w.flags, epoch);
-    } else {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(grid);
-        cfg.blockDim = dim3(256);
-        cfg.dynamicSmemBytes = Cfg::SMEM;
-        cfg.stream = st;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 2;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        static bool dbg_once = false;
-        if (!dbg_once && getenv("TPIPE_GEMM_DEBUG")) {
-            dbg_once = true;
-            int ncl = -1;
-            cudaError_t e = cudaOccupancyMaxActiveClusters(&ncl, (void*)kern, &cfg);
-            fprintf(stderr, "[gemm] pair kernel: max active clusters %d (%s), grid %d, smem %d\n", ncl,
-                    cudaGetErrorString(e), grid, Cfg::SMEM);
-        }
-        if (cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tc2, g, num_m, num_n, num_kb, sk, w.ws, w.flags, epoch) !=
-            cudaSuccess)
-            return -3;
-    }
+    if (launch_k(kern, dim3(grid), dim3(TC_THREADS), Cfg::SMEM, st, CG, ta, tb, tc, tc2, g, num_m, num_n,
+                 num_kb, sk, w.ws, w.flags, epoch) != cudaSuccess)
+        return -3;
     note_launches(1);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
+template <int BN, int CG, int EW>
+static int launch_majors_ew(const GemmDesc& g, cudaStream_t st) {
+    const bool amn = !g.a_kmajor, bmn = !g.b_kmajor;
+    if (!amn && !bmn) return launch_tc<BN, false, false, CG, EW>(g, st);
+    if (!amn && bmn) return launch_tc<BN, false, true, CG, EW>(g, st);
+    if (amn && bmn) return launch_tc<BN, true, true, CG, EW>(g, st);
+    return launch_tc<BN, true, false, CG, EW>(g, st);
+}
 template <int BN, int CG>
 static int launch_majors(const GemmDesc& g, cudaStream_t st) {
-    const bool amn = !g.a_kmajor, bmn = !g.b_kmajor;
-    if (!amn && !bmn) return launch_tc<BN, false, false, CG>(g, st);
-    if (!amn && bmn) return launch_tc<BN, false, true, CG>(g, st);
-    if (amn && bmn) return launch_tc<BN, true, true, CG>(g, st);
-    return launch_tc<BN, true, false, CG>(g, st);
+    const bool heavy = g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU || g.epi == EPI_BIAS_RES;
+    return heavy ? launch_majors_ew<BN, CG, 8>(g, st) : launch_majors_ew<BN, CG, 4>(g, st);
 }
 
 int gemm_tc(const GemmDesc& g, cudaStream_t st) {

@@ -107,6 +107,9 @@ void adamw_host(float* master, float* m, float* v, const float* grad, uint16_t* 
                 int decay, const AdamHyper& hp);
 
 // ---------------------------------------------------------------- misc
+// programmatic dependent launch of the hot-path kernels (common.cuh)
+bool pdl_enabled();
+void set_pdl(int on);
 // count of kernels launched by this library (gpu_launches evidence)
 void note_launches(int n);
 long launch_count();

@@ -144,6 +144,8 @@ __device__ __forceinline__ void unpack8(const uint4& u, float (&o)[8]) {
 constexpr int CS_COLS = 2048;
 __global__ void __launch_bounds__(256)
 colsum_wide_kernel(const bf16* __restrict__ X, float* __restrict__ ws, int rows, int n) {
+    pdl_wait();
+    pdl_trigger();
     const int c = blockIdx.x * CS_COLS + threadIdx.x * 8;
     if (c >= n) return;
     const int r0 = blockIdx.y * RB, r1 = min(rows, r0 + RB);
@@ -179,6 +181,8 @@ colsum_wide_kernel(const bf16* __restrict__ X, float* __restrict__ ws, int rows,
 __global__ void __launch_bounds__(256)
 reduce_parts_kernel(const float* __restrict__ ws, float* __restrict__ out0, float* __restrict__ out1,
                     float* __restrict__ out2, int n, int nblk) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ float4 red[32][8];
     const int t = blockIdx.y;
     float* out = t == 0 ? out0 : (t == 1 ? out1 : out2);
@@ -230,6 +234,8 @@ __global__ void __launch_bounds__(256)
 ln_fwd_warp_kernel(const bf16* __restrict__ x, const bf16* __restrict__ gamma,
                    const bf16* __restrict__ beta, bf16* __restrict__ y, float* __restrict__ mean,
                    float* __restrict__ rstd, int rows, int apply_only) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int h = NV * 256;
     const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -286,7 +292,8 @@ ln_fwd_warp_kernel(const bf16* __restrict__ x, const bf16* __restrict__ gamma,
 template <int NV>
 static void launch_ln_fwd_warp(const bf16* x, const bf16* g, const bf16* b, bf16* y, float* mean, float* rstd,
                                int rows, int apply_only, cudaStream_t st) {
-    ln_fwd_warp_kernel<NV><<<(rows + 7) / 8, 256, 0, st>>>(x, g, b, y, mean, rstd, rows, apply_only);
+    launch_k(ln_fwd_warp_kernel<NV>, dim3((rows + 7) / 8), dim3(256), 0, st, 1, x, g, b, y, mean, rstd, rows,
+             apply_only);
 }
 
 static int ln_fwd_warp(const bf16* x, const bf16* g, const bf16* b, bf16* y, float* mean, float* rstd, int rows,
@@ -318,6 +325,8 @@ ln_bwd_stage_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
                     const float* __restrict__ rstd, const bf16* __restrict__ resid,
                     bf16* __restrict__ dx, float* __restrict__ ws, int rows, int h, int nblk,
                     int with_rsum, int RC) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ float red[4][32][2];
     __shared__ float smu[RB], srs[RB];
     extern __shared__ __align__(128) uint8_t smraw[];
@@ -561,11 +570,11 @@ int ln_bwd(int dtype, const void* dy, const void* x, const void* gamma, const fl
                                  LNB_SMEM_ROWS_BYTES);
             attr = true;
         }
-        ln_bwd_stage_kernel<<<nb, G * (h / 8), smem, st>>>((const bf16*)dy, (const bf16*)x, (const bf16*)gamma,
-                                                           mean, rstd, (const bf16*)resid, (bf16*)dx, ws, rows,
-                                                           h, nb, rs, RC);
-        reduce_parts_kernel<<<dim3((h + 31) / 32, 2 + rs), 256, 0, st>>>(ws, dgamma, dbeta, dresid_sum,
-                                                                         h, nb);
+        launch_k(ln_bwd_stage_kernel, dim3(nb), dim3(G * (h / 8)), smem, st, 1, (const bf16*)dy,
+                 (const bf16*)x, (const bf16*)gamma, (const float*)mean, (const float*)rstd, (const bf16*)resid,
+                 (bf16*)dx, ws, rows, h, nb, rs, RC);
+        launch_k(reduce_parts_kernel, dim3((h + 31) / 32, 2 + rs), dim3(256), 0, st, 1, (const float*)ws, dgamma,
+                 dbeta, dresid_sum, h, nb);
         note_launches(2);
         return cudaGetLastError() == cudaSuccess ? 0 : -3;
     }
@@ -611,9 +620,10 @@ int colsum_acc(int dtype, const void* X, float* out, float* ws, int rows, int n,
     if (rows <= 0 || n <= 0) return 0;
     if (dtype == DT_BF16 && n % 8 == 0) {   // any width: CTAs tile 2048 columns
         const int nb = (rows + RB - 1) / RB;
-        colsum_wide_kernel<<<dim3((n + CS_COLS - 1) / CS_COLS, nb), 256, 0, st>>>((const bf16*)X, ws,
-                                                                                 rows, n);
-        reduce_parts_kernel<<<dim3((n + 31) / 32, 1), 256, 0, st>>>(ws, out, nullptr, nullptr, n, nb);
+        launch_k(colsum_wide_kernel, dim3((n + CS_COLS - 1) / CS_COLS, nb), dim3(256), 0, st, 1, (const bf16*)X, ws,
+                 rows, n);
+        launch_k(reduce_parts_kernel, dim3((n + 31) / 32, 1), dim3(256), 0, st, 1, (const float*)ws, out,
+                 (float*)nullptr, (float*)nullptr, n, nb);
         note_launches(2);
         return cudaGetLastError() == cudaSuccess ? 0 : -3;
     }

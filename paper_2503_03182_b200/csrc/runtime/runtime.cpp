@@ -778,6 +778,7 @@ TP_API int tpipe_runtime_get_stats(const tpipe_runtime* rt, tpipe_runtime_stats*
 TP_API void* tpipe_runtime_stream(const tpipe_runtime* rt) { return rt ? (void*)rt->stream : nullptr; }
 
 TP_API void tpipe_set_side_stream(int on) { stage_set_side_stream(on); }
+TP_API void tpipe_set_pdl(int on) { tpipe::set_pdl(on); }
 
 TP_API int tpipe_nccl_unique_id(void* out128) {
     const NcclApi* N = nccl();

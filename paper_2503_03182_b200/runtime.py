@@ -83,6 +83,11 @@ class Runtime:
         return lib().tpipe_runtime_stream(self._h) or 0
 
 
+def set_pdl(on: bool) -> None:
+    """Programmatic dependent launch of the hot-path kernels (tpipe_set_pdl)."""
+    lib().tpipe_set_pdl(1 if on else 0)
+
+
 def set_side_stream(on: bool) -> None:
     """Weight-gradient GEMMs of each layer backward on a side stream (default on)."""
     lib().tpipe_set_side_stream(1 if on else 0)
