@@ -97,6 +97,56 @@ __device__ __forceinline__ void tma_tile(uint8_t* sm, const CUtensorMap* map, ui
 }
 
 
+// ---- packed fp32x2 arithmetic (FFMA2 / FADD2 / FMUL2 on sm_100) and the
+// single-instruction ex2 (MUFU.EX2; the .ftz flush only touches results below
+// 2^-126). The elementwise warps of the backward kernels were issue-bound
+// (~21 instructions per score); these cut it to ~4.
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void upk2(uint64_t r, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ uint32_t bf2(float lo, float hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+// write 16 packed bf16x2 words (cols col0..col0+31, col0 < 64) of row r of a one-atom tile
+__device__ __forceinline__ void st_row32_pk(uint8_t* tile, int r, int col0, const uint32_t (&w)[16]) {
+    const int c0 = col0 >> 3;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<uint4*>(tile + swz(r, c0 + q)) = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+}
+
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+
 // ---------------------------------------------------------------- persistent schedule
 // grid = min(items, SMs); items are numbered heaviest first (causal work falls
 // with the item index) and dealt to CTAs in zigzag rounds: round r gives item
@@ -137,9 +187,13 @@ __global__ void __launch_bounds__(384, 1)
     uint64_t* bar = reinterpret_cast<uint64_t*>(sSum + 2 * BR);
     uint64_t* q_full = bar;                  // [2]
     uint64_t* q_empty = bar + 2;             // [2]
-    uint64_t* kv_full = bar + 4;             // [STAGES]
-    uint64_t* kv_empty = kv_full + STAGES;   // [STAGES]
-    uint64_t* s_full = kv_empty + STAGES;    // [2] S buffer ready
+    // K and V stages have their own barriers: K_{g+2} is fetched once S_g has
+    // read K_g, a whole softmax earlier than PV_g releases V_g
+    uint64_t* k_full = bar + 4;              // [STAGES]
+    uint64_t* k_empty = k_full + STAGES;     // [STAGES]
+    uint64_t* v_full = k_empty + STAGES;     // [STAGES]
+    uint64_t* v_empty = v_full + STAGES;     // [STAGES]
+    uint64_t* s_full = v_empty + STAGES;     // [2] S buffer ready
     uint64_t* p_full = s_full + 2;           // P_g in TMEM + O corrected (256 arrivals)
     uint64_t* pv_done = p_full + 1;          // PV_g complete
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 1);
@@ -163,8 +217,10 @@ __global__ void __launch_bounds__(384, 1)
             mbar_init(&s_full[i], 1);
         }
         for (int i = 0; i < STAGES; ++i) {
-            mbar_init(&kv_full[i], 1);
-            mbar_init(&kv_empty[i], 1);
+            mbar_init(&k_full[i], 1);
+            mbar_init(&k_empty[i], 1);
+            mbar_init(&v_full[i], 1);
+            mbar_init(&v_empty[i], 1);
         }
         mbar_init(p_full, 256);
         mbar_init(pv_done, 1);
@@ -193,10 +249,13 @@ __global__ void __launch_bounds__(384, 1)
                 tma_tile<D>(sQ + sl * TB, &tm_qkv, &q_full[sl], head * D, b * s + qb * BR);
                 for (int j = 0; j <= qb; ++j, ++g) {
                     const int st = g % STAGES;
-                    mbar_wait(&kv_empty[st], ((g / STAGES) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&kv_full[st], 2 * TB);
-                    tma_tile<D>(sK + st * TB, &tm_qkv, &kv_full[st], h + head * D, b * s + j * BR);
-                    tma_tile<D>(sV + st * TB, &tm_qkv, &kv_full[st], 2 * h + head * D, b * s + j * BR);
+                    const uint32_t ph = ((g / STAGES) & 1) ^ 1;
+                    mbar_wait(&k_empty[st], ph);
+                    mbar_arrive_expect_tx(&k_full[st], TB);
+                    tma_tile<D>(sK + st * TB, &tm_qkv, &k_full[st], h + head * D, b * s + j * BR);
+                    mbar_wait(&v_empty[st], ph);
+                    mbar_arrive_expect_tx(&v_full[st], TB);
+                    tma_tile<D>(sV + st * TB, &tm_qkv, &v_full[st], 2 * h + head * D, b * s + j * BR);
                 }
             }
         }
@@ -216,7 +275,7 @@ __global__ void __launch_bounds__(384, 1)
                 const int sl = k_s & 1;
                 if (j_s == 0) mbar_wait(&q_full[sl], (k_s >> 1) & 1);
                 const int st = gs % STAGES;
-                mbar_wait(&kv_full[st], (gs / STAGES) & 1);
+                mbar_wait(&k_full[st], (gs / STAGES) & 1);
                 tc_fence_after();
                 const uint32_t aQ = smem_u32(sQ + sl * TB);
                 const uint32_t aK = smem_u32(sK + st * TB);
@@ -224,6 +283,7 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) umma_bf16(tS, desc_k(aQ, kk), desc_k(aK, kk), iS, kk > 0);
                 umma_commit(&s_full[gs & 1]);
+                umma_commit(&k_empty[st]);
                 if (j_s == nkb_s - 1) umma_commit(&q_empty[sl]);   // Q of this item fully consumed
                 ++gs;
                 if (++j_s == nkb_s) {
@@ -245,15 +305,16 @@ __global__ void __launch_bounds__(384, 1)
                         issue_s();
                     }
                     mbar_wait(p_full, g & 1);
-                    tc_fence_after();
                     const int st = g % STAGES;
+                    mbar_wait(&v_full[st], (g / STAGES) & 1);
+                    tc_fence_after();
                     const uint32_t aV = smem_u32(sV + st * TB);
                     const uint32_t tP = tmem + (g & 1) * 128;
 #pragma unroll
                     for (int kk = 0; kk < BR / 16; ++kk)
                         umma_bf16_ts(tO, tP + kk * 8, desc_mn(aV, kk), iO, (j | kk) > 0);
                     umma_commit(pv_done);
-                    umma_commit(&kv_empty[st]);
+                    umma_commit(&v_empty[st]);
                 }
             }
         }
@@ -279,37 +340,46 @@ __global__ void __launch_bounds__(384, 1)
                 tc_fence_after();
                 float sv[64];
                 {
-                    uint32_t rr[32];
-                    tmem_ld32(tS + cg * 64, rr);
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) sv[e] = __uint_as_float(rr[e]);
-                    tmem_ld32(tS + cg * 64 + 32, rr);
+                    uint32_t ra[32], rb[32];
+                    tmem_ld32(tS + cg * 64, ra);
+                    tmem_ld32(tS + cg * 64 + 32, rb);
                     tmem_wait_ld();
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) sv[32 + e] = __uint_as_float(rr[e]);
+                    for (int e = 0; e < 32; ++e) {
+                        sv[e] = __uint_as_float(ra[e]);
+                        sv[32 + e] = __uint_as_float(rb[e]);
+                    }
                 }
-                const bool diag = (j == nkb - 1);
+                if (j == nkb - 1) {   // diagonal tile: keys after the query are masked
+                    const int k0 = j * BR + cg * 64;
+#pragma unroll
+                    for (int e = 0; e < 64; ++e)
+                        if (k0 + e > q) sv[e] = -INFINITY;
+                }
+                // running max in scaled units: max(s) * sc == max(s * sc) (sc > 0)
                 float lmx = -INFINITY;
 #pragma unroll
-                for (int e = 0; e < 64; ++e) {
-                    const float x = (diag && j * BR + cg * 64 + e > q) ? -INFINITY : sv[e] * sc;
-                    sv[e] = x;
-                    lmx = fmaxf(lmx, x);
-                }
+                for (int e = 0; e < 64; e += 2) lmx = fmax3(lmx, sv[e], sv[e + 1]);
+                lmx *= sc;
                 float* mb = sMax + (g & 1) * 2 * BR;
                 mb[cg * BR + r] = lmx;
                 named_bar_sync(1, 256);
-                const float mx = fmaxf(m, fmaxf(lmx, mb[(cg ^ 1) * BR + r]));
-                float rs = 0.f;
+                const float mx = fmax3(m, lmx, mb[(cg ^ 1) * BR + r]);
+                const uint64_t sc2 = pk2(sc, sc), nm2 = pk2(-mx, -mx);
+                uint64_t rs2 = pk2(0.f, 0.f);
                 uint32_t pk[32];
 #pragma unroll
                 for (int e = 0; e < 64; e += 2) {
-                    const float p0 = exp2f(sv[e] - mx), p1 = exp2f(sv[e + 1] - mx);
-                    rs += p0 + p1;
-                    __nv_bfloat162 v2 = __floats2bfloat162_rn(p0, p1);
-                    pk[e / 2] = *reinterpret_cast<uint32_t*>(&v2);
+                    float x0, x1;
+                    upk2(ffma2(pk2(sv[e], sv[e + 1]), sc2, nm2), x0, x1);
+                    const float p0 = ex2(x0), p1 = ex2(x1);
+                    rs2 = fadd2(rs2, pk2(p0, p1));
+                    pk[e / 2] = bf2(p0, p1);
                 }
-                const float corr = exp2f(m - mx);
+                float rs0, rs1;
+                upk2(rs2, rs0, rs1);
+                const float rs = rs0 + rs1;
+                const float corr = ex2(m - mx);
                 l = l * corr + rs;        // partial (this group's columns), same m history
                 m = mx;
                 tmem_st32(tS + cg * 32, pk);   // P_g over S_g: packed cols [32cg, 32cg+32)
@@ -398,6 +468,16 @@ __device__ __forceinline__ void st_row32_h(uint8_t* tile, int r, int col0, const
     }
 }
 
+// operand ring depths of the backward kernels: the Q/dO (dK/dV kernel) or
+// K/V (dQ kernel) half tile of step g+2 is loaded while step g's dV/dK (dQ)
+// MMAs still read their slot, so the TMA latency is off the MMA issue chain
+// (with 2 slots every half paid one L2 round trip). Sized to the 227 KB limit.
+template <int D>
+struct BwdCfg {
+    static constexpr int NQ = D == 128 ? 3 : 4;
+    static constexpr int NK = 4;
+};
+
 // dK/dV (persistent): an item is 128 keys of one (sequence, head); it loops
 // over 64-query halves from the diagonal. Item t (heaviest first):
 // kb = t/(a*nb), head = t%a, batch = (t/a)%nb. Half rings (Q/dO halves, S/dP
@@ -412,23 +492,26 @@ __global__ void __launch_bounds__(384, 1)
     constexpr int HB = (D / 64) * HR * 128;      // 64-row tile
     extern __shared__ uint8_t smraw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+    constexpr int NQ = BwdCfg<D>::NQ;            // Q/dO half-tile ring depth
     uint8_t* sK = sm;
     uint8_t* sV = sK + TB;
-    uint8_t* sQ = sV + TB;                 // [2] half tiles
-    uint8_t* sO = sQ + 2 * HB;             // [2] dO half tiles
-    uint8_t* sP = sO + 2 * HB;             // [2] P^T  [128 keys][64 q] (one atom, 16 KB)
+    uint8_t* sQ = sV + TB;                 // [NQ] half tiles
+    uint8_t* sO = sQ + NQ * HB;            // [NQ] dO half tiles
+    uint8_t* sP = sO + NQ * HB;            // [2] P^T  [128 keys][64 q] (one atom, 16 KB)
     uint8_t* sS = sP + 2 * BR * 128;       // [2] dS^T
     float* sL = reinterpret_cast<float*>(sS + 2 * BR * 128);   // [2][64]
     float* sD = sL + 2 * HR;                                   // [2][64]
     uint64_t* bar = reinterpret_cast<uint64_t*>(sD + 2 * HR);
     uint64_t* kv_full = bar;
     uint64_t* kv_empty = bar + 1;
-    uint64_t* q_full = bar + 2;     // [2]
-    uint64_t* q_empty = bar + 4;    // [2]
-    uint64_t* s_full = bar + 6;     // [2]
-    uint64_t* p_full = bar + 8;     // 256 arrivals per half
-    uint64_t* g_done = bar + 9;     // [2] dV/dK MMAs of a half complete
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 11);
+    uint64_t* q_full = bar + 2;          // [NQ]
+    uint64_t* q_empty = q_full + NQ;     // [NQ]
+    uint64_t* s_full = q_empty + NQ;     // [2]
+    uint64_t* p_full = s_full + 2;       // [2] 256 arrivals per half (by g & 1: a fast warp may be one half ahead)
+    uint64_t* g_done = p_full + 2;       // [2] dV/dK MMAs of a half complete
+    uint64_t* ld_full = g_done + 2;      // [2] sL/sD of a half staged (warp 3)
+    uint64_t* ld_empty = ld_full + 2;    // [2] sL/sD of a half consumed (256 arrivals)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ld_empty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nkb = (s + BR - 1) / BR;
@@ -449,13 +532,18 @@ __global__ void __launch_bounds__(384, 1)
         tma_prefetch_desc(&tm_do64);
         mbar_init(kv_full, 1);
         mbar_init(kv_empty, 1);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < NQ; ++i) {
             mbar_init(&q_full[i], 1);
             mbar_init(&q_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
             mbar_init(&s_full[i], 1);
             mbar_init(&g_done[i], 1);
+            mbar_init(&ld_full[i], 32);
+            mbar_init(&ld_empty[i], 256);
         }
-        mbar_init(p_full, 256);
+        mbar_init(&p_full[0], 256);
+        mbar_init(&p_full[1], 256);
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc(tmem_slot, 512);
@@ -482,8 +570,8 @@ __global__ void __launch_bounds__(384, 1)
                 tma_tile<D>(sV, &tm_qkv, kv_full, 2 * h + head * D, row0 + kb * BR);
                 const int nh = halves(t);
                 for (int hh = 0; hh < nh; ++hh, ++g) {
-                    const int sl = g & 1;
-                    mbar_wait(&q_empty[sl], ((g >> 1) & 1) ^ 1);
+                    const int sl = g % NQ;
+                    mbar_wait(&q_empty[sl], ((g / NQ) & 1) ^ 1);
                     mbar_arrive_expect_tx(&q_full[sl], 2 * HB);
                     const int qrow = row0 + (2 * kb + hh) * HR;
                     tma_half<D>(sQ + sl * HB, &tm_qkv64, &q_full[sl], head * D, qrow);
@@ -504,18 +592,18 @@ __global__ void __launch_bounds__(384, 1)
                 if (have_s) nh_s = halves(t);
             }
             auto issue_s = [&]() {
-                const int sl = gs & 1;
+                const int sl = gs % NQ;
                 if (h_s == 0) mbar_wait(kv_full, k_s & 1);
-                mbar_wait(&q_full[sl], (gs >> 1) & 1);
+                mbar_wait(&q_full[sl], (gs / NQ) & 1);
                 tc_fence_after();
                 const uint32_t aQ = smem_u32(sQ + sl * HB), aO = smem_u32(sO + sl * HB);
-                const uint32_t tS = tmem + sl * 128, tP = tS + 64;
+                const uint32_t tS = tmem + (gs & 1) * 128, tP = tS + 64;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
                     umma_bf16(tS, desc_k(aK, kk), desc_k_h(aQ, kk), iS, kk > 0);   // S^T = K Q^T
                     umma_bf16(tP, desc_k(aV, kk), desc_k_h(aO, kk), iS, kk > 0);   // dP^T = V dO^T
                 }
-                umma_commit(&s_full[sl]);
+                umma_commit(&s_full[gs & 1]);
                 if (h_s == nh_s - 1) umma_commit(kv_empty);   // K, V of this item consumed
                 ++gs;
                 if (++h_s == nh_s) {
@@ -534,9 +622,10 @@ __global__ void __launch_bounds__(384, 1)
                 for (int hh = 0; hh < nh; ++hh, ++g) {
                     const int sl = g & 1;
                     if (have_s) issue_s();   // TMEM buffer (g+1)&1 freed by p_full(g-1)
-                    mbar_wait(p_full, g & 1);
+                    mbar_wait(&p_full[g & 1], (g >> 1) & 1);
                     tc_fence_after();
-                    const uint32_t aQ = smem_u32(sQ + sl * HB), aO = smem_u32(sO + sl * HB);
+                    const int qs = g % NQ;
+                    const uint32_t aQ = smem_u32(sQ + qs * HB), aO = smem_u32(sO + qs * HB);
                     const uint32_t aP = smem_u32(sP + sl * BR * 128), aS = smem_u32(sS + sl * BR * 128);
 #pragma unroll
                     for (int kk = 0; kk < HR / 16; ++kk) {
@@ -544,8 +633,33 @@ __global__ void __launch_bounds__(384, 1)
                         umma_bf16(tdK, desc_k(aS, kk), desc_mn_h(aQ, kk), iG, (hh | kk) > 0);  // dK += dS^T Q
                     }
                     umma_commit(&g_done[sl]);
-                    umma_commit(&q_empty[sl]);
+                    umma_commit(&q_empty[qs]);
                 }
+            }
+        }
+    } else if (warp == 3) {
+        // lse / D of each 64-query half, negated and pre-scaled, staged one half
+        // ahead so the elementwise warps never wait on a global load
+        int g = 0;
+        for (int k = 0;; ++k) {
+            const int t = sched_item(k, T);
+            if (t < 0) break;
+            int kb, head, b;
+            decode(t, kb, head, b);
+            const int nh = halves(t);
+            const float* lseb = lse + ((long)b * a + head) * s;
+            const float* Db = Dv + ((long)b * a + head) * s;
+            for (int hh = 0; hh < nh; ++hh, ++g) {
+                const int sl = g & 1;
+                const int q0 = (2 * kb + hh) * HR;
+                mbar_wait(&ld_empty[sl], ((g >> 1) & 1) ^ 1);
+#pragma unroll
+                for (int i = lane; i < HR; i += 32) {
+                    const int qq = q0 + i;
+                    sL[sl * HR + i] = qq < s ? -lseb[qq] * LOG2E : 0.f;
+                    sD[sl * HR + i] = qq < s ? -Db[qq] : 0.f;
+                }
+                mbar_arrive(&ld_full[sl]);
             }
         }
     } else if (warp >= 4) {
@@ -564,19 +678,12 @@ __global__ void __launch_bounds__(384, 1)
             decode(t, kb, head, b);
             const int nh = halves(t);
             const int key = kb * BR + r;
-            const float* lseb = lse + ((long)b * a + head) * s;
-            const float* Db = Dv + ((long)b * a + head) * s;
             for (int hh = 0; hh < nh; ++hh, ++g) {
                 const int sl = g & 1;
                 const int q0 = (2 * kb + hh) * HR;
                 // P/dS buffer `sl` was last read by the MMAs of half g-2
                 if (g >= 2) mbar_wait(&g_done[sl], ((g - 2) >> 1) & 1);
-                if (et < HR) {
-                    const int qq = q0 + et;
-                    sL[sl * HR + et] = qq < s ? lseb[qq] * LOG2E : 0.f;
-                    sD[sl * HR + et] = qq < s ? Db[qq] : 0.f;
-                }
-                named_bar_sync(1, 256);
+                mbar_wait(&ld_full[sl], (g >> 1) & 1);
                 mbar_wait(&s_full[sl], (g >> 1) & 1);
                 tc_fence_after();
                 const uint32_t tS = tmem + sl * 128 + lane_off, tP = tS + 64;
@@ -586,22 +693,52 @@ __global__ void __launch_bounds__(384, 1)
                 const float* Dq = sD + sl * HR;
                 {
                     const int c = cg;
-                    float sv[32], pv[32];
-                    tmem_ld32f(tS + c * 32, sv);
-                    tmem_ld32f(tP + c * 32, pv);
+                    uint32_t sr[32], pr[32];
+                    tmem_ld32(tS + c * 32, sr);
+                    tmem_ld32(tP + c * 32, pr);
+                    tmem_wait_ld();
+                    // P^T = exp2(S^T sc - L_q); every key of the block precedes every
+                    // query of this column group except on the diagonal halves
+                    const int qc = q0 + c * 32;
+                    const bool full = qc >= kb * BR + BR - 1 && qc + 32 <= s;
+                    const uint64_t sc2 = pk2(sc, sc);
+                    const float* nL = L + c * 32;
+                    const float* nD = Dq + c * 32;
+                    float p[32];
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        const int ql = c * 32 + e, qq = q0 + ql;
-                        const float p = (qq >= key && qq < s) ? exp2f(sv[e] * sc - L[ql]) : 0.f;
-                        sv[e] = p;
-                        pv[e] = p * (pv[e] - Dq[ql]);
+                    for (int e = 0; e < 32; e += 2) {
+                        const uint64_t x2 = ffma2(pk2(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])), sc2,
+                                                  *reinterpret_cast<const uint64_t*>(nL + e));
+                        float x0, x1;
+                        upk2(x2, x0, x1);
+                        p[e] = ex2(x0);
+                        p[e + 1] = ex2(x1);
                     }
-                    st_row32_h(P, r, c * 32, sv);
-                    st_row32_h(Sd, r, c * 32, pv);
+                    if (!full) {
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) {
+                            const int qq = qc + e;
+                            if (!(qq >= key && qq < s)) p[e] = 0.f;
+                        }
+                    }
+                    uint32_t wp[16], wd[16];
+#pragma unroll
+                    for (int e = 0; e < 32; e += 2) {
+                        const uint64_t p2 = pk2(p[e], p[e + 1]);
+                        const uint64_t d2 = fmul2(p2, fadd2(pk2(__uint_as_float(pr[e]), __uint_as_float(pr[e + 1])),
+                                                            *reinterpret_cast<const uint64_t*>(nD + e)));
+                        float d0, d1;
+                        upk2(d2, d0, d1);
+                        wp[e / 2] = bf2(p[e], p[e + 1]);
+                        wd[e / 2] = bf2(d0, d1);
+                    }
+                    st_row32_pk(P, r, c * 32, wp);
+                    st_row32_pk(Sd, r, c * 32, wd);
                 }
+                mbar_arrive(&ld_empty[sl]);
                 fence_async_smem();
                 tc_fence_before();
-                mbar_arrive(p_full);
+                mbar_arrive(&p_full[sl]);
             }
             mbar_wait(&g_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
             tc_fence_after();
@@ -658,20 +795,21 @@ __global__ void __launch_bounds__(384, 1)
     constexpr int HB = (D / 64) * HR * 128;
     extern __shared__ uint8_t smraw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+    constexpr int NK = BwdCfg<D>::NK;   // K/V half-tile ring depth
     uint8_t* sQ = sm;
     uint8_t* sO = sQ + TB;
-    uint8_t* sK = sO + TB;              // [2] half tiles
-    uint8_t* sV = sK + 2 * HB;          // [2]
-    uint8_t* sS = sV + 2 * HB;          // [2] dS [128 q][64 keys] (one atom)
+    uint8_t* sK = sO + TB;              // [NK] half tiles
+    uint8_t* sV = sK + NK * HB;         // [NK]
+    uint8_t* sS = sV + NK * HB;         // [2] dS [128 q][64 keys] (one atom)
     uint64_t* bar = reinterpret_cast<uint64_t*>(sS + 2 * BR * 128);
     uint64_t* q_full = bar;
     uint64_t* q_empty = bar + 1;
-    uint64_t* kv_full = bar + 2;        // [2]
-    uint64_t* kv_empty = bar + 4;       // [2]
-    uint64_t* s_full = bar + 6;         // [2]
-    uint64_t* p_full = bar + 8;
-    uint64_t* g_done = bar + 9;         // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 11);
+    uint64_t* kv_full = bar + 2;          // [NK]
+    uint64_t* kv_empty = kv_full + NK;    // [NK]
+    uint64_t* s_full = kv_empty + NK;     // [2]
+    uint64_t* p_full = s_full + 2;        // [2] by g & 1 (a fast warp may be one half ahead)
+    uint64_t* g_done = p_full + 2;        // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(g_done + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nqb = (s + BR - 1) / BR;
@@ -694,13 +832,16 @@ __global__ void __launch_bounds__(384, 1)
         tma_prefetch_desc(&tm_qkv64);
         mbar_init(q_full, 1);
         mbar_init(q_empty, 1);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < NK; ++i) {
             mbar_init(&kv_full[i], 1);
             mbar_init(&kv_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
             mbar_init(&s_full[i], 1);
             mbar_init(&g_done[i], 1);
         }
-        mbar_init(p_full, 256);
+        mbar_init(&p_full[0], 256);
+        mbar_init(&p_full[1], 256);
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc(tmem_slot, 512);
@@ -727,8 +868,8 @@ __global__ void __launch_bounds__(384, 1)
                 tma_tile<D>(sO, &tm_do, q_full, head * D, row0 + qb * BR);
                 const int nh = halves(t);
                 for (int hh = 0; hh < nh; ++hh, ++g) {
-                    const int sl = g & 1;
-                    mbar_wait(&kv_empty[sl], ((g >> 1) & 1) ^ 1);
+                    const int sl = g % NK;
+                    mbar_wait(&kv_empty[sl], ((g / NK) & 1) ^ 1);
                     mbar_arrive_expect_tx(&kv_full[sl], 2 * HB);
                     tma_half<D>(sK + sl * HB, &tm_qkv64, &kv_full[sl], h + head * D, row0 + hh * HR);
                     tma_half<D>(sV + sl * HB, &tm_qkv64, &kv_full[sl], 2 * h + head * D, row0 + hh * HR);
@@ -748,18 +889,18 @@ __global__ void __launch_bounds__(384, 1)
                 if (have_s) nh_s = halves(t);
             }
             auto issue_s = [&]() {
-                const int sl = gs & 1;
+                const int sl = gs % NK;
                 if (h_s == 0) mbar_wait(q_full, k_s & 1);
-                mbar_wait(&kv_full[sl], (gs >> 1) & 1);
+                mbar_wait(&kv_full[sl], (gs / NK) & 1);
                 tc_fence_after();
                 const uint32_t aK = smem_u32(sK + sl * HB), aV = smem_u32(sV + sl * HB);
-                const uint32_t tS = tmem + sl * 128, tP = tS + 64;
+                const uint32_t tS = tmem + (gs & 1) * 128, tP = tS + 64;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
                     umma_bf16(tS, desc_k(aQ, kk), desc_k_h(aK, kk), iS, kk > 0);   // S = Q K^T
                     umma_bf16(tP, desc_k(aO, kk), desc_k_h(aV, kk), iS, kk > 0);   // dP = dO V^T
                 }
-                umma_commit(&s_full[sl]);
+                umma_commit(&s_full[gs & 1]);
                 if (h_s == nh_s - 1) umma_commit(q_empty);   // Q, dO of this item consumed
                 ++gs;
                 if (++h_s == nh_s) {
@@ -778,14 +919,15 @@ __global__ void __launch_bounds__(384, 1)
                 for (int hh = 0; hh < nh; ++hh, ++g) {
                     const int sl = g & 1;
                     if (have_s) issue_s();
-                    mbar_wait(p_full, g & 1);
+                    mbar_wait(&p_full[g & 1], (g >> 1) & 1);
                     tc_fence_after();
-                    const uint32_t aK = smem_u32(sK + sl * HB), aS = smem_u32(sS + sl * BR * 128);
+                    const int ks = g % NK;
+                    const uint32_t aK = smem_u32(sK + ks * HB), aS = smem_u32(sS + sl * BR * 128);
 #pragma unroll
                     for (int kk = 0; kk < HR / 16; ++kk)
                         umma_bf16(tdQ, desc_k(aS, kk), desc_mn_h(aK, kk), iG, (hh | kk) > 0);   // dQ += dS K
                     umma_commit(&g_done[sl]);
-                    umma_commit(&kv_empty[sl]);
+                    umma_commit(&kv_empty[ks]);
                 }
             }
         }
@@ -816,20 +958,42 @@ __global__ void __launch_bounds__(384, 1)
                 uint8_t* Sd = sS + sl * BR * 128;
                 {
                     const int c = cg;
-                    float sv[32], pv[32];
-                    tmem_ld32f(tS + c * 32, sv);
-                    tmem_ld32f(tP + c * 32, pv);
+                    uint32_t sr[32], pr[32];
+                    tmem_ld32(tS + c * 32, sr);
+                    tmem_ld32(tP + c * 32, pr);
+                    tmem_wait_ld();
+                    const int kc = hh * HR + c * 32;
+                    const bool full = kc + 31 <= qb * BR;   // below the diagonal for every row
+                    const uint64_t sc2 = pk2(sc, sc), nl2 = pk2(-L, -L), nd2 = pk2(-Dq, -Dq);
+                    float p[32];
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        const int key = hh * HR + c * 32 + e;
-                        const float p = (key <= q) ? exp2f(sv[e] * sc - L) : 0.f;
-                        pv[e] = p * (pv[e] - Dq);
+                    for (int e = 0; e < 32; e += 2) {
+                        const uint64_t x2 =
+                            ffma2(pk2(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])), sc2, nl2);
+                        float x0, x1;
+                        upk2(x2, x0, x1);
+                        p[e] = ex2(x0);
+                        p[e + 1] = ex2(x1);
                     }
-                    st_row32_h(Sd, r, c * 32, pv);
+                    if (!full) {
+#pragma unroll
+                        for (int e = 0; e < 32; ++e)
+                            if (kc + e > q) p[e] = 0.f;
+                    }
+                    uint32_t wd[16];
+#pragma unroll
+                    for (int e = 0; e < 32; e += 2) {
+                        const uint64_t d2 = fmul2(pk2(p[e], p[e + 1]),
+                                                  fadd2(pk2(__uint_as_float(pr[e]), __uint_as_float(pr[e + 1])), nd2));
+                        float d0, d1;
+                        upk2(d2, d0, d1);
+                        wd[e / 2] = bf2(d0, d1);
+                    }
+                    st_row32_pk(Sd, r, c * 32, wd);
                 }
                 fence_async_smem();
                 tc_fence_before();
-                mbar_arrive(p_full);
+                mbar_arrive(&p_full[sl]);
             }
             mbar_wait(&g_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
             tc_fence_after();
@@ -949,8 +1113,9 @@ static int bwd5(const void* qkv, const void* o, const void* dout, const float* l
                 float* ws, int b, int s, int a, cudaStream_t st) {
     constexpr int TB = fa5::Tile<D>::BYTES;
     constexpr int HB = (D / 64) * 64 * 128;
-    constexpr int smem_kv = 1024 + 2 * TB + 4 * HB + 4 * 128 * 128 + 4 * 64 * 4 + 256;
-    constexpr int smem_q = 1024 + 2 * TB + 4 * HB + 2 * 128 * 128 + 256;
+    constexpr int smem_kv = 1024 + 2 * TB + 2 * fa5::BwdCfg<D>::NQ * HB + 4 * 128 * 128 + 4 * 64 * 4 + 256;
+    constexpr int smem_q = 1024 + 2 * TB + 2 * fa5::BwdCfg<D>::NK * HB + 2 * 128 * 128 + 256;
+    static_assert(smem_kv <= 232448 && smem_q <= 232448, "backward smem over the 227 KB limit");
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(fa5::dkdv2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kv);
