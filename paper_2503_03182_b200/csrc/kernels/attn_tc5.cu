@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t tO = tmem + 256;
 
     if (warp == 0) {
-        if (lane == 0) {
+        {   // whole warp waits; the elected lane issues the TMA loads
             int g = 0;
             for (int k = 0;; ++k) {
                 const int t = sched_item(k, T);
@@ -245,22 +245,31 @@ __global__ void __launch_bounds__(384, 1)
                 decode(t, qb, head, b);
                 const int sl = k & 1;
                 mbar_wait(&q_empty[sl], ((k >> 1) & 1) ^ 1);
-                mbar_arrive_expect_tx(&q_full[sl], TB);
-                tma_tile<D>(sQ + sl * TB, &tm_qkv, &q_full[sl], head * D, b * s + qb * BR);
+                if (elect_one()) {
+                    mbar_arrive_expect_tx(&q_full[sl], TB);
+                    tma_tile<D>(sQ + sl * TB, &tm_qkv, &q_full[sl], head * D, b * s + qb * BR);
+                }
+                __syncwarp();
                 for (int j = 0; j <= qb; ++j, ++g) {
                     const int st = g % STAGES;
                     const uint32_t ph = ((g / STAGES) & 1) ^ 1;
                     mbar_wait(&k_empty[st], ph);
-                    mbar_arrive_expect_tx(&k_full[st], TB);
-                    tma_tile<D>(sK + st * TB, &tm_qkv, &k_full[st], h + head * D, b * s + j * BR);
+                    if (elect_one()) {
+                        mbar_arrive_expect_tx(&k_full[st], TB);
+                        tma_tile<D>(sK + st * TB, &tm_qkv, &k_full[st], h + head * D, b * s + j * BR);
+                    }
+                    __syncwarp();
                     mbar_wait(&v_empty[st], ph);
-                    mbar_arrive_expect_tx(&v_full[st], TB);
-                    tma_tile<D>(sV + st * TB, &tm_qkv, &v_full[st], 2 * h + head * D, b * s + j * BR);
+                    if (elect_one()) {
+                        mbar_arrive_expect_tx(&v_full[st], TB);
+                        tma_tile<D>(sV + st * TB, &tm_qkv, &v_full[st], 2 * h + head * D, b * s + j * BR);
+                    }
+                    __syncwarp();
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {   // whole warp: loop state stays warp-uniform, the elected lane issues
             const uint32_t iS = idesc(BR, false, false);
             const uint32_t iO = idesc(D, false, true);
             // S-issue cursor: item k_s (tiles 0..qb_s), tile j_s, global index gs
@@ -280,11 +289,14 @@ __global__ void __launch_bounds__(384, 1)
                 const uint32_t aQ = smem_u32(sQ + sl * TB);
                 const uint32_t aK = smem_u32(sK + st * TB);
                 const uint32_t tS = tmem + (gs & 1) * 128;
+                if (elect_one()) {
 #pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk) umma_bf16(tS, desc_k(aQ, kk), desc_k(aK, kk), iS, kk > 0);
-                umma_commit(&s_full[gs & 1]);
-                umma_commit(&k_empty[st]);
-                if (j_s == nkb_s - 1) umma_commit(&q_empty[sl]);   // Q of this item fully consumed
+                    for (int kk = 0; kk < D / 16; ++kk) umma_bf16(tS, desc_k(aQ, kk), desc_k(aK, kk), iS, kk > 0);
+                    umma_commit(&s_full[gs & 1]);
+                    umma_commit(&k_empty[st]);
+                    if (j_s == nkb_s - 1) umma_commit(&q_empty[sl]);   // Q of this item fully consumed
+                }
+                __syncwarp();
                 ++gs;
                 if (++j_s == nkb_s) {
                     j_s = 0;
@@ -310,11 +322,14 @@ __global__ void __launch_bounds__(384, 1)
                     tc_fence_after();
                     const uint32_t aV = smem_u32(sV + st * TB);
                     const uint32_t tP = tmem + (g & 1) * 128;
+                    if (elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < BR / 16; ++kk)
-                        umma_bf16_ts(tO, tP + kk * 8, desc_mn(aV, kk), iO, (j | kk) > 0);
-                    umma_commit(pv_done);
-                    umma_commit(&v_empty[st]);
+                        for (int kk = 0; kk < BR / 16; ++kk)
+                            umma_bf16_ts(tO, tP + kk * 8, desc_mn(aV, kk), iO, (j | kk) > 0);
+                        umma_commit(pv_done);
+                        umma_commit(&v_empty[st]);
+                    }
+                    __syncwarp();
                 }
             }
         }
@@ -556,7 +571,7 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t tdV = tmem + 256, tdK = tmem + 256 + D;   // D <= 128
 
     if (warp == 0) {
-        if (lane == 0) {
+        {   // whole warp waits; the elected lane issues the TMA loads
             int g = 0;
             for (int k = 0;; ++k) {
                 const int t = sched_item(k, T);
@@ -565,22 +580,28 @@ __global__ void __launch_bounds__(384, 1)
                 decode(t, kb, head, b);
                 const int row0 = b * s;
                 mbar_wait(kv_empty, (k & 1) ^ 1);
-                mbar_arrive_expect_tx(kv_full, 2 * TB);
-                tma_tile<D>(sK, &tm_qkv, kv_full, h + head * D, row0 + kb * BR);
-                tma_tile<D>(sV, &tm_qkv, kv_full, 2 * h + head * D, row0 + kb * BR);
+                if (elect_one()) {
+                    mbar_arrive_expect_tx(kv_full, 2 * TB);
+                    tma_tile<D>(sK, &tm_qkv, kv_full, h + head * D, row0 + kb * BR);
+                    tma_tile<D>(sV, &tm_qkv, kv_full, 2 * h + head * D, row0 + kb * BR);
+                }
+                __syncwarp();
                 const int nh = halves(t);
                 for (int hh = 0; hh < nh; ++hh, ++g) {
                     const int sl = g % NQ;
                     mbar_wait(&q_empty[sl], ((g / NQ) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&q_full[sl], 2 * HB);
                     const int qrow = row0 + (2 * kb + hh) * HR;
-                    tma_half<D>(sQ + sl * HB, &tm_qkv64, &q_full[sl], head * D, qrow);
-                    tma_half<D>(sO + sl * HB, &tm_do64, &q_full[sl], head * D, qrow);
+                    if (elect_one()) {
+                        mbar_arrive_expect_tx(&q_full[sl], 2 * HB);
+                        tma_half<D>(sQ + sl * HB, &tm_qkv64, &q_full[sl], head * D, qrow);
+                        tma_half<D>(sO + sl * HB, &tm_do64, &q_full[sl], head * D, qrow);
+                    }
+                    __syncwarp();
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {   // whole warp; the elected lane issues
             const uint32_t iS = idesc(HR, false, false);   // M=128 keys, N=64 queries
             const uint32_t iG = idesc(D, false, true);
             const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
@@ -598,13 +619,16 @@ __global__ void __launch_bounds__(384, 1)
                 tc_fence_after();
                 const uint32_t aQ = smem_u32(sQ + sl * HB), aO = smem_u32(sO + sl * HB);
                 const uint32_t tS = tmem + (gs & 1) * 128, tP = tS + 64;
+                if (elect_one()) {
 #pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk) {
-                    umma_bf16(tS, desc_k(aK, kk), desc_k_h(aQ, kk), iS, kk > 0);   // S^T = K Q^T
-                    umma_bf16(tP, desc_k(aV, kk), desc_k_h(aO, kk), iS, kk > 0);   // dP^T = V dO^T
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        umma_bf16(tS, desc_k(aK, kk), desc_k_h(aQ, kk), iS, kk > 0);   // S^T = K Q^T
+                        umma_bf16(tP, desc_k(aV, kk), desc_k_h(aO, kk), iS, kk > 0);   // dP^T = V dO^T
+                    }
+                    umma_commit(&s_full[gs & 1]);
+                    if (h_s == nh_s - 1) umma_commit(kv_empty);   // K, V of this item consumed
                 }
-                umma_commit(&s_full[gs & 1]);
-                if (h_s == nh_s - 1) umma_commit(kv_empty);   // K, V of this item consumed
+                __syncwarp();
                 ++gs;
                 if (++h_s == nh_s) {
                     h_s = 0;
@@ -627,13 +651,16 @@ __global__ void __launch_bounds__(384, 1)
                     const int qs = g % NQ;
                     const uint32_t aQ = smem_u32(sQ + qs * HB), aO = smem_u32(sO + qs * HB);
                     const uint32_t aP = smem_u32(sP + sl * BR * 128), aS = smem_u32(sS + sl * BR * 128);
+                    if (elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < HR / 16; ++kk) {
-                        umma_bf16(tdV, desc_k(aP, kk), desc_mn_h(aO, kk), iG, (hh | kk) > 0);  // dV += P^T dO
-                        umma_bf16(tdK, desc_k(aS, kk), desc_mn_h(aQ, kk), iG, (hh | kk) > 0);  // dK += dS^T Q
+                        for (int kk = 0; kk < HR / 16; ++kk) {
+                            umma_bf16(tdV, desc_k(aP, kk), desc_mn_h(aO, kk), iG, (hh | kk) > 0);  // dV += P^T dO
+                            umma_bf16(tdK, desc_k(aS, kk), desc_mn_h(aQ, kk), iG, (hh | kk) > 0);  // dK += dS^T Q
+                        }
+                        umma_commit(&g_done[sl]);
+                        umma_commit(&q_empty[qs]);
                     }
-                    umma_commit(&g_done[sl]);
-                    umma_commit(&q_empty[qs]);
+                    __syncwarp();
                 }
             }
         }
@@ -854,7 +881,7 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t tdQ = tmem + 256;
 
     if (warp == 0) {
-        if (lane == 0) {
+        {   // whole warp waits; the elected lane issues the TMA loads
             int g = 0;
             for (int k = 0;; ++k) {
                 const int t = sched_item(k, T);
@@ -863,21 +890,27 @@ __global__ void __launch_bounds__(384, 1)
                 decode(t, qb, head, b);
                 const int row0 = b * s;
                 mbar_wait(q_empty, (k & 1) ^ 1);
-                mbar_arrive_expect_tx(q_full, 2 * TB);
-                tma_tile<D>(sQ, &tm_qkv, q_full, head * D, row0 + qb * BR);
-                tma_tile<D>(sO, &tm_do, q_full, head * D, row0 + qb * BR);
+                if (elect_one()) {
+                    mbar_arrive_expect_tx(q_full, 2 * TB);
+                    tma_tile<D>(sQ, &tm_qkv, q_full, head * D, row0 + qb * BR);
+                    tma_tile<D>(sO, &tm_do, q_full, head * D, row0 + qb * BR);
+                }
+                __syncwarp();
                 const int nh = halves(t);
                 for (int hh = 0; hh < nh; ++hh, ++g) {
                     const int sl = g % NK;
                     mbar_wait(&kv_empty[sl], ((g / NK) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&kv_full[sl], 2 * HB);
-                    tma_half<D>(sK + sl * HB, &tm_qkv64, &kv_full[sl], h + head * D, row0 + hh * HR);
-                    tma_half<D>(sV + sl * HB, &tm_qkv64, &kv_full[sl], 2 * h + head * D, row0 + hh * HR);
+                    if (elect_one()) {
+                        mbar_arrive_expect_tx(&kv_full[sl], 2 * HB);
+                        tma_half<D>(sK + sl * HB, &tm_qkv64, &kv_full[sl], h + head * D, row0 + hh * HR);
+                        tma_half<D>(sV + sl * HB, &tm_qkv64, &kv_full[sl], 2 * h + head * D, row0 + hh * HR);
+                    }
+                    __syncwarp();
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {   // whole warp; the elected lane issues
             const uint32_t iS = idesc(HR, false, false);   // M=128 q, N=64 keys
             const uint32_t iG = idesc(D, false, true);
             const uint32_t aQ = smem_u32(sQ), aO = smem_u32(sO);
@@ -895,13 +928,16 @@ __global__ void __launch_bounds__(384, 1)
                 tc_fence_after();
                 const uint32_t aK = smem_u32(sK + sl * HB), aV = smem_u32(sV + sl * HB);
                 const uint32_t tS = tmem + (gs & 1) * 128, tP = tS + 64;
+                if (elect_one()) {
 #pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk) {
-                    umma_bf16(tS, desc_k(aQ, kk), desc_k_h(aK, kk), iS, kk > 0);   // S = Q K^T
-                    umma_bf16(tP, desc_k(aO, kk), desc_k_h(aV, kk), iS, kk > 0);   // dP = dO V^T
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        umma_bf16(tS, desc_k(aQ, kk), desc_k_h(aK, kk), iS, kk > 0);   // S = Q K^T
+                        umma_bf16(tP, desc_k(aO, kk), desc_k_h(aV, kk), iS, kk > 0);   // dP = dO V^T
+                    }
+                    umma_commit(&s_full[gs & 1]);
+                    if (h_s == nh_s - 1) umma_commit(q_empty);   // Q, dO of this item consumed
                 }
-                umma_commit(&s_full[gs & 1]);
-                if (h_s == nh_s - 1) umma_commit(q_empty);   // Q, dO of this item consumed
+                __syncwarp();
                 ++gs;
                 if (++h_s == nh_s) {
                     h_s = 0;
@@ -923,11 +959,14 @@ __global__ void __launch_bounds__(384, 1)
                     tc_fence_after();
                     const int ks = g % NK;
                     const uint32_t aK = smem_u32(sK + ks * HB), aS = smem_u32(sS + sl * BR * 128);
+                    if (elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < HR / 16; ++kk)
-                        umma_bf16(tdQ, desc_k(aS, kk), desc_mn_h(aK, kk), iG, (hh | kk) > 0);   // dQ += dS K
-                    umma_commit(&g_done[sl]);
-                    umma_commit(&kv_empty[ks]);
+                        for (int kk = 0; kk < HR / 16; ++kk)
+                            umma_bf16(tdQ, desc_k(aS, kk), desc_mn_h(aK, kk), iG, (hh | kk) > 0);   // dQ += dS K
+                        umma_commit(&g_done[sl]);
+                        umma_commit(&kv_empty[ks]);
+                    }
+                    __syncwarp();
                 }
             }
         }
@@ -1025,23 +1064,38 @@ __global__ void __launch_bounds__(384, 1)
 }
 
 // D[b,head,i] = sum_e dO O (fp32), one warp per row
-__global__ void d_kernel(const bf16* __restrict__ o, const bf16* __restrict__ dout,
-                         float* __restrict__ Dv, int s, int a, int d) {
-    const int lane = threadIdx.x & 31;
-    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int head = blockIdx.y, b = blockIdx.z;
+// D[b,head,q] = sum_e dO O (fp32). One 16-byte chunk of O and of dO per
+// thread (TPR = d/8 threads per (token, head) row, rows ordered token-major so
+// a warp reads contiguous memory), reduced over the row's lanes by shuffles.
+template <int TPR>
+__global__ void __launch_bounds__(256) d_kernel(const bf16* __restrict__ o, const bf16* __restrict__ dout,
+                                                float* __restrict__ Dv, int s, int a, long rows) {
+    const long gt = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long row = gt / TPR;   // = (b*s + q)*a + head
     pdl_wait();
     pdl_trigger();
-    if (i >= s) return;
-    const long off = ((long)b * s + i) * a * d + head * d;
     float part = 0.f;
-    for (int e = lane * 2; e < d; e += 64) {
-        const __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162*>(o + off + e);
-        const __nv_bfloat162 y = *reinterpret_cast<const __nv_bfloat162*>(dout + off + e);
-        part += __bfloat162float(x.x) * __bfloat162float(y.x) + __bfloat162float(x.y) * __bfloat162float(y.y);
+    if (row < rows) {
+        const long off = gt * 8;   // row * (TPR*8) + chunk*8
+        const uint4 x = __ldg(reinterpret_cast<const uint4*>(o + off));
+        const uint4 y = __ldg(reinterpret_cast<const uint4*>(dout + off));
+        const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&x);
+        const __nv_bfloat162* yh = reinterpret_cast<const __nv_bfloat162*>(&y);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float2 xf = __bfloat1622float2(xh[j]), yf = __bfloat1622float2(yh[j]);
+            part = fmaf(xf.x, yf.x, part);
+            part = fmaf(xf.y, yf.y, part);
+        }
     }
-    part = warp_sum(part);
-    if (lane == 0) Dv[((long)b * a + head) * s + i] = part;
+#pragma unroll
+    for (int w = TPR / 2; w > 0; w >>= 1) part += __shfl_xor_sync(0xffffffffu, part, w);
+    if (row < rows && (threadIdx.x % TPR) == 0) {
+        const long tok = row / a;
+        const int head = (int)(row % a);
+        const long b = tok / s, q = tok % s;
+        Dv[(b * a + head) * s + q] = part;
+    }
 }
 
 }  // namespace fa5
@@ -1127,9 +1181,10 @@ static int bwd5(const void* qkv, const void* o, const void* dout, const float* l
     if (map2d(&mq64, qkv, 3L * a * D, (long)b * s, 3L * a * D, 64)) return -2;
     if (map2d(&md, dout, (long)a * D, (long)b * s, (long)a * D)) return -2;
     if (map2d(&md64, dout, (long)a * D, (long)b * s, (long)a * D, 64)) return -2;
-    dim3 gd((s + 3) / 4, a, b);
-    if (launch_k(fa5::d_kernel, gd, dim3(128), 0, st, 1, (const bf16*)o, (const bf16*)dout, ws, s, a, D) !=
-        cudaSuccess)
+    const long drows = (long)b * s * a;
+    const unsigned dblocks = (unsigned)((drows * (D / 8) + 255) / 256);
+    if (launch_k(fa5::d_kernel<D / 8>, dim3(dblocks), dim3(256), 0, st, 1, (const bf16*)o, (const bf16*)dout, ws, s,
+                 a, drows) != cudaSuccess)
         return -3;
     const int grid = persistent_grid(((s + 127) / 128) * a * b);
     if (launch_k(fa5::dkdv2_kernel<D>, dim3(grid), dim3(384), smem_kv, st, 1, mq, mq64, md64, lse,

@@ -208,6 +208,21 @@ __device__ __forceinline__ void tc_fence_after() {
 }
 
 // D[tmem] (+)= A[smem] * B[smem]^T, kind::f16 (bf16 inputs, fp32 accumulate)
+// elect.sync: true in exactly one lane (the lowest active one) of a converged
+// warp. MMA issue roles run on the whole warp (so descriptors and loop state
+// are warp-uniform and live in uniform registers) and issue tcgen05.mma /
+// tcgen05.commit from the elected lane; a `lane == 0` region instead makes the
+// compiler wrap every UTCHMMA in a uniformity waterfall loop.
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "elect.sync _|P, 0xffffffff;\n\t"
+        "selp.b32 %0, 1, 0, P;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b,
                                           uint32_t idesc, uint32_t accumulate) {
     asm volatile(
