@@ -478,8 +478,7 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
     pdl_trigger();
 
     if (warp == 0) {
-        if (lane == 0) {
-            // ---------------- TMA producer
+        {   // ---------------- TMA producer (whole warp waits, the elected lane issues)
             int stage = 0;
             uint32_t phase = 0;
             TcSched sch;
@@ -493,7 +492,8 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* a = sA + stage * Cfg::A_BYTES;
                     uint8_t* b = sB + stage * Cfg::B_BYTES;
-                    if (CG == 1) {
+                    if (!elect_one()) {
+                    } else if (CG == 1) {
                         if (!A_MN) {
                             tma_load_2d(a, &tmA, &full[stage], kb * TC_BK, am);
                         } else {
@@ -528,13 +528,14 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
                         }
                         if (rank != 0) mbar_arrive_cluster(fb);
                     }
+                    __syncwarp();
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && rank == 0) {
-            // ---------------- MMA issuer (single thread; the pair leader for CG = 2)
+        if (rank == 0) {
+            // ---------------- MMA issuer (whole warp of the pair leader; the elected lane issues)
             const uint32_t idesc = tc_idesc<BN, A_MN, B_MN, CG>();
             int stage = 0;
             uint32_t phase = 0;
@@ -553,6 +554,7 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
                     tc_fence_after();
                     const uint32_t a_addr = smem_u32(sA + stage * Cfg::A_BYTES);
                     const uint32_t b_addr = smem_u32(sB + stage * Cfg::B_BYTES);
+                    if (elect_one()) {
 #pragma unroll
                     for (int k = 0; k < TC_BK / 16; ++k) {
                         // K-major: 16 elements = 32 bytes inside the 128B swizzle atom row;
@@ -567,10 +569,15 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
                     }
                     if (CG == 2) umma_commit_pair(&empty[stage], 3);
                     else umma_commit(&empty[stage]);
+                    }
+                    __syncwarp();
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                if (CG == 2) umma_commit_pair(&tfull[acc], 3);
-                else umma_commit(&tfull[acc]);
+                if (elect_one()) {
+                    if (CG == 2) umma_commit_pair(&tfull[acc], 3);
+                    else umma_commit(&tfull[acc]);
+                }
+                __syncwarp();
             }
         }
     } else if (warp >= 4) {
