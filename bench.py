@@ -183,6 +183,96 @@ def capacity(p, strategies=("1f1b", "tpipe", "tpipe_trecomp", "tpipe_all")):
     return out
 
 
+def gemm_traffic():
+    """Per-launch DRAM traffic of the tcgen05 GEMM class from the committed
+    `ncu --set full` capture of the 12 layer GEMM shapes (scripts/
+    gemm_shapes_once.py): mean dram__bytes_read.sum + dram__bytes_write.sum."""
+    path = os.path.join(ROOT, "profiles", "r1_gemm_ncu_full_v2.jsonl")
+    try:
+        with open(path) as f:
+            for line in f:
+                d = json.loads(line)
+                if "summary" in d:
+                    return int(d["mean_dram_bytes"]), int(d["mean_alg_bytes"])
+    except Exception:
+        pass
+    return None, None
+
+
+def host_link_peak():
+    """Pinned host <-> HBM copy bandwidth (GB/s) for 1 GiB, best of 3 each way."""
+    import torch
+    n = 1 << 30
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(n, dtype=torch.uint8, device="cuda")
+    out = {}
+    for name, fn in (("h2d", lambda: d.copy_(h, non_blocking=True)),
+                     ("d2h", lambda: h.copy_(d, non_blocking=True))):
+        best = 1e30
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        out[name + "_GBs"] = round(n / (best / 1e3) / 1e9, 1)
+    del h, d
+    return out
+
+
+def measure_offload(N, m, dtok, dtgt, args, base_ms):
+    """T-Offload of the deep chunk's model states on top of T-Recomp at
+    N=1: step time, the copy engines' busy time and achieved host-link GB/s,
+    the host AdamW time, and the overlap fraction
+    1 - (t_offload - t_trecomp) / (D2H + host AdamW + H2D)."""
+    import torch
+    from paper_2503_03182_b200 import plan as P, runtime as RT
+    c = C2
+    md = P.Model(c["n_layers"], c["hidden"], c["n_heads"], c["ffn_hidden"], c["vocab"],
+                 c["seq_len"], c["micro_batch"], P.BF16)
+    plan = P.Plan(md, N, m, strategy="tpipe_trecomp", offload=1)
+    rt = RT.Runtime(plan, stage=-1, lr=1e-4)
+    rng = np.random.default_rng(99)
+    for s in range(N):
+        for ch in range(1, plan.v + 1):
+            rt.set_params(s, ch, init_chunk(plan, s, ch, rng))
+    ext = torch.cuda.ExternalStream(rt.stream())
+    for _ in range(2):
+        rt.step_device(dtok.data_ptr(), dtgt.data_ptr())
+    torch.cuda.synchronize()
+    k = max(2, args.steps // 2)
+    tot = 0.0
+    st = None
+    for _ in range(k):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(ext)
+        rt.step_device(dtok.data_ptr(), dtgt.data_ptr())
+        e1.record(ext)
+        torch.cuda.synchronize()
+        tot += e0.elapsed_time(e1)
+        st = rt.stats()
+    ms = tot / k
+    d2h_b, h2d_b = st["offload_d2h_bytes"], st["offload_h2d_bytes"]
+    d2h_ms, h2d_ms, host_ms = st["offload_d2h_ms"], st["offload_h2d_ms"], st["host_opt_ms"]
+    serial = d2h_ms + h2d_ms + host_ms
+    exposed = max(0.0, ms - base_ms)
+    res = {"strategy": "tpipe_trecomp + T-Offload(model states of chunk 2)",
+           "tokens_s": round(m * c["seq_len"] / (ms / 1e3), 1), "ms_per_step": round(ms, 2),
+           "plan_peak_GiB": round(plan.peak(0)["total_peak"] / 2 ** 30, 2),
+           "d2h_bytes": int(d2h_b), "h2d_bytes": int(h2d_b),
+           "d2h_ms": round(d2h_ms, 2), "h2d_ms": round(h2d_ms, 2), "host_adamw_ms": round(host_ms, 2),
+           "d2h_GBs": round(d2h_b / (d2h_ms / 1e3) / 1e9, 1) if d2h_ms else None,
+           "h2d_GBs": round(h2d_b / (h2d_ms / 1e3) / 1e9, 1) if h2d_ms else None,
+           "exposed_ms": round(exposed, 2),
+           "overlap_fraction": round(1.0 - min(1.0, exposed / serial), 3) if serial else None,
+           "note": "p=1: the Eq. 5/7 windows 2(p-b-1), (p-a-1) T_unit are empty at one stage, "
+                   "so only the copy-engine / host-thread concurrency with the remaining "
+                   "backward and next forward hides the offload"}
+    rt.close()
+    return res
+
+
 def quick_measure(strategy, N, m, dtok, dtgt, args):
     """tokens/s of another schedule on the same kernels/workload (N=1)."""
     import torch
@@ -296,6 +386,13 @@ def run_tpipe(args):
     e2e = tokens * args.steps / (ms_e2e / 1e3)
     hbm, pk_burst, pk_sust, src = peaks()
     gemm_tf = kfl[0] / (kms[0] / 1e3) / 1e12 if kms[0] else None
+    # executed FLOPs per step: every GEMM launch (incl. recompute), attention
+    # forward, and attention backward at 7 of its 5 algorithmic GEMMs (S and dP
+    # are recomputed in both the dK/dV and the dQ kernel)
+    hw_flops = (kfl[0] + kfl[1] + kfl[2] * 7.0 / 5.0) / args.steps
+    mk, busy = plan.simulate()   # unit-model replay of this plan (F=1, B=2, R=1 T_unit)
+    bubble = [round(1.0 - b / mk, 4) for b in busy[:N]] if mk else None
+    traffic, alg_bytes = gemm_traffic()
     step_ms = ms / args.steps
     prof_step_ms = None
     out = None
@@ -313,7 +410,9 @@ def run_tpipe(args):
                        "layers_per_chunk": list(plan.layers_chunk),
                        "l2": "working set >> 126 MB L2 (no flush needed)"},
             "mfu": round(mfu, 4),
+            "hfu": round(hw_flops / (step_ms / 1e3) / (N * pk_sust * 1e12), 4),
             "mfu_peak": f"{pk_sust} TFLOP/s bf16 sustained ({src})",
+            "bubble_fraction_unit_model": bubble,
             "gpu_launches": int(launches) * args.steps,
             "pool_high_water_bytes": hw,
             "e2e": {"value": round(e2e, 1), "unit": "tokens/s",
@@ -322,7 +421,10 @@ def run_tpipe(args):
                          "achieved": round(gemm_tf, 1) if gemm_tf else None, "peak": pk_sust,
                          "unit": "TFLOP/s",
                          "frac": round(gemm_tf / pk_sust, 4) if gemm_tf else None,
-                         "traffic": None, "peak_src": f"bf16_tflops_sustained ({src})",
+                         "traffic": traffic, "traffic_alg_bytes": alg_bytes,
+                         "traffic_src": "profiles/r1_gemm_ncu_full_v2.jsonl: mean DRAM bytes per launch "
+                                        "over the 12 layer GEMM shapes (ncu --set full)",
+                         "peak_src": f"bf16_tflops_sustained ({src})",
                          "launches_per_step": int(kcnt[0] / args.steps),
                          "share_of_step": round(kms[0] / args.steps / step_ms, 3)},
             "kernel_classes": {
@@ -348,6 +450,12 @@ def run_tpipe(args):
                 continue
             comp[st] = quick_measure(st, N, m, dtok, dtgt, args)
         out["compare"] = comp
+        try:
+            comp["tpipe_trecomp_offload"] = measure_offload(N, m, dtok, dtgt, args,
+                                                            comp["tpipe_trecomp"]["ms_per_step"])
+        except Exception as e:   # reported, not fatal
+            comp["tpipe_trecomp_offload"] = {"error": str(e)[:200]}
+        out["host_link_peak"] = host_link_peak()
         out["capacity_80GiB"] = {"p": max(N, 8) if N == 1 else N, "shape": "h=4096 a=32 s=8192 V=32000 b=1 m=32",
                                  **capacity(max(N, 8) if N == 1 else N)}
         out["cpu_baseline"] = cpu_baseline(c)

@@ -191,6 +191,9 @@ typedef struct {
     double   kernel_ms[4];
     double   kernel_flops[4];
     int64_t  kernel_count[4];
+    /* copy-engine time of the last step's offload copies (sum of CUDA-event
+     * spans on the D2H / H2D side streams, ms); bytes / ms = host-link GB/s */
+    double   offload_d2h_ms, offload_h2d_ms;
 } tpipe_runtime_stats;
 
 typedef struct tpipe_runtime tpipe_runtime;

@@ -111,6 +111,10 @@ struct tpipe_runtime {
     long t = 0;
     long launches_last = 0;
     double d2h_bytes = 0, h2d_bytes = 0;
+    // timing-enabled event pairs bracketing each offload copy of the last step
+    std::vector<cudaEvent_t> tevpool;
+    size_t tevnext = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> d2h_ev, h2d_ev;
     int* h_tok_stage = nullptr;   // pinned staging for tpipe_step host inputs
     size_t h_tok_bytes = 0;
     std::vector<cudaEvent_t> evpool;
@@ -122,6 +126,26 @@ struct tpipe_runtime {
 };
 
 namespace {
+
+cudaEvent_t next_timed_event(tpipe_runtime* rt) {
+    if (rt->tevnext == rt->tevpool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        rt->tevpool.push_back(e);
+    }
+    return rt->tevpool[rt->tevnext++];
+}
+
+// offload copy on a copy-engine stream, bracketed by timing events
+cudaError_t timed_copy(tpipe_runtime* rt, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind,
+                       cudaStream_t st, bool down) {
+    cudaEvent_t a = next_timed_event(rt), b = next_timed_event(rt);
+    cudaError_t e = cudaEventRecord(a, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dst, src, bytes, kind, st);
+    if (e == cudaSuccess) e = cudaEventRecord(b, st);
+    (down ? rt->d2h_ev : rt->h2d_ev).push_back({a, b});
+    return e;
+}
 
 cudaEvent_t next_event(tpipe_runtime* rt) {
     if (rt->evnext == rt->evpool.size()) {
@@ -343,7 +367,7 @@ int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags
             cudaEvent_t e0 = next_event(rt);
             CU(cudaEventRecord(e0, cs));
             CU(cudaStreamWaitEvent(rt->d2h, e0, 0));
-            CU(cudaMemcpyAsync(C.h_grad, C.grad, (size_t)C.P * 4, cudaMemcpyDeviceToHost, rt->d2h));
+            CU(timed_copy(rt, C.h_grad, C.grad, (size_t)C.P * 4, cudaMemcpyDeviceToHost, rt->d2h, true));
             CU(cudaMemsetAsync(C.grad, 0, (size_t)C.P * 4, rt->d2h));
             CU(cudaEventRecord(C.ev_d2h, rt->d2h));
             C.d2h_pending = true;
@@ -360,7 +384,7 @@ int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags
         case TPIPE_OP_W_H2D: {
             ChunkState& C = S.ch[c];
             join_host(C);
-            CU(cudaMemcpyAsync(C.w, C.h_w, (size_t)C.P * D.es, cudaMemcpyHostToDevice, rt->h2d));
+            CU(timed_copy(rt, C.w, C.h_w, (size_t)C.P * D.es, cudaMemcpyHostToDevice, rt->h2d, false));
             CU(cudaEventRecord(C.ev_h2d, rt->h2d));
             C.h2d_pending = true;
             rt->h2d_bytes += (double)C.P * D.es;
@@ -389,7 +413,7 @@ int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags
             cudaEvent_t e0 = next_event(rt), e1 = next_event(rt);
             CU(cudaEventRecord(e0, cs));
             CU(cudaStreamWaitEvent(rt->d2h, e0, 0));
-            CU(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, rt->d2h));
+            CU(timed_copy(rt, host, dev, bytes, cudaMemcpyDeviceToHost, rt->d2h, true));
             CU(cudaEventRecord(e1, rt->d2h));
             S.act_ev_d2h[i] = e1;
             rt->d2h_bytes += (double)bytes;
@@ -406,7 +430,7 @@ int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags
             cudaEvent_t e0 = next_event(rt), e1 = next_event(rt);
             CU(cudaEventRecord(e0, cs));   // previous users of `dev` are done
             CU(cudaStreamWaitEvent(rt->h2d, e0, 0));
-            CU(cudaMemcpyAsync(dev, host, (size_t)C.sl.total, cudaMemcpyHostToDevice, rt->h2d));
+            CU(timed_copy(rt, dev, host, (size_t)C.sl.total, cudaMemcpyHostToDevice, rt->h2d, false));
             CU(cudaEventRecord(e1, rt->h2d));
             S.act_ev_h2d[i] = e1;
             rt->h2d_bytes += (double)C.sl.total;
@@ -445,6 +469,9 @@ int run_step(tpipe_runtime* rt, const int32_t* tok_dev, const int32_t* tgt_dev, 
     cudaStream_t cs = rt->stream;
     const size_t io_bytes = (size_t)P.m * D.M * 4;
     rt->evnext = 0;
+    rt->tevnext = 0;
+    rt->d2h_ev.clear();
+    rt->h2d_ev.clear();
     rt->d2h_bytes = rt->h2d_bytes = 0;
     const long l0 = launch_count();
     profiler().begin_step((flags & TPIPE_STEP_PROFILE) != 0);
@@ -767,6 +794,17 @@ TP_API int tpipe_runtime_get_stats(const tpipe_runtime* rt, tpipe_runtime_stats*
     out->offload_h2d_bytes = rt->h2d_bytes;
     for (int s : rt->owned)
         for (auto& C : rt->st[s]->ch) out->host_opt_ms += C.host_ms;
+    auto span_ms = [](const std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
+        double ms = 0;
+        for (auto& pr : v) {
+            float x = 0;
+            if (cudaEventSynchronize(pr.second) == cudaSuccess && cudaEventElapsedTime(&x, pr.first, pr.second) == cudaSuccess)
+                ms += x;
+        }
+        return ms;
+    };
+    out->offload_d2h_ms = span_ms(rt->d2h_ev);
+    out->offload_h2d_ms = span_ms(rt->h2d_ev);
     for (int c = 0; c < 4; ++c) {
         out->kernel_ms[c] = rt->kms[c];
         out->kernel_flops[c] = rt->kflops[c];

@@ -77,7 +77,8 @@ class Runtime:
                     step=s.step, offload_d2h_bytes=s.offload_d2h_bytes,
                     offload_h2d_bytes=s.offload_h2d_bytes, host_opt_ms=s.host_opt_ms,
                     kernel_ms=list(s.kernel_ms), kernel_flops=list(s.kernel_flops),
-                    kernel_count=list(s.kernel_count))
+                    kernel_count=list(s.kernel_count), offload_d2h_ms=s.offload_d2h_ms,
+                    offload_h2d_ms=s.offload_h2d_ms)
 
     def stream(self) -> int:
         return lib().tpipe_runtime_stream(self._h) or 0
