@@ -20,14 +20,39 @@ static inline uint16_t f32_to_bf16_rne(float f) {
     return (uint16_t)(u >> 16);
 }
 
-static void adamw_host_range(float* master, float* m, float* v, const float* grad,
-                             uint16_t* w_bf16, long lo, long hi, int decay, const AdamHyper& hp) {
-    for (long i = lo; i < hi; ++i) {
-        AdamOut o = adam_elem(master[i], m[i], v[i], grad[i], decay, hp);
-        master[i] = o.w;
-        m[i] = o.m;
-        v[i] = o.v;
-        if (w_bf16) w_bf16[i] = f32_to_bf16_rne(o.w);
+// branch-free RNE (vectorisable); NaN -> quiet NaN as above
+static inline uint16_t f32_to_bf16_rne_v(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    const uint32_t r = (u + 0x7fffu + ((u >> 16) & 1u)) >> 16;
+    const uint32_t q = (u >> 16) | 0x40u;
+    return (uint16_t)(((u & 0x7fffffffu) > 0x7f800000u) ? q : r);
+}
+
+// The loop is compiled -O3 -fno-math-errno (sqrt inline) with FMA contraction
+// off, in AVX-512 / AVX2 / baseline clones picked at load time: vector
+// mul/add/div/sqrt are correctly rounded IEEE ops, so every clone is
+// bit-identical to the scalar arithmetic and to the device kernel.
+__attribute__((target_clones("avx512f", "avx2", "default")))
+static void adamw_host_range(float* __restrict__ master, float* __restrict__ m, float* __restrict__ v,
+                             const float* __restrict__ grad, uint16_t* __restrict__ w_bf16, long lo, long hi,
+                             int decay, const AdamHyper& hp) {
+    const AdamHyper h = hp;
+    if (w_bf16) {
+        for (long i = lo; i < hi; ++i) {
+            AdamOut o = adam_elem(master[i], m[i], v[i], grad[i], decay, h);
+            master[i] = o.w;
+            m[i] = o.m;
+            v[i] = o.v;
+            w_bf16[i] = f32_to_bf16_rne_v(o.w);
+        }
+    } else {
+        for (long i = lo; i < hi; ++i) {
+            AdamOut o = adam_elem(master[i], m[i], v[i], grad[i], decay, h);
+            master[i] = o.w;
+            m[i] = o.m;
+            v[i] = o.v;
+        }
     }
 }
 
