@@ -77,6 +77,15 @@ enum {
 
 #define TPIPE_OFFLOAD_MODEL_STATE 1   /* T-Offload of chunk-2 grads/optimizer/weights */
 #define TPIPE_OFFLOAD_ACTIVATIONS 2   /* chunk-1 stash to pinned host and back (R23) */
+/* With TPIPE_OFFLOAD_MODEL_STATE: run the offloaded chunk's AdamW on the
+ * device instead of the host (SURVEY §8(d), B200-native option for Q11;
+ * DESIGN R24). fp32 master / m / v stay in pinned host memory and are streamed
+ * through a double-buffered device staging area in slices of
+ * TPIPE_SOPT_SLICE_PARAMS parameters (H2D -> device AdamW -> D2H); the fp32
+ * grads never leave HBM and the bf16 weights are written in place. The
+ * staging area, 2 x min(P, slice) x 12 bytes, is static model-state memory. */
+#define TPIPE_OFFLOAD_DEVICE_OPT 4
+#define TPIPE_SOPT_SLICE_PARAMS 8388608
 
 typedef struct {
     int32_t strategy;      /* TPIPE_S_*, or -1 = auto: escalate TPIPE -> TPIPE_TRECOMP ->
@@ -97,7 +106,9 @@ enum {
     TPIPE_OP_ACT_D2H = 13,       /* copy STASH(1,i) to pinned host (after F) */
     TPIPE_OP_ACT_D2H_WAIT = 14,  /* copy done -> release STASH(1,i) on the device */
     TPIPE_OP_ACT_H2D = 15,       /* re-allocate STASH(1,i), start the prefetch */
-    TPIPE_OP_ACT_H2D_WAIT = 16   /* prefetch landed (before B(1,i)) */
+    TPIPE_OP_ACT_H2D_WAIT = 16,  /* prefetch landed (before B(1,i)) */
+    TPIPE_OP_STREAM_OPT = 17     /* TPIPE_OFFLOAD_DEVICE_OPT: streamed device AdamW of the
+                                    offloaded chunk (replaces GRAD_D2H, HOST_OPT, W_H2D) */
 };
 
 /* One instruction of a stage's stream. Buffers listed in

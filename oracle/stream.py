@@ -91,6 +91,15 @@ def model_state_bytes(d: ModelDesc, P: int, offloaded: bool) -> int:
     return P * (d.es + 4 + master + 8)
 
 
+SOPT_SLICE = 8388608   # parameters per streamed-optimizer slice (include/tpipe.h)
+
+
+def sopt_staging_bytes(P: int) -> int:
+    """Streamed device AdamW (R24; SURVEY §8(d) B200-native option
+    for Q11): fp32 master, m, v (12 B/param) of one slice, double-buffered."""
+    return 2 * 12 * min(P, SOPT_SLICE)
+
+
 def n_partials(M: int) -> int:
     """Row blocks of 16 for deterministic column reductions."""
     return -(-M // 16)
@@ -142,7 +151,7 @@ def sizes(d: ModelDesc, p: int, v: int, s: int, c: int, full_recomp: bool = Fals
 class Instr:
     kind: str                      # F B R RECV_ACT RECV_GRAD SEND_ACT SEND_GRAD SEND_WAIT
                                    # OPT GRAD_D2H HOST_OPT W_H2D W_WAIT
-                                   # ACT_D2H ACT_D2H_WAIT ACT_H2D ACT_H2D_WAIT
+                                   # ACT_D2H ACT_D2H_WAIT ACT_H2D ACT_H2D_WAIT STREAM_OPT
     chunk: int = 0
     mb: int = 0
     peer: int = -1
@@ -184,12 +193,15 @@ def act_offload_sets(order, d_release: int, d_prefetch: int):
 
 def build_streams(d: ModelDesc, p: int, m: int, strategy: str, k=None,
                   window: int = 2, offload_model_state: bool = False,
-                  offload_activations: bool = False, act_distance: int = 2):
+                  offload_activations: bool = False, act_distance: int = 2,
+                  offload_device_opt: bool = False):
     """Per-stage instruction streams. Returns (streams, static)
     where static[s] = list of (name, category, bytes) live for the whole step."""
     ostrat, v, trecomp, full = STRATS[strategy]
     if offload_model_state and v != 2:
         raise ValueError("offload requires v=2")
+    if offload_device_opt and not offload_model_state:
+        raise ValueError("device optimizer streaming applies to model-state offload")
     if offload_activations and (v != 2 or trecomp):
         raise ValueError("activation offload applies to T-Pipe chunk 1 (no T-Recomp)")
     orders = S.strategy_orders(ostrat, p, m, k=k)[0]
@@ -202,7 +214,8 @@ def build_streams(d: ModelDesc, p: int, m: int, strategy: str, k=None,
         for c in range(1, v + 1):
             P = chunk_params(d, p, v, s, c)
             off = offload_model_state and c == v
-            st.append((f"MS{c}", "model_state", model_state_bytes(d, P, off)))
+            extra = sopt_staging_bytes(P) if (off and offload_device_opt) else 0
+            st.append((f"MS{c}", "model_state", model_state_bytes(d, P, off) + extra))
         if s == 0:
             st.append(("TOKENS", "io", 4 * m * d.tokens))
         if s == p - 1:
@@ -302,13 +315,15 @@ def build_streams(d: ModelDesc, p: int, m: int, strategy: str, k=None,
                 out.append(Instr("ACT_D2H", 1, i))
             # 5. optimizer / offload after the chunk's last backward
             if kind == "B" and i == last_b[c]:
-                if offload_model_state and c == v:
+                if offload_model_state and c == v and offload_device_opt:
+                    out.append(Instr("STREAM_OPT", chunk=c))
+                elif offload_model_state and c == v:
                     out.append(Instr("GRAD_D2H", chunk=c))
                     out.append(Instr("HOST_OPT", chunk=c))
                 else:
                     out.append(Instr("OPT", chunk=c))
             # weight upload right after the stage's first forward
-            if offload_model_state and not first_op_done and kind == "F":
+            if offload_model_state and not offload_device_opt and not first_op_done and kind == "F":
                 out.append(Instr("W_H2D", chunk=v))
             first_op_done = first_op_done or kind == "F"
         # 6. flush outstanding sends (channels sorted, then message order)

@@ -259,6 +259,7 @@ static int build(tpipe_plan* P, bool trecomp, bool full_recomp) {
     }
 
     const bool off = (P->offload & TPIPE_OFFLOAD_MODEL_STATE) != 0;
+    const bool sopt = off && (P->offload & TPIPE_OFFLOAD_DEVICE_OPT) != 0;
     const bool aoff_on = (P->offload & TPIPE_OFFLOAD_ACTIVATIONS) != 0 && v == 2 && !trecomp;
     const uint64_t es = d.dtype == TPIPE_BF16 ? 2 : 4;
     const uint64_t M = (uint64_t)d.micro_batch * d.seq_len;
@@ -273,7 +274,9 @@ static int build(tpipe_plan* P, bool trecomp, bool full_recomp) {
             P->params_total += np;
             const bool o = off && c == v;
             const uint64_t per = o ? (es + 4) : (es + 4 + (d.dtype == TPIPE_BF16 ? 4 : 0) + 8);
-            B.bufs.push_back({TPIPE_BUF_STATIC, TPIPE_CAT_MODEL_STATE, c, 0, np * per});
+            // streamed device AdamW (R24): + double-buffered master/m/v slice staging
+            const uint64_t stg = (o && sopt) ? 2ull * 12ull * std::min<uint64_t>(np, TPIPE_SOPT_SLICE_PARAMS) : 0;
+            B.bufs.push_back({TPIPE_BUF_STATIC, TPIPE_CAT_MODEL_STATE, c, 0, np * per + stg});
         }
         if (s == 0) B.bufs.push_back({TPIPE_BUF_STATIC, TPIPE_CAT_IO, 0, 0, 4ull * m * M});
         if (s == p - 1) B.bufs.push_back({TPIPE_BUF_STATIC, TPIPE_CAT_IO, 0, 1, 4ull * m * M + 4ull * m});
@@ -407,7 +410,9 @@ static int build(tpipe_plan* P, bool trecomp, bool full_recomp) {
             if (kind == KF && c == 1 && aoff.count(i)) B.emit(TPIPE_OP_ACT_D2H, 1, i, -1, -1, -1, {});
             // 5. optimizer after the chunk's last backward
             if (kind == KB && i == last_b[c]) {
-                if (off && c == v) {
+                if (off && c == v && sopt) {
+                    B.emit(TPIPE_OP_STREAM_OPT, c, 0, -1, -1, -1, {});
+                } else if (off && c == v) {
                     B.emit(TPIPE_OP_GRAD_D2H, c, 0, -1, -1, -1, {});
                     B.emit(TPIPE_OP_HOST_OPT, c, 0, -1, -1, -1, {});
                 } else {
@@ -415,7 +420,7 @@ static int build(tpipe_plan* P, bool trecomp, bool full_recomp) {
                 }
             }
             // 6. weight upload after the first forward
-            if (off && !first_f_done && kind == KF) B.emit(TPIPE_OP_W_H2D, v, 0, -1, -1, -1, {});
+            if (off && !sopt && !first_f_done && kind == KF) B.emit(TPIPE_OP_W_H2D, v, 0, -1, -1, -1, {});
             first_f_done = first_f_done || kind == KF;
         }
         // flush outstanding sends, channels in id order (= sorted (kind, src, dst))
@@ -535,6 +540,8 @@ using namespace tpipe;
 
 static int make_plan(const tpipe_model_desc* model, int p, int m, int strategy, int k, int W,
                      int offload, int act_distance, tpipe_plan** out) {
+    if ((offload & TPIPE_OFFLOAD_DEVICE_OPT) && !(offload & TPIPE_OFFLOAD_MODEL_STATE))
+        return set_error(TPIPE_E_INVALID, "offload: DEVICE_OPT needs MODEL_STATE");
     if ((offload & TPIPE_OFFLOAD_ACTIVATIONS) && strategy != TPIPE_S_TPIPE)
         return set_error(TPIPE_E_INCOMPAT, "activation offload applies to T-Pipe without T-Recomp");
     tpipe_plan* P = new (std::nothrow) tpipe_plan();

@@ -68,6 +68,14 @@ struct ChunkState {
     bool d2h_pending = false, h2d_pending = false;
     std::thread host_thr;
     double host_ms = 0;
+    // streamed device AdamW (TPIPE_OFFLOAD_DEVICE_OPT, DESIGN R24): two
+    // staging slots of [master | m | v] x slice fp32 in the static block
+    bool sopt = false;
+    long slice = 0;
+    float* stg[2] = {nullptr, nullptr};
+    cudaEvent_t ev_sopt_done = nullptr;   // last slice's AdamW done (w, grad final)
+    cudaEvent_t ev_sopt_out = nullptr;    // last slice's master/m/v back on the host
+    bool sopt_done_pending = false, sopt_out_pending = false;
 };
 
 struct StageState {
@@ -104,7 +112,7 @@ struct tpipe_runtime {
     std::vector<std::unique_ptr<StageState>> st;   // indexed by stage (null if not owned)
     std::vector<Channel> ch;
     Pool pool;
-    cudaStream_t stream = nullptr, d2h = nullptr, h2d = nullptr;
+    cudaStream_t stream = nullptr, d2h = nullptr, h2d = nullptr, opt = nullptr;
     cudaEvent_t ev_tmp = nullptr;
     AdamHyper hp{};
     float lr = 3e-4f, b1 = 0.9f, b2 = 0.95f, eps = 1e-8f, wd = 0.1f;
@@ -215,6 +223,62 @@ void host_opt_run(tpipe_runtime* rt, ChunkState* C, AdamHyper hp) {
 
 void join_host(ChunkState& C) {
     if (C.host_thr.joinable()) C.host_thr.join();
+    if (C.sopt_out_pending) {
+        cudaEventSynchronize(C.ev_sopt_out);
+        C.sopt_out_pending = false;
+    }
+}
+
+// Streamed device AdamW of an offloaded chunk (R24): slice k's fp32
+// master/m/v go H2D into staging slot k&1 (h2d stream), the AdamW kernel
+// updates them with the chunk's device grads and writes the bf16 weights in
+// place (opt stream), and the slice returns D2H (d2h stream); slot reuse waits
+// for the D2H of slice k-2. Same kernel and per-segment decay as OPT, so the
+// parameters are bit-identical to the device and host optimizers.
+int stream_opt(tpipe_runtime* rt, ChunkState& C, const AdamHyper& hp, cudaStream_t cs) {
+    const int dt = rt->D.dtype;
+    cudaEvent_t ready = next_event(rt);
+    CU(cudaEventRecord(ready, cs));                      // the chunk's grads are final
+    CU(cudaStreamWaitEvent(rt->h2d, ready, 0));
+    CU(cudaStreamWaitEvent(rt->opt, ready, 0));
+    if (C.sopt_out_pending) CU(cudaStreamWaitEvent(rt->h2d, C.ev_sopt_out, 0));   // last step's D2H
+    const long SL = C.slice;
+    std::vector<cudaEvent_t> out_ev;
+    int k = 0;
+    for (long lo = 0; lo < C.P; lo += SL, ++k) {
+        const long n = std::min(SL, C.P - lo);
+        float* st = C.stg[k & 1];
+        if (k >= 2) CU(cudaStreamWaitEvent(rt->h2d, out_ev[k - 2], 0));
+        CU(timed_copy(rt, st, C.h_master + lo, (size_t)n * 4, cudaMemcpyHostToDevice, rt->h2d, false));
+        CU(timed_copy(rt, st + SL, C.h_m + lo, (size_t)n * 4, cudaMemcpyHostToDevice, rt->h2d, false));
+        CU(timed_copy(rt, st + 2 * SL, C.h_v + lo, (size_t)n * 4, cudaMemcpyHostToDevice, rt->h2d, false));
+        rt->h2d_bytes += (double)n * 12;
+        cudaEvent_t in = next_event(rt);
+        CU(cudaEventRecord(in, rt->h2d));
+        CU(cudaStreamWaitEvent(rt->opt, in, 0));
+        for (auto& sg : C.lay.segments) {
+            const long a = std::max(lo, (long)sg[0]), b = std::min(lo + n, (long)(sg[0] + sg[1]));
+            if (a >= b) continue;
+            const long r = a - lo;
+            void* w = dt == DT_BF16 ? (void*)((uint16_t*)C.w + a) : (void*)((float*)C.w + a);
+            if (adamw(dt, st + r, st + SL + r, st + 2 * SL + r, C.grad + a, w, b - a, (int)sg[2], hp, rt->opt))
+                return set_error(TPIPE_E_CUDA, "adamw launch failed");
+        }
+        cudaEvent_t done = next_event(rt);
+        CU(cudaEventRecord(done, rt->opt));
+        CU(cudaStreamWaitEvent(rt->d2h, done, 0));
+        CU(timed_copy(rt, C.h_master + lo, st, (size_t)n * 4, cudaMemcpyDeviceToHost, rt->d2h, true));
+        CU(timed_copy(rt, C.h_m + lo, st + SL, (size_t)n * 4, cudaMemcpyDeviceToHost, rt->d2h, true));
+        CU(timed_copy(rt, C.h_v + lo, st + 2 * SL, (size_t)n * 4, cudaMemcpyDeviceToHost, rt->d2h, true));
+        rt->d2h_bytes += (double)n * 12;
+        cudaEvent_t out = next_event(rt);
+        CU(cudaEventRecord(out, rt->d2h));
+        out_ev.push_back(out);
+    }
+    CU(cudaEventRecord(C.ev_sopt_done, rt->opt));
+    CU(cudaEventRecord(C.ev_sopt_out, rt->d2h));
+    C.sopt_done_pending = C.sopt_out_pending = true;
+    return 0;
 }
 
 // ------------------------------------------------------------------ one instruction
@@ -390,8 +454,15 @@ int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags
             rt->h2d_bytes += (double)C.P * D.es;
             break;
         }
+        case TPIPE_OP_STREAM_OPT: {
+            if (no_opt) break;
+            TRY(stream_opt(rt, S.ch[c], hyper(rt, rt->t + 1), cs));
+            break;
+        }
         case TPIPE_OP_W_WAIT: {
             ChunkState& C = S.ch[c];
+            if (C.sopt_done_pending) CU(cudaStreamWaitEvent(cs, C.ev_sopt_done, 0));
+            C.sopt_done_pending = false;
             if (C.h2d_pending) CU(cudaStreamWaitEvent(cs, C.ev_h2d, 0));
             if (C.d2h_pending) CU(cudaStreamWaitEvent(cs, C.ev_d2h, 0));
             C.h2d_pending = C.d2h_pending = false;
@@ -551,6 +622,7 @@ TP_API int tpipe_runtime_create(const tpipe_plan* plan, const tpipe_runtime_opts
     CU(cudaStreamCreateWithFlags(&rt->stream, cudaStreamNonBlocking));
     CU(cudaStreamCreateWithFlags(&rt->d2h, cudaStreamNonBlocking));
     CU(cudaStreamCreateWithFlags(&rt->h2d, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&rt->opt, cudaStreamNonBlocking));
     const tpipe_plan& P = rt->plan;
     const Dims& D = rt->D;
     if (o.stage < 0) {
@@ -564,6 +636,7 @@ TP_API int tpipe_runtime_create(const tpipe_plan* plan, const tpipe_runtime_opts
         return set_error(TPIPE_E_CUDA, "pool: cudaMalloc of %llu bytes failed", (unsigned long long)need);
     rt->st.resize(P.p);
     const bool off = (P.offload & TPIPE_OFFLOAD_MODEL_STATE) != 0;
+    const bool sopt = off && (P.offload & TPIPE_OFFLOAD_DEVICE_OPT) != 0;
     for (int s : rt->owned) {
         rt->pool.set_cap(s, o.pool_cap ? o.pool_cap : P.peak[s].total_peak);
         auto S = std::make_unique<StageState>();
@@ -613,6 +686,14 @@ TP_API int tpipe_runtime_create(const tpipe_plan* plan, const tpipe_runtime_opts
                     else C.h_w = C.h_master;
                     CU(cudaEventCreateWithFlags(&C.ev_d2h, cudaEventDisableTiming));
                     CU(cudaEventCreateWithFlags(&C.ev_h2d, cudaEventDisableTiming));
+                    if (sopt) {   // staging slots follow w | grad in the static block
+                        C.sopt = true;
+                        C.slice = std::min<long>(C.P, TPIPE_SOPT_SLICE_PARAMS);
+                        C.stg[0] = (float*)q;
+                        C.stg[1] = C.stg[0] + 3 * C.slice;
+                        CU(cudaEventCreateWithFlags(&C.ev_sopt_done, cudaEventDisableTiming));
+                        CU(cudaEventCreateWithFlags(&C.ev_sopt_out, cudaEventDisableTiming));
+                    }
                 }
             } else if (b.category == TPIPE_CAT_IO) {
                 if (b.mb == 0) S->tokens = (int*)ptr;
@@ -671,6 +752,8 @@ TP_API void tpipe_runtime_destroy(tpipe_runtime* rt) {
             if (C.h_w && C.h_w != C.h_master) cudaFreeHost(C.h_w);
             if (C.ev_d2h) cudaEventDestroy(C.ev_d2h);
             if (C.ev_h2d) cudaEventDestroy(C.ev_h2d);
+            if (C.ev_sopt_done) cudaEventDestroy(C.ev_sopt_done);
+            if (C.ev_sopt_out) cudaEventDestroy(C.ev_sopt_out);
         }
     }
     if (const NcclApi* N = nccl())
@@ -679,11 +762,13 @@ TP_API void tpipe_runtime_destroy(tpipe_runtime* rt) {
     for (auto& c : rt->ch)
         if (c.st) cudaStreamDestroy(c.st);
     for (auto e : rt->evpool) cudaEventDestroy(e);
+    for (auto e : rt->tevpool) cudaEventDestroy(e);
     if (rt->h_tok_stage) cudaFreeHost(rt->h_tok_stage);
     rt->pool.release();
     cudaStreamDestroy(rt->stream);
     cudaStreamDestroy(rt->d2h);
     cudaStreamDestroy(rt->h2d);
+    cudaStreamDestroy(rt->opt);
     delete rt;
 }
 
@@ -743,6 +828,7 @@ TP_API int tpipe_runtime_get_grads(tpipe_runtime* rt, int32_t s, int32_t c, floa
     TRY(chunk_of(rt, s, c, n, &C));
     CU(cudaStreamSynchronize(rt->stream));
     CU(cudaStreamSynchronize(rt->d2h));
+    CU(cudaStreamSynchronize(rt->opt));
     CU(cudaMemcpyAsync(dst, C->grad, n * 4, cudaMemcpyDeviceToHost, rt->stream));
     CU(cudaStreamSynchronize(rt->stream));
     return 0;

@@ -15,9 +15,10 @@ STRATEGY = {"1f1b": S_1F1B, "1f1b_full_recomp": S_1F1B_FULL_RECOMP, "tpipe": S_T
             "tpipe_trecomp": S_TPIPE_TRECOMP}
 OFFLOAD_MODEL_STATE = 1
 OFFLOAD_ACTIVATIONS = 2
+OFFLOAD_DEVICE_OPT = 4   # with OFFLOAD_MODEL_STATE: streamed device AdamW (DESIGN R24)
 OP_NAMES = ["F", "B", "R", "RECV_ACT", "RECV_GRAD", "SEND_ACT", "SEND_GRAD", "SEND_WAIT", "OPT",
             "GRAD_D2H", "HOST_OPT", "W_H2D", "W_WAIT", "ACT_D2H", "ACT_D2H_WAIT", "ACT_H2D",
-            "ACT_H2D_WAIT"]
+            "ACT_H2D_WAIT", "STREAM_OPT"]
 CATS = ["model_state", "io", "act", "recomp_buf", "comm", "workspace"]
 
 

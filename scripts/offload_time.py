@@ -14,3 +14,4 @@ dtgt = torch.tensor(tgt, dtype=torch.int32, device="cuda")
 base = bench.quick_measure("tpipe_trecomp", 1, c["m"], dtok, dtgt, A)
 print(json.dumps({"tpipe_trecomp": base}))
 print(json.dumps(bench.measure_offload(1, c["m"], dtok, dtgt, A, base["ms_per_step"])))
+print(json.dumps(bench.measure_offload(1, c["m"], dtok, dtgt, A, base["ms_per_step"], device_opt=True)))

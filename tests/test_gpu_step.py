@@ -150,15 +150,42 @@ def test_offload_bitexact(dtype):
     _P, RT, _PR = mods()
     p, m = 4, 8
     res = []
-    for off in (0, 1):
+    P = mods()[0]
+    for off in (0, P.OFFLOAD_MODEL_STATE, P.OFFLOAD_MODEL_STATE | P.OFFLOAD_DEVICE_OPT):
         plan, rt, _W = build(C1, p, m, "tpipe_trecomp", dtype, offload=off)
         losses = []
         for step in range(3):
             tok, tgt = synth.tokens(C1["vocab"], m, C1["micro_batch"], C1["seq_len"], step=step)
             losses.append(rt.step(tok, tgt))
         res.append((losses, [rt.get_params(s, c) for s in range(p) for c in (1, 2)]))
+        st = rt.stats()
         if off:
-            assert rt.stats()["offload_d2h_bytes"] > 0
+            assert st["offload_d2h_bytes"] > 0 and st["offload_d2h_ms"] > 0
+        assert all(st["pool_high_water"][s] == plan.peak(s)["total_peak"] for s in range(p))
+    for r in res[1:]:
+        assert res[0][0] == r[0]
+        for a, b in zip(res[0][1], r[1]):
+            assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def test_device_opt_offload_multislice_bitexact():
+    """Streamed device AdamW (R24) with chunks of 4 slices (the slot reuse and
+    the cross-step ordering of the staging area are exercised): parameters
+    after 3 steps are bit-identical to the host optimizer's."""
+    P, RT, _PR = mods()
+    cfg = dict(n_layers=4, hidden=1024, n_heads=8, ffn_hidden=4096, vocab=512, seq_len=64,
+               micro_batch=1)
+    p, m = 1, 4
+    res = []
+    for off in (P.OFFLOAD_MODEL_STATE, P.OFFLOAD_MODEL_STATE | P.OFFLOAD_DEVICE_OPT):
+        plan, rt, _W = build(cfg, p, m, "tpipe_trecomp", P.BF16, offload=off)
+        assert plan.chunk_params(0, 2) > 3 * 8388608
+        losses = []
+        for step in range(3):
+            tok, tgt = synth.tokens(cfg["vocab"], m, 1, cfg["seq_len"], step=step)
+            losses.append(rt.step(tok, tgt))
+        res.append((losses, [rt.get_params(0, c) for c in (1, 2)]))
+        rt.close()
     assert res[0][0] == res[1][0]
     for a, b in zip(res[0][1], res[1][1]):
         assert np.array_equal(a.view(np.uint32), b.view(np.uint32))

@@ -107,6 +107,38 @@ def test_offload_streams_match_oracle(p):
         assert plan.peak(s)["total_peak"] == T.replay(st[s], static[s])["total_peak"]
 
 
+@pytest.mark.parametrize("p", [1, 2, 4, 8])
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_device_opt_offload_streams_match_oracle(p, dtype):
+    """Streamed device AdamW (R24): STREAM_OPT replaces GRAD_D2H / HOST_OPT /
+    W_H2D; the double-buffered slice staging is static model-state bytes, so
+    the peak is the host-optimizer plan's plus 2 * 12 * min(P, slice)."""
+    P = _plan_mod()
+    dt = T.BF16 if dtype == "bf16" else T.FP32
+    od = T.ModelDesc(2 * p, 64, 4, 256, 128, 32, 2, dt)
+    pd = P.Model(2 * p, 64, 4, 256, 128, 32, 2, P.BF16 if dtype == "bf16" else P.FP32)
+    flags = P.OFFLOAD_MODEL_STATE | P.OFFLOAD_DEVICE_OPT
+    plan = P.Plan(pd, p, 16, strategy="tpipe_trecomp", offload=flags)
+    host = P.Plan(pd, p, 16, strategy="tpipe_trecomp", offload=P.OFFLOAD_MODEL_STATE)
+    st, static = T.build_streams(od, p, 16, "tpipe_trecomp", offload_model_state=True,
+                                 offload_device_opt=True)
+    for s in range(p):
+        got, _ = plan.ops(s)
+        strip = [{k: o[k] for k in ("kind", "chunk", "mb", "peer", "channel", "msg")} for o in got]
+        assert strip == oracle_ops(st[s])
+        kinds = [o["kind"] for o in got]
+        assert kinds.count("STREAM_OPT") == 1
+        assert not {"GRAD_D2H", "HOST_OPT", "W_H2D"} & set(kinds)
+        assert kinds.count("W_WAIT") == 1
+        rep = T.replay(st[s], static[s])
+        assert plan.peak(s)["total_peak"] == rep["total_peak"]
+        extra = T.sopt_staging_bytes(plan.chunk_params(s, 2))
+        assert plan.peak(s)["total_peak"] == host.peak(s)["total_peak"] + extra
+    from paper_2503_03182_b200._lib import TPipeError
+    with pytest.raises(TPipeError):
+        P.Plan(pd, p, 16, strategy="tpipe_trecomp", offload=P.OFFLOAD_DEVICE_OPT)
+
+
 @pytest.mark.parametrize("strategy", ["tpipe", "tpipe_trecomp", "1f1b", "1f1b_full_recomp"])
 @pytest.mark.parametrize("p", [1, 2, 4, 5, 8, 16])
 def test_simulate_matches_oracle(strategy, p):
