@@ -245,8 +245,7 @@ constexpr int TC_BM = 128, TC_BK = 64;
 // column half (w - 4) / 4 of every tile, so the fused math runs on 2 warps per
 // scheduler and stays under the next tile's main loop (with 4 warps it was the
 // critical path of the dGELU GEMM: 775 -> 1029 TFLOP/s). The light epilogues
-// (store, bias, fp32 reduce-add) keep EW = 4 and the deeper operand ring that
-// the smaller staging area leaves room for.
+// (store, bias, fp32 reduce-add) keep EW = 4.
 __host__ __device__ constexpr int tc_threads(int ew) { return 128 + 32 * ew; }
 static bool g_stream_k_enabled = false;   // measured slower on the model shapes
 static bool g_pair_enabled = true;
@@ -259,13 +258,15 @@ void gemm_set_pair(int on) { g_pair_enabled = on != 0; }
 // and smem->tensor core) is 2/3 of the CG = 1, BN = 256 tile's.
 template <int BN, int CG = 1, int EPI_WARPS = 4>
 struct TcCfg {
-    static constexpr int STAGES = EPI_WARPS == 8 ? (CG == 2 ? 5 : (BN == 256 ? 3 : 5))
-                                                 : (CG == 2 ? 6 : (BN == 256 ? 4 : 6));
+    static constexpr int STAGES = CG == 2 ? 6 : (BN == 256 ? 4 : 6);
     static constexpr int A_BYTES = TC_BM * TC_BK * 2;
     static constexpr int B_BYTES = (BN / CG) * TC_BK * 2;
     static constexpr int TMEM_COLS = 2 * BN;
-    // epilogue staging: EPI_WARPS warps x 2 buffers x (32 rows x 128 B)
-    static constexpr int STAGING = EPI_WARPS * 2 * 4096;
+    // epilogue staging: EPI_WARPS warps x 2 buffers x one 32 x 32 chunk; the
+    // 8-warp epilogues (GELU, dGELU, residual) only store bf16 (2 KB chunks),
+    // so both variants fit the same operand ring depth
+    static constexpr int STG_BUF = EPI_WARPS == 8 ? 2048 : 4096;
+    static constexpr int STAGING = EPI_WARPS * 2 * STG_BUF;
     static constexpr int SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + STAGING + 256;
 };
 
@@ -584,7 +585,7 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
         // ---------------- epilogue: TMEM -> registers -> fused math -> swizzled smem -> TMA
         const int ew = warp & 3;             // TMEM lane quarter = tile rows [32ew, 32ew+32)
         const int chalf = (warp - 4) >> 2;   // column half of the tile
-        uint8_t* mystg = stg + (warp - 4) * 2 * 4096;
+        uint8_t* mystg = stg + (warp - 4) * 2 * Cfg::STG_BUF;
         const bool f32out = (g.epi == EPI_ACC_F32 || g.epi == EPI_STORE_F32);
         const bool reduce = (g.epi == EPI_ACC_F32);
         const bool two = (g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU);
@@ -666,10 +667,10 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
                     }
                 }
                 epi_math(g, m, n0, m < g.M, v, v2);
-                stage_store(mystg + sb * 4096, v, f32out, reduce, &tmC, n0, m0, lane);
+                stage_store(mystg + sb * Cfg::STG_BUF, v, f32out, reduce, &tmC, n0, m0, lane);
                 sb ^= 1;
                 if (two) {
-                    stage_store(mystg + sb * 4096, v2, false, false, &tmC2, n0, m0, lane);
+                    stage_store(mystg + sb * Cfg::STG_BUF, v2, false, false, &tmC2, n0, m0, lane);
                     sb ^= 1;
                 }
             }
@@ -847,6 +848,7 @@ static int launch_majors_ew(const GemmDesc& g, cudaStream_t st) {
 }
 template <int BN, int CG>
 static int launch_majors(const GemmDesc& g, cudaStream_t st) {
+    // (all three store bf16 only: the 8-warp variant stages 2 KB chunks)
     const bool heavy = g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU || g.epi == EPI_BIAS_RES;
     return heavy ? launch_majors_ew<BN, CG, 8>(g, st) : launch_majors_ew<BN, CG, 4>(g, st);
 }
