@@ -136,9 +136,9 @@ __device__ __forceinline__ uint32_t bf2(float lo, float hi) {
 // write 16 packed bf16x2 words (cols col0..col0+31, col0 < 64) of row r of a one-atom tile
 __device__ __forceinline__ void st_row32_pk(uint8_t* tile, int r, int col0, const uint32_t (&w)[16]) {
     const int c0 = col0 >> 3;
+    const uint32_t base = smem_u32(tile);
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-        *reinterpret_cast<uint4*>(tile + swz(r, c0 + q)) = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+    for (int q = 0; q < 4; ++q) sts128(base + swz(r, c0 + q), w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
 }
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
@@ -729,13 +729,13 @@ __global__ void __launch_bounds__(384, 1)
                     const int qc = q0 + c * 32;
                     const bool full = qc >= kb * BR + BR - 1 && qc + 32 <= s;
                     const uint64_t sc2 = pk2(sc, sc);
-                    const float* nL = L + c * 32;
-                    const float* nD = Dq + c * 32;
+                    const uint32_t nL = smem_u32(L + c * 32);
+                    const uint32_t nD = smem_u32(Dq + c * 32);
                     float p[32];
 #pragma unroll
                     for (int e = 0; e < 32; e += 2) {
                         const uint64_t x2 = ffma2(pk2(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])), sc2,
-                                                  *reinterpret_cast<const uint64_t*>(nL + e));
+                                                  lds64(nL + 4 * e));
                         float x0, x1;
                         upk2(x2, x0, x1);
                         p[e] = ex2(x0);
@@ -753,7 +753,7 @@ __global__ void __launch_bounds__(384, 1)
                     for (int e = 0; e < 32; e += 2) {
                         const uint64_t p2 = pk2(p[e], p[e + 1]);
                         const uint64_t d2 = fmul2(p2, fadd2(pk2(__uint_as_float(pr[e]), __uint_as_float(pr[e + 1])),
-                                                            *reinterpret_cast<const uint64_t*>(nD + e)));
+                                                            lds64(nD + 4 * e)));
                         float d0, d1;
                         upk2(d2, d0, d1);
                         wp[e / 2] = bf2(p[e], p[e + 1]);

@@ -208,6 +208,19 @@ __device__ __forceinline__ void tc_fence_after() {
 }
 
 // D[tmem] (+)= A[smem] * B[smem]^T, kind::f16 (bf16 inputs, fp32 accumulate)
+// explicit shared-space accesses: tile pointers derived from the aligned
+// dynamic-smem base (via uintptr_t) lose their address space, and the compiler
+// then emits generic ST.E / LD.E (slower, and fence.proxy.async waits on them)
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
+}
+__device__ __forceinline__ uint64_t lds64(uint32_t addr) {
+    uint64_t v;
+    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(addr) : "memory");
+    return v;
+}
+
 // elect.sync: true in exactly one lane (the lowest active one) of a converged
 // warp. MMA issue roles run on the whole warp (so descriptors and loop state
 // are warp-uniform and live in uniform registers) and issue tcgen05.mma /

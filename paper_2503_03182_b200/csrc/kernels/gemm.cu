@@ -331,19 +331,22 @@ __device__ __forceinline__ void stage_store(uint8_t* buf, const float (&v)[32], 
                                             const CUtensorMap* map, int n0, int m0, int lane) {
     if (lane == 0) bulk_wait_read1();   // the store that last used `buf` has read it
     __syncwarp();
+    const uint32_t sb = smem_u32(buf);
     if (f32) {   // 128 B rows, 128B swizzle: chunk q of row r at (q ^ (r & 7))
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-            *reinterpret_cast<float4*>(buf + lane * 128 + ((q ^ (lane & 7)) << 4)) =
-                make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            sts128(sb + lane * 128 + ((q ^ (lane & 7)) << 4), __float_as_uint(v[4 * q]),
+                   __float_as_uint(v[4 * q + 1]), __float_as_uint(v[4 * q + 2]), __float_as_uint(v[4 * q + 3]));
     } else {     // 64 B rows, 64B swizzle: chunk q of row r at (q ^ ((r >> 1) & 3))
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            uint4 u;
-            bf16* hh = reinterpret_cast<bf16*>(&u);
+            uint32_t w[4];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) hh[j] = __float2bfloat16_rn(v[q * 8 + j]);
-            *reinterpret_cast<uint4*>(buf + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) = u;
+            for (int j = 0; j < 4; ++j) {
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(v[q * 8 + 2 * j], v[q * 8 + 2 * j + 1]);
+                w[j] = *reinterpret_cast<uint32_t*>(&h2);
+            }
+            sts128(sb + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4), w[0], w[1], w[2], w[3]);
         }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
