@@ -183,6 +183,145 @@ def capacity(p, strategies=("1f1b", "tpipe", "tpipe_trecomp", "tpipe_all")):
     return out
 
 
+def fast_init_chunk(plan, s, c, pool):
+    """init_chunk's layout (N(0,0.02) matrices, gamma 1, zero biases) with the
+    matrix values tiled from one pre-drawn N(0,0.02) pool: multi-billion-param
+    models initialise in seconds (throughput does not depend on the values)."""
+    from paper_2503_03182_b200 import params as PR
+    import synth
+    h, f = plan.model.hidden, plan.model.ffn_hidden
+    V, sl = plan.model.vocab, plan.model.seq_len
+    shapes = {"wte": (V, h), "wpe": (sl, h), "lnf_g": (h,), "lnf_b": (h,), "w_head": (V, h)}
+    shapes.update(synth.layer_shapes(h, f))
+    ents = PR.chunk_entries(plan.p, plan.v, plan.layers_chunk, s, c)
+    out = np.empty(sum(int(np.prod(shapes[k])) for k, _ in ents), np.float32)
+    off = 0
+    for k, _l in ents:
+        shp = shapes[k]
+        n = int(np.prod(shp))
+        if len(shp) == 2:
+            for o in range(0, n, pool.size):
+                w = min(pool.size, n - o)
+                out[off + o: off + o + w] = pool[:w]
+        else:
+            out[off: off + n] = 1.0 if k.endswith("_g") else 0.0
+        off += n
+    return out
+
+
+CAP_P, CAP_BUDGET_GIB, CAP_M = 8, 20, 16
+
+
+def capacity_plans(p=CAP_P, budget=CAP_BUDGET_GIB * 2 ** 30, m=CAP_M):
+    """Largest L (multiple of p) each strategy fits under `budget` bytes per
+    stage for the C5 shape (h=4096, s=8192), from the planner's byte model."""
+    from paper_2503_03182_b200 import plan as P
+    from paper_2503_03182_b200._lib import TPipeError
+    strategies = {"1f1b": ("1f1b", 0), "1f1b_full_recomp": ("1f1b_full_recomp", 0),
+                  "tpipe": ("tpipe", 0), "tpipe_trecomp": ("tpipe_trecomp", 0),
+                  "tpipe_all": ("tpipe_trecomp", P.OFFLOAD_MODEL_STATE | P.OFFLOAD_DEVICE_OPT)}
+    best = {}
+    for name, (strat, off) in strategies.items():
+        for L in range(p, 400, p):
+            md = P.Model(L, C5["hidden"], C5["n_heads"], C5["ffn_hidden"], C5["vocab"],
+                         C5["seq_len"], C5["micro_batch"], P.BF16)
+            try:
+                P.Plan(md, p, m, hbm_budget=budget, strategy=strat, offload=off)
+                best[name] = (L, strat, off)
+            except TPipeError:
+                # odd chunk splits are invalid for v=2 at small L; a budget
+                # failure at L means every larger L fails too
+                if L >= 4 * p:
+                    break
+    return best
+
+
+def run_capacity(args):
+    """Executed capacity at a fixed per-stage HBM budget on ONE B200: all p=8
+    pipeline stages of the C5 shape run in one process (virtual pipeline, the
+    in-process D2D transport), each stage's pool ledger capped at the budget
+    (a plan/ledger bug would raise E_OOM). For every strategy the largest
+    model its plan fits is built, stepped, and timed: the pool high-water of
+    every stage is read back from the runtime, and model TFLOP/s (causal
+    F_tok) is reported next to tokens/s (Q18: a 2x larger model halves
+    tokens/s at equal MFU). Also: T-Pipe-ALL at the 1F1B+full-recompute size
+    (north star: beat 1F1B+full recompute at equal model size)."""
+    import torch
+    from paper_2503_03182_b200 import plan as P, runtime as RT
+    import synth
+    p, m, budget = CAP_P, CAP_M, CAP_BUDGET_GIB * 2 ** 30
+    best = capacity_plans()
+    runs = [(n, *best[n]) for n in ("1f1b", "1f1b_full_recomp", "tpipe", "tpipe_trecomp", "tpipe_all")
+            if n in best]
+    if "1f1b_full_recomp" in best and "tpipe_all" in best:
+        runs.append(("tpipe_all@1f1b_full_recomp_size", best["1f1b_full_recomp"][0], *best["tpipe_all"][1:]))
+    pool = (np.random.default_rng(5).standard_normal(1 << 24, dtype=np.float32)
+            * np.float32(0.02))
+    tok, tgt = synth.tokens(C5["vocab"], m, C5["micro_batch"], C5["seq_len"], step=0)
+    dtok = torch.tensor(tok, dtype=torch.int32, device="cuda")
+    dtgt = torch.tensor(tgt, dtype=torch.int32, device="cuda")
+    tokens = m * C5["micro_batch"] * C5["seq_len"]
+    _, _, pk_sust, src = peaks()
+    res = {}
+    for name, L, strat, off in runs:
+        md = P.Model(L, C5["hidden"], C5["n_heads"], C5["ffn_hidden"], C5["vocab"],
+                     C5["seq_len"], C5["micro_batch"], P.BF16)
+        plan = P.Plan(md, p, m, hbm_budget=budget, strategy=strat, offload=off)
+        t0 = time.perf_counter()
+        rt = RT.Runtime(plan, stage=-1, lr=1e-5, pool_cap=budget)
+        for s in range(p):
+            for ch in range(1, plan.v + 1):
+                rt.set_params(s, ch, fast_init_chunk(plan, s, ch, pool))
+        setup_s = time.perf_counter() - t0
+        free_b, total_b = torch.cuda.mem_get_info()
+        ext = torch.cuda.ExternalStream(rt.stream())
+        loss0 = rt.step_device(dtok.data_ptr(), dtgt.data_ptr())
+        torch.cuda.synchronize()
+        k = 2
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(ext)
+        for _ in range(k):
+            loss = rt.step_device(dtok.data_ptr(), dtgt.data_ptr())
+        e1.record(ext)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / k
+        hw = rt.stats()["pool_high_water"]
+        fl = model_flops_per_token(dict(n_layers=L, hidden=C5["hidden"], seq_len=C5["seq_len"],
+                                        vocab=C5["vocab"]))
+        tf = tokens * fl / (ms / 1e3) / 1e12
+        res[name] = {"strategy": strat, "offload": off, "n_layers": L,
+                     "params_B": round(plan.params_total / 1e9, 3),
+                     "plan_peak_GiB": [round(plan.peak(s)["total_peak"] / 2 ** 30, 3) for s in range(p)],
+                     "pool_high_water_GiB": [round(x / 2 ** 30, 3) for x in hw],
+                     "high_water_eq_plan": all(hw[s] == plan.peak(s)["total_peak"] for s in range(p)),
+                     "max_stage_GiB": round(max(hw) / 2 ** 30, 3),
+                     "fits_budget": max(hw) <= budget,
+                     "device_used_GiB": round((total_b - free_b) / 2 ** 30, 1),
+                     "loss_first": round(float(loss0), 4), "loss_last": round(float(loss), 4),
+                     "ms_per_step": round(ms, 1), "tokens_s": round(tokens / (ms / 1e3), 1),
+                     "model_tflops": round(tf, 1), "mfu_1gpu": round(tf / pk_sust, 4),
+                     "setup_s": round(setup_s, 1)}
+        print(json.dumps({name: res[name]}), file=sys.stderr, flush=True)
+        rt.close()
+        del rt, plan
+        torch.cuda.synchronize()
+    out = {"capacity_measured": {
+        "how": f"one B200, all p={p} stages in one process (virtual pipeline), pool ledger per stage "
+               f"capped at {CAP_BUDGET_GIB} GiB, shape h=4096 a=32 f=16384 V=32000 s=8192 b=1 m={m}, "
+               f"largest L (multiple of p) the planner fits, then built and stepped ({src} peak {pk_sust})",
+        "runs": res}}
+    b = res.get("1f1b")
+    if b:
+        for n, r in res.items():
+            r["params_vs_1f1b"] = round(r["params_B"] / b["params_B"], 3)
+            r["model_tflops_vs_1f1b"] = round(r["model_tflops"] / b["model_tflops"], 3)
+    fr, ta = res.get("1f1b_full_recomp"), res.get("tpipe_all@1f1b_full_recomp_size")
+    if fr and ta:
+        out["capacity_measured"]["equal_size_tpipe_all_vs_1f1b_full_recomp_tokens_s"] = \
+            round(ta["tokens_s"] / fr["tokens_s"], 3)
+    return out
+
+
 def gemm_traffic():
     """Per-launch DRAM traffic of the tcgen05 GEMM class from the committed
     `ncu --set full` capture of the 12 layer GEMM shapes (scripts/
@@ -522,7 +661,12 @@ def main():
     ap.add_argument("--impl", default="tpipe", choices=["tpipe", "reference"])
     ap.add_argument("--strategy", default="tpipe", choices=["tpipe", "tpipe_trecomp", "1f1b"])
     ap.add_argument("--no-extras", action="store_true", help="skip capacity sweep and CPU oracle")
+    ap.add_argument("--capacity-run", action="store_true",
+                    help="executed capacity at a fixed per-stage HBM budget (p=8 virtual pipeline, one GPU)")
     args = ap.parse_args()
+    if args.capacity_run:
+        print(json.dumps(run_capacity(args)), flush=True)
+        return
     if args.warmup < 3:
         args.warmup = 3
     out = run_reference(args) if args.impl == "reference" else run_tpipe(args)
