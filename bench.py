@@ -255,6 +255,16 @@ def run_capacity(args):
             if n in best]
     if "1f1b_full_recomp" in best and "tpipe_all" in best:
         runs.append(("tpipe_all@1f1b_full_recomp_size", best["1f1b_full_recomp"][0], *best["tpipe_all"][1:]))
+    if "1f1b" in best:
+        # north star: a model >= 2x the 1F1B-max params, planned by the auto ladder
+        # (T-Pipe -> partial T-Recomp r=1..n1 -> + T-Offload), least recompute that fits
+        def params_at(L):
+            md = P.Model(L, C5["hidden"], C5["n_heads"], C5["ffn_hidden"], C5["vocab"],
+                         C5["seq_len"], C5["micro_batch"], P.BF16)
+            return P.Plan(md, p, m, strategy="1f1b").params_total
+        target = 2 * params_at(best["1f1b"][0])
+        L2 = next(L for L in range(p, 400, p) if params_at(L) >= target)
+        runs.append(("auto@2x_1f1b_params", L2, "auto", P.OFFLOAD_MODEL_STATE | P.OFFLOAD_DEVICE_OPT))
     pool = (np.random.default_rng(5).standard_normal(1 << 24, dtype=np.float32)
             * np.float32(0.02))
     tok, tgt = synth.tokens(C5["vocab"], m, C5["micro_batch"], C5["seq_len"], step=0)
@@ -289,7 +299,9 @@ def run_capacity(args):
         fl = model_flops_per_token(dict(n_layers=L, hidden=C5["hidden"], seq_len=C5["seq_len"],
                                         vocab=C5["vocab"]))
         tf = tokens * fl / (ms / 1e3) / 1e12
-        res[name] = {"strategy": strat, "offload": off, "n_layers": L,
+        res[name] = {"strategy": strat, "offload": plan.offload, "n_layers": L,
+                     "plan_strategy": ["1f1b", "1f1b_full_recomp", "tpipe", "tpipe_trecomp"][plan.strategy],
+                     "recomp_layers": plan.recomp_layers, "layers_chunk": list(plan.layers_chunk),
                      "params_B": round(plan.params_total / 1e9, 3),
                      "plan_peak_GiB": [round(plan.peak(s)["total_peak"] / 2 ** 30, 3) for s in range(p)],
                      "pool_high_water_GiB": [round(x / 2 ** 30, 3) for x in hw],
@@ -319,6 +331,68 @@ def run_capacity(args):
     if fr and ta:
         out["capacity_measured"]["equal_size_tpipe_all_vs_1f1b_full_recomp_tokens_s"] = \
             round(ta["tokens_s"] / fr["tokens_s"], 3)
+    return out
+
+
+def hbm_kernels(c, hbm_peak):
+    """HBM-bound stage-executor kernels at the workload's launch shape (M = b*s
+    rows): achieved GB/s = algorithmic bytes (each operand read
+    once, each result written once) / CUDA-event time of 20 back-to-back
+    launches on torch's current stream (the kernels' launch stream), vs the
+    measured HBM copy peak. Working sets of 8-100 MB partly hit L2 between
+    launches, so back-to-back figures are an upper bound on the in-step rate."""
+    import torch
+    from paper_2503_03182_b200 import kernels as K
+    M, h, f, V = c["seq_len"] * c["micro_batch"], c["hidden"], c["ffn_hidden"], c["vocab"]
+    dev = "cuda"
+    bf = torch.bfloat16
+
+    def tm(fn, iters=20):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / iters
+
+    x = torch.randn((M, h), device=dev).to(bf)
+    dy = torch.randn((M, h), device=dev).to(bf)
+    res = torch.randn((M, h), device=dev).to(bf)
+    y = torch.empty_like(x)
+    dx = torch.empty_like(x)
+    g = torch.ones(h, device=dev, dtype=bf)
+    b = torch.zeros(h, device=dev, dtype=bf)
+    mean = torch.empty(M, device=dev)
+    rstd = torch.empty(M, device=dev)
+    dg = torch.zeros(h, device=dev)
+    db = torch.zeros(h, device=dev)
+    drs = torch.zeros(h, device=dev)
+    ws = torch.empty(((M + 15) // 16) * max(f, 3 * h), device=dev)
+    du = torch.randn((M, f), device=dev).to(bf)
+    dbias = torch.zeros(f, device=dev)
+    n_p = 1 << 26
+    master = torch.randn(n_p, device=dev)
+    mm_, vv = torch.zeros(n_p, device=dev), torch.zeros(n_p, device=dev)
+    grad = torch.randn(n_p, device=dev)
+    w = torch.empty(n_p, device=dev, dtype=bf)
+    cases = [
+        ("ln_fwd", lambda: K.tpipe_k_ln_fwd(1, x, g, b, y, mean, rstd, M, h), 2 * 2 * M * h + 8 * M),
+        ("ln_bwd_rsum", lambda: K.tpipe_k_ln_bwd_rsum(1, dy, x, g, mean, rstd, res, dx, dg, db, drs, ws, M, h),
+         4 * 2 * M * h + 8 * M),
+        ("colsum_ffn", lambda: K.tpipe_k_colsum(1, du, dbias, ws, M, f), 2 * M * f),
+        ("adamw_64M", lambda: K.tpipe_k_adamw(1, master, mm_, vv, grad, w, n_p, 1, 1e-4, 0.9, 0.95, 1e-8,
+                                                0.1, 0.1, 0.05), 30 * n_p),
+    ]
+    out = {}
+    for name, fn, nbytes in cases:
+        ms = tm(fn)
+        gbs = nbytes / (ms / 1e3) / 1e9
+        out[name] = {"us": round(ms * 1e3, 2), "alg_bytes": int(nbytes), "GBs": round(gbs, 1),
+                     "frac": round(gbs / hbm_peak, 3)}
     return out
 
 
@@ -417,14 +491,15 @@ def measure_offload(N, m, dtok, dtgt, args, base_ms, device_opt=False):
     return res
 
 
-def quick_measure(strategy, N, m, dtok, dtgt, args):
+def quick_measure(strategy, N, m, dtok, dtgt, args, recomp_layers=0, offload=0, act_distance=0):
     """tokens/s of another schedule on the same kernels/workload (N=1)."""
     import torch
     from paper_2503_03182_b200 import plan as P, runtime as RT
     c = C2
     md = P.Model(c["n_layers"], c["hidden"], c["n_heads"], c["ffn_hidden"], c["vocab"],
                  c["seq_len"], c["micro_batch"], P.BF16)
-    plan = P.Plan(md, N, m, strategy=strategy)
+    plan = P.Plan(md, N, m, strategy=strategy, recomp_layers=recomp_layers, offload=offload,
+                  act_distance=act_distance)
     rt = RT.Runtime(plan, stage=-1, lr=1e-4)
     rng = np.random.default_rng(99)
     for s in range(N):
@@ -443,9 +518,16 @@ def quick_measure(strategy, N, m, dtok, dtgt, args):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / k
     tokens = m * c["micro_batch"] * c["seq_len"]
+    st = rt.stats()
     res = {"tokens_s": round(tokens / (ms / 1e3), 1), "ms_per_step": round(ms, 2),
            "steps": k, "plan_peak_GiB": round(plan.peak(0)["total_peak"] / 2 ** 30, 2),
-           "pool_high_water_GiB": round(rt.stats()["pool_high_water"][0] / 2 ** 30, 2)}
+           "pool_high_water_GiB": round(st["pool_high_water"][0] / 2 ** 30, 2)}
+    if offload & P.OFFLOAD_ACTIVATIONS:
+        d2h_b, h2d_b = st["offload_d2h_bytes"], st["offload_h2d_bytes"]
+        res.update({"act_d2h_bytes": int(d2h_b), "act_h2d_bytes": int(h2d_b),
+                    "d2h_GBs": round(d2h_b / (st["offload_d2h_ms"] / 1e3) / 1e9, 1) if st["offload_d2h_ms"] else None,
+                    "h2d_GBs": round(h2d_b / (st["offload_h2d_ms"] / 1e3) / 1e9, 1) if st["offload_h2d_ms"] else None,
+                    "act_distance": plan.act_distance})
     rt.close()
     return res
 
@@ -593,6 +675,18 @@ def run_tpipe(args):
             if st in comp:
                 continue
             comp[st] = quick_measure(st, N, m, dtok, dtgt, args)
+        # partial T-Recomp (R25): half of chunk 1's layers regenerated
+        r_half = max(1, plan.layers_chunk[0] // 2)
+        comp[f"tpipe_trecomp_r{r_half}"] = quick_measure("tpipe_trecomp", N, m, dtok, dtgt, args,
+                                                          recomp_layers=r_half)
+        # a7: chunk-1 activation offload instead of recompute (R23; bandwidth-bound)
+        try:
+            # at p = 1 the F(1,i) -> B(1,i) distance is 4 ops: distance 1 offloads every block
+            comp["tpipe_act_offload"] = quick_measure("tpipe", N, m, dtok, dtgt, args,
+                                                      offload=P.OFFLOAD_ACTIVATIONS,
+                                                      act_distance=1 if N == 1 else 0)
+        except Exception as e:   # reported, not fatal
+            comp["tpipe_act_offload"] = {"error": str(e)[:200]}
         out["compare"] = comp
         for key, dev in (("tpipe_trecomp_offload", False), ("tpipe_trecomp_offload_devopt", True)):
             try:
@@ -601,6 +695,10 @@ def run_tpipe(args):
             except Exception as e:   # reported, not fatal
                 comp[key] = {"error": str(e)[:200]}
         out["host_link_peak"] = host_link_peak()
+        out["hbm_kernels"] = {"peak_GBs": hbm, "peak_src": f"hbm_gbs ({src})",
+                              "shape": f"M={c['seq_len'] * c['micro_batch']} rows, h={c['hidden']}, "
+                                       f"f={c['ffn_hidden']}; adamw 64M params",
+                              **hbm_kernels(c, hbm)}
         out["capacity_80GiB"] = {"p": max(N, 8) if N == 1 else N, "shape": "h=4096 a=32 s=8192 V=32000 b=1 m=32",
                                  **capacity(max(N, 8) if N == 1 else N)}
         out["cpu_baseline"] = cpu_baseline(c)

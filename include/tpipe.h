@@ -95,6 +95,12 @@ typedef struct {
     int32_t offload;       /* TPIPE_OFFLOAD_* bitmask (explicit strategies); -1 = auto */
     int32_t act_distance;  /* activation offload: release / prefetch distance in compute
                               ops (0 = default 2); blocks with F->B distance <= 2x are kept */
+    int32_t recomp_layers; /* partial T-Recomp (the recompute ratio of
+                              P:551, Fig. E56): chunk-1 layers per stage that R regenerates,
+                              shallowest first; the deeper n1 - r layers keep their stash
+                              from F to B. 0 = all n1 layers (block-wise T-Recomp).
+                              Must be <= n1. With strategy -1 (auto) and 0 here, the
+                              escalation tries r = 1..n1 at each rung (DESIGN R25) */
 } tpipe_plan_opts;
 
 enum {
@@ -153,6 +159,7 @@ typedef struct {
     int32_t layers_chunk[2];
     int32_t n_channels;
     uint64_t params_total;
+    int32_t recomp_layers;   /* effective r of partial T-Recomp (0 unless T-Recomp) */
 } tpipe_plan_info;
 
 typedef struct {

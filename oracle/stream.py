@@ -138,9 +138,21 @@ def sizes(d: ModelDesc, p: int, v: int, s: int, c: int, full_recomp: bool = Fals
     if emb:
         ws_b += 8 * M
     return {
-        "act": act, "stash": stash, "ws_f": ws_f, "ws_b": ws_b,
+        "act": act, "stash": stash, "ws_f": ws_f, "ws_b": ws_b, "layer_stash": LS,
         "input_is_act": not emb, "has_output": not head,
     }
+
+
+def partial_trecomp_split(z: dict, n1: int, r: int):
+    """Partial T-Recomp (NEXT-1; the recompute ratio r/n1 of P:551, Fig. E56;
+    DESIGN.md R25): R regenerates chunk-1 layers 1..r (shallowest first) from
+    the checkpoint, so only their stash is transient (TSTASH during F, RBUF
+    from R to B); layers r+1..n1 keep theirs from F to B like plain T-Pipe.
+    Returns (kept bytes, recomputed bytes) of the chunk-1 stash ``z``."""
+    if not 1 <= r <= n1:
+        raise ValueError("recomp_layers")
+    keep = (n1 - r) * z["layer_stash"]
+    return keep, z["stash"] - keep
 
 
 # --------------------------------------------------------------------------
@@ -194,9 +206,10 @@ def act_offload_sets(order, d_release: int, d_prefetch: int):
 def build_streams(d: ModelDesc, p: int, m: int, strategy: str, k=None,
                   window: int = 2, offload_model_state: bool = False,
                   offload_activations: bool = False, act_distance: int = 2,
-                  offload_device_opt: bool = False):
+                  offload_device_opt: bool = False, recomp_layers: int = 0):
     """Per-stage instruction streams. Returns (streams, static)
-    where static[s] = list of (name, category, bytes) live for the whole step."""
+    where static[s] = list of (name, category, bytes) live for the whole step.
+    ``recomp_layers`` = r of partial T-Recomp (0 = all chunk-1 layers)."""
     ostrat, v, trecomp, full = STRATS[strategy]
     if offload_model_state and v != 2:
         raise ValueError("offload requires v=2")
@@ -207,6 +220,12 @@ def build_streams(d: ModelDesc, p: int, m: int, strategy: str, k=None,
     orders = S.strategy_orders(ostrat, p, m, k=k)[0]
     sz = {(s, c): sizes(d, p, v, s, c, full_recomp=full)
           for s in range(p) for c in range(1, v + 1)}
+    keep1, rec1 = {}, {}
+    if trecomp:
+        n1 = layers_per_chunk(d, p, v)[0]
+        r = recomp_layers if recomp_layers else n1
+        for s in range(p):
+            keep1[s], rec1[s] = partial_trecomp_split(sz[(s, 1)], n1, r)
 
     static = []
     for s in range(p):
@@ -277,8 +296,10 @@ def build_streams(d: ModelDesc, p: int, m: int, strategy: str, k=None,
             ins = Instr(kind, c, i)
             if kind == "F":
                 if trecomp and c == 1:
-                    ins.allocs.append((("TSTASH", c, i), "act", z["stash"]))
+                    ins.allocs.append((("TSTASH", c, i), "act", rec1[s]))
                     ins.frees.append(("TSTASH", c, i))
+                    if keep1[s]:
+                        ins.allocs.append((("STASH", c, i), "act", keep1[s]))
                 else:
                     ins.allocs.append((("STASH", c, i), "act", z["stash"]))
                 if msg is not None:
@@ -289,7 +310,7 @@ def build_streams(d: ModelDesc, p: int, m: int, strategy: str, k=None,
                 ins.allocs.append((("WSF", c, i), "workspace", z["ws_f"]))
                 ins.frees.append(("WSF", c, i))
             elif kind == "R":
-                ins.allocs.append((("RBUF", c, i), "recomp_buf", z["stash"]))
+                ins.allocs.append((("RBUF", c, i), "recomp_buf", rec1[s]))
                 ins.allocs.append((("WSR", c, i), "workspace", z["ws_f"]))
                 ins.frees.append(("WSR", c, i))
             else:  # B
@@ -299,7 +320,12 @@ def build_streams(d: ModelDesc, p: int, m: int, strategy: str, k=None,
                     ins.allocs.append((("GIN", c - 1, i), "comm", z["act"]))
                 ins.allocs.append((("WSB", c, i), "workspace", z["ws_b"]))
                 ins.frees.append(("WSB", c, i))
-                ins.frees.append(("RBUF", c, i) if (trecomp and c == 1) else ("STASH", c, i))
+                if trecomp and c == 1:
+                    ins.frees.append(("RBUF", c, i))
+                    if keep1[s]:
+                        ins.frees.append(("STASH", c, i))
+                else:
+                    ins.frees.append(("STASH", c, i))
                 if z["input_is_act"]:
                     ins.frees.append(("IN", c, i))
                 if z["has_output"]:

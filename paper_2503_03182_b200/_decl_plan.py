@@ -13,7 +13,7 @@ class ModelDesc(C.Structure):
 
 class PlanOpts(C.Structure):
     _fields_ = [("strategy", i32), ("delay_rounds", i32), ("send_window", i32), ("offload", i32),
-                ("act_distance", i32)]
+                ("act_distance", i32), ("recomp_layers", i32)]
 
 
 class Op(C.Structure):
@@ -36,7 +36,8 @@ class MemReport(C.Structure):
 class PlanInfo(C.Structure):
     _fields_ = [("n_stages", i32), ("n_microbatches", i32), ("v", i32), ("strategy", i32),
                 ("delay_rounds", i32), ("send_window", i32), ("offload", i32), ("act_distance", i32),
-                ("layers_chunk", i32 * 2), ("n_channels", i32), ("params_total", u64)]
+                ("layers_chunk", i32 * 2), ("n_channels", i32), ("params_total", u64),
+                ("recomp_layers", i32)]
 
 
 class SimReport(C.Structure):

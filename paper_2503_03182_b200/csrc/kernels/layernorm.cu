@@ -348,14 +348,20 @@ ln_bwd_stage_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
         const int nr = min(RC, r1 - q0);
         // each thread fetches only the 16-byte slices it will read itself
         // (cp.async, no registers held), so no CTA barrier is needed before use
+        // two commit groups (rows [0, half), [half, nr)): the first half's
+        // rows are processed and stored while the second half is still landing
+        const int half = (nr + 1) / 2;
         for (int i = grp; i < nr; i += G) {
             const long off = (long)(q0 + i) * h + c;
             cp_async16(sdy + (size_t)i * h + c, dy + off);
             cp_async16(sx + (size_t)i * h + c, x + off);
             if (resid) cp_async16(sr + (size_t)i * h + c, resid + off);
+            if (i < half && i + G >= half) asm volatile("cp.async.commit_group;" ::: "memory");
         }
-        asm volatile("cp.async.wait_all;" ::: "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
         for (int i = grp; i < nr; i += G) {
+            if (i < half) asm volatile("cp.async.wait_group 1;" ::: "memory");
+            else asm volatile("cp.async.wait_group 0;" ::: "memory");
             const int r = q0 + i;
             float d[8], v[8], rr[8];
             Vec<bf16>::load(sdy + (size_t)i * h + c, d);

@@ -57,6 +57,13 @@ uint64_t chunk_params(const tpipe_model_desc& d, int p, int v, const int layers[
     return P;
 }
 
+// per-layer stash: x_in, ln1 stats, qkv, attn out, lse, x_mid, ln2 stats, u (fc1 pre-act)
+static uint64_t layer_stash_bytes(const tpipe_model_desc& d) {
+    const uint64_t M = (uint64_t)d.micro_batch * d.seq_len, h = d.hidden, a = d.n_heads,
+                   f = d.ffn_hidden, es = d.dtype == TPIPE_BF16 ? 2 : 4;
+    return M * h * es + 8 * M + 3 * M * h * es + M * h * es + 4 * a * M + M * h * es + 8 * M + M * f * es;
+}
+
 static ChunkSizes chunk_sizes(const tpipe_model_desc& d, int p, int v, const int layers[2], int s,
                               int c, bool full_recomp) {
     const uint64_t M = (uint64_t)d.micro_batch * d.seq_len, h = d.hidden, a = d.n_heads,
@@ -67,9 +74,7 @@ static ChunkSizes chunk_sizes(const tpipe_model_desc& d, int p, int v, const int
     z.act = M * h * es;
     z.input_is_act = !emb;
     z.has_output = !head;
-    // per-layer stash: x_in, ln1 stats, qkv, attn out, lse, x_mid, ln2 stats, u (fc1 pre-act)
-    const uint64_t LS = M * h * es + 8 * M + 3 * M * h * es + M * h * es + 4 * a * M +
-                        M * h * es + 8 * M + M * f * es;
+    const uint64_t LS = layer_stash_bytes(d);
     const uint64_t head_stash = M * h * es + 8 * M + 4 * M;   // x_f, ln_f stats, CE lse
     uint64_t stash = full_recomp ? n * M * h * es : n * LS;
     if (!emb) stash -= z.act;
@@ -283,6 +288,14 @@ static int build(tpipe_plan* P, bool trecomp, bool full_recomp) {
 
         ChunkSizes z[3];
         for (int c = 1; c <= v; ++c) z[c] = chunk_sizes(d, p, v, P->layers, s, c, full_recomp);
+        // partial T-Recomp (R25): layers 1..r of chunk 1 are regenerated by R (TSTASH during
+        // F, RBUF from R to B); the stash of layers r+1..n1 is kept from F to B (STASH).
+        // The two parts add up to the full chunk-1 stash.
+        uint64_t keep1 = 0, rec1 = z[1].stash;
+        if (trecomp && P->rl < P->layers[0]) {
+            keep1 = (uint64_t)(P->layers[0] - P->rl) * layer_stash_bytes(d);
+            rec1 = z[1].stash - keep1;
+        }
 
         const auto& order = P->order[s];
         std::map<int, int> sent, waited;  // channel -> count
@@ -366,9 +379,10 @@ static int build(tpipe_plan* P, bool trecomp, bool full_recomp) {
             Builder::Pending pe;
             if (kind == KF) {
                 if (trecomp && c == 1) {
-                    int id = B.newbuf(TPIPE_BUF_TSTASH, TPIPE_CAT_ACT, c, i, zz.stash);
+                    int id = B.newbuf(TPIPE_BUF_TSTASH, TPIPE_CAT_ACT, c, i, rec1);
                     pe.allocs.push_back(id);
                     pe.frees.push_back(B.take(TPIPE_BUF_TSTASH, c, i));
+                    if (keep1) pe.allocs.push_back(B.newbuf(TPIPE_BUF_STASH, TPIPE_CAT_ACT, c, i, keep1));
                 } else {
                     pe.allocs.push_back(B.newbuf(TPIPE_BUF_STASH, TPIPE_CAT_ACT, c, i, zz.stash));
                 }
@@ -381,7 +395,7 @@ static int build(tpipe_plan* P, bool trecomp, bool full_recomp) {
                 pe.allocs.push_back(ws);
                 pe.frees.push_back(B.take(TPIPE_BUF_WS, c, i, 1));
             } else if (kind == KR) {
-                pe.allocs.push_back(B.newbuf(TPIPE_BUF_RBUF, TPIPE_CAT_RECOMP_BUF, c, i, zz.stash));
+                pe.allocs.push_back(B.newbuf(TPIPE_BUF_RBUF, TPIPE_CAT_RECOMP_BUF, c, i, rec1));
                 pe.allocs.push_back(B.newbuf(TPIPE_BUF_WS, TPIPE_CAT_WORKSPACE, c, i, zz.ws_f, 2));
                 pe.frees.push_back(B.take(TPIPE_BUF_WS, c, i, 2));
             } else {
@@ -392,10 +406,12 @@ static int build(tpipe_plan* P, bool trecomp, bool full_recomp) {
                 }
                 pe.allocs.push_back(B.newbuf(TPIPE_BUF_WS, TPIPE_CAT_WORKSPACE, c, i, zz.ws_b, 3));
                 pe.frees.push_back(B.take(TPIPE_BUF_WS, c, i, 3));
-                if (trecomp && c == 1)
+                if (trecomp && c == 1) {
                     pe.frees.push_back(B.take(TPIPE_BUF_RBUF, c, i));
-                else
+                    if (keep1) pe.frees.push_back(B.take(TPIPE_BUF_STASH, c, i));
+                } else {
                     pe.frees.push_back(B.take(TPIPE_BUF_STASH, c, i));
+                }
                 if (zz.input_is_act) pe.frees.push_back(B.take(TPIPE_BUF_IN, c, i));
                 if (zz.has_output) pe.frees.push_back(B.take(TPIPE_BUF_GIN, c, i));
             }
@@ -539,7 +555,7 @@ using namespace tpipe;
 #define TP_API extern "C" __attribute__((visibility("default")))
 
 static int make_plan(const tpipe_model_desc* model, int p, int m, int strategy, int k, int W,
-                     int offload, int act_distance, tpipe_plan** out) {
+                     int offload, int act_distance, int recomp_layers, tpipe_plan** out) {
     if ((offload & TPIPE_OFFLOAD_DEVICE_OPT) && !(offload & TPIPE_OFFLOAD_MODEL_STATE))
         return set_error(TPIPE_E_INVALID, "offload: DEVICE_OPT needs MODEL_STATE");
     if ((offload & TPIPE_OFFLOAD_ACTIVATIONS) && strategy != TPIPE_S_TPIPE)
@@ -581,6 +597,13 @@ static int make_plan(const tpipe_model_desc* model, int p, int m, int strategy, 
         P->layers[0] = n;
     }
     const bool trecomp = strategy == TPIPE_S_TPIPE_TRECOMP;
+    if (trecomp && recomp_layers > P->layers[0]) {
+        const int n1 = P->layers[0];
+        delete P;
+        return set_error(TPIPE_E_INVALID, "recomp_layers %d exceeds the %d chunk-1 layers per stage",
+                         recomp_layers, n1);
+    }
+    P->rl = trecomp ? (recomp_layers > 0 ? recomp_layers : P->layers[0]) : 0;
     P->k = trecomp ? (k < 0 ? delay_rounds_appB(p) : k) : 0;
     if (is_tp) {
         auto ord = tpipe_order(p, m, trecomp, P->k);
@@ -616,16 +639,17 @@ TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, in
     if (!out) return set_error(TPIPE_E_INVALID, "out is NULL");
     *out = nullptr;
     if (int rc = validate(model, n_stages, n_microbatches)) return rc;
-    tpipe_plan_opts o{-1, -1, 0, -1, 0};
+    tpipe_plan_opts o{-1, -1, 0, -1, 0, 0};
     if (opts) o = *opts;
     const int W = o.send_window > 0 ? o.send_window : 2;
     if (o.strategy < -1 || o.strategy > TPIPE_S_TPIPE_TRECOMP) return set_error(TPIPE_E_INVALID, "strategy");
     if (o.delay_rounds < -1) return set_error(TPIPE_E_INVALID, "delay_rounds");
+    if (o.recomp_layers < 0) return set_error(TPIPE_E_INVALID, "recomp_layers");
     if (o.strategy >= 0) {
         const int off = o.offload < 0 ? 0 : o.offload;
         tpipe_plan* P = nullptr;
         int rc = make_plan(model, n_stages, n_microbatches, o.strategy, o.delay_rounds, W, off,
-                           o.act_distance, &P);
+                           o.act_distance, o.recomp_layers, &P);
         if (rc) return rc;
         if (hbm_budget_bytes && max_peak(P) > hbm_budget_bytes) {
             const uint64_t pk = max_peak(P);
@@ -636,16 +660,24 @@ TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, in
         *out = P;
         return 0;
     }
-    // auto escalation: T-Pipe -> + T-Recomp -> + model-state T-Offload
-    const int ladder[3][2] = {{TPIPE_S_TPIPE, 0},
-                              {TPIPE_S_TPIPE_TRECOMP, 0},
-                              {TPIPE_S_TPIPE_TRECOMP, TPIPE_OFFLOAD_MODEL_STATE}};
+    // auto escalation (fit the budget with the least throughput loss):
+    // T-Pipe -> + T-Recomp of r = 1..n1 chunk-1 layers (R25) -> + model-state
+    // T-Offload (device AdamW streaming if requested in `offload`) with r = 1..n1
+    const int n1 = model->layers_chunk[0] ? model->layers_chunk[0] : (model->n_layers / n_stages + 1) / 2;
+    const int rmin = o.recomp_layers > 0 ? o.recomp_layers : 1;
+    const int rmax = o.recomp_layers > 0 ? o.recomp_layers : n1;
+    const int off_flags = TPIPE_OFFLOAD_MODEL_STATE |
+                          (o.offload > 0 ? (o.offload & TPIPE_OFFLOAD_DEVICE_OPT) : 0);
+    std::vector<std::array<int, 3>> ladder;   // {strategy, offload, r}
+    ladder.push_back({TPIPE_S_TPIPE, 0, 0});
+    for (int r = rmin; r <= rmax; ++r) ladder.push_back({TPIPE_S_TPIPE_TRECOMP, 0, r});
+    if (o.offload < 0 || (o.offload & TPIPE_OFFLOAD_MODEL_STATE))
+        for (int r = rmin; r <= rmax; ++r) ladder.push_back({TPIPE_S_TPIPE_TRECOMP, off_flags, r});
     uint64_t best = 0;
     for (auto& rung : ladder) {
-        if (o.offload >= 0 && rung[1] && !(o.offload & TPIPE_OFFLOAD_MODEL_STATE)) continue;
         tpipe_plan* P = nullptr;
         int rc = make_plan(model, n_stages, n_microbatches, rung[0], o.delay_rounds, W, rung[1],
-                           o.act_distance, &P);
+                           o.act_distance, rung[2], &P);
         if (rc) return rc;
         best = max_peak(P);
         if (!hbm_budget_bytes || best <= hbm_budget_bytes) {
@@ -674,6 +706,7 @@ TP_API int tpipe_plan_get_info(const tpipe_plan* P, tpipe_plan_info* out) {
     out->layers_chunk[1] = P->layers[1];
     out->n_channels = (int32_t)P->channels.size();
     out->params_total = P->params_total;
+    out->recomp_layers = P->rl;
     return 0;
 }
 

@@ -12,6 +12,7 @@ struct tpipe_plan {
     int p = 0, m = 0, v = 0;
     int strategy = 0, k = 0, W = 2, offload = 0, act_distance = 2;
     int layers[2] = {0, 0};
+    int rl = 0;   // partial T-Recomp: chunk-1 layers recomputed (R25); 0 unless T-Recomp
     uint64_t params_total = 0;
     // per stage
     std::vector<std::vector<tpipe_op>> ops;

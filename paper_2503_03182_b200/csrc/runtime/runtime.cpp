@@ -320,17 +320,24 @@ int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags
             void* ws = nullptr;
             op_alloc_ptr(rt, S, op, TPIPE_BUF_WS, -1, &ws);
             a.ws = (uint8_t*)ws;
+            const bool partial = trecomp && c == 1 && P.rl < P.layers[0];
             if (op.kind == TPIPE_OP_R) {
                 void* rb;
                 op_alloc_ptr(rt, S, op, TPIPE_BUF_RBUF, -1, &rb);
                 a.stash = (uint8_t*)rb;
                 a.out = nullptr;
                 a.targets = nullptr;
+                if (partial) a.split = a.n_run = P.rl;   // regenerate layers 1..r only
             } else {
-                void* stp;
-                if (!op_alloc_ptr(rt, S, op, TPIPE_BUF_STASH, -1, &stp))
-                    op_alloc_ptr(rt, S, op, TPIPE_BUF_TSTASH, -1, &stp);
-                a.stash = (uint8_t*)stp;
+                void *tst = nullptr, *kst = nullptr;
+                op_alloc_ptr(rt, S, op, TPIPE_BUF_TSTASH, -1, &tst);
+                op_alloc_ptr(rt, S, op, TPIPE_BUF_STASH, -1, &kst);
+                a.stash = (uint8_t*)(tst ? tst : kst);
+                if (tst && partial) {
+                    if (!kst) return set_error(TPIPE_E_STATE, "stage %d F(1,%d): kept stash missing", s, i);
+                    a.stash2 = (uint8_t*)kst;
+                    a.split = P.rl;
+                }
                 void* out = nullptr;
                 if (!op_alloc_ptr(rt, S, op, TPIPE_BUF_MSG, -1, &out))
                     op_alloc_ptr(rt, S, op, TPIPE_BUF_IN, c + 1, &out);
@@ -355,6 +362,11 @@ int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags
             void* stp = (trecomp && c == 1) ? live_get(S, TPIPE_BUF_RBUF, c, i)
                                             : live_get(S, TPIPE_BUF_STASH, c, i);
             a.stash = (uint8_t*)stp;
+            if (trecomp && c == 1 && P.rl < P.layers[0]) {   // partial T-Recomp (R25)
+                a.stash2 = (uint8_t*)live_get(S, TPIPE_BUF_STASH, c, i);
+                a.split = P.rl;
+                if (!a.stash2) return set_error(TPIPE_E_STATE, "stage %d B(1,%d): kept stash missing", s, i);
+            }
             void* ws = nullptr;
             op_alloc_ptr(rt, S, op, TPIPE_BUF_WS, -1, &ws);
             a.ws = (uint8_t*)ws;

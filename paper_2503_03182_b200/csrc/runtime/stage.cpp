@@ -230,6 +230,13 @@ static LayerPtrs layer_ptrs(const StashLayout::L& L, uint8_t* stash, const void*
     return p;
 }
 
+// partial T-Recomp (R25): base pointer for layer l's StashLayout offsets; the
+// kept part [split, n) of the chunk stash starts at layer split's x_in
+static uint8_t* stash_base(const StashLayout& SL, uint8_t* stash, uint8_t* stash2, int split, int l) {
+    if (split <= 0 || l < split) return stash;
+    return stash2 - SL.layer[split].x_in;
+}
+
 // full recompute: layer input from the checkpoint stash, internals in `scratch`
 static LayerPtrs scratch_ptrs(const StashLayout& SL, int l, uint8_t* stash, const void* x_in,
                               uint8_t* scratch) {
@@ -460,11 +467,13 @@ int chunk_forward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P,
             TRY(embed_fwd(D.dtype, a.tokens, wb + lay.wte * D.es, wb + lay.wpe * D.es,
                       a.stash + SL.layer[0].x_in, D.M, D.s, D.h, st));
         }
-    for (int l = 0; l < n; ++l) {
+    const int n_run = a.n_run > 0 ? a.n_run : n;
+    for (int l = 0; l < n_run; ++l) {
         LayerPtrs lp = SL.ckpt_only ? scratch_ptrs(SL, l, a.stash, a.in, scratch)
-                                    : layer_ptrs(SL.layer[l], a.stash, a.in);
+                                    : layer_ptrs(SL.layer[l], stash_base(SL, a.stash, a.stash2, a.split, l), a.in);
         void* out;
-        if (l + 1 < n) out = a.stash + SL.layer[l + 1].x_in;
+        if (l + 1 < n_run) out = stash_base(SL, a.stash, a.stash2, a.split, l + 1) + SL.layer[l + 1].x_in;
+        else if (l + 1 < n) out = ws_ln;    // partial recompute: layer n_run's input is kept
         else if (lay.head) out = a.stash + SL.x_f;
         else out = a.out ? a.out : ws_ln;   // recompute: discard into free scratch
         TRY(layer_forward(D, layer_w(D, P, l), lp, ws_ln, ws_g, out, st));
@@ -533,7 +542,7 @@ int chunk_backward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P
             lp = scratch_ptrs(SL, l, a.stash, a.in, w.rbuf);
             TRY(layer_forward(D, layer_w(D, P, l), lp, w.ln, w.g, w.dout, st));
         } else {
-            lp = layer_ptrs(SL.layer[l], a.stash, a.in);
+            lp = layer_ptrs(SL.layer[l], stash_base(SL, a.stash, a.stash2, a.split, l), a.in);
         }
         void* dx = (l > 0 || lay.emb) ? w.G0 : a.gout;
         TRY(layer_backward(D, layer_w(D, P, l), lp, dy, dx, w, st));

@@ -66,6 +66,11 @@ struct FwdArgs {
     uint8_t* stash;          // STASH / TSTASH / RBUF
     uint8_t* ws;             // forward workspace (ws_f bytes)
     void* out;               // chunk output [M,h] (nullptr: head chunk, or recompute -> scratch)
+    // partial T-Recomp (DESIGN R25): layers [0, split) live in `stash`
+    // (TSTASH / RBUF), layers [split, n) in `stash2` (the kept STASH); split 0 =
+    // every layer in `stash`. n_run > 0: run only layers [0, n_run) (R op).
+    uint8_t* stash2;
+    int split, n_run;
 };
 
 struct BwdArgs {
@@ -74,6 +79,8 @@ struct BwdArgs {
     const int* targets;
     float loss_scale;
     uint8_t* stash;
+    uint8_t* stash2;         // partial T-Recomp: kept stash of layers [split, n)
+    int split;               // 0 = every layer in `stash`
     uint8_t* ws;             // backward workspace (ws_b bytes)
     const void* gin;         // d(chunk output) [M,h]; nullptr for the head chunk
     void* gout;              // d(chunk input) [M,h]; nullptr for the embedding chunk

@@ -46,10 +46,12 @@ class Plan:
 
     def __init__(self, model: Model, n_stages: int, n_microbatches: int, hbm_budget: int = 0,
                  strategy="tpipe", delay_rounds: int = -1, send_window: int = 0, offload: int = 0,
-                 act_distance: int = 0):
+                 act_distance: int = 0, recomp_layers: int = 0):
         L = lib()
         st = -1 if strategy in (None, "auto") else STRATEGY.get(strategy, strategy)
-        opts = D.PlanOpts(st, delay_rounds, send_window, offload if st >= 0 else -1, act_distance)
+        if st < 0 and offload == 0:
+            offload = -1
+        opts = D.PlanOpts(st, delay_rounds, send_window, offload, act_distance, recomp_layers)
         self._h = C.c_void_p()
         self.model = model
         check(L.tpipe_plan_create(C.byref(model.c()), n_stages, n_microbatches, hbm_budget,
@@ -60,6 +62,7 @@ class Plan:
         self.strategy, self.k, self.W, self.offload = (info.strategy, info.delay_rounds,
                                                        info.send_window, info.offload)
         self.act_distance = info.act_distance
+        self.recomp_layers = info.recomp_layers
         self.layers_chunk = (info.layers_chunk[0], info.layers_chunk[1])
         self.params_total = info.params_total
         self.channels = []

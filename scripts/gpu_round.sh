@@ -1,0 +1,10 @@
+#!/bin/bash
+# GPU pass: parity tests, smoke, bench line, executed capacity run.
+cd "${GRAFT_REPO_ROOT:-.}"
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+if [ "$1" = "cap" ]; then
+timeout 1200 python bench.py --capacity-run > gpurun_out/capacity.json 2> gpurun_out/capacity.err
+fi

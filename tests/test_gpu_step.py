@@ -25,11 +25,11 @@ def mods():
     return plan, runtime, params
 
 
-def build(cfg, p, m, strategy, dtype, offload=0, lr=1e-3, seed=11):
+def build(cfg, p, m, strategy, dtype, offload=0, lr=1e-3, seed=11, recomp_layers=0):
     P, RT, PR = mods()
     md = P.Model(cfg["n_layers"], cfg["hidden"], cfg["n_heads"], cfg["ffn_hidden"], cfg["vocab"],
                  cfg["seq_len"], cfg["micro_batch"], dtype)
-    plan = P.Plan(md, p, m, strategy=strategy, offload=offload)
+    plan = P.Plan(md, p, m, strategy=strategy, offload=offload, recomp_layers=recomp_layers)
     rt = RT.Runtime(plan, stage=-1, lr=lr)
     W = synth.weights(cfg["n_layers"], cfg["hidden"], cfg["ffn_hidden"], cfg["vocab"],
                       cfg["seq_len"], seed=seed, std=0.05, bias_std=0.02, ln_jitter=0.05)
@@ -110,6 +110,35 @@ def test_trecomp_bitexact_vs_tpipe(dtype):
         out.append((loss, [rt.get_grads(s, c) for s in range(p) for c in (1, 2)]))
     assert out[0][0] == out[1][0]
     for a, b in zip(out[0][1], out[1][1]):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+@pytest.mark.parametrize("dtype", [0, 1])
+@pytest.mark.parametrize("p,r", [(1, 1), (1, 3), (2, 1)])
+def test_partial_trecomp_bitexact_vs_tpipe(dtype, p, r):
+    """Partial T-Recomp (R25): R regenerates chunk-1 layers 1..r into the
+    recompute buffer while layers r+1..n1 keep their stash; loss and every
+    gradient are bit-identical to T-Pipe's, the updated parameters after one
+    optimizer step too, and the pool ledger high-water equals the plan peak."""
+    _P, RT, _PR = mods()
+    m = 8
+    tok, tgt = synth.tokens(C1["vocab"], m, C1["micro_batch"], C1["seq_len"], step=5)
+    out = []
+    for strategy, rl in (("tpipe", 0), ("tpipe_trecomp", r)):
+        plan, rt, _W = build(C1, p, m, strategy, dtype, recomp_layers=rl)
+        if rl:
+            assert plan.recomp_layers == r < plan.layers_chunk[0]
+        loss = rt.step(tok, tgt, RT.STEP_NO_OPT)
+        grads = [rt.get_grads(s, c) for s in range(p) for c in (1, 2)]
+        rt.step(tok, tgt)
+        params = [rt.get_params(s, c) for s in range(p) for c in (1, 2)]
+        st = rt.stats()
+        for s in range(p):
+            assert st["pool_high_water"][s] == plan.peak(s)["total_peak"]
+        out.append((loss, grads, params))
+        rt.close()
+    assert out[0][0] == out[1][0]
+    for a, b in zip(out[0][1] + out[0][2], out[1][1] + out[1][2]):
         assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
 
 

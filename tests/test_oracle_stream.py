@@ -69,3 +69,70 @@ def test_trecomp_bytes_below_tpipe():
     a = T.replay(*[x[0] for x in T.build_streams(d, 8, 32, "tpipe")])
     b = T.replay(*[x[0] for x in T.build_streams(d, 8, 32, "tpipe_trecomp")])
     assert b["total_peak"] < a["total_peak"]
+
+
+# ---------------------------------------------------------------- partial T-Recomp (R25)
+def _kept_live_count(order, upto):
+    """Chunk-1 micro-batches whose forward has started and whose backward has
+    not ended after the first `upto` compute ops of the stage's order (the
+    P:611 lifespan F(1,i) start -> B(1,i) end), counted from the schedule."""
+    started = {op[2] for op in order[:upto] if op[0] == "F" and op[1] == 1}
+    ended = {op[2] for op in order[:upto] if op[0] == "B" and op[1] == 1}
+    return len(started - ended)
+
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+@pytest.mark.parametrize("n", [4, 6])
+def test_partial_trecomp_kept_stash_follows_schedule(p, n):
+    """Partial T-Recomp of r of the n1 chunk-1 layers: after every compute op
+    of the T-Recomp order (oracle.schedule, independent of the stream
+    builder), the live kept-stash bytes equal (n1 - r) x per-layer stash x the
+    number of chunk-1 micro-batches inside their F -> B lifespan, and the
+    recompute buffer holds at most one micro-batch's r layers (P:666's one
+    buffer block)."""
+    d = desc(n * p)
+    n1 = T.layers_per_chunk(d, p, 2)[0]
+    m = 2 * p + 1
+    orders = S.strategy_orders("tpipe_trecomp", p, m)[0]
+    for r in range(1, n1):
+        st, _static = T.build_streams(d, p, m, "tpipe_trecomp", recomp_layers=r)
+        for s in range(p):
+            z = T.sizes(d, p, 2, s, 1)
+            keep, rec = T.partial_trecomp_split(z, n1, r)
+            assert keep == (n1 - r) * z["layer_stash"] and keep + rec == z["stash"]
+            live = {}
+            k = 0
+            for ins in st[s]:
+                for name, _cat, b in ins.allocs:
+                    live[name] = b
+                if ins.kind in ("F", "B", "R"):
+                    k += 1
+                    kept = sum(b for nm, b in live.items() if nm[0] == "STASH" and nm[1] == 1)
+                    rbuf = [b for nm, b in live.items() if nm[0] == "RBUF"]
+                    assert kept == keep * _kept_live_count(orders[s], k - (ins.kind == "B"))
+                    assert len(rbuf) <= 1 and all(b == rec for b in rbuf)
+                for name in ins.frees:
+                    live.pop(name)
+
+
+@pytest.mark.parametrize("p", [1, 4, 8])
+def test_partial_trecomp_endpoints(p):
+    """r = n1 is exactly block-wise T-Recomp; peaks are non-increasing in r,
+    and r = 1 already stores less than plain T-Pipe whenever more than one
+    chunk-1 block is in flight (m >= 2p)."""
+    d = desc(6 * p)
+    n1 = T.layers_per_chunk(d, p, 2)[0]
+    m = 4 * p
+    full, fst = T.build_streams(d, p, m, "tpipe_trecomp")
+    same, sst = T.build_streams(d, p, m, "tpipe_trecomp", recomp_layers=n1)
+    assert [[(i.key(), i.allocs, i.frees) for i in x] for x in full] == \
+        [[(i.key(), i.allocs, i.frees) for i in x] for x in same]
+    tp, tst = T.build_streams(d, p, m, "tpipe")
+    for s in range(p):
+        pk = [T.replay(*[x[s] for x in T.build_streams(d, p, m, "tpipe_trecomp", recomp_layers=r)])
+              ["total_peak"] for r in range(1, n1 + 1)]
+        assert pk == sorted(pk, reverse=True)
+        if p > 1:
+            assert pk[0] < T.replay(tp[s], tst[s])["total_peak"]
+    with pytest.raises(ValueError):
+        T.build_streams(d, p, m, "tpipe_trecomp", recomp_layers=n1 + 1)

@@ -236,3 +236,61 @@ def test_activation_offload_streams_match_oracle(p, dist):
     from paper_2503_03182_b200._lib import TPipeError
     with pytest.raises(TPipeError, match="activation offload"):
         P.Plan(pd, p, 16, strategy="tpipe_trecomp", offload=P.OFFLOAD_ACTIVATIONS)
+
+
+@pytest.mark.parametrize("p", [1, 2, 4, 8])
+@pytest.mark.parametrize("n", [4, 6])
+@pytest.mark.parametrize("dtype", [T.BF16, T.FP32])
+def test_partial_trecomp_streams_match_oracle(p, n, dtype):
+    """Partial T-Recomp (R25, NEXT-1): for every r in 1..n1 the planner's
+    instruction streams, buffer sizes and per-category peaks equal the
+    oracle's; r = n1 is block-wise T-Recomp."""
+    P = _plan_mod()
+    L = n * p
+    od = T.ModelDesc(L, 64, 4, 256, 128, 32, 2, dtype)
+    pd = P.Model(L, 64, 4, 256, 128, 32, 2, dtype)
+    n1 = T.layers_per_chunk(od, p, 2)[0]
+    m = 2 * p + 2
+    full = P.Plan(pd, p, m, strategy="tpipe_trecomp")
+    assert full.recomp_layers == n1
+    for r in range(1, n1 + 1):
+        plan = P.Plan(pd, p, m, strategy="tpipe_trecomp", recomp_layers=r)
+        assert plan.recomp_layers == r
+        st, static = T.build_streams(od, p, m, "tpipe_trecomp", recomp_layers=r)
+        for s in range(p):
+            got, bufs = plan.ops(s)
+            strip = [{k: o[k] for k in ("kind", "chunk", "mb", "peer", "channel", "msg")} for o in got]
+            assert strip == oracle_ops(st[s])
+            for g, w in zip(got, st[s]):
+                assert [(bufs[a][1], bufs[a][4]) for a in g["allocs"]] == [(c, b) for _n, c, b in w.allocs]
+                assert len(g["frees"]) == len(w.frees)
+            rep = T.replay(st[s], static[s])
+            pk = plan.peak(s)
+            for cat in ("model_state", "io", "act", "recomp_buf", "comm", "workspace"):
+                assert pk[cat] == rep.get(cat, 0), cat
+            assert pk["total_peak"] == rep["total_peak"]
+            if r == n1:
+                assert pk == full.peak(s)
+    from paper_2503_03182_b200._lib import TPipeError
+    with pytest.raises(TPipeError, match="recomp_layers"):
+        P.Plan(pd, p, m, strategy="tpipe_trecomp", recomp_layers=n1 + 1)
+
+
+def test_auto_escalation_partial_trecomp():
+    """The auto ladder spends the least recompute that fits: a budget between
+    the r=1 and r=2 peaks selects r=2 (of n1=3), before model-state offload."""
+    P = _plan_mod()
+    md = P.Model(48, 64, 4, 256, 128, 32, 2)            # p=8: n=6 -> n1=3
+    pk = {r: max(P.Plan(md, 8, 32, strategy="tpipe_trecomp", recomp_layers=r).peak(s)["total_peak"]
+                 for s in range(8)) for r in (1, 2, 3)}
+    tp = max(P.Plan(md, 8, 32, strategy="tpipe").peak(s)["total_peak"] for s in range(8))
+    assert tp > pk[1] > pk[2] > pk[3]
+    auto = P.Plan(md, 8, 32, hbm_budget=pk[2], strategy="auto")
+    assert (auto.strategy, auto.offload, auto.recomp_layers) == (P.S_TPIPE_TRECOMP, 0, 2)
+    auto = P.Plan(md, 8, 32, hbm_budget=pk[1], strategy="auto")
+    assert auto.recomp_layers == 1
+    off = max(P.Plan(md, 8, 32, strategy="tpipe_trecomp", recomp_layers=1,
+                     offload=P.OFFLOAD_MODEL_STATE).peak(s)["total_peak"] for s in range(8))
+    if off < pk[3]:
+        auto = P.Plan(md, 8, 32, hbm_budget=off, strategy="auto")
+        assert (auto.offload, auto.recomp_layers) == (P.OFFLOAD_MODEL_STATE, 1)
