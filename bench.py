@@ -338,8 +338,8 @@ def hbm_kernels(c, hbm_peak):
     """HBM-bound stage-executor kernels at the workload's launch shape (M = b*s
     rows): achieved GB/s = algorithmic bytes (each operand read
     once, each result written once) / CUDA-event time of 20 back-to-back
-    launches on torch's current stream (the kernels' launch stream), vs the
-    measured HBM copy peak. Working sets of 8-100 MB partly hit L2 between
+    launches on torch's current stream (the kernels' launch stream), captured
+    in one CUDA graph, vs the measured HBM copy peak. Working sets of 8-100 MB partly hit L2 between
     launches, so back-to-back figures are an upper bound on the in-step rate."""
     import torch
     from paper_2503_03182_b200 import kernels as K
@@ -348,13 +348,24 @@ def hbm_kernels(c, hbm_peak):
     bf = torch.bfloat16
 
     def tm(fn, iters=20):
+        # the launches are captured in a CUDA graph so that the ctypes call
+        # overhead (~10 us) does not starve the GPU between launches
         for _ in range(3):
             fn()
         torch.cuda.synchronize()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(gr, stream=side):
+                for _ in range(iters):
+                    fn()
+        torch.cuda.current_stream().wait_stream(side)
+        gr.replay()
+        torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(iters):
-            fn()
+        gr.replay()
         e1.record()
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / iters
