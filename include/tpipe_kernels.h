@@ -66,6 +66,13 @@ void tpipe_k_gemm_set_stream_k(int on);
  * half of the A and B operands. Used when the shape yields >= 32 such tiles. */
 void tpipe_k_gemm_set_pair(int on);
 
+/* Enable (1) or disable (0, default) 256 x 512 CTA-pair tiles (two N = 256
+ * tcgen05.mma per K step sharing the A stage; one TMEM accumulator): fewer
+ * operand bytes per flop for the L2 -> SM bound mainloop. Chosen for pair
+ * shapes whose 256 x 512 tile count fills the 74 pairs' waves as well as the
+ * 256 x 256 tiling (process-wide; for A/B measurement). */
+void tpipe_k_gemm_set_wide(int on);
+
 /* LayerNorm forward over rows of length h (eps 1e-5, biased variance):
  * y = (x-mean)*rstd*gamma + beta; mean/rstd fp32 [rows]. */
 int tpipe_k_ln_fwd(int dtype, const void* x, const void* gamma, const void* beta,

@@ -249,19 +249,34 @@ constexpr int TC_BM = 128, TC_BK = 64;
 __host__ __device__ constexpr int tc_threads(int ew) { return 128 + 32 * ew; }
 static bool g_stream_k_enabled = false;   // measured slower on the model shapes
 static bool g_pair_enabled = true;
+// 256 x 512 pair tiles measured slower on the model shapes (fc1 fprop 54 -> 70 us,
+// fc2 dgrad 58 -> 81 us: the exposed single-accumulator epilogue outweighs the
+// 25% fewer operand bytes; profiles/r1_gemm_wide_ab.jsonl): off by default
+static bool g_wide_enabled = false;
 void gemm_set_stream_k(int on) { g_stream_k_enabled = on != 0; }
 void gemm_set_pair(int on) { g_pair_enabled = on != 0; }
+void gemm_set_wide(int on) { g_wide_enabled = on != 0; }
 
 // CG = 1: one CTA computes a 128 x BN tile. CG = 2: a CTA pair (cluster of 2
 // on one TPC) computes a 256 x BN tile with tcgen05.mma.cta_group::2; each CTA
 // stages 128 rows of A and BN/2 rows of B, so per-SM operand traffic (L2->smem
 // and smem->tensor core) is 2/3 of the CG = 1, BN = 256 tile's.
+// BN = 512 (CG = 2 only): the pair computes a 256 x 512 tile as two N = 256
+// MMAs per K step that share the A stage; per SM 48 KB of operands feed 1024
+// MMA clocks (47 B/clk vs 64 B/clk for 256 x 256: the mainloop is bound by
+// L2 -> SM operand delivery, profiles/r1_gemm_l2_analysis.txt). The 512
+// accumulator columns fill TMEM, so there is one accumulator (the epilogue of
+// a tile is not overlapped with the next tile's mainloop).
 template <int BN, int CG = 1, int EPI_WARPS = 4>
 struct TcCfg {
-    static constexpr int STAGES = CG == 2 ? 6 : (BN == 256 ? 4 : 6);
+    static_assert(BN <= 256 || (BN == 512 && CG == 2), "BN = 512 needs a CTA pair");
+    static constexpr int STAGES = BN == 512 ? 4 : (CG == 2 ? 6 : (BN == 256 ? 4 : 6));
     static constexpr int A_BYTES = TC_BM * TC_BK * 2;
     static constexpr int B_BYTES = (BN / CG) * TC_BK * 2;
-    static constexpr int TMEM_COLS = 2 * BN;
+    static constexpr int NACC = BN == 512 ? 1 : 2;          // TMEM accumulator buffers
+    static constexpr int TMEM_COLS = NACC * BN;
+    static constexpr int MMA_N = BN > 256 ? 256 : BN;       // N of one tcgen05.mma
+    static constexpr int B_LOAD_ROWS = BN == 512 ? 128 : BN / CG;   // rows per B TMA box (K-major)
     // epilogue staging: EPI_WARPS warps x 2 buffers x one 32 x 32 chunk; the
     // 8-warp epilogues (GELU, dGELU, residual) only store bf16 (2 KB chunks),
     // so both variants fit the same operand ring depth
@@ -491,7 +506,9 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
             while (sch.next(tile, kb0, kb1)) {
                 const int mb = tile % num_m, nb = tile / num_m;
                 const int am = mb * TM + rank * TC_BM;     // this CTA's A rows
-                const int bn = nb * BN + rank * BNC;       // this CTA's B rows
+                // this CTA's B rows: [bn, bn + BNC); BN = 512: [bn, +128) and [bn + 256, +128)
+                // (MMA h of the pair reads tile columns [256h, 256h + 256), 128 per CTA)
+                const int bn = BN == 512 ? nb * BN + rank * 128 : nb * BN + rank * BNC;
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* a = sA + stage * Cfg::A_BYTES;
@@ -524,11 +541,16 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
                                 tma_load_2d_pair(a + i * 64 * TC_BK * 2, &tmA, fb, am + i * 64, kb * TC_BK);
                         }
                         if (!B_MN) {
-                            tma_load_2d_pair(b, &tmB, fb, kb * TC_BK, bn);
+#pragma unroll
+                            for (int hh = 0; hh < BNC / Cfg::B_LOAD_ROWS; ++hh)
+                                tma_load_2d_pair(b + hh * Cfg::B_LOAD_ROWS * TC_BK * 2, &tmB, fb, kb * TC_BK,
+                                                 bn + hh * 256);
                         } else {
 #pragma unroll
                             for (int i = 0; i < BNC / 64; ++i)
-                                tma_load_2d_pair(b + i * 64 * TC_BK * 2, &tmB, fb, bn + i * 64, kb * TC_BK);
+                                tma_load_2d_pair(b + i * 64 * TC_BK * 2, &tmB, fb,
+                                                 BN == 512 ? bn + (i >> 1) * 256 + (i & 1) * 64 : bn + i * 64,
+                                                 kb * TC_BK);
                         }
                         if (rank != 0) mbar_arrive_cluster(fb);
                     }
@@ -540,7 +562,7 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
     } else if (warp == 1) {
         if (rank == 0) {
             // ---------------- MMA issuer (whole warp of the pair leader; the elected lane issues)
-            const uint32_t idesc = tc_idesc<BN, A_MN, B_MN, CG>();
+            const uint32_t idesc = tc_idesc<Cfg::MMA_N, A_MN, B_MN, CG>();
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
@@ -548,8 +570,8 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
             sch.init(num_tiles, num_kb, sk, CG);
             int tile, kb0, kb1;
             for (; sch.next(tile, kb0, kb1); ++it) {
-                const int acc = it & 1;
-                const uint32_t aph = (it >> 1) & 1;
+                const int acc = Cfg::NACC == 2 ? (it & 1) : 0;
+                const uint32_t aph = Cfg::NACC == 2 ? ((it >> 1) & 1) : (it & 1);
                 mbar_wait(&tempty[acc], aph ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem_base + acc * BN;
@@ -570,6 +592,11 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
                         const uint32_t accum = (kb != kb0 || k != 0) ? 1u : 0u;
                         if (CG == 2) umma_bf16_pair(d, da, db, idesc, accum);
                         else umma_bf16(d, da, db, idesc, accum);
+                        if (BN == 512) {   // second N half: B rows [128, 256) of the stage (+16 KB)
+                            const uint64_t db2 = B_MN ? umma_desc_sw128(b_addr + 16384 + k * 2048, TC_BK * 128, 1024)
+                                                      : umma_desc_sw128(b_addr + 16384 + k * 32, 0, 1024);
+                            umma_bf16_pair(d + 256, da, db2, idesc, accum);
+                        }
                     }
                     if (CG == 2) umma_commit_pair(&empty[stage], 3);
                     else umma_commit(&empty[stage]);
@@ -604,8 +631,8 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
         int tile, kb0, kb1;
         for (; sch.next(tile, kb0, kb1); ++it) {
             const int mb = tile % num_m, nb = tile / num_m;
-            const int acc = it & 1;
-            const uint32_t aph = (it >> 1) & 1;
+            const int acc = Cfg::NACC == 2 ? (it & 1) : 0;
+            const uint32_t aph = Cfg::NACC == 2 ? ((it >> 1) & 1) : (it & 1);
             mbar_wait(&tfull[acc], aph);
             tc_fence_after();
             const int m0 = mb * TM + rank * TC_BM + ew * 32;
@@ -799,7 +826,7 @@ static int launch_tc(const GemmDesc& g, cudaStream_t st) {
         rc = make_map(&ta, g.A, g.M, g.K, g.lda, 64, TC_BK);
     if (rc) return rc;
     if (!B_MN)
-        rc = make_map(&tb, g.B, g.K, g.N, g.ldb, TC_BK, BNC);
+        rc = make_map(&tb, g.B, g.K, g.N, g.ldb, TC_BK, Cfg::B_LOAD_ROWS);
     else
         rc = make_map(&tb, g.B, g.N, g.K, g.ldb, 64, TC_BK);
     if (rc) return rc;
@@ -820,7 +847,8 @@ static int launch_tc(const GemmDesc& g, cudaStream_t st) {
     const int num_kb = (g.K + TC_BK - 1) / TC_BK;
     const int tiles = num_m * num_n;
     const int units = num_sms() / CG;
-    const int sk = g_stream_k_enabled && use_stream_k(tiles, num_kb, units) ? 1 : 0;
+    // (stream-K partial slots are 128 x 256: not for BN = 512)
+    const int sk = BN <= 256 && g_stream_k_enabled && use_stream_k(tiles, num_kb, units) ? 1 : 0;
     const int grid = CG * (sk ? units : (tiles < units ? tiles : units));
     SkWs w;
     unsigned epoch = 0;
@@ -869,8 +897,16 @@ int gemm_tc(const GemmDesc& g, cudaStream_t st) {
     // loop is long (>= 4096); a 2048 x 2048 x 2048 GEMM (64 pair tiles on 74
     // pairs) is faster as 128 single-CTA tiles.
     const long pair_tiles = (long)((g.M + 255) / 256) * ((g.N + 255) / 256);
-    if (g_pair_enabled && (pair_tiles >= 96 || (pair_tiles >= 32 && g.K >= 4096)))
+    if (g_pair_enabled && (pair_tiles >= 96 || (pair_tiles >= 32 && g.K >= 4096))) {
+        // 256 x 512 pair tiles when they fill the 74 pairs' waves as well as
+        // 256 x 256 does (same wave efficiency, half the tiles)
+        const long units = num_sms() / 2;
+        const long wide_tiles = (long)((g.M + 255) / 256) * ((g.N + 511) / 512);
+        auto eff = [&](long t) { return (double)t / (double)(((t + units - 1) / units) * units); };
+        if (g_wide_enabled && wide_tiles >= units && eff(wide_tiles) >= eff(pair_tiles) - 0.02)
+            return launch_majors<512, 2>(g, st);
         return launch_majors<256, 2>(g, st);
+    }
     const int num_m = (g.M + TC_BM - 1) / TC_BM;
     // N=128 tiles read 8 KB of operands per 64-cycle MMA (128 B/cycle, the
     // shared-memory limit); N=256 tiles need 96 B/cycle. Prefer 256 whenever

@@ -106,3 +106,7 @@ def tpipe_k_gemm_set_stream_k(on):
 
 def tpipe_k_gemm_set_pair(on):
     lib().tpipe_k_gemm_set_pair(1 if on else 0)
+
+
+def tpipe_k_gemm_set_wide(on):
+    lib().tpipe_k_gemm_set_wide(1 if on else 0)

@@ -172,6 +172,55 @@ def test_gemm_cta_pair(M, N, Kd, majors):
     assert max_rel(h(Acc), h(single[1])) < 1e-5
 
 
+@pytest.mark.parametrize("M,N,Kd", [(2048, 8192, 2048), (8192, 2048, 1024), (2000, 8992, 320),
+                                    (2048, 50304, 256)])
+@pytest.mark.parametrize("majors", [(1, 1), (1, 0), (0, 0)])
+def test_gemm_wide_pair(M, N, Kd, majors):
+    """256 x 512 CTA-pair tiles (two N = 256 MMAs per K step, one TMEM
+    accumulator) incl. ragged M / N / K edges and a last N tile whose second
+    half lies wholly beyond N: matches fp64 and is bit-identical to the
+    256 x 256 pair tiling (same per-element K order) for fp32 store, fp32
+    accumulate, bias+GELU and dGELU epilogues."""
+    ak, bk = majors
+    k = K()
+    rng = np.random.default_rng(M + 5 * N + Kd)
+    A = rng.standard_normal((M, Kd)).astype(np.float32)
+    B = rng.standard_normal((N, Kd)).astype(np.float32)
+    At = t(A if ak else A.T.copy(), "bf16")
+    Bt = t(B if bk else B.T.copy(), "bf16")
+    ref = h(At if ak else At.T) @ h(Bt if bk else Bt.T).T
+    U = t(rng.standard_normal((M, N)), "bf16")
+    bias = t(rng.standard_normal(N), "bf16")
+    args = (M, N, Kd, At, Kd if ak else M, ak, Bt, Kd if bk else N, bk)
+
+    def run():
+        C = torch.zeros((M, N), device=dev, dtype=torch.float32)
+        k.tpipe_k_gemm(1, *args, k.EPI_STORE_F32, C, N)
+        Acc = torch.full((M, N), 2.0, device=dev, dtype=torch.float32)
+        k.tpipe_k_gemm(1, *args, k.EPI_ACC_F32, Acc, N)
+        Cd = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
+        Cg = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
+        k.tpipe_k_gemm(1, *args, k.EPI_DGELU, Cd, N, C2=Cg, ldc2=N, aux=U, ldaux=N)
+        Cu = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
+        Cgl = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
+        k.tpipe_k_gemm(1, *args, k.EPI_BIAS_GELU, Cu, N, bias=bias, C2=Cgl, ldc2=N)
+        torch.cuda.synchronize()
+        return C, Acc, Cd, Cg, Cu, Cgl
+    try:
+        k.tpipe_k_gemm_set_wide(1)
+        wide = run()
+    finally:
+        k.tpipe_k_gemm_set_wide(0)
+    narrow = run()
+    C, Acc, Cd, Cg, Cu, Cgl = wide
+    assert max_rel(h(C), ref) < 1e-4
+    assert max_rel(h(Acc), 2 + ref) < 1e-4
+    assert rel_l2(h(Cd), ref * R.gelu_grad(h(U))) < 1e-2
+    assert rel_l2(h(Cu), ref + h(bias)) < 1e-2
+    for u, v in zip(wide, narrow):
+        assert torch.equal(u, v)
+
+
 @pytest.mark.parametrize("dtype", ["bf16", "fp32"])
 def test_gemm_epilogues(dtype):
     """bias / residual / GELU / dGELU epilogues vs fp64 definitions."""
