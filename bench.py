@@ -713,6 +713,13 @@ def run_tpipe(args):
         out["capacity_80GiB"] = {"p": max(N, 8) if N == 1 else N, "shape": "h=4096 a=32 s=8192 V=32000 b=1 m=32",
                                  **capacity(max(N, 8) if N == 1 else N)}
         out["cpu_baseline"] = cpu_baseline(c)
+        out["paper_context"] = {
+            "note": "the paper's own figures, other hardware (64 BirenTech GPUs, PP8xTP8, 32 GB HBM each, "
+                    "P:443, P:471); context, not targets",
+            "max_size_vs_1f1b": 2.4, "max_size_vs_1f1b_r50": 1.5,
+            "tpipe_all_throughput_vs_1f1b_r50": 0.9758,
+            "this_build": "capacity_80GiB (planner, p=8) and bench.py --capacity-run "
+                          "(executed, profiles/r1_capacity_measured_v2.json: 3.53x params at 0.906x model TFLOP/s)"}
     if dist:
         dist.barrier()
     return out
