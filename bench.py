@@ -159,7 +159,8 @@ def cpu_baseline(c, seconds_cap=30.0):
                       f"in {dt:.1f}s; model tokens/s = layer tokens/s / L={c['n_layers']}"}
 
 
-def capacity(p, strategies=("1f1b", "tpipe", "tpipe_trecomp", "tpipe_all")):
+def capacity(p, strategies=("1f1b", "tpipe", "tpipe_trecomp", "tpipe_all", "interleave",
+                            "interleave_trecomp")):
     """Max trainable layers / params under an 80 GiB per-GPU plan peak for the
     C5 sweep shape (h=4096, s=8192), L in steps of p (planner byte model)."""
     from paper_2503_03182_b200 import plan as P
@@ -219,7 +220,8 @@ def capacity_plans(p=CAP_P, budget=CAP_BUDGET_GIB * 2 ** 30, m=CAP_M):
     from paper_2503_03182_b200._lib import TPipeError
     strategies = {"1f1b": ("1f1b", 0), "1f1b_full_recomp": ("1f1b_full_recomp", 0),
                   "tpipe": ("tpipe", 0), "tpipe_trecomp": ("tpipe_trecomp", 0),
-                  "tpipe_all": ("tpipe_trecomp", P.OFFLOAD_MODEL_STATE | P.OFFLOAD_DEVICE_OPT)}
+                  "tpipe_all": ("tpipe_trecomp", P.OFFLOAD_MODEL_STATE | P.OFFLOAD_DEVICE_OPT),
+                  "interleave": ("interleave", 0), "interleave_trecomp": ("interleave_trecomp", 0)}
     best = {}
     for name, (strat, off) in strategies.items():
         for L in range(p, 400, p):
@@ -251,7 +253,8 @@ def run_capacity(args):
     import synth
     p, m, budget = CAP_P, CAP_M, CAP_BUDGET_GIB * 2 ** 30
     best = capacity_plans()
-    runs = [(n, *best[n]) for n in ("1f1b", "1f1b_full_recomp", "tpipe", "tpipe_trecomp", "tpipe_all")
+    runs = [(n, *best[n]) for n in ("1f1b", "1f1b_full_recomp", "tpipe", "tpipe_trecomp", "tpipe_all",
+                                     "interleave", "interleave_trecomp")
             if n in best]
     if "1f1b_full_recomp" in best and "tpipe_all" in best:
         runs.append(("tpipe_all@1f1b_full_recomp_size", best["1f1b_full_recomp"][0], *best["tpipe_all"][1:]))
@@ -300,7 +303,8 @@ def run_capacity(args):
                                         vocab=C5["vocab"]))
         tf = tokens * fl / (ms / 1e3) / 1e12
         res[name] = {"strategy": strat, "offload": plan.offload, "n_layers": L,
-                     "plan_strategy": ["1f1b", "1f1b_full_recomp", "tpipe", "tpipe_trecomp"][plan.strategy],
+                     "plan_strategy": ["1f1b", "1f1b_full_recomp", "tpipe", "tpipe_trecomp", "interleave",
+                                       "interleave_trecomp"][plan.strategy],
                      "recomp_layers": plan.recomp_layers, "layers_chunk": list(plan.layers_chunk),
                      "params_B": round(plan.params_total / 1e9, 3),
                      "plan_peak_GiB": [round(plan.peak(s)["total_peak"] / 2 ** 30, 3) for s in range(p)],

@@ -72,7 +72,11 @@ enum {
     TPIPE_S_1F1B = 0,             /* DAPPLE 1F1B, P:202 (baseline) */
     TPIPE_S_1F1B_FULL_RECOMP = 1, /* 1F1B + full layer-grouped recompute */
     TPIPE_S_TPIPE = 2,            /* T-Pipe, v = 2 */
-    TPIPE_S_TPIPE_TRECOMP = 3     /* T-Pipe + block-wise T-Recomp of chunk 1 */
+    TPIPE_S_TPIPE_TRECOMP = 3,    /* T-Pipe + block-wise T-Recomp of chunk 1 */
+    TPIPE_S_INTERLEAVE = 4,       /* Interleave-1F1B, v = 2 (Megatron virtual pipeline);
+                                     needs n_microbatches % n_stages == 0 */
+    TPIPE_S_INTERLEAVE_TRECOMP = 5 /* Interleave-1F1B + block-wise T-Recomp of chunk 1 (P:367,
+                                     Fig. 6(e); DESIGN R26) */
 };
 
 #define TPIPE_OFFLOAD_MODEL_STATE 1   /* T-Offload of chunk-2 grads/optimizer/weights */

@@ -29,6 +29,10 @@ Schedules
   Fig. 6(b)): recompute fused into B(s,1,i) (B1 = 3).
 * Interleave-1F1B (Megatron virtual pipeline), for the paper's
   m_a(1+(p-1)/(pv)) and bubble/v statements.
+* Interleave-1F1B + T-Recomp (Fig. 6(e)):
+  the interleave order with R(s,1,i) inserted immediately before B(s,1,i),
+  chunk 1 (the chunk with the poorest temporal locality) recomputed
+  block-wise exactly as in T-Recomp (R26).
 """
 
 from __future__ import annotations
@@ -141,6 +145,20 @@ def onef1b_orders(p: int, m: int):
             lst.append(("B", 1, i))
         orders.append(lst)
     return orders
+
+
+def interleave_trecomp_orders(p: int, m: int, v: int = 2):
+    """Interleave-1F1B + block-wise T-Recomp of chunk 1 (DESIGN R26):
+    R(s,1,i) right before each B(s,1,i) of the interleave order."""
+    out = []
+    for lst in interleave_orders(p, m, v):
+        withr = []
+        for op in lst:
+            if op[0] == "B" and op[1] == 1:
+                withr.append(("R", 1, op[2]))
+            withr.append(op)
+        out.append(withr)
+    return out
 
 
 def interleave_orders(p: int, m: int, v: int):
@@ -426,4 +444,8 @@ def strategy_orders(strategy: str, p: int, m: int, k: int | None = None):
         return onef1b_orders(p, m), 1, False, default_durations(1, b_extra=1)
     if strategy == "1f1b_full_recomp":
         return onef1b_orders(p, m), 1, False, default_durations(1, b_extra=2)
+    if strategy == "interleave":
+        return interleave_orders(p, m, 2), 2, False, default_durations(2)
+    if strategy == "interleave_trecomp":
+        return interleave_trecomp_orders(p, m, 2), 2, True, default_durations(2)
     raise ValueError(strategy)

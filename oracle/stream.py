@@ -182,6 +182,8 @@ STRATS = {
     "tpipe_trecomp": ("tpipe_trecomp", 2, True, False),
     "1f1b": ("1f1b", 1, False, False),
     "1f1b_full_recomp": ("1f1b_full_recomp", 1, False, True),
+    "interleave": ("interleave", 2, False, False),
+    "interleave_trecomp": ("interleave_trecomp", 2, True, False),
 }
 
 

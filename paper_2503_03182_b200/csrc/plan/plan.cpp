@@ -145,6 +145,36 @@ static std::vector<std::vector<COp>> tpipe_order(int p, int m, bool recomp, int 
     return out;
 }
 
+// Interleave-1F1B (Megatron virtual pipeline) for v = 2, m % p == 0:
+// virtual forward q (0 .. 2m-1) runs chunk (q mod 2p)/p + 1 of micro-batch
+// (q / 2p) p + q mod p + 1; virtual backward q runs the mirrored chunk
+// 2 - (q mod 2p)/p of the same micro-batch. Stage s warms up with
+// min(2(p-s-1) + p, 2m) forwards, then alternates one forward / one backward,
+// then drains. recomp: R(s,1,i) right before each B(s,1,i) (R26).
+static std::vector<std::vector<COp>> interleave_order(int p, int m, bool recomp) {
+    const int total = 2 * m;
+    auto fwd = [&](int q) -> COp { return {KF, (q % (2 * p)) / p + 1, (q / (2 * p)) * p + q % p + 1}; };
+    auto bwd = [&](int q) -> COp { return {KB, 2 - (q % (2 * p)) / p, (q / (2 * p)) * p + q % p + 1}; };
+    std::vector<std::vector<COp>> out(p);
+    for (int s = 0; s < p; ++s) {
+        const int w = std::min(2 * (p - s - 1) + p, total);
+        std::vector<COp> lst;
+        auto push_b = [&](int q) {
+            const COp b = bwd(q);
+            if (recomp && b[1] == 1) lst.push_back({KR, 1, b[2]});
+            lst.push_back(b);
+        };
+        for (int q = 0; q < w; ++q) lst.push_back(fwd(q));
+        for (int q = 0; q < total - w; ++q) {
+            lst.push_back(fwd(w + q));
+            push_b(q);
+        }
+        for (int q = total - w; q < total; ++q) push_b(q);
+        out[s] = lst;
+    }
+    return out;
+}
+
 static std::vector<std::vector<COp>> onef1b_order(int p, int m) {
     std::vector<std::vector<COp>> out(p);
     for (int s = 0; s < p; ++s) {
@@ -569,7 +599,12 @@ static int make_plan(const tpipe_model_desc* model, int p, int m, int strategy, 
     P->W = W;
     P->offload = offload;
     P->act_distance = act_distance > 0 ? act_distance : 2;
-    const bool is_tp = strategy == TPIPE_S_TPIPE || strategy == TPIPE_S_TPIPE_TRECOMP;
+    const bool is_il = strategy == TPIPE_S_INTERLEAVE || strategy == TPIPE_S_INTERLEAVE_TRECOMP;
+    const bool is_tp = strategy == TPIPE_S_TPIPE || strategy == TPIPE_S_TPIPE_TRECOMP || is_il;
+    if (is_il && m % p) {
+        delete P;
+        return set_error(TPIPE_E_INCOMPAT, "interleave-1F1B needs n_microbatches %% n_stages == 0");
+    }
     P->v = is_tp ? 2 : 1;
     const int n = model->n_layers / p;
     if (P->v == 2) {
@@ -596,7 +631,7 @@ static int make_plan(const tpipe_model_desc* model, int p, int m, int strategy, 
         }
         P->layers[0] = n;
     }
-    const bool trecomp = strategy == TPIPE_S_TPIPE_TRECOMP;
+    const bool trecomp = strategy == TPIPE_S_TPIPE_TRECOMP || strategy == TPIPE_S_INTERLEAVE_TRECOMP;
     if (trecomp && recomp_layers > P->layers[0]) {
         const int n1 = P->layers[0];
         delete P;
@@ -604,8 +639,12 @@ static int make_plan(const tpipe_model_desc* model, int p, int m, int strategy, 
                          recomp_layers, n1);
     }
     P->rl = trecomp ? (recomp_layers > 0 ? recomp_layers : P->layers[0]) : 0;
-    P->k = trecomp ? (k < 0 ? delay_rounds_appB(p) : k) : 0;
-    if (is_tp) {
+    P->k = (trecomp && !is_il) ? (k < 0 ? delay_rounds_appB(p) : k) : 0;
+    if (is_il) {
+        auto ord = interleave_order(p, m, trecomp);
+        P->order.assign(p, {});
+        for (int s = 0; s < p; ++s) P->order[s] = ord[s];
+    } else if (is_tp) {
         auto ord = tpipe_order(p, m, trecomp, P->k);
         P->order.assign(p, {});
         for (int s = 0; s < p; ++s) P->order[s] = ord[s];
@@ -642,7 +681,7 @@ TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, in
     tpipe_plan_opts o{-1, -1, 0, -1, 0, 0};
     if (opts) o = *opts;
     const int W = o.send_window > 0 ? o.send_window : 2;
-    if (o.strategy < -1 || o.strategy > TPIPE_S_TPIPE_TRECOMP) return set_error(TPIPE_E_INVALID, "strategy");
+    if (o.strategy < -1 || o.strategy > TPIPE_S_INTERLEAVE_TRECOMP) return set_error(TPIPE_E_INVALID, "strategy");
     if (o.delay_rounds < -1) return set_error(TPIPE_E_INVALID, "delay_rounds");
     if (o.recomp_layers < 0) return set_error(TPIPE_E_INVALID, "recomp_layers");
     if (o.strategy >= 0) {
@@ -756,7 +795,7 @@ TP_API int tpipe_plan_chunk_params(const tpipe_plan* P, int32_t s, int32_t c, ui
 TP_API int tpipe_plan_simulate(const tpipe_plan* P, tpipe_sim_report* out) {
     if (!P || !out) return set_error(TPIPE_E_INVALID, "NULL argument");
     const int p = P->p, v = P->v;
-    const bool rec = P->strategy == TPIPE_S_TPIPE_TRECOMP;
+    const bool rec = P->strategy == TPIPE_S_TPIPE_TRECOMP || P->strategy == TPIPE_S_INTERLEAVE_TRECOMP;
     auto dur = [&](int kind) -> long {
         if (v == 2) return kind == KB ? 2 : 1;
         if (kind == KF) return 2;

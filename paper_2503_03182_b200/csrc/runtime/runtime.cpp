@@ -290,7 +290,7 @@ int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags
     const Dims& D = rt->D;
     cudaStream_t cs = rt->stream;
     const int p = P.p, v = P.v;
-    const bool trecomp = P.strategy == TPIPE_S_TPIPE_TRECOMP;
+    const bool trecomp = P.strategy == TPIPE_S_TPIPE_TRECOMP || P.strategy == TPIPE_S_INTERLEAVE_TRECOMP;
     const bool no_opt = flags & TPIPE_STEP_NO_OPT;
 
     // allocations at instruction start

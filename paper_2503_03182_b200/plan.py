@@ -10,9 +10,10 @@ from . import _decl_plan as D
 from ._lib import check, lib
 
 FP32, BF16 = 0, 1
-S_1F1B, S_1F1B_FULL_RECOMP, S_TPIPE, S_TPIPE_TRECOMP = 0, 1, 2, 3
+S_1F1B, S_1F1B_FULL_RECOMP, S_TPIPE, S_TPIPE_TRECOMP, S_INTERLEAVE, S_INTERLEAVE_TRECOMP = range(6)
 STRATEGY = {"1f1b": S_1F1B, "1f1b_full_recomp": S_1F1B_FULL_RECOMP, "tpipe": S_TPIPE,
-            "tpipe_trecomp": S_TPIPE_TRECOMP}
+            "tpipe_trecomp": S_TPIPE_TRECOMP, "interleave": S_INTERLEAVE,
+            "interleave_trecomp": S_INTERLEAVE_TRECOMP}
 OFFLOAD_MODEL_STATE = 1
 OFFLOAD_ACTIVATIONS = 2
 OFFLOAD_DEVICE_OPT = 4   # with OFFLOAD_MODEL_STATE: streamed device AdamW (DESIGN R24)

@@ -66,7 +66,8 @@ def rel_l2(a, b):
     return float(np.linalg.norm(a - b) / (np.linalg.norm(b) + 1e-30))
 
 
-@pytest.mark.parametrize("strategy", ["tpipe", "tpipe_trecomp", "1f1b", "1f1b_full_recomp"])
+@pytest.mark.parametrize("strategy", ["tpipe", "tpipe_trecomp", "1f1b", "1f1b_full_recomp",
+                                      "interleave", "interleave_trecomp"])
 @pytest.mark.parametrize("p", [1, 2, 4])
 def test_step_fp32_parity(strategy, p):
     _P, RT, _PR = mods()
@@ -99,18 +100,21 @@ def test_step_bf16_parity(strategy):
 @pytest.mark.parametrize("dtype", [0, 1])
 def test_trecomp_bitexact_vs_tpipe(dtype):
     """T-Recomp regenerates chunk-1 activations with the same kernels, so the
-    gradients are bit-identical to T-Pipe's (BASELINE north_star)."""
+    gradients are bit-identical to T-Pipe's (BASELINE north_star); the
+    Interleave-1F1B orders (NEXT-2, with and without T-Recomp) accumulate each
+    chunk's gradients in the same micro-batch order, so they match too."""
     _P, RT, _PR = mods()
     p, m = 4, 8
     tok, tgt = synth.tokens(C1["vocab"], m, C1["micro_batch"], C1["seq_len"], step=3)
     out = []
-    for strategy in ("tpipe", "tpipe_trecomp"):
+    for strategy in ("tpipe", "tpipe_trecomp", "interleave", "interleave_trecomp"):
         plan, rt, _W = build(C1, p, m, strategy, dtype)
         loss = rt.step(tok, tgt, RT.STEP_NO_OPT)
         out.append((loss, [rt.get_grads(s, c) for s in range(p) for c in (1, 2)]))
-    assert out[0][0] == out[1][0]
-    for a, b in zip(out[0][1], out[1][1]):
-        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    for o in out[1:]:
+        assert out[0][0] == o[0]
+        for a, b in zip(out[0][1], o[1]):
+            assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
 
 
 @pytest.mark.parametrize("dtype", [0, 1])

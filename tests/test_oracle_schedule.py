@@ -360,3 +360,28 @@ def test_brute_force(p, m, want_min):
     assert n > 0
     tp = S.simulate(S.tpipe_orders(p, m), p, v, dur)["makespan"]
     assert tp == 6 * (m + p - 1) and tp >= best
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 8, 16])
+def test_interleave_trecomp_d9(p):
+    """P:367 / SURVEY D-9: Interleave-1F1B + block-wise T-Recomp of chunk 1
+    holds (p+1) blocks = (p+1)/(2p) m_a at stage 0 (-> 50%, vs plain
+    interleave's m_a(1 + (p-1)/(2p))); at p=8, m=16 its unit-model makespan is
+    133 vs 7(m+p-1) = 161 for 1F1B + 50% layer recompute."""
+    m = 2 * p
+    orders, v, rec, dur = S.strategy_orders("interleave_trecomp", p, m)
+    assert v == 2 and rec
+    for s in range(p):
+        lst = orders[s]
+        assert sum(op[0] == "R" for op in lst) == m
+        for n, op in enumerate(lst):
+            if op[0] == "B" and op[1] == 1:
+                assert lst[n - 1] == ("R", 1, op[2])
+    _pk, tot = S.block_replay(orders[0], "tpipe_trecomp")
+    assert Fraction(tot, 2 * p) == Fraction(p + 1, 2 * p)
+    sim = S.simulate(orders, p, v, dur, rec)
+    if p == 8:
+        assert sim["makespan"] == 133
+        r50 = S.simulate(*[S.strategy_orders("1f1b_r50", p, m)[i] for i in (0,)], p, 1,
+                         S.strategy_orders("1f1b_r50", p, m)[3])
+        assert r50["makespan"] == 7 * (m + p - 1) == 161

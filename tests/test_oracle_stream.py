@@ -12,7 +12,8 @@ def desc(L, dtype=T.BF16):
     return T.ModelDesc(L, 64, 4, 256, 256, 32, 2, dtype)
 
 
-@pytest.mark.parametrize("strategy", ["tpipe", "tpipe_trecomp", "1f1b", "1f1b_full_recomp"])
+@pytest.mark.parametrize("strategy", ["tpipe", "tpipe_trecomp", "1f1b", "1f1b_full_recomp",
+                                      "interleave", "interleave_trecomp"])
 @pytest.mark.parametrize("p", [1, 2, 4, 8])
 def test_stream_invariants(strategy, p):
     """Deadlock-free with W=2 (static acyclicity, D-14), channel FIFO
@@ -136,3 +137,26 @@ def test_partial_trecomp_endpoints(p):
             assert pk[0] < T.replay(tp[s], tst[s])["total_peak"]
     with pytest.raises(ValueError):
         T.build_streams(d, p, m, "tpipe_trecomp", recomp_layers=n1 + 1)
+
+
+@pytest.mark.parametrize("p", [4, 8])
+def test_interleave_bytes_match_blocks(p):
+    """Interleave-1F1B byte replay of a middle stage's activations equals the
+    block replay (P:210 pin m_a(1 + (p-1)/(pv)) lives there) times the
+    per-chunk stash + input bytes; with T-Recomp the chunk-2 blocks plus the
+    one recompute buffer match the (p+1)-block D-9 count."""
+    d = desc(2 * p)
+    m = 2 * p
+    z = T.sizes(d, p, 2, 1, 1)
+    st, static = T.build_streams(d, p, m, "interleave")
+    orders = S.interleave_orders(p, m, 2)
+    for s in range(1, p - 1):
+        r = T.replay(st[s], static[s])
+        _pk, tot = S.block_replay(orders[s], "interleave")
+        assert r["act"] == tot * (z["stash"] + z["act"])
+    st, static = T.build_streams(d, p, m, "interleave_trecomp")
+    orders = S.strategy_orders("interleave_trecomp", p, m)[0]
+    for s in range(1, p - 1):
+        r = T.replay(st[s], static[s])
+        pk, _tot = S.block_replay(orders[s], "tpipe_trecomp")
+        assert r["recomp_buf"] == pk["buf"] * z["stash"]

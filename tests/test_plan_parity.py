@@ -60,6 +60,9 @@ for strat in ("tpipe", "tpipe_trecomp", "1f1b", "1f1b_full_recomp"):
     for p in (1, 2, 3, 4, 8):
         for m in (1, 3, 8, 32):
             CASES.append((strat, p, m))
+for strat in ("interleave", "interleave_trecomp"):          # NEXT-2 (m % p == 0)
+    for p, m in ((1, 3), (2, 8), (3, 6), (4, 8), (4, 32), (8, 8), (8, 32)):
+        CASES.append((strat, p, m))
 
 
 @pytest.mark.parametrize("strategy,p,m", CASES)
@@ -139,12 +142,13 @@ def test_device_opt_offload_streams_match_oracle(p, dtype):
         P.Plan(pd, p, 16, strategy="tpipe_trecomp", offload=P.OFFLOAD_DEVICE_OPT)
 
 
-@pytest.mark.parametrize("strategy", ["tpipe", "tpipe_trecomp", "1f1b", "1f1b_full_recomp"])
+@pytest.mark.parametrize("strategy", ["tpipe", "tpipe_trecomp", "1f1b", "1f1b_full_recomp",
+                                      "interleave", "interleave_trecomp"])
 @pytest.mark.parametrize("p", [1, 2, 4, 5, 8, 16])
 def test_simulate_matches_oracle(strategy, p):
     """C++ unit-time replay == oracle simulator (makespan and busy time)."""
     P = _plan_mod()
-    m = 2 * p + 3
+    m = 2 * p + 3 if not strategy.startswith("interleave") else 3 * p
     plan = P.Plan(P.Model(2 * p if p > 1 else 2, 64, 4, 256, 128, 32, 2), p, m, strategy=strategy)
     orders, v, rec, dur = S.strategy_orders(strategy, p, m)
     sim = S.simulate(orders, p, v, dur, rec)
@@ -294,3 +298,15 @@ def test_auto_escalation_partial_trecomp():
     if off < pk[3]:
         auto = P.Plan(md, 8, 32, hbm_budget=off, strategy="auto")
         assert (auto.offload, auto.recomp_layers) == (P.OFFLOAD_MODEL_STATE, 1)
+
+
+def test_interleave_needs_m_multiple_of_p_and_simulates():
+    """Interleave-1F1B needs m % p == 0 (Megatron order); the C++ unit-time
+    replay of Interleave + T-Recomp reproduces D-9's 133 at p=8, m=16."""
+    P = _plan_mod()
+    from paper_2503_03182_b200._lib import TPipeError
+    md = P.Model(16, 64, 4, 256, 128, 32, 2)
+    with pytest.raises(TPipeError, match="interleave"):
+        P.Plan(md, 8, 12, strategy="interleave")
+    mk, _busy = P.Plan(md, 8, 16, strategy="interleave_trecomp").simulate()
+    assert mk == 133
