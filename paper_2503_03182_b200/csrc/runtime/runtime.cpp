@@ -358,6 +358,7 @@ int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags
             a.in = emb ? nullptr : live_get(S, TPIPE_BUF_IN, c, i);
             a.tokens = S.tokens ? S.tokens + (long)(i - 1) * D.M : nullptr;
             a.targets = head ? S.targets + (long)(i - 1) * D.M : nullptr;
+            a.loss_slot = (head && S.loss_slots) ? S.loss_slots + (i - 1) : nullptr;
             a.loss_scale = 1.0f / ((float)P.m * (float)D.M);
             void* stp = (trecomp && c == 1) ? live_get(S, TPIPE_BUF_RBUF, c, i)
                                             : live_get(S, TPIPE_BUF_STASH, c, i);

@@ -479,20 +479,16 @@ int chunk_forward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P,
         TRY(layer_forward(D, layer_w(D, P, l), lp, ws_ln, ws_g, out, st));
     }
     if (lay.head && a.targets) {
+        // LN_f forward only: its statistics are stashed for the backward. The
+        // logits, LSE, loss and dlogits are all produced in the head chunk's
+        // backward (the loss is read after the step), so the [M, V] LM-head
+        // GEMM runs once per micro-batch instead of once in F and again in B.
+        // (On the last stage B(p-1,c,i) directly follows F(p-1,c,i) in T-Pipe,
+        // B = F+1, and in 1F1B, so nothing is held longer.)
         uint8_t* lnf = scratch + SL.scratch_bytes;
-        float* logits = reinterpret_cast<float*>(lnf + M * h * D.es);
-        {
-            ProfScope _ps(3, 0.0, st);
-            TRY(ln_fwd(D.dtype, a.stash + SL.x_f, wb + lay.lnf_g * D.es, wb + lay.lnf_b * D.es, lnf,
+        ProfScope _ps(3, 0.0, st);
+        TRY(ln_fwd(D.dtype, a.stash + SL.x_f, wb + lay.lnf_g * D.es, wb + lay.lnf_b * D.es, lnf,
                    at<float>(a.stash, SL.lnf_mean), at<float>(a.stash, SL.lnf_rstd), M, h, st));
-        }
-        TRY(mm(D, M, D.V, h, lnf, h, 1, wb + lay.w_head * D.es, h, 1, EPI_STORE_F32, logits, D.V,
-               nullptr, nullptr, 0, nullptr, 0, nullptr, 0, st));
-        {
-            ProfScope _ps(3, 0.0, st);
-            TRY(ce_fwd(logits, a.targets, at<float>(a.stash, SL.ce_lse), a.loss_slot, a.loss_scale, M,
-                   D.V, st));
-        }
     }
     return 0;
 }
@@ -519,6 +515,9 @@ int chunk_backward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P
                0, nullptr, 0, nullptr, 0, st));
         {
             ProfScope _ps(3, 0.0, st);
+            // LSE and loss (the forward deferred them: see chunk_forward), then dlogits
+            TRY(ce_fwd(w.logits, a.targets, at<float>(a.stash, SL.ce_lse), a.loss_slot, a.loss_scale, M,
+                       D.V, st));
             TRY(ce_bwd(D.dtype, w.logits, a.targets, at<float>(a.stash, SL.ce_lse), w.dlogits,
                    a.loss_scale, M, D.V, st));
         }

@@ -61,7 +61,7 @@ struct FwdArgs {
     const void* in;          // chunk input (IN buffer) or nullptr for the embedding chunk
     const int* tokens;       // [M] (embedding chunk)
     const int* targets;      // [M] (head chunk)
-    float* loss_slot;        // head chunk: += scale * sum CE
+    float* loss_slot;        // unused: the head chunk's loss is computed in its backward
     float loss_scale;
     uint8_t* stash;          // STASH / TSTASH / RBUF
     uint8_t* ws;             // forward workspace (ws_f bytes)
@@ -77,6 +77,7 @@ struct BwdArgs {
     const void* in;          // chunk input (layer-0 x_in) or nullptr (embedding chunk)
     const int* tokens;
     const int* targets;
+    float* loss_slot;        // head chunk: += scale * sum CE (computed with the logits in B)
     float loss_scale;
     uint8_t* stash;
     uint8_t* stash2;         // partial T-Recomp: kept stash of layers [split, n)
