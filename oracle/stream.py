@@ -129,7 +129,7 @@ def sizes(d: ModelDesc, p: int, v: int, s: int, c: int, full_recomp: bool = Fals
     if full_recomp:
         ws_f += LS - M * h * es                  # one layer's transient internals
     if head:
-        ws_f += M * h * es + 4 * M * V + 4 * M
+        ws_f += M * h * es                       # LN_f output (logits and CE run in B)
     ws_b = M * (2 * f + 8 * h) * es + 4 * a * M + 4 * nb * max(f, 3 * h)
     if full_recomp:
         ws_b += LS - M * h * es                  # one-layer recompute buffer
