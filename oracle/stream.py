@@ -130,7 +130,7 @@ def sizes(d: ModelDesc, p: int, v: int, s: int, c: int, full_recomp: bool = Fals
         ws_f += LS - M * h * es                  # one layer's transient internals
     if head:
         ws_f += M * h * es                       # LN_f output (logits and CE run in B)
-    ws_b = M * (2 * f + 8 * h) * es + 4 * a * M + 4 * nb * max(f, 3 * h)
+    ws_b = M * (2 * f + 8 * h) * es + 4 * a * M + 4 * nb * max(f + 3 * h, 6 * h)
     if full_recomp:
         ws_b += LS - M * h * es                  # one-layer recompute buffer
     if head:

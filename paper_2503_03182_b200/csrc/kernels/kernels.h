@@ -94,6 +94,17 @@ int ce_bwd(int dtype, const float* logits, const int* tgt, const float* lse, voi
 // ---------------------------------------------------------------- reductions
 // out[n] += sum_r X[r, n] (deterministic; 16-row partials into ws fp32 [ceil(rows/16), n]).
 int colsum_acc(int dtype, const void* X, float* out, float* ws, int rows, int n, cudaStream_t st);
+// Deferred-reduce variants (bf16, wide rows; return -1 when the shape is not
+// supported and the caller should use ln_bwd / colsum_acc): write RB-row-block
+// partials only ([nb][n]; LN: [2 or 3][nb][h]); reduce_segments then adds up to
+// 4 partial sets (src[i] [nb][n[i]], n[i] % 4 == 0) into out[i] in one launch,
+// in the same fixed order as the immediate variants.
+int colsum_partials(int dtype, const void* X, float* ws, int rows, int n, cudaStream_t st);
+int ln_bwd_partials(int dtype, const void* dy, const void* x, const void* gamma, const float* mean,
+                    const float* rstd, const void* resid, void* dx, float* ws, int rows, int h, int with_rsum,
+                    cudaStream_t st);
+int reduce_segments(const float* const* src, float* const* out, const int* n, int nseg, int rows,
+                    cudaStream_t st);
 
 // ---------------------------------------------------------------- optimizer
 struct AdamHyper {

@@ -224,6 +224,61 @@ reduce_parts_kernel(const float* __restrict__ ws, float* __restrict__ out0, floa
     }
 }
 
+// Segmented variant: up to 4 (partials, output, width) segments in one launch
+// (blockIdx.y = segment); same per-column order as reduce_parts_kernel. Lets a
+// layer backward reduce its bias / LayerNorm-affine partials in 2 launches
+// instead of 4.
+struct ReduceSegs {
+    const float* src[4];
+    float* out[4];
+    int n[4];
+};
+__global__ void __launch_bounds__(256) reduce_segs_kernel(const ReduceSegs segs, int nblk) {
+    pdl_wait();
+    pdl_trigger();
+    __shared__ float4 red[32][8];
+    const int t = blockIdx.y;
+    const int n = segs.n[t];
+    if (blockIdx.x * 32 >= n) return;   // CTA-uniform
+    const float* src = segs.src[t];
+    float* out = segs.out[t];
+    const int cg = threadIdx.x & 7, g = threadIdx.x >> 3;
+    const int col = blockIdx.x * 32 + cg * 4;
+    float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (col < n) {
+#pragma unroll 4
+        for (int b = g; b < nblk; b += 32) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(src + (long)b * n + col));
+            sum.x += v.x;
+            sum.y += v.y;
+            sum.z += v.z;
+            sum.w += v.w;
+        }
+    }
+    red[g][cg] = sum;
+    __syncthreads();
+    for (int stride = 16; stride > 0; stride >>= 1) {
+        if (g < stride) {
+            const float4 o = red[g + stride][cg];
+            red[g][cg].x += o.x;
+            red[g][cg].y += o.y;
+            red[g][cg].z += o.z;
+            red[g][cg].w += o.w;
+        }
+        __syncthreads();
+    }
+    if (g == 0 && col < n) {
+        float4* po = reinterpret_cast<float4*>(out + col);
+        float4 a = *po;
+        const float4 r = red[0][cg];
+        a.x += r.x;
+        a.y += r.y;
+        a.z += r.z;
+        a.w += r.w;
+        *po = a;
+    }
+}
+
 // ---------------------------------------------------------------- warp-per-row forward
 // bf16, h = 256*NV: one warp per row, the whole row register-resident (NV
 // 16-byte vectors per lane, all loads issued before any use), warp-shuffle
@@ -641,6 +696,59 @@ int colsum_acc(int dtype, const void* X, float* out, float* ws, int rows, int n,
         colsum_partial_kernel<float><<<pg, 256, 0, st>>>((const float*)X, ws, rows, n);
     reduce_blocks_kernel<<<(n + 255) / 256, 256, 0, st>>>(ws, out, n, nblk);
     note_launches(2);
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+// ---------------------------------------------------------------- deferred reductions
+// bf16 wide path only (return -1 otherwise: the caller uses ln_bwd / colsum_acc):
+// write the RB-row-block partials, leave the reduce to reduce_segments.
+int colsum_partials(int dtype, const void* X, float* ws, int rows, int n, cudaStream_t st) {
+    if (rows <= 0 || n <= 0) return 0;
+    if (!(dtype == DT_BF16 && n % 8 == 0)) return -1;
+    const int nb = (rows + RB - 1) / RB;
+    launch_k(colsum_wide_kernel, dim3((n + CS_COLS - 1) / CS_COLS, nb), dim3(256), 0, st, 1, (const bf16*)X, ws,
+             rows, n);
+    note_launches(1);
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+int ln_bwd_partials(int dtype, const void* dy, const void* x, const void* gamma, const float* mean,
+                    const float* rstd, const void* resid, void* dx, float* ws, int rows, int h, int with_rsum,
+                    cudaStream_t st) {
+    if (rows <= 0) return 0;
+    if (!wide_ok(dtype, h) || (with_rsum && !resid)) return -1;
+    const int nb = (rows + RB - 1) / RB;
+    const int G = wide_groups(h);
+    int RC = LNB_SMEM_ROWS_BYTES / (3 * h * 2);
+    if (RC > RB) RC = RB;
+    const size_t smem = (size_t)RC * 3 * h * 2;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(ln_bwd_stage_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, LNB_SMEM_ROWS_BYTES);
+        attr = true;
+    }
+    launch_k(ln_bwd_stage_kernel, dim3(nb), dim3(G * (h / 8)), smem, st, 1, (const bf16*)dy, (const bf16*)x,
+             (const bf16*)gamma, (const float*)mean, (const float*)rstd, (const bf16*)resid, (bf16*)dx, ws, rows,
+             h, nb, with_rsum ? 1 : 0, RC);
+    note_launches(1);
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+int reduce_segments(const float* const* src, float* const* out, const int* n, int nseg, int rows,
+                    cudaStream_t st) {
+    if (nseg <= 0 || nseg > 4 || rows <= 0) return nseg == 0 ? 0 : -1;
+    ReduceSegs sg{};
+    int maxn = 0;
+    for (int i = 0; i < nseg; ++i) {
+        if (n[i] % 4) return -1;
+        sg.src[i] = src[i];
+        sg.out[i] = out[i];
+        sg.n[i] = n[i];
+        maxn = n[i] > maxn ? n[i] : maxn;
+    }
+    const int nb = (rows + RB - 1) / RB;
+    launch_k(reduce_segs_kernel, dim3((maxn + 31) / 32, nseg), dim3(256), 0, st, 1, sg, nb);
+    note_launches(1);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 

@@ -84,7 +84,7 @@ static ChunkSizes chunk_sizes(const tpipe_model_desc& d, int p, int v, const int
     uint64_t ws_f = M * (h + f) * es;
     if (full_recomp) ws_f += LS - M * h * es;  // one layer's transient internals
     if (head) ws_f += M * h * es;   // LN_f output only: logits / CE run in the head backward
-    uint64_t ws_b = M * (2 * f + 8 * h) * es + 4 * a * M + 4 * nb * std::max(f, 3 * h);
+    uint64_t ws_b = M * (2 * f + 8 * h) * es + 4 * a * M + 4 * nb * std::max(f + 3 * h, 6 * h);
     if (full_recomp) ws_b += LS - M * h * es;
     if (head) ws_b += 2 * M * h * es + 4 * M * V + M * V * es;
     if (emb) ws_b += 8 * M;

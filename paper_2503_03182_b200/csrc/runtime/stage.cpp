@@ -398,18 +398,35 @@ static int layer_backward(const Dims& D, const LW& W, const LayerPtrs& lp, const
     }
     TRY(mm(D, f, h, M, w.du, f, 0, w.ln, h, 0, EPI_ACC_F32, W.g[W_1], h, nullptr, nullptr, 0,
            nullptr, 0, nullptr, 0, ax));
-    // ---- main: data-gradient chain
+    // ---- main: data-gradient chain. bf16: the b1 column partials and LN2's
+    // (gamma, beta, b2) partials sit side by side in w.part and are reduced by
+    // one launch after the LN2 backward (same per-column order)
+    const long nb16 = (M + 15) / 16;
+    float* part_b = w.part + nb16 * f;
+    bool deferred = false;
     {
         ProfScope _ps(3, 0.0, st);
-        TRY(colsum_acc(dt, w.du, W.g[B_1], w.part, M, f, st));
+        const int rc = colsum_partials(dt, w.du, w.part, M, f, st);
+        if (rc > 0 || rc < -1) return rc;
+        deferred = rc == 0;
+        if (!deferred) TRY(colsum_acc(dt, w.du, W.g[B_1], w.part, M, f, st));
     }
     TRY(mm(D, M, h, f, w.du, f, 1, W.w[W_1], h, 0, EPI_STORE, w.dln, h, nullptr, nullptr, 0,
            nullptr, 0, nullptr, 0, st));
     {
         ProfScope _ps(3, 0.0, st);
         // + dB2 = colsum(dy), fused (dy is LN2's residual-branch gradient)
-        TRY(ln_bwd(dt, w.dln, lp.x_mid, W.w[LN2_G], lp.ln2_mean, lp.ln2_rstd, dy, w.G1, W.g[LN2_G],
-                   W.g[LN2_B], w.part, M, h, st, W.g[B_2]));
+        if (deferred && ln_bwd_partials(dt, w.dln, lp.x_mid, W.w[LN2_G], lp.ln2_mean, lp.ln2_rstd, dy, w.G1,
+                                        part_b, M, h, 1, st) == 0) {
+            const float* src[4] = {w.part, part_b, part_b + nb16 * h, part_b + 2 * nb16 * h};
+            float* out[4] = {W.g[B_1], W.g[LN2_G], W.g[LN2_B], W.g[B_2]};
+            const int n[4] = {f, h, h, h};
+            TRY(reduce_segments(src, out, n, 4, M, st));
+        } else {
+            if (deferred) TRY(reduce_segments((const float* const*)&w.part, &W.g[B_1], &f, 1, M, st));
+            TRY(ln_bwd(dt, w.dln, lp.x_mid, W.w[LN2_G], lp.ln2_mean, lp.ln2_rstd, dy, w.G1, W.g[LN2_G],
+                       W.g[LN2_B], w.part, M, h, st, W.g[B_2]));
+        }
     }
     // aux (in order after FC1 wgrad, so w.ln is free): LN1 recompute; then,
     // once G1 exists, the out-proj weight gradient
@@ -432,10 +449,15 @@ static int layer_backward(const Dims& D, const LW& W, const LayerPtrs& lp, const
     // aux: QKV weight gradient
     TRY(mm(D, 3 * h, h, M, w.dqkv, 3 * h, 0, w.ln, h, 0, EPI_ACC_F32, W.g[W_QKV], h, nullptr,
            nullptr, 0, nullptr, 0, nullptr, 0, ax));
-    // main: QKV bias / dgrad, LN1 backward
+    // main: QKV bias / dgrad, LN1 backward (bqkv and LN1's (gamma, beta, bo)
+    // partials reduced together, as above)
+    float* part_q = w.part + nb16 * 3 * h;
     {
         ProfScope _ps(3, 0.0, st);
-        TRY(colsum_acc(dt, w.dqkv, W.g[B_QKV], w.part, M, 3 * h, st));
+        const int rc = colsum_partials(dt, w.dqkv, w.part, M, 3 * h, st);
+        if (rc > 0 || rc < -1) return rc;
+        deferred = rc == 0;
+        if (!deferred) TRY(colsum_acc(dt, w.dqkv, W.g[B_QKV], w.part, M, 3 * h, st));
     }
     TRY(mm(D, M, h, 3 * h, w.dqkv, 3 * h, 1, W.w[W_QKV], h, 0, EPI_STORE, w.dln, h, nullptr,
            nullptr, 0, nullptr, 0, nullptr, 0, st));
@@ -443,8 +465,20 @@ static int layer_backward(const Dims& D, const LW& W, const LayerPtrs& lp, const
     {
         ProfScope _ps(3, 0.0, st);
         // + dBo = colsum(G1), fused (G1 is LN1's residual-branch gradient)
-        TRY(ln_bwd(dt, w.dln, lp.x_in, W.w[LN1_G], lp.ln1_mean, lp.ln1_rstd, w.G1, dx, W.g[LN1_G],
-                   W.g[LN1_B], w.part, M, h, st, W.g[B_O]));
+        if (deferred && ln_bwd_partials(dt, w.dln, lp.x_in, W.w[LN1_G], lp.ln1_mean, lp.ln1_rstd, w.G1, dx,
+                                        part_q, M, h, 1, st) == 0) {
+            const float* src[4] = {w.part, part_q, part_q + nb16 * h, part_q + 2 * nb16 * h};
+            float* out[4] = {W.g[B_QKV], W.g[LN1_G], W.g[LN1_B], W.g[B_O]};
+            const int n[4] = {3 * h, h, h, h};
+            TRY(reduce_segments(src, out, n, 4, M, st));
+        } else {
+            if (deferred) {
+                const int n3 = 3 * h;
+                TRY(reduce_segments((const float* const*)&w.part, &W.g[B_QKV], &n3, 1, M, st));
+            }
+            TRY(ln_bwd(dt, w.dln, lp.x_in, W.w[LN1_G], lp.ln1_mean, lp.ln1_rstd, w.G1, dx, W.g[LN1_G],
+                       W.g[LN1_B], w.part, M, h, st, W.g[B_O]));
+        }
     }
     // join: the layer's gradients are complete and w.* free for the next layer
     if (ss) TRY(stream_dep(ax, st, ev[4]));
@@ -498,7 +532,8 @@ int chunk_backward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P
     const ParamLayout& lay = *P.lay;
     const int n = (int)lay.layer.size();
     const long M = D.M, h = D.h;
-    const long part = ((M + 15) / 16) * (D.f > 3 * h ? D.f : 3 * h);
+    // column-partial workspace: b1 [nb][f] + LN2 [3][nb][h], or bqkv [nb][3h] + LN1 [3][nb][h]
+    const long part = ((M + 15) / 16) * (D.f + 3 * h > 6 * h ? D.f + 3 * h : 6 * h);
     BwdWs w = carve_bwd(D, a.ws, lay.head, lay.emb, part, SL.ckpt_only ? SL.scratch_bytes : 0);
     const uint8_t* wb = reinterpret_cast<const uint8_t*>(P.w);
     const void* dy = a.gin;
