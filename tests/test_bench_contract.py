@@ -1,0 +1,35 @@
+"""CPU checks of bench.py's contract: the reference arm (the fp64 oracle,
+DESIGN.md §10) prints one JSON line with the driver's keys, and the planner's
+capacity sweep (SURVEY D-13) gives T-Pipe-ALL >= 2x the 1F1B model size at a
+fixed 80 GiB per-GPU budget (the north star's size target, byte model)."""
+
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_reference_arm_json_line():
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                          "--steps", "1", "--warmup", "3"], capture_output=True, text=True,
+                         timeout=600, cwd=ROOT, check=True).stdout.strip().splitlines()
+    assert len(out) == 1
+    d = json.loads(out[0])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "dtype", "config", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "tokens/s"
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_capacity_sweep_size_target():
+    sys.path.insert(0, ROOT)
+    import bench
+    cap = bench.capacity(8)
+    assert cap["tpipe_all"]["max_params_B"] >= 2 * cap["1f1b"]["max_params_B"]
+    assert cap["tpipe_trecomp"]["max_layers"] > cap["tpipe"]["max_layers"] >= cap["1f1b"]["max_layers"]
+    # plain Interleave-1F1B stores more than 1F1B; with T-Recomp it stores less
+    assert cap["interleave"]["max_layers"] < cap["1f1b"]["max_layers"] < cap["interleave_trecomp"]["max_layers"]
