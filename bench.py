@@ -411,6 +411,62 @@ def hbm_kernels(c, hbm_peak):
     return out
 
 
+def pipeline_replay(ps=(8,), strategies=("1f1b", "tpipe", "tpipe_trecomp", "1f1b_full_recomp"), m=None):
+    """Measured-duration replay of the p-stage pipeline (SURVEY §8(d) bubble
+    fraction, D-12 stage balance): all p stages of the C2 model run on this
+    GPU as a virtual pipeline with TPIPE_STEP_OP_TIMES, so every F / B / R op
+    is timed on its own (CUDA events on the stage stream); the planner's
+    ASAP replay (tpipe_plan_simulate_durations) then schedules those measured
+    durations on p GPUs. Stage transport (one [b*s, h] bf16 message per hop,
+    8 MiB here, ~10 us over NVLink 5) is not modelled. Returns, per p and
+    strategy: predicted ms/step, tokens/s on p GPUs, MFU, per-stage bubble
+    fraction and the ratio to 1F1B."""
+    import torch
+    from paper_2503_03182_b200 import plan as P, runtime as RT
+    import synth
+    c = C2
+    m = m or c["m"]
+    pool = (np.random.default_rng(5).standard_normal(1 << 22, dtype=np.float32) * np.float32(0.02))
+    tok, tgt = synth.tokens(c["vocab"], m, c["micro_batch"], c["seq_len"], step=0, vocab_eff=c["vocab_eff"])
+    dtok = torch.tensor(tok, dtype=torch.int32, device="cuda")
+    dtgt = torch.tensor(tgt, dtype=torch.int32, device="cuda")
+    tokens = m * c["micro_batch"] * c["seq_len"]
+    _, _, pk_sust, _src = peaks()
+    out = {}
+    for p in ps:
+        res = {}
+        for st in strategies:
+            md = P.Model(c["n_layers"], c["hidden"], c["n_heads"], c["ffn_hidden"], c["vocab"],
+                         c["seq_len"], c["micro_batch"], P.BF16)
+            try:
+                plan = P.Plan(md, p, m, strategy=st)
+            except Exception as e:   # e.g. an invalid chunk split
+                res[st] = {"error": str(e)[:120]}
+                continue
+            rt = RT.Runtime(plan, stage=-1, lr=1e-5)
+            for s in range(p):
+                for ch in range(1, plan.v + 1):
+                    rt.set_params(s, ch, fast_init_chunk(plan, s, ch, pool))
+            rt.step_device(dtok.data_ptr(), dtgt.data_ptr())
+            rt.step_device(dtok.data_ptr(), dtgt.data_ptr(), RT.STEP_OP_TIMES)
+            op_ms = [rt.op_times(s) for s in range(p)]
+            rt.close()
+            mk, busy = plan.simulate_durations(op_ms)
+            tps = tokens / (mk / 1e3)
+            res[st] = {"layers_chunk": list(plan.layers_chunk), "ms_per_step": round(mk, 2),
+                       "tokens_s": round(tps, 1),
+                       "mfu": round(tps * model_flops_per_token(c) / (p * pk_sust * 1e12), 4),
+                       "bubble_fraction": [round(1.0 - b / mk, 4) for b in busy[:p]],
+                       "compute_ms_per_stage": [round(b, 2) for b in busy[:p]]}
+        base = res.get("1f1b", {}).get("tokens_s")
+        if base:
+            for st, r in res.items():
+                if "tokens_s" in r:
+                    r["vs_1f1b"] = round(r["tokens_s"] / base, 3)
+        out[f"p{p}"] = res
+    return out
+
+
 def gemm_traffic():
     """Per-launch DRAM traffic of the tcgen05 GEMM class from the committed
     `ncu --set full` capture of the 12 layer GEMM shapes (scripts/
@@ -710,6 +766,14 @@ def run_tpipe(args):
             except Exception as e:   # reported, not fatal
                 comp[key] = {"error": str(e)[:200]}
         out["host_link_peak"] = host_link_peak()
+        try:
+            out["pipeline_replay"] = {
+                "how": "C2 on one GPU as a p-stage virtual pipeline, every F/B/R op timed with CUDA events "
+                       "(TPIPE_STEP_OP_TIMES), measured durations replayed ASAP on p GPUs by "
+                       "tpipe_plan_simulate_durations; stage transport not modelled (prediction, not a "
+                       "multi-GPU measurement)", **pipeline_replay((8,))}
+        except Exception as e:   # reported, not fatal
+            out["pipeline_replay"] = {"error": str(e)[:200]}
         out["hbm_kernels"] = {"peak_GBs": hbm, "peak_src": f"hbm_gbs ({src})",
                               "shape": f"M={c['seq_len'] * c['micro_batch']} rows, h={c['hidden']}, "
                                        f"f={c['ffn_hidden']}; adamw 64M params",
@@ -781,11 +845,20 @@ def main():
     ap.add_argument("--impl", default="tpipe", choices=["tpipe", "reference"])
     ap.add_argument("--strategy", default="tpipe", choices=["tpipe", "tpipe_trecomp", "1f1b"])
     ap.add_argument("--no-extras", action="store_true", help="skip capacity sweep and CPU oracle")
+    ap.add_argument("--pipeline-replay", action="store_true",
+                    help="measured-op-duration replay of p = 2, 4, 8 stage pipelines (C2)")
     ap.add_argument("--capacity-run", action="store_true",
                     help="executed capacity at a fixed per-stage HBM budget (p=8 virtual pipeline, one GPU)")
     args = ap.parse_args()
     if args.capacity_run:
         print(json.dumps(run_capacity(args)), flush=True)
+        return
+    if args.pipeline_replay:
+        print(json.dumps({"pipeline_replay": pipeline_replay((2, 4, 8), ("1f1b", "tpipe", "tpipe_trecomp",
+                                                                        "1f1b_full_recomp",
+                                                                        "interleave",
+                                                                        "interleave_trecomp"))}),
+              flush=True)
         return
     if args.warmup < 3:
         args.warmup = 3

@@ -185,6 +185,16 @@ int tpipe_plan_stage_peak(const tpipe_plan* plan, int32_t stage, tpipe_mem_repor
 int tpipe_plan_channel(const tpipe_plan* plan, int32_t c, int32_t* kind, int32_t* src, int32_t* dst);
 /* unit-time ASAP replay of the compute order (mirror of the oracle simulator) */
 int tpipe_plan_simulate(const tpipe_plan* plan, tpipe_sim_report* out);
+/* The same ASAP replay with given durations: op_ms[s][j] = duration of the
+ * j-th compute op (F / B / R, plan order) of stage s, e.g. measured with
+ * TPIPE_STEP_OP_TIMES (caller-owned arrays of the stage's compute-op count).
+ * Transport time is not modelled. makespan_ms, busy_ms[s] out. */
+typedef struct {
+    double makespan_ms;
+    double busy_ms[64];
+} tpipe_sim_report_ms;
+int tpipe_plan_simulate_durations(const tpipe_plan* plan, const float* const* op_ms,
+                                  tpipe_sim_report_ms* out);
 /* parameters of (stage, chunk) in the packed order of DESIGN.md §2.3 */
 int tpipe_plan_chunk_params(const tpipe_plan* plan, int32_t stage, int32_t chunk, uint64_t* n);
 
@@ -222,6 +232,8 @@ typedef struct tpipe_runtime tpipe_runtime;
 
 #define TPIPE_STEP_NO_OPT 1u        /* skip optimizer ops: gradients stay accumulated */
 #define TPIPE_STEP_PROFILE 2u       /* bracket GEMM / attention launches with CUDA events */
+#define TPIPE_STEP_OP_TIMES 4u      /* record each compute op's (F / B / R) duration with CUDA
+                                       events on the stage stream (tpipe_runtime_op_times) */
 
 int tpipe_runtime_create(const tpipe_plan* plan, const tpipe_runtime_opts* opts,
                          tpipe_runtime** out);
@@ -242,6 +254,14 @@ int tpipe_step(tpipe_runtime* rt, const int32_t* tokens, const int32_t* targets,
 int tpipe_step_device(tpipe_runtime* rt, const int32_t* tokens_dev, const int32_t* targets_dev,
                       uint32_t flags, float* loss_out);
 int tpipe_runtime_get_stats(const tpipe_runtime* rt, tpipe_runtime_stats* out);
+
+/* Durations (ms) of stage `stage`'s compute ops (F, B, R only, in the plan's
+ * order) from the last tpipe_step run with TPIPE_STEP_OP_TIMES; *n = count
+ * (0 if the last step did not record), at most `cap` written to `ms`
+ * (caller-owned, may be NULL to query n). In the virtual pipeline (stage -1)
+ * the ops of all stages run one after another on one GPU, so each duration is
+ * the op's own GPU time. */
+int tpipe_runtime_op_times(const tpipe_runtime* rt, int32_t stage, float* ms, size_t cap, size_t* n);
 /* CUDA stream the runtime launches compute on (cudaStream_t), for event timing */
 void* tpipe_runtime_stream(const tpipe_runtime* rt);
 

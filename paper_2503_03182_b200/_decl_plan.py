@@ -44,6 +44,10 @@ class SimReport(C.Structure):
     _fields_ = [("makespan", i64), ("busy", i64 * 64)]
 
 
+class SimReportMs(C.Structure):
+    _fields_ = [("makespan_ms", C.c_double), ("busy_ms", C.c_double * 64)]
+
+
 class RuntimeOpts(C.Structure):
     _fields_ = [("stage", i32), ("device", i32), ("nccl_ids", vp), ("pool_cap", u64),
                 ("lr", f32), ("beta1", f32), ("beta2", f32), ("eps", f32), ("weight_decay", f32)]
@@ -70,6 +74,7 @@ def declare(L):
     L.tpipe_plan_stage_peak.argtypes = [vp, i32, P(MemReport)]
     L.tpipe_plan_channel.argtypes = [vp, i32, P(i32), P(i32), P(i32)]
     L.tpipe_plan_simulate.argtypes = [vp, P(SimReport)]
+    L.tpipe_plan_simulate_durations.argtypes = [vp, P(P(f32)), P(SimReportMs)]
     L.tpipe_plan_chunk_params.argtypes = [vp, i32, i32, P(u64)]
     L.tpipe_version.argtypes = []
     if hasattr(L, "tpipe_runtime_create"):
@@ -81,6 +86,7 @@ def declare(L):
         L.tpipe_step.argtypes = [vp, vp, vp, u32, P(f32)]
         L.tpipe_step_device.argtypes = [vp, vp, vp, u32, P(f32)]
         L.tpipe_runtime_get_stats.argtypes = [vp, P(RuntimeStats)]
+        L.tpipe_runtime_op_times.argtypes = [vp, i32, P(f32), C.c_size_t, P(C.c_size_t)]
         L.tpipe_runtime_stream.argtypes = [vp]
         L.tpipe_runtime_stream.restype = vp
         L.tpipe_nccl_unique_id.argtypes = [vp]

@@ -791,19 +791,15 @@ TP_API int tpipe_plan_chunk_params(const tpipe_plan* P, int32_t s, int32_t c, ui
     return 0;
 }
 
-// unit-time ASAP replay of the compute order (F=1,B=2,R=1 at v=2; F=2,B=4(+2) at v=1)
-TP_API int tpipe_plan_simulate(const tpipe_plan* P, tpipe_sim_report* out) {
-    if (!P || !out) return set_error(TPIPE_E_INVALID, "NULL argument");
+// ASAP replay of the compute order with per-op durations dur(s, j) (j = index
+// of the op in stage s's compute order); returns makespan and busy per stage
+template <typename T, typename DurFn>
+static int replay_order(const tpipe_plan* P, DurFn dur, T* makespan, T* busy_out) {
     const int p = P->p, v = P->v;
     const bool rec = P->strategy == TPIPE_S_TPIPE_TRECOMP || P->strategy == TPIPE_S_INTERLEAVE_TRECOMP;
-    auto dur = [&](int kind) -> long {
-        if (v == 2) return kind == KB ? 2 : 1;
-        if (kind == KF) return 2;
-        return P->strategy == TPIPE_S_1F1B_FULL_RECOMP ? 6 : 4;
-    };
-    std::map<std::tuple<int, int, int, int>, long> endt;  // (stage, kind, chunk, mb)
+    std::map<std::tuple<int, int, int, int>, T> endt;  // (stage, kind, chunk, mb)
     std::vector<size_t> pos(p, 0);
-    std::vector<long> freet(p, 0), busy(p, 0);
+    std::vector<T> freet(p, 0), busy(p, 0);
     size_t total = 0, done = 0;
     for (auto& o : P->order) total += o.size();
     while (done < total) {
@@ -824,7 +820,7 @@ TP_API int tpipe_plan_simulate(const tpipe_plan* P, tpipe_sim_report* out) {
                     if (s < p - 1) deps.push_back({s + 1, KB, c, i});
                     else if (c < v) deps.push_back({0, KB, c + 1, i});
                 }
-                long t0 = freet[s];
+                T t0 = freet[s];
                 bool ready = true;
                 for (auto& dd : deps) {
                     auto it = endt.find(dd);
@@ -832,7 +828,7 @@ TP_API int tpipe_plan_simulate(const tpipe_plan* P, tpipe_sim_report* out) {
                     t0 = std::max(t0, it->second);
                 }
                 if (!ready) break;
-                const long t1 = t0 + dur(kind);
+                const T t1 = t0 + dur(s, (int)pos[s], kind);
                 endt[{s, kind, c, i}] = t1;
                 freet[s] = t1;
                 busy[s] += t1 - t0;
@@ -843,10 +839,34 @@ TP_API int tpipe_plan_simulate(const tpipe_plan* P, tpipe_sim_report* out) {
         }
         if (!prog) return set_error(TPIPE_E_DEADLOCK, "compute order deadlocks");
     }
-    out->makespan = 0;
-    for (int s = 0; s < p; ++s) out->makespan = std::max<int64_t>(out->makespan, freet[s]);
-    for (int s = 0; s < 64; ++s) out->busy[s] = s < p ? busy[s] : 0;
+    *makespan = 0;
+    for (int s = 0; s < p; ++s) *makespan = std::max(*makespan, freet[s]);
+    for (int s = 0; s < 64; ++s) busy_out[s] = s < p ? busy[s] : 0;
     return 0;
+}
+
+// unit-time ASAP replay of the compute order (F=1,B=2,R=1 at v=2; F=2,B=4(+2) at v=1)
+TP_API int tpipe_plan_simulate(const tpipe_plan* P, tpipe_sim_report* out) {
+    if (!P || !out) return set_error(TPIPE_E_INVALID, "NULL argument");
+    const int v = P->v;
+    auto dur = [&](int, int, int kind) -> int64_t {
+        if (v == 2) return kind == KB ? 2 : 1;
+        if (kind == KF) return 2;
+        return P->strategy == TPIPE_S_1F1B_FULL_RECOMP ? 6 : 4;
+    };
+    int64_t mk = 0;
+    int rc = replay_order<int64_t>(P, dur, &mk, out->busy);
+    out->makespan = mk;
+    return rc;
+}
+
+TP_API int tpipe_plan_simulate_durations(const tpipe_plan* P, const float* const* op_ms,
+                                         tpipe_sim_report_ms* out) {
+    if (!P || !out || !op_ms) return set_error(TPIPE_E_INVALID, "NULL argument");
+    for (int s = 0; s < P->p; ++s)
+        if (!op_ms[s]) return set_error(TPIPE_E_INVALID, "op_ms[%d] is NULL", s);
+    auto dur = [&](int s, int j, int) -> double { return (double)op_ms[s][j]; };
+    return replay_order<double>(P, dur, &out->makespan_ms, out->busy_ms);
 }
 
 TP_API int tpipe_version(void) { return 1; }

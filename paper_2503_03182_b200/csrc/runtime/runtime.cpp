@@ -129,6 +129,10 @@ struct tpipe_runtime {
     size_t evnext = 0;
     double kms[4] = {0, 0, 0, 0}, kflops[4] = {0, 0, 0, 0};
     int64_t kcount[4] = {0, 0, 0, 0};
+    // TPIPE_STEP_OP_TIMES: per stage, (start, end) events of each compute op
+    // (F / B / R, plan order) of the last step, and their durations (ms)
+    std::vector<std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> op_ev;
+    std::vector<std::vector<float>> op_ms;
 
     explicit tpipe_runtime(const tpipe_plan& p) : plan(p), D(p.model) {}
 };
@@ -575,13 +579,28 @@ int run_step(tpipe_runtime* rt, const int32_t* tok_dev, const int32_t* tgt_dev, 
     }
     size_t remaining = 0;
     for (int s : rt->owned) remaining += P.ops[s].size();
+    const bool op_times = (flags & TPIPE_STEP_OP_TIMES) != 0;
+    rt->op_ev.assign(P.p, {});
+    rt->op_ms.assign(P.p, {});
     while (remaining) {
         bool prog = false;
         for (int s : rt->owned) {
             StageState& S = *rt->st[s];
             const auto& ops = P.ops[s];
             while (S.pc < ops.size() && op_ready(rt, ops[S.pc])) {
+                const int k = ops[S.pc].kind;
+                const bool timed = op_times && (k == TPIPE_OP_F || k == TPIPE_OP_B || k == TPIPE_OP_R);
+                cudaEvent_t ea = nullptr, eb = nullptr;
+                if (timed) {
+                    ea = next_timed_event(rt);
+                    eb = next_timed_event(rt);
+                    CU(cudaEventRecord(ea, cs));
+                }
                 TRY(exec_op(rt, S, ops[S.pc], flags));
+                if (timed) {
+                    CU(cudaEventRecord(eb, cs));   // the layer side stream joins cs inside the op
+                    rt->op_ev[s].push_back({ea, eb});
+                }
                 S.pc++;
                 remaining--;
                 prog = true;
@@ -603,6 +622,14 @@ int run_step(tpipe_runtime* rt, const int32_t* tok_dev, const int32_t* tgt_dev, 
     if (flags & TPIPE_STEP_PROFILE) {
         profiler().collect(rt->kms, rt->kflops, rt->kcount);
         profiler().on = false;
+    }
+    if (op_times) {
+        for (int s : rt->owned)
+            for (auto& pr : rt->op_ev[s]) {
+                float ms = 0.f;
+                CU(cudaEventElapsedTime(&ms, pr.first, pr.second));
+                rt->op_ms[s].push_back(ms);
+            }
     }
     if (!(flags & TPIPE_STEP_NO_OPT)) rt->t += 1;
     rt->launches_last = launch_count() - l0;
@@ -913,6 +940,15 @@ TP_API int tpipe_runtime_get_stats(const tpipe_runtime* rt, tpipe_runtime_stats*
 }
 
 TP_API void* tpipe_runtime_stream(const tpipe_runtime* rt) { return rt ? (void*)rt->stream : nullptr; }
+
+TP_API int tpipe_runtime_op_times(const tpipe_runtime* rt, int32_t stage, float* ms, size_t cap, size_t* n) {
+    if (!rt || !n || stage < 0 || stage >= rt->plan.p) return set_error(TPIPE_E_INVALID, "stage");
+    const auto& v = rt->op_ms.size() > (size_t)stage ? rt->op_ms[stage] : std::vector<float>();
+    *n = v.size();
+    if (ms)
+        for (size_t i = 0; i < v.size() && i < cap; ++i) ms[i] = v[i];
+    return 0;
+}
 
 TP_API void tpipe_set_side_stream(int on) { stage_set_side_stream(on); }
 TP_API void tpipe_set_pdl(int on) { tpipe::set_pdl(on); }

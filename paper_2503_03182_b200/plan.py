@@ -117,6 +117,23 @@ class Plan:
         check(lib().tpipe_plan_simulate(self._h, C.byref(r)))
         return r.makespan, [r.busy[i] for i in range(min(self.p, 64))]
 
+    def n_compute_ops(self, stage):
+        return sum(o["kind"] in ("F", "B", "R") for o in self.ops(stage)[0])
+
+    def simulate_durations(self, op_ms):
+        """ASAP replay with per-op durations: op_ms[s] = durations (ms) of stage
+        s's compute ops (F/B/R, plan order). Returns (makespan_ms, busy_ms)."""
+        arrs = []
+        for s in range(self.p):
+            a = (C.c_float * len(op_ms[s]))(*[float(x) for x in op_ms[s]])
+            if len(op_ms[s]) != self.n_compute_ops(s):
+                raise ValueError(f"stage {s}: {len(op_ms[s])} durations for {self.n_compute_ops(s)} ops")
+            arrs.append(a)
+        ptrs = (C.POINTER(C.c_float) * self.p)(*[C.cast(a, C.POINTER(C.c_float)) for a in arrs])
+        r = D.SimReportMs()
+        check(lib().tpipe_plan_simulate_durations(self._h, ptrs, C.byref(r)))
+        return r.makespan_ms, [r.busy_ms[i] for i in range(min(self.p, 64))]
+
     def chunk_params(self, stage, chunk):
         n = C.c_uint64()
         check(lib().tpipe_plan_chunk_params(self._h, stage, chunk, C.byref(n)))

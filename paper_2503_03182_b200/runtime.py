@@ -12,6 +12,7 @@ from ._lib import check, lib
 
 STEP_NO_OPT = 1
 STEP_PROFILE = 2
+STEP_OP_TIMES = 4
 
 
 class Runtime:
@@ -79,6 +80,14 @@ class Runtime:
                     kernel_ms=list(s.kernel_ms), kernel_flops=list(s.kernel_flops),
                     kernel_count=list(s.kernel_count), offload_d2h_ms=s.offload_d2h_ms,
                     offload_h2d_ms=s.offload_h2d_ms)
+
+    def op_times(self, stage):
+        """Per compute op (F/B/R, plan order) GPU ms of the last STEP_OP_TIMES step."""
+        n = C.c_size_t()
+        check(lib().tpipe_runtime_op_times(self._h, stage, None, 0, C.byref(n)))
+        a = (C.c_float * max(1, n.value))()
+        check(lib().tpipe_runtime_op_times(self._h, stage, a, n.value, C.byref(n)))
+        return [a[i] for i in range(n.value)]
 
     def stream(self) -> int:
         return lib().tpipe_runtime_stream(self._h) or 0

@@ -300,3 +300,23 @@ def test_activation_offload_bitexact(dtype, p):
     assert out[0][0] == out[1][0]
     for a, b in zip(out[0][1], out[1][1]):
         assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def test_op_times_and_replay():
+    """TPIPE_STEP_OP_TIMES records one positive duration per compute op of
+    every stage; the measured-duration replay's busy time per stage equals the
+    sum of that stage's op times and the makespan bounds it."""
+    _P, RT, _PR = mods()
+    p, m = 4, 8
+    plan, rt, _W = build(C1, p, m, "tpipe_trecomp", 1)
+    tok, tgt = synth.tokens(C1["vocab"], m, C1["micro_batch"], C1["seq_len"], step=0)
+    rt.step(tok, tgt, RT.STEP_NO_OPT | RT.STEP_OP_TIMES)
+    ms = [rt.op_times(s) for s in range(p)]
+    for s in range(p):
+        assert len(ms[s]) == plan.n_compute_ops(s) == 5 * m
+        assert all(x > 0 for x in ms[s])
+    mk, busy = plan.simulate_durations(ms)
+    for s in range(p):
+        assert busy[s] == pytest.approx(sum(ms[s]), rel=1e-6)
+        assert mk >= busy[s]
+    rt.close()

@@ -310,3 +310,28 @@ def test_interleave_needs_m_multiple_of_p_and_simulates():
         P.Plan(md, 8, 12, strategy="interleave")
     mk, _busy = P.Plan(md, 8, 16, strategy="interleave_trecomp").simulate()
     assert mk == 133
+
+
+@pytest.mark.parametrize("strategy", ["tpipe", "tpipe_trecomp", "1f1b", "1f1b_full_recomp",
+                                      "interleave_trecomp"])
+@pytest.mark.parametrize("p", [1, 2, 4, 8])
+def test_simulate_durations_matches_oracle(strategy, p):
+    """tpipe_plan_simulate_durations (ASAP replay with per-op durations, used
+    to replay measured op times) == the oracle simulator with the same
+    durations; with the unit durations it equals tpipe_plan_simulate."""
+    import random
+    P = _plan_mod()
+    m = 2 * p
+    plan = P.Plan(P.Model(2 * p if p > 1 else 2, 64, 4, 256, 128, 32, 2), p, m, strategy=strategy)
+    orders, v, rec, dur = S.strategy_orders(strategy, p, m)
+    rng = random.Random(p * 31 + len(strategy))
+    ms = [[rng.randint(1, 40) / 8.0 for _ in orders[s]] for s in range(p)]
+    mk, busy = plan.simulate_durations(ms)
+    idx = {(s, op): j for s in range(p) for j, op in enumerate(orders[s])}
+    sim = S.simulate(orders, p, v, lambda s, op: ms[s][idx[(s, op)]], rec)
+    assert mk == pytest.approx(sim["makespan"], abs=1e-9)
+    for s in range(p):
+        assert busy[s] == pytest.approx(sum(ms[s]), abs=1e-9)
+    unit = [[float(dur.get("B1", dur["B"]) if (op[0] == "B" and op[1] == 1) else dur[op[0]])
+             for op in orders[s]] for s in range(p)]
+    assert plan.simulate_durations(unit)[0] == plan.simulate()[0]
