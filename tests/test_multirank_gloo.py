@@ -132,7 +132,7 @@ def _worker(rank, world, port, strategy, m, errq):
 
 
 @pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("strategy", ["tpipe", "tpipe_trecomp", "1f1b"])
+@pytest.mark.parametrize("strategy", ["tpipe", "tpipe_trecomp", "1f1b", "interleave", "interleave_trecomp"])
 def test_streams_execute_over_gloo(world, strategy):
     ctx = mp.get_context("spawn")
     errq = ctx.SimpleQueue()
