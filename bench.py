@@ -114,7 +114,7 @@ def init_chunk(plan, s, c, rng):
     import synth
     shapes.update(synth.layer_shapes(h, f))
     parts = []
-    for k, _l in PR.chunk_entries(plan.p, plan.v, plan.layers_chunk, s, c):
+    for k, _l in PR.chunk_entries(plan.p, plan.v, plan.partition, s, c):
         shp = shapes[k]
         n = int(np.prod(shp))
         if len(shp) == 2:
@@ -194,7 +194,7 @@ def fast_init_chunk(plan, s, c, pool):
     V, sl = plan.model.vocab, plan.model.seq_len
     shapes = {"wte": (V, h), "wpe": (sl, h), "lnf_g": (h,), "lnf_b": (h,), "w_head": (V, h)}
     shapes.update(synth.layer_shapes(h, f))
-    ents = PR.chunk_entries(plan.p, plan.v, plan.layers_chunk, s, c)
+    ents = PR.chunk_entries(plan.p, plan.v, plan.partition, s, c)
     out = np.empty(sum(int(np.prod(shapes[k])) for k, _ in ents), np.float32)
     off = 0
     for k, _l in ents:
@@ -411,7 +411,31 @@ def hbm_kernels(c, hbm_peak):
     return out
 
 
-def pipeline_replay(ps=(8,), strategies=("1f1b", "tpipe", "tpipe_trecomp", "1f1b_full_recomp"), m=None):
+def balanced_partition(L, p, v, head_layers):
+    """Cost-balanced per-stage layer vector (DESIGN R27, SURVEY D-12): the last
+    stage also runs the LM head, worth `head_layers` layers of work (6hV vs
+    72h^2 + 6sh FLOPs per token); choose its layer count n_last >= v to
+    minimise the largest stage cost, spread the other L - n_last layers as
+    evenly as possible (extra layers on the earliest stages)."""
+    best = None
+    for n_last in range(v, L // p + 1):
+        rest = L - n_last
+        if rest < v * (p - 1):
+            break
+        hi = -(-rest // (p - 1)) if p > 1 else 0
+        cost = max(hi, n_last + head_layers)
+        if best is None or cost < best[0] - 1e-9:
+            best = (cost, n_last)
+    if p == 1 or best is None:
+        return None
+    n_last = best[1]
+    rest = L - n_last
+    base, extra = divmod(rest, p - 1)
+    return [base + (1 if s < extra else 0) for s in range(p - 1)] + [n_last]
+
+
+def pipeline_replay(ps=(8,), strategies=("1f1b", "tpipe", "tpipe_trecomp", "1f1b_full_recomp",
+                                         "1f1b_bal", "tpipe_bal", "tpipe_trecomp_bal"), m=None):
     """Measured-duration replay of the p-stage pipeline (SURVEY §8(d) bubble
     fraction, D-12 stage balance): all p stages of the C2 model run on this
     GPU as a virtual pipeline with TPIPE_STEP_OP_TIMES, so every F / B / R op
@@ -433,13 +457,21 @@ def pipeline_replay(ps=(8,), strategies=("1f1b", "tpipe", "tpipe_trecomp", "1f1b
     tokens = m * c["micro_batch"] * c["seq_len"]
     _, _, pk_sust, _src = peaks()
     out = {}
+    head_layers = 6 * c["hidden"] * c["vocab"] / (72 * c["hidden"] ** 2 + 6 * c["seq_len"] * c["hidden"])
     for p in ps:
         res = {}
         for st in strategies:
             md = P.Model(c["n_layers"], c["hidden"], c["n_heads"], c["ffn_hidden"], c["vocab"],
                          c["seq_len"], c["micro_batch"], P.BF16)
+            base_st = st[:-4] if st.endswith("_bal") else st
+            part = None
+            if st.endswith("_bal"):
+                v = 1 if base_st.startswith("1f1b") else 2
+                part = balanced_partition(c["n_layers"], p, v, head_layers)
+                if part is None:
+                    continue
             try:
-                plan = P.Plan(md, p, m, strategy=st)
+                plan = P.Plan(md, p, m, strategy=base_st, stage_layers=part)
             except Exception as e:   # e.g. an invalid chunk split
                 res[st] = {"error": str(e)[:120]}
                 continue
@@ -453,7 +485,8 @@ def pipeline_replay(ps=(8,), strategies=("1f1b", "tpipe", "tpipe_trecomp", "1f1b
             rt.close()
             mk, busy = plan.simulate_durations(op_ms)
             tps = tokens / (mk / 1e3)
-            res[st] = {"layers_chunk": list(plan.layers_chunk), "ms_per_step": round(mk, 2),
+            res[st] = {"layers_chunk": list(plan.layers_chunk), "stage_layers": part,
+                       "ms_per_step": round(mk, 2),
                        "tokens_s": round(tps, 1),
                        "mfu": round(tps * model_flops_per_token(c) / (p * pk_sust * 1e12), 4),
                        "bubble_fraction": [round(1.0 - b / mk, 4) for b in busy[:p]],
@@ -857,7 +890,9 @@ def main():
         print(json.dumps({"pipeline_replay": pipeline_replay((2, 4, 8), ("1f1b", "tpipe", "tpipe_trecomp",
                                                                         "1f1b_full_recomp",
                                                                         "interleave",
-                                                                        "interleave_trecomp"))}),
+                                                                        "interleave_trecomp",
+                                                                        "1f1b_bal", "tpipe_bal",
+                                                                        "tpipe_trecomp_bal"))}),
               flush=True)
         return
     if args.warmup < 3:

@@ -104,7 +104,13 @@ typedef struct {
                               shallowest first; the deeper n1 - r layers keep their stash
                               from F to B. 0 = all n1 layers (block-wise T-Recomp).
                               Must be <= n1. With strategy -1 (auto) and 0 here, the
-                              escalation tries r = 1..n1 at each rung (DESIGN R25) */
+                              escalation tries r = 1..n1 at each rung (DESIGN R25);
+                              with stage_layers, stage s recomputes min(r, n1(s)) layers */
+    int32_t stage_layers[64]; /* cost-balanced partition (SURVEY D-12, DESIGN R27): transformer
+                              layers held by stage s (chunk split ceil/floor of n(s)/2 at
+                              v = 2); all zero = uniform n_layers / n_stages. When set: the
+                              first n_stages entries sum to n_layers, each >= 2 at v = 2 (>= 1
+                              at v = 1), model.layers_chunk must be {0, 0} */
 } tpipe_plan_opts;
 
 enum {
@@ -195,6 +201,8 @@ typedef struct {
 } tpipe_sim_report_ms;
 int tpipe_plan_simulate_durations(const tpipe_plan* plan, const float* const* op_ms,
                                   tpipe_sim_report_ms* out);
+/* layers of (stage, chunk 1) and (stage, chunk 2) (chunk 2 = 0 at v = 1) */
+int tpipe_plan_stage_layers(const tpipe_plan* plan, int32_t stage, int32_t out[2]);
 /* parameters of (stage, chunk) in the packed order of DESIGN.md §2.3 */
 int tpipe_plan_chunk_params(const tpipe_plan* plan, int32_t stage, int32_t chunk, uint64_t* n);
 

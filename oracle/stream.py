@@ -34,6 +34,7 @@ class ModelDesc:
     micro_batch: int
     dtype: int = BF16
     layers_chunk: tuple = (0, 0)  # per-stage (chunk1, chunk2) layers; 0 = auto
+    stage_layers: tuple = ()      # cost-balanced partition: layers of each stage (DESIGN R27)
 
     @property
     def es(self) -> int:
@@ -44,9 +45,17 @@ class ModelDesc:
         return self.seq_len * self.micro_batch
 
 
-def layers_per_chunk(d: ModelDesc, p: int, v: int):
+def layers_per_chunk(d: ModelDesc, p: int, v: int, s: int = 0):
     """n = L/p layers per stage (p | L required). v=2: the extra layer of an odd
-    n goes to chunk 1. Override via d.layers_chunk."""
+    n goes to chunk 1. Override via d.layers_chunk. With
+    d.stage_layers (DESIGN R27) stage s holds n(s) layers, split the same way."""
+    if d.stage_layers:
+        if len(d.stage_layers) != p or sum(d.stage_layers) != d.n_layers:
+            raise ValueError("stage_layers")
+        n = d.stage_layers[s]
+        if n < v:
+            raise ValueError("stage_layers")
+        return (n,) if v == 1 else ((n + 1) // 2, n // 2)
     if d.n_layers % p:
         raise ValueError("n_layers")
     n = d.n_layers // p
@@ -72,7 +81,7 @@ def layer_params(d: ModelDesc) -> int:
 
 
 def chunk_params(d: ModelDesc, p: int, v: int, s: int, c: int) -> int:
-    n = layers_per_chunk(d, p, v)[c - 1]
+    n = layers_per_chunk(d, p, v, s)[c - 1]
     P = n * layer_params(d)
     if s == 0 and c == 1:
         P += d.vocab * d.hidden + d.seq_len * d.hidden          # wte, wpe
@@ -108,7 +117,7 @@ def n_partials(M: int) -> int:
 def sizes(d: ModelDesc, p: int, v: int, s: int, c: int, full_recomp: bool = False):
     """Byte model per (stage, chunk), DESIGN.md §4."""
     M, h, a, f, V, es = d.tokens, d.hidden, d.n_heads, d.ffn_hidden, d.vocab, d.es
-    n = layers_per_chunk(d, p, v)[c - 1]
+    n = layers_per_chunk(d, p, v, s)[c - 1]
     act = M * h * es
     emb = (s == 0 and c == 1)
     head = (s == p - 1 and c == v)
@@ -224,10 +233,13 @@ def build_streams(d: ModelDesc, p: int, m: int, strategy: str, k=None,
           for s in range(p) for c in range(1, v + 1)}
     keep1, rec1 = {}, {}
     if trecomp:
-        n1 = layers_per_chunk(d, p, v)[0]
-        r = recomp_layers if recomp_layers else n1
+        n1max = max(layers_per_chunk(d, p, v, s)[0] for s in range(p))
+        r = recomp_layers if recomp_layers else n1max
+        if r > n1max:
+            raise ValueError("recomp_layers")
         for s in range(p):
-            keep1[s], rec1[s] = partial_trecomp_split(sz[(s, 1)], n1, r)
+            n1 = layers_per_chunk(d, p, v, s)[0]
+            keep1[s], rec1[s] = partial_trecomp_split(sz[(s, 1)], n1, min(r, n1))
 
     static = []
     for s in range(p):

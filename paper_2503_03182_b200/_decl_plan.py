@@ -13,7 +13,7 @@ class ModelDesc(C.Structure):
 
 class PlanOpts(C.Structure):
     _fields_ = [("strategy", i32), ("delay_rounds", i32), ("send_window", i32), ("offload", i32),
-                ("act_distance", i32), ("recomp_layers", i32)]
+                ("act_distance", i32), ("recomp_layers", i32), ("stage_layers", i32 * 64)]
 
 
 class Op(C.Structure):
@@ -76,6 +76,7 @@ def declare(L):
     L.tpipe_plan_simulate.argtypes = [vp, P(SimReport)]
     L.tpipe_plan_simulate_durations.argtypes = [vp, P(P(f32)), P(SimReportMs)]
     L.tpipe_plan_chunk_params.argtypes = [vp, i32, i32, P(u64)]
+    L.tpipe_plan_stage_layers.argtypes = [vp, i32, P(i32)]
     L.tpipe_version.argtypes = []
     if hasattr(L, "tpipe_runtime_create"):
         L.tpipe_runtime_create.argtypes = [vp, P(RuntimeOpts), P(vp)]

@@ -304,7 +304,7 @@ static int build(tpipe_plan* P, bool trecomp, bool full_recomp) {
         Builder B(P, s);
         // static buffers: model state per chunk, io
         for (int c = 1; c <= v; ++c) {
-            const uint64_t np = chunk_params(d, p, v, P->layers, s, c);
+            const uint64_t np = chunk_params(d, p, v, P->sl[s].data(), s, c);
             P->chunk_params[s][c - 1] = np;
             P->params_total += np;
             const bool o = off && c == v;
@@ -317,13 +317,13 @@ static int build(tpipe_plan* P, bool trecomp, bool full_recomp) {
         if (s == p - 1) B.bufs.push_back({TPIPE_BUF_STATIC, TPIPE_CAT_IO, 0, 1, 4ull * m * M + 4ull * m});
 
         ChunkSizes z[3];
-        for (int c = 1; c <= v; ++c) z[c] = chunk_sizes(d, p, v, P->layers, s, c, full_recomp);
+        for (int c = 1; c <= v; ++c) z[c] = chunk_sizes(d, p, v, P->sl[s].data(), s, c, full_recomp);
         // partial T-Recomp (R25): layers 1..r of chunk 1 are regenerated by R (TSTASH during
         // F, RBUF from R to B); the stash of layers r+1..n1 is kept from F to B (STASH).
         // The two parts add up to the full chunk-1 stash.
         uint64_t keep1 = 0, rec1 = z[1].stash;
-        if (trecomp && P->rl < P->layers[0]) {
-            keep1 = (uint64_t)(P->layers[0] - P->rl) * layer_stash_bytes(d);
+        if (trecomp && P->rl_of(s) < P->sl[s][0]) {
+            keep1 = (uint64_t)(P->sl[s][0] - P->rl_of(s)) * layer_stash_bytes(d);
             rec1 = z[1].stash - keep1;
         }
 
@@ -566,7 +566,7 @@ static int validate(const tpipe_model_desc* d, int p, int m) {
     if (p < 1 || p > 64) return set_error(TPIPE_E_INVALID, "n_stages must be in [1, 64]");
     if (m < 1) return set_error(TPIPE_E_INVALID, "n_microbatches must be >= 1");
     if (d->dtype != TPIPE_FP32 && d->dtype != TPIPE_BF16) return set_error(TPIPE_E_INVALID, "dtype");
-    if (d->n_layers < 1 || d->n_layers % p) return set_error(TPIPE_E_INVALID, "n_layers must be a positive multiple of n_stages");
+    if (d->n_layers < 1) return set_error(TPIPE_E_INVALID, "n_layers must be a positive multiple of n_stages");
     if (d->hidden < 64 || d->hidden % 64) return set_error(TPIPE_E_INVALID, "hidden must be a multiple of 64");
     if (d->ffn_hidden < 64 || d->ffn_hidden % 64) return set_error(TPIPE_E_INVALID, "ffn_hidden must be a multiple of 64");
     if (d->vocab < 64 || d->vocab % 64 || d->vocab >= (1 << 17)) return set_error(TPIPE_E_INVALID, "vocab must be a multiple of 64 below 131072");
@@ -585,7 +585,8 @@ using namespace tpipe;
 #define TP_API extern "C" __attribute__((visibility("default")))
 
 static int make_plan(const tpipe_model_desc* model, int p, int m, int strategy, int k, int W,
-                     int offload, int act_distance, int recomp_layers, tpipe_plan** out) {
+                     int offload, int act_distance, int recomp_layers, const int32_t* stage_layers,
+                     tpipe_plan** out) {
     if ((offload & TPIPE_OFFLOAD_DEVICE_OPT) && !(offload & TPIPE_OFFLOAD_MODEL_STATE))
         return set_error(TPIPE_E_INVALID, "offload: DEVICE_OPT needs MODEL_STATE");
     if ((offload & TPIPE_OFFLOAD_ACTIVATIONS) && strategy != TPIPE_S_TPIPE)
@@ -607,7 +608,31 @@ static int make_plan(const tpipe_model_desc* model, int p, int m, int strategy, 
     }
     P->v = is_tp ? 2 : 1;
     const int n = model->n_layers / p;
-    if (P->v == 2) {
+    const bool part = stage_layers && stage_layers[0] != 0;
+    if (part) {   // cost-balanced partition (R27)
+        long sum = 0;
+        for (int s = 0; s < p; ++s) {
+            const int ns = stage_layers[s];
+            if (ns < P->v || (model->layers_chunk[0] || model->layers_chunk[1])) {
+                const int vv = P->v;
+                delete P;
+                return set_error(TPIPE_E_INVALID, "stage_layers[%d] = %d: need >= %d layers per stage "
+                                 "(and layers_chunk {0,0})", s, ns, vv);
+            }
+            sum += ns;
+            P->sl.push_back(P->v == 2 ? std::array<int, 2>{(ns + 1) / 2, ns / 2} : std::array<int, 2>{ns, 0});
+        }
+        if (sum != model->n_layers) {
+            delete P;
+            return set_error(TPIPE_E_INVALID, "stage_layers sum %ld != n_layers %d", sum, model->n_layers);
+        }
+        if (offload & TPIPE_OFFLOAD_MODEL_STATE && P->v != 2) {
+            delete P;
+            return set_error(TPIPE_E_INCOMPAT, "model-state offload requires T-Pipe (v = 2)");
+        }
+        P->layers[0] = P->sl[0][0];
+        P->layers[1] = P->sl[0][1];
+    } else if (P->v == 2) {
         if (model->layers_chunk[0] || model->layers_chunk[1]) {
             if (model->layers_chunk[0] < 1 || model->layers_chunk[1] < 1 ||
                 model->layers_chunk[0] + model->layers_chunk[1] != n) {
@@ -631,14 +656,16 @@ static int make_plan(const tpipe_model_desc* model, int p, int m, int strategy, 
         }
         P->layers[0] = n;
     }
+    if (!part) P->sl.assign(p, std::array<int, 2>{P->layers[0], P->v == 2 ? P->layers[1] : 0});
+    int n1max = 0;
+    for (auto& x : P->sl) n1max = std::max(n1max, x[0]);
     const bool trecomp = strategy == TPIPE_S_TPIPE_TRECOMP || strategy == TPIPE_S_INTERLEAVE_TRECOMP;
-    if (trecomp && recomp_layers > P->layers[0]) {
-        const int n1 = P->layers[0];
+    if (trecomp && recomp_layers > n1max) {
         delete P;
         return set_error(TPIPE_E_INVALID, "recomp_layers %d exceeds the %d chunk-1 layers per stage",
-                         recomp_layers, n1);
+                         recomp_layers, n1max);
     }
-    P->rl = trecomp ? (recomp_layers > 0 ? recomp_layers : P->layers[0]) : 0;
+    P->rl = trecomp ? (recomp_layers > 0 ? recomp_layers : n1max) : 0;
     P->k = (trecomp && !is_il) ? (k < 0 ? delay_rounds_appB(p) : k) : 0;
     if (is_il) {
         auto ord = interleave_order(p, m, trecomp);
@@ -678,8 +705,10 @@ TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, in
     if (!out) return set_error(TPIPE_E_INVALID, "out is NULL");
     *out = nullptr;
     if (int rc = validate(model, n_stages, n_microbatches)) return rc;
-    tpipe_plan_opts o{-1, -1, 0, -1, 0, 0};
+    tpipe_plan_opts o{-1, -1, 0, -1, 0, 0, {}};
     if (opts) o = *opts;
+    if (o.stage_layers[0] == 0 && model && n_stages > 0 && model->n_layers % n_stages)
+        return set_error(TPIPE_E_INVALID, "n_layers must be a positive multiple of n_stages");
     const int W = o.send_window > 0 ? o.send_window : 2;
     if (o.strategy < -1 || o.strategy > TPIPE_S_INTERLEAVE_TRECOMP) return set_error(TPIPE_E_INVALID, "strategy");
     if (o.delay_rounds < -1) return set_error(TPIPE_E_INVALID, "delay_rounds");
@@ -688,7 +717,7 @@ TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, in
         const int off = o.offload < 0 ? 0 : o.offload;
         tpipe_plan* P = nullptr;
         int rc = make_plan(model, n_stages, n_microbatches, o.strategy, o.delay_rounds, W, off,
-                           o.act_distance, o.recomp_layers, &P);
+                           o.act_distance, o.recomp_layers, o.stage_layers, &P);
         if (rc) return rc;
         if (hbm_budget_bytes && max_peak(P) > hbm_budget_bytes) {
             const uint64_t pk = max_peak(P);
@@ -702,7 +731,9 @@ TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, in
     // auto escalation (fit the budget with the least throughput loss):
     // T-Pipe -> + T-Recomp of r = 1..n1 chunk-1 layers (R25) -> + model-state
     // T-Offload (device AdamW streaming if requested in `offload`) with r = 1..n1
-    const int n1 = model->layers_chunk[0] ? model->layers_chunk[0] : (model->n_layers / n_stages + 1) / 2;
+    int n1 = model->layers_chunk[0] ? model->layers_chunk[0] : (model->n_layers / n_stages + 1) / 2;
+    if (o.stage_layers[0])
+        for (int s = 0; s < n_stages && s < 64; ++s) n1 = std::max(n1, (o.stage_layers[s] + 1) / 2);
     const int rmin = o.recomp_layers > 0 ? o.recomp_layers : 1;
     const int rmax = o.recomp_layers > 0 ? o.recomp_layers : n1;
     const int off_flags = TPIPE_OFFLOAD_MODEL_STATE |
@@ -716,7 +747,7 @@ TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, in
     for (auto& rung : ladder) {
         tpipe_plan* P = nullptr;
         int rc = make_plan(model, n_stages, n_microbatches, rung[0], o.delay_rounds, W, rung[1],
-                           o.act_distance, rung[2], &P);
+                           o.act_distance, rung[2], o.stage_layers, &P);
         if (rc) return rc;
         best = max_peak(P);
         if (!hbm_budget_bytes || best <= hbm_budget_bytes) {
@@ -782,6 +813,13 @@ TP_API int tpipe_plan_channel(const tpipe_plan* P, int32_t c, int32_t* kind, int
     if (kind) *kind = P->channels[c][0];
     if (src) *src = P->channels[c][1];
     if (dst) *dst = P->channels[c][2];
+    return 0;
+}
+
+TP_API int tpipe_plan_stage_layers(const tpipe_plan* P, int32_t s, int32_t out[2]) {
+    if (!P || !out || s < 0 || s >= P->p) return set_error(TPIPE_E_INVALID, "stage");
+    out[0] = P->sl[s][0];
+    out[1] = P->sl[s][1];
     return 0;
 }
 

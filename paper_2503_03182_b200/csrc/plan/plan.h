@@ -13,6 +13,10 @@ struct tpipe_plan {
     int strategy = 0, k = 0, W = 2, offload = 0, act_distance = 2;
     int layers[2] = {0, 0};
     int rl = 0;   // partial T-Recomp: chunk-1 layers recomputed (R25); 0 unless T-Recomp
+    // per-stage (chunk-1, chunk-2) layers (R27; all equal to `layers` unless a
+    // stage_layers partition was requested)
+    std::vector<std::array<int, 2>> sl;
+    int rl_of(int s) const { return rl < sl[s][0] ? rl : sl[s][0]; }
     uint64_t params_total = 0;
     // per stage
     std::vector<std::vector<tpipe_op>> ops;

@@ -324,14 +324,14 @@ int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags
             void* ws = nullptr;
             op_alloc_ptr(rt, S, op, TPIPE_BUF_WS, -1, &ws);
             a.ws = (uint8_t*)ws;
-            const bool partial = trecomp && c == 1 && P.rl < P.layers[0];
+            const bool partial = trecomp && c == 1 && P.rl_of(s) < P.sl[s][0];
             if (op.kind == TPIPE_OP_R) {
                 void* rb;
                 op_alloc_ptr(rt, S, op, TPIPE_BUF_RBUF, -1, &rb);
                 a.stash = (uint8_t*)rb;
                 a.out = nullptr;
                 a.targets = nullptr;
-                if (partial) a.split = a.n_run = P.rl;   // regenerate layers 1..r only
+                if (partial) a.split = a.n_run = P.rl_of(s);   // regenerate layers 1..r only
             } else {
                 void *tst = nullptr, *kst = nullptr;
                 op_alloc_ptr(rt, S, op, TPIPE_BUF_TSTASH, -1, &tst);
@@ -340,7 +340,7 @@ int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags
                 if (tst && partial) {
                     if (!kst) return set_error(TPIPE_E_STATE, "stage %d F(1,%d): kept stash missing", s, i);
                     a.stash2 = (uint8_t*)kst;
-                    a.split = P.rl;
+                    a.split = P.rl_of(s);
                 }
                 void* out = nullptr;
                 if (!op_alloc_ptr(rt, S, op, TPIPE_BUF_MSG, -1, &out))
@@ -367,9 +367,9 @@ int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags
             void* stp = (trecomp && c == 1) ? live_get(S, TPIPE_BUF_RBUF, c, i)
                                             : live_get(S, TPIPE_BUF_STASH, c, i);
             a.stash = (uint8_t*)stp;
-            if (trecomp && c == 1 && P.rl < P.layers[0]) {   // partial T-Recomp (R25)
+            if (trecomp && c == 1 && P.rl_of(s) < P.sl[s][0]) {   // partial T-Recomp (R25)
                 a.stash2 = (uint8_t*)live_get(S, TPIPE_BUF_STASH, c, i);
-                a.split = P.rl;
+                a.split = P.rl_of(s);
                 if (!a.stash2) return set_error(TPIPE_E_STATE, "stage %d B(1,%d): kept stash missing", s, i);
             }
             void* ws = nullptr;
@@ -693,8 +693,8 @@ TP_API int tpipe_runtime_create(const tpipe_plan* plan, const tpipe_runtime_opts
                 const int c = b.chunk;
                 ChunkState& C = S->ch[c];
                 const bool emb = (s == 0 && c == 1), head = (s == P.p - 1 && c == P.v);
-                C.lay = make_param_layout(P.model, P.layers[c - 1], emb, head);
-                C.sl = make_stash_layout(P.model, P.layers[c - 1], emb, head,
+                C.lay = make_param_layout(P.model, P.sl[s][c - 1], emb, head);
+                C.sl = make_stash_layout(P.model, P.sl[s][c - 1], emb, head,
                                          P.strategy == TPIPE_S_1F1B_FULL_RECOMP);
                 C.P = C.lay.total;
                 if ((uint64_t)C.P != P.chunk_params[s][c - 1])

@@ -17,14 +17,22 @@ LAYER_TENSORS = ("ln1_g", "ln1_b", "w_qkv", "b_qkv", "w_o", "b_o",
 
 
 def global_layers(p: int, v: int, layers_chunk, s: int, c: int):
-    """Global layer indices held by (stage s, chunk c)."""
+    """Global layer indices held by (stage s, chunk c). `layers_chunk` is the
+    uniform per-stage (n1, n2) (or (n,) at v = 1), or a per-stage list of such
+    tuples (plan.partition, DESIGN R27): chunk-1 layers are numbered through
+    the stages first, then chunk-2 layers (P:210 layout)."""
+    if layers_chunk and isinstance(layers_chunk[0], (tuple, list)):
+        part = [tuple(x) for x in layers_chunk]
+    else:
+        part = [tuple(layers_chunk)] * p
     if v == 1:
-        n = layers_chunk[0]
-        return list(range(s * n, (s + 1) * n))
-    n1, n2 = layers_chunk
+        off = sum(part[t][0] for t in range(s))
+        return list(range(off, off + part[s][0]))
     if c == 1:
-        return list(range(s * n1, (s + 1) * n1))
-    return list(range(p * n1 + s * n2, p * n1 + (s + 1) * n2))
+        off = sum(part[t][0] for t in range(s))
+        return list(range(off, off + part[s][0]))
+    off = sum(x[0] for x in part) + sum(part[t][1] for t in range(s))
+    return list(range(off, off + part[s][1]))
 
 
 def chunk_entries(p, v, layers_chunk, s, c):

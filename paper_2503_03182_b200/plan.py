@@ -47,12 +47,13 @@ class Plan:
 
     def __init__(self, model: Model, n_stages: int, n_microbatches: int, hbm_budget: int = 0,
                  strategy="tpipe", delay_rounds: int = -1, send_window: int = 0, offload: int = 0,
-                 act_distance: int = 0, recomp_layers: int = 0):
+                 act_distance: int = 0, recomp_layers: int = 0, stage_layers=None):
         L = lib()
         st = -1 if strategy in (None, "auto") else STRATEGY.get(strategy, strategy)
         if st < 0 and offload == 0:
             offload = -1
-        opts = D.PlanOpts(st, delay_rounds, send_window, offload, act_distance, recomp_layers)
+        sl = (C.c_int32 * 64)(*(list(stage_layers or [])[:64]))
+        opts = D.PlanOpts(st, delay_rounds, send_window, offload, act_distance, recomp_layers, sl)
         self._h = C.c_void_p()
         self.model = model
         check(L.tpipe_plan_create(C.byref(model.c()), n_stages, n_microbatches, hbm_budget,
@@ -64,6 +65,14 @@ class Plan:
                                                        info.send_window, info.offload)
         self.act_distance = info.act_distance
         self.recomp_layers = info.recomp_layers
+        # per-stage (chunk-1, chunk-2) layers (DESIGN R27); == [layers_chunk] * p when uniform
+        self.partition = []
+        for s in range(self.p):
+            a = (C.c_int32 * 2)()
+            check(L.tpipe_plan_stage_layers(self._h, s, a))
+            self.partition.append((a[0], a[1]))
+        if self.v == 1:
+            self.partition = [(x[0],) for x in self.partition]
         self.layers_chunk = (info.layers_chunk[0], info.layers_chunk[1])
         self.params_total = info.params_total
         self.channels = []

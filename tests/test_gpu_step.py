@@ -25,17 +25,18 @@ def mods():
     return plan, runtime, params
 
 
-def build(cfg, p, m, strategy, dtype, offload=0, lr=1e-3, seed=11, recomp_layers=0):
+def build(cfg, p, m, strategy, dtype, offload=0, lr=1e-3, seed=11, recomp_layers=0, stage_layers=None):
     P, RT, PR = mods()
     md = P.Model(cfg["n_layers"], cfg["hidden"], cfg["n_heads"], cfg["ffn_hidden"], cfg["vocab"],
                  cfg["seq_len"], cfg["micro_batch"], dtype)
-    plan = P.Plan(md, p, m, strategy=strategy, offload=offload, recomp_layers=recomp_layers)
+    plan = P.Plan(md, p, m, strategy=strategy, offload=offload, recomp_layers=recomp_layers,
+                  stage_layers=stage_layers)
     rt = RT.Runtime(plan, stage=-1, lr=lr)
     W = synth.weights(cfg["n_layers"], cfg["hidden"], cfg["ffn_hidden"], cfg["vocab"],
                       cfg["seq_len"], seed=seed, std=0.05, bias_std=0.02, ln_jitter=0.05)
     for s in range(p):
         for c in range(1, plan.v + 1):
-            rt.set_params(s, c, PR.pack(W, p, plan.v, plan.layers_chunk, s, c))
+            rt.set_params(s, c, PR.pack(W, p, plan.v, plan.partition, s, c))
     return plan, rt, W
 
 
@@ -48,7 +49,7 @@ def compare(plan, rt, W, G, metric, tol):
     worst = 0.0
     for s in range(plan.p):
         for c in range(1, plan.v + 1):
-            got = PR.unpack(rt.get_grads(s, c), W, plan.p, plan.v, plan.layers_chunk, s, c)
+            got = PR.unpack(rt.get_grads(s, c), W, plan.p, plan.v, plan.partition, s, c)
             for (k, l), g in got.items():
                 ref = G["layers"][l][k] if l is not None else G[k]
                 err = metric(g, ref)
@@ -320,3 +321,38 @@ def test_op_times_and_replay():
         assert busy[s] == pytest.approx(sum(ms[s]), rel=1e-6)
         assert mk >= busy[s]
     rt.close()
+
+
+@pytest.mark.parametrize("strategy,p,part", [("tpipe_trecomp", 2, (5, 3)), ("1f1b", 4, (3, 2, 2, 1)),
+                                             ("tpipe", 4, (2, 2, 2, 2))])
+def test_partition_step(strategy, p, part):
+    """Cost-balanced partition (R27): per-stage layer vector. fp32 gradients
+    match the oracle (<= 1e-4), bf16 gradients are bit-identical per tensor to
+    the uniform partition's (layer math does not depend on chunk boundaries),
+    and the pool ledger high-water equals the plan peak on every stage."""
+    _P, RT, PR = mods()
+    m = 8
+    tok, tgt = synth.tokens(C1["vocab"], m, C1["micro_batch"], C1["seq_len"], step=2)
+    plan, rt, W = build(C1, p, m, strategy, 0, stage_layers=part)
+    assert [sum(x) for x in plan.partition] == list(part)
+    rt.step(tok, tgt, RT.STEP_NO_OPT)
+    lref, G = oracle_grads(C1, W, tok, tgt)
+    compare(plan, rt, W, G, max_rel, 1e-4)
+    st = rt.stats()
+    for s in range(p):
+        assert st["pool_high_water"][s] == plan.peak(s)["total_peak"]
+    rt.close()
+    grads = []
+    for sl in (part, None):
+        plan, rt, W = build(C1, p, m, strategy, 1, stage_layers=sl)
+        rt.step(tok, tgt, RT.STEP_NO_OPT)
+        g = {}
+        for s in range(p):
+            for c in range(1, plan.v + 1):
+                g.update(PR.unpack(rt.get_grads(s, c), W, p, plan.v, plan.partition, s, c))
+        grads.append(g)
+        rt.close()
+    assert grads[0].keys() == grads[1].keys()
+    for k in grads[0]:
+        assert np.array_equal(np.asarray(grads[0][k], np.float32).view(np.uint32),
+                              np.asarray(grads[1][k], np.float32).view(np.uint32)), k

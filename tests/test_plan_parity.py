@@ -335,3 +335,51 @@ def test_simulate_durations_matches_oracle(strategy, p):
     unit = [[float(dur.get("B1", dur["B"]) if (op[0] == "B" and op[1] == 1) else dur[op[0]])
              for op in orders[s]] for s in range(p)]
     assert plan.simulate_durations(unit)[0] == plan.simulate()[0]
+
+
+PARTITIONS = [(4, (3, 3, 2, 2)), (4, (2, 2, 2, 4)), (2, (5, 3)), (8, (3, 3, 3, 3, 3, 3, 4, 2))]
+
+
+@pytest.mark.parametrize("p,part", PARTITIONS)
+@pytest.mark.parametrize("strategy", ["tpipe", "tpipe_trecomp", "1f1b", "1f1b_full_recomp",
+                                      "interleave_trecomp"])
+def test_partition_streams_match_oracle(p, part, strategy):
+    """Cost-balanced partition (R27, SURVEY D-12): a per-stage layer vector;
+    instruction streams, buffer sizes and per-category peaks equal the
+    oracle's; chunk parameter counts follow the per-stage layers."""
+    P = _plan_mod()
+    L = sum(part)
+    m = 2 * p
+    od = T.ModelDesc(L, 64, 4, 256, 128, 32, 2, T.BF16, stage_layers=part)
+    pd = P.Model(L, 64, 4, 256, 128, 32, 2, P.BF16)
+    plan = P.Plan(pd, p, m, strategy=strategy, stage_layers=part)
+    st, static = T.build_streams(od, p, m, strategy)
+    for s in range(p):
+        got, bufs = plan.ops(s)
+        strip = [{k: o[k] for k in ("kind", "chunk", "mb", "peer", "channel", "msg")} for o in got]
+        assert strip == oracle_ops(st[s])
+        for g, w in zip(got, st[s]):
+            assert [(bufs[a][1], bufs[a][4]) for a in g["allocs"]] == [(c, b) for _n, c, b in w.allocs]
+        rep = T.replay(st[s], static[s])
+        pk = plan.peak(s)
+        for cat in ("model_state", "io", "act", "recomp_buf", "comm", "workspace"):
+            assert pk[cat] == rep.get(cat, 0), cat
+        for c in range(1, plan.v + 1):
+            assert plan.chunk_params(s, c) == T.chunk_params(od, p, plan.v, s, c)
+        assert sum(plan.partition[s]) == part[s]
+    from paper_2503_03182_b200._lib import TPipeError
+    with pytest.raises(TPipeError, match="stage_layers"):
+        P.Plan(pd, p, m, strategy=strategy, stage_layers=list(part[:-1]) + [part[-1] + 1])
+
+
+def test_partition_partial_trecomp_matches_oracle():
+    """Partial T-Recomp with a partition: stage s recomputes min(r, n1(s))."""
+    P = _plan_mod()
+    part = (6, 4, 2, 4)
+    od = T.ModelDesc(16, 64, 4, 256, 128, 32, 2, T.BF16, stage_layers=part)
+    pd = P.Model(16, 64, 4, 256, 128, 32, 2, P.BF16)
+    for r in (1, 2, 3):
+        plan = P.Plan(pd, 4, 8, strategy="tpipe_trecomp", recomp_layers=r, stage_layers=part)
+        st, static = T.build_streams(od, 4, 8, "tpipe_trecomp", recomp_layers=r)
+        for s in range(4):
+            assert plan.peak(s)["total_peak"] == T.replay(st[s], static[s])["total_peak"]
