@@ -434,6 +434,47 @@ def balanced_partition(L, p, v, head_layers):
     return [base + (1 if s < extra else 0) for s in range(p - 1)] + [n_last]
 
 
+def modeled_makespan(plan, head_layers):
+    """Unit-model makespan of a plan with per-op durations from its layer
+    counts (F = layers of the chunk + the LM head's layer-equivalents on the
+    last stage's last chunk, B = 2F, R = the recomputed layers), replayed by
+    tpipe_plan_simulate_durations."""
+    ms = []
+    for s in range(plan.p):
+        ops, _ = plan.ops(s)
+        d = []
+        for o in ops:
+            if o["kind"] not in ("F", "B", "R"):
+                continue
+            ch = o["chunk"]
+            f = plan.partition[s][ch - 1] + (head_layers if (s == plan.p - 1 and ch == plan.v) else 0.0)
+            if o["kind"] == "R":
+                f = min(plan.recomp_layers, plan.partition[s][0])
+            d.append(2 * f if o["kind"] == "B" else f)
+        ms.append(d)
+    return plan.simulate_durations(ms)[0]
+
+
+def choose_partition(md, p, m, strategy, c=None):
+    """Balanced per-stage layer vector (R27) when the duration model predicts
+    >= 3% shorter steps than the uniform split, else None (uniform)."""
+    from paper_2503_03182_b200 import plan as P
+    c = c or C2
+    if p < 2:
+        return None
+    hl = 6 * c["hidden"] * c["vocab"] / (72 * c["hidden"] ** 2 + 6 * c["seq_len"] * c["hidden"])
+    v = 1 if strategy.startswith("1f1b") else 2
+    part = balanced_partition(md.n_layers, p, v, hl)
+    if not part:
+        return None
+    try:
+        u = modeled_makespan(P.Plan(md, p, m, strategy=strategy), hl)
+        b = modeled_makespan(P.Plan(md, p, m, strategy=strategy, stage_layers=part), hl)
+    except Exception:
+        return None
+    return part if b < 0.97 * u else None
+
+
 def pipeline_replay(ps=(8,), strategies=("1f1b", "tpipe", "tpipe_trecomp", "1f1b_full_recomp",
                                          "1f1b_bal", "tpipe_bal", "tpipe_trecomp_bal"), m=None):
     """Measured-duration replay of the p-stage pipeline (SURVEY §8(d) bubble
@@ -652,7 +693,9 @@ def run_tpipe(args):
     md = P.Model(c["n_layers"], c["hidden"], c["n_heads"], c["ffn_hidden"], c["vocab"],
                  c["seq_len"], c["micro_batch"], P.BF16)
     m = c["m"]
-    plan = P.Plan(md, N, m, strategy=args.strategy)
+    # p > 1: cost-balanced stage partition when the duration model says it pays (R27)
+    part = choose_partition(md, N, m, args.strategy) if N > 1 else None
+    plan = P.Plan(md, N, m, strategy=args.strategy, stage_layers=part)
     ids = None
     if world > 1:
         ids = [b"".join(RT.nccl_unique_id() for _ in plan.channels)] if rank == 0 else [None]
@@ -738,6 +781,7 @@ def run_tpipe(args):
                        "micro_batch": 1, "n_microbatches": m, "global_batch_tokens": tokens,
                        "strategy": args.strategy, "parallelism": f"pp{N}",
                        "layers_per_chunk": list(plan.layers_chunk),
+                       "stage_layers": [sum(x) for x in plan.partition],
                        "l2": "working set >> 126 MB L2 (no flush needed)"},
             "mfu": round(mfu, 4),
             "hfu": round(hw_flops / (step_ms / 1e3) / (N * pk_sust * 1e12), 4),
