@@ -33,3 +33,24 @@ def test_capacity_sweep_size_target():
     assert cap["tpipe_trecomp"]["max_layers"] > cap["tpipe"]["max_layers"] >= cap["1f1b"]["max_layers"]
     # plain Interleave-1F1B stores more than 1F1B; with T-Recomp it stores less
     assert cap["interleave"]["max_layers"] < cap["1f1b"]["max_layers"] < cap["interleave_trecomp"]["max_layers"]
+
+
+def test_balanced_partition_and_choice():
+    """R27: the balanced split keeps every stage >= v layers, sums to L and
+    lowers the largest stage cost (head counted in layer-equivalents); the
+    bench picks it only when the duration-model replay predicts >= 3% gain."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2503_03182_b200 import plan as P
+    c = bench.C2
+    hl = 6 * c["hidden"] * c["vocab"] / (72 * c["hidden"] ** 2 + 6 * c["seq_len"] * c["hidden"])
+    for p in (2, 4, 8):
+        for v in (1, 2):
+            part = bench.balanced_partition(24, p, v, hl)
+            assert sum(part) == 24 and min(part) >= v and len(part) == p
+            cost = max(max(part[:-1]), part[-1] + hl)
+            assert cost <= max(24 // p, 24 // p + hl)
+    md = P.Model(24, 2048, 16, 8192, 50304, 2048, 1, P.BF16)
+    assert bench.choose_partition(md, 8, 32, "tpipe") == [4, 3, 3, 3, 3, 3, 3, 2]
+    assert bench.choose_partition(md, 4, 32, "tpipe") is None
+    assert bench.choose_partition(md, 1, 32, "tpipe") is None
