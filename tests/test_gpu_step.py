@@ -356,3 +356,29 @@ def test_partition_step(strategy, p, part):
     for k in grads[0]:
         assert np.array_equal(np.asarray(grads[0][k], np.float32).view(np.uint32),
                               np.asarray(grads[1][k], np.float32).view(np.uint32)), k
+
+
+@pytest.mark.parametrize("dtype", [0, 1])
+def test_partition_offload_partial_bitexact(dtype):
+    """Features compose: an uneven partition (5, 3) with partial T-Recomp
+    (r = 1) and T-Offload of the chunk-2 model states (host AdamW and streamed
+    device AdamW) gives parameters after 2 optimizer steps bit-identical to
+    plain T-Pipe on the same partition; ledger high-water == plan peak."""
+    P = mods()[0]
+    p, m = 2, 8
+    res = []
+    for strat, off, rl in (("tpipe", 0, 0), ("tpipe_trecomp", P.OFFLOAD_MODEL_STATE, 1),
+                           ("tpipe_trecomp", P.OFFLOAD_MODEL_STATE | P.OFFLOAD_DEVICE_OPT, 1)):
+        plan, rt, _W = build(C1, p, m, strat, dtype, offload=off, recomp_layers=rl, stage_layers=(5, 3))
+        losses = []
+        for step in range(2):
+            tok, tgt = synth.tokens(C1["vocab"], m, C1["micro_batch"], C1["seq_len"], step=step)
+            losses.append(rt.step(tok, tgt))
+        res.append((losses, [rt.get_params(s, c) for s in range(p) for c in (1, 2)]))
+        st = rt.stats()
+        assert all(st["pool_high_water"][s] == plan.peak(s)["total_peak"] for s in range(p))
+        rt.close()
+    for r in res[1:]:
+        assert res[0][0] == r[0]
+        for a, b in zip(res[0][1], r[1]):
+            assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
