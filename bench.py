@@ -153,8 +153,23 @@ def cpu_baseline(c, seconds_cap=30.0):
     except Exception:
         blas = None
     cores = len(os.sched_getaffinity(0))
+    # SURVEY §8(d) "oracle timing beside the GPU": (i) the exact schedule simulator
+    # for p = 8, m = 32, all strategies; (ii) one full fp64 training step of C1
+    from oracle import schedule as S
+    t1 = time.perf_counter()
+    for st in ("tpipe", "tpipe_trecomp", "1f1b", "1f1b_full_recomp", "interleave", "interleave_trecomp"):
+        orders, v, rec, dur = S.strategy_orders(st, 8, 32)
+        S.simulate(orders, 8, v, dur, rec)
+    sim_s = time.perf_counter() - t1
+    W1 = synth.weights(8, 64, 256, 256, 32, seed=1)
+    tok1, tgt1 = synth.tokens(256, 8, 2, 32, step=0)
+    t2 = time.perf_counter()
+    R.step_grads(R.to64(W1), tok1, tgt1, 4)
+    c1_s = time.perf_counter() - t2
     return {"value": layer_tps / c["n_layers"], "unit": "tokens/s", "cores": cores,
             "blas_threads": blas, "kind": "oracle",
+            "schedule_sim_p8_m32_all_strategies_s": round(sim_s, 3),
+            "c1_fp64_step_s": round(c1_s, 3),
             "sample": f"{n} x (1 micro-batch fwd+bwd of 1 layer, h={h}, s={s}, fp64 NumPy) "
                       f"in {dt:.1f}s; model tokens/s = layer tokens/s / L={c['n_layers']}"}
 
