@@ -370,6 +370,35 @@ static int ln_fwd_warp(const bf16* x, const bf16* g, const bf16* b, bf16* y, flo
 // memory.
 constexpr int LNB_SMEM_ROWS_BYTES = 192 * 1024;
 
+// packed fp32x2 helpers (sm_100 FFMA2 / FADD2 / FMUL2)
+__device__ __forceinline__ uint64_t fpair(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void funpair(uint64_t r, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+// bf16x2 word (lo = element 0) -> (float lo, float hi)
+__device__ __forceinline__ uint64_t bfpair(uint32_t w) {
+    return fpair(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+}
+__device__ __forceinline__ uint64_t ffma2x(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t fadd2x(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ uint64_t fmul2x(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
@@ -397,14 +426,24 @@ ln_bwd_stage_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
         srs[threadIdx.x] = rstd[r0 + threadIdx.x];
     }
     __syncthreads();
-    float g[8], pg[8] = {}, pb[8] = {}, pr[8] = {};
-    Vec<bf16>::load(gamma + c, g);
+    // packed fp32x2 arithmetic (FFMA2 / FADD2 / FMUL2): the kernel is issue-bound
+    // (profiles/r1_hbm_kernels_ncu.txt), bf16 pairs unpack with one shift / mask each
+    uint64_t g2[4], pg2[4], pb2[4], pr2[4];
+    {
+        const uint4 gu = *reinterpret_cast<const uint4*>(gamma + c);
+        const uint32_t gw[4] = {gu.x, gu.y, gu.z, gu.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            g2[j] = bfpair(gw[j]);
+            pg2[j] = pb2[j] = pr2[j] = 0ull;
+        }
+    }
     for (int q0 = r0; q0 < r1; q0 += RC) {
         const int nr = min(RC, r1 - q0);
         // each thread fetches only the 16-byte slices it will read itself
-        // (cp.async, no registers held), so no CTA barrier is needed before use
-        // two commit groups (rows [0, half), [half, nr)): the first half's
-        // rows are processed and stored while the second half is still landing
+        // (cp.async, no registers held), so no CTA barrier is needed before use;
+        // two commit groups (rows [0, half), [half, nr)): the first half's rows
+        // are processed and stored while the second half is still landing
         const int half = (nr + 1) / 2;
         for (int i = grp; i < nr; i += G) {
             const long off = (long)(q0 + i) * h + c;
@@ -418,35 +457,58 @@ ln_bwd_stage_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
             if (i < half) asm volatile("cp.async.wait_group 1;" ::: "memory");
             else asm volatile("cp.async.wait_group 0;" ::: "memory");
             const int r = q0 + i;
-            float d[8], v[8], rr[8];
-            Vec<bf16>::load(sdy + (size_t)i * h + c, d);
-            Vec<bf16>::load(sx + (size_t)i * h + c, v);
+            const uint4 du = *reinterpret_cast<const uint4*>(sdy + (size_t)i * h + c);
+            const uint4 xu = *reinterpret_cast<const uint4*>(sx + (size_t)i * h + c);
+            const uint32_t dw[4] = {du.x, du.y, du.z, du.w}, xw[4] = {xu.x, xu.y, xu.z, xu.w};
+            uint64_t r2[4] = {0ull, 0ull, 0ull, 0ull};
             if (resid) {
-                Vec<bf16>::load(sr + (size_t)i * h + c, rr);
-            } else {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) rr[j] = 0.f;
+                const uint4 ru = *reinterpret_cast<const uint4*>(sr + (size_t)i * h + c);
+                r2[0] = bfpair(ru.x);
+                r2[1] = bfpair(ru.y);
+                r2[2] = bfpair(ru.z);
+                r2[3] = bfpair(ru.w);
             }
             const float mu = smu[r - r0], rs = srs[r - r0];
-            float xh[8], dxh[8], s1 = 0.f, s2 = 0.f;
+            const uint64_t rs2 = fpair(rs, rs), nm2 = fpair(-mu, -mu);
+            uint64_t xh2[4], dxh2[4], s1_2 = 0ull, s2_2 = 0ull;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                xh[j] = (v[j] - mu) * rs;
-                dxh[j] = d[j] * g[j];
-                s1 += dxh[j];
-                s2 += dxh[j] * xh[j];
-                pg[j] += d[j] * xh[j];
-                pb[j] += d[j];
-                pr[j] += rr[j];
+            for (int j = 0; j < 4; ++j) {
+                const uint64_t d2 = bfpair(dw[j]);
+                xh2[j] = fmul2x(fadd2x(bfpair(xw[j]), nm2), rs2);   // (x - mu) * rstd
+                dxh2[j] = fmul2x(d2, g2[j]);
+                s1_2 = fadd2x(s1_2, dxh2[j]);
+                s2_2 = ffma2x(dxh2[j], xh2[j], s2_2);
+                pg2[j] = ffma2x(d2, xh2[j], pg2[j]);
+                pb2[j] = fadd2x(pb2[j], d2);
+                if (resid) pr2[j] = fadd2x(pr2[j], r2[j]);
             }
+            float s1a, s1b, s2a, s2b;
+            funpair(s1_2, s1a, s1b);
+            funpair(s2_2, s2a, s2b);
+            float s1 = s1a + s1b, s2 = s2a + s2b;
             group_sum2(s1, s2, red[grp], grp, tpr);
             const float c1 = s1 / (float)h, c2 = s2 / (float)h;
-            float o[8];
+            const uint64_t nc1 = fpair(-c1, -c1), nc2 = fpair(-c2, -c2);
+            uint32_t ow[4];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) o[j] = rs * (dxh[j] - c1 - xh[j] * c2) + (resid ? rr[j] : 0.f);
-            Vec<bf16>::store(dx + (long)r * h + c, o);
+            for (int j = 0; j < 4; ++j) {
+                // rstd * (dxh - c1 - xh * c2) + resid
+                const uint64_t t = ffma2x(xh2[j], nc2, fadd2x(dxh2[j], nc1));
+                float o0, o1;
+                funpair(ffma2x(t, rs2, r2[j]), o0, o1);
+                __nv_bfloat162 hv = __floats2bfloat162_rn(o0, o1);
+                ow[j] = *reinterpret_cast<uint32_t*>(&hv);
+            }
+            *reinterpret_cast<uint4*>(dx + (long)r * h + c) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
         }
         __syncthreads();   // chunk buffer free for the next chunk / the combine below
+    }
+    float pg[8], pb[8], pr[8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        funpair(pg2[j], pg[2 * j], pg[2 * j + 1]);
+        funpair(pb2[j], pb[2 * j], pb[2 * j + 1]);
+        funpair(pr2[j], pr[2 * j], pr[2 * j + 1]);
     }
     // combine row groups in fixed order: p_0 + (p_1 + (... + p_{G-1}))
     for (int k = G - 1; k >= 1; --k) {
