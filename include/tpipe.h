@@ -92,8 +92,9 @@ enum {
 #define TPIPE_SOPT_SLICE_PARAMS 8388608
 
 typedef struct {
-    int32_t strategy;      /* TPIPE_S_*, or -1 = auto: escalate TPIPE -> TPIPE_TRECOMP ->
-                              TPIPE_TRECOMP + model-state offload until hbm_budget fits */
+    int32_t strategy;      /* TPIPE_S_*, or -1 = auto: escalate TPIPE -> TPIPE_TRECOMP with
+                              r = 1..n1 recomputed layers -> + model-state offload (r = 1..n1;
+                              DEVICE_OPT if requested in `offload`) until hbm_budget fits */
     int32_t delay_rounds;  /* T-Recomp k; -1 = App. B constraint as printed */
     int32_t send_window;   /* W, max in-flight sends per channel; 0 = default 2 (DESIGN R12) */
     int32_t offload;       /* TPIPE_OFFLOAD_* bitmask (explicit strategies); -1 = auto */
