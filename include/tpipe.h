@@ -51,6 +51,7 @@ extern "C" {
 #define TPIPE_E_NCCL       -8
 #define TPIPE_E_OOM        -9   /* runtime pool cap hit (a ledger bug) */
 #define TPIPE_E_STATE     -10   /* call not valid in the current state */
+#define TPIPE_E_TIMEOUT   -11   /* a transport wait or the step exceeded timeout_ms (peer hung) */
 
 #define TPIPE_FP32 0
 #define TPIPE_BF16 1
@@ -208,13 +209,39 @@ int tpipe_plan_stage_layers(const tpipe_plan* plan, int32_t stage, int32_t out[2
 int tpipe_plan_chunk_params(const tpipe_plan* plan, int32_t stage, int32_t chunk, uint64_t* n);
 
 /* ------------------------------------------------------------------ runtime */
+/* Stage transport of a one-stage-per-process runtime (stage >= 0, P:195/P:210
+ * pipeline P2P). Both carry the same FIFO channel messages with the
+ * plan's send window; see paper_2503_03182_b200/csrc/runtime/transport.h. */
+#define TPIPE_TRANSPORT_NCCL 0   /* ncclSend / ncclRecv, one 2-rank communicator per channel */
+#define TPIPE_TRANSPORT_IPC  1   /* CUDA IPC: copy-engine pull from the sender's pool arena,
+                                    interprocess events, POSIX-shm mailbox (`ipc_name`); works
+                                    across GPUs (NVLink peer access) and for several ranks on
+                                    one GPU (tests) */
+
+/* debug_flags */
+#define TPIPE_DEBUG_POOL_CANARY 1u  /* guard bytes after every pool allocation, checked after
+                                       each instruction: a kernel writing past a buffer's
+                                       planned bytes fails the step with TPIPE_E_STATE (slow) */
+#define TPIPE_DEBUG_POOL_CANARY_SELFTEST 2u  /* with POOL_CANARY: the first instruction that
+                                       allocates writes one byte past its first buffer (proves
+                                       the check fires; tests only) */
+
 typedef struct {
     int32_t stage;          /* stage executed by this process; -1 = all stages in-process
                                (virtual pipeline on one GPU, device-local transport) */
     int32_t device;         /* CUDA device ordinal */
-    const void* nccl_ids;   /* n_channels x 128-byte ncclUniqueId (stage >= 0, n_stages > 1) */
+    const void* nccl_ids;   /* n_channels x 128-byte ncclUniqueId (NCCL transport, stage >= 0,
+                               n_stages > 1) */
     uint64_t pool_cap;      /* hard cap of the HBM pool in bytes; 0 = plan peak of owned stages */
     float lr, beta1, beta2, eps, weight_decay;   /* AdamW (DESIGN R16); 0 -> defaults */
+    int32_t transport;      /* TPIPE_TRANSPORT_* (stage >= 0, n_stages > 1) */
+    int32_t timeout_ms;     /* bound on every transport wait and on the step's completion
+                               (TPIPE_E_TIMEOUT; NCCL asynchronous errors are polled meanwhile);
+                               0 = 300000 */
+    const char* ipc_name;   /* IPC transport: POSIX shm name ("/..."), the same string on the
+                               n_stages ranks of one job and unique per job; unlinked once
+                               every rank has attached */
+    uint32_t debug_flags;   /* TPIPE_DEBUG_* */
 } tpipe_runtime_opts;
 
 typedef struct {
@@ -235,6 +262,10 @@ typedef struct {
     /* copy-engine time of the last step's offload copies (sum of CUDA-event
      * spans on the D2H / H2D side streams, ms); bytes / ms = host-link GB/s */
     double   offload_d2h_ms, offload_h2d_ms;
+    /* physical bytes the pool had to place outside its arena (fragmentation
+     * overflow; 0 in a healthy run, TPIPE_E_OOM if it would exceed pool_cap) */
+    uint64_t pool_overflow_bytes;
+    int32_t  transport;             /* -1 virtual, else TPIPE_TRANSPORT_* in use */
 } tpipe_runtime_stats;
 
 typedef struct tpipe_runtime tpipe_runtime;

@@ -50,7 +50,9 @@ class SimReportMs(C.Structure):
 
 class RuntimeOpts(C.Structure):
     _fields_ = [("stage", i32), ("device", i32), ("nccl_ids", vp), ("pool_cap", u64),
-                ("lr", f32), ("beta1", f32), ("beta2", f32), ("eps", f32), ("weight_decay", f32)]
+                ("lr", f32), ("beta1", f32), ("beta2", f32), ("eps", f32), ("weight_decay", f32),
+                ("transport", i32), ("timeout_ms", i32), ("ipc_name", C.c_char_p),
+                ("debug_flags", u32)]
 
 
 class RuntimeStats(C.Structure):
@@ -59,7 +61,7 @@ class RuntimeStats(C.Structure):
                 ("offload_h2d_bytes", C.c_double), ("host_opt_ms", C.c_double),
                 ("kernel_ms", C.c_double * 4), ("kernel_flops", C.c_double * 4),
                 ("kernel_count", i64 * 4), ("offload_d2h_ms", C.c_double),
-                ("offload_h2d_ms", C.c_double)]
+                ("offload_h2d_ms", C.c_double), ("pool_overflow_bytes", u64), ("transport", i32)]
 
 
 def declare(L):

@@ -725,6 +725,7 @@ TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, in
             return set_error(TPIPE_E_BUDGET, "peak %llu bytes exceeds budget %llu",
                              (unsigned long long)pk, (unsigned long long)hbm_budget_bytes);
         }
+        P->hbm_budget = hbm_budget_bytes;
         *out = P;
         return 0;
     }
@@ -751,6 +752,7 @@ TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, in
         if (rc) return rc;
         best = max_peak(P);
         if (!hbm_budget_bytes || best <= hbm_budget_bytes) {
+            P->hbm_budget = hbm_budget_bytes;
             *out = P;
             return 0;
         }

@@ -18,6 +18,7 @@ struct tpipe_plan {
     std::vector<std::array<int, 2>> sl;
     int rl_of(int s) const { return rl < sl[s][0] ? rl : sl[s][0]; }
     uint64_t params_total = 0;
+    uint64_t hbm_budget = 0;   // per-stage budget the plan was fitted to (0 = none)
     // per stage
     std::vector<std::vector<tpipe_op>> ops;
     std::vector<std::vector<tpipe_buf>> bufs;

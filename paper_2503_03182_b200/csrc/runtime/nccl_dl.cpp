@@ -23,6 +23,8 @@ const NcclApi* nccl() {
         SYM(GroupStart, "ncclGroupStart");
         SYM(GroupEnd, "ncclGroupEnd");
         SYM(GetErrorString, "ncclGetErrorString");
+        SYM(CommGetAsyncError, "ncclCommGetAsyncError");
+        SYM(CommAbort, "ncclCommAbort");
 #undef SYM
         api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv &&
                  api.GroupStart && api.GroupEnd && api.GetErrorString;

@@ -35,8 +35,12 @@ void Pool::release() {
     req_.clear();
 }
 
+static constexpr unsigned char CANARY_BYTE = 0xA7;
+
 void* Pool::alloc(int stage, uint64_t bytes) {
-    const size_t need = std::max<size_t>(ALIGN, (bytes + ALIGN - 1) / ALIGN * ALIGN);
+    last_fail_phys_ = false;
+    const uint64_t phys = bytes + (canary_ ? CANARY : 0);
+    const size_t need = std::max<size_t>(ALIGN, (phys + ALIGN - 1) / ALIGN * ALIGN);
     // best fit
     auto best = free_.end();
     for (auto it = free_.begin(); it != free_.end(); ++it)
@@ -50,13 +54,18 @@ void* Pool::alloc(int stage, uint64_t bytes) {
         used_[p] = {off, need};
     } else {
         // arena exhausted by fragmentation: dedicated block (physical only; the
-        // ledger below is unaffected)
+        // ledger below is unaffected), bounded by the physical limit
+        if (phys_limit_ && std::max(cap_, phys_limit_) < cap_ + overflow_bytes_ + need) {
+            last_fail_phys_ = true;
+            return nullptr;
+        }
         if (cudaMalloc(&p, need) != cudaSuccess) return nullptr;
         overflow_.push_back(p);
         overflow_bytes_ += need;
         used_[p] = {SIZE_MAX, need};
     }
     req_[p] = bytes;
+    if (canary_) cudaMemsetAsync((char*)p + bytes, CANARY_BYTE, CANARY, canary_st_);
     cur_[stage] += bytes;
     hw_[stage] = std::max(hw_[stage], cur_[stage]);
     if (limit_[stage] && cur_[stage] > limit_[stage]) over_cap_ = true;
@@ -91,6 +100,22 @@ void Pool::free(int stage, void* p) {
         }
     }
     free_[o] = s;
+}
+
+void* Pool::check_canaries(cudaStream_t st, uint64_t* req_bytes) {
+    if (!canary_) return nullptr;
+    cudaStreamSynchronize(st);
+    std::vector<unsigned char> g(CANARY);
+    for (auto& kv : req_) {
+        if (cudaMemcpy(g.data(), (char*)kv.first + kv.second, CANARY, cudaMemcpyDeviceToHost) != cudaSuccess)
+            return kv.first;
+        for (unsigned char x : g)
+            if (x != CANARY_BYTE) {
+                if (req_bytes) *req_bytes = kv.second;
+                return kv.first;
+            }
+    }
+    return nullptr;
 }
 
 }  // namespace tpipe

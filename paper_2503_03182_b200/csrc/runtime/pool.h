@@ -30,8 +30,25 @@ public:
         for (size_t s = 0; s < hw_.size(); ++s) hw_[s] = cur_[s];
     }
     size_t reserved() const { return cap_ + overflow_bytes_; }
+    size_t overflow_bytes() const { return overflow_bytes_; }
     void set_cap(int stage, uint64_t cap) { limit_[stage] = cap; }
     bool over_cap() const { return over_cap_; }
+    // the arena (exported to peer ranks by the IPC transport)
+    void* arena() const { return base_; }
+    size_t arena_bytes() const { return cap_; }
+    // physical bound: a fragmentation overflow block may be cudaMalloc'ed
+    // only while arena + overflow stays within `bytes` (0 = unbounded); beyond
+    // it alloc() fails (the runtime reports TPIPE_E_OOM) instead of silently
+    // exceeding the HBM budget the plan was made for
+    void set_phys_limit(size_t bytes) { phys_limit_ = bytes; }
+    bool last_fail_physical() const { return last_fail_phys_; }
+    // debug canaries (TPIPE_DEBUG_POOL_CANARY): CANARY guard bytes of a fixed
+    // pattern right after each allocation's requested bytes, written on
+    // `st` at alloc; check_canaries() returns the first live allocation whose
+    // guard changed (nullptr if none), after synchronising `st`
+    static constexpr size_t CANARY = 512;
+    void set_canary(bool on, cudaStream_t st) { canary_ = on; canary_st_ = st; }
+    void* check_canaries(cudaStream_t st, uint64_t* req_bytes);
 
 private:
     char* base_ = nullptr;
@@ -43,6 +60,10 @@ private:
     size_t overflow_bytes_ = 0;
     std::vector<uint64_t> cur_, hw_, limit_;
     bool over_cap_ = false;
+    size_t phys_limit_ = 0;
+    bool last_fail_phys_ = false;
+    bool canary_ = false;
+    cudaStream_t canary_st_ = nullptr;
 };
 
 }  // namespace tpipe

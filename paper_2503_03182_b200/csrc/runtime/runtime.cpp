@@ -4,10 +4,11 @@
 // * Every buffer is allocated from the HBM pool at the instruction the plan
 //   names and released at the instruction the plan names, so the pool's
 //   ledger high-water equals the plan's byte-exact peak (tpipe_plan_stage_peak).
-// * Transport: stage >= 0 -> one process per GPU, one 2-rank NCCL
-//   communicator + stream per FIFO channel (kind, src, dst), send window by
-//   SEND_WAIT events; stage == -1 -> all stages in this process on one GPU
-//   with device-to-device copies (a virtual pipeline used for parity tests).
+// * Transport (runtime/transport.h): stage >= 0 -> one process per stage
+//   (one GPU each, or several on one GPU for tests), FIFO channels over NCCL
+//   send/recv or CUDA IPC copy-engine pulls, send window by SEND_WAIT;
+//   stage == -1 -> all stages in this process on one GPU with
+//   device-to-device copies (a virtual pipeline used for parity tests).
 // * T-Offload: GRAD_D2H on a copy-engine stream, HOST_OPT on a host
 //   thread (bit-identical AdamW), W_H2D on a second copy stream in the next
 //   step's warm-up, W_WAIT before the first deep-chunk forward.
@@ -31,6 +32,7 @@
 #include "runtime/nccl_dl.h"
 #include "runtime/pool.h"
 #include "runtime/stage.h"
+#include "runtime/transport.h"
 #include "tpipe.h"
 
 
@@ -93,15 +95,6 @@ struct StageState {
     std::map<int, cudaEvent_t> act_ev_d2h, act_ev_h2d;
 };
 
-struct Channel {
-    int kind = 0, src = 0, dst = 0;
-    std::deque<void*> q;  // virtual transport: sender buffers in FIFO order
-    int popped = 0;
-    ncclComm_t comm = nullptr;
-    cudaStream_t st = nullptr;
-    std::vector<cudaEvent_t> send_done;
-};
-
 }  // namespace
 
 struct tpipe_runtime {
@@ -110,7 +103,11 @@ struct tpipe_runtime {
     Dims D;
     std::vector<int> owned;
     std::vector<std::unique_ptr<StageState>> st;   // indexed by stage (null if not owned)
-    std::vector<Channel> ch;
+    std::unique_ptr<Transport> tr;
+    int transport_kind = -1;           // -1 virtual, else TPIPE_TRANSPORT_*
+    int timeout_ms = 300000;
+    uint32_t debug = 0;
+    bool selftest_done = false;
     Pool pool;
     cudaStream_t stream = nullptr, d2h = nullptr, h2d = nullptr, opt = nullptr;
     cudaEvent_t ev_tmp = nullptr;
@@ -301,6 +298,10 @@ int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags
     for (int e = 0; e < op.n_alloc; ++e) {
         const int id = ev[op.alloc_first + e];
         void* ptr = rt->pool.alloc(s, bufs[id].bytes);
+        if (!ptr && rt->pool.last_fail_physical())
+            return set_error(TPIPE_E_OOM, "stage %d: pool fragmentation would place %llu bytes beyond the "
+                             "HBM budget (arena %zu + overflow %zu)", s, (unsigned long long)bufs[id].bytes,
+                             rt->pool.arena_bytes(), rt->pool.overflow_bytes());
         if (!ptr) return set_error(TPIPE_E_CUDA, "pool allocation of %llu bytes failed",
                                    (unsigned long long)bufs[id].bytes);
         S.bufptr[id] = ptr;
@@ -308,6 +309,11 @@ int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags
     }
     if (rt->pool.over_cap())
         return set_error(TPIPE_E_OOM, "stage %d ledger exceeds the plan peak (ledger bug)", s);
+    if ((rt->debug & TPIPE_DEBUG_POOL_CANARY_SELFTEST) && !rt->selftest_done && op.n_alloc > 0) {
+        const int id = ev[op.alloc_first];
+        CU(cudaMemsetAsync((uint8_t*)S.bufptr[id] + bufs[id].bytes, 0x5A, 1, cs));
+        rt->selftest_done = true;
+    }
 
     const int c = op.chunk, i = op.mb;
     switch (op.kind) {
@@ -390,55 +396,22 @@ int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags
         }
         case TPIPE_OP_RECV_ACT:
         case TPIPE_OP_RECV_GRAD: {
-            Channel& chn = rt->ch[op.channel];
             void* dst = nullptr;
             op_alloc_ptr(rt, S, op, op.kind == TPIPE_OP_RECV_ACT ? TPIPE_BUF_IN : TPIPE_BUF_GIN, -1, &dst);
-            const size_t bytes = (size_t)D.M * D.h * D.es;
-            if (rt->stage_sel < 0) {
-                void* src = chn.q.front();
-                chn.q.pop_front();
-                chn.popped++;
-                CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, cs));
-            } else {
-                const NcclApi* N = nccl();
-                cudaEvent_t e0 = next_event(rt), e1 = next_event(rt);
-                CU(cudaEventRecord(e0, cs));
-                CU(cudaStreamWaitEvent(chn.st, e0, 0));
-                ncclResult_t r = N->Recv(dst, bytes, ncclUint8, 0, chn.comm, chn.st);
-                if (r != ncclSuccess) return set_error(TPIPE_E_NCCL, "ncclRecv: %s", N->GetErrorString(r));
-                CU(cudaEventRecord(e1, chn.st));
-                CU(cudaStreamWaitEvent(cs, e1, 0));
-            }
+            if (!dst) return set_error(TPIPE_E_STATE, "stage %d RECV: receive buffer missing", s);
+            TRY(rt->tr->recv(op.channel, dst, (size_t)D.M * D.h * D.es, cs));
             break;
         }
         case TPIPE_OP_SEND_ACT:
         case TPIPE_OP_SEND_GRAD: {
-            Channel& chn = rt->ch[op.channel];
             void* src = live_get(S, TPIPE_BUF_MSG, op.channel, op.msg);
             if (!src) return set_error(TPIPE_E_STATE, "send buffer missing");
-            const size_t bytes = (size_t)D.M * D.h * D.es;
-            if (rt->stage_sel < 0) {
-                chn.q.push_back(src);
-            } else {
-                const NcclApi* N = nccl();
-                cudaEvent_t e0 = next_event(rt);
-                CU(cudaEventRecord(e0, cs));
-                CU(cudaStreamWaitEvent(chn.st, e0, 0));
-                ncclResult_t r = N->Send(src, bytes, ncclUint8, 1, chn.comm, chn.st);
-                if (r != ncclSuccess) return set_error(TPIPE_E_NCCL, "ncclSend: %s", N->GetErrorString(r));
-                if ((int)chn.send_done.size() <= op.msg) chn.send_done.resize(op.msg + 1, nullptr);
-                chn.send_done[op.msg] = next_event(rt);
-                CU(cudaEventRecord(chn.send_done[op.msg], chn.st));
-            }
+            TRY(rt->tr->send(op.channel, op.msg, src, (size_t)D.M * D.h * D.es, cs));
             break;
         }
-        case TPIPE_OP_SEND_WAIT: {
-            if (rt->stage_sel >= 0) {
-                Channel& chn = rt->ch[op.channel];
-                CU(cudaStreamWaitEvent(cs, chn.send_done[op.msg], 0));
-            }
+        case TPIPE_OP_SEND_WAIT:
+            TRY(rt->tr->send_wait(op.channel, op.msg, cs));
             break;
-        }
         case TPIPE_OP_OPT:
             if (!no_opt) TRY(adam_chunk(rt, S.ch[c], hyper(rt, rt->t + 1), cs));
             break;
@@ -533,6 +506,23 @@ int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags
             return set_error(TPIPE_E_STATE, "unknown op kind %d", op.kind);
     }
 
+    // debug: a kernel of this instruction wrote past a buffer's planned bytes
+    if (rt->debug & TPIPE_DEBUG_POOL_CANARY) {
+        uint64_t rb = 0;
+        if (void* bad = rt->pool.check_canaries(cs, &rb)) {
+            int role = -1, chunk = -1, mb = -1;
+            for (int s2 : rt->owned)
+                for (size_t id = 0; id < rt->st[s2]->bufptr.size(); ++id)
+                    if (rt->st[s2]->bufptr[id] == bad) {
+                        role = P.bufs[s2][id].role;
+                        chunk = P.bufs[s2][id].chunk;
+                        mb = P.bufs[s2][id].mb;
+                    }
+            return set_error(TPIPE_E_STATE, "pool canary: stage %d op kind %d (chunk %d, mb %d) overran a "
+                             "%llu-byte buffer (role %d, chunk %d, mb %d)", s, op.kind, op.chunk, op.mb,
+                             (unsigned long long)rb, role, chunk, mb);
+        }
+    }
     // releases at instruction end
     for (int e = 0; e < op.n_free; ++e) {
         const int id = ev[op.free_first + e];
@@ -544,13 +534,23 @@ int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags
 }
 
 bool op_ready(tpipe_runtime* rt, const tpipe_op& op) {
-    if (rt->stage_sel >= 0) return true;
-    if (op.kind == TPIPE_OP_RECV_ACT || op.kind == TPIPE_OP_RECV_GRAD) return !rt->ch[op.channel].q.empty();
-    if (op.kind == TPIPE_OP_SEND_WAIT) return rt->ch[op.channel].popped > op.msg;
+    if (op.kind == TPIPE_OP_RECV_ACT || op.kind == TPIPE_OP_RECV_GRAD) return rt->tr->recv_ready(op.channel);
+    if (op.kind == TPIPE_OP_SEND_WAIT) return rt->tr->send_wait_ready(op.channel, op.msg);
     return true;
 }
 
+int run_step_impl(tpipe_runtime* rt, const int32_t* tok_dev, const int32_t* tgt_dev, uint32_t flags,
+                  float* loss_out);
+
+// a failed step releases peers blocked on this rank (IPC abort flag)
 int run_step(tpipe_runtime* rt, const int32_t* tok_dev, const int32_t* tgt_dev, uint32_t flags,
+             float* loss_out) {
+    const int rc = run_step_impl(rt, tok_dev, tgt_dev, flags, loss_out);
+    if (rc && rt->tr) rt->tr->abort();
+    return rc;
+}
+
+int run_step_impl(tpipe_runtime* rt, const int32_t* tok_dev, const int32_t* tgt_dev, uint32_t flags,
              float* loss_out) {
     const auto& P = rt->plan;
     const Dims& D = rt->D;
@@ -572,11 +572,7 @@ int run_step(tpipe_runtime* rt, const int32_t* tok_dev, const int32_t* tgt_dev, 
             CU(cudaMemsetAsync(S.loss_slots, 0, (size_t)P.m * 4, cs));
         }
     }
-    for (auto& c : rt->ch) {
-        c.q.clear();
-        c.popped = 0;
-        c.send_done.clear();
-    }
+    rt->tr->begin_step();
     size_t remaining = 0;
     for (int s : rt->owned) remaining += P.ops[s].size();
     const bool op_times = (flags & TPIPE_STEP_OP_TIMES) != 0;
@@ -613,10 +609,10 @@ int run_step(tpipe_runtime* rt, const int32_t* tok_dev, const int32_t* tgt_dev, 
         std::vector<float> slots(P.m);
         CU(cudaMemcpyAsync(slots.data(), rt->st[P.p - 1]->loss_slots, (size_t)P.m * 4,
                            cudaMemcpyDeviceToHost, cs));
-        CU(cudaStreamSynchronize(cs));
+        TRY(rt->tr->sync(cs, rt->timeout_ms));
         for (float x : slots) loss += x;   // micro-batch index order
     } else {
-        CU(cudaStreamSynchronize(cs));
+        TRY(rt->tr->sync(cs, rt->timeout_ms));
     }
     if (loss_out) *loss_out = loss;
     if (flags & TPIPE_STEP_PROFILE) {
@@ -633,6 +629,54 @@ int run_step(tpipe_runtime* rt, const int32_t* tok_dev, const int32_t* tgt_dev, 
     }
     if (!(flags & TPIPE_STEP_NO_OPT)) rt->t += 1;
     rt->launches_last = launch_count() - l0;
+    return 0;
+}
+
+// Every buffer the plan sizes must equal what the kernels carve out of it
+// (StashLayout for STASH / TSTASH / RBUF, chunk_forward / chunk_backward for
+// the workspaces): the byte model and the layouts are written separately,
+// and a drift would silently overrun a neighbouring pool block.
+int check_layouts(const tpipe_plan& P, const std::vector<int>& owned) {
+    const Dims D(P.model);
+    const bool full = P.strategy == TPIPE_S_1F1B_FULL_RECOMP;
+    const bool trecomp = P.strategy == TPIPE_S_TPIPE_TRECOMP || P.strategy == TPIPE_S_INTERLEAVE_TRECOMP;
+    for (int s : owned) {
+        for (const tpipe_op& op : P.ops[s]) {
+            for (int e = 0; e < op.n_alloc; ++e) {
+                const tpipe_buf& b = P.bufs[s][P.events[s][op.alloc_first + e]];
+                if (b.role == TPIPE_BUF_STATIC || b.role == TPIPE_BUF_IN || b.role == TPIPE_BUF_GIN ||
+                    b.role == TPIPE_BUF_MSG)
+                    continue;
+                const int c = b.chunk;
+                const bool emb = (s == 0 && c == 1), head = (s == P.p - 1 && c == P.v);
+                const StashLayout SL = make_stash_layout(P.model, P.sl[s][c - 1], emb, head, full);
+                const int split = (trecomp && c == 1 && P.rl_of(s) < P.sl[s][0]) ? P.rl_of(s) : 0;
+                const uint64_t front = split ? (uint64_t)SL.layer[split].x_in : (uint64_t)SL.total;
+                uint64_t want = 0;
+                const char* what = "";
+                switch (b.role) {
+                    case TPIPE_BUF_STASH:   // kept part [split, n) under partial T-Recomp
+                        want = split ? (uint64_t)SL.total - front : (uint64_t)SL.total;
+                        what = "stash";
+                        break;
+                    case TPIPE_BUF_TSTASH:
+                    case TPIPE_BUF_RBUF:
+                        want = front;
+                        what = b.role == TPIPE_BUF_RBUF ? "recompute buffer" : "transient stash";
+                        break;
+                    case TPIPE_BUF_WS:
+                        want = op.kind == TPIPE_OP_B ? bwd_ws_bytes(D, SL, head, emb) : fwd_ws_bytes(D, SL, head);
+                        what = op.kind == TPIPE_OP_B ? "backward workspace" : "forward workspace";
+                        break;
+                    default:
+                        continue;
+                }
+                if (b.bytes != want)
+                    return set_error(TPIPE_E_STATE, "stage %d chunk %d: plan %s %llu bytes != kernel layout %llu",
+                                     s, c, what, (unsigned long long)b.bytes, (unsigned long long)want);
+            }
+        }
+    }
     return 0;
 }
 
@@ -674,6 +718,13 @@ TP_API int tpipe_runtime_create(const tpipe_plan* plan, const tpipe_runtime_opts
     for (int s : rt->owned) need += P.peak[s].total_peak;
     if (rt->pool.init((size_t)(need * 1.08) + (256ull << 20), P.p))
         return set_error(TPIPE_E_CUDA, "pool: cudaMalloc of %llu bytes failed", (unsigned long long)need);
+    if (P.hbm_budget) rt->pool.set_phys_limit((size_t)P.hbm_budget * rt->owned.size());
+    rt->debug = o.debug_flags;
+    rt->timeout_ms = o.timeout_ms > 0 ? o.timeout_ms : 300000;
+    rt->pool.set_canary((o.debug_flags & TPIPE_DEBUG_POOL_CANARY) != 0, rt->stream);
+    // the kernels' buffer carve-ups must equal the plan's byte model (a drift
+    // would overrun a neighbouring pool block): checked once per stage / chunk
+    TRY(check_layouts(P, rt->owned));
     rt->st.resize(P.p);
     const bool off = (P.offload & TPIPE_OFFLOAD_MODEL_STATE) != 0;
     const bool sopt = off && (P.offload & TPIPE_OFFLOAD_DEVICE_OPT) != 0;
@@ -745,31 +796,20 @@ TP_API int tpipe_runtime_create(const tpipe_plan* plan, const tpipe_runtime_opts
         }
         rt->st[s] = std::move(S);
     }
-    // channels
-    rt->ch.resize(P.channels.size());
-    for (size_t c = 0; c < P.channels.size(); ++c) {
-        rt->ch[c].kind = P.channels[c][0];
-        rt->ch[c].src = P.channels[c][1];
-        rt->ch[c].dst = P.channels[c][2];
-    }
-    if (o.stage >= 0 && P.p > 1) {
-        const NcclApi* N = nccl();
-        if (!N) return set_error(TPIPE_E_NCCL, "libnccl.so.2 not loadable");
-        if (!o.nccl_ids) return set_error(TPIPE_E_INVALID, "nccl_ids required for stage >= 0");
-        const ncclUniqueId* ids = (const ncclUniqueId*)o.nccl_ids;
-        N->GroupStart();
-        for (size_t c = 0; c < rt->ch.size(); ++c) {
-            Channel& chn = rt->ch[c];
-            if (chn.src != o.stage && chn.dst != o.stage) continue;
-            CU(cudaStreamCreateWithFlags(&chn.st, cudaStreamNonBlocking));
-            ncclResult_t r = N->CommInitRank(&chn.comm, 2, ids[c], chn.src == o.stage ? 0 : 1);
-            if (r != ncclSuccess && r != ncclInProgress) {
-                N->GroupEnd();
-                return set_error(TPIPE_E_NCCL, "ncclCommInitRank: %s", N->GetErrorString(r));
-            }
-        }
-        ncclResult_t r = N->GroupEnd();
-        if (r != ncclSuccess) return set_error(TPIPE_E_NCCL, "ncclGroupEnd: %s", N->GetErrorString(r));
+    // stage transport (runtime/transport.h)
+    CU(cudaDeviceSynchronize());   // static buffers initialised before peers map the arena
+    if (o.stage < 0 || P.p == 1) {
+        rt->tr = make_virtual_transport(P.channels);
+        rt->transport_kind = -1;
+    } else if (o.transport == TPIPE_TRANSPORT_IPC) {
+        TRY(make_ipc_transport(P.channels, P.p, o.stage, o.device, o.ipc_name, rt->pool.arena(),
+                               rt->pool.arena_bytes(), P.W, rt->timeout_ms, &rt->tr));
+        rt->transport_kind = TPIPE_TRANSPORT_IPC;
+    } else if (o.transport == TPIPE_TRANSPORT_NCCL) {
+        TRY(make_nccl_transport(P.channels, o.stage, o.nccl_ids, rt->timeout_ms, &rt->tr));
+        rt->transport_kind = TPIPE_TRANSPORT_NCCL;
+    } else {
+        return set_error(TPIPE_E_INVALID, "transport %d", o.transport);
     }
     CU(cudaDeviceSynchronize());
     *out = rt.release();
@@ -796,11 +836,7 @@ TP_API void tpipe_runtime_destroy(tpipe_runtime* rt) {
             if (C.ev_sopt_out) cudaEventDestroy(C.ev_sopt_out);
         }
     }
-    if (const NcclApi* N = nccl())
-        for (auto& c : rt->ch)
-            if (c.comm) N->CommDestroy(c.comm);
-    for (auto& c : rt->ch)
-        if (c.st) cudaStreamDestroy(c.st);
+    rt->tr.reset();
     for (auto e : rt->evpool) cudaEventDestroy(e);
     for (auto e : rt->tevpool) cudaEventDestroy(e);
     if (rt->h_tok_stage) cudaFreeHost(rt->h_tok_stage);
@@ -931,6 +967,8 @@ TP_API int tpipe_runtime_get_stats(const tpipe_runtime* rt, tpipe_runtime_stats*
     };
     out->offload_d2h_ms = span_ms(rt->d2h_ev);
     out->offload_h2d_ms = span_ms(rt->h2d_ev);
+    out->pool_overflow_bytes = rt->pool.overflow_bytes();
+    out->transport = rt->transport_kind;
     for (int c = 0; c < 4; ++c) {
         out->kernel_ms[c] = rt->kms[c];
         out->kernel_flops[c] = rt->kflops[c];

@@ -297,6 +297,7 @@ struct BwdWs {
     float* logits;
     void* dlogits;
     int* emb_ws;
+    long total;     // bytes carved (== the plan's ws_b; checked at runtime creation)
 };
 
 static BwdWs carve_bwd(const Dims& D, uint8_t* ws, bool head, bool emb, long part_elems,
@@ -329,7 +330,25 @@ static BwdWs carve_bwd(const Dims& D, uint8_t* ws, bool head, bool emb, long par
         w.dlogits = take(M * D.V * es);
     }
     w.emb_ws = emb ? reinterpret_cast<int*>(take(8 * M)) : nullptr;
+    w.total = off;
     return w;
+}
+
+static long part_elems(const Dims& D) {
+    // column-partial workspace: b1 [nb][f] + LN2 [3][nb][h], or bqkv [nb][3h] + LN1 [3][nb][h]
+    const long nb = (D.M + 15) / 16;
+    return nb * (D.f + 3L * D.h > 6L * D.h ? D.f + 3L * D.h : 6L * D.h);
+}
+
+uint64_t bwd_ws_bytes(const Dims& D, const StashLayout& SL, bool head, bool emb) {
+    return (uint64_t)carve_bwd(D, nullptr, head, emb, part_elems(D), SL.ckpt_only ? SL.scratch_bytes : 0).total;
+}
+
+// chunk_forward's workspace: [ln out M·h | gelu out M·f | full recompute: one
+// layer's internals | head: LN_f out M·h]
+uint64_t fwd_ws_bytes(const Dims& D, const StashLayout& SL, bool head) {
+    return (uint64_t)D.M * (D.h + D.f) * D.es + (SL.ckpt_only ? SL.scratch_bytes : 0) +
+           (head ? (uint64_t)D.M * D.h * D.es : 0);
 }
 
 // Side stream for the backward of a layer: weight-gradient GEMMs (and the LN
@@ -532,9 +551,7 @@ int chunk_backward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P
     const ParamLayout& lay = *P.lay;
     const int n = (int)lay.layer.size();
     const long M = D.M, h = D.h;
-    // column-partial workspace: b1 [nb][f] + LN2 [3][nb][h], or bqkv [nb][3h] + LN1 [3][nb][h]
-    const long part = ((M + 15) / 16) * (D.f + 3 * h > 6 * h ? D.f + 3 * h : 6 * h);
-    BwdWs w = carve_bwd(D, a.ws, lay.head, lay.emb, part, SL.ckpt_only ? SL.scratch_bytes : 0);
+    BwdWs w = carve_bwd(D, a.ws, lay.head, lay.emb, part_elems(D), SL.ckpt_only ? SL.scratch_bytes : 0);
     const uint8_t* wb = reinterpret_cast<const uint8_t*>(P.w);
     const void* dy = a.gin;
     if (lay.head) {

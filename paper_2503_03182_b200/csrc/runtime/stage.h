@@ -107,6 +107,11 @@ struct KernelProfiler {
 };
 KernelProfiler& profiler();
 
+// workspace bytes chunk_forward / chunk_backward carve (must equal the plan's
+// ws_f / ws_b: tpipe_runtime_create checks every (stage, chunk))
+uint64_t fwd_ws_bytes(const Dims& D, const StashLayout& SL, bool head);
+uint64_t bwd_ws_bytes(const Dims& D, const StashLayout& SL, bool head, bool emb);
+
 int chunk_forward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P, const FwdArgs& a,
                   cudaStream_t st);
 // layer backward: run weight-gradient GEMMs on a side stream (default on;

@@ -1,0 +1,486 @@
+// Stage transport implementations (see transport.h).
+#include "runtime/transport.h"
+
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <atomic>
+#include <chrono>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <thread>
+
+#include "runtime/errors.h"
+#include "runtime/nccl_dl.h"
+#include "tpipe.h"
+
+namespace tpipe {
+
+using Clock = std::chrono::steady_clock;
+
+static double ms_since(Clock::time_point t0) {
+    return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+}
+
+// poll-wait: spin briefly, then sleep in short steps (the waits are on other
+// processes' host progress, normally microseconds to milliseconds)
+template <typename Pred, typename Abort>
+static int poll_until(Pred pred, Abort aborted, int timeout_ms, const char* what) {
+    const auto t0 = Clock::now();
+    for (int it = 0;; ++it) {
+        if (pred()) return 0;
+        if (aborted()) return set_error(TPIPE_E_STATE, "%s: a peer rank aborted", what);
+        if (it > 256) {
+            if (ms_since(t0) > timeout_ms)
+                return set_error(TPIPE_E_TIMEOUT, "%s: timed out after %d ms", what, timeout_ms);
+            std::this_thread::sleep_for(std::chrono::microseconds(it < 4096 ? 2 : 50));
+        }
+    }
+}
+
+int Transport::sync(cudaStream_t cs, int timeout_ms) {
+    const auto t0 = Clock::now();
+    for (;;) {
+        cudaError_t e = cudaStreamQuery(cs);
+        if (e == cudaSuccess) return 0;
+        if (e != cudaErrorNotReady)
+            return set_error(TPIPE_E_CUDA, "step stream: %s", cudaGetErrorString(e));
+        if (ms_since(t0) > timeout_ms)
+            return set_error(TPIPE_E_TIMEOUT, "step did not complete within %d ms", timeout_ms);
+        std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+}
+
+// ================================================================ virtual
+namespace {
+
+class VirtualTransport final : public Transport {
+public:
+    explicit VirtualTransport(size_t n) : q_(n), popped_(n, 0) {}
+    const char* name() const override { return "virtual"; }
+    void begin_step() override {
+        for (auto& q : q_) q.clear();
+        for (auto& n : popped_) n = 0;
+    }
+    int send(int ch, int, const void* src, size_t, cudaStream_t) override {
+        q_[ch].push_back(src);
+        return 0;
+    }
+    int recv(int ch, void* dst, size_t bytes, cudaStream_t cs) override {
+        if (q_[ch].empty()) return set_error(TPIPE_E_STATE, "virtual recv on an empty channel %d", ch);
+        const void* src = q_[ch].front();
+        q_[ch].pop_front();
+        popped_[ch]++;
+        cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, cs);
+        return e == cudaSuccess ? 0 : set_error(TPIPE_E_CUDA, "virtual recv copy: %s", cudaGetErrorString(e));
+    }
+    // single stream: the copy above is ordered before any later reuse of src
+    int send_wait(int, int, cudaStream_t) override { return 0; }
+    bool recv_ready(int ch) const override { return !q_[ch].empty(); }
+    bool send_wait_ready(int ch, int msg) const override { return popped_[ch] > msg; }
+
+private:
+    std::vector<std::deque<const void*>> q_;
+    std::vector<int> popped_;
+};
+
+// ================================================================ nccl
+class NcclTransport final : public Transport {
+public:
+    struct Ch {
+        ncclComm_t comm = nullptr;
+        cudaStream_t st = nullptr;
+        std::vector<cudaEvent_t> done;   // per message of the step
+    };
+    ~NcclTransport() override {
+        const NcclApi* N = nccl();
+        for (auto& c : ch_) {
+            if (c.comm && N) {
+                if (aborted_ && N->CommAbort) N->CommAbort(c.comm);
+                else N->CommDestroy(c.comm);
+            }
+            if (c.st) cudaStreamDestroy(c.st);
+        }
+        for (auto e : ev_) cudaEventDestroy(e);
+    }
+    const char* name() const override { return "nccl"; }
+    void begin_step() override {
+        evnext_ = 0;
+        for (auto& c : ch_) c.done.clear();
+    }
+    cudaEvent_t ev() {
+        if (evnext_ == ev_.size()) {
+            cudaEvent_t e;
+            cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+            ev_.push_back(e);
+        }
+        return ev_[evnext_++];
+    }
+    int send(int ch, int msg, const void* src, size_t bytes, cudaStream_t cs) override {
+        Ch& c = ch_[ch];
+        const NcclApi* N = nccl();
+        cudaEvent_t e0 = ev();
+        if (cudaEventRecord(e0, cs) || cudaStreamWaitEvent(c.st, e0, 0))
+            return set_error(TPIPE_E_CUDA, "nccl send: event");
+        ncclResult_t r = N->Send(src, bytes, ncclUint8, 1, c.comm, c.st);
+        if (r != ncclSuccess) return set_error(TPIPE_E_NCCL, "ncclSend: %s", N->GetErrorString(r));
+        if ((int)c.done.size() <= msg) c.done.resize(msg + 1, nullptr);
+        c.done[msg] = ev();
+        if (cudaEventRecord(c.done[msg], c.st)) return set_error(TPIPE_E_CUDA, "nccl send: event");
+        return 0;
+    }
+    int recv(int ch, void* dst, size_t bytes, cudaStream_t cs) override {
+        Ch& c = ch_[ch];
+        const NcclApi* N = nccl();
+        cudaEvent_t e0 = ev(), e1 = ev();
+        if (cudaEventRecord(e0, cs) || cudaStreamWaitEvent(c.st, e0, 0))
+            return set_error(TPIPE_E_CUDA, "nccl recv: event");
+        ncclResult_t r = N->Recv(dst, bytes, ncclUint8, 0, c.comm, c.st);
+        if (r != ncclSuccess) return set_error(TPIPE_E_NCCL, "ncclRecv: %s", N->GetErrorString(r));
+        if (cudaEventRecord(e1, c.st) || cudaStreamWaitEvent(cs, e1, 0))
+            return set_error(TPIPE_E_CUDA, "nccl recv: event");
+        return 0;
+    }
+    int send_wait(int ch, int msg, cudaStream_t cs) override {
+        Ch& c = ch_[ch];
+        if (msg >= (int)c.done.size() || !c.done[msg])
+            return set_error(TPIPE_E_STATE, "SEND_WAIT(%d) on channel %d before its SEND", msg, ch);
+        return cudaStreamWaitEvent(cs, c.done[msg], 0) ? set_error(TPIPE_E_CUDA, "send_wait") : 0;
+    }
+    // step completion with asynchronous-error polling (a failed or hung peer
+    // surfaces as an error instead of a silent hang)
+    int sync(cudaStream_t cs, int timeout_ms) override {
+        const NcclApi* N = nccl();
+        const auto t0 = Clock::now();
+        for (;;) {
+            cudaError_t e = cudaStreamQuery(cs);
+            if (e == cudaSuccess) return 0;
+            if (e != cudaErrorNotReady) return set_error(TPIPE_E_CUDA, "step stream: %s", cudaGetErrorString(e));
+            for (auto& c : ch_) {
+                if (!c.comm) continue;
+                ncclResult_t ae = ncclSuccess;
+                if (N->CommGetAsyncError && N->CommGetAsyncError(c.comm, &ae) == ncclSuccess &&
+                    ae != ncclSuccess && ae != ncclInProgress) {
+                    abort();
+                    return set_error(TPIPE_E_NCCL, "NCCL asynchronous error: %s", N->GetErrorString(ae));
+                }
+            }
+            if (ms_since(t0) > timeout_ms) {
+                abort();
+                return set_error(TPIPE_E_TIMEOUT, "step did not complete within %d ms (NCCL peers hung?)",
+                                 timeout_ms);
+            }
+            std::this_thread::sleep_for(std::chrono::microseconds(50));
+        }
+    }
+    void abort() override { aborted_ = true; }
+
+    std::vector<Ch> ch_;
+    std::vector<cudaEvent_t> ev_;
+    size_t evnext_ = 0;
+    bool aborted_ = false;
+};
+
+// ================================================================ ipc
+constexpr int RING = 4;
+constexpr uint64_t SHM_MAGIC = 0x7470697065495043ull;   // "tpipeIPC"
+
+struct alignas(64) ShmSlot {
+    std::atomic<uint64_t> posted;     // sender: 1 + global message index
+    uint64_t offset, bytes;           // message location in the sender's arena
+};
+struct alignas(64) ShmCons {
+    std::atomic<uint64_t> consumed;   // receiver: 1 + global index whose copy is issued
+};
+struct ShmChan {
+    cudaIpcEventHandle_t ready[RING];     // sender-owned
+    cudaIpcEventHandle_t used[RING];      // receiver-owned
+    ShmSlot slot[RING];
+    ShmCons cons[RING];
+};
+struct alignas(64) ShmRank {
+    cudaIpcMemHandle_t arena;
+    uint64_t arena_bytes;
+    int32_t device, pid;
+};
+struct alignas(64) ShmHeader {
+    std::atomic<uint64_t> magic;
+    std::atomic<int32_t> p, n_ch;
+    std::atomic<int32_t> arrived;
+    std::atomic<int32_t> abort;
+};
+static_assert(std::atomic<uint64_t>::is_always_lock_free, "shared-memory atomics");
+
+static size_t shm_size(int p, int n_ch) {
+    return sizeof(ShmHeader) + (size_t)p * sizeof(ShmRank) + (size_t)n_ch * sizeof(ShmChan);
+}
+
+class IpcTransport final : public Transport {
+public:
+    struct Ch {
+        int src = 0, dst = 0;
+        bool out = false, in = false;
+        cudaStream_t st = nullptr;
+        cudaEvent_t own[RING] = {};       // sender: ready; receiver: used
+        cudaEvent_t peer[RING] = {};      // sender: peer's used; receiver: peer's ready
+        uint64_t sent = 0, base = 0, recvd = 0;
+        uint8_t* peer_arena = nullptr;
+    };
+    ~IpcTransport() override {
+        for (auto& c : ch_) {
+            for (int r = 0; r < RING; ++r) {
+                if (c.own[r]) cudaEventDestroy(c.own[r]);
+                if (c.peer[r]) cudaEventDestroy(c.peer[r]);
+            }
+            if (c.st) cudaStreamDestroy(c.st);
+        }
+        for (auto& kv : peer_arena_) cudaIpcCloseMemHandle(kv.second);
+        for (auto e : ev_) cudaEventDestroy(e);
+        if (shm_) munmap(shm_, shm_bytes_);
+    }
+    const char* name() const override { return "ipc"; }
+    void begin_step() override {
+        evnext_ = 0;
+        for (auto& c : ch_) c.base = c.sent;
+    }
+    cudaEvent_t ev() {
+        if (evnext_ == ev_.size()) {
+            cudaEvent_t e;
+            cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+            ev_.push_back(e);
+        }
+        return ev_[evnext_++];
+    }
+    bool aborted() const { return hdr()->abort.load(std::memory_order_acquire) != 0; }
+    int send(int ch, int msg, const void* src, size_t bytes, cudaStream_t cs) override {
+        Ch& c = ch_[ch];
+        const uint64_t n = c.base + (uint64_t)msg;
+        if (!c.out || n != c.sent)
+            return set_error(TPIPE_E_STATE, "ipc send: channel %d message %d out of order", ch, msg);
+        const uint8_t* p = (const uint8_t*)src;
+        if (p < arena_ || p + bytes > arena_ + arena_bytes_)
+            return set_error(TPIPE_E_STATE, "ipc send: message buffer outside the exported pool arena");
+        const int r = (int)(n % RING);
+        ShmChan& S = chan(ch);
+        // the slot's previous message (n - RING) must have been picked up; the
+        // plan's send window W <= RING already guarantees it (defensive)
+        if (n >= RING)
+            if (int rc = poll_until([&] { return S.cons[r].consumed.load(std::memory_order_acquire) >= n - RING + 1; },
+                                    [&] { return aborted(); }, timeout_ms_, "ipc send slot"))
+                return rc;
+        if (cudaEventRecord(c.own[r], cs)) return set_error(TPIPE_E_CUDA, "ipc send: event record");
+        S.slot[r].offset = (uint64_t)(p - arena_);
+        S.slot[r].bytes = bytes;
+        S.slot[r].posted.store(n + 1, std::memory_order_release);
+        c.sent++;
+        return 0;
+    }
+    int recv(int ch, void* dst, size_t bytes, cudaStream_t cs) override {
+        Ch& c = ch_[ch];
+        if (!c.in) return set_error(TPIPE_E_STATE, "ipc recv: channel %d not inbound", ch);
+        const uint64_t n = c.recvd;
+        const int r = (int)(n % RING);
+        ShmChan& S = chan(ch);
+        if (int rc = poll_until([&] { return S.slot[r].posted.load(std::memory_order_acquire) == n + 1; },
+                                [&] { return aborted(); }, timeout_ms_, "ipc recv"))
+            return rc;
+        if (S.slot[r].bytes != bytes)
+            return set_error(TPIPE_E_STATE, "ipc recv: %llu-byte message, expected %zu",
+                             (unsigned long long)S.slot[r].bytes, bytes);
+        const uint8_t* src = c.peer_arena + S.slot[r].offset;
+        cudaEvent_t e0 = ev();
+        cudaError_t e = cudaEventRecord(e0, cs);                      // dst is free for writing
+        if (!e) e = cudaStreamWaitEvent(c.st, e0, 0);
+        if (!e) e = cudaStreamWaitEvent(c.st, c.peer[r], 0);          // the sender's message is complete
+        if (!e) e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c.st);   // copy-engine pull
+        if (!e) e = cudaEventRecord(c.own[r], c.st);
+        if (!e) e = cudaStreamWaitEvent(cs, c.own[r], 0);
+        if (e) return set_error(TPIPE_E_CUDA, "ipc recv: %s", cudaGetErrorString(e));
+        S.cons[r].consumed.store(n + 1, std::memory_order_release);
+        c.recvd++;
+        return 0;
+    }
+    int send_wait(int ch, int msg, cudaStream_t cs) override {
+        Ch& c = ch_[ch];
+        const uint64_t n = c.base + (uint64_t)msg;
+        if (!c.out || n >= c.sent) return set_error(TPIPE_E_STATE, "ipc SEND_WAIT(%d) before its SEND", msg);
+        const int r = (int)(n % RING);
+        ShmChan& S = chan(ch);
+        if (int rc = poll_until([&] { return S.cons[r].consumed.load(std::memory_order_acquire) >= n + 1; },
+                                [&] { return aborted(); }, timeout_ms_, "ipc send_wait"))
+            return rc;
+        return cudaStreamWaitEvent(cs, c.peer[r], 0) ? set_error(TPIPE_E_CUDA, "ipc send_wait") : 0;
+    }
+    int sync(cudaStream_t cs, int timeout_ms) override {
+        const auto t0 = Clock::now();
+        for (;;) {
+            cudaError_t e = cudaStreamQuery(cs);
+            if (e == cudaSuccess) return 0;
+            if (e != cudaErrorNotReady) return set_error(TPIPE_E_CUDA, "step stream: %s", cudaGetErrorString(e));
+            if (aborted()) return set_error(TPIPE_E_STATE, "a peer rank aborted the step");
+            if (ms_since(t0) > timeout_ms) {
+                abort();
+                return set_error(TPIPE_E_TIMEOUT, "step did not complete within %d ms", timeout_ms);
+            }
+            std::this_thread::sleep_for(std::chrono::microseconds(50));
+        }
+    }
+    void abort() override {
+        if (shm_) hdr()->abort.store(1, std::memory_order_release);
+    }
+
+    ShmHeader* hdr() const { return (ShmHeader*)shm_; }
+    ShmRank& rank(int s) const { return ((ShmRank*)(shm_ + sizeof(ShmHeader)))[s]; }
+    ShmChan& chan(int c) const {
+        return ((ShmChan*)(shm_ + sizeof(ShmHeader) + (size_t)p_ * sizeof(ShmRank)))[c];
+    }
+
+    int init(const ChannelList& chl, int p, int stage, int device, const char* name, void* arena,
+             size_t arena_bytes, int window, int timeout_ms) {
+        p_ = p;
+        timeout_ms_ = timeout_ms;
+        arena_ = (uint8_t*)arena;
+        arena_bytes_ = arena_bytes;
+        if (!name || !name[0] || name[0] != '/')
+            return set_error(TPIPE_E_INVALID, "ipc_name must be a POSIX shm name starting with '/'");
+        if (window > RING) return set_error(TPIPE_E_INVALID, "send window %d > ipc mailbox ring %d", window, RING);
+        shm_bytes_ = shm_size(p, (int)chl.size());
+        int fd = shm_open(name, O_CREAT | O_RDWR, 0600);
+        if (fd < 0) return set_error(TPIPE_E_INVALID, "shm_open(%s): %s", name, strerror(errno));
+        if (ftruncate(fd, (off_t)shm_bytes_) != 0) {
+            close(fd);
+            return set_error(TPIPE_E_INVALID, "ftruncate(%s): %s", name, strerror(errno));
+        }
+        void* m = mmap(nullptr, shm_bytes_, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+        close(fd);
+        if (m == MAP_FAILED) return set_error(TPIPE_E_INVALID, "mmap(%s): %s", name, strerror(errno));
+        shm_ = (uint8_t*)m;
+        ShmHeader* H = hdr();
+        uint64_t zero = 0;
+        if (H->magic.compare_exchange_strong(zero, SHM_MAGIC)) {
+            H->p.store(p);
+            H->n_ch.store((int)chl.size());
+        } else if (zero != SHM_MAGIC) {
+            return set_error(TPIPE_E_INVALID, "shm %s holds foreign data", name);
+        }
+        // publish this rank's arena and events
+        ShmRank& me = rank(stage);
+        if (cudaIpcGetMemHandle(&me.arena, arena) != cudaSuccess)
+            return set_error(TPIPE_E_CUDA, "cudaIpcGetMemHandle of the pool arena failed");
+        me.arena_bytes = arena_bytes;
+        me.device = device;
+        me.pid = (int32_t)getpid();
+        ch_.resize(chl.size());
+        for (size_t k = 0; k < chl.size(); ++k) {
+            Ch& c = ch_[k];
+            c.src = chl[k][1];
+            c.dst = chl[k][2];
+            c.out = c.src == stage;
+            c.in = c.dst == stage;
+            if (!c.out && !c.in) continue;
+            for (int r = 0; r < RING; ++r) {
+                if (cudaEventCreateWithFlags(&c.own[r], cudaEventDisableTiming | cudaEventInterprocess))
+                    return set_error(TPIPE_E_CUDA, "interprocess event");
+                cudaIpcEventHandle_t* h = c.out ? &chan((int)k).ready[r] : &chan((int)k).used[r];
+                if (cudaIpcGetEventHandle(h, c.own[r])) return set_error(TPIPE_E_CUDA, "cudaIpcGetEventHandle");
+            }
+            if (c.in && cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking))
+                return set_error(TPIPE_E_CUDA, "ipc channel stream");
+        }
+        std::atomic_thread_fence(std::memory_order_seq_cst);
+        H->arrived.fetch_add(1, std::memory_order_acq_rel);
+        if (int rc = poll_until([&] { return H->arrived.load(std::memory_order_acquire) >= p; },
+                                [&] { return aborted(); }, timeout_ms, "ipc rendezvous"))
+            return rc;
+        if (H->p.load() != p || H->n_ch.load() != (int)chl.size())
+            return set_error(TPIPE_E_INVALID, "ipc rendezvous: ranks disagree on the plan (p, channels)");
+        if (stage == 0) shm_unlink(name);   // every rank has it mapped; the name is no longer needed
+        // open the peers' arenas and events
+        for (size_t k = 0; k < chl.size(); ++k) {
+            Ch& c = ch_[k];
+            if (!c.out && !c.in) continue;
+            const int peer = c.out ? c.dst : c.src;
+            for (int r = 0; r < RING; ++r) {
+                cudaIpcEventHandle_t h = c.out ? chan((int)k).used[r] : chan((int)k).ready[r];
+                if (cudaIpcOpenEventHandle(&c.peer[r], h))
+                    return set_error(TPIPE_E_CUDA, "cudaIpcOpenEventHandle (peer %d)", peer);
+            }
+            if (c.in) {
+                auto it = peer_arena_.find(peer);
+                if (it == peer_arena_.end()) {
+                    void* pa = nullptr;
+                    cudaError_t e = cudaIpcOpenMemHandle(&pa, rank(peer).arena, cudaIpcMemLazyEnablePeerAccess);
+                    if (e) return set_error(TPIPE_E_CUDA, "cudaIpcOpenMemHandle (peer %d): %s", peer,
+                                            cudaGetErrorString(e));
+                    it = peer_arena_.emplace(peer, pa).first;
+                }
+                c.peer_arena = (uint8_t*)it->second;
+            }
+        }
+        return 0;
+    }
+
+    std::vector<Ch> ch_;
+    std::map<int, void*> peer_arena_;
+    std::vector<cudaEvent_t> ev_;
+    size_t evnext_ = 0;
+    uint8_t* shm_ = nullptr;
+    size_t shm_bytes_ = 0;
+    uint8_t* arena_ = nullptr;
+    size_t arena_bytes_ = 0;
+    int p_ = 0, timeout_ms_ = 0;
+};
+
+}  // namespace
+
+std::unique_ptr<Transport> make_virtual_transport(const ChannelList& ch) {
+    return std::unique_ptr<Transport>(new VirtualTransport(ch.size()));
+}
+
+int make_nccl_transport(const ChannelList& chl, int stage, const void* ids_, int timeout_ms,
+                        std::unique_ptr<Transport>* out) {
+    (void)timeout_ms;
+    const NcclApi* N = nccl();
+    if (!N) return set_error(TPIPE_E_NCCL, "libnccl.so.2 not loadable");
+    if (!ids_) return set_error(TPIPE_E_INVALID, "nccl_ids required for the NCCL transport");
+    const ncclUniqueId* ids = (const ncclUniqueId*)ids_;
+    std::unique_ptr<NcclTransport> T(new NcclTransport);
+    T->ch_.resize(chl.size());
+    N->GroupStart();
+    for (size_t c = 0; c < chl.size(); ++c) {
+        const int src = chl[c][1], dst = chl[c][2];
+        if (src != stage && dst != stage) continue;
+        auto& C = T->ch_[c];
+        if (cudaStreamCreateWithFlags(&C.st, cudaStreamNonBlocking)) {
+            N->GroupEnd();
+            return set_error(TPIPE_E_CUDA, "nccl channel stream");
+        }
+        ncclResult_t r = N->CommInitRank(&C.comm, 2, ids[c], src == stage ? 0 : 1);
+        if (r != ncclSuccess && r != ncclInProgress) {
+            N->GroupEnd();
+            return set_error(TPIPE_E_NCCL, "ncclCommInitRank: %s", N->GetErrorString(r));
+        }
+    }
+    ncclResult_t r = N->GroupEnd();
+    if (r != ncclSuccess) return set_error(TPIPE_E_NCCL, "ncclGroupEnd: %s", N->GetErrorString(r));
+    *out = std::move(T);
+    return 0;
+}
+
+int make_ipc_transport(const ChannelList& ch, int p, int stage, int device, const char* shm_name,
+                       void* arena, size_t arena_bytes, int window, int timeout_ms,
+                       std::unique_ptr<Transport>* out) {
+    std::unique_ptr<IpcTransport> T(new IpcTransport);
+    int rc = T->init(ch, p, stage, device, shm_name, arena, arena_bytes, window, timeout_ms);
+    if (rc) {
+        T->abort();
+        return rc;
+    }
+    *out = std::move(T);
+    return 0;
+}
+
+}  // namespace tpipe

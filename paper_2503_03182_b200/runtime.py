@@ -14,14 +14,26 @@ STEP_NO_OPT = 1
 STEP_PROFILE = 2
 STEP_OP_TIMES = 4
 
+TRANSPORT_NCCL = 0
+TRANSPORT_IPC = 1
+DEBUG_POOL_CANARY = 1
+DEBUG_POOL_CANARY_SELFTEST = 2
+
 
 class Runtime:
     def __init__(self, plan, stage: int = -1, device: int = 0, nccl_ids: bytes | None = None,
-                 lr=3e-4, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1, pool_cap: int = 0):
+                 lr=3e-4, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1, pool_cap: int = 0,
+                 transport: int = TRANSPORT_NCCL, timeout_ms: int = 0, ipc_name: str | None = None,
+                 debug_flags: int = 0):
+        """stage -1: every stage in this process (virtual pipeline); stage >= 0:
+        this process runs one stage and talks to its peers over `transport`
+        (NCCL with `nccl_ids`, or CUDA IPC with the job-unique shm `ipc_name`)."""
         self.plan = plan                     # keep the plan alive
         self._ids = C.create_string_buffer(nccl_ids) if nccl_ids else None
+        self._ipc = ipc_name.encode() if ipc_name else None
         o = D.RuntimeOpts(stage, device, C.cast(self._ids, C.c_void_p) if self._ids else None,
-                          pool_cap, lr, beta1, beta2, eps, weight_decay)
+                          pool_cap, lr, beta1, beta2, eps, weight_decay, transport, timeout_ms,
+                          self._ipc, debug_flags)
         self._h = C.c_void_p()
         check(lib().tpipe_runtime_create(plan.handle, C.byref(o), C.byref(self._h)),
               "tpipe_runtime_create")
@@ -79,7 +91,8 @@ class Runtime:
                     offload_h2d_bytes=s.offload_h2d_bytes, host_opt_ms=s.host_opt_ms,
                     kernel_ms=list(s.kernel_ms), kernel_flops=list(s.kernel_flops),
                     kernel_count=list(s.kernel_count), offload_d2h_ms=s.offload_d2h_ms,
-                    offload_h2d_ms=s.offload_h2d_ms)
+                    offload_h2d_ms=s.offload_h2d_ms, pool_overflow_bytes=s.pool_overflow_bytes,
+                    transport=s.transport)
 
     def op_times(self, stage):
         """Per compute op (F/B/R, plan order) GPU ms of the last STEP_OP_TIMES step."""

@@ -1,0 +1,168 @@
+"""Multi-process pipeline: one process per stage (tpipe_runtime_create with
+stage = s), all on cuda:0, stages connected by the CUDA-IPC transport
+(TPIPE_TRANSPORT_IPC: copy-engine pulls from the peer's pool arena,
+interprocess events, a POSIX-shm mailbox). This runs the runtime's
+one-stage-per-rank path — SEND / RECV / SEND_WAIT through a real
+inter-process transport, per-rank pools and ledgers, the host optimizer
+thread with p > 1 Eq. 5/7 windows — and checks it against the
+fp64 oracle (fp32: max-rel <= 1e-4) and bit for bit against the in-process
+virtual pipeline (same kernels; R21).
+
+Stage-to-stage P2P of the pipeline: P:195. p = 8 with L = 16 gives
+T-Recomp delay rounds k = 1 (App. B; SURVEY D-3).
+"""
+
+import os
+import subprocess
+import sys
+import uuid
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+import synth  # noqa: E402
+from oracle import model as R  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+WORKER = os.path.join(ROOT, "tests", "mp_stage_worker.py")
+C1 = dict(L=8, h=64, a=4, f=256, V=256, s=32, b=2)
+C1_16 = dict(C1, L=16)     # C1 width, 16 layers: p = 8 with two chunks of one layer
+
+
+def run_job(tmp_path, cfg, p, m, strategy, dtype, steps=1, offload=0, timeout_ms=120000,
+            stages=None, wall=600):
+    name = f"/tpipe_t_{os.getpid()}_{uuid.uuid4().hex[:12]}"
+    procs = []
+    for s in (range(p) if stages is None else stages):
+        out = str(tmp_path / f"stage{s}.npz")
+        args = [sys.executable, WORKER, out, str(s), str(p), str(m), strategy, str(dtype), name,
+                *(str(cfg[k]) for k in ("L", "h", "a", "f", "V", "s", "b")), str(steps),
+                str(offload), str(timeout_ms)]
+        procs.append((s, out, subprocess.Popen(args, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
+                                               cwd=ROOT)))
+    res, logs = {}, {}
+    for s, out, pr in procs:
+        try:
+            o, _ = pr.communicate(timeout=wall)
+        except subprocess.TimeoutExpired:
+            for _, _, q in procs:
+                q.kill()
+            raise
+        logs[s] = (pr.returncode, o.decode(errors="replace"))
+        if pr.returncode == 0:
+            res[s] = dict(np.load(out))
+    return res, logs
+
+
+def assert_ok(res, logs):
+    bad = {s: l for s, l in logs.items() if l[0] != 0}
+    assert not bad, "\n".join(f"stage {s} rc={rc}:\n{o[-3000:]}" for s, (rc, o) in bad.items())
+
+
+def max_rel(a, b):
+    return float(np.abs(np.asarray(a, np.float64) - b).max() / (np.abs(b).max() + 1e-30))
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64)
+    return float(np.linalg.norm(a - b) / (np.linalg.norm(b) + 1e-30))
+
+
+def _plan(cfg, p, m, strategy, dtype, offload=0):
+    from paper_2503_03182_b200 import plan as P
+    return P.Plan(P.Model(cfg["L"], cfg["h"], cfg["a"], cfg["f"], cfg["V"], cfg["s"], cfg["b"], dtype),
+                  p, m, strategy=strategy, offload=offload)
+
+
+def check_vs_oracle(cfg, p, m, strategy, dtype, res, tol, metric):
+    from paper_2503_03182_b200 import params as PR
+    plan = _plan(cfg, p, m, strategy, dtype)
+    W = synth.weights(cfg["L"], cfg["h"], cfg["f"], cfg["V"], cfg["s"], seed=11, std=0.05,
+                      bias_std=0.02, ln_jitter=0.05)
+    tok, tgt = synth.tokens(cfg["V"], m, cfg["b"], cfg["s"], step=0)
+    lref, G = R.step_grads(R.to64(W), tok, tgt, cfg["a"])
+    assert abs(float(res[p - 1]["loss0"]) - lref) / abs(lref) < tol
+    worst = 0.0
+    for s in range(p):
+        assert int(res[s]["transport"]) == 1          # ran over the IPC transport
+        assert int(res[s]["launches"]) > 0
+        assert int(res[s]["high_water"]) == int(res[s]["plan_peak"])   # per-rank ledger
+        for c in range(1, plan.v + 1):
+            got = PR.unpack(res[s][f"grad{c}"], W, p, plan.v, plan.partition, s, c)
+            for (k, l), g in got.items():
+                ref = G["layers"][l][k] if l is not None else G[k]
+                err = metric(g, ref)
+                worst = max(worst, err)
+                assert err <= tol, (s, c, k, l, err)
+    return worst
+
+
+@pytest.mark.parametrize("strategy", ["tpipe", "tpipe_trecomp", "1f1b", "interleave_trecomp"])
+@pytest.mark.parametrize("p", [2, 4])
+def test_multiprocess_fp32_parity(tmp_path, p, strategy):
+    res, logs = run_job(tmp_path, C1, p, 8, strategy, 0)
+    assert_ok(res, logs)
+    check_vs_oracle(C1, p, 8, strategy, 0, res, 1e-4, max_rel)
+
+
+@pytest.mark.parametrize("strategy,offload", [("tpipe_trecomp", 0), ("tpipe", 1), ("interleave", 0)])
+def test_multiprocess_p8_fp32_parity(tmp_path, strategy, offload):
+    """p = 8 (k = 1 delay round for T-Recomp), 8 processes."""
+    if strategy == "tpipe_trecomp":
+        assert _plan(C1_16, 8, 16, strategy, 0).k == 1
+    res, logs = run_job(tmp_path, C1_16, 8, 16, strategy, 0, offload=offload)
+    assert_ok(res, logs)
+    check_vs_oracle(C1_16, 8, 16, strategy, 0, res, 1e-4, max_rel)
+
+
+def _virtual(cfg, p, m, strategy, dtype, steps, offload=0):
+    from paper_2503_03182_b200 import params as PR, runtime as RT
+    plan = _plan(cfg, p, m, strategy, dtype, offload)
+    rt = RT.Runtime(plan, stage=-1, lr=1e-3)
+    W = synth.weights(cfg["L"], cfg["h"], cfg["f"], cfg["V"], cfg["s"], seed=11, std=0.05,
+                      bias_std=0.02, ln_jitter=0.05)
+    for s in range(p):
+        for c in range(1, plan.v + 1):
+            rt.set_params(s, c, PR.pack(W, p, plan.v, plan.partition, s, c))
+    tok, tgt = synth.tokens(cfg["V"], m, cfg["b"], cfg["s"], step=0)
+    loss0 = rt.step(tok, tgt, RT.STEP_NO_OPT)
+    grads = {(s, c): rt.get_grads(s, c) for s in range(p) for c in range(1, plan.v + 1)}
+    for s in range(p):
+        for c in range(1, plan.v + 1):
+            rt.set_params(s, c, PR.pack(W, p, plan.v, plan.partition, s, c))
+    losses = []
+    for k in range(steps):
+        tok, tgt = synth.tokens(cfg["V"], m, cfg["b"], cfg["s"], step=k)
+        losses.append(rt.step(tok, tgt, 0))
+    params = {(s, c): rt.get_params(s, c) for s in range(p) for c in range(1, plan.v + 1)}
+    rt.close()
+    return loss0, grads, losses, params
+
+
+@pytest.mark.parametrize("p,strategy,offload,cfg,m", [
+    (4, "tpipe_trecomp", 0, C1, 8),
+    (4, "tpipe_trecomp", 1, C1, 8),       # host AdamW of chunk 2 with p > 1 windows
+    (8, "tpipe_trecomp", 5, C1_16, 16),   # streamed device AdamW, k = 1
+])
+def test_multiprocess_bf16_bitexact_vs_virtual(tmp_path, p, strategy, offload, cfg, m):
+    """bf16, 2 optimizer steps: the multi-process run reproduces the virtual
+    pipeline bit for bit (loss, gradients, updated parameters)."""
+    res, logs = run_job(tmp_path, cfg, p, m, strategy, 1, steps=2, offload=offload)
+    assert_ok(res, logs)
+    loss0, grads, losses, params = _virtual(cfg, p, m, strategy, 1, 2, offload)
+    assert float(res[p - 1]["loss0"]) == loss0
+    assert list(res[p - 1]["losses"]) == losses
+    for (s, c), g in grads.items():
+        assert np.array_equal(res[s][f"grad{c}"].view(np.uint32), g.view(np.uint32)), (s, c)
+    for (s, c), w in params.items():
+        assert np.array_equal(res[s][f"param{c}"].view(np.uint32), w.view(np.uint32)), (s, c)
+
+
+def test_multiprocess_missing_peer_times_out(tmp_path):
+    """A rank whose peer never arrives fails with TPIPE_E_TIMEOUT instead of hanging."""
+    res, logs = run_job(tmp_path, C1, 2, 8, "tpipe", 0, timeout_ms=3000, stages=[0], wall=120)
+    rc, out = logs[0]
+    assert rc != 0
+    assert "timed out" in out and "rc=-11" in out

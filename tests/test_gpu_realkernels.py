@@ -1,0 +1,166 @@
+"""Parity and bit-exactness where the production kernels run.
+
+* p = 8 virtual pipeline (C1 width, L = 16): fp32 against the fp64 oracle
+  (max-rel <= 1e-4) and bf16 (rel-L2 <= 2e-2) for every strategy, including
+  T-Recomp with k = 1 delay round (App. B; SURVEY D-3), model-state
+  T-Offload at p = 8 and Interleave-1F1B.
+* head_dim 128 with production tiles: C_MID (h = 256, a = 2, d = 128) and
+  the 2-layer GPT-3 1.3B shape (h = 2048, a = 16, s = 2048, V = 50304) route
+  attention to the tcgen05 kernels (fa5::*) and GEMMs to the CTA-pair
+  tcgen05 kernels. T-Recomp (full and partial), T-Offload (host and streamed
+  device AdamW), activation offload and Interleave-1F1B give gradients and
+  updated parameters bit-identical to T-Pipe (BASELINE north_star, R21).
+* pool canaries (TPIPE_DEBUG_POOL_CANARY): no kernel writes past the bytes
+  the plan gave its buffer, on C1 and C_MID for every strategy; the
+  self-test proves the check fires.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+import synth  # noqa: E402
+from oracle import model as R  # noqa: E402
+
+C1_16 = dict(L=16, h=64, a=4, f=256, V=256, s=32, b=2)
+C_MID8 = dict(L=8, h=256, a=2, f=1024, V=512, s=256, b=1)
+G13 = dict(L=2, h=2048, a=16, f=8192, V=50304, s=2048, b=1)
+
+
+def mods():
+    from paper_2503_03182_b200 import params, plan, runtime
+    return plan, runtime, params
+
+
+def build(cfg, p, m, strategy, dtype, offload=0, recomp_layers=0, seed=11, debug_flags=0,
+          std=0.05):
+    P, RT, PR = mods()
+    md = P.Model(cfg["L"], cfg["h"], cfg["a"], cfg["f"], cfg["V"], cfg["s"], cfg["b"], dtype)
+    plan = P.Plan(md, p, m, strategy=strategy, offload=offload, recomp_layers=recomp_layers)
+    rt = RT.Runtime(plan, stage=-1, lr=1e-3, debug_flags=debug_flags)
+    W = synth.weights(cfg["L"], cfg["h"], cfg["f"], cfg["V"], cfg["s"], seed=seed, std=std,
+                      bias_std=0.02, ln_jitter=0.05)
+    for s in range(p):
+        for c in range(1, plan.v + 1):
+            rt.set_params(s, c, PR.pack(W, p, plan.v, plan.partition, s, c))
+    return plan, rt, W
+
+
+def max_rel(a, b):
+    return float(np.abs(np.asarray(a, np.float64) - b).max() / (np.abs(b).max() + 1e-30))
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64)
+    return float(np.linalg.norm(a - b) / (np.linalg.norm(b) + 1e-30))
+
+
+P8_STRATS = [("tpipe", 0), ("tpipe_trecomp", 0), ("tpipe", 1), ("tpipe_trecomp", 5),
+             ("1f1b", 0), ("1f1b_full_recomp", 0), ("interleave", 0), ("interleave_trecomp", 0)]
+
+
+@pytest.mark.parametrize("strategy,offload", P8_STRATS)
+@pytest.mark.parametrize("dtype", [0, 1])
+def test_p8_parity(strategy, offload, dtype):
+    _P, RT, PR = mods()
+    p, m, cfg = 8, 16, C1_16
+    plan, rt, W = build(cfg, p, m, strategy, dtype, offload)
+    if strategy == "tpipe_trecomp":
+        assert plan.k == 1
+    tok, tgt = synth.tokens(cfg["V"], m, cfg["b"], cfg["s"], step=0)
+    loss = rt.step(tok, tgt, RT.STEP_NO_OPT)
+    lref, G = R.step_grads(R.to64(W), tok, tgt, cfg["a"])
+    tol, metric = (1e-4, max_rel) if dtype == 0 else (2e-2, rel_l2)
+    assert abs(loss - lref) / abs(lref) < (1e-5 if dtype == 0 else 2e-2)
+    for s in range(p):
+        for c in range(1, plan.v + 1):
+            got = PR.unpack(rt.get_grads(s, c), W, p, plan.v, plan.partition, s, c)
+            for (k, l), g in got.items():
+                ref = G["layers"][l][k] if l is not None else G[k]
+                assert metric(g, ref) <= tol, (s, c, k, l)
+    st = rt.stats()
+    for s in range(p):
+        assert st["pool_high_water"][s] == plan.peak(s)["total_peak"]
+    rt.close()
+
+
+def _run(cfg, p, m, strategy, offload=0, recomp_layers=0, steps=2, std=0.05):
+    """bf16: step-0 loss and gradients (no optimizer), then `steps` optimizer
+    steps from the same initial parameters; returns everything as raw bits."""
+    _P, RT, _PR = mods()
+    plan, rt, W = build(cfg, p, m, strategy, 1, offload, recomp_layers, std=std)
+    tok, tgt = synth.tokens(cfg["V"], m, cfg["b"], cfg["s"], step=0,
+                            vocab_eff=50257 if cfg["V"] == 50304 else None)
+    loss0 = rt.step(tok, tgt, RT.STEP_NO_OPT)
+    grads = [rt.get_grads(s, c).view(np.uint32).copy() for s in range(p) for c in range(1, plan.v + 1)]
+    from paper_2503_03182_b200 import params as PR
+    for s in range(p):
+        for c in range(1, plan.v + 1):
+            rt.set_params(s, c, PR.pack(W, p, plan.v, plan.partition, s, c))
+    losses = []
+    for k in range(steps):
+        tok, tgt = synth.tokens(cfg["V"], m, cfg["b"], cfg["s"], step=k,
+                                vocab_eff=50257 if cfg["V"] == 50304 else None)
+        losses.append(rt.step(tok, tgt, 0))
+    params = [rt.get_params(s, c).view(np.uint32).copy() for s in range(p) for c in range(1, plan.v + 1)]
+    rt.close()
+    return loss0, grads, losses, params
+
+
+def _assert_same(a, b, what):
+    assert a[0] == b[0], (what, "loss", a[0], b[0])
+    for x, y in zip(a[1], b[1]):
+        assert np.array_equal(x, y), (what, "grads")
+    assert a[2] == b[2], (what, "losses")
+    for x, y in zip(a[3], b[3]):
+        assert np.array_equal(x, y), (what, "params")
+
+
+CMID_VARIANTS = [("tpipe_trecomp", 0, 0), ("tpipe_trecomp", 0, 1), ("tpipe", 1, 0),
+                 ("tpipe", 5, 0), ("tpipe_trecomp", 5, 1), ("tpipe", 2, 0),
+                 ("interleave", 0, 0), ("interleave_trecomp", 0, 0)]
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_cmid_d128_bitexact_vs_tpipe(p):
+    """C_MID (d = 128 -> fa5 tcgen05 attention; tcgen05 GEMMs): every
+    recompute / offload variant reproduces T-Pipe bit for bit."""
+    m = 4
+    ref = _run(C_MID8, p, m, "tpipe")
+    for strategy, offload, r in CMID_VARIANTS:
+        if p == 1 and strategy.startswith("interleave"):
+            continue
+        _assert_same(ref, _run(C_MID8, p, m, strategy, offload, r), (strategy, offload, r))
+
+
+@pytest.mark.parametrize("strategy,offload", [("tpipe_trecomp", 0), ("tpipe", 1), ("tpipe", 5),
+                                              ("tpipe", 2)])
+def test_gpt13b_shape_bitexact_vs_tpipe(strategy, offload):
+    """The bench's layer / vocabulary shape (2 layers of GPT-3 1.3B, p = 1,
+    m = 2): CTA-pair GEMMs, fa5 attention at s = 2048."""
+    ref = _run(G13, 1, 2, "tpipe", steps=1, std=0.02)
+    _assert_same(ref, _run(G13, 1, 2, strategy, offload, steps=1, std=0.02), (strategy, offload))
+
+
+@pytest.mark.parametrize("cfg,p,m", [(C1_16, 4, 8), (C_MID8, 2, 4)])
+@pytest.mark.parametrize("strategy,offload", [("tpipe", 0), ("tpipe_trecomp", 0), ("tpipe", 2),
+                                              ("tpipe_trecomp", 5), ("1f1b_full_recomp", 0),
+                                              ("interleave_trecomp", 0)])
+def test_pool_canaries_clean(cfg, p, m, strategy, offload):
+    _P, RT, _PR = mods()
+    plan, rt, W = build(cfg, p, m, strategy, 1, offload, debug_flags=RT.DEBUG_POOL_CANARY)
+    tok, tgt = synth.tokens(cfg["V"], m, cfg["b"], cfg["s"], step=0)
+    rt.step(tok, tgt, 0)
+    rt.close()
+
+
+def test_pool_canary_selftest_fires():
+    _P, RT, _PR = mods()
+    from paper_2503_03182_b200._lib import TPipeError
+    plan, rt, W = build(C1_16, 4, 8, "tpipe", 1,
+                        debug_flags=RT.DEBUG_POOL_CANARY | RT.DEBUG_POOL_CANARY_SELFTEST)
+    tok, tgt = synth.tokens(C1_16["V"], 8, C1_16["b"], C1_16["s"], step=0)
+    with pytest.raises(TPipeError, match="pool canary"):
+        rt.step(tok, tgt, 0)
+    rt.close()
