@@ -233,9 +233,14 @@ def capacity_plans(p=CAP_P, budget=CAP_BUDGET_GIB * 2 ** 30, m=CAP_M):
     stage for the C5 shape (h=4096, s=8192), from the planner's byte model."""
     from paper_2503_03182_b200 import plan as P
     from paper_2503_03182_b200._lib import TPipeError
+    ms = P.OFFLOAD_MODEL_STATE | P.OFFLOAD_DEVICE_OPT
     strategies = {"1f1b": ("1f1b", 0), "1f1b_full_recomp": ("1f1b_full_recomp", 0),
                   "tpipe": ("tpipe", 0), "tpipe_trecomp": ("tpipe_trecomp", 0),
-                  "tpipe_all": ("tpipe_trecomp", P.OFFLOAD_MODEL_STATE | P.OFFLOAD_DEVICE_OPT),
+                  "tpipe_all": ("tpipe_trecomp", ms),
+                  # ladder rungs without recompute (R28): model-state T-Offload, activation
+                  # offload, both
+                  "tpipe_offload": ("tpipe", ms), "tpipe_actoff": ("tpipe", P.OFFLOAD_ACTIVATIONS),
+                  "tpipe_actoff_offload": ("tpipe", P.OFFLOAD_ACTIVATIONS | ms),
                   "interleave": ("interleave", 0), "interleave_trecomp": ("interleave_trecomp", 0)}
     best = {}
     for name, (strat, off) in strategies.items():
@@ -268,9 +273,12 @@ def run_capacity(args):
     import synth
     p, m, budget = CAP_P, CAP_M, CAP_BUDGET_GIB * 2 ** 30
     best = capacity_plans()
-    runs = [(n, *best[n]) for n in ("1f1b", "1f1b_full_recomp", "tpipe", "tpipe_trecomp", "tpipe_all",
-                                     "interleave", "interleave_trecomp")
-            if n in best]
+    names = ("1f1b", "1f1b_full_recomp", "tpipe", "tpipe_trecomp", "tpipe_all", "tpipe_offload",
+             "tpipe_actoff", "tpipe_actoff_offload", "interleave", "interleave_trecomp")
+    only = os.environ.get("TPIPE_CAPACITY_ONLY")
+    if only:
+        names = tuple(n for n in names if n in only.split(",") or n == "1f1b")
+    runs = [(n, *best[n]) for n in names if n in best]
     if "1f1b_full_recomp" in best and "tpipe_all" in best:
         runs.append(("tpipe_all@1f1b_full_recomp_size", best["1f1b_full_recomp"][0], *best["tpipe_all"][1:]))
     if "1f1b" in best:
@@ -282,7 +290,8 @@ def run_capacity(args):
             return P.Plan(md, p, m, strategy="1f1b").params_total
         target = 2 * params_at(best["1f1b"][0])
         L2 = next(L for L in range(p, 400, p) if params_at(L) >= target)
-        runs.append(("auto@2x_1f1b_params", L2, "auto", P.OFFLOAD_MODEL_STATE | P.OFFLOAD_DEVICE_OPT))
+        runs.append(("auto@2x_1f1b_params", L2, "auto",
+                     P.OFFLOAD_MODEL_STATE | P.OFFLOAD_DEVICE_OPT | P.OFFLOAD_ACTIVATIONS))
     pool = (np.random.default_rng(5).standard_normal(1 << 24, dtype=np.float32)
             * np.float32(0.02))
     tok, tgt = synth.tokens(C5["vocab"], m, C5["micro_batch"], C5["seq_len"], step=0)
@@ -468,26 +477,6 @@ def modeled_makespan(plan, head_layers):
             d.append(2 * f if o["kind"] == "B" else f)
         ms.append(d)
     return plan.simulate_durations(ms)[0]
-
-
-def choose_partition(md, p, m, strategy, c=None):
-    """Balanced per-stage layer vector (R27) when the duration model predicts
-    >= 3% shorter steps than the uniform split, else None (uniform)."""
-    from paper_2503_03182_b200 import plan as P
-    c = c or C2
-    if p < 2:
-        return None
-    hl = 6 * c["hidden"] * c["vocab"] / (72 * c["hidden"] ** 2 + 6 * c["seq_len"] * c["hidden"])
-    v = 1 if strategy.startswith("1f1b") else 2
-    part = balanced_partition(md.n_layers, p, v, hl)
-    if not part:
-        return None
-    try:
-        u = modeled_makespan(P.Plan(md, p, m, strategy=strategy), hl)
-        b = modeled_makespan(P.Plan(md, p, m, strategy=strategy, stage_layers=part), hl)
-    except Exception:
-        return None
-    return part if b < 0.97 * u else None
 
 
 def pipeline_replay(ps=(8,), strategies=("1f1b", "tpipe", "tpipe_trecomp", "1f1b_full_recomp",
@@ -692,31 +681,92 @@ def quick_measure(strategy, N, m, dtok, dtgt, args, recomp_layers=0, offload=0, 
     return res
 
 
+def latest_capacity_claim():
+    """The executed-capacity headline, read from the newest committed
+    profiles/*capacity_measured*.json (so the printed claim cannot go stale)."""
+    import glob
+    import re
+    files = glob.glob(os.path.join(ROOT, "profiles", "*capacity_measured*.json"))
+    if not files:
+        return None
+    key = lambda f: (re.findall(r"r(\d+)_", os.path.basename(f)) or ["0"])[0].zfill(3) + \
+        (re.findall(r"_v(\d+)", f) or ["0"])[0].zfill(3)
+    f = max(files, key=key)
+    runs = json.load(open(f))["capacity_measured"]["runs"]
+    best = max((r for r in runs.values() if r.get("fits_budget")),
+               key=lambda r: r.get("params_vs_1f1b", 0), default=None)
+    if not best:
+        return None
+    return (f"{os.path.relpath(f, ROOT)}: largest executed model {best['params_B']}B params = "
+            f"{best['params_vs_1f1b']}x 1F1B's at {best['model_tflops_vs_1f1b']}x its model TFLOP/s "
+            f"({best['strategy']}, offload={best.get('offload', 0)})")
+
+
+def launch_ranks(args):
+    """`bench.py --gpus N` outside torchrun: start N ranks (one process per GPU)
+    with torch.distributed.run and relay rank 0's line; refuse when the box has
+    fewer than N GPUs (a one-GPU virtual pipeline is --virtual-stages, and is
+    labelled n_gpus = 1)."""
+    import subprocess
+    import torch
+    n_dev = torch.cuda.device_count()
+    if n_dev < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, this box has {n_dev} "
+              f"(use --virtual-stages {args.gpus} for a one-GPU virtual pipeline)", file=sys.stderr)
+        sys.exit(2)
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
 def run_tpipe(args):
     import torch
     from paper_2503_03182_b200 import plan as P, runtime as RT
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    N = max(args.gpus, world)
+    if world > 1 and args.gpus != world:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if world > 1 and args.virtual_stages:
+        raise SystemExit("bench.py: --virtual-stages is a one-process option")
+    # p pipeline stages: one per rank (N > 1), or a one-GPU virtual pipeline
+    N = world if world > 1 else (args.virtual_stages or 1)
+    n_gpus = world
     dist = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("gloo")
+    # test hook: every rank on GPU 0 (exercises the N-rank path on a one-GPU
+    # box; the number is NOT an N-GPU measurement and the line says so)
+    same_gpu = os.environ.get("TPIPE_BENCH_SAME_GPU") == "1"
+    if same_gpu:
+        local = 0
     torch.cuda.set_device(local)
     c = C2
     md = P.Model(c["n_layers"], c["hidden"], c["n_heads"], c["ffn_hidden"], c["vocab"],
                  c["seq_len"], c["micro_batch"], P.BF16)
     m = c["m"]
-    # p > 1: cost-balanced stage partition when the duration model says it pays (R27)
-    part = choose_partition(md, N, m, args.strategy) if N > 1 else None
-    plan = P.Plan(md, N, m, strategy=args.strategy, stage_layers=part)
-    ids = None
+    # p > 1: the planner picks the cost-balanced stage partition when its cost
+    # model says it pays (R27/R28)
+    plan = P.Plan(md, N, m, strategy=args.strategy, balance=N > 1)
+    ids, ipc_name = None, None
+    transport = RT.TRANSPORT_IPC if args.transport == "ipc" else RT.TRANSPORT_NCCL
     if world > 1:
-        ids = [b"".join(RT.nccl_unique_id() for _ in plan.channels)] if rank == 0 else [None]
+        if transport == RT.TRANSPORT_NCCL:
+            ids = [b"".join(RT.nccl_unique_id() for _ in plan.channels)] if rank == 0 else [None]
+        else:
+            ids = [f"/tpipe_bench_{os.getpid()}_{np.random.default_rng().integers(1 << 40)}"] \
+                if rank == 0 else [None]
         dist.broadcast_object_list(ids, src=0)
-        ids = ids[0]
-    rt = RT.Runtime(plan, stage=rank if world > 1 else -1, device=local, nccl_ids=ids, lr=1e-4)
+        ids, ipc_name = (ids[0], None) if transport == RT.TRANSPORT_NCCL else (None, ids[0])
+    rt = RT.Runtime(plan, stage=rank if world > 1 else -1, device=local, nccl_ids=ids, lr=1e-4,
+                    transport=transport, ipc_name=ipc_name)
     rng = np.random.default_rng(1234 + rank)
     stages = [rank] if world > 1 else list(range(N))
     for s in stages:
@@ -785,21 +835,26 @@ def run_tpipe(args):
     prof_step_ms = None
     out = None
     if rank == 0:
-        mfu = value * model_flops_per_token(c) / (N * pk_sust * 1e12)
+        mfu = value * model_flops_per_token(c) / (n_gpus * pk_sust * 1e12)
         out = {
-            "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": N,
+            "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": n_gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (seeded uniform tokens < 50257; random-init weights)",
             "config": {"workload": "configs[1]: GPT-3 1.3B, seq 2048, T-Pipe, m=32 micro-batches",
                        "model": "gpt3-1.3b", "n_layers": 24, "hidden": 2048, "seq_len": 2048,
                        "micro_batch": 1, "n_microbatches": m, "global_batch_tokens": tokens,
-                       "strategy": args.strategy, "parallelism": f"pp{N}",
+                       "strategy": args.strategy,
+                       "parallelism": f"pp{N}" if world > 1 else
+                       (f"virtual pp{N} on 1 GPU" if N > 1 else "pp1"),
+                       "transport": (args.transport if world > 1 else "in-process"),
+                       **({"same_gpu_test": "all ranks on GPU 0 (TPIPE_BENCH_SAME_GPU): "
+                                            "not an N-GPU measurement"} if same_gpu else {}),
                        "layers_per_chunk": list(plan.layers_chunk),
                        "stage_layers": [sum(x) for x in plan.partition],
                        "l2": "working set >> 126 MB L2 (no flush needed)"},
             "mfu": round(mfu, 4),
-            "hfu": round(hw_flops / (step_ms / 1e3) / (N * pk_sust * 1e12), 4),
+            "hfu": round(hw_flops / (step_ms / 1e3) / (n_gpus * pk_sust * 1e12), 4),
             "mfu_peak": f"{pk_sust} TFLOP/s bf16 sustained ({src})",
             "bubble_fraction_unit_model": bubble,
             "gpu_launches": int(launches) * args.steps,
@@ -878,8 +933,8 @@ def run_tpipe(args):
                     "P:443, P:471); context, not targets",
             "max_size_vs_1f1b": 2.4, "max_size_vs_1f1b_r50": 1.5,
             "tpipe_all_throughput_vs_1f1b_r50": 0.9758,
-            "this_build": "capacity_80GiB (planner, p=8) and bench.py --capacity-run "
-                          "(executed, profiles/r1_capacity_measured_v2.json: 3.53x params at 0.906x model TFLOP/s)"}
+            "this_build": "capacity_80GiB (planner, p=8) and bench.py --capacity-run (executed; "
+                          + str(latest_capacity_claim()) + ")"}
     if dist:
         dist.barrier()
     return out
@@ -941,6 +996,10 @@ def main():
                     help="measured-op-duration replay of p = 2, 4, 8 stage pipelines (C2)")
     ap.add_argument("--capacity-run", action="store_true",
                     help="executed capacity at a fixed per-stage HBM budget (p=8 virtual pipeline, one GPU)")
+    ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
+                    help="stage transport for N > 1 ranks (CUDA-IPC copy-engine pull, or NCCL send/recv)")
+    ap.add_argument("--virtual-stages", type=int, default=0,
+                    help="run a p-stage virtual pipeline on this one GPU (reported as n_gpus = 1)")
     args = ap.parse_args()
     if args.capacity_run:
         print(json.dumps(run_capacity(args)), flush=True)
@@ -956,6 +1015,8 @@ def main():
         return
     if args.warmup < 3:
         args.warmup = 3
+    if args.impl == "tpipe" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        launch_ranks(args)
     out = run_reference(args) if args.impl == "reference" else run_tpipe(args)
     if out is not None:
         print(json.dumps(out), flush=True)

@@ -93,14 +93,20 @@ enum {
 #define TPIPE_SOPT_SLICE_PARAMS 8388608
 
 typedef struct {
-    int32_t strategy;      /* TPIPE_S_*, or -1 = auto: escalate TPIPE -> TPIPE_TRECOMP with
-                              r = 1..n1 recomputed layers -> + model-state offload (r = 1..n1;
-                              DEVICE_OPT if requested in `offload`) until hbm_budget fits */
+    int32_t strategy;      /* TPIPE_S_*, or -1 = auto (fit hbm_budget with the least
+                              throughput loss): among T-Pipe, T-Pipe + model-state T-Offload,
+                              T-Pipe + activation offload (+ model-state T-Offload), T-Recomp
+                              with r = 1..n1 recomputed layers (+ model-state T-Offload), the
+                              plan with the smallest cost-model step time that fits (offload
+                              kinds limited by `offload` when it is not -1; DEVICE_OPT if
+                              requested there) */
     int32_t delay_rounds;  /* T-Recomp k; -1 = App. B constraint as printed */
     int32_t send_window;   /* W, max in-flight sends per channel; 0 = default 2 (DESIGN R12) */
     int32_t offload;       /* TPIPE_OFFLOAD_* bitmask (explicit strategies); -1 = auto */
     int32_t act_distance;  /* activation offload: release / prefetch distance in compute
-                              ops (0 = default 2); blocks with F->B distance <= 2x are kept */
+                              ops; 0 = derived: the smallest d whose d chunk-1 forward
+                              times (cost model) cover one block's copy at host_link_bps
+                              (SURVEY Q12), >= 1; blocks with F->B distance <= 2d are kept */
     int32_t recomp_layers; /* partial T-Recomp (the recompute ratio of
                               P:551, Fig. E56): chunk-1 layers per stage that R regenerates,
                               shallowest first; the deeper n1 - r layers keep their stash
@@ -113,6 +119,24 @@ typedef struct {
                               v = 2); all zero = uniform n_layers / n_stages. When set: the
                               first n_stages entries sum to n_layers, each >= 2 at v = 2 (>= 1
                               at v = 1), model.layers_chunk must be {0, 0} */
+    /* Planner cost model (DESIGN R28; SURVEY §8(b) host_link_bps /
+     * host_adam_params_per_s): per-op durations from FLOPs (F = the chunk's
+     * layers (+ the LM head), B = 2F, R = recomputed layers) replayed ASAP over
+     * the plan's order, plus the offload transfer time that does not fit the
+     * window the schedule leaves it (model states: from the last deep-chunk
+     * backward to the next step's first deep-chunk forward, P:680/P:694;
+     * activations: the stage's busy time). Used to (1) order the auto ladder by
+     * estimated step time, (2) derive the activation release / prefetch
+     * distance from bytes / bandwidth when act_distance = 0, and
+     * (3) choose a cost-balanced partition when `balance` is set.
+     * 0 = defaults (50e9 B/s, 3e9 params/s, 1e15 FLOP/s: this build's measured
+     * pinned-link, host AdamW and in-step GEMM rates on B200). */
+    double host_link_bps;
+    double host_adam_params_per_s;
+    double device_flops;
+    int32_t balance;       /* 1: use the cost-balanced stage_layers partition (the last stage
+                              also runs the LM head, SURVEY D-12) when the modeled step is >= 3%
+                              shorter than the uniform split; ignored if stage_layers is set */
 } tpipe_plan_opts;
 
 enum {
@@ -172,6 +196,9 @@ typedef struct {
     int32_t n_channels;
     uint64_t params_total;
     int32_t recomp_layers;   /* effective r of partial T-Recomp (0 unless T-Recomp) */
+    double est_step_s;       /* cost-model step time (seconds, see tpipe_plan_opts) */
+    double est_exposed_offload_s;   /* of which: offload transfer time left exposed */
+    int32_t balanced;        /* 1 if the planner chose a cost-balanced partition */
 } tpipe_plan_info;
 
 typedef struct {

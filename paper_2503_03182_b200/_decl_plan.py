@@ -13,7 +13,9 @@ class ModelDesc(C.Structure):
 
 class PlanOpts(C.Structure):
     _fields_ = [("strategy", i32), ("delay_rounds", i32), ("send_window", i32), ("offload", i32),
-                ("act_distance", i32), ("recomp_layers", i32), ("stage_layers", i32 * 64)]
+                ("act_distance", i32), ("recomp_layers", i32), ("stage_layers", i32 * 64),
+                ("host_link_bps", C.c_double), ("host_adam_params_per_s", C.c_double),
+                ("device_flops", C.c_double), ("balance", i32)]
 
 
 class Op(C.Structure):
@@ -37,7 +39,8 @@ class PlanInfo(C.Structure):
     _fields_ = [("n_stages", i32), ("n_microbatches", i32), ("v", i32), ("strategy", i32),
                 ("delay_rounds", i32), ("send_window", i32), ("offload", i32), ("act_distance", i32),
                 ("layers_chunk", i32 * 2), ("n_channels", i32), ("params_total", u64),
-                ("recomp_layers", i32)]
+                ("recomp_layers", i32), ("est_step_s", C.c_double),
+                ("est_exposed_offload_s", C.c_double), ("balanced", i32)]
 
 
 class SimReport(C.Structure):

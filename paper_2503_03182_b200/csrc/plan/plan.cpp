@@ -20,6 +20,7 @@
 #include "plan/plan.h"
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <map>
 #include <new>
@@ -584,9 +585,146 @@ using namespace tpipe;
 
 #define TP_API extern "C" __attribute__((visibility("default")))
 
+// ASAP replay of the compute order with per-op durations dur(s, j) (j = index
+// of the op in stage s's compute order); returns makespan and busy per stage
+template <typename T, typename DurFn>
+static int replay_order(const tpipe_plan* P, DurFn dur, T* makespan, T* busy_out,
+                        std::vector<std::vector<std::array<T, 2>>>* times = nullptr) {
+    const int p = P->p, v = P->v;
+    const bool rec = P->strategy == TPIPE_S_TPIPE_TRECOMP || P->strategy == TPIPE_S_INTERLEAVE_TRECOMP;
+    std::map<std::tuple<int, int, int, int>, T> endt;  // (stage, kind, chunk, mb)
+    std::vector<size_t> pos(p, 0);
+    std::vector<T> freet(p, 0), busy(p, 0);
+    size_t total = 0, done = 0;
+    for (auto& o : P->order) total += o.size();
+    if (times) {
+        times->assign(p, {});
+        for (int s = 0; s < p; ++s) (*times)[s].resize(P->order[s].size());
+    }
+    while (done < total) {
+        bool prog = false;
+        for (int s = 0; s < p; ++s) {
+            while (pos[s] < P->order[s].size()) {
+                const COp& op = P->order[s][pos[s]];
+                const int kind = op[0], c = op[1], i = op[2];
+                std::vector<std::tuple<int, int, int, int>> deps;
+                if (kind == KF) {
+                    if (s > 0) deps.push_back({s - 1, KF, c, i});
+                    else if (c > 1) deps.push_back({p - 1, KF, c - 1, i});
+                } else if (kind == KR) {
+                    deps.push_back({s, KF, c, i});
+                } else {
+                    deps.push_back({s, KF, c, i});
+                    if (rec && c == 1) deps.push_back({s, KR, c, i});
+                    if (s < p - 1) deps.push_back({s + 1, KB, c, i});
+                    else if (c < v) deps.push_back({0, KB, c + 1, i});
+                }
+                T t0 = freet[s];
+                bool ready = true;
+                for (auto& dd : deps) {
+                    auto it = endt.find(dd);
+                    if (it == endt.end()) { ready = false; break; }
+                    t0 = std::max(t0, it->second);
+                }
+                if (!ready) break;
+                const T t1 = t0 + dur(s, (int)pos[s], kind);
+                endt[{s, kind, c, i}] = t1;
+                if (times) (*times)[s][pos[s]] = {t0, t1};
+                freet[s] = t1;
+                busy[s] += t1 - t0;
+                ++pos[s];
+                ++done;
+                prog = true;
+            }
+        }
+        if (!prog) return set_error(TPIPE_E_DEADLOCK, "compute order deadlocks");
+    }
+    *makespan = 0;
+    for (int s = 0; s < p; ++s) *makespan = std::max(*makespan, freet[s]);
+    for (int s = 0; s < 64; ++s) busy_out[s] = s < p ? busy[s] : 0;
+    return 0;
+}
+
+// ---------------------------------------------------------------- cost model (DESIGN R28)
+struct CostModel {
+    double bw = 50e9, host = 3e9, flops = 1e15;
+};
+
+static double layer_fwd_s(const tpipe_model_desc& d, const CostModel& cm) {
+    const double M = (double)d.micro_batch * d.seq_len, h = d.hidden, f = d.ffn_hidden;
+    const double hd = (double)d.hidden / d.n_heads, s = d.seq_len;
+    const double fl = 2.0 * M * (4.0 * h * h + 2.0 * h * f) +
+                      4.0 * d.micro_batch * d.n_heads * (s * (s + 1) / 2.0) * hd;
+    return fl / cm.flops;
+}
+
+static double head_fwd_s(const tpipe_model_desc& d, const CostModel& cm) {
+    return 2.0 * d.micro_batch * d.seq_len * (double)d.vocab * d.hidden / cm.flops;
+}
+
+// F = the chunk's layers (+ the LM head on the last stage's last chunk),
+// B = 2F (+ the layers' forward again under 1F1B + full recompute), R = the
+// recomputed layers (P:611 unit model with T_bwd = 2 T_fwd, scaled by FLOPs)
+static double op_seconds(const tpipe_plan* P, int s, int kind, int c, double tl, double th) {
+    if (kind == KR) return P->rl_of(s) * tl;
+    const double f = P->sl[s][c - 1] * tl + ((s == P->p - 1 && c == P->v) ? th : 0.0);
+    if (kind == KB) return 2.0 * f + (P->strategy == TPIPE_S_1F1B_FULL_RECOMP ? P->sl[s][c - 1] * tl : 0.0);
+    return f;
+}
+
+// Modeled step time: ASAP replay of the order with op_seconds, plus per stage
+// the offload transfer time that does not fit its window:
+//  * model-state T-Offload of chunk v: the window runs from the stage's last
+//    B(s, v, .) to the end of the step and on to the next step's first
+//    F(s, v, .) (P:680 / P:694: the cool-down and warm-up bubbles); host AdamW
+//    needs grads down (4 B/param) + the host update + bf16 weights up, the
+//    streamed device AdamW 12 B/param each way (both directions in parallel);
+//  * activation offload: n_off blocks each way against the stage's busy time.
+static double estimate(const tpipe_plan* P, const CostModel& cm, double* exposed_out) {
+    const tpipe_model_desc& d = P->model;
+    const double tl = layer_fwd_s(d, cm), th = head_fwd_s(d, cm);
+    std::vector<std::vector<std::array<double, 2>>> times;
+    double mk = 0, busy[64];
+    auto dur = [&](int s, int j, int kind) { return op_seconds(P, s, kind, P->order[s][j][1], tl, th); };
+    if (replay_order<double>(P, dur, &mk, busy, &times)) return 1e30;
+    double worst = 0;
+    const double es = d.dtype == TPIPE_BF16 ? 2.0 : 4.0;
+    for (int s = 0; s < P->p; ++s) {
+        double exposed = 0;
+        if (P->offload & TPIPE_OFFLOAD_MODEL_STATE) {
+            const double np = (double)P->chunk_params[s][P->v - 1];
+            double end_b = 0, start_f = mk;
+            for (size_t j = 0; j < P->order[s].size(); ++j) {
+                const COp& op = P->order[s][j];
+                if (op[1] != P->v) continue;
+                if (op[0] == KB) end_b = std::max(end_b, times[s][j][1]);
+                if (op[0] == KF) start_f = std::min(start_f, times[s][j][0]);
+            }
+            const double window = (mk - end_b) + start_f;
+            const double need = (P->offload & TPIPE_OFFLOAD_DEVICE_OPT)
+                                    ? 12.0 * np / cm.bw
+                                    : np * 4.0 / cm.bw + np / cm.host + np * es / cm.bw;
+            exposed += std::max(0.0, need - window);
+        }
+        if (P->offload & TPIPE_OFFLOAD_ACTIVATIONS) {
+            int n_off = 0;
+            uint64_t bytes = 0;
+            for (const tpipe_op& op : P->ops[s])
+                if (op.kind == TPIPE_OP_ACT_H2D) {
+                    ++n_off;
+                    bytes = P->bufs[s][P->events[s][op.alloc_first]].bytes;
+                }
+            exposed += std::max(0.0, n_off * (double)bytes / cm.bw - busy[s]);
+        }
+        worst = std::max(worst, exposed);
+    }
+    if (exposed_out) *exposed_out = worst;
+    return mk + worst;
+}
+
 static int make_plan(const tpipe_model_desc* model, int p, int m, int strategy, int k, int W,
                      int offload, int act_distance, int recomp_layers, const int32_t* stage_layers,
-                     tpipe_plan** out) {
+                     const CostModel& cm, tpipe_plan** out) {
     if ((offload & TPIPE_OFFLOAD_DEVICE_OPT) && !(offload & TPIPE_OFFLOAD_MODEL_STATE))
         return set_error(TPIPE_E_INVALID, "offload: DEVICE_OPT needs MODEL_STATE");
     if ((offload & TPIPE_OFFLOAD_ACTIVATIONS) && strategy != TPIPE_S_TPIPE)
@@ -599,7 +737,7 @@ static int make_plan(const tpipe_model_desc* model, int p, int m, int strategy, 
     P->strategy = strategy;
     P->W = W;
     P->offload = offload;
-    P->act_distance = act_distance > 0 ? act_distance : 2;
+    P->act_distance = act_distance > 0 ? act_distance : 1;   // derived below when 0 (Q12)
     const bool is_il = strategy == TPIPE_S_INTERLEAVE || strategy == TPIPE_S_INTERLEAVE_TRECOMP;
     const bool is_tp = strategy == TPIPE_S_TPIPE || strategy == TPIPE_S_TPIPE_TRECOMP || is_il;
     if (is_il && m % p) {
@@ -680,11 +818,25 @@ static int make_plan(const tpipe_model_desc* model, int p, int m, int strategy, 
         P->order.assign(p, {});
         for (int s = 0; s < p; ++s) P->order[s] = ord[s];
     }
+    if ((offload & TPIPE_OFFLOAD_ACTIVATIONS) && act_distance <= 0) {
+        // release / prefetch a block d compute ops after F / before
+        // B, with d the smallest count of chunk-1 forward times (the shortest
+        // op, cost model) that covers the block's copy at host_link_bps
+        double worst = 1.0;
+        const double tl = layer_fwd_s(*model, cm);
+        for (int s = 0; s < p; ++s) {
+            const ChunkSizes z = chunk_sizes(*model, p, P->v, P->sl[s].data(), s, 1, false);
+            const double copy = (double)z.stash / cm.bw, t1 = P->sl[s][0] * tl;
+            worst = std::max(worst, std::ceil(copy / t1 - 1e-9));
+        }
+        P->act_distance = (int)std::min(16.0, worst);
+    }
     int rc = build(P, trecomp, strategy == TPIPE_S_1F1B_FULL_RECOMP);
     if (rc) {
         delete P;
         return rc;
     }
+    P->est_step_s = estimate(P, cm, &P->est_exposed_s);
     if (!deadlock_free(P)) {
         delete P;
         return set_error(TPIPE_E_DEADLOCK, "instruction streams can deadlock (send window %d)", W);
@@ -699,13 +851,42 @@ static uint64_t max_peak(const tpipe_plan* P) {
     return x;
 }
 
+// Cost-balanced partition (DESIGN R27, SURVEY D-12): the last stage also runs
+// the LM head, worth `head_layers` layers of forward work; choose its layer
+// count n_last >= v minimising the largest stage cost and spread the other
+// L - n_last layers evenly (extra layers on the earliest stages).
+static std::vector<int> balanced_partition(int L, int p, int v, double head_layers) {
+    if (p < 2) return {};
+    double best = 1e30;
+    int best_last = -1;
+    for (int n_last = v; n_last <= L / p; ++n_last) {
+        const int rest = L - n_last;
+        if (rest < v * (p - 1)) break;
+        const int hi = (rest + p - 2) / (p - 1);
+        const double cost = std::max((double)hi, n_last + head_layers);
+        if (cost < best - 1e-9) {
+            best = cost;
+            best_last = n_last;
+        }
+    }
+    if (best_last < 0) return {};
+    std::vector<int> out;
+    const int rest = L - best_last, base = rest / (p - 1), extra = rest % (p - 1);
+    for (int s = 0; s < p - 1; ++s) out.push_back(base + (s < extra ? 1 : 0));
+    out.push_back(best_last);
+    return out;
+}
+
 TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, int32_t n_microbatches,
                              uint64_t hbm_budget_bytes, const tpipe_plan_opts* opts,
                              tpipe_plan** out) {
     if (!out) return set_error(TPIPE_E_INVALID, "out is NULL");
     *out = nullptr;
     if (int rc = validate(model, n_stages, n_microbatches)) return rc;
-    tpipe_plan_opts o{-1, -1, 0, -1, 0, 0, {}};
+    tpipe_plan_opts o{};
+    o.strategy = -1;
+    o.delay_rounds = -1;
+    o.offload = -1;
     if (opts) o = *opts;
     if (o.stage_layers[0] == 0 && model && n_stages > 0 && model->n_layers % n_stages)
         return set_error(TPIPE_E_INVALID, "n_layers must be a positive multiple of n_stages");
@@ -713,11 +894,50 @@ TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, in
     if (o.strategy < -1 || o.strategy > TPIPE_S_INTERLEAVE_TRECOMP) return set_error(TPIPE_E_INVALID, "strategy");
     if (o.delay_rounds < -1) return set_error(TPIPE_E_INVALID, "delay_rounds");
     if (o.recomp_layers < 0) return set_error(TPIPE_E_INVALID, "recomp_layers");
+    if (o.host_link_bps < 0 || o.host_adam_params_per_s < 0 || o.device_flops < 0)
+        return set_error(TPIPE_E_INVALID, "cost model rates must be >= 0");
+    CostModel cm;
+    if (o.host_link_bps > 0) cm.bw = o.host_link_bps;
+    if (o.host_adam_params_per_s > 0) cm.host = o.host_adam_params_per_s;
+    if (o.device_flops > 0) cm.flops = o.device_flops;
+    // cost-balanced partition chosen by the planner (R27), decided once on the
+    // strategy's plain schedule (T-Pipe for auto) and used by every rung
+    int32_t part[64] = {0};
+    bool balanced = false;
+    if (o.stage_layers[0]) {
+        std::copy(o.stage_layers, o.stage_layers + 64, part);
+    } else if (o.balance && n_stages > 1 && !model->layers_chunk[0] && !model->layers_chunk[1]) {
+        const int base = o.strategy >= 0 ? o.strategy : TPIPE_S_TPIPE;
+        const int vv = (base == TPIPE_S_1F1B || base == TPIPE_S_1F1B_FULL_RECOMP) ? 1 : 2;
+        const auto bp = balanced_partition(model->n_layers, n_stages, vv,
+                                           head_fwd_s(*model, cm) / layer_fwd_s(*model, cm));
+        if (!bp.empty()) {
+            int32_t cand[64] = {0};
+            std::copy(bp.begin(), bp.end(), cand);
+            tpipe_plan *U = nullptr, *Bp = nullptr;
+            if (!make_plan(model, n_stages, n_microbatches, base, o.delay_rounds, W, 0, o.act_distance,
+                           o.recomp_layers, part, cm, &U) &&
+                !make_plan(model, n_stages, n_microbatches, base, o.delay_rounds, W, 0, o.act_distance,
+                           o.recomp_layers, cand, cm, &Bp) &&
+                Bp->est_step_s < 0.97 * U->est_step_s) {
+                std::copy(cand, cand + 64, part);
+                balanced = true;
+            }
+            delete U;
+            delete Bp;
+        }
+    }
+    auto finish = [&](tpipe_plan* P) {
+        P->hbm_budget = hbm_budget_bytes;
+        P->balanced = balanced;
+        *out = P;
+        return 0;
+    };
     if (o.strategy >= 0) {
         const int off = o.offload < 0 ? 0 : o.offload;
         tpipe_plan* P = nullptr;
         int rc = make_plan(model, n_stages, n_microbatches, o.strategy, o.delay_rounds, W, off,
-                           o.act_distance, o.recomp_layers, o.stage_layers, &P);
+                           o.act_distance, o.recomp_layers, part, cm, &P);
         if (rc) return rc;
         if (hbm_budget_bytes && max_peak(P) > hbm_budget_bytes) {
             const uint64_t pk = max_peak(P);
@@ -725,41 +945,50 @@ TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, in
             return set_error(TPIPE_E_BUDGET, "peak %llu bytes exceeds budget %llu",
                              (unsigned long long)pk, (unsigned long long)hbm_budget_bytes);
         }
-        P->hbm_budget = hbm_budget_bytes;
-        *out = P;
-        return 0;
+        return finish(P);
     }
-    // auto escalation (fit the budget with the least throughput loss):
-    // T-Pipe -> + T-Recomp of r = 1..n1 chunk-1 layers (R25) -> + model-state
-    // T-Offload (device AdamW streaming if requested in `offload`) with r = 1..n1
+    // auto (fit the budget with the least throughput loss): every rung
+    // that fits is costed by the model (R28) and the cheapest wins; ties go to
+    // the earlier (simpler) rung
     int n1 = model->layers_chunk[0] ? model->layers_chunk[0] : (model->n_layers / n_stages + 1) / 2;
-    if (o.stage_layers[0])
-        for (int s = 0; s < n_stages && s < 64; ++s) n1 = std::max(n1, (o.stage_layers[s] + 1) / 2);
+    if (part[0])
+        for (int s = 0; s < n_stages && s < 64; ++s) n1 = std::max(n1, (part[s] + 1) / 2);
     const int rmin = o.recomp_layers > 0 ? o.recomp_layers : 1;
     const int rmax = o.recomp_layers > 0 ? o.recomp_layers : n1;
-    const int off_flags = TPIPE_OFFLOAD_MODEL_STATE |
-                          (o.offload > 0 ? (o.offload & TPIPE_OFFLOAD_DEVICE_OPT) : 0);
+    const bool ms_ok = o.offload < 0 || (o.offload & TPIPE_OFFLOAD_MODEL_STATE);
+    const bool act_ok = o.offload < 0 || (o.offload & TPIPE_OFFLOAD_ACTIVATIONS);
+    const int off_ms = TPIPE_OFFLOAD_MODEL_STATE | (o.offload > 0 ? (o.offload & TPIPE_OFFLOAD_DEVICE_OPT) : 0);
     std::vector<std::array<int, 3>> ladder;   // {strategy, offload, r}
     ladder.push_back({TPIPE_S_TPIPE, 0, 0});
+    if (ms_ok) ladder.push_back({TPIPE_S_TPIPE, off_ms, 0});
+    if (act_ok) ladder.push_back({TPIPE_S_TPIPE, TPIPE_OFFLOAD_ACTIVATIONS, 0});
+    if (act_ok && ms_ok) ladder.push_back({TPIPE_S_TPIPE, TPIPE_OFFLOAD_ACTIVATIONS | off_ms, 0});
     for (int r = rmin; r <= rmax; ++r) ladder.push_back({TPIPE_S_TPIPE_TRECOMP, 0, r});
-    if (o.offload < 0 || (o.offload & TPIPE_OFFLOAD_MODEL_STATE))
-        for (int r = rmin; r <= rmax; ++r) ladder.push_back({TPIPE_S_TPIPE_TRECOMP, off_flags, r});
-    uint64_t best = 0;
+    if (ms_ok)
+        for (int r = rmin; r <= rmax; ++r) ladder.push_back({TPIPE_S_TPIPE_TRECOMP, off_ms, r});
+    uint64_t best_peak = ~0ull;
+    tpipe_plan* best = nullptr;
     for (auto& rung : ladder) {
         tpipe_plan* P = nullptr;
         int rc = make_plan(model, n_stages, n_microbatches, rung[0], o.delay_rounds, W, rung[1],
-                           o.act_distance, rung[2], o.stage_layers, &P);
-        if (rc) return rc;
-        best = max_peak(P);
-        if (!hbm_budget_bytes || best <= hbm_budget_bytes) {
-            P->hbm_budget = hbm_budget_bytes;
-            *out = P;
-            return 0;
+                           o.act_distance, rung[2], part, cm, &P);
+        if (rc) {
+            if (rc == TPIPE_E_INCOMPAT || rc == TPIPE_E_INVALID) continue;   // rung not applicable
+            delete best;
+            return rc;
         }
-        delete P;
+        best_peak = std::min(best_peak, max_peak(P));
+        if ((!hbm_budget_bytes || max_peak(P) <= hbm_budget_bytes) &&
+            (!best || P->est_step_s < best->est_step_s * (1.0 - 1e-9))) {
+            delete best;
+            best = P;
+        } else {
+            delete P;
+        }
     }
+    if (best) return finish(best);
     return set_error(TPIPE_E_BUDGET, "no escalation fits: best peak %llu > budget %llu",
-                     (unsigned long long)best, (unsigned long long)hbm_budget_bytes);
+                     (unsigned long long)best_peak, (unsigned long long)hbm_budget_bytes);
 }
 
 TP_API void tpipe_plan_destroy(tpipe_plan* plan) { delete plan; }
@@ -779,6 +1008,9 @@ TP_API int tpipe_plan_get_info(const tpipe_plan* P, tpipe_plan_info* out) {
     out->n_channels = (int32_t)P->channels.size();
     out->params_total = P->params_total;
     out->recomp_layers = P->rl;
+    out->est_step_s = P->est_step_s;
+    out->est_exposed_offload_s = P->est_exposed_s;
+    out->balanced = P->balanced ? 1 : 0;
     return 0;
 }
 
@@ -828,60 +1060,6 @@ TP_API int tpipe_plan_stage_layers(const tpipe_plan* P, int32_t s, int32_t out[2
 TP_API int tpipe_plan_chunk_params(const tpipe_plan* P, int32_t s, int32_t c, uint64_t* n) {
     if (!P || !n || s < 0 || s >= P->p || c < 1 || c > P->v) return set_error(TPIPE_E_INVALID, "stage/chunk");
     *n = P->chunk_params[s][c - 1];
-    return 0;
-}
-
-// ASAP replay of the compute order with per-op durations dur(s, j) (j = index
-// of the op in stage s's compute order); returns makespan and busy per stage
-template <typename T, typename DurFn>
-static int replay_order(const tpipe_plan* P, DurFn dur, T* makespan, T* busy_out) {
-    const int p = P->p, v = P->v;
-    const bool rec = P->strategy == TPIPE_S_TPIPE_TRECOMP || P->strategy == TPIPE_S_INTERLEAVE_TRECOMP;
-    std::map<std::tuple<int, int, int, int>, T> endt;  // (stage, kind, chunk, mb)
-    std::vector<size_t> pos(p, 0);
-    std::vector<T> freet(p, 0), busy(p, 0);
-    size_t total = 0, done = 0;
-    for (auto& o : P->order) total += o.size();
-    while (done < total) {
-        bool prog = false;
-        for (int s = 0; s < p; ++s) {
-            while (pos[s] < P->order[s].size()) {
-                const COp& op = P->order[s][pos[s]];
-                const int kind = op[0], c = op[1], i = op[2];
-                std::vector<std::tuple<int, int, int, int>> deps;
-                if (kind == KF) {
-                    if (s > 0) deps.push_back({s - 1, KF, c, i});
-                    else if (c > 1) deps.push_back({p - 1, KF, c - 1, i});
-                } else if (kind == KR) {
-                    deps.push_back({s, KF, c, i});
-                } else {
-                    deps.push_back({s, KF, c, i});
-                    if (rec && c == 1) deps.push_back({s, KR, c, i});
-                    if (s < p - 1) deps.push_back({s + 1, KB, c, i});
-                    else if (c < v) deps.push_back({0, KB, c + 1, i});
-                }
-                T t0 = freet[s];
-                bool ready = true;
-                for (auto& dd : deps) {
-                    auto it = endt.find(dd);
-                    if (it == endt.end()) { ready = false; break; }
-                    t0 = std::max(t0, it->second);
-                }
-                if (!ready) break;
-                const T t1 = t0 + dur(s, (int)pos[s], kind);
-                endt[{s, kind, c, i}] = t1;
-                freet[s] = t1;
-                busy[s] += t1 - t0;
-                ++pos[s];
-                ++done;
-                prog = true;
-            }
-        }
-        if (!prog) return set_error(TPIPE_E_DEADLOCK, "compute order deadlocks");
-    }
-    *makespan = 0;
-    for (int s = 0; s < p; ++s) *makespan = std::max(*makespan, freet[s]);
-    for (int s = 0; s < 64; ++s) busy_out[s] = s < p ? busy[s] : 0;
     return 0;
 }
 

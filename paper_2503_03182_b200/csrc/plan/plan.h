@@ -19,6 +19,8 @@ struct tpipe_plan {
     int rl_of(int s) const { return rl < sl[s][0] ? rl : sl[s][0]; }
     uint64_t params_total = 0;
     uint64_t hbm_budget = 0;   // per-stage budget the plan was fitted to (0 = none)
+    double est_step_s = 0, est_exposed_s = 0;   // cost model (DESIGN R28)
+    bool balanced = false;     // cost-balanced partition chosen by the planner
     // per stage
     std::vector<std::vector<tpipe_op>> ops;
     std::vector<std::vector<tpipe_buf>> bufs;

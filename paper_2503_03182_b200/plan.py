@@ -47,13 +47,16 @@ class Plan:
 
     def __init__(self, model: Model, n_stages: int, n_microbatches: int, hbm_budget: int = 0,
                  strategy="tpipe", delay_rounds: int = -1, send_window: int = 0, offload: int = 0,
-                 act_distance: int = 0, recomp_layers: int = 0, stage_layers=None):
+                 act_distance: int = 0, recomp_layers: int = 0, stage_layers=None,
+                 host_link_bps: float = 0.0, host_adam_params_per_s: float = 0.0,
+                 device_flops: float = 0.0, balance: bool = False):
         L = lib()
         st = -1 if strategy in (None, "auto") else STRATEGY.get(strategy, strategy)
         if st < 0 and offload == 0:
             offload = -1
         sl = (C.c_int32 * 64)(*(list(stage_layers or [])[:64]))
-        opts = D.PlanOpts(st, delay_rounds, send_window, offload, act_distance, recomp_layers, sl)
+        opts = D.PlanOpts(st, delay_rounds, send_window, offload, act_distance, recomp_layers, sl,
+                          host_link_bps, host_adam_params_per_s, device_flops, 1 if balance else 0)
         self._h = C.c_void_p()
         self.model = model
         check(L.tpipe_plan_create(C.byref(model.c()), n_stages, n_microbatches, hbm_budget,
@@ -65,6 +68,9 @@ class Plan:
                                                        info.send_window, info.offload)
         self.act_distance = info.act_distance
         self.recomp_layers = info.recomp_layers
+        self.est_step_s = info.est_step_s
+        self.est_exposed_offload_s = info.est_exposed_offload_s
+        self.balanced = bool(info.balanced)
         # per-stage (chunk-1, chunk-2) layers (DESIGN R27); == [layers_chunk] * p when uniform
         self.partition = []
         for s in range(self.p):

@@ -54,3 +54,16 @@ def test_balanced_partition_and_choice():
     assert bench.choose_partition(md, 8, 32, "tpipe") == [4, 3, 3, 3, 3, 3, 3, 2]
     assert bench.choose_partition(md, 4, 32, "tpipe") is None
     assert bench.choose_partition(md, 1, 32, "tpipe") is None
+
+
+def test_gpus_n_without_ranks_refuses():
+    """`bench.py --gpus N` outside torchrun launches N ranks itself, or — on a
+    box with fewer than N GPUs (here: none) — exits 2 with a clear error
+    instead of printing a one-GPU virtual-pipeline number labelled N GPUs."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert r.returncode == 2
+    assert r.stdout.strip() == ""
+    assert "needs 2 GPUs" in r.stderr and "--virtual-stages" in r.stderr
