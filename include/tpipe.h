@@ -136,7 +136,13 @@ typedef struct {
     double device_flops;
     int32_t balance;       /* 1: use the cost-balanced stage_layers partition (the last stage
                               also runs the LM head, SURVEY D-12) when the modeled step is >= 3%
-                              shorter than the uniform split; ignored if stage_layers is set */
+                              shorter than the uniform split; ignored if stage_layers is set.
+                              The partition is found by steepest descent over per-stage layer
+                              counts and chunk splits on the cost model's ASAP replay of the
+                              strategy's own order (duration-aware T-Pipe, SURVEY NEXT-5,
+                              DESIGN R29), started from the uniform split and the R27 closed form */
+    int32_t stage_chunk1[64]; /* with stage_layers at v = 2: chunk-1 layers of stage s
+                              (1 .. n(s)-1); 0 = ceil(n(s)/2) */
 } tpipe_plan_opts;
 
 enum {

@@ -132,6 +132,17 @@ int tpipe_k_ce_fwd(const float* logits, const int* tgt, float* lse, float* loss_
 int tpipe_k_ce_bwd(int dtype, const float* logits, const int* tgt, const float* lse,
                    void* dlogits, float scale, int rows, int V, void* stream);
 
+/* Fused LM head + softmax cross-entropy (K8, DESIGN R30), bf16, tcgen05:
+ * logits z = x · W^T (x [rows, h] bf16 row-major, W [V, h] bf16 row-major)
+ * are never written to HBM. Pass 1 (head GEMM, epilogue) -> per row and
+ * 64-column group (max, sum exp(z - max)) + z[r, tgt[r]]; combine ->
+ * lse[r] (fp32) and loss_out[0] += scale * sum_r (lse[r] - z[r, tgt[r]]) in
+ * row order; pass 2 (head GEMM again) -> dlogits [rows, V] bf16 =
+ * scale * (exp(z - lse) - onehot(tgt)). ws: fp32 scratch of
+ * 2*rows*ceil(V/64) + 2*rows floats. V % 64 == 0, h % 64 == 0. */
+int tpipe_k_head_ce(const void* x, const void* w, const int* tgt, float* lse, void* dlogits,
+                    float* loss_out, float scale, int rows, int V, int h, float* ws, void* stream);
+
 /* out[n] += sum_r X[r, n] (fp32, deterministic). ws fp32 [ceil(rows/16)*n]. */
 int tpipe_k_colsum(int dtype, const void* X, float* out, float* ws, int rows, int n,
                    void* stream);

@@ -35,6 +35,7 @@ class ModelDesc:
     dtype: int = BF16
     layers_chunk: tuple = (0, 0)  # per-stage (chunk1, chunk2) layers; 0 = auto
     stage_layers: tuple = ()      # cost-balanced partition: layers of each stage (DESIGN R27)
+    stage_chunk1: tuple = ()      # with stage_layers, v=2: chunk-1 layers of each stage (R29)
 
     @property
     def es(self) -> int:
@@ -55,7 +56,12 @@ def layers_per_chunk(d: ModelDesc, p: int, v: int, s: int = 0):
         n = d.stage_layers[s]
         if n < v:
             raise ValueError("stage_layers")
-        return (n,) if v == 1 else ((n + 1) // 2, n // 2)
+        if v == 1:
+            return (n,)
+        n1 = d.stage_chunk1[s] if d.stage_chunk1 and d.stage_chunk1[s] else (n + 1) // 2
+        if not 1 <= n1 <= n - 1:
+            raise ValueError("stage_chunk1")
+        return (n1, n - n1)
     if d.n_layers % p:
         raise ValueError("n_layers")
     n = d.n_layers // p
@@ -143,7 +149,11 @@ def sizes(d: ModelDesc, p: int, v: int, s: int, c: int, full_recomp: bool = Fals
     if full_recomp:
         ws_b += LS - M * h * es                  # one-layer recompute buffer
     if head:
-        ws_b += 2 * M * h * es + 4 * M * V + M * V * es
+        # LN_f output and its gradient, dlogits (es); bf16 runs the fused LM head
+        # + CE (DESIGN R30): per-row (max, sum-exp) partials per 64-column group
+        # (8 B), target logit and row loss (4 B each) instead of fp32 logits
+        ws_b += 2 * M * h * es + M * V * es
+        ws_b += 8 * M * (-(-V // 64)) + 8 * M if d.dtype == BF16 else 4 * M * V
     if emb:
         ws_b += 8 * M
     return {

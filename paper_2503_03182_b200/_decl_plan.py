@@ -15,7 +15,7 @@ class PlanOpts(C.Structure):
     _fields_ = [("strategy", i32), ("delay_rounds", i32), ("send_window", i32), ("offload", i32),
                 ("act_distance", i32), ("recomp_layers", i32), ("stage_layers", i32 * 64),
                 ("host_link_bps", C.c_double), ("host_adam_params_per_s", C.c_double),
-                ("device_flops", C.c_double), ("balance", i32)]
+                ("device_flops", C.c_double), ("balance", i32), ("stage_chunk1", i32 * 64)]
 
 
 class Op(C.Structure):

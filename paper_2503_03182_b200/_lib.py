@@ -59,6 +59,7 @@ def _declare(L):
     L.tpipe_k_embed_bwd.argtypes = [i32, vp, vp, vp, vp, vp, i32, i32, i32, vp]
     L.tpipe_k_ce_fwd.argtypes = [vp, vp, vp, vp, f32, i32, i32, vp]
     L.tpipe_k_ce_bwd.argtypes = [i32, vp, vp, vp, vp, f32, i32, i32, vp]
+    L.tpipe_k_head_ce.argtypes = [vp, vp, vp, vp, vp, vp, f32, i32, i32, i32, vp, vp]
     L.tpipe_k_colsum.argtypes = [i32, vp, vp, vp, i32, i32, vp]
     L.tpipe_k_adamw.argtypes = [i32, vp, vp, vp, vp, vp, i64, i32, f32, f32, f32, f32, f32, f32,
                                 f32, vp]

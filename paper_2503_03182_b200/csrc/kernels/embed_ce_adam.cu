@@ -235,6 +235,65 @@ __global__ void ce_bwd4_kernel(const float* __restrict__ logits, const int* __re
     reinterpret_cast<uint2*>(d)[i4] = u;
 }
 
+// one warp per row: lane l folds groups l, l+32, ... in order, then a fixed
+// xor-tree combines the lanes (deterministic)
+__global__ void ce_combine_kernel(const float2* __restrict__ part, int ngrp, const float* __restrict__ zt,
+                                  float* __restrict__ lse, float* __restrict__ lrow, int rows) {
+    const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (r >= rows) return;
+    const float2* p = part + (size_t)r * ngrp;
+    float m = -INFINITY, s = 0.f;
+    for (int j = lane; j < ngrp; j += 32) {
+        const float2 q = p[j];
+        const float mm = fmaxf(m, q.x);
+        s = (m == -INFINITY ? 0.f : s * expf(m - mm)) + (q.x == -INFINITY ? 0.f : q.y * expf(q.x - mm));
+        m = mm;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+        const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+        const float mm = fmaxf(m, m2);
+        s = (m == -INFINITY ? 0.f : s * expf(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * expf(m2 - mm));
+        m = mm;
+    }
+    if (lane == 0) {
+        const float L = m + logf(s);
+        lse[r] = L;
+        lrow[r] = L - zt[r];
+    }
+}
+
+// one block: loss_out[0] += scale * sum_r x[r]; fixed tree order
+__global__ void ordered_sum_kernel(const float* __restrict__ x, float* __restrict__ loss_out, float scale,
+                                   int rows) {
+    __shared__ float red[32];
+    float s = 0.f;
+    for (int r = threadIdx.x; r < rows; r += blockDim.x) s += x[r];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+        v = warp_sum(v);
+        if (threadIdx.x == 0) loss_out[0] += v * scale;
+    }
+}
+
+int ce_combine(const float* part, int ngrp, const float* zt, float* lse, float* lrow, float* loss_out,
+               float scale, int rows, cudaStream_t st) {
+    if (rows <= 0) return 0;
+    ce_combine_kernel<<<(rows + 7) / 8, 256, 0, st>>>(reinterpret_cast<const float2*>(part), ngrp, zt, lse,
+                                                       lrow, rows);
+    int n = 1;
+    if (loss_out) {
+        ordered_sum_kernel<<<1, 1024, 0, st>>>(lrow, loss_out, scale, rows);
+        ++n;
+    }
+    note_launches(n);
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
 int ce_fwd(const float* logits, const int* tgt, float* lse, float* loss_out, float scale, int rows,
            int V, cudaStream_t st) {
     if (rows <= 0) return 0;

@@ -674,6 +674,14 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
                     while (ld_acquire_u32(sk_flags + cc * CG + rank) != epoch) {
                     }
             }
+            // fused LM head + CE (K8): this thread owns row m of the tile
+            const bool lse_mode = g.epi == EPI_LSE_PART, ce_mode = g.epi == EPI_CE_GRAD;
+            int tgt = -1;
+            float lse_m = 0.f, gmax = -INFINITY, gsum = 0.f;
+            if ((lse_mode || ce_mode) && m < g.M) {
+                tgt = g.targets[m];
+                if (ce_mode) lse_m = g.lse[m];
+            }
 #pragma unroll 1
             for (int c = c_lo; c < c_hi; ++c) {
                 uint32_t r[32];
@@ -696,7 +704,46 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
                         v[4 * q + 3] += p.w;
                     }
                 }
-                epi_math(g, m, n0, m < g.M, v, v2);
+                if (lse_mode) {
+                    // online (max, sum exp) over the 64-column group, fp32 from
+                    // the accumulators; the target logit captured in passing
+                    float cm = v[0];
+#pragma unroll
+                    for (int j = 1; j < 32; ++j) cm = fmaxf(cm, v[j]);
+                    if (cm > gmax) {
+                        gsum *= exp2f((gmax - cm) * 1.4426950408889634f);
+                        gmax = cm;
+                    }
+                    float zt = 0.f;
+                    bool hit = false;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        gsum += exp2f((v[j] - gmax) * 1.4426950408889634f);
+                        if (n0 + j == tgt) {
+                            zt = v[j];
+                            hit = true;
+                        }
+                    }
+                    if (hit) g.zt[m] = zt;
+                    if ((((n0 + 32) & 63) == 0 || n0 + 32 >= g.N)) {
+                        if (m < g.M)
+                            reinterpret_cast<float2*>(g.part)[(size_t)m * ((g.N + 63) >> 6) + (n0 >> 6)] =
+                                make_float2(gmax, gsum);
+                        gmax = -INFINITY;
+                        gsum = 0.f;
+                    }
+                    continue;
+                }
+                if (ce_mode) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        float pj = exp2f((v[j] - lse_m) * 1.4426950408889634f);
+                        if (n0 + j == tgt) pj -= 1.f;
+                        v[j] = pj * g.scale;
+                    }
+                } else {
+                    epi_math(g, m, n0, m < g.M, v, v2);
+                }
                 stage_store(mystg + sb * Cfg::STG_BUF, v, f32out, reduce, &tmC, n0, m0, lane);
                 sb ^= 1;
                 if (two) {
@@ -833,9 +880,13 @@ static int launch_tc(const GemmDesc& g, cudaStream_t st) {
     // output maps: 32 x 32 boxes (fp32: 128 B rows, 128B swizzle; bf16: 64 B rows, 64B swizzle)
     CUtensorMap tc, tc2;
     const bool f32out = (g.epi == EPI_ACC_F32 || g.epi == EPI_STORE_F32);
-    rc = make_map(&tc, g.C, g.N, g.M, g.ldc, 32, 32, f32out,
-                  f32out ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
-    if (rc) return rc;
+    if (g.epi == EPI_LSE_PART) {
+        tc = ta;   // no C store: the map is never used
+    } else {
+        rc = make_map(&tc, g.C, g.N, g.M, g.ldc, 32, 32, f32out,
+                      f32out ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
+        if (rc) return rc;
+    }
     if (g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU) {
         rc = make_map(&tc2, g.C2, g.N, g.M, g.ldc2, 32, 32, false, CU_TENSOR_MAP_SWIZZLE_64B);
         if (rc) return rc;
@@ -880,7 +931,8 @@ static int launch_majors_ew(const GemmDesc& g, cudaStream_t st) {
 template <int BN, int CG>
 static int launch_majors(const GemmDesc& g, cudaStream_t st) {
     // (all three store bf16 only: the 8-warp variant stages 2 KB chunks)
-    const bool heavy = g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU || g.epi == EPI_BIAS_RES;
+    const bool heavy = g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU || g.epi == EPI_BIAS_RES ||
+                       g.epi == EPI_LSE_PART || g.epi == EPI_CE_GRAD;
     return heavy ? launch_majors_ew<BN, CG, 8>(g, st) : launch_majors_ew<BN, CG, 4>(g, st);
 }
 
@@ -888,7 +940,9 @@ int gemm_tc(const GemmDesc& g, cudaStream_t st) {
     if (g.M <= 0 || g.N <= 0) return 0;
     if (g.K <= 0) return -4;
     // TMA: 16-byte aligned bases and row strides; 32-column epilogue chunks
-    if ((g.N % 32) || (g.lda % 8) || (g.ldb % 8) || (g.ldc % 8) ||
+    if ((g.epi == EPI_LSE_PART || g.epi == EPI_CE_GRAD) && (!g.targets || (g.epi == EPI_LSE_PART ? !g.part || !g.zt : !g.lse)))
+        return -4;
+    if ((g.N % 32) || (g.lda % 8) || (g.ldb % 8) || (g.epi != EPI_LSE_PART && (g.ldc % 8)) ||
         ((g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU) && (g.ldc2 % 8)))
         return -5;
     // CTA-pair 256 x 256 tiles: per SM they move 32 KB of operands per 64-deep

@@ -18,6 +18,11 @@ enum Epi : int {
     EPI_DGELU = 4,      // C(es)  = acc * gelu'(U[m,n]); C2(es) = gelu(U[m,n])
     EPI_ACC_F32 = 5,    // Cf32  += acc
     EPI_STORE_F32 = 6,  // Cf32   = acc
+    // fused LM head + softmax cross-entropy (K8, DESIGN R30; tcgen05 path only).
+    // The logits z = acc never reach HBM:
+    EPI_LSE_PART = 7,   // part[m][n/64] = (max, sum exp(z - max)) over each 64-column
+                        // group; zt[m] = z[m, targets[m]]; no C store
+    EPI_CE_GRAD = 8,    // C(bf16) = (exp(z - lse[m]) - [n == targets[m]]) * scale
 };
 
 struct GemmDesc {
@@ -30,7 +35,17 @@ struct GemmDesc {
     const void* res = nullptr; long ldr = 0;
     void* C2 = nullptr; long ldc2 = 0;
     const void* aux = nullptr; long ldaux = 0;
+    // EPI_LSE_PART / EPI_CE_GRAD
+    const int* targets = nullptr;
+    const float* lse = nullptr;
+    float* part = nullptr;     // [M][ceil(N/64)][2]
+    float* zt = nullptr;       // [M]
+    float scale = 0.f;
 };
+
+// 64-column groups of the fused head's LSE partials (the narrowest column span
+// one epilogue thread owns: BN = 128 split over two 4-warp groups)
+inline int ce_groups(int V) { return (V + 63) / 64; }
 
 // dtype DT_BF16 -> tcgen05/TMA tensor-core kernel; DT_FP32 -> exact fp32 SIMT kernel.
 int gemm(int dtype, const GemmDesc& g, cudaStream_t st);
@@ -90,6 +105,11 @@ int ce_fwd(const float* logits, const int* tgt, float* lse, float* loss_out, flo
 // dlogits(es) [rows, V] = (exp(logit - lse) - onehot) * scale
 int ce_bwd(int dtype, const float* logits, const int* tgt, const float* lse, void* dlogits,
            float scale, int rows, int V, cudaStream_t st);
+// fused LM head + CE (K8, DESIGN R30): combine the head GEMM's per-128-column
+// (max, sum exp) partials [rows][ngrp] in a fixed order into lse[r]; lrow[r] =
+// lse[r] - zt[r] (row CE); loss_out[0] += scale * sum_r lrow[r] in a fixed order.
+int ce_combine(const float* part, int ngrp, const float* zt, float* lse, float* lrow, float* loss_out,
+               float scale, int rows, cudaStream_t st);
 
 // ---------------------------------------------------------------- reductions
 // out[n] += sum_r X[r, n] (deterministic; 16-row partials into ws fp32 [ceil(rows/16), n]).

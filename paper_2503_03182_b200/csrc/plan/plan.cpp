@@ -87,7 +87,11 @@ static ChunkSizes chunk_sizes(const tpipe_model_desc& d, int p, int v, const int
     if (head) ws_f += M * h * es;   // LN_f output only: logits / CE run in the head backward
     uint64_t ws_b = M * (2 * f + 8 * h) * es + 4 * a * M + 4 * nb * std::max(f + 3 * h, 6 * h);
     if (full_recomp) ws_b += LS - M * h * es;
-    if (head) ws_b += 2 * M * h * es + 4 * M * V + M * V * es;
+    // head: LN_f out / grad; bf16: dlogits + the fused head's LSE partials
+    // (8 B per 64-column group), target logit and row loss (K8, R30); fp32:
+    // fp32 logits + dlogits
+    if (head) ws_b += 2 * M * h * es + M * V * es +
+                      (d.dtype == TPIPE_BF16 ? 8 * M * ((V + 63) / 64) + 8 * M : 4 * M * V);
     if (emb) ws_b += 8 * M;
     z.ws_f = ws_f;
     z.ws_b = ws_b;
@@ -724,7 +728,7 @@ static double estimate(const tpipe_plan* P, const CostModel& cm, double* exposed
 
 static int make_plan(const tpipe_model_desc* model, int p, int m, int strategy, int k, int W,
                      int offload, int act_distance, int recomp_layers, const int32_t* stage_layers,
-                     const CostModel& cm, tpipe_plan** out) {
+                     const int32_t* stage_chunk1, const CostModel& cm, tpipe_plan** out) {
     if ((offload & TPIPE_OFFLOAD_DEVICE_OPT) && !(offload & TPIPE_OFFLOAD_MODEL_STATE))
         return set_error(TPIPE_E_INVALID, "offload: DEVICE_OPT needs MODEL_STATE");
     if ((offload & TPIPE_OFFLOAD_ACTIVATIONS) && strategy != TPIPE_S_TPIPE)
@@ -758,7 +762,12 @@ static int make_plan(const tpipe_model_desc* model, int p, int m, int strategy, 
                                  "(and layers_chunk {0,0})", s, ns, vv);
             }
             sum += ns;
-            P->sl.push_back(P->v == 2 ? std::array<int, 2>{(ns + 1) / 2, ns / 2} : std::array<int, 2>{ns, 0});
+            const int c1 = (stage_chunk1 && stage_chunk1[s] > 0) ? stage_chunk1[s] : (ns + 1) / 2;
+            if (P->v == 2 && (c1 < 1 || c1 > ns - 1)) {
+                delete P;
+                return set_error(TPIPE_E_INVALID, "stage_chunk1[%d] = %d: need 1 .. %d", s, c1, ns - 1);
+            }
+            P->sl.push_back(P->v == 2 ? std::array<int, 2>{c1, ns - c1} : std::array<int, 2>{ns, 0});
         }
         if (sum != model->n_layers) {
             delete P;
@@ -877,6 +886,94 @@ static std::vector<int> balanced_partition(int L, int p, int v, double head_laye
     return out;
 }
 
+// Modeled makespan of a plan's compute order with per-stage (chunk-1, chunk-2)
+// layer counts `sl` (no offload terms): the cost model's ASAP replay.
+static double order_makespan(tpipe_plan* S, const std::vector<std::array<int, 2>>& sl, const CostModel& cm) {
+    S->sl = sl;
+    const double tl = layer_fwd_s(S->model, cm), th = head_fwd_s(S->model, cm);
+    double mk = 0, busy[64];
+    auto dur = [&](int s, int j, int kind) { return op_seconds(S, s, kind, S->order[s][j][1], tl, th); };
+    if (replay_order<double>(S, dur, &mk, busy)) return 1e30;
+    return mk;
+}
+
+// Duration-aware partition (DESIGN R29): steepest descent over
+// per-stage layer counts n(s) and (v = 2) chunk splits n1(s), minimising the
+// modeled makespan of the plan's own order (T-Pipe's slot order stays the
+// paper's; what adapts to the unequal durations — the LM head on the last
+// stage's deep chunk — is how many layers each stage and chunk holds).
+// Moves, in this fixed order: one layer from stage i to stage j (both chunks
+// re-split ceil/floor), then n1(s) +- 1; the best strictly improving move is
+// taken until none improves. Started from the uniform split and from the R27
+// closed form; the better end point wins (ties: uniform start).
+static double search_partition(const tpipe_plan* U, const CostModel& cm, std::vector<int>* n_out,
+                               std::vector<int>* c1_out) {
+    tpipe_plan S = *U;   // order, p, v, strategy, model, rl
+    const int p = S.p, v = S.v, L = S.model.n_layers;
+    auto split = [&](int n) { return v == 2 ? std::array<int, 2>{(n + 1) / 2, n / 2} : std::array<int, 2>{n, 0}; };
+    auto descend = [&](std::vector<std::array<int, 2>> sl) {
+        double cur = order_makespan(&S, sl, cm);
+        for (int it = 0; it < 256; ++it) {
+            double best = cur;
+            std::vector<std::array<int, 2>> best_sl;
+            for (int i = 0; i < p; ++i)
+                for (int j = 0; j < p; ++j) {
+                    if (i == j) continue;
+                    const int ni = sl[i][0] + sl[i][1], nj = sl[j][0] + sl[j][1];
+                    if (ni - 1 < v) continue;
+                    auto t = sl;
+                    t[i] = split(ni - 1);
+                    t[j] = split(nj + 1);
+                    const double c = order_makespan(&S, t, cm);
+                    if (c < best * (1.0 - 1e-12)) {
+                        best = c;
+                        best_sl = t;
+                    }
+                }
+            if (v == 2)
+                for (int s = 0; s < p; ++s)
+                    for (int dlt : {1, -1}) {
+                        auto t = sl;
+                        t[s][0] += dlt;
+                        t[s][1] -= dlt;
+                        if (t[s][0] < 1 || t[s][1] < 1) continue;
+                        const double c = order_makespan(&S, t, cm);
+                        if (c < best * (1.0 - 1e-12)) {
+                            best = c;
+                            best_sl = t;
+                        }
+                    }
+            if (best_sl.empty()) break;
+            sl = best_sl;
+            cur = best;
+        }
+        return std::make_pair(cur, sl);
+    };
+    std::vector<std::array<int, 2>> starts[2];
+    starts[0] = U->sl;
+    const auto r27 = balanced_partition(L, p, v, head_fwd_s(S.model, cm) / layer_fwd_s(S.model, cm));
+    double best = 1e30;
+    std::vector<std::array<int, 2>> best_sl;
+    for (int k = 0; k < 2; ++k) {
+        if (k == 1) {
+            if (r27.empty()) break;
+            for (int x : r27) starts[1].push_back(split(x));
+        }
+        auto r = descend(starts[k]);
+        if (r.first < best * (1.0 - 1e-12)) {
+            best = r.first;
+            best_sl = r.second;
+        }
+    }
+    n_out->clear();
+    c1_out->clear();
+    for (auto& x : best_sl) {
+        n_out->push_back(x[0] + x[1]);
+        c1_out->push_back(x[0]);
+    }
+    return best;
+}
+
 TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, int32_t n_microbatches,
                              uint64_t hbm_budget_bytes, const tpipe_plan_opts* opts,
                              tpipe_plan** out) {
@@ -900,31 +997,29 @@ TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, in
     if (o.host_link_bps > 0) cm.bw = o.host_link_bps;
     if (o.host_adam_params_per_s > 0) cm.host = o.host_adam_params_per_s;
     if (o.device_flops > 0) cm.flops = o.device_flops;
-    // cost-balanced partition chosen by the planner (R27), decided once on the
-    // strategy's plain schedule (T-Pipe for auto) and used by every rung
-    int32_t part[64] = {0};
+    // cost-balanced, duration-aware partition chosen by the planner (R27 / R29),
+    // decided once on the strategy's plain schedule (T-Pipe for auto) and used
+    // by every rung
+    int32_t part[64] = {0}, chunk1[64] = {0};
     bool balanced = false;
     if (o.stage_layers[0]) {
         std::copy(o.stage_layers, o.stage_layers + 64, part);
+        std::copy(o.stage_chunk1, o.stage_chunk1 + 64, chunk1);
     } else if (o.balance && n_stages > 1 && !model->layers_chunk[0] && !model->layers_chunk[1]) {
         const int base = o.strategy >= 0 ? o.strategy : TPIPE_S_TPIPE;
-        const int vv = (base == TPIPE_S_1F1B || base == TPIPE_S_1F1B_FULL_RECOMP) ? 1 : 2;
-        const auto bp = balanced_partition(model->n_layers, n_stages, vv,
-                                           head_fwd_s(*model, cm) / layer_fwd_s(*model, cm));
-        if (!bp.empty()) {
-            int32_t cand[64] = {0};
-            std::copy(bp.begin(), bp.end(), cand);
-            tpipe_plan *U = nullptr, *Bp = nullptr;
-            if (!make_plan(model, n_stages, n_microbatches, base, o.delay_rounds, W, 0, o.act_distance,
-                           o.recomp_layers, part, cm, &U) &&
-                !make_plan(model, n_stages, n_microbatches, base, o.delay_rounds, W, 0, o.act_distance,
-                           o.recomp_layers, cand, cm, &Bp) &&
-                Bp->est_step_s < 0.97 * U->est_step_s) {
-                std::copy(cand, cand + 64, part);
+        tpipe_plan* U = nullptr;
+        if (!make_plan(model, n_stages, n_microbatches, base, o.delay_rounds, W, 0, o.act_distance,
+                       o.recomp_layers, part, chunk1, cm, &U)) {
+            std::vector<int> bn, bc;
+            const double best = search_partition(U, cm, &bn, &bc);
+            if (best < 0.97 * U->est_step_s) {
+                for (int s = 0; s < n_stages; ++s) {
+                    part[s] = bn[s];
+                    chunk1[s] = U->v == 2 ? bc[s] : 0;
+                }
                 balanced = true;
             }
             delete U;
-            delete Bp;
         }
     }
     auto finish = [&](tpipe_plan* P) {
@@ -937,7 +1032,7 @@ TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, in
         const int off = o.offload < 0 ? 0 : o.offload;
         tpipe_plan* P = nullptr;
         int rc = make_plan(model, n_stages, n_microbatches, o.strategy, o.delay_rounds, W, off,
-                           o.act_distance, o.recomp_layers, part, cm, &P);
+                           o.act_distance, o.recomp_layers, part, chunk1, cm, &P);
         if (rc) return rc;
         if (hbm_budget_bytes && max_peak(P) > hbm_budget_bytes) {
             const uint64_t pk = max_peak(P);
@@ -971,7 +1066,7 @@ TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, in
     for (auto& rung : ladder) {
         tpipe_plan* P = nullptr;
         int rc = make_plan(model, n_stages, n_microbatches, rung[0], o.delay_rounds, W, rung[1],
-                           o.act_distance, rung[2], part, cm, &P);
+                           o.act_distance, rung[2], part, chunk1, cm, &P);
         if (rc) {
             if (rc == TPIPE_E_INCOMPAT || rc == TPIPE_E_INVALID) continue;   // rung not applicable
             delete best;

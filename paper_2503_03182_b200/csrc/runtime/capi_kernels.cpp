@@ -135,6 +135,33 @@ TP_API int tpipe_k_ce_bwd(int dtype, const float* logits, const int* tgt, const 
     return launch_rc(ce_bwd(dtype, logits, tgt, lse, dlogits, scale, rows, V, S(stream)), "ce_bwd");
 }
 
+TP_API int tpipe_k_head_ce(const void* x, const void* w, const int* tgt, float* lse, void* dlogits,
+                           float* loss_out, float scale, int rows, int V, int h, float* ws, void* stream) {
+    if (!x || !w || !tgt || !lse || !dlogits || !ws) return set_error(TPIPE_E_INVALID, "NULL argument");
+    if (V % 64 || h % 64 || rows <= 0) return set_error(TPIPE_E_INVALID, "V, h multiples of 64; rows > 0");
+    const int ng = ce_groups(V);
+    float* part = ws;
+    float* zt = ws + 2L * rows * ng;
+    float* lrow = zt + rows;
+    GemmDesc g;
+    g.M = rows; g.N = V; g.K = h;
+    g.A = x; g.lda = h; g.a_kmajor = 1;
+    g.B = w; g.ldb = h; g.b_kmajor = 1;
+    g.epi = EPI_LSE_PART;
+    g.targets = tgt;
+    g.part = part;
+    g.zt = zt;
+    if (int rc = launch_rc(gemm(DT_BF16, g, S(stream)), "head gemm (lse)")) return rc;
+    if (int rc = launch_rc(ce_combine(part, ng, zt, lse, lrow, loss_out, scale, rows, S(stream)), "ce_combine"))
+        return rc;
+    g.epi = EPI_CE_GRAD;
+    g.lse = lse;
+    g.C = dlogits;
+    g.ldc = V;
+    g.scale = scale;
+    return launch_rc(gemm(DT_BF16, g, S(stream)), "head gemm (dlogits)");
+}
+
 TP_API int tpipe_k_colsum(int dtype, const void* X, float* out, float* ws, int rows, int n,
                           void* stream) {
     if (int e = chk_dtype(dtype)) return e;

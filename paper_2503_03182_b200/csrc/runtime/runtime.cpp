@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <map>
@@ -82,6 +83,12 @@ struct ChunkState {
 
 struct StageState {
     int s = 0;
+    // compute stream of this stage: the runtime stream, or (virtual pipeline,
+    // opt-in) its own stream so that a stage waiting on a message or an offload
+    // copy does not hold back the other stages' work; the step stream
+    // rt->stream forks into it at step start and joins it at the end
+    cudaStream_t own = nullptr, cs = nullptr;
+    std::unique_ptr<Pool> pool;   // this stage's HBM pool (reuse stays on one stream)
     ChunkState ch[3];
     int* tokens = nullptr;
     int* targets = nullptr;
@@ -108,7 +115,6 @@ struct tpipe_runtime {
     int timeout_ms = 300000;
     uint32_t debug = 0;
     bool selftest_done = false;
-    Pool pool;
     cudaStream_t stream = nullptr, d2h = nullptr, h2d = nullptr, opt = nullptr;
     cudaEvent_t ev_tmp = nullptr;
     AdamHyper hp{};
@@ -289,7 +295,8 @@ int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags
     const auto& bufs = P.bufs[s];
     const auto& ev = P.events[s];
     const Dims& D = rt->D;
-    cudaStream_t cs = rt->stream;
+    cudaStream_t cs = S.cs;
+    Pool& pool = *S.pool;
     const int p = P.p, v = P.v;
     const bool trecomp = P.strategy == TPIPE_S_TPIPE_TRECOMP || P.strategy == TPIPE_S_INTERLEAVE_TRECOMP;
     const bool no_opt = flags & TPIPE_STEP_NO_OPT;
@@ -297,17 +304,17 @@ int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags
     // allocations at instruction start
     for (int e = 0; e < op.n_alloc; ++e) {
         const int id = ev[op.alloc_first + e];
-        void* ptr = rt->pool.alloc(s, bufs[id].bytes);
-        if (!ptr && rt->pool.last_fail_physical())
+        void* ptr = pool.alloc(s, bufs[id].bytes);
+        if (!ptr && pool.last_fail_physical())
             return set_error(TPIPE_E_OOM, "stage %d: pool fragmentation would place %llu bytes beyond the "
                              "HBM budget (arena %zu + overflow %zu)", s, (unsigned long long)bufs[id].bytes,
-                             rt->pool.arena_bytes(), rt->pool.overflow_bytes());
+                             pool.arena_bytes(), pool.overflow_bytes());
         if (!ptr) return set_error(TPIPE_E_CUDA, "pool allocation of %llu bytes failed",
                                    (unsigned long long)bufs[id].bytes);
         S.bufptr[id] = ptr;
         S.live[key_of(bufs[id])] = ptr;
     }
-    if (rt->pool.over_cap())
+    if (pool.over_cap())
         return set_error(TPIPE_E_OOM, "stage %d ledger exceeds the plan peak (ledger bug)", s);
     if ((rt->debug & TPIPE_DEBUG_POOL_CANARY_SELFTEST) && !rt->selftest_done && op.n_alloc > 0) {
         const int id = ev[op.alloc_first];
@@ -509,7 +516,7 @@ int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags
     // debug: a kernel of this instruction wrote past a buffer's planned bytes
     if (rt->debug & TPIPE_DEBUG_POOL_CANARY) {
         uint64_t rb = 0;
-        if (void* bad = rt->pool.check_canaries(cs, &rb)) {
+        if (void* bad = pool.check_canaries(cs, &rb)) {
             int role = -1, chunk = -1, mb = -1;
             for (int s2 : rt->owned)
                 for (size_t id = 0; id < rt->st[s2]->bufptr.size(); ++id)
@@ -526,7 +533,7 @@ int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags
     // releases at instruction end
     for (int e = 0; e < op.n_free; ++e) {
         const int id = ev[op.free_first + e];
-        rt->pool.free(s, S.bufptr[id]);
+        pool.free(s, S.bufptr[id]);
         S.live.erase(key_of(bufs[id]));
         S.bufptr[id] = nullptr;
     }
@@ -563,6 +570,10 @@ int run_step_impl(tpipe_runtime* rt, const int32_t* tok_dev, const int32_t* tgt_
     rt->d2h_bytes = rt->h2d_bytes = 0;
     const long l0 = launch_count();
     profiler().begin_step((flags & TPIPE_STEP_PROFILE) != 0);
+    const bool op_times = (flags & TPIPE_STEP_OP_TIMES) != 0;
+    // stage streams: separate per stage in the virtual pipeline, except while
+    // timing ops or kernel classes (OP_TIMES / PROFILE: serial, each op's or
+    // kernel's own GPU time)
     for (int s : rt->owned) {
         StageState& S = *rt->st[s];
         S.pc = 0;
@@ -572,10 +583,18 @@ int run_step_impl(tpipe_runtime* rt, const int32_t* tok_dev, const int32_t* tgt_
             CU(cudaMemsetAsync(S.loss_slots, 0, (size_t)P.m * 4, cs));
         }
     }
+    // (after the token / target copies above, so every stage sees them)
+    cudaEvent_t fork = next_event(rt);
+    CU(cudaEventRecord(fork, cs));
+    for (int s : rt->owned) {
+        StageState& S = *rt->st[s];
+        S.cs = (S.own && !op_times && !(flags & TPIPE_STEP_PROFILE)) ? S.own : cs;
+        if (S.cs != cs) CU(cudaStreamWaitEvent(S.cs, fork, 0));
+        S.pool->set_canary((rt->debug & TPIPE_DEBUG_POOL_CANARY) != 0, S.cs);
+    }
     rt->tr->begin_step();
     size_t remaining = 0;
     for (int s : rt->owned) remaining += P.ops[s].size();
-    const bool op_times = (flags & TPIPE_STEP_OP_TIMES) != 0;
     rt->op_ev.assign(P.p, {});
     rt->op_ms.assign(P.p, {});
     while (remaining) {
@@ -590,11 +609,11 @@ int run_step_impl(tpipe_runtime* rt, const int32_t* tok_dev, const int32_t* tgt_
                 if (timed) {
                     ea = next_timed_event(rt);
                     eb = next_timed_event(rt);
-                    CU(cudaEventRecord(ea, cs));
+                    CU(cudaEventRecord(ea, S.cs));
                 }
                 TRY(exec_op(rt, S, ops[S.pc], flags));
                 if (timed) {
-                    CU(cudaEventRecord(eb, cs));   // the layer side stream joins cs inside the op
+                    CU(cudaEventRecord(eb, S.cs));   // the layer side stream joins cs inside the op
                     rt->op_ev[s].push_back({ea, eb});
                 }
                 S.pc++;
@@ -603,6 +622,13 @@ int run_step_impl(tpipe_runtime* rt, const int32_t* tok_dev, const int32_t* tgt_
             }
         }
         if (!prog) return set_error(TPIPE_E_DEADLOCK, "virtual transport made no progress");
+    }
+    for (int s : rt->owned) {   // join: the step stream waits for every stage
+        StageState& S = *rt->st[s];
+        if (S.cs == cs) continue;
+        cudaEvent_t j = next_event(rt);
+        CU(cudaEventRecord(j, S.cs));
+        CU(cudaStreamWaitEvent(cs, j, 0));
     }
     float loss = 0.f;
     if (std::find(rt->owned.begin(), rt->owned.end(), P.p - 1) != rt->owned.end()) {
@@ -714,14 +740,8 @@ TP_API int tpipe_runtime_create(const tpipe_plan* plan, const tpipe_runtime_opts
     } else {
         rt->owned.push_back(o.stage);
     }
-    uint64_t need = 0;
-    for (int s : rt->owned) need += P.peak[s].total_peak;
-    if (rt->pool.init((size_t)(need * 1.08) + (256ull << 20), P.p))
-        return set_error(TPIPE_E_CUDA, "pool: cudaMalloc of %llu bytes failed", (unsigned long long)need);
-    if (P.hbm_budget) rt->pool.set_phys_limit((size_t)P.hbm_budget * rt->owned.size());
     rt->debug = o.debug_flags;
     rt->timeout_ms = o.timeout_ms > 0 ? o.timeout_ms : 300000;
-    rt->pool.set_canary((o.debug_flags & TPIPE_DEBUG_POOL_CANARY) != 0, rt->stream);
     // the kernels' buffer carve-ups must equal the plan's byte model (a drift
     // would overrun a neighbouring pool block): checked once per stage / chunk
     TRY(check_layouts(P, rt->owned));
@@ -729,14 +749,28 @@ TP_API int tpipe_runtime_create(const tpipe_plan* plan, const tpipe_runtime_opts
     const bool off = (P.offload & TPIPE_OFFLOAD_MODEL_STATE) != 0;
     const bool sopt = off && (P.offload & TPIPE_OFFLOAD_DEVICE_OPT) != 0;
     for (int s : rt->owned) {
-        rt->pool.set_cap(s, o.pool_cap ? o.pool_cap : P.peak[s].total_peak);
         auto S = std::make_unique<StageState>();
         S->s = s;
+        // one pool (arena) per stage: a block freed by one stage is never handed
+        // to another stage's stream
+        const uint64_t need = P.peak[s].total_peak;
+        S->pool.reset(new Pool);
+        if (S->pool->init((size_t)(need * 1.08) + (256ull << 20), P.p))
+            return set_error(TPIPE_E_CUDA, "pool: cudaMalloc of %llu bytes failed", (unsigned long long)need);
+        if (P.hbm_budget) S->pool->set_phys_limit((size_t)P.hbm_budget);
+        S->pool->set_cap(s, o.pool_cap ? o.pool_cap : P.peak[s].total_peak);
+        S->pool->set_canary((o.debug_flags & TPIPE_DEBUG_POOL_CANARY) != 0, rt->stream);
+        S->cs = rt->stream;
+        // (opt-in, env TPIPE_VIRTUAL_STAGE_STREAMS=1: measured slower on one GPU —
+        // the stages' persistent GEMM grids contend — profiles/r2_capacity_v2.json)
+        if (o.stage < 0 && P.p > 1 && getenv("TPIPE_VIRTUAL_STAGE_STREAMS") &&
+            getenv("TPIPE_VIRTUAL_STAGE_STREAMS")[0] == '1')
+            CU(cudaStreamCreateWithFlags(&S->own, cudaStreamNonBlocking));
         S->bufptr.assign(P.bufs[s].size(), nullptr);
         for (size_t id = 0; id < P.bufs[s].size(); ++id) {
             const tpipe_buf& b = P.bufs[s][id];
             if (b.role != TPIPE_BUF_STATIC) continue;
-            void* ptr = rt->pool.alloc(s, b.bytes);
+            void* ptr = S->pool->alloc(s, b.bytes);
             if (!ptr) return set_error(TPIPE_E_CUDA, "pool: static allocation failed");
             S->bufptr[id] = ptr;
             CU(cudaMemset(ptr, 0, b.bytes));
@@ -802,8 +836,9 @@ TP_API int tpipe_runtime_create(const tpipe_plan* plan, const tpipe_runtime_opts
         rt->tr = make_virtual_transport(P.channels);
         rt->transport_kind = -1;
     } else if (o.transport == TPIPE_TRANSPORT_IPC) {
-        TRY(make_ipc_transport(P.channels, P.p, o.stage, o.device, o.ipc_name, rt->pool.arena(),
-                               rt->pool.arena_bytes(), P.W, rt->timeout_ms, &rt->tr));
+        Pool& pl = *rt->st[o.stage]->pool;
+        TRY(make_ipc_transport(P.channels, P.p, o.stage, o.device, o.ipc_name, pl.arena(),
+                               pl.arena_bytes(), P.W, rt->timeout_ms, &rt->tr));
         rt->transport_kind = TPIPE_TRANSPORT_IPC;
     } else if (o.transport == TPIPE_TRANSPORT_NCCL) {
         TRY(make_nccl_transport(P.channels, o.stage, o.nccl_ids, rt->timeout_ms, &rt->tr));
@@ -840,7 +875,10 @@ TP_API void tpipe_runtime_destroy(tpipe_runtime* rt) {
     for (auto e : rt->evpool) cudaEventDestroy(e);
     for (auto e : rt->tevpool) cudaEventDestroy(e);
     if (rt->h_tok_stage) cudaFreeHost(rt->h_tok_stage);
-    rt->pool.release();
+    for (int s : rt->owned) {
+        rt->st[s]->pool.reset();
+        if (rt->st[s]->own) cudaStreamDestroy(rt->st[s]->own);
+    }
     cudaStreamDestroy(rt->stream);
     cudaStreamDestroy(rt->d2h);
     cudaStreamDestroy(rt->h2d);
@@ -947,9 +985,11 @@ TP_API int tpipe_step(tpipe_runtime* rt, const int32_t* tokens, const int32_t* t
 TP_API int tpipe_runtime_get_stats(const tpipe_runtime* rt, tpipe_runtime_stats* out) {
     if (!rt || !out) return set_error(TPIPE_E_INVALID, "NULL argument");
     std::memset(out, 0, sizeof(*out));
-    for (int s : rt->owned)
-        if (s < 64) out->pool_high_water[s] = rt->pool.high_water(s);
-    out->pool_reserved = rt->pool.reserved();
+    for (int s : rt->owned) {
+        if (s < 64) out->pool_high_water[s] = rt->st[s]->pool->high_water(s);
+        out->pool_reserved += rt->st[s]->pool->reserved();
+        out->pool_overflow_bytes += rt->st[s]->pool->overflow_bytes();
+    }
     out->kernel_launches = rt->launches_last;
     out->step = rt->t;
     out->offload_d2h_bytes = rt->d2h_bytes;
@@ -967,7 +1007,6 @@ TP_API int tpipe_runtime_get_stats(const tpipe_runtime* rt, tpipe_runtime_stats*
     };
     out->offload_d2h_ms = span_ms(rt->d2h_ev);
     out->offload_h2d_ms = span_ms(rt->h2d_ev);
-    out->pool_overflow_bytes = rt->pool.overflow_bytes();
     out->transport = rt->transport_kind;
     for (int c = 0; c < 4; ++c) {
         out->kernel_ms[c] = rt->kms[c];

@@ -294,8 +294,9 @@ struct BwdWs {
     float* part;
     uint8_t* rbuf;  // one-layer recompute buffer (full-recompute strategy)
     void *lnf, *dlnf;
-    float* logits;
+    float* logits;     // fp32 mode only
     void* dlogits;
+    float *ce_part, *ce_zt, *ce_lrow;   // bf16 fused head (K8)
     int* emb_ws;
     long total;     // bytes carved (== the plan's ws_b; checked at runtime creation)
 };
@@ -323,11 +324,19 @@ static BwdWs carve_bwd(const Dims& D, uint8_t* ws, bool head, bool emb, long par
     w.rbuf = rbuf_bytes ? take(rbuf_bytes) : nullptr;
     w.lnf = w.dlnf = w.dlogits = nullptr;
     w.logits = nullptr;
+    w.ce_part = w.ce_zt = w.ce_lrow = nullptr;
     if (head) {
         w.lnf = take(M * h * es);
         w.dlnf = take(M * h * es);
-        w.logits = reinterpret_cast<float*>(take(4 * M * D.V));
-        w.dlogits = take(M * D.V * es);
+        if (D.dtype == DT_BF16) {   // fused LM head + CE (K8, DESIGN R30): no [M, V] logits
+            w.dlogits = take(M * D.V * es);
+            w.ce_part = reinterpret_cast<float*>(take(8 * M * (long)ce_groups(D.V)));
+            w.ce_zt = reinterpret_cast<float*>(take(4 * M));
+            w.ce_lrow = reinterpret_cast<float*>(take(4 * M));
+        } else {
+            w.logits = reinterpret_cast<float*>(take(4 * M * D.V));
+            w.dlogits = take(M * D.V * es);
+        }
     }
     w.emb_ws = emb ? reinterpret_cast<int*>(take(8 * M)) : nullptr;
     w.total = off;
@@ -563,15 +572,46 @@ int chunk_backward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P
                      st));
         }
         const void* wh = wb + lay.w_head * D.es;
-        TRY(mm(D, M, D.V, h, w.lnf, h, 1, wh, h, 1, EPI_STORE_F32, w.logits, D.V, nullptr, nullptr,
-               0, nullptr, 0, nullptr, 0, st));
-        {
+        float* lse = at<float>(a.stash, SL.ce_lse);
+        if (D.dtype == DT_BF16) {
+            // fused LM head + softmax CE (K8, DESIGN R30): the head GEMM runs twice
+            // and the logits live only in TMEM / registers. Pass 1: per-row
+            // (max, sum exp) over 128-column groups + the target logit; a small
+            // combine gives LSE and the loss; pass 2 recomputes the logits and
+            // writes dlogits = (softmax - onehot) * scale in bf16.
+            GemmDesc g;
+            g.M = M; g.N = D.V; g.K = h;
+            g.A = w.lnf; g.lda = h; g.a_kmajor = 1;
+            g.B = wh; g.ldb = h; g.b_kmajor = 1;
+            g.epi = EPI_LSE_PART;
+            g.targets = a.targets;
+            g.part = w.ce_part;
+            g.zt = w.ce_zt;
+            {
+                ProfScope ps(0, 2.0 * M * D.V * h, st);
+                if (gemm(D.dtype, g, st)) return -7;
+            }
+            {
+                ProfScope _ps(3, 0.0, st);
+                TRY(ce_combine(w.ce_part, ce_groups(D.V), w.ce_zt, lse, w.ce_lrow, a.loss_slot, a.loss_scale,
+                               M, st));
+            }
+            g.epi = EPI_CE_GRAD;
+            g.lse = lse;
+            g.C = w.dlogits;
+            g.ldc = D.V;
+            g.scale = a.loss_scale;
+            {
+                ProfScope ps(0, 2.0 * M * D.V * h, st);
+                if (gemm(D.dtype, g, st)) return -7;
+            }
+        } else {
+            TRY(mm(D, M, D.V, h, w.lnf, h, 1, wh, h, 1, EPI_STORE_F32, w.logits, D.V, nullptr, nullptr,
+                   0, nullptr, 0, nullptr, 0, st));
             ProfScope _ps(3, 0.0, st);
             // LSE and loss (the forward deferred them: see chunk_forward), then dlogits
-            TRY(ce_fwd(w.logits, a.targets, at<float>(a.stash, SL.ce_lse), a.loss_slot, a.loss_scale, M,
-                       D.V, st));
-            TRY(ce_bwd(D.dtype, w.logits, a.targets, at<float>(a.stash, SL.ce_lse), w.dlogits,
-                   a.loss_scale, M, D.V, st));
+            TRY(ce_fwd(w.logits, a.targets, lse, a.loss_slot, a.loss_scale, M, D.V, st));
+            TRY(ce_bwd(D.dtype, w.logits, a.targets, lse, w.dlogits, a.loss_scale, M, D.V, st));
         }
         TRY(mm(D, D.V, h, M, w.dlogits, D.V, 0, w.lnf, h, 0, EPI_ACC_F32, P.grad + lay.w_head, h,
                nullptr, nullptr, 0, nullptr, 0, nullptr, 0, st));

@@ -59,32 +59,64 @@ namespace {
 
 class VirtualTransport final : public Transport {
 public:
-    explicit VirtualTransport(size_t n) : q_(n), popped_(n, 0) {}
+    // each stage may run on its own stream: a message carries the sender's
+    // "ready" event, the receiver copies after it and records "done", which
+    // the sender's SEND_WAIT waits for before the buffer is reused
+    struct Msg {
+        const void* src;
+        cudaEvent_t ready;
+    };
+    explicit VirtualTransport(size_t n) : q_(n), popped_(n, 0), done_(n) {}
+    ~VirtualTransport() override {
+        for (auto e : ev_) cudaEventDestroy(e);
+    }
     const char* name() const override { return "virtual"; }
     void begin_step() override {
         for (auto& q : q_) q.clear();
         for (auto& n : popped_) n = 0;
+        for (auto& d : done_) d.clear();
+        evnext_ = 0;
     }
-    int send(int ch, int, const void* src, size_t, cudaStream_t) override {
-        q_[ch].push_back(src);
+    cudaEvent_t ev() {
+        if (evnext_ == ev_.size()) {
+            cudaEvent_t e;
+            cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+            ev_.push_back(e);
+        }
+        return ev_[evnext_++];
+    }
+    int send(int ch, int, const void* src, size_t, cudaStream_t cs) override {
+        cudaEvent_t e = ev();
+        if (cudaEventRecord(e, cs)) return set_error(TPIPE_E_CUDA, "virtual send: event");
+        q_[ch].push_back({src, e});
         return 0;
     }
     int recv(int ch, void* dst, size_t bytes, cudaStream_t cs) override {
         if (q_[ch].empty()) return set_error(TPIPE_E_STATE, "virtual recv on an empty channel %d", ch);
-        const void* src = q_[ch].front();
+        const Msg mg = q_[ch].front();
         q_[ch].pop_front();
+        cudaEvent_t d = ev();
+        cudaError_t e = cudaStreamWaitEvent(cs, mg.ready, 0);
+        if (!e) e = cudaMemcpyAsync(dst, mg.src, bytes, cudaMemcpyDeviceToDevice, cs);
+        if (!e) e = cudaEventRecord(d, cs);
+        if (e) return set_error(TPIPE_E_CUDA, "virtual recv copy: %s", cudaGetErrorString(e));
+        done_[ch].push_back(d);
         popped_[ch]++;
-        cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, cs);
-        return e == cudaSuccess ? 0 : set_error(TPIPE_E_CUDA, "virtual recv copy: %s", cudaGetErrorString(e));
+        return 0;
     }
-    // single stream: the copy above is ordered before any later reuse of src
-    int send_wait(int, int, cudaStream_t) override { return 0; }
+    int send_wait(int ch, int msg, cudaStream_t cs) override {
+        if (msg >= (int)done_[ch].size()) return set_error(TPIPE_E_STATE, "virtual SEND_WAIT before RECV");
+        return cudaStreamWaitEvent(cs, done_[ch][msg], 0) ? set_error(TPIPE_E_CUDA, "send_wait") : 0;
+    }
     bool recv_ready(int ch) const override { return !q_[ch].empty(); }
     bool send_wait_ready(int ch, int msg) const override { return popped_[ch] > msg; }
 
 private:
-    std::vector<std::deque<const void*>> q_;
+    std::vector<std::deque<Msg>> q_;
     std::vector<int> popped_;
+    std::vector<std::vector<cudaEvent_t>> done_;
+    std::vector<cudaEvent_t> ev_;
+    size_t evnext_ = 0;
 };
 
 // ================================================================ nccl

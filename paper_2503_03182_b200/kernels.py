@@ -79,6 +79,11 @@ def tpipe_k_ce_fwd(logits, tgt, lse, loss, scale, rows, V):
           "ce_fwd")
 
 
+def tpipe_k_head_ce(x, w, tgt, lse, dlogits, loss, scale, rows, V, h, ws):
+    check(lib().tpipe_k_head_ce(_p(x), _p(w), _p(tgt), _p(lse), _p(dlogits), _p(loss), scale, rows, V,
+                                h, _p(ws), _stream()), "tpipe_k_head_ce")
+
+
 def tpipe_k_ce_bwd(dtype, logits, tgt, lse, dlogits, scale, rows, V):
     check(lib().tpipe_k_ce_bwd(dtype, _p(logits), _p(tgt), _p(lse), _p(dlogits), scale, rows, V,
                                _stream()), "ce_bwd")

@@ -49,14 +49,15 @@ class Plan:
                  strategy="tpipe", delay_rounds: int = -1, send_window: int = 0, offload: int = 0,
                  act_distance: int = 0, recomp_layers: int = 0, stage_layers=None,
                  host_link_bps: float = 0.0, host_adam_params_per_s: float = 0.0,
-                 device_flops: float = 0.0, balance: bool = False):
+                 device_flops: float = 0.0, balance: bool = False, stage_chunk1=None):
         L = lib()
         st = -1 if strategy in (None, "auto") else STRATEGY.get(strategy, strategy)
         if st < 0 and offload == 0:
             offload = -1
         sl = (C.c_int32 * 64)(*(list(stage_layers or [])[:64]))
         opts = D.PlanOpts(st, delay_rounds, send_window, offload, act_distance, recomp_layers, sl,
-                          host_link_bps, host_adam_params_per_s, device_flops, 1 if balance else 0)
+                          host_link_bps, host_adam_params_per_s, device_flops, 1 if balance else 0,
+                          (C.c_int32 * 64)(*(list(stage_chunk1 or [])[:64])))
         self._h = C.c_void_p()
         self.model = model
         check(L.tpipe_plan_create(C.byref(model.c()), n_stages, n_microbatches, hbm_budget,

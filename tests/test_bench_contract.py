@@ -38,7 +38,7 @@ def test_capacity_sweep_size_target():
 def test_balanced_partition_and_choice():
     """R27: the balanced split keeps every stage >= v layers, sums to L and
     lowers the largest stage cost (head counted in layer-equivalents); the
-    bench picks it only when the duration-model replay predicts >= 3% gain."""
+    planner picks a partition only when its cost model predicts >= 3% gain."""
     sys.path.insert(0, ROOT)
     import bench
     from paper_2503_03182_b200 import plan as P
@@ -50,10 +50,10 @@ def test_balanced_partition_and_choice():
             assert sum(part) == 24 and min(part) >= v and len(part) == p
             cost = max(max(part[:-1]), part[-1] + hl)
             assert cost <= max(24 // p, 24 // p + hl)
+    # the choice itself now lives in the planner (tpipe_plan_opts.balance, R28/R29)
     md = P.Model(24, 2048, 16, 8192, 50304, 2048, 1, P.BF16)
-    assert bench.choose_partition(md, 8, 32, "tpipe") == [4, 3, 3, 3, 3, 3, 3, 2]
-    assert bench.choose_partition(md, 4, 32, "tpipe") is None
-    assert bench.choose_partition(md, 1, 32, "tpipe") is None
+    assert P.Plan(md, 8, 32, strategy="tpipe", balance=True).balanced
+    assert not P.Plan(md, 1, 32, strategy="tpipe", balance=True).balanced
 
 
 def test_gpus_n_without_ranks_refuses():

@@ -85,13 +85,17 @@ def test_workspace_lower_bounds(h, a, s, b):
     pre-activation gradient and GELU(u) (2·M·f), one recomputed LN output
     and its gradient (2·M·h), the attention-output gradient (M·h) and dqkv
     (3·M·h) plus D = rowsum(dO∘O) (4·a·M); the forward a LN output (M·h) and
-    GELU output (M·f). The head chunk's backward additionally holds the LM
-    head's logits (fp32, 4·M·V) and their gradient (es·M·V) in this build
-    (K8 without fusion)."""
+    GELU output (M·f). The head chunk's backward additionally holds the
+    logits' gradient (es·M·V; the bf16 fused head never stores the logits,
+    DESIGN R30) plus, in fp32 mode, the fp32 logits (4·M·V)."""
     d = desc(h, a, s, b, L=8)
     M, f, V = b * s, 4 * h, d.vocab
     z = T.sizes(d, 4, 2, 1, 1)
     assert z["ws_b"] >= 2 * (2 * M * h + 2 * M * f + 2 * M * h + M * h + 3 * M * h) + 4 * a * M
     assert z["ws_f"] >= 2 * (M * h + M * f)
     zh = T.sizes(d, 4, 2, 3, 2)
-    assert zh["ws_b"] - z["ws_b"] >= 4 * M * V + 2 * M * V
+    assert zh["ws_b"] - z["ws_b"] >= 2 * M * V
+    # no fp32 [M, V] logits in bf16 (R30): below the unfused 4·M·V + 2·M·V
+    assert zh["ws_b"] - z["ws_b"] < 6 * M * V
+    d32 = desc(h, a, s, b, L=8, dtype=T.FP32)
+    assert T.sizes(d32, 4, 2, 3, 2)["ws_b"] - T.sizes(d32, 4, 2, 1, 1)["ws_b"] >= 8 * M * V

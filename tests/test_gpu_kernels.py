@@ -494,3 +494,33 @@ def test_adamw_device_host_bitexact(decay):
     rw, rm, rv = R.adamw(w0, g0.astype(np.float64), m0.astype(np.float64),
                          v0.astype(np.float64), step, hp["lr"], bool(decay))
     assert max_rel(hw, rw) < 1e-6
+
+
+@pytest.mark.parametrize("rows,V,h", [(2048, 50304, 2048), (256, 512, 256), (200, 320, 128)])
+def test_head_ce_fused_vs_fp64(rows, V, h):
+    """Fused LM head + softmax CE (K8, DESIGN R30): the logits never reach HBM.
+    LSE / loss / dlogits against an fp64 reference of the same bf16 operands
+    (ragged rows and a partial 128-column group covered)."""
+    from paper_2503_03182_b200 import kernels as K
+    g = torch.Generator(device="cpu").manual_seed(rows + V)
+    x = torch.randn(rows, h, generator=g).to(torch.bfloat16).cuda()
+    w = (torch.randn(V, h, generator=g) * 0.05).to(torch.bfloat16).cuda()
+    tgt = torch.randint(0, V, (rows,), generator=g, dtype=torch.int32).cuda()
+    lse = torch.empty(rows, device="cuda")
+    dl = torch.empty(rows, V, device="cuda", dtype=torch.bfloat16)
+    loss = torch.zeros(1, device="cuda")
+    ng = (V + 63) // 64
+    ws = torch.empty(2 * rows * ng + 2 * rows, device="cuda")
+    scale = 1.0 / rows
+    K.tpipe_k_head_ce(x, w, tgt, lse, dl, loss, scale, rows, V, h, ws)
+    torch.cuda.synchronize()
+    z = x.double() @ w.double().T
+    lref = torch.logsumexp(z, dim=1)
+    loss_ref = float((lref - z.gather(1, tgt.long()[:, None])[:, 0]).sum() * scale)
+    p = torch.softmax(z, dim=1)
+    p[torch.arange(rows), tgt.long()] -= 1.0
+    dref = p * scale
+    assert float((lse.double() - lref).abs().max()) < 2e-5 * max(1.0, float(lref.abs().max()))
+    assert abs(float(loss) - loss_ref) / abs(loss_ref) < 1e-5
+    err = float(torch.linalg.norm(dl.double() - dref) / torch.linalg.norm(dref))
+    assert err < 1e-2, err

@@ -37,7 +37,11 @@ def build(cfg, p, m, strategy, dtype, offload=0, recomp_layers=0, seed=11, debug
           std=0.05):
     P, RT, PR = mods()
     md = P.Model(cfg["L"], cfg["h"], cfg["a"], cfg["f"], cfg["V"], cfg["s"], cfg["b"], dtype)
-    plan = P.Plan(md, p, m, strategy=strategy, offload=offload, recomp_layers=recomp_layers)
+    # activation offload: distance 1 so that these small shapes really offload
+    # (the bandwidth-derived distance, Q12, would keep every block on the device)
+    ad = 1 if offload & P.OFFLOAD_ACTIVATIONS else 0
+    plan = P.Plan(md, p, m, strategy=strategy, offload=offload, recomp_layers=recomp_layers,
+                  act_distance=ad)
     rt = RT.Runtime(plan, stage=-1, lr=1e-3, debug_flags=debug_flags)
     W = synth.weights(cfg["L"], cfg["h"], cfg["f"], cfg["V"], cfg["s"], seed=seed, std=std,
                       bias_std=0.02, ln_jitter=0.05)
@@ -164,3 +168,43 @@ def test_pool_canary_selftest_fires():
     with pytest.raises(TPipeError, match="pool canary"):
         rt.step(tok, tgt, 0)
     rt.close()
+
+
+@pytest.mark.parametrize("strategy", ["tpipe", "tpipe_trecomp"])
+def test_duration_aware_partition_step(strategy):
+    """R29 (NEXT-5): per-stage layer counts and chunk splits chosen freely —
+    fp32 gradients match the oracle, bf16 gradients are bit-identical to the
+    uniform partition's (the layer math does not depend on where chunk
+    boundaries fall), and the ledger high-water equals the plan peak."""
+    P, RT, PR = mods()
+    cfg, p, m = C1_16, 4, 8
+    part, ch1 = (5, 4, 4, 3), (4, 1, 2, 2)
+    tok, tgt = synth.tokens(cfg["V"], m, cfg["b"], cfg["s"], step=1)
+    W = synth.weights(cfg["L"], cfg["h"], cfg["f"], cfg["V"], cfg["s"], seed=11, std=0.05,
+                      bias_std=0.02, ln_jitter=0.05)
+    lref, G = R.step_grads(R.to64(W), tok, tgt, cfg["a"])
+    grads = []
+    for dtype, sl, c1 in ((0, part, ch1), (1, part, ch1), (1, None, None)):
+        md = P.Model(cfg["L"], cfg["h"], cfg["a"], cfg["f"], cfg["V"], cfg["s"], cfg["b"], dtype)
+        plan = P.Plan(md, p, m, strategy=strategy, stage_layers=sl, stage_chunk1=c1)
+        rt = RT.Runtime(plan, stage=-1)
+        for s in range(p):
+            for c in (1, 2):
+                rt.set_params(s, c, PR.pack(W, p, 2, plan.partition, s, c))
+        rt.step(tok, tgt, RT.STEP_NO_OPT)
+        g = {}
+        for s in range(p):
+            for c in (1, 2):
+                g.update(PR.unpack(rt.get_grads(s, c), W, p, 2, plan.partition, s, c))
+        st = rt.stats()
+        assert all(st["pool_high_water"][s] == plan.peak(s)["total_peak"] for s in range(p))
+        rt.close()
+        if dtype == 0:
+            for (k, l), v in g.items():
+                ref = G["layers"][l][k] if l is not None else G[k]
+                assert max_rel(v, ref) <= 1e-4, (k, l)
+        else:
+            grads.append(g)
+    for k in grads[0]:
+        assert np.array_equal(np.asarray(grads[0][k], np.float32).view(np.uint32),
+                              np.asarray(grads[1][k], np.float32).view(np.uint32)), k

@@ -25,12 +25,17 @@ def mods():
     return plan, runtime, params
 
 
-def build(cfg, p, m, strategy, dtype, offload=0, lr=1e-3, seed=11, recomp_layers=0, stage_layers=None):
+def build(cfg, p, m, strategy, dtype, offload=0, lr=1e-3, seed=11, recomp_layers=0, stage_layers=None,
+          act_distance=None):
     P, RT, PR = mods()
     md = P.Model(cfg["n_layers"], cfg["hidden"], cfg["n_heads"], cfg["ffn_hidden"], cfg["vocab"],
                  cfg["seq_len"], cfg["micro_batch"], dtype)
+    if act_distance is None:
+        # activation offload at these tiny sizes: the bandwidth-derived distance
+        # (Q12) would keep every block on the device; use round 1's fixed 2
+        act_distance = 2 if offload & P.OFFLOAD_ACTIVATIONS else 0
     plan = P.Plan(md, p, m, strategy=strategy, offload=offload, recomp_layers=recomp_layers,
-                  stage_layers=stage_layers)
+                  stage_layers=stage_layers, act_distance=act_distance)
     rt = RT.Runtime(plan, stage=-1, lr=lr)
     W = synth.weights(cfg["n_layers"], cfg["hidden"], cfg["ffn_hidden"], cfg["vocab"],
                       cfg["seq_len"], seed=seed, std=0.05, bias_std=0.02, ln_jitter=0.05)

@@ -383,3 +383,30 @@ def test_partition_partial_trecomp_matches_oracle():
         st, static = T.build_streams(od, 4, 8, "tpipe_trecomp", recomp_layers=r)
         for s in range(4):
             assert plan.peak(s)["total_peak"] == T.replay(st[s], static[s])["total_peak"]
+
+
+@pytest.mark.parametrize("p,part,chunk1", [(4, (5, 4, 4, 3), (4, 1, 2, 2)), (2, (7, 5), (3, 4)),
+                                           (8, (2, 2, 3, 2, 2, 3, 2, 2), (1, 1, 2, 1, 1, 1, 1, 1))])
+@pytest.mark.parametrize("strategy", ["tpipe", "tpipe_trecomp", "interleave_trecomp"])
+def test_partition_chunk_split_streams_match_oracle(p, part, chunk1, strategy):
+    """Duration-aware partition (R29): per-stage chunk-1
+    layer counts; streams, buffer sizes and peaks equal the oracle's."""
+    P = _plan_mod()
+    L = sum(part)
+    m = 2 * p
+    od = T.ModelDesc(L, 64, 4, 256, 128, 32, 2, T.BF16, stage_layers=part, stage_chunk1=chunk1)
+    pd = P.Model(L, 64, 4, 256, 128, 32, 2, P.BF16)
+    plan = P.Plan(pd, p, m, strategy=strategy, stage_layers=part, stage_chunk1=chunk1)
+    assert [x[0] for x in plan.partition] == list(chunk1)
+    st, static = T.build_streams(od, p, m, strategy)
+    for s in range(p):
+        got, bufs = plan.ops(s)
+        strip = [{k: o[k] for k in ("kind", "chunk", "mb", "peer", "channel", "msg")} for o in got]
+        assert strip == oracle_ops(st[s])
+        for g, w in zip(got, st[s]):
+            assert [(bufs[a][1], bufs[a][4]) for a in g["allocs"]] == [(c, b) for _n, c, b in w.allocs]
+        assert plan.peak(s)["total_peak"] == T.replay(st[s], static[s])["total_peak"]
+    from paper_2503_03182_b200._lib import TPipeError
+    with pytest.raises(TPipeError, match="stage_chunk1"):
+        P.Plan(pd, p, m, strategy=strategy, stage_layers=part,
+               stage_chunk1=[part[0]] + list(chunk1[1:]))
