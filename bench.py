@@ -697,9 +697,15 @@ def latest_capacity_claim():
                key=lambda r: r.get("params_vs_1f1b", 0), default=None)
     if not best:
         return None
-    return (f"{os.path.relpath(f, ROOT)}: largest executed model {best['params_B']}B params = "
-            f"{best['params_vs_1f1b']}x 1F1B's at {best['model_tflops_vs_1f1b']}x its model TFLOP/s "
-            f"({best['strategy']}, offload={best.get('offload', 0)})")
+    two = max((r for r in runs.values() if r.get("fits_budget") and r.get("params_vs_1f1b", 0) >= 2),
+              key=lambda r: r.get("model_tflops_vs_1f1b", 0), default=None)
+    s = (f"{os.path.relpath(f, ROOT)}: largest executed model {best['params_B']}B params = "
+         f"{best['params_vs_1f1b']}x 1F1B's at {best['model_tflops_vs_1f1b']}x its model TFLOP/s "
+         f"({best['plan_strategy']}, offload={best.get('offload', 0)})")
+    if two:
+        s += (f"; fastest >= 2x model: {two['params_vs_1f1b']}x params at {two['model_tflops_vs_1f1b']}x "
+              f"({two['plan_strategy']}, offload={two.get('offload', 0)}, r={two.get('recomp_layers', 0)})")
+    return s
 
 
 def launch_ranks(args):
