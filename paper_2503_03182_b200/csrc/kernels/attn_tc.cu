@@ -513,10 +513,9 @@ __global__ void fa_bwd_d_kernel(const bf16* __restrict__ o, const bf16* __restri
 template <int D>
 static int launch_fwd(const void* qkv, void* o, float* lse, int b, int s, int a, cudaStream_t st) {
     constexpr int smem = (128 * D + 4 * 64 * D) * 2;
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce attr;
+    if (attr.first()) {
         cudaFuncSetAttribute(fa::fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
     }
     dim3 grid((s + 127) / 128, a, b);
     fa::fwd_kernel<D><<<grid, 256, smem, st>>>((const bf16*)qkv, (bf16*)o, lse, s, a);
@@ -529,11 +528,10 @@ static int launch_bwd(const void* qkv, const void* o, const void* dout, const fl
                       void* dqkv, float* ws, int b, int s, int a, cudaStream_t st) {
     constexpr int smem_kv = (2 * 64 * D + 4 * 64 * D) * 2 + 4 * 64 * 4;
     constexpr int smem_q = (2 * 64 * D + 4 * 64 * D) * 2;
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce attr;
+    if (attr.first()) {
         cudaFuncSetAttribute(fa::bwd_dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kv);
         cudaFuncSetAttribute(fa::bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_q);
-        attr = true;
     }
     dim3 gd((s + 3) / 4, a, b);
     fa_bwd_d_kernel<<<gd, 128, 0, st>>>((const bf16*)o, (const bf16*)dout, ws, s, a, D);

@@ -1147,10 +1147,9 @@ template <int D>
 static int fwd5(const void* qkv, void* o, float* lse, int b, int s, int a, cudaStream_t st) {
     constexpr int TB = fa5::Tile<D>::BYTES;
     constexpr int smem = 1024 + TB * 6 + 6 * 128 * 4 + 256;
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce attr;
+    if (attr.first()) {
         cudaFuncSetAttribute(fa5::fwd2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
     }
     CUtensorMap m;
     if (map2d(&m, qkv, 3L * a * D, (long)b * s, 3L * a * D)) return -2;
@@ -1170,11 +1169,10 @@ static int bwd5(const void* qkv, const void* o, const void* dout, const float* l
     constexpr int smem_kv = 1024 + 2 * TB + 2 * fa5::BwdCfg<D>::NQ * HB + 4 * 128 * 128 + 4 * 64 * 4 + 256;
     constexpr int smem_q = 1024 + 2 * TB + 2 * fa5::BwdCfg<D>::NK * HB + 2 * 128 * 128 + 256;
     static_assert(smem_kv <= 232448 && smem_q <= 232448, "backward smem over the 227 KB limit");
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce attr;
+    if (attr.first()) {
         cudaFuncSetAttribute(fa5::dkdv2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kv);
         cudaFuncSetAttribute(fa5::dq2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_q);
-        attr = true;
     }
     CUtensorMap mq, mq64, md, md64;
     if (map2d(&mq, qkv, 3L * a * D, (long)b * s, 3L * a * D)) return -2;

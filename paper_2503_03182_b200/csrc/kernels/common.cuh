@@ -8,6 +8,20 @@
 
 namespace tpipe {
 
+// True once per (call site, CUDA device): per-device one-time setup such as
+// cudaFuncSetAttribute (function attributes are per device, so a process-wide
+// flag would leave a second device at the default shared-memory limit).
+struct PerDeviceOnce {
+    unsigned long long mask = 0;
+    bool first() {
+        int d = 0;
+        cudaGetDevice(&d);
+        const unsigned long long bit = 1ull << (d & 63);
+        return !(__atomic_fetch_or(&mask, bit, __ATOMIC_ACQ_REL) & bit);
+    }
+};
+
+
 using bf16 = __nv_bfloat16;
 
 // ---------------------------------------------------------------- conversions

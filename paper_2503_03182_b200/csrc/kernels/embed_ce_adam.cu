@@ -99,11 +99,10 @@ int embed_bwd(int dtype, const int* tok, const void* dx, float* dwte, float* dwp
     int n2 = 1;
     while (n2 < rows) n2 <<= 1;
     const size_t smem = (size_t)n2 * 4;
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce attr;
+    if (attr.first()) {
         cudaFuncSetAttribute(embed_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              32768 * 4);
-        attr = true;
     }
     embed_sort_kernel<<<1, 1024, smem, st>>>(tok, ws, rows, n2);
     const int wpe_blocks = (int)(((long)s * h + 255) / 256);

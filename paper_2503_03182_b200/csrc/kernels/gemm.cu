@@ -908,10 +908,9 @@ static int launch_tc(const GemmDesc& g, cudaStream_t st) {
         epoch = next_epoch();
     }
     auto kern = gemm_tc_kernel<BN, A_MN, B_MN, CG, EPI_WARPS>;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static PerDeviceOnce attr_set;
+    if (attr_set.first()) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
-        attr_set = true;
     }
     if (launch_k(kern, dim3(grid), dim3(TC_THREADS), Cfg::SMEM, st, CG, ta, tb, tc, tc2, g, num_m, num_n,
                  num_kb, sk, w.ws, w.flags, epoch) != cudaSuccess)

@@ -687,11 +687,10 @@ int ln_bwd(int dtype, const void* dy, const void* x, const void* gamma, const fl
         int RC = LNB_SMEM_ROWS_BYTES / (3 * h * 2);
         if (RC > RB) RC = RB;
         const size_t smem = (size_t)RC * 3 * h * 2;
-        static bool attr = false;
-        if (!attr) {
+        static PerDeviceOnce attr;
+        if (attr.first()) {
             cudaFuncSetAttribute(ln_bwd_stage_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  LNB_SMEM_ROWS_BYTES);
-            attr = true;
         }
         launch_k(ln_bwd_stage_kernel, dim3(nb), dim3(G * (h / 8)), smem, st, 1, (const bf16*)dy,
                  (const bf16*)x, (const bf16*)gamma, (const float*)mean, (const float*)rstd, (const bf16*)resid,
@@ -784,10 +783,9 @@ int ln_bwd_partials(int dtype, const void* dy, const void* x, const void* gamma,
     int RC = LNB_SMEM_ROWS_BYTES / (3 * h * 2);
     if (RC > RB) RC = RB;
     const size_t smem = (size_t)RC * 3 * h * 2;
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce attr;
+    if (attr.first()) {
         cudaFuncSetAttribute(ln_bwd_stage_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, LNB_SMEM_ROWS_BYTES);
-        attr = true;
     }
     launch_k(ln_bwd_stage_kernel, dim3(nb), dim3(G * (h / 8)), smem, st, 1, (const bf16*)dy, (const bf16*)x,
              (const bf16*)gamma, (const float*)mean, (const float*)rstd, (const bf16*)resid, (bf16*)dx, ws, rows,

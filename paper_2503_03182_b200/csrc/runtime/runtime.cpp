@@ -877,8 +877,12 @@ TP_API void tpipe_runtime_destroy(tpipe_runtime* rt) {
     if (rt->h_tok_stage) cudaFreeHost(rt->h_tok_stage);
     for (int s : rt->owned) {
         rt->st[s]->pool.reset();
-        if (rt->st[s]->own) cudaStreamDestroy(rt->st[s]->own);
+        if (rt->st[s]->own) {
+            stage_release_side_streams(rt->st[s]->own);
+            cudaStreamDestroy(rt->st[s]->own);
+        }
     }
+    stage_release_side_streams(rt->stream);
     cudaStreamDestroy(rt->stream);
     cudaStreamDestroy(rt->d2h);
     cudaStreamDestroy(rt->h2d);

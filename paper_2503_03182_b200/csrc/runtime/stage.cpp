@@ -367,25 +367,49 @@ uint64_t fwd_ws_bytes(const Dims& D, const StashLayout& SL, bool head) {
 // of <= #SMs CTAs; a 2048-multiple shape occupies ~86% of the SM-waves).
 // One side stream + events per compute stream, created on first use.
 struct SideStream {
+    int dev = 0;
     cudaStream_t main = nullptr, aux = nullptr;
     cudaEvent_t ev[5] = {};
 };
+static std::mutex g_side_mu;
+static std::vector<SideStream*> g_side;
 static SideStream* side_stream(cudaStream_t main) {
-    static std::mutex mu;
-    static std::vector<SideStream*> all;
     int dev = 0;
     cudaGetDevice(&dev);
-    std::lock_guard<std::mutex> lk(mu);
-    for (auto* s : all)
-        if (s->main == main) return s;
+    std::lock_guard<std::mutex> lk(g_side_mu);
+    for (auto* s : g_side)
+        if (s->main == main && s->dev == dev) return s;
     auto* s = new SideStream;
+    s->dev = dev;
     s->main = main;
-    if (cudaStreamCreateWithFlags(&s->aux, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    if (cudaStreamCreateWithFlags(&s->aux, cudaStreamNonBlocking) != cudaSuccess) {
+        delete s;
+        return nullptr;
+    }
     for (auto& e : s->ev)
-        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
-    all.push_back(s);
-    (void)dev;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+            delete s;
+            return nullptr;
+        }
+    g_side.push_back(s);
     return s;
+}
+void stage_release_side_streams(cudaStream_t main) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_side_mu);
+    for (size_t i = 0; i < g_side.size();) {
+        SideStream* s = g_side[i];
+        if (s->main == main && s->dev == dev) {
+            cudaStreamSynchronize(s->aux);
+            cudaStreamDestroy(s->aux);
+            for (auto e : s->ev) cudaEventDestroy(e);
+            delete s;
+            g_side.erase(g_side.begin() + i);
+        } else {
+            ++i;
+        }
+    }
 }
 static bool g_side_stream_enabled = true;
 void stage_set_side_stream(int on) { g_side_stream_enabled = on != 0; }

@@ -117,6 +117,8 @@ int chunk_forward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P,
 // layer backward: run weight-gradient GEMMs on a side stream (default on;
 // always off while TPIPE_STEP_PROFILE is timing kernel classes)
 void stage_set_side_stream(int on);
+// release the side stream + events cached for `main` on the current device
+void stage_release_side_streams(cudaStream_t main);
 int chunk_backward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P, const BwdArgs& a,
                    cudaStream_t st);
 
