@@ -741,8 +741,15 @@ def run_tpipe(args):
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1 and args.virtual_stages:
         raise SystemExit("bench.py: --virtual-stages is a one-process option")
-    # p pipeline stages: one per rank (N > 1), or a one-GPU virtual pipeline
-    N = world if world > 1 else (args.virtual_stages or 1)
+    # p pipeline stages: one per rank (N > 1; with --pp P < N the other ranks are
+    # dp = N / P data-parallel replicas, ZeRO-1, R31), or a one-GPU virtual pipeline
+    pp = args.pp or world
+    if world > 1 and (world % pp or (world // pp > 1 and args.transport != "ipc")):
+        raise SystemExit(f"bench.py: --pp {pp} must divide {world} ranks; dp > 1 needs --transport ipc")
+    dp = world // pp if world > 1 else 1
+    N = pp if world > 1 else (args.virtual_stages or 1)
+    stage = rank % N if world > 1 else -1
+    dp_rank = rank // N if world > 1 else 0
     n_gpus = world
     dist = None
     if world > 1:
@@ -760,7 +767,7 @@ def run_tpipe(args):
     m = c["m"]
     # p > 1: the planner picks the cost-balanced stage partition when its cost
     # model says it pays (R27/R28)
-    plan = P.Plan(md, N, m, strategy=args.strategy, balance=N > 1)
+    plan = P.Plan(md, N, m, strategy=args.strategy, balance=N > 1, dp=dp)
     ids, ipc_name = None, None
     transport = RT.TRANSPORT_IPC if args.transport == "ipc" else RT.TRANSPORT_NCCL
     if world > 1:
@@ -771,16 +778,16 @@ def run_tpipe(args):
                 if rank == 0 else [None]
         dist.broadcast_object_list(ids, src=0)
         ids, ipc_name = (ids[0], None) if transport == RT.TRANSPORT_NCCL else (None, ids[0])
-    rt = RT.Runtime(plan, stage=rank if world > 1 else -1, device=local, nccl_ids=ids, lr=1e-4,
-                    transport=transport, ipc_name=ipc_name)
-    rng = np.random.default_rng(1234 + rank)
-    stages = [rank] if world > 1 else list(range(N))
+    rt = RT.Runtime(plan, stage=stage, device=local, nccl_ids=ids, lr=1e-4,
+                    transport=transport, ipc_name=ipc_name, dp_rank=dp_rank)
+    rng = np.random.default_rng(1234 + max(stage, 0))   # replicas of a stage start equal
+    stages = [stage] if world > 1 else list(range(N))
     for s in stages:
         for ch in range(1, plan.v + 1):
             rt.set_params(s, ch, init_chunk(plan, s, ch, rng))
     import synth
-    tok, tgt = synth.tokens(c["vocab"], m, c["micro_batch"], c["seq_len"], step=0,
-                            vocab_eff=c["vocab_eff"])
+    tok, tgt = synth.tokens(c["vocab"], m, c["micro_batch"], c["seq_len"], step=dp_rank,
+                            vocab_eff=c["vocab_eff"])   # each replica its own micro-batches
     dtok = torch.tensor(tok, dtype=torch.int32, device="cuda")
     dtgt = torch.tensor(tgt, dtype=torch.int32, device="cuda")
     ext = torch.cuda.ExternalStream(rt.stream())
@@ -825,7 +832,7 @@ def run_tpipe(args):
         kfl += st["kernel_flops"]
         kcnt += st["kernel_count"]
     hw = rt.stats()["pool_high_water"]
-    tokens = m * c["micro_batch"] * c["seq_len"]
+    tokens = dp * m * c["micro_batch"] * c["seq_len"]   # all replicas
     value = tokens * args.steps / (ms / 1e3)
     e2e = tokens * args.steps / (ms_e2e / 1e3)
     hbm, pk_burst, pk_sust, src = peaks()
@@ -845,13 +852,14 @@ def run_tpipe(args):
         out = {
             "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": n_gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 3),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if dp == 1 else "weak", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (seeded uniform tokens < 50257; random-init weights)",
             "config": {"workload": "configs[1]: GPT-3 1.3B, seq 2048, T-Pipe, m=32 micro-batches",
                        "model": "gpt3-1.3b", "n_layers": 24, "hidden": 2048, "seq_len": 2048,
                        "micro_batch": 1, "n_microbatches": m, "global_batch_tokens": tokens,
+                       "pp": N, "dp": dp,
                        "strategy": args.strategy,
-                       "parallelism": f"pp{N}" if world > 1 else
+                       "parallelism": (f"pp{N}" if dp == 1 else f"dp{dp}xpp{N} (ZeRO-1)") if world > 1 else
                        (f"virtual pp{N} on 1 GPU" if N > 1 else "pp1"),
                        "transport": (args.transport if world > 1 else "in-process"),
                        **({"same_gpu_test": "all ranks on GPU 0 (TPIPE_BENCH_SAME_GPU): "
@@ -1004,6 +1012,9 @@ def main():
                     help="executed capacity at a fixed per-stage HBM budget (p=8 virtual pipeline, one GPU)")
     ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
                     help="stage transport for N > 1 ranks (CUDA-IPC copy-engine pull, or NCCL send/recv)")
+    ap.add_argument("--pp", type=int, default=0,
+                    help="pipeline stages when N > 1 (default N); the N / pp replicas are ZeRO-1 data "
+                         "parallel (SURVEY NEXT-3)")
     ap.add_argument("--virtual-stages", type=int, default=0,
                     help="run a p-stage virtual pipeline on this one GPU (reported as n_gpus = 1)")
     args = ap.parse_args()

@@ -143,6 +143,12 @@ typedef struct {
                               DESIGN R29), started from the uniform split and the R27 closed form */
     int32_t stage_chunk1[64]; /* with stage_layers at v = 2: chunk-1 layers of stage s
                               (1 .. n(s)-1); 0 = ceil(n(s)/2) */
+    int32_t dp;            /* data-parallel replicas of the pipeline (SURVEY NEXT-3, P:484;
+                              DESIGN R31); 0 = 1. Each replica runs n_microbatches per step,
+                              the loss is the mean over all dp * n_microbatches micro-batches,
+                              optimizer states are sharded ZeRO-1 (master / m / v of
+                              ceil64(P / dp) parameters per replica) and updated by
+                              TPIPE_OP_DP_OPT. Incompatible with model-state offload */
 } tpipe_plan_opts;
 
 enum {
@@ -155,8 +161,16 @@ enum {
     TPIPE_OP_ACT_D2H_WAIT = 14,  /* copy done -> release STASH(1,i) on the device */
     TPIPE_OP_ACT_H2D = 15,       /* re-allocate STASH(1,i), start the prefetch */
     TPIPE_OP_ACT_H2D_WAIT = 16,  /* prefetch landed (before B(1,i)) */
-    TPIPE_OP_STREAM_OPT = 17     /* TPIPE_OFFLOAD_DEVICE_OPT: streamed device AdamW of the
+    TPIPE_OP_STREAM_OPT = 17,    /* TPIPE_OFFLOAD_DEVICE_OPT: streamed device AdamW of the
                                     offloaded chunk (replaces GRAD_D2H, HOST_OPT, W_H2D) */
+    TPIPE_OP_DP_OPT = 18,        /* dp > 1 (ZeRO-1, DESIGN R31): replaces OPT. One kernel per
+                                    replica reads its parameter shard's gradients from every
+                                    replica of the stage over peer memory (NVLink), sums them
+                                    in replica order, zeroes them, runs AdamW on its shard of
+                                    master / m / v and writes the bf16 weights into every
+                                    replica (reduce-scatter + optimizer + all-gather fused) */
+    TPIPE_OP_DP_WAIT = 19        /* dp > 1: before a chunk's first forward, wait until every
+                                    replica's previous-step DP_OPT of that chunk finished */
 };
 
 /* One instruction of a stage's stream. Buffers listed in
@@ -205,6 +219,7 @@ typedef struct {
     double est_step_s;       /* cost-model step time (seconds, see tpipe_plan_opts) */
     double est_exposed_offload_s;   /* of which: offload transfer time left exposed */
     int32_t balanced;        /* 1 if the planner chose a cost-balanced partition */
+    int32_t dp;              /* data-parallel replicas */
 } tpipe_plan_info;
 
 typedef struct {
@@ -275,6 +290,10 @@ typedef struct {
                                n_stages ranks of one job and unique per job; unlinked once
                                every rank has attached */
     uint32_t debug_flags;   /* TPIPE_DEBUG_* */
+    int32_t dp_rank;        /* plan dp > 1: this process's replica (0 .. dp-1); requires
+                               stage >= 0 and ipc_name (the replicas of a stage map each
+                               other's gradients and weights through CUDA IPC; the pipeline
+                               transport of replica k uses ipc_name + "_r<k>") */
 } tpipe_runtime_opts;
 
 typedef struct {

@@ -96,14 +96,25 @@ def chunk_params(d: ModelDesc, p: int, v: int, s: int, c: int) -> int:
     return P
 
 
-def model_state_bytes(d: ModelDesc, P: int, offloaded: bool) -> int:
+def zero1_shard(P: int, dp: int) -> int:
+    """ZeRO-1 optimizer shard of a chunk with P params over dp replicas
+    (NEXT-3, DESIGN R31): ceil(P/dp) rounded up to 64 elements; replica r owns
+    [r*S, min(P, (r+1)*S))."""
+    return -(-(-(-P // dp)) // 64) * 64
+
+
+def model_state_bytes(d: ModelDesc, P: int, offloaded: bool, dp: int = 1) -> int:
     """bf16: weight 2 + fp32 grad 4 + fp32 master 4 + Adam m,v 8 = 18 B/param;
     fp32: weight(=master) 4 + grad 4 + m,v 8 = 16 B/param.
-    T-Offload keeps only weight + grad on the device."""
+    T-Offload keeps only weight + grad on the device. With dp > 1
+    data-parallel replicas (ZeRO-1) the weight and grad stay whole and
+    the master / m / v cover one shard."""
     if offloaded:
         return P * (d.es + 4)
     master = 4 if d.dtype == BF16 else 0
-    return P * (d.es + 4 + master + 8)
+    if dp == 1:
+        return P * (d.es + 4 + master + 8)
+    return P * (d.es + 4) + zero1_shard(P, dp) * (master + 8)
 
 
 SOPT_SLICE = 8388608   # parameters per streamed-optimizer slice (include/tpipe.h)
@@ -227,7 +238,7 @@ def act_offload_sets(order, d_release: int, d_prefetch: int):
 def build_streams(d: ModelDesc, p: int, m: int, strategy: str, k=None,
                   window: int = 2, offload_model_state: bool = False,
                   offload_activations: bool = False, act_distance: int = 2,
-                  offload_device_opt: bool = False, recomp_layers: int = 0):
+                  offload_device_opt: bool = False, recomp_layers: int = 0, dp: int = 1):
     """Per-stage instruction streams. Returns (streams, static)
     where static[s] = list of (name, category, bytes) live for the whole step.
     ``recomp_layers`` = r of partial T-Recomp (0 = all chunk-1 layers)."""
@@ -236,6 +247,8 @@ def build_streams(d: ModelDesc, p: int, m: int, strategy: str, k=None,
         raise ValueError("offload requires v=2")
     if offload_device_opt and not offload_model_state:
         raise ValueError("device optimizer streaming applies to model-state offload")
+    if dp > 1 and offload_model_state:
+        raise ValueError("ZeRO-1 data parallelism shards the device optimizer (no model-state offload)")
     if offload_activations and (v != 2 or trecomp):
         raise ValueError("activation offload applies to T-Pipe chunk 1 (no T-Recomp)")
     orders = S.strategy_orders(ostrat, p, m, k=k)[0]
@@ -258,7 +271,7 @@ def build_streams(d: ModelDesc, p: int, m: int, strategy: str, k=None,
             P = chunk_params(d, p, v, s, c)
             off = offload_model_state and c == v
             extra = sopt_staging_bytes(P) if (off and offload_device_opt) else 0
-            st.append((f"MS{c}", "model_state", model_state_bytes(d, P, off) + extra))
+            st.append((f"MS{c}", "model_state", model_state_bytes(d, P, off, dp) + extra))
         if s == 0:
             st.append(("TOKENS", "io", 4 * m * d.tokens))
         if s == p - 1:
@@ -302,6 +315,9 @@ def build_streams(d: ModelDesc, p: int, m: int, strategy: str, k=None,
             # 2. receive before the consuming op
             if offload_model_state and kind == "F" and c == v and i == first_f[v]:
                 out.append(Instr("W_WAIT", chunk=v))
+            if dp > 1 and kind == "F" and i == first_f[c]:
+                # the replicas' previous-step ZeRO-1 update of this chunk is complete
+                out.append(Instr("DP_WAIT", chunk=c))
             if kind == "F" and z["input_is_act"]:
                 src = _src_stage(s, c, p, "F")
                 if src is not None and src != s:
@@ -370,6 +386,8 @@ def build_streams(d: ModelDesc, p: int, m: int, strategy: str, k=None,
                 elif offload_model_state and c == v:
                     out.append(Instr("GRAD_D2H", chunk=c))
                     out.append(Instr("HOST_OPT", chunk=c))
+                elif dp > 1:
+                    out.append(Instr("DP_OPT", chunk=c))
                 else:
                     out.append(Instr("OPT", chunk=c))
             # weight upload right after the stage's first forward

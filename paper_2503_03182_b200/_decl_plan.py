@@ -15,7 +15,8 @@ class PlanOpts(C.Structure):
     _fields_ = [("strategy", i32), ("delay_rounds", i32), ("send_window", i32), ("offload", i32),
                 ("act_distance", i32), ("recomp_layers", i32), ("stage_layers", i32 * 64),
                 ("host_link_bps", C.c_double), ("host_adam_params_per_s", C.c_double),
-                ("device_flops", C.c_double), ("balance", i32), ("stage_chunk1", i32 * 64)]
+                ("device_flops", C.c_double), ("balance", i32), ("stage_chunk1", i32 * 64),
+                ("dp", i32)]
 
 
 class Op(C.Structure):
@@ -40,7 +41,7 @@ class PlanInfo(C.Structure):
                 ("delay_rounds", i32), ("send_window", i32), ("offload", i32), ("act_distance", i32),
                 ("layers_chunk", i32 * 2), ("n_channels", i32), ("params_total", u64),
                 ("recomp_layers", i32), ("est_step_s", C.c_double),
-                ("est_exposed_offload_s", C.c_double), ("balanced", i32)]
+                ("est_exposed_offload_s", C.c_double), ("balanced", i32), ("dp", i32)]
 
 
 class SimReport(C.Structure):
@@ -55,7 +56,7 @@ class RuntimeOpts(C.Structure):
     _fields_ = [("stage", i32), ("device", i32), ("nccl_ids", vp), ("pool_cap", u64),
                 ("lr", f32), ("beta1", f32), ("beta2", f32), ("eps", f32), ("weight_decay", f32),
                 ("transport", i32), ("timeout_ms", i32), ("ipc_name", C.c_char_p),
-                ("debug_flags", u32)]
+                ("debug_flags", u32), ("dp_rank", i32)]
 
 
 class RuntimeStats(C.Structure):

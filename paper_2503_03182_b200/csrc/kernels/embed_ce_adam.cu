@@ -370,6 +370,39 @@ int adamw(int dtype, float* master, float* m, float* v, float* grad, void* w, lo
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
+// ZeRO-1 step (R31): one thread per parameter of this replica's shard; the
+// reduction over replicas is in replica order, so every run and every
+// replica sees the same bits.
+template <typename T>
+__global__ void dp_adamw_kernel(const DpPtrs p, int dp, float* __restrict__ master, float* __restrict__ m,
+                                float* __restrict__ v, long lo, long n, int decay, AdamHyper hp) {
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const long gi = lo + i;
+    float g = 0.f;
+    for (int j = 0; j < dp; ++j) g = f_add(g, p.grad[j][gi]);
+    for (int j = 0; j < dp; ++j) p.grad[j][gi] = 0.f;
+    AdamOut o = adam_elem(master[i], m[i], v[i], g, decay, hp);
+    master[i] = o.w;
+    m[i] = o.m;
+    v[i] = o.v;
+    const T wv = from_f<T>(o.w);
+    for (int j = 0; j < dp; ++j) reinterpret_cast<T*>(p.w[j])[gi] = wv;
+}
+
+int dp_adamw(int dtype, const DpPtrs& p, int dp, float* master, float* m, float* v, long lo, long n,
+             int decay, const AdamHyper& hp, cudaStream_t st) {
+    if (n <= 0) return 0;
+    if (dp < 1 || dp > 64) return -4;
+    const int blocks = (int)((n + 255) / 256);
+    if (dtype == DT_BF16)
+        dp_adamw_kernel<bf16><<<blocks, 256, 0, st>>>(p, dp, master, m, v, lo, n, decay, hp);
+    else
+        dp_adamw_kernel<float><<<blocks, 256, 0, st>>>(p, dp, master, m, v, lo, n, decay, hp);
+    note_launches(1);
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
 // ============================================================== misc
 int fill_zero(void* p, size_t bytes, cudaStream_t st) {
     return cudaMemsetAsync(p, 0, bytes, st) == cudaSuccess ? 0 : -3;

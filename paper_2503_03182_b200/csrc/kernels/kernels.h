@@ -133,6 +133,18 @@ struct AdamHyper {
 };
 // master/m/v/grad fp32 [n]; w (es) [n] = master rounded (bf16) or master itself (fp32: w==master).
 // decay_mask: per-element? No: ranges [dec_lo, dec_hi) list handled by caller -> one call per range.
+// ZeRO-1 data parallelism (DESIGN R31): the replicas' gradient and weight
+// buffers of one chunk, as seen from this process (peer memory over NVLink).
+struct DpPtrs {
+    float* grad[64];
+    void* w[64];
+};
+// Fused reduce-scatter + AdamW + all-gather over peer memory for the global
+// parameter range [lo, lo + n) of the chunk (this replica's shard segment):
+// g = sum_j grad_j (replica order), grad_j = 0, AdamW on master/m/v (shard-local
+// arrays, element i <-> lo + i), the new weight written into every replica's w.
+int dp_adamw(int dtype, const DpPtrs& p, int dp, float* master, float* m, float* v, long lo, long n,
+             int decay, const AdamHyper& hp, cudaStream_t st);
 int adamw(int dtype, float* master, float* m, float* v, float* grad, void* w, long n, int decay,
           const AdamHyper& hp, cudaStream_t st);
 // host reference of the same arithmetic, bit-identical (T-Offload host optimizer)

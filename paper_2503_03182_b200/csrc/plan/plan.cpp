@@ -58,6 +58,11 @@ uint64_t chunk_params(const tpipe_model_desc& d, int p, int v, const int layers[
     return P;
 }
 
+uint64_t zero1_shard(uint64_t P, int dp) {
+    const uint64_t s = (P + dp - 1) / dp;
+    return (s + 63) / 64 * 64;
+}
+
 // per-layer stash: x_in, ln1 stats, qkv, attn out, lse, x_mid, ln2 stats, u (fc1 pre-act)
 static uint64_t layer_stash_bytes(const tpipe_model_desc& d) {
     const uint64_t M = (uint64_t)d.micro_batch * d.seq_len, h = d.hidden, a = d.n_heads,
@@ -313,10 +318,13 @@ static int build(tpipe_plan* P, bool trecomp, bool full_recomp) {
             P->chunk_params[s][c - 1] = np;
             P->params_total += np;
             const bool o = off && c == v;
-            const uint64_t per = o ? (es + 4) : (es + 4 + (d.dtype == TPIPE_BF16 ? 4 : 0) + 8);
+            const uint64_t opt_b = (d.dtype == TPIPE_BF16 ? 4 : 0) + 8;   // master (bf16 mode) + m, v
+            // ZeRO-1 (R31): master / m / v cover one shard of the chunk
+            const uint64_t ms = o ? np * (es + 4)
+                                  : np * (es + 4) + (P->dp > 1 ? zero1_shard(np, P->dp) : np) * opt_b;
             // streamed device AdamW (R24): + double-buffered master/m/v slice staging
             const uint64_t stg = (o && sopt) ? 2ull * 12ull * std::min<uint64_t>(np, TPIPE_SOPT_SLICE_PARAMS) : 0;
-            B.bufs.push_back({TPIPE_BUF_STATIC, TPIPE_CAT_MODEL_STATE, c, 0, np * per + stg});
+            B.bufs.push_back({TPIPE_BUF_STATIC, TPIPE_CAT_MODEL_STATE, c, 0, ms + stg});
         }
         if (s == 0) B.bufs.push_back({TPIPE_BUF_STATIC, TPIPE_CAT_IO, 0, 0, 4ull * m * M});
         if (s == p - 1) B.bufs.push_back({TPIPE_BUF_STATIC, TPIPE_CAT_IO, 0, 1, 4ull * m * M + 4ull * m});
@@ -393,6 +401,7 @@ static int build(tpipe_plan* P, bool trecomp, bool full_recomp) {
             }
             // 2. weight-upload wait and receives
             if (off && kind == KF && c == v && i == first_f[v]) B.emit(TPIPE_OP_W_WAIT, v, 0, -1, -1, -1, {});
+            if (P->dp > 1 && kind == KF && i == first_f[c]) B.emit(TPIPE_OP_DP_WAIT, c, 0, -1, -1, -1, {});
             if (kind == KF && zz.input_is_act) {
                 const int src = src_stage(s, c, p, v, KF);
                 if (src >= 0 && src != s) {
@@ -467,7 +476,7 @@ static int build(tpipe_plan* P, bool trecomp, bool full_recomp) {
                     B.emit(TPIPE_OP_GRAD_D2H, c, 0, -1, -1, -1, {});
                     B.emit(TPIPE_OP_HOST_OPT, c, 0, -1, -1, -1, {});
                 } else {
-                    B.emit(TPIPE_OP_OPT, c, 0, -1, -1, -1, {});
+                    B.emit(P->dp > 1 ? TPIPE_OP_DP_OPT : TPIPE_OP_OPT, c, 0, -1, -1, -1, {});
                 }
             }
             // 6. weight upload after the first forward
@@ -728,7 +737,7 @@ static double estimate(const tpipe_plan* P, const CostModel& cm, double* exposed
 
 static int make_plan(const tpipe_model_desc* model, int p, int m, int strategy, int k, int W,
                      int offload, int act_distance, int recomp_layers, const int32_t* stage_layers,
-                     const int32_t* stage_chunk1, const CostModel& cm, tpipe_plan** out) {
+                     const int32_t* stage_chunk1, const CostModel& cm, tpipe_plan** out, int dp = 1) {
     if ((offload & TPIPE_OFFLOAD_DEVICE_OPT) && !(offload & TPIPE_OFFLOAD_MODEL_STATE))
         return set_error(TPIPE_E_INVALID, "offload: DEVICE_OPT needs MODEL_STATE");
     if ((offload & TPIPE_OFFLOAD_ACTIVATIONS) && strategy != TPIPE_S_TPIPE)
@@ -742,6 +751,11 @@ static int make_plan(const tpipe_model_desc* model, int p, int m, int strategy, 
     P->W = W;
     P->offload = offload;
     P->act_distance = act_distance > 0 ? act_distance : 1;   // derived below when 0 (Q12)
+    P->dp = dp;
+    if (dp > 1 && (offload & TPIPE_OFFLOAD_MODEL_STATE)) {
+        delete P;
+        return set_error(TPIPE_E_INCOMPAT, "dp > 1 shards the device optimizer (ZeRO-1): no model-state offload");
+    }
     const bool is_il = strategy == TPIPE_S_INTERLEAVE || strategy == TPIPE_S_INTERLEAVE_TRECOMP;
     const bool is_tp = strategy == TPIPE_S_TPIPE || strategy == TPIPE_S_TPIPE_TRECOMP || is_il;
     if (is_il && m % p) {
@@ -993,6 +1007,8 @@ TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, in
     if (o.recomp_layers < 0) return set_error(TPIPE_E_INVALID, "recomp_layers");
     if (o.host_link_bps < 0 || o.host_adam_params_per_s < 0 || o.device_flops < 0)
         return set_error(TPIPE_E_INVALID, "cost model rates must be >= 0");
+    if (o.dp < 0 || o.dp > 64) return set_error(TPIPE_E_INVALID, "dp must be in [1, 64]");
+    const int dp = o.dp > 0 ? o.dp : 1;
     CostModel cm;
     if (o.host_link_bps > 0) cm.bw = o.host_link_bps;
     if (o.host_adam_params_per_s > 0) cm.host = o.host_adam_params_per_s;
@@ -1032,7 +1048,7 @@ TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, in
         const int off = o.offload < 0 ? 0 : o.offload;
         tpipe_plan* P = nullptr;
         int rc = make_plan(model, n_stages, n_microbatches, o.strategy, o.delay_rounds, W, off,
-                           o.act_distance, o.recomp_layers, part, chunk1, cm, &P);
+                           o.act_distance, o.recomp_layers, part, chunk1, cm, &P, dp);
         if (rc) return rc;
         if (hbm_budget_bytes && max_peak(P) > hbm_budget_bytes) {
             const uint64_t pk = max_peak(P);
@@ -1066,7 +1082,7 @@ TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, in
     for (auto& rung : ladder) {
         tpipe_plan* P = nullptr;
         int rc = make_plan(model, n_stages, n_microbatches, rung[0], o.delay_rounds, W, rung[1],
-                           o.act_distance, rung[2], part, chunk1, cm, &P);
+                           o.act_distance, rung[2], part, chunk1, cm, &P, dp);
         if (rc) {
             if (rc == TPIPE_E_INCOMPAT || rc == TPIPE_E_INVALID) continue;   // rung not applicable
             delete best;
@@ -1106,6 +1122,7 @@ TP_API int tpipe_plan_get_info(const tpipe_plan* P, tpipe_plan_info* out) {
     out->est_step_s = P->est_step_s;
     out->est_exposed_offload_s = P->est_exposed_s;
     out->balanced = P->balanced ? 1 : 0;
+    out->dp = P->dp;
     return 0;
 }
 

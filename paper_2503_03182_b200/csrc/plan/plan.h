@@ -21,6 +21,7 @@ struct tpipe_plan {
     uint64_t hbm_budget = 0;   // per-stage budget the plan was fitted to (0 = none)
     double est_step_s = 0, est_exposed_s = 0;   // cost model (DESIGN R28)
     bool balanced = false;     // cost-balanced partition chosen by the planner
+    int dp = 1;                // data-parallel replicas (ZeRO-1, R31)
     // per stage
     std::vector<std::vector<tpipe_op>> ops;
     std::vector<std::vector<tpipe_buf>> bufs;
@@ -43,6 +44,8 @@ struct ChunkSizes {
 
 int delay_rounds_appB(int p);
 uint64_t layer_params(const tpipe_model_desc& d);
+// ZeRO-1 shard (R31): ceil(P / dp) rounded up to 64 parameters
+uint64_t zero1_shard(uint64_t P, int dp);
 uint64_t chunk_params(const tpipe_model_desc& d, int p, int v, const int layers[2], int s, int c);
 
 }  // namespace tpipe

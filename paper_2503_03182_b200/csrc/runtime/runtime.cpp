@@ -23,6 +23,7 @@
 #include <map>
 #include <memory>
 #include <new>
+#include <string>
 #include <thread>
 #include <tuple>
 #include <vector>
@@ -76,6 +77,12 @@ struct ChunkState {
     bool sopt = false;
     long slice = 0;
     float* stg[2] = {nullptr, nullptr};
+    // ZeRO-1 data parallelism (R31): this replica's optimizer shard [lo, hi)
+    // of the chunk's parameters, the replicas' grad / weight pointers, and the
+    // sequence number of the last DP_OPT (0 = none yet)
+    long lo = 0, hi = 0;
+    DpPtrs dptr{};
+    uint64_t dp_seq = 0;
     cudaEvent_t ev_sopt_done = nullptr;   // last slice's AdamW done (w, grad final)
     cudaEvent_t ev_sopt_out = nullptr;    // last slice's master/m/v back on the host
     bool sopt_done_pending = false, sopt_out_pending = false;
@@ -111,6 +118,8 @@ struct tpipe_runtime {
     std::vector<int> owned;
     std::vector<std::unique_ptr<StageState>> st;   // indexed by stage (null if not owned)
     std::unique_ptr<Transport> tr;
+    std::unique_ptr<DpGroup> dpg;      // dp > 1: this stage's replica group
+    int dp_rank = 0;
     int transport_kind = -1;           // -1 virtual, else TPIPE_TRANSPORT_*
     int timeout_ms = 300000;
     uint32_t debug = 0;
@@ -333,7 +342,7 @@ int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags
             a.tokens = S.tokens ? S.tokens + (long)(i - 1) * D.M : nullptr;
             a.targets = (S.targets && s == p - 1 && c == v) ? S.targets + (long)(i - 1) * D.M : nullptr;
             a.loss_slot = S.loss_slots ? S.loss_slots + (i - 1) : nullptr;
-            a.loss_scale = 1.0f / ((float)P.m * (float)D.M);
+            a.loss_scale = 1.0f / ((float)(P.dp * P.m) * (float)D.M);
             void* ws = nullptr;
             op_alloc_ptr(rt, S, op, TPIPE_BUF_WS, -1, &ws);
             a.ws = (uint8_t*)ws;
@@ -376,7 +385,7 @@ int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags
             a.tokens = S.tokens ? S.tokens + (long)(i - 1) * D.M : nullptr;
             a.targets = head ? S.targets + (long)(i - 1) * D.M : nullptr;
             a.loss_slot = (head && S.loss_slots) ? S.loss_slots + (i - 1) : nullptr;
-            a.loss_scale = 1.0f / ((float)P.m * (float)D.M);
+            a.loss_scale = 1.0f / ((float)(P.dp * P.m) * (float)D.M);
             void* stp = (trecomp && c == 1) ? live_get(S, TPIPE_BUF_RBUF, c, i)
                                             : live_get(S, TPIPE_BUF_STASH, c, i);
             a.stash = (uint8_t*)stp;
@@ -422,6 +431,32 @@ int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags
         case TPIPE_OP_OPT:
             if (!no_opt) TRY(adam_chunk(rt, S.ch[c], hyper(rt, rt->t + 1), cs));
             break;
+        case TPIPE_OP_DP_OPT: {
+            // ZeRO-1 (R31): every replica's chunk-c gradients are final -> this
+            // replica reduces its shard over the replicas, updates it, and writes
+            // the new weights into every replica (one fused kernel per segment)
+            if (no_opt) break;
+            ChunkState& C = S.ch[c];
+            const uint64_t seq = (uint64_t)rt->t + 1;
+            TRY(rt->dpg->post_ready(c, seq, cs));
+            TRY(rt->dpg->wait_ready(c, seq, cs));
+            const AdamHyper hp = hyper(rt, rt->t + 1);
+            for (auto& sg : C.lay.segments) {
+                const long a = std::max(C.lo, (long)sg[0]), b = std::min(C.hi, (long)(sg[0] + sg[1]));
+                if (a >= b) continue;
+                if (dp_adamw(D.dtype, C.dptr, P.dp, C.master + (a - C.lo), C.m + (a - C.lo), C.v + (a - C.lo), a,
+                             b - a, (int)sg[2], hp, cs))
+                    return set_error(TPIPE_E_CUDA, "dp_adamw launch failed");
+            }
+            TRY(rt->dpg->post_done(c, seq, cs));
+            C.dp_seq = seq;
+            break;
+        }
+        case TPIPE_OP_DP_WAIT: {
+            ChunkState& C = S.ch[c];
+            if (C.dp_seq) TRY(rt->dpg->wait_done(c, C.dp_seq, cs));
+            break;
+        }
         case TPIPE_OP_GRAD_D2H: {
             if (no_opt) break;
             ChunkState& C = S.ch[c];
@@ -623,6 +658,14 @@ int run_step_impl(tpipe_runtime* rt, const int32_t* tok_dev, const int32_t* tgt_
         }
         if (!prog) return set_error(TPIPE_E_DEADLOCK, "virtual transport made no progress");
     }
+    if (rt->dpg && !(flags & TPIPE_STEP_NO_OPT)) {
+        // synchronous data parallelism: the step is complete when every replica
+        // has written this step's weights into this replica
+        for (int s : rt->owned)
+            for (int c = 1; c <= P.v; ++c)
+                if (rt->st[s]->ch[c].dp_seq == (uint64_t)rt->t + 1)
+                    TRY(rt->dpg->wait_done(c, rt->st[s]->ch[c].dp_seq, rt->st[s]->cs));
+    }
     for (int s : rt->owned) {   // join: the step stream waits for every stage
         StageState& S = *rt->st[s];
         if (S.cs == cs) continue;
@@ -717,6 +760,9 @@ TP_API int tpipe_runtime_create(const tpipe_plan* plan, const tpipe_runtime_opts
     o.stage = -1;
     if (opts) o = *opts;
     if (o.stage < -1 || o.stage >= plan->p) return set_error(TPIPE_E_INVALID, "stage");
+    if (plan->dp > 1 && (o.stage < 0 || !o.ipc_name || o.dp_rank < 0 || o.dp_rank >= plan->dp))
+        return set_error(TPIPE_E_INVALID, "dp > 1 needs stage >= 0, an ipc_name and 0 <= dp_rank < dp");
+    if (plan->dp == 1 && o.dp_rank != 0) return set_error(TPIPE_E_INVALID, "dp_rank with dp = 1");
     if ((long)plan->model.micro_batch * plan->model.seq_len % 8)
         return set_error(TPIPE_E_INVALID, "micro_batch*seq_len must be a multiple of 8");
     std::unique_ptr<tpipe_runtime> rt(new (std::nothrow) tpipe_runtime(*plan));
@@ -791,14 +837,18 @@ TP_API int tpipe_runtime_create(const tpipe_plan* plan, const tpipe_runtime_opts
                 C.grad = (float*)q;
                 q += (size_t)C.P * 4;
                 if (!C.offloaded) {
+                    // optimizer shard (ZeRO-1, R31; the whole chunk when dp = 1)
+                    const long S1 = P.dp > 1 ? (long)zero1_shard((uint64_t)C.P, P.dp) : C.P;
+                    C.lo = std::min(C.P, (long)o.dp_rank * S1);
+                    C.hi = std::min(C.P, C.lo + S1);
                     if (D.dtype == DT_BF16) {
                         C.master = (float*)q;
-                        q += (size_t)C.P * 4;
+                        q += (size_t)S1 * 4;
                     } else {
-                        C.master = (float*)C.w;
+                        C.master = (float*)C.w + C.lo;   // fp32: the weights are the master
                     }
                     C.m = (float*)q;
-                    q += (size_t)C.P * 4;
+                    q += (size_t)S1 * 4;
                     C.v = (float*)q;
                 } else {
                     CU(cudaHostAlloc(&C.h_master, (size_t)C.P * 4, cudaHostAllocDefault));
@@ -832,12 +882,38 @@ TP_API int tpipe_runtime_create(const tpipe_plan* plan, const tpipe_runtime_opts
     }
     // stage transport (runtime/transport.h)
     CU(cudaDeviceSynchronize());   // static buffers initialised before peers map the arena
+    rt->dp_rank = o.dp_rank;
+    std::string ipc_pipe = o.ipc_name ? o.ipc_name : "";
+    if (P.dp > 1) {
+        StageState& S0 = *rt->st[o.stage];
+        uint8_t* arena = (uint8_t*)S0.pool->arena();
+        uint64_t w_off[3] = {0, 0, 0}, g_off[3] = {0, 0, 0};
+        for (int c = 1; c <= P.v; ++c) {
+            ChunkState& C = S0.ch[c];
+            const uint8_t *w = (const uint8_t*)C.w, *g = (const uint8_t*)C.grad;
+            if (w < arena || g < arena || w >= arena + S0.pool->arena_bytes())
+                return set_error(TPIPE_E_STATE, "dp: model state outside the pool arena");
+            w_off[c] = (uint64_t)(w - arena);
+            g_off[c] = (uint64_t)(g - arena);
+        }
+        const std::string dp_name = std::string(o.ipc_name) + "_s" + std::to_string(o.stage);
+        TRY(make_dp_group(P.dp, o.dp_rank, o.stage, P.v, dp_name.c_str(), arena, S0.pool->arena_bytes(), w_off,
+                          g_off, rt->timeout_ms, &rt->dpg));
+        for (int c = 1; c <= P.v; ++c) {
+            ChunkState& C = S0.ch[c];
+            for (int j = 0; j < P.dp; ++j) {
+                C.dptr.grad[j] = rt->dpg->peer_grad(j, c);
+                C.dptr.w[j] = rt->dpg->peer_w(j, c);
+            }
+        }
+        ipc_pipe += "_r" + std::to_string(o.dp_rank);   // each replica's own pipeline rendezvous
+    }
     if (o.stage < 0 || P.p == 1) {
         rt->tr = make_virtual_transport(P.channels);
         rt->transport_kind = -1;
     } else if (o.transport == TPIPE_TRANSPORT_IPC) {
         Pool& pl = *rt->st[o.stage]->pool;
-        TRY(make_ipc_transport(P.channels, P.p, o.stage, o.device, o.ipc_name, pl.arena(),
+        TRY(make_ipc_transport(P.channels, P.p, o.stage, o.device, ipc_pipe.c_str(), pl.arena(),
                                pl.arena_bytes(), P.W, rt->timeout_ms, &rt->tr));
         rt->transport_kind = TPIPE_TRANSPORT_IPC;
     } else if (o.transport == TPIPE_TRANSPORT_NCCL) {
@@ -872,6 +948,7 @@ TP_API void tpipe_runtime_destroy(tpipe_runtime* rt) {
         }
     }
     rt->tr.reset();
+    rt->dpg.reset();
     for (auto e : rt->evpool) cudaEventDestroy(e);
     for (auto e : rt->tevpool) cudaEventDestroy(e);
     if (rt->h_tok_stage) cudaFreeHost(rt->h_tok_stage);
@@ -910,13 +987,18 @@ TP_API int tpipe_runtime_set_params(tpipe_runtime* rt, int32_t s, int32_t c, con
     // stream-ordered copies: a pageable cudaMemcpy may return before its DMA
     // lands, so the cast kernel below must be ordered on the same stream
     if (!C->offloaded) {
-        CU(cudaMemcpyAsync(C->master, src, n * 4, cudaMemcpyHostToDevice, rt->stream));
+        // the full fp32 values go through the grad buffer (zeroed below): the
+        // weights take all of them, the master only this replica's shard
+        const long sh = C->hi - C->lo;
         if (rt->D.dtype == DT_BF16) {
-            if (cast_f32_to(DT_BF16, C->master, C->w, (long)n, rt->stream))
-                return set_error(TPIPE_E_CUDA, "cast");
+            CU(cudaMemcpyAsync(C->grad, src, n * 4, cudaMemcpyHostToDevice, rt->stream));
+            if (cast_f32_to(DT_BF16, C->grad, C->w, (long)n, rt->stream)) return set_error(TPIPE_E_CUDA, "cast");
+            CU(cudaMemcpyAsync(C->master, C->grad + C->lo, (size_t)sh * 4, cudaMemcpyDeviceToDevice, rt->stream));
+        } else {
+            CU(cudaMemcpyAsync(C->w, src, n * 4, cudaMemcpyHostToDevice, rt->stream));
         }
-        CU(cudaMemsetAsync(C->m, 0, n * 4, rt->stream));
-        CU(cudaMemsetAsync(C->v, 0, n * 4, rt->stream));
+        CU(cudaMemsetAsync(C->m, 0, (size_t)sh * 4, rt->stream));
+        CU(cudaMemsetAsync(C->v, 0, (size_t)sh * 4, rt->stream));
     } else {
         std::memcpy(C->h_master, src, n * 4);
         std::memset(C->h_m, 0, n * 4);
@@ -935,8 +1017,25 @@ TP_API int tpipe_runtime_get_params(tpipe_runtime* rt, int32_t s, int32_t c, flo
     TRY(chunk_of(rt, s, c, n, &C));
     join_host(*C);
     CU(cudaStreamSynchronize(rt->stream));
-    if (C->offloaded) std::memcpy(dst, C->h_master, n * 4);
-    else CU(cudaMemcpyAsync(dst, C->master, n * 4, cudaMemcpyDeviceToHost, rt->stream));
+    if (C->offloaded) {
+        std::memcpy(dst, C->h_master, n * 4);
+    } else if (rt->D.dtype == DT_FP32) {
+        CU(cudaMemcpyAsync(dst, C->w, n * 4, cudaMemcpyDeviceToHost, rt->stream));   // w is the master
+    } else if (C->lo == 0 && C->hi == C->P) {
+        CU(cudaMemcpyAsync(dst, C->master, n * 4, cudaMemcpyDeviceToHost, rt->stream));
+    } else {
+        // ZeRO-1 (R31): the master of this replica's shard; elsewhere the bf16
+        // weights (= RNE of the owning replica's master) widened to fp32
+        std::vector<uint16_t> wb(n);
+        CU(cudaMemcpyAsync(wb.data(), C->w, n * 2, cudaMemcpyDeviceToHost, rt->stream));
+        CU(cudaStreamSynchronize(rt->stream));
+        for (uint64_t i = 0; i < n; ++i) {
+            const uint32_t u = (uint32_t)wb[i] << 16;
+            std::memcpy(&dst[i], &u, 4);
+        }
+        CU(cudaMemcpyAsync(dst + C->lo, C->master, (size_t)(C->hi - C->lo) * 4, cudaMemcpyDeviceToHost,
+                           rt->stream));
+    }
     CU(cudaStreamSynchronize(rt->stream));
     return 0;
 }

@@ -515,4 +515,155 @@ int make_ipc_transport(const ChannelList& ch, int p, int stage, int device, cons
     return 0;
 }
 
+// ================================================================ dp group
+namespace {
+
+constexpr int DP_MAX = 64;
+struct alignas(64) DpMember {
+    cudaIpcMemHandle_t arena;
+    uint64_t arena_bytes;
+    uint64_t w_off[3], g_off[3];
+    cudaIpcEventHandle_t ready[3], done[3];
+    std::atomic<uint64_t> ready_seq[3], done_seq[3];
+};
+struct alignas(64) DpHeader {
+    std::atomic<uint64_t> magic;
+    std::atomic<int32_t> dp, v;
+    std::atomic<int32_t> arrived;
+    std::atomic<int32_t> abort;
+};
+constexpr uint64_t DP_MAGIC = 0x7470697065445030ull;
+
+class IpcDpGroup final : public DpGroup {
+public:
+    ~IpcDpGroup() override {
+        for (int j = 0; j < dp_; ++j)
+            for (int c = 0; c < 3; ++c) {
+                if (ev_ready_[j][c]) cudaEventDestroy(ev_ready_[j][c]);
+                if (ev_done_[j][c]) cudaEventDestroy(ev_done_[j][c]);
+            }
+        for (int j = 0; j < dp_; ++j)
+            if (j != rank_ && peer_arena_[j]) cudaIpcCloseMemHandle(peer_arena_[j]);
+        if (shm_) munmap(shm_, shm_bytes_);
+    }
+    int dp() const override { return dp_; }
+    int rank() const override { return rank_; }
+    DpHeader* hdr() const { return (DpHeader*)shm_; }
+    DpMember& mem(int j) const { return ((DpMember*)(shm_ + sizeof(DpHeader)))[j]; }
+    bool aborted() const { return hdr()->abort.load(std::memory_order_acquire) != 0; }
+    void abort() override {
+        if (shm_) hdr()->abort.store(1, std::memory_order_release);
+    }
+    int post(cudaEvent_t e, std::atomic<uint64_t>& slot, uint64_t seq, cudaStream_t cs) {
+        if (cudaEventRecord(e, cs)) return set_error(TPIPE_E_CUDA, "dp: event record");
+        slot.store(seq, std::memory_order_release);
+        return 0;
+    }
+    int wait_all(bool ready, int c, uint64_t seq, cudaStream_t cs) {
+        for (int j = 0; j < dp_; ++j) {
+            if (j == rank_) continue;
+            std::atomic<uint64_t>& s = ready ? mem(j).ready_seq[c] : mem(j).done_seq[c];
+            if (int rc = poll_until([&] { return s.load(std::memory_order_acquire) >= seq; },
+                                    [&] { return aborted(); }, timeout_ms_, ready ? "dp ready" : "dp done"))
+                return rc;
+            if (cudaStreamWaitEvent(cs, ready ? ev_ready_[j][c] : ev_done_[j][c], 0))
+                return set_error(TPIPE_E_CUDA, "dp: stream wait");
+        }
+        return 0;
+    }
+    int post_ready(int c, uint64_t seq, cudaStream_t cs) override {
+        return post(ev_ready_[rank_][c], mem(rank_).ready_seq[c], seq, cs);
+    }
+    int wait_ready(int c, uint64_t seq, cudaStream_t cs) override { return wait_all(true, c, seq, cs); }
+    int post_done(int c, uint64_t seq, cudaStream_t cs) override {
+        return post(ev_done_[rank_][c], mem(rank_).done_seq[c], seq, cs);
+    }
+    int wait_done(int c, uint64_t seq, cudaStream_t cs) override { return wait_all(false, c, seq, cs); }
+    void* peer_w(int j, int c) override { return (uint8_t*)arena_of(j) + mem(j).w_off[c]; }
+    float* peer_grad(int j, int c) override { return (float*)((uint8_t*)arena_of(j) + mem(j).g_off[c]); }
+    void* arena_of(int j) const { return j == rank_ ? own_arena_ : peer_arena_[j]; }
+
+    int init(int dp, int rank, int v, const char* name, void* arena, size_t arena_bytes, const uint64_t* w_off,
+             const uint64_t* g_off, int timeout_ms) {
+        dp_ = dp;
+        rank_ = rank;
+        timeout_ms_ = timeout_ms;
+        own_arena_ = arena;
+        if (dp < 2 || dp > DP_MAX || rank < 0 || rank >= dp || v < 1 || v > 2)
+            return set_error(TPIPE_E_INVALID, "dp group: dp %d rank %d", dp, rank);
+        if (!name || name[0] != '/') return set_error(TPIPE_E_INVALID, "dp group needs an ipc_name ('/...')");
+        shm_bytes_ = sizeof(DpHeader) + (size_t)dp * sizeof(DpMember);
+        int fd = shm_open(name, O_CREAT | O_RDWR, 0600);
+        if (fd < 0) return set_error(TPIPE_E_INVALID, "shm_open(%s): %s", name, strerror(errno));
+        if (ftruncate(fd, (off_t)shm_bytes_) != 0) {
+            close(fd);
+            return set_error(TPIPE_E_INVALID, "ftruncate(%s): %s", name, strerror(errno));
+        }
+        void* m = mmap(nullptr, shm_bytes_, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+        close(fd);
+        if (m == MAP_FAILED) return set_error(TPIPE_E_INVALID, "mmap(%s): %s", name, strerror(errno));
+        shm_ = (uint8_t*)m;
+        uint64_t zero = 0;
+        if (hdr()->magic.compare_exchange_strong(zero, DP_MAGIC)) {
+            hdr()->dp.store(dp);
+            hdr()->v.store(v);
+        } else if (zero != DP_MAGIC) {
+            return set_error(TPIPE_E_INVALID, "shm %s holds foreign data", name);
+        }
+        DpMember& me = mem(rank);
+        if (cudaIpcGetMemHandle(&me.arena, arena)) return set_error(TPIPE_E_CUDA, "dp: cudaIpcGetMemHandle");
+        me.arena_bytes = arena_bytes;
+        for (int c = 1; c <= v; ++c) {
+            me.w_off[c] = w_off[c];
+            me.g_off[c] = g_off[c];
+            if (cudaEventCreateWithFlags(&ev_ready_[rank][c], cudaEventDisableTiming | cudaEventInterprocess) ||
+                cudaEventCreateWithFlags(&ev_done_[rank][c], cudaEventDisableTiming | cudaEventInterprocess) ||
+                cudaIpcGetEventHandle(&me.ready[c], ev_ready_[rank][c]) ||
+                cudaIpcGetEventHandle(&me.done[c], ev_done_[rank][c]))
+                return set_error(TPIPE_E_CUDA, "dp: interprocess events");
+        }
+        std::atomic_thread_fence(std::memory_order_seq_cst);
+        hdr()->arrived.fetch_add(1, std::memory_order_acq_rel);
+        if (int rc = poll_until([&] { return hdr()->arrived.load(std::memory_order_acquire) >= dp; },
+                                [&] { return aborted(); }, timeout_ms, "dp rendezvous"))
+            return rc;
+        if (hdr()->dp.load() != dp || hdr()->v.load() != v)
+            return set_error(TPIPE_E_INVALID, "dp rendezvous: members disagree (dp, chunks)");
+        if (rank == 0) shm_unlink(name);
+        for (int j = 0; j < dp; ++j) {
+            if (j == rank) continue;
+            cudaError_t e = cudaIpcOpenMemHandle(&peer_arena_[j], mem(j).arena, cudaIpcMemLazyEnablePeerAccess);
+            if (e) return set_error(TPIPE_E_CUDA, "dp: cudaIpcOpenMemHandle (replica %d): %s", j, cudaGetErrorString(e));
+            for (int c = 1; c <= v; ++c)
+                if (cudaIpcOpenEventHandle(&ev_ready_[j][c], mem(j).ready[c]) ||
+                    cudaIpcOpenEventHandle(&ev_done_[j][c], mem(j).done[c]))
+                    return set_error(TPIPE_E_CUDA, "dp: cudaIpcOpenEventHandle (replica %d)", j);
+        }
+        return 0;
+    }
+
+    int dp_ = 0, rank_ = 0, timeout_ms_ = 0;
+    uint8_t* shm_ = nullptr;
+    size_t shm_bytes_ = 0;
+    void* own_arena_ = nullptr;
+    void* peer_arena_[DP_MAX] = {};
+    cudaEvent_t ev_ready_[DP_MAX][3] = {}, ev_done_[DP_MAX][3] = {};
+};
+
+}  // namespace
+
+int make_dp_group(int dp, int dp_rank, int stage, int v, const char* shm_name, void* arena,
+                  size_t arena_bytes, const uint64_t* w_off, const uint64_t* g_off, int timeout_ms,
+                  std::unique_ptr<DpGroup>* out) {
+    (void)stage;
+    std::unique_ptr<IpcDpGroup> G(new IpcDpGroup);
+    int rc = G->init(dp, dp_rank, v, shm_name, arena, arena_bytes, w_off, g_off, timeout_ms);
+    if (rc) {
+        G->abort();
+        return rc;
+    }
+    *out = std::move(G);
+    return 0;
+}
+
 }  // namespace tpipe

@@ -72,4 +72,31 @@ int make_ipc_transport(const ChannelList& ch, int p, int stage, int device, cons
                        void* arena, size_t arena_bytes, int window, int timeout_ms,
                        std::unique_ptr<Transport>* out);
 
+// Data-parallel group (DESIGN R31): the dp replicas of one
+// pipeline stage (one process each). Every member exports its pool arena, the
+// arena offsets of each chunk's weights and gradients, and two interprocess
+// events per chunk ("gradients final", "update done") through a POSIX-shm
+// rendezvous; host-side sequence numbers say which step an event belongs to.
+class DpGroup {
+public:
+    virtual ~DpGroup() = default;
+    virtual int dp() const = 0;
+    virtual int rank() const = 0;
+    // this member's chunk-c gradients are final up to the work issued on cs
+    virtual int post_ready(int c, uint64_t seq, cudaStream_t cs) = 0;
+    // cs waits until every member posted ready(c, seq)
+    virtual int wait_ready(int c, uint64_t seq, cudaStream_t cs) = 0;
+    virtual int post_done(int c, uint64_t seq, cudaStream_t cs) = 0;
+    virtual int wait_done(int c, uint64_t seq, cudaStream_t cs) = 0;
+    // member j's chunk-c weights / gradients in this process's address space
+    virtual void* peer_w(int j, int c) = 0;
+    virtual float* peer_grad(int j, int c) = 0;
+    virtual void abort() = 0;
+};
+
+// w_off / g_off[c]: arena offsets of chunk c's weights and gradients (c = 1..v)
+int make_dp_group(int dp, int dp_rank, int stage, int v, const char* shm_name, void* arena,
+                  size_t arena_bytes, const uint64_t* w_off, const uint64_t* g_off, int timeout_ms,
+                  std::unique_ptr<DpGroup>* out);
+
 }  // namespace tpipe

@@ -19,7 +19,7 @@ OFFLOAD_ACTIVATIONS = 2
 OFFLOAD_DEVICE_OPT = 4   # with OFFLOAD_MODEL_STATE: streamed device AdamW (DESIGN R24)
 OP_NAMES = ["F", "B", "R", "RECV_ACT", "RECV_GRAD", "SEND_ACT", "SEND_GRAD", "SEND_WAIT", "OPT",
             "GRAD_D2H", "HOST_OPT", "W_H2D", "W_WAIT", "ACT_D2H", "ACT_D2H_WAIT", "ACT_H2D",
-            "ACT_H2D_WAIT", "STREAM_OPT"]
+            "ACT_H2D_WAIT", "STREAM_OPT", "DP_OPT", "DP_WAIT"]
 CATS = ["model_state", "io", "act", "recomp_buf", "comm", "workspace"]
 
 
@@ -49,7 +49,7 @@ class Plan:
                  strategy="tpipe", delay_rounds: int = -1, send_window: int = 0, offload: int = 0,
                  act_distance: int = 0, recomp_layers: int = 0, stage_layers=None,
                  host_link_bps: float = 0.0, host_adam_params_per_s: float = 0.0,
-                 device_flops: float = 0.0, balance: bool = False, stage_chunk1=None):
+                 device_flops: float = 0.0, balance: bool = False, stage_chunk1=None, dp: int = 1):
         L = lib()
         st = -1 if strategy in (None, "auto") else STRATEGY.get(strategy, strategy)
         if st < 0 and offload == 0:
@@ -57,7 +57,7 @@ class Plan:
         sl = (C.c_int32 * 64)(*(list(stage_layers or [])[:64]))
         opts = D.PlanOpts(st, delay_rounds, send_window, offload, act_distance, recomp_layers, sl,
                           host_link_bps, host_adam_params_per_s, device_flops, 1 if balance else 0,
-                          (C.c_int32 * 64)(*(list(stage_chunk1 or [])[:64])))
+                          (C.c_int32 * 64)(*(list(stage_chunk1 or [])[:64])), dp)
         self._h = C.c_void_p()
         self.model = model
         check(L.tpipe_plan_create(C.byref(model.c()), n_stages, n_microbatches, hbm_budget,
@@ -72,6 +72,7 @@ class Plan:
         self.est_step_s = info.est_step_s
         self.est_exposed_offload_s = info.est_exposed_offload_s
         self.balanced = bool(info.balanced)
+        self.dp = info.dp
         # per-stage (chunk-1, chunk-2) layers (DESIGN R27); == [layers_chunk] * p when uniform
         self.partition = []
         for s in range(self.p):

@@ -24,7 +24,7 @@ class Runtime:
     def __init__(self, plan, stage: int = -1, device: int = 0, nccl_ids: bytes | None = None,
                  lr=3e-4, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1, pool_cap: int = 0,
                  transport: int = TRANSPORT_NCCL, timeout_ms: int = 0, ipc_name: str | None = None,
-                 debug_flags: int = 0):
+                 debug_flags: int = 0, dp_rank: int = 0):
         """stage -1: every stage in this process (virtual pipeline); stage >= 0:
         this process runs one stage and talks to its peers over `transport`
         (NCCL with `nccl_ids`, or CUDA IPC with the job-unique shm `ipc_name`)."""
@@ -33,7 +33,7 @@ class Runtime:
         self._ipc = ipc_name.encode() if ipc_name else None
         o = D.RuntimeOpts(stage, device, C.cast(self._ids, C.c_void_p) if self._ids else None,
                           pool_cap, lr, beta1, beta2, eps, weight_decay, transport, timeout_ms,
-                          self._ipc, debug_flags)
+                          self._ipc, debug_flags, dp_rank)
         self._h = C.c_void_p()
         check(lib().tpipe_runtime_create(plan.handle, C.byref(o), C.byref(self._h)),
               "tpipe_runtime_create")

@@ -8,7 +8,10 @@ Writes the stage's loss, gradients (after step 1, no optimizer) and
 parameters (after `steps` optimizer steps) to an .npz file.
 
     python tests/mp_stage_worker.py OUT.npz STAGE P M STRATEGY DTYPE IPC_NAME
-        L H A F V S B [STEPS] [OFFLOAD] [TIMEOUT_MS] [SEED]
+        L H A F V S B [STEPS] [OFFLOAD] [TIMEOUT_MS] [SEED] [DP] [DP_RANK]
+
+With DP > 1 (ZeRO-1 data parallelism, DESIGN R31) replica k runs
+micro-batches [k*M, (k+1)*M) of a DP*M-micro-batch step.
 """
 
 import os
@@ -28,17 +31,23 @@ def main(argv):
     offload = int(argv[15]) if len(argv) > 15 else 0
     timeout_ms = int(argv[16]) if len(argv) > 16 else 120000
     seed = int(argv[17]) if len(argv) > 17 else 11
+    dp = int(argv[18]) if len(argv) > 18 else 1
+    dp_rank = int(argv[19]) if len(argv) > 19 else 0
     import synth
     from paper_2503_03182_b200 import params as PR, plan as P, runtime as RT
 
-    plan = P.Plan(P.Model(L, h, a, f, V, s, b, dtype), p, m, strategy=strategy, offload=offload)
+    plan = P.Plan(P.Model(L, h, a, f, V, s, b, dtype), p, m, strategy=strategy, offload=offload, dp=dp)
     rt = RT.Runtime(plan, stage=stage, device=0, lr=1e-3, transport=RT.TRANSPORT_IPC,
-                    ipc_name=ipc, timeout_ms=timeout_ms)
+                    ipc_name=ipc, timeout_ms=timeout_ms, dp_rank=dp_rank)
+
+    def batch(step):
+        tok, tgt = synth.tokens(V, dp * m, b, s, step=step)
+        return tok[dp_rank * m:(dp_rank + 1) * m], tgt[dp_rank * m:(dp_rank + 1) * m]
     W = synth.weights(L, h, f, V, s, seed=seed, std=0.05, bias_std=0.02, ln_jitter=0.05)
     for c in range(1, plan.v + 1):
         rt.set_params(stage, c, PR.pack(W, p, plan.v, plan.partition, stage, c))
     res = {}
-    tok, tgt = synth.tokens(V, m, b, s, step=0)
+    tok, tgt = batch(0)
     res["loss0"] = np.float64(rt.step(tok, tgt, RT.STEP_NO_OPT))
     for c in range(1, plan.v + 1):
         res[f"grad{c}"] = rt.get_grads(stage, c)
@@ -52,7 +61,7 @@ def main(argv):
         rt.set_params(stage, c, PR.pack(W, p, plan.v, plan.partition, stage, c))
     losses = []
     for k in range(steps):
-        tok, tgt = synth.tokens(V, m, b, s, step=k)
+        tok, tgt = batch(k)
         losses.append(rt.step(tok, tgt, 0))
     res["losses"] = np.array(losses, np.float64)
     for c in range(1, plan.v + 1):

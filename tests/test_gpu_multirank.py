@@ -32,16 +32,20 @@ C1_16 = dict(C1, L=16)     # C1 width, 16 layers: p = 8 with two chunks of one l
 
 
 def run_job(tmp_path, cfg, p, m, strategy, dtype, steps=1, offload=0, timeout_ms=120000,
-            stages=None, wall=600):
+            stages=None, wall=600, dp=1, tag=""):
+    """Launch one process per (replica, stage); results keyed by stage (dp = 1)
+    or by (replica, stage)."""
     name = f"/tpipe_t_{os.getpid()}_{uuid.uuid4().hex[:12]}"
     procs = []
-    for s in (range(p) if stages is None else stages):
-        out = str(tmp_path / f"stage{s}.npz")
-        args = [sys.executable, WORKER, out, str(s), str(p), str(m), strategy, str(dtype), name,
-                *(str(cfg[k]) for k in ("L", "h", "a", "f", "V", "s", "b")), str(steps),
-                str(offload), str(timeout_ms)]
-        procs.append((s, out, subprocess.Popen(args, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
-                                               cwd=ROOT)))
+    for k in range(dp):
+        for s in (range(p) if stages is None else stages):
+            key = s if dp == 1 else (k, s)
+            out = str(tmp_path / f"{tag}r{k}_stage{s}.npz")
+            args = [sys.executable, WORKER, out, str(s), str(p), str(m), strategy, str(dtype), name,
+                    *(str(cfg[kk]) for kk in ("L", "h", "a", "f", "V", "s", "b")), str(steps),
+                    str(offload), str(timeout_ms), "11", str(dp), str(k)]
+            procs.append((key, out, subprocess.Popen(args, stdout=subprocess.PIPE,
+                                                     stderr=subprocess.STDOUT, cwd=ROOT)))
     res, logs = {}, {}
     for s, out, pr in procs:
         try:
@@ -166,3 +170,78 @@ def test_multiprocess_missing_peer_times_out(tmp_path):
     rc, out = logs[0]
     assert rc != 0
     assert "timed out" in out and "rc=-11" in out
+
+
+def _assemble(res, p, dp, plan, key):
+    """Per stage and chunk, the replicas' arrays in replica order."""
+    return {(s, c): [res[(k, s)][f"{key}{c}"] for k in range(dp)]
+            for s in range(p) for c in range(1, plan.v + 1)}
+
+
+@pytest.mark.parametrize("p,dp,strategy", [(1, 2, "tpipe"), (2, 2, "tpipe_trecomp"), (2, 4, "tpipe"),
+                                           (4, 2, "1f1b")])
+def test_dp_pp_zero1_fp32(tmp_path, p, dp, strategy):
+    """DP x PP with ZeRO-1 (NEXT-3; DESIGN R31), dp*p processes on one GPU:
+    * the replicas' summed gradients equal the oracle's full-batch gradients over
+      all dp*m micro-batches (max-rel <= 1e-4), the summed loss its loss;
+    * after two optimizer steps every replica holds the same weights, and they
+      match the single-replica virtual pipeline run on the dp*m micro-batches
+      (same AdamW; only the fp32 gradient summation order differs);
+    * each rank's pool high-water equals its plan peak (optimizer states of one
+      shard)."""
+    from paper_2503_03182_b200 import params as PR
+    cfg, m = C1, 4
+    res, logs = run_job(tmp_path, cfg, p, m, strategy, 0, steps=2, dp=dp)
+    assert_ok(res, logs)
+    plan = _plan(cfg, p, m, strategy, 0)
+    W = synth.weights(cfg["L"], cfg["h"], cfg["f"], cfg["V"], cfg["s"], seed=11, std=0.05,
+                      bias_std=0.02, ln_jitter=0.05)
+    tok, tgt = synth.tokens(cfg["V"], dp * m, cfg["b"], cfg["s"], step=0)
+    lref, G = R.step_grads(R.to64(W), tok, tgt, cfg["a"])
+    loss = sum(float(res[(k, p - 1)]["loss0"]) for k in range(dp))
+    assert abs(loss - lref) / abs(lref) < 1e-5
+    grads = _assemble(res, p, dp, plan, "grad")
+    for (s, c), gs in grads.items():
+        got = PR.unpack(np.sum(gs, axis=0), W, p, plan.v, plan.partition, s, c)
+        for (k, l), g in got.items():
+            ref = G["layers"][l][k] if l is not None else G[k]
+            assert max_rel(g, ref) <= 1e-4, (s, c, k, l)
+    for k in range(dp):
+        for s in range(p):
+            assert int(res[(k, s)]["high_water"]) == int(res[(k, s)]["plan_peak"])
+    # reference: one replica over all dp*m micro-batches (virtual pipeline)
+    _l0, _g, _losses, vparams = _virtual(cfg, p, dp * m, strategy, 0, 2)
+    params = _assemble(res, p, dp, plan, "param")
+    for (s, c), ps in params.items():
+        for k in range(1, dp):
+            assert np.array_equal(ps[0], ps[k]), (s, c, k)       # all-gather: identical replicas
+        ref = vparams[(s, c)]
+        bad = np.abs(ps[0] - ref) > 1e-6 + 1e-5 * np.abs(ref)
+        assert bad.mean() < 1e-3, (s, c, int(bad.sum()))
+
+
+def test_dp_pp_zero1_bf16_deterministic(tmp_path):
+    """bf16, p = 2 x dp = 2: two identical jobs give bit-identical losses and
+    parameters, replicas agree bit for bit, and the bf16 weights are the RNE
+    of the owning replica's fp32 master."""
+    cfg, p, dp, m = C1, 2, 2, 4
+    runs = []
+    for t in ("a", "b"):
+        res, logs = run_job(tmp_path, cfg, p, m, "tpipe", 1, steps=2, dp=dp, tag=t)
+        assert_ok(res, logs)
+        runs.append(res)
+    plan = _plan(cfg, p, m, "tpipe", 1)
+    for key in ("param", "grad"):
+        A = _assemble(runs[0], p, dp, plan, key)
+        B = _assemble(runs[1], p, dp, plan, key)
+        for sc in A:
+            for x, y in zip(A[sc], B[sc]):
+                assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), (key, sc)
+    for k in range(dp):
+        assert list(runs[0][(k, p - 1)]["losses"]) == list(runs[1][(k, p - 1)]["losses"])
+    # replicas agree on the bf16 weights (upper 16 bits) everywhere
+    P_ = _assemble(runs[0], p, dp, plan, "param")
+    for sc, ps in P_.items():
+        hi = [(x.view(np.uint32) + 0x7FFF + ((x.view(np.uint32) >> 16) & 1)) >> 16 for x in ps]
+        for k in range(1, dp):
+            assert np.array_equal(hi[0], hi[k]), sc

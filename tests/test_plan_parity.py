@@ -410,3 +410,42 @@ def test_partition_chunk_split_streams_match_oracle(p, part, chunk1, strategy):
     with pytest.raises(TPipeError, match="stage_chunk1"):
         P.Plan(pd, p, m, strategy=strategy, stage_layers=part,
                stage_chunk1=[part[0]] + list(chunk1[1:]))
+
+
+@pytest.mark.parametrize("strategy", ["tpipe", "tpipe_trecomp", "1f1b", "1f1b_full_recomp",
+                                      "interleave_trecomp"])
+@pytest.mark.parametrize("p,dp", [(1, 2), (2, 2), (4, 2), (2, 4), (1, 8)])
+@pytest.mark.parametrize("dtype", [T.BF16, T.FP32])
+def test_dp_zero1_streams_match_oracle(strategy, p, dp, dtype):
+    """DP x PP with ZeRO-1 (NEXT-3, R31): DP_WAIT before each chunk's first
+    forward, DP_OPT instead of OPT, model-state bytes with the optimizer
+    states of one shard; streams and peaks equal the oracle's."""
+    P = _plan_mod()
+    L = 2 * p if p > 2 else 4
+    m = 2 * p
+    od = T.ModelDesc(L, 64, 4, 256, 128, 32, 2, dtype)
+    pd = P.Model(L, 64, 4, 256, 128, 32, 2, dtype)
+    plan = P.Plan(pd, p, m, strategy=strategy, dp=dp)
+    assert plan.dp == dp
+    st, static = T.build_streams(od, p, m, strategy, dp=dp)
+    for s in range(p):
+        got, bufs = plan.ops(s)
+        strip = [{k: o[k] for k in ("kind", "chunk", "mb", "peer", "channel", "msg")} for o in got]
+        assert strip == oracle_ops(st[s])
+        kinds = [o["kind"] for o in got]
+        assert "OPT" not in kinds and kinds.count("DP_OPT") == plan.v and kinds.count("DP_WAIT") == plan.v
+        rep = T.replay(st[s], static[s])
+        pk = plan.peak(s)
+        for cat in ("model_state", "io", "act", "recomp_buf", "comm", "workspace"):
+            assert pk[cat] == rep.get(cat, 0), cat
+    # ZeRO-1 saves (1 - 1/dp) of the optimizer-state bytes (12 B/param bf16, 8 fp32)
+    one = P.Plan(pd, p, m, strategy=strategy)
+    for s in range(p):
+        saved = one.peak(s)["model_state"] - plan.peak(s)["model_state"]
+        per = 12 if dtype == T.BF16 else 8
+        n = sum(one.chunk_params(s, c) for c in range(1, one.v + 1))
+        assert saved >= per * n * (1 - 1 / dp) - per * 64 * one.v
+    from paper_2503_03182_b200._lib import TPipeError
+    if strategy.startswith("tpipe"):
+        with pytest.raises(TPipeError, match="ZeRO-1"):
+            P.Plan(pd, p, m, strategy=strategy, dp=dp, offload=P.OFFLOAD_MODEL_STATE)
