@@ -101,7 +101,8 @@ typedef struct {
                               kinds limited by `offload` when it is not -1; DEVICE_OPT if
                               requested there) */
     int32_t delay_rounds;  /* T-Recomp k; -1 = App. B constraint as printed */
-    int32_t send_window;   /* W, max in-flight sends per channel; 0 = default 2 (DESIGN R12) */
+    int32_t send_window;   /* W, max in-flight sends per channel; 0 = default max(2, chunks)
+                              (DESIGN R12, R32); the IPC transport supports W <= 4 */
     int32_t offload;       /* TPIPE_OFFLOAD_* bitmask (explicit strategies); -1 = auto */
     int32_t act_distance;  /* activation offload: release / prefetch distance in compute
                               ops; 0 = derived: the smallest d whose d chunk-1 forward
@@ -149,6 +150,12 @@ typedef struct {
                               optimizer states are sharded ZeRO-1 (master / m / v of
                               ceil64(P / dp) parameters per replica) and updated by
                               TPIPE_OP_DP_OPT. Incompatible with model-state offload */
+    int32_t chunks;        /* v, chunks per stage of the T-Pipe and Interleave strategies
+                              (DESIGN R32): 0 = 2, or 3, 4.
+                              Per stage n / v layers per chunk, the extra ones to the
+                              shallowest chunks; T-Pipe uses the period-3v slot table (D-11);
+                              T-Recomp regenerates chunk 1; model-state T-Offload moves chunks
+                              2..v. layers_chunk, stage_chunk1 and balance need v = 2 */
 } tpipe_plan_opts;
 
 enum {
@@ -253,6 +260,8 @@ int tpipe_plan_simulate_durations(const tpipe_plan* plan, const float* const* op
                                   tpipe_sim_report_ms* out);
 /* layers of (stage, chunk 1) and (stage, chunk 2) (chunk 2 = 0 at v = 1) */
 int tpipe_plan_stage_layers(const tpipe_plan* plan, int32_t stage, int32_t out[2]);
+/* transformer layers of (stage, chunk), chunk 1..v */
+int tpipe_plan_chunk_layers(const tpipe_plan* plan, int32_t stage, int32_t chunk, int32_t* n);
 /* parameters of (stage, chunk) in the packed order of DESIGN.md §2.3 */
 int tpipe_plan_chunk_params(const tpipe_plan* plan, int32_t stage, int32_t chunk, uint64_t* n);
 

@@ -76,23 +76,57 @@ def delay_rounds(p: int) -> int:
 # Per-stage orders
 # --------------------------------------------------------------------------
 
-def tpipe_slots(p: int, m: int) -> dict:
-    """D-1 slot table; keys (stage, kind, chunk, mb)."""
-    a, b = tpipe_ab(p)
+def tpipe_slots(p: int, m: int, v: int = 2) -> dict:
+    """D-1 slot table; keys (stage, kind, chunk, mb).
+
+    v > 2 (D-11's generalisation, DESIGN R32): the slot period
+    per micro-batch is 3v units;
+      F(s,1,i)   = 3v(i-1) + s
+      F(0,c+1,i) = the first t >= F(0,c,i) + p with t = 3c (mod 3v)
+      B(0,v,i)   = F(0,v,i) + 3p - 2          (= F(p-1,v,i) + 1 + 2(p-1))
+      B(0,c-1,i) = the first t >= B(0,c,i) + 2p with t = B(0,c,i) + 3 (mod 3v)
+      F(s,c,i)   = F(0,c,i) + s,   B(s,c,i) = B(0,c,i) - 2s.
+    At v = 2 this is exactly D-1 (a = ceil((p-3)/6), b = ceil((2p-3)/6))."""
+    if v == 2:
+        a, b = tpipe_ab(p)
+        t = {}
+        for i in range(1, m + 1):
+            for s in range(p):
+                t[(s, "F", 1, i)] = 6 * (i - 1) + s
+                t[(s, "F", 2, i)] = 6 * (i - 1) + 3 + 6 * a + s
+            for s in range(p):
+                t[(s, "B", 2, i)] = t[(p - 1, "F", 2, i)] + 1 + 2 * (p - 1 - s)
+            for s in range(p):
+                t[(s, "B", 1, i)] = t[(0, "B", 2, i)] + 3 + 6 * b - 2 * s
+        return t
+    return tpipe_slots_general(p, m, v)
+
+
+def tpipe_slots_general(p: int, m: int, v: int) -> dict:
+    """The period-3v slot table of tpipe_slots for any v >= 1 (written from
+    the recurrences, not from D-1's closed form; equal to it at v = 2)."""
+    per = 3 * v
+
+    def first_at_least(lo, residue):
+        return lo + ((residue - lo) % per)
+
     t = {}
     for i in range(1, m + 1):
+        f0 = {1: per * (i - 1)}
+        for ch in range(1, v):
+            f0[ch + 1] = first_at_least(f0[ch] + p, 3 * ch)
+        b0 = {v: f0[v] + 3 * p - 2}
+        for ch in range(v, 1, -1):
+            b0[ch - 1] = first_at_least(b0[ch] + 2 * p, b0[ch] + 3)
         for s in range(p):
-            t[(s, "F", 1, i)] = 6 * (i - 1) + s
-            t[(s, "F", 2, i)] = 6 * (i - 1) + 3 + 6 * a + s
-        for s in range(p):
-            t[(s, "B", 2, i)] = t[(p - 1, "F", 2, i)] + 1 + 2 * (p - 1 - s)
-        for s in range(p):
-            t[(s, "B", 1, i)] = t[(0, "B", 2, i)] + 3 + 6 * b - 2 * s
+            for ch in range(1, v + 1):
+                t[(s, "F", ch, i)] = f0[ch] + s
+                t[(s, "B", ch, i)] = b0[ch] - 2 * s
     return t
 
 
 def tpipe_orders(p: int, m: int, recomp: bool = False, k: int | None = None,
-                 layer_grouped: bool = False):
+                 layer_grouped: bool = False, v: int = 2):
     """T-Pipe per-stage compute order (v=2).
 
     recomp=True: block-wise T-Recomp (R before each B1, chunk-1 forwards run k
@@ -100,9 +134,10 @@ def tpipe_orders(p: int, m: int, recomp: bool = False, k: int | None = None,
     layer_grouped=True: the negative design (recompute fused into B1, no R op,
     no delay) for P:345's dependency conflict.
     """
-    slots = tpipe_slots(p, m)
+    slots = tpipe_slots(p, m, v)
     if recomp and k is None:
-        k = delay_rounds(p)
+        # App. B's delay analysis is for two chunks; v > 2 runs undelayed (R32)
+        k = delay_rounds(p) if v == 2 else 0
     if not recomp:
         k = 0
     orders = []
@@ -429,12 +464,13 @@ def idle_between(sim, s, t0, t1):
     return (t1 - t0) - busy
 
 
-def strategy_orders(strategy: str, p: int, m: int, k: int | None = None):
-    """Convenience: (orders, v, recomputed, durations) for a named strategy."""
+def strategy_orders(strategy: str, p: int, m: int, k: int | None = None, v: int = 2):
+    """Convenience: (orders, v, recomputed, durations) for a named strategy;
+    v = chunks per stage for the T-Pipe and Interleave strategies."""
     if strategy == "tpipe":
-        return tpipe_orders(p, m), 2, False, default_durations(2)
+        return tpipe_orders(p, m, v=v), v, False, default_durations(2)
     if strategy == "tpipe_trecomp":
-        return tpipe_orders(p, m, recomp=True, k=k), 2, True, default_durations(2)
+        return tpipe_orders(p, m, recomp=True, k=k, v=v), v, True, default_durations(2)
     if strategy == "tpipe_layer_grouped":
         return (tpipe_orders(p, m, layer_grouped=True), 2, False,
                 default_durations(2, layer_grouped_b1=True))
@@ -445,7 +481,7 @@ def strategy_orders(strategy: str, p: int, m: int, k: int | None = None):
     if strategy == "1f1b_full_recomp":
         return onef1b_orders(p, m), 1, False, default_durations(1, b_extra=2)
     if strategy == "interleave":
-        return interleave_orders(p, m, 2), 2, False, default_durations(2)
+        return interleave_orders(p, m, v), v, False, default_durations(2)
     if strategy == "interleave_trecomp":
-        return interleave_trecomp_orders(p, m, 2), 2, True, default_durations(2)
+        return interleave_trecomp_orders(p, m, v), v, True, default_durations(2)
     raise ValueError(strategy)

@@ -50,6 +50,11 @@ def layers_per_chunk(d: ModelDesc, p: int, v: int, s: int = 0):
     """n = L/p layers per stage (p | L required). v=2: the extra layer of an odd
     n goes to chunk 1. Override via d.layers_chunk. With
     d.stage_layers (DESIGN R27) stage s holds n(s) layers, split the same way."""
+    def split(n):
+        # v chunks: n // v each, the extra layers to the shallowest chunks
+        # (SURVEY Q14's "extra layer to chunk 1", generalised; DESIGN R32)
+        return tuple(n // v + (1 if c < n % v else 0) for c in range(v))
+
     if d.stage_layers:
         if len(d.stage_layers) != p or sum(d.stage_layers) != d.n_layers:
             raise ValueError("stage_layers")
@@ -58,6 +63,8 @@ def layers_per_chunk(d: ModelDesc, p: int, v: int, s: int = 0):
             raise ValueError("stage_layers")
         if v == 1:
             return (n,)
+        if v > 2:
+            return split(n)
         n1 = d.stage_chunk1[s] if d.stage_chunk1 and d.stage_chunk1[s] else (n + 1) // 2
         if not 1 <= n1 <= n - 1:
             raise ValueError("stage_chunk1")
@@ -67,13 +74,13 @@ def layers_per_chunk(d: ModelDesc, p: int, v: int, s: int = 0):
     n = d.n_layers // p
     if v == 1:
         return (n,)
-    if d.layers_chunk[0] or d.layers_chunk[1]:
+    if v == 2 and (d.layers_chunk[0] or d.layers_chunk[1]):
         if sum(d.layers_chunk) != n or min(d.layers_chunk) < 1:
             raise ValueError("layers_chunk")
         return tuple(d.layers_chunk)
-    if n < 2:
+    if n < v:
         raise ValueError("n_layers")
-    return ((n + 1) // 2, n // 2)
+    return split(n)
 
 
 def layer_params(d: ModelDesc) -> int:
@@ -236,22 +243,32 @@ def act_offload_sets(order, d_release: int, d_prefetch: int):
 
 
 def build_streams(d: ModelDesc, p: int, m: int, strategy: str, k=None,
-                  window: int = 2, offload_model_state: bool = False,
+                  window: int | None = None, offload_model_state: bool = False,
                   offload_activations: bool = False, act_distance: int = 2,
-                  offload_device_opt: bool = False, recomp_layers: int = 0, dp: int = 1):
+                  offload_device_opt: bool = False, recomp_layers: int = 0, dp: int = 1,
+                  chunks: int = 2):
     """Per-stage instruction streams. Returns (streams, static)
     where static[s] = list of (name, category, bytes) live for the whole step.
     ``recomp_layers`` = r of partial T-Recomp (0 = all chunk-1 layers)."""
     ostrat, v, trecomp, full = STRATS[strategy]
-    if offload_model_state and v != 2:
-        raise ValueError("offload requires v=2")
+    if v == 2:
+        v = chunks          # T-Pipe / Interleave with v chunks per stage (NEXT-4, R32)
+    elif chunks != 2:
+        raise ValueError("chunks applies to the T-Pipe and Interleave strategies")
+    if window is None:
+        # send window (R12, D-14): 2; v chunks put v - 1 chunk turnarounds on the
+        # wrap channel, and W = v is the smallest deadlock-free window at v = 4
+        # (R32, tests/test_multichunk.py)
+        window = max(2, v)
+    if offload_model_state and v < 2:
+        raise ValueError("offload requires T-Pipe chunks (v >= 2)")
     if offload_device_opt and not offload_model_state:
         raise ValueError("device optimizer streaming applies to model-state offload")
     if dp > 1 and offload_model_state:
         raise ValueError("ZeRO-1 data parallelism shards the device optimizer (no model-state offload)")
     if offload_activations and (v != 2 or trecomp):
         raise ValueError("activation offload applies to T-Pipe chunk 1 (no T-Recomp)")
-    orders = S.strategy_orders(ostrat, p, m, k=k)[0]
+    orders = S.strategy_orders(ostrat, p, m, k=k, v=v)[0]
     sz = {(s, c): sizes(d, p, v, s, c, full_recomp=full)
           for s in range(p) for c in range(1, v + 1)}
     keep1, rec1 = {}, {}
@@ -269,7 +286,7 @@ def build_streams(d: ModelDesc, p: int, m: int, strategy: str, k=None,
         st = []
         for c in range(1, v + 1):
             P = chunk_params(d, p, v, s, c)
-            off = offload_model_state and c == v
+            off = offload_model_state and c >= 2        # chunks 2..v (R32)
             extra = sopt_staging_bytes(P) if (off and offload_device_opt) else 0
             st.append((f"MS{c}", "model_state", model_state_bytes(d, P, off, dp) + extra))
         if s == 0:
@@ -313,8 +330,8 @@ def build_streams(d: ModelDesc, p: int, m: int, strategy: str, k=None,
                                      frees=[_msgbuf(ch, jj)]))
                     waited[ch] += 1
             # 2. receive before the consuming op
-            if offload_model_state and kind == "F" and c == v and i == first_f[v]:
-                out.append(Instr("W_WAIT", chunk=v))
+            if offload_model_state and kind == "F" and c >= 2 and i == first_f[c]:
+                out.append(Instr("W_WAIT", chunk=c))
             if dp > 1 and kind == "F" and i == first_f[c]:
                 # the replicas' previous-step ZeRO-1 update of this chunk is complete
                 out.append(Instr("DP_WAIT", chunk=c))
@@ -381,9 +398,9 @@ def build_streams(d: ModelDesc, p: int, m: int, strategy: str, k=None,
                 out.append(Instr("ACT_D2H", 1, i))
             # 5. optimizer / offload after the chunk's last backward
             if kind == "B" and i == last_b[c]:
-                if offload_model_state and c == v and offload_device_opt:
+                if offload_model_state and c >= 2 and offload_device_opt:
                     out.append(Instr("STREAM_OPT", chunk=c))
-                elif offload_model_state and c == v:
+                elif offload_model_state and c >= 2:
                     out.append(Instr("GRAD_D2H", chunk=c))
                     out.append(Instr("HOST_OPT", chunk=c))
                 elif dp > 1:
@@ -392,7 +409,8 @@ def build_streams(d: ModelDesc, p: int, m: int, strategy: str, k=None,
                     out.append(Instr("OPT", chunk=c))
             # weight upload right after the stage's first forward
             if offload_model_state and not offload_device_opt and not first_op_done and kind == "F":
-                out.append(Instr("W_H2D", chunk=v))
+                for cc in range(2, v + 1):
+                    out.append(Instr("W_H2D", chunk=cc))
             first_op_done = first_op_done or kind == "F"
         # 6. flush outstanding sends (channels sorted, then message order)
         for ch in sorted(sent):

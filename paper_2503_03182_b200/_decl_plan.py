@@ -16,7 +16,7 @@ class PlanOpts(C.Structure):
                 ("act_distance", i32), ("recomp_layers", i32), ("stage_layers", i32 * 64),
                 ("host_link_bps", C.c_double), ("host_adam_params_per_s", C.c_double),
                 ("device_flops", C.c_double), ("balance", i32), ("stage_chunk1", i32 * 64),
-                ("dp", i32)]
+                ("dp", i32), ("chunks", i32)]
 
 
 class Op(C.Structure):
@@ -83,6 +83,7 @@ def declare(L):
     L.tpipe_plan_simulate_durations.argtypes = [vp, P(P(f32)), P(SimReportMs)]
     L.tpipe_plan_chunk_params.argtypes = [vp, i32, i32, P(u64)]
     L.tpipe_plan_stage_layers.argtypes = [vp, i32, P(i32)]
+    L.tpipe_plan_chunk_layers.argtypes = [vp, i32, i32, P(i32)]
     L.tpipe_version.argtypes = []
     if hasattr(L, "tpipe_runtime_create"):
         L.tpipe_runtime_create.argtypes = [vp, P(RuntimeOpts), P(vp)]

@@ -51,7 +51,7 @@ uint64_t layer_params(const tpipe_model_desc& d) {
     return 2 * h + (3 * h * h + 3 * h) + (h * h + h) + 2 * h + (f * h + f) + (h * f + h);
 }
 
-uint64_t chunk_params(const tpipe_model_desc& d, int p, int v, const int layers[2], int s, int c) {
+uint64_t chunk_params(const tpipe_model_desc& d, int p, int v, const int* layers, int s, int c) {
     uint64_t P = (uint64_t)layers[c - 1] * layer_params(d);
     if (s == 0 && c == 1) P += (uint64_t)d.vocab * d.hidden + (uint64_t)d.seq_len * d.hidden;
     if (s == p - 1 && c == v) P += 2ull * d.hidden + (uint64_t)d.vocab * d.hidden;
@@ -70,7 +70,7 @@ static uint64_t layer_stash_bytes(const tpipe_model_desc& d) {
     return M * h * es + 8 * M + 3 * M * h * es + M * h * es + 4 * a * M + M * h * es + 8 * M + M * f * es;
 }
 
-static ChunkSizes chunk_sizes(const tpipe_model_desc& d, int p, int v, const int layers[2], int s,
+static ChunkSizes chunk_sizes(const tpipe_model_desc& d, int p, int v, const int* layers, int s,
                               int c, bool full_recomp) {
     const uint64_t M = (uint64_t)d.micro_batch * d.seq_len, h = d.hidden, a = d.n_heads,
                    f = d.ffn_hidden, V = d.vocab, es = d.dtype == TPIPE_BF16 ? 2 : 4;
@@ -107,22 +107,28 @@ static ChunkSizes chunk_sizes(const tpipe_model_desc& d, int p, int v, const int
 using COp = std::array<int, 3>;  // {kind, chunk, mb}; kind: 0 F, 1 B, 2 R
 enum { KF = 0, KB = 1, KR = 2 };
 
-static std::vector<std::vector<COp>> tpipe_order(int p, int m, bool recomp, int k) {
-    const int a = cdiv(p - 3, 6), b = cdiv(2 * p - 3, 6);
+// T-Pipe slot order (D-1; v > 2: D-11's generalisation with period 3v,
+// DESIGN R32): F(s,1,i) = 3v(i-1) + s; F(0,c+1,i) = first t >= F(0,c,i) + p
+// with t = 3c mod 3v; B(0,v,i) = F(0,v,i) + 3p - 2; B(0,c-1,i) = first
+// t >= B(0,c,i) + 2p with t = B(0,c,i) + 3 mod 3v; F(s,c,i) = F(0,c,i) + s,
+// B(s,c,i) = B(0,c,i) - 2s. At v = 2 this is the App. A table
+// (a = ceil((p-3)/6), b = ceil((2p-3)/6)).
+static std::vector<std::vector<COp>> tpipe_order(int p, int m, bool recomp, int k, int v = 2) {
+    const long per = 3L * v;
+    auto first_at_least = [&](long lo, long residue) { return lo + (((residue - lo) % per) + per) % per; };
     std::vector<std::vector<COp>> out(p);
     for (int s = 0; s < p; ++s) {
         std::vector<std::pair<long, COp>> slots;
         for (int i = 1; i <= m; ++i) {
-            const long f1 = 6L * (i - 1) + s;
-            const long f2 = 6L * (i - 1) + 3 + 6L * a + s;
-            const long f2last = 6L * (i - 1) + 3 + 6L * a + (p - 1);
-            const long b2 = f2last + 1 + 2L * (p - 1 - s);
-            const long b2first = f2last + 1 + 2L * (p - 1);
-            const long b1 = b2first + 3 + 6L * b - 2L * s;
-            slots.push_back({f1, {KF, 1, i}});
-            slots.push_back({f2, {KF, 2, i}});
-            slots.push_back({b2, {KB, 2, i}});
-            slots.push_back({b1, {KB, 1, i}});
+            long f0[5], b0[5];
+            f0[1] = per * (i - 1);
+            for (int c = 1; c < v; ++c) f0[c + 1] = first_at_least(f0[c] + p, 3L * c);
+            b0[v] = f0[v] + 3L * p - 2;
+            for (int c = v; c > 1; --c) b0[c - 1] = first_at_least(b0[c] + 2L * p, b0[c] + 3);
+            for (int c = 1; c <= v; ++c) {
+                slots.push_back({f0[c] + s, {KF, c, i}});
+                slots.push_back({b0[c] - 2L * s, {KB, c, i}});
+            }
         }
         std::sort(slots.begin(), slots.end(),
                   [](const auto& x, const auto& y) { return x.first < y.first; });
@@ -161,13 +167,13 @@ static std::vector<std::vector<COp>> tpipe_order(int p, int m, bool recomp, int 
 // 2 - (q mod 2p)/p of the same micro-batch. Stage s warms up with
 // min(2(p-s-1) + p, 2m) forwards, then alternates one forward / one backward,
 // then drains. recomp: R(s,1,i) right before each B(s,1,i) (R26).
-static std::vector<std::vector<COp>> interleave_order(int p, int m, bool recomp) {
-    const int total = 2 * m;
-    auto fwd = [&](int q) -> COp { return {KF, (q % (2 * p)) / p + 1, (q / (2 * p)) * p + q % p + 1}; };
-    auto bwd = [&](int q) -> COp { return {KB, 2 - (q % (2 * p)) / p, (q / (2 * p)) * p + q % p + 1}; };
+static std::vector<std::vector<COp>> interleave_order(int p, int m, bool recomp, int v = 2) {
+    const int total = v * m;
+    auto fwd = [&](int q) -> COp { return {KF, (q % (v * p)) / p + 1, (q / (v * p)) * p + q % p + 1}; };
+    auto bwd = [&](int q) -> COp { return {KB, v - (q % (v * p)) / p, (q / (v * p)) * p + q % p + 1}; };
     std::vector<std::vector<COp>> out(p);
     for (int s = 0; s < p; ++s) {
-        const int w = std::min(2 * (p - s - 1) + p, total);
+        const int w = std::min(2 * (p - s - 1) + (v - 1) * p, total);
         std::vector<COp> lst;
         auto push_b = [&](int q) {
             const COp b = bwd(q);
@@ -288,7 +294,7 @@ static int build(tpipe_plan* P, bool trecomp, bool full_recomp) {
     P->bufs.assign(p, {});
     P->events.assign(p, {});
     P->peak.assign(p, {});
-    P->chunk_params.assign(p, {0, 0});
+    P->chunk_params.assign(p, std::array<uint64_t, 4>{});
 
     // channel table sorted by (kind, src, dst)
     std::map<std::tuple<int, int, int>, int> chan_id;
@@ -317,7 +323,7 @@ static int build(tpipe_plan* P, bool trecomp, bool full_recomp) {
             const uint64_t np = chunk_params(d, p, v, P->sl[s].data(), s, c);
             P->chunk_params[s][c - 1] = np;
             P->params_total += np;
-            const bool o = off && c == v;
+            const bool o = off && c >= 2;   // T-Offload of chunks 2..v (R32)
             const uint64_t opt_b = (d.dtype == TPIPE_BF16 ? 4 : 0) + 8;   // master (bf16 mode) + m, v
             // ZeRO-1 (R31): master / m / v cover one shard of the chunk
             const uint64_t ms = o ? np * (es + 4)
@@ -329,7 +335,7 @@ static int build(tpipe_plan* P, bool trecomp, bool full_recomp) {
         if (s == 0) B.bufs.push_back({TPIPE_BUF_STATIC, TPIPE_CAT_IO, 0, 0, 4ull * m * M});
         if (s == p - 1) B.bufs.push_back({TPIPE_BUF_STATIC, TPIPE_CAT_IO, 0, 1, 4ull * m * M + 4ull * m});
 
-        ChunkSizes z[3];
+        ChunkSizes z[5];
         for (int c = 1; c <= v; ++c) z[c] = chunk_sizes(d, p, v, P->sl[s].data(), s, c, full_recomp);
         // partial T-Recomp (R25): layers 1..r of chunk 1 are regenerated by R (TSTASH during
         // F, RBUF from R to B); the stash of layers r+1..n1 is kept from F to B (STASH).
@@ -342,7 +348,7 @@ static int build(tpipe_plan* P, bool trecomp, bool full_recomp) {
 
         const auto& order = P->order[s];
         std::map<int, int> sent, waited;  // channel -> count
-        int last_b[3] = {0, 0, 0}, first_f[3] = {1 << 30, 1 << 30, 1 << 30};
+        int last_b[5] = {0, 0, 0, 0, 0}, first_f[5] = {1 << 30, 1 << 30, 1 << 30, 1 << 30, 1 << 30};
         for (auto& op : order) {
             if (op[0] == KB) last_b[op[1]] = std::max(last_b[op[1]], op[2]);
             if (op[0] == KF) first_f[op[1]] = std::min(first_f[op[1]], op[2]);
@@ -400,7 +406,7 @@ static int build(tpipe_plan* P, bool trecomp, bool full_recomp) {
                 }
             }
             // 2. weight-upload wait and receives
-            if (off && kind == KF && c == v && i == first_f[v]) B.emit(TPIPE_OP_W_WAIT, v, 0, -1, -1, -1, {});
+            if (off && kind == KF && c >= 2 && i == first_f[c]) B.emit(TPIPE_OP_W_WAIT, c, 0, -1, -1, -1, {});
             if (P->dp > 1 && kind == KF && i == first_f[c]) B.emit(TPIPE_OP_DP_WAIT, c, 0, -1, -1, -1, {});
             if (kind == KF && zz.input_is_act) {
                 const int src = src_stage(s, c, p, v, KF);
@@ -470,9 +476,9 @@ static int build(tpipe_plan* P, bool trecomp, bool full_recomp) {
             if (kind == KF && c == 1 && aoff.count(i)) B.emit(TPIPE_OP_ACT_D2H, 1, i, -1, -1, -1, {});
             // 5. optimizer after the chunk's last backward
             if (kind == KB && i == last_b[c]) {
-                if (off && c == v && sopt) {
+                if (off && c >= 2 && sopt) {
                     B.emit(TPIPE_OP_STREAM_OPT, c, 0, -1, -1, -1, {});
-                } else if (off && c == v) {
+                } else if (off && c >= 2) {
                     B.emit(TPIPE_OP_GRAD_D2H, c, 0, -1, -1, -1, {});
                     B.emit(TPIPE_OP_HOST_OPT, c, 0, -1, -1, -1, {});
                 } else {
@@ -480,7 +486,8 @@ static int build(tpipe_plan* P, bool trecomp, bool full_recomp) {
                 }
             }
             // 6. weight upload after the first forward
-            if (off && !sopt && !first_f_done && kind == KF) B.emit(TPIPE_OP_W_H2D, v, 0, -1, -1, -1, {});
+            if (off && !sopt && !first_f_done && kind == KF)
+                for (int cc = 2; cc <= v; ++cc) B.emit(TPIPE_OP_W_H2D, cc, 0, -1, -1, -1, {});
             first_f_done = first_f_done || kind == KF;
         }
         // flush outstanding sends, channels in id order (= sorted (kind, src, dst))
@@ -704,12 +711,14 @@ static double estimate(const tpipe_plan* P, const CostModel& cm, double* exposed
     const double es = d.dtype == TPIPE_BF16 ? 2.0 : 4.0;
     for (int s = 0; s < P->p; ++s) {
         double exposed = 0;
-        if (P->offload & TPIPE_OFFLOAD_MODEL_STATE) {
-            const double np = (double)P->chunk_params[s][P->v - 1];
+        // offloaded chunks 2..v (R32): each chunk's transfer against its own
+        // window; the chunks share one link, so the exposures add up
+        for (int ch = 2; (P->offload & TPIPE_OFFLOAD_MODEL_STATE) && ch <= P->v; ++ch) {
+            const double np = (double)P->chunk_params[s][ch - 1];
             double end_b = 0, start_f = mk;
             for (size_t j = 0; j < P->order[s].size(); ++j) {
                 const COp& op = P->order[s][j];
-                if (op[1] != P->v) continue;
+                if (op[1] != ch) continue;
                 if (op[0] == KB) end_b = std::max(end_b, times[s][j][1]);
                 if (op[0] == KF) start_f = std::min(start_f, times[s][j][0]);
             }
@@ -737,7 +746,8 @@ static double estimate(const tpipe_plan* P, const CostModel& cm, double* exposed
 
 static int make_plan(const tpipe_model_desc* model, int p, int m, int strategy, int k, int W,
                      int offload, int act_distance, int recomp_layers, const int32_t* stage_layers,
-                     const int32_t* stage_chunk1, const CostModel& cm, tpipe_plan** out, int dp = 1) {
+                     const int32_t* stage_chunk1, const CostModel& cm, tpipe_plan** out, int dp = 1,
+                     int chunks = 2) {
     if ((offload & TPIPE_OFFLOAD_DEVICE_OPT) && !(offload & TPIPE_OFFLOAD_MODEL_STATE))
         return set_error(TPIPE_E_INVALID, "offload: DEVICE_OPT needs MODEL_STATE");
     if ((offload & TPIPE_OFFLOAD_ACTIVATIONS) && strategy != TPIPE_S_TPIPE)
@@ -762,7 +772,21 @@ static int make_plan(const tpipe_model_desc* model, int p, int m, int strategy, 
         delete P;
         return set_error(TPIPE_E_INCOMPAT, "interleave-1F1B needs n_microbatches %% n_stages == 0");
     }
-    P->v = is_tp ? 2 : 1;
+    P->v = is_tp ? chunks : 1;
+    if (!is_tp && chunks != 2) {
+        delete P;
+        return set_error(TPIPE_E_INCOMPAT, "chunks applies to the T-Pipe and Interleave strategies");
+    }
+    if (P->v > 2 && ((stage_chunk1 && stage_chunk1[0]) || model->layers_chunk[0] || model->layers_chunk[1])) {
+        delete P;
+        return set_error(TPIPE_E_INVALID, "layers_chunk / stage_chunk1 are two-chunk options (chunks = 2)");
+    }
+    // v chunks: n / v layers each, the extra ones to the shallowest chunks (R14, R32)
+    auto split = [&](int ns) {
+        std::array<int, 4> x{};
+        for (int c = 0; c < P->v; ++c) x[c] = ns / P->v + (c < ns % P->v ? 1 : 0);
+        return x;
+    };
     const int n = model->n_layers / p;
     const bool part = stage_layers && stage_layers[0] != 0;
     if (part) {   // cost-balanced partition (R27)
@@ -781,18 +805,25 @@ static int make_plan(const tpipe_model_desc* model, int p, int m, int strategy, 
                 delete P;
                 return set_error(TPIPE_E_INVALID, "stage_chunk1[%d] = %d: need 1 .. %d", s, c1, ns - 1);
             }
-            P->sl.push_back(P->v == 2 ? std::array<int, 2>{c1, ns - c1} : std::array<int, 2>{ns, 0});
+            P->sl.push_back(P->v == 2 ? std::array<int, 4>{c1, ns - c1}
+                            : P->v == 1 ? std::array<int, 4>{ns, 0} : split(ns));
         }
         if (sum != model->n_layers) {
             delete P;
             return set_error(TPIPE_E_INVALID, "stage_layers sum %ld != n_layers %d", sum, model->n_layers);
         }
-        if (offload & TPIPE_OFFLOAD_MODEL_STATE && P->v != 2) {
+        if (offload & TPIPE_OFFLOAD_MODEL_STATE && P->v < 2) {
             delete P;
-            return set_error(TPIPE_E_INCOMPAT, "model-state offload requires T-Pipe (v = 2)");
+            return set_error(TPIPE_E_INCOMPAT, "model-state offload requires T-Pipe (v >= 2)");
         }
-        P->layers[0] = P->sl[0][0];
-        P->layers[1] = P->sl[0][1];
+        for (int c = 0; c < 4; ++c) P->layers[c] = P->sl[0][c];
+    } else if (P->v > 2) {
+        if (n < P->v) {
+            delete P;
+            return set_error(TPIPE_E_INCOMPAT, "%d chunks need >= %d layers per stage", P->v, P->v);
+        }
+        const auto x = split(n);
+        for (int c = 0; c < 4; ++c) P->layers[c] = x[c];
     } else if (P->v == 2) {
         if (model->layers_chunk[0] || model->layers_chunk[1]) {
             if (model->layers_chunk[0] < 1 || model->layers_chunk[1] < 1 ||
@@ -813,11 +844,11 @@ static int make_plan(const tpipe_model_desc* model, int p, int m, int strategy, 
     } else {
         if (offload) {
             delete P;
-            return set_error(TPIPE_E_INCOMPAT, "model-state offload requires T-Pipe (v = 2)");
+            return set_error(TPIPE_E_INCOMPAT, "model-state offload requires T-Pipe (v >= 2)");
         }
         P->layers[0] = n;
     }
-    if (!part) P->sl.assign(p, std::array<int, 2>{P->layers[0], P->v == 2 ? P->layers[1] : 0});
+    if (!part) P->sl.assign(p, std::array<int, 4>{P->layers[0], P->layers[1], P->layers[2], P->layers[3]});
     int n1max = 0;
     for (auto& x : P->sl) n1max = std::max(n1max, x[0]);
     const bool trecomp = strategy == TPIPE_S_TPIPE_TRECOMP || strategy == TPIPE_S_INTERLEAVE_TRECOMP;
@@ -827,13 +858,14 @@ static int make_plan(const tpipe_model_desc* model, int p, int m, int strategy, 
                          recomp_layers, n1max);
     }
     P->rl = trecomp ? (recomp_layers > 0 ? recomp_layers : n1max) : 0;
-    P->k = (trecomp && !is_il) ? (k < 0 ? delay_rounds_appB(p) : k) : 0;
+    // App. B's delay rounds are derived for two chunks; v > 2 runs undelayed (R32)
+    P->k = (trecomp && !is_il) ? (k < 0 ? (P->v == 2 ? delay_rounds_appB(p) : 0) : k) : 0;
     if (is_il) {
-        auto ord = interleave_order(p, m, trecomp);
+        auto ord = interleave_order(p, m, trecomp, P->v);
         P->order.assign(p, {});
         for (int s = 0; s < p; ++s) P->order[s] = ord[s];
     } else if (is_tp) {
-        auto ord = tpipe_order(p, m, trecomp, P->k);
+        auto ord = tpipe_order(p, m, trecomp, P->k, P->v);
         P->order.assign(p, {});
         for (int s = 0; s < p; ++s) P->order[s] = ord[s];
     } else {
@@ -902,7 +934,7 @@ static std::vector<int> balanced_partition(int L, int p, int v, double head_laye
 
 // Modeled makespan of a plan's compute order with per-stage (chunk-1, chunk-2)
 // layer counts `sl` (no offload terms): the cost model's ASAP replay.
-static double order_makespan(tpipe_plan* S, const std::vector<std::array<int, 2>>& sl, const CostModel& cm) {
+static double order_makespan(tpipe_plan* S, const std::vector<std::array<int, 4>>& sl, const CostModel& cm) {
     S->sl = sl;
     const double tl = layer_fwd_s(S->model, cm), th = head_fwd_s(S->model, cm);
     double mk = 0, busy[64];
@@ -924,12 +956,12 @@ static double search_partition(const tpipe_plan* U, const CostModel& cm, std::ve
                                std::vector<int>* c1_out) {
     tpipe_plan S = *U;   // order, p, v, strategy, model, rl
     const int p = S.p, v = S.v, L = S.model.n_layers;
-    auto split = [&](int n) { return v == 2 ? std::array<int, 2>{(n + 1) / 2, n / 2} : std::array<int, 2>{n, 0}; };
-    auto descend = [&](std::vector<std::array<int, 2>> sl) {
+    auto split = [&](int n) { return v == 2 ? std::array<int, 4>{(n + 1) / 2, n / 2} : std::array<int, 4>{n, 0}; };
+    auto descend = [&](std::vector<std::array<int, 4>> sl) {
         double cur = order_makespan(&S, sl, cm);
         for (int it = 0; it < 256; ++it) {
             double best = cur;
-            std::vector<std::array<int, 2>> best_sl;
+            std::vector<std::array<int, 4>> best_sl;
             for (int i = 0; i < p; ++i)
                 for (int j = 0; j < p; ++j) {
                     if (i == j) continue;
@@ -963,11 +995,11 @@ static double search_partition(const tpipe_plan* U, const CostModel& cm, std::ve
         }
         return std::make_pair(cur, sl);
     };
-    std::vector<std::array<int, 2>> starts[2];
+    std::vector<std::array<int, 4>> starts[2];
     starts[0] = U->sl;
     const auto r27 = balanced_partition(L, p, v, head_fwd_s(S.model, cm) / layer_fwd_s(S.model, cm));
     double best = 1e30;
-    std::vector<std::array<int, 2>> best_sl;
+    std::vector<std::array<int, 4>> best_sl;
     for (int k = 0; k < 2; ++k) {
         if (k == 1) {
             if (r27.empty()) break;
@@ -1001,7 +1033,9 @@ TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, in
     if (opts) o = *opts;
     if (o.stage_layers[0] == 0 && model && n_stages > 0 && model->n_layers % n_stages)
         return set_error(TPIPE_E_INVALID, "n_layers must be a positive multiple of n_stages");
-    const int W = o.send_window > 0 ? o.send_window : 2;
+    // send window (R12): 2; W = v chunks (the v - 1 chunk turnarounds share the
+    // wrap channel; W = 2 deadlocks at v = 4, R32)
+    const int W = o.send_window > 0 ? o.send_window : std::max(2, o.chunks > 0 ? o.chunks : 2);
     if (o.strategy < -1 || o.strategy > TPIPE_S_INTERLEAVE_TRECOMP) return set_error(TPIPE_E_INVALID, "strategy");
     if (o.delay_rounds < -1) return set_error(TPIPE_E_INVALID, "delay_rounds");
     if (o.recomp_layers < 0) return set_error(TPIPE_E_INVALID, "recomp_layers");
@@ -1009,6 +1043,9 @@ TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, in
         return set_error(TPIPE_E_INVALID, "cost model rates must be >= 0");
     if (o.dp < 0 || o.dp > 64) return set_error(TPIPE_E_INVALID, "dp must be in [1, 64]");
     const int dp = o.dp > 0 ? o.dp : 1;
+    if (o.chunks < 0 || o.chunks == 1 || o.chunks > 4) return set_error(TPIPE_E_INVALID, "chunks must be 2, 3 or 4");
+    const int chunks = o.chunks > 0 ? o.chunks : 2;
+    if (chunks > 2 && o.balance) return set_error(TPIPE_E_INVALID, "balance is a two-chunk option");
     CostModel cm;
     if (o.host_link_bps > 0) cm.bw = o.host_link_bps;
     if (o.host_adam_params_per_s > 0) cm.host = o.host_adam_params_per_s;
@@ -1048,7 +1085,7 @@ TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, in
         const int off = o.offload < 0 ? 0 : o.offload;
         tpipe_plan* P = nullptr;
         int rc = make_plan(model, n_stages, n_microbatches, o.strategy, o.delay_rounds, W, off,
-                           o.act_distance, o.recomp_layers, part, chunk1, cm, &P, dp);
+                           o.act_distance, o.recomp_layers, part, chunk1, cm, &P, dp, chunks);
         if (rc) return rc;
         if (hbm_budget_bytes && max_peak(P) > hbm_budget_bytes) {
             const uint64_t pk = max_peak(P);
@@ -1082,7 +1119,7 @@ TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, in
     for (auto& rung : ladder) {
         tpipe_plan* P = nullptr;
         int rc = make_plan(model, n_stages, n_microbatches, rung[0], o.delay_rounds, W, rung[1],
-                           o.act_distance, rung[2], part, chunk1, cm, &P, dp);
+                           o.act_distance, rung[2], part, chunk1, cm, &P, dp, chunks);
         if (rc) {
             if (rc == TPIPE_E_INCOMPAT || rc == TPIPE_E_INVALID) continue;   // rung not applicable
             delete best;
@@ -1166,6 +1203,12 @@ TP_API int tpipe_plan_stage_layers(const tpipe_plan* P, int32_t s, int32_t out[2
     if (!P || !out || s < 0 || s >= P->p) return set_error(TPIPE_E_INVALID, "stage");
     out[0] = P->sl[s][0];
     out[1] = P->sl[s][1];
+    return 0;
+}
+
+TP_API int tpipe_plan_chunk_layers(const tpipe_plan* P, int32_t s, int32_t c, int32_t* n) {
+    if (!P || !n || s < 0 || s >= P->p || c < 1 || c > P->v) return set_error(TPIPE_E_INVALID, "stage/chunk");
+    *n = P->sl[s][c - 1];
     return 0;
 }
 

@@ -96,7 +96,7 @@ struct StageState {
     // rt->stream forks into it at step start and joins it at the end
     cudaStream_t own = nullptr, cs = nullptr;
     std::unique_ptr<Pool> pool;   // this stage's HBM pool (reuse stays on one stream)
-    ChunkState ch[3];
+    ChunkState ch[5];   // chunks 1..v (v <= 4)
     int* tokens = nullptr;
     int* targets = nullptr;
     float* loss_slots = nullptr;
@@ -830,7 +830,7 @@ TP_API int tpipe_runtime_create(const tpipe_plan* plan, const tpipe_runtime_opts
                 C.P = C.lay.total;
                 if ((uint64_t)C.P != P.chunk_params[s][c - 1])
                     return set_error(TPIPE_E_STATE, "param layout mismatch");
-                C.offloaded = off && c == P.v;
+                C.offloaded = off && c >= 2;   // T-Offload of chunks 2..v (R32)
                 uint8_t* q = (uint8_t*)ptr;
                 C.w = q;
                 q += (size_t)C.P * D.es;
@@ -887,7 +887,7 @@ TP_API int tpipe_runtime_create(const tpipe_plan* plan, const tpipe_runtime_opts
     if (P.dp > 1) {
         StageState& S0 = *rt->st[o.stage];
         uint8_t* arena = (uint8_t*)S0.pool->arena();
-        uint64_t w_off[3] = {0, 0, 0}, g_off[3] = {0, 0, 0};
+        uint64_t w_off[5] = {0, 0, 0, 0, 0}, g_off[5] = {0, 0, 0, 0, 0};
         for (int c = 1; c <= P.v; ++c) {
             ChunkState& C = S0.ch[c];
             const uint8_t *w = (const uint8_t*)C.w, *g = (const uint8_t*)C.grad;

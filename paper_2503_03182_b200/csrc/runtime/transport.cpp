@@ -522,9 +522,9 @@ constexpr int DP_MAX = 64;
 struct alignas(64) DpMember {
     cudaIpcMemHandle_t arena;
     uint64_t arena_bytes;
-    uint64_t w_off[3], g_off[3];
-    cudaIpcEventHandle_t ready[3], done[3];
-    std::atomic<uint64_t> ready_seq[3], done_seq[3];
+    uint64_t w_off[5], g_off[5];
+    cudaIpcEventHandle_t ready[5], done[5];
+    std::atomic<uint64_t> ready_seq[5], done_seq[5];
 };
 struct alignas(64) DpHeader {
     std::atomic<uint64_t> magic;
@@ -538,7 +538,7 @@ class IpcDpGroup final : public DpGroup {
 public:
     ~IpcDpGroup() override {
         for (int j = 0; j < dp_; ++j)
-            for (int c = 0; c < 3; ++c) {
+            for (int c = 0; c < 5; ++c) {
                 if (ev_ready_[j][c]) cudaEventDestroy(ev_ready_[j][c]);
                 if (ev_done_[j][c]) cudaEventDestroy(ev_done_[j][c]);
             }
@@ -589,7 +589,7 @@ public:
         rank_ = rank;
         timeout_ms_ = timeout_ms;
         own_arena_ = arena;
-        if (dp < 2 || dp > DP_MAX || rank < 0 || rank >= dp || v < 1 || v > 2)
+        if (dp < 2 || dp > DP_MAX || rank < 0 || rank >= dp || v < 1 || v > 4)
             return set_error(TPIPE_E_INVALID, "dp group: dp %d rank %d", dp, rank);
         if (!name || name[0] != '/') return set_error(TPIPE_E_INVALID, "dp group needs an ipc_name ('/...')");
         shm_bytes_ = sizeof(DpHeader) + (size_t)dp * sizeof(DpMember);
@@ -647,7 +647,7 @@ public:
     size_t shm_bytes_ = 0;
     void* own_arena_ = nullptr;
     void* peer_arena_[DP_MAX] = {};
-    cudaEvent_t ev_ready_[DP_MAX][3] = {}, ev_done_[DP_MAX][3] = {};
+    cudaEvent_t ev_ready_[DP_MAX][5] = {}, ev_done_[DP_MAX][5] = {};
 };
 
 }  // namespace

@@ -18,21 +18,16 @@ LAYER_TENSORS = ("ln1_g", "ln1_b", "w_qkv", "b_qkv", "w_o", "b_o",
 
 def global_layers(p: int, v: int, layers_chunk, s: int, c: int):
     """Global layer indices held by (stage s, chunk c). `layers_chunk` is the
-    uniform per-stage (n1, n2) (or (n,) at v = 1), or a per-stage list of such
-    tuples (plan.partition, DESIGN R27): chunk-1 layers are numbered through
-    the stages first, then chunk-2 layers (P:210 layout)."""
+    uniform per-stage (n1, .., nv) (or (n,) at v = 1), or a per-stage list of
+    such tuples (plan.partition, DESIGN R27): chunk-1 layers are numbered
+    through the stages first, then chunk-2 layers, ... (P:210 layout)."""
     if layers_chunk and isinstance(layers_chunk[0], (tuple, list)):
         part = [tuple(x) for x in layers_chunk]
     else:
         part = [tuple(layers_chunk)] * p
-    if v == 1:
-        off = sum(part[t][0] for t in range(s))
-        return list(range(off, off + part[s][0]))
-    if c == 1:
-        off = sum(part[t][0] for t in range(s))
-        return list(range(off, off + part[s][0]))
-    off = sum(x[0] for x in part) + sum(part[t][1] for t in range(s))
-    return list(range(off, off + part[s][1]))
+    # chunk c's layers come after every stage's chunks 1..c-1 (v chunks, R32)
+    off = sum(x[cc] for x in part for cc in range(c - 1)) + sum(part[t][c - 1] for t in range(s))
+    return list(range(off, off + part[s][c - 1]))
 
 
 def chunk_entries(p, v, layers_chunk, s, c):

@@ -49,7 +49,8 @@ class Plan:
                  strategy="tpipe", delay_rounds: int = -1, send_window: int = 0, offload: int = 0,
                  act_distance: int = 0, recomp_layers: int = 0, stage_layers=None,
                  host_link_bps: float = 0.0, host_adam_params_per_s: float = 0.0,
-                 device_flops: float = 0.0, balance: bool = False, stage_chunk1=None, dp: int = 1):
+                 device_flops: float = 0.0, balance: bool = False, stage_chunk1=None, dp: int = 1,
+                 chunks: int = 2):
         L = lib()
         st = -1 if strategy in (None, "auto") else STRATEGY.get(strategy, strategy)
         if st < 0 and offload == 0:
@@ -57,7 +58,7 @@ class Plan:
         sl = (C.c_int32 * 64)(*(list(stage_layers or [])[:64]))
         opts = D.PlanOpts(st, delay_rounds, send_window, offload, act_distance, recomp_layers, sl,
                           host_link_bps, host_adam_params_per_s, device_flops, 1 if balance else 0,
-                          (C.c_int32 * 64)(*(list(stage_chunk1 or [])[:64])), dp)
+                          (C.c_int32 * 64)(*(list(stage_chunk1 or [])[:64])), dp, chunks)
         self._h = C.c_void_p()
         self.model = model
         check(L.tpipe_plan_create(C.byref(model.c()), n_stages, n_microbatches, hbm_budget,
@@ -76,11 +77,12 @@ class Plan:
         # per-stage (chunk-1, chunk-2) layers (DESIGN R27); == [layers_chunk] * p when uniform
         self.partition = []
         for s in range(self.p):
-            a = (C.c_int32 * 2)()
-            check(L.tpipe_plan_stage_layers(self._h, s, a))
-            self.partition.append((a[0], a[1]))
-        if self.v == 1:
-            self.partition = [(x[0],) for x in self.partition]
+            row = []
+            for ch in range(1, self.v + 1):
+                n = C.c_int32()
+                check(L.tpipe_plan_chunk_layers(self._h, s, ch, C.byref(n)))
+                row.append(n.value)
+            self.partition.append(tuple(row))
         self.layers_chunk = (info.layers_chunk[0], info.layers_chunk[1])
         self.params_total = info.params_total
         self.channels = []

@@ -1,5 +1,5 @@
 """Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv) by kernel:
-python scripts/launch_summary.py launches.csv [header-comment]"""
+python scripts/launch_summary.py launches.csv [header-comment] [last-N-launches]"""
 import csv, sys, collections
 
 path = sys.argv[1]
@@ -13,6 +13,8 @@ for r in csv.DictReader(lines):
     unit = r.get("Metric Unit", "ns")
     us = v / 1e3 if unit == "ns" else v * 1e3 if unit == "ms" else v if unit == "us" else v / 1e3
     rows.append((r["Kernel Name"], us))
+if len(sys.argv) > 3:
+    rows = rows[-int(sys.argv[3]):]
 tot = sum(u for _, u in rows)
 agg = collections.defaultdict(lambda: [0, 0.0])
 for k, u in rows:

@@ -208,3 +208,59 @@ def test_duration_aware_partition_step(strategy):
     for k in grads[0]:
         assert np.array_equal(np.asarray(grads[0][k], np.float32).view(np.uint32),
                               np.asarray(grads[1][k], np.float32).view(np.uint32)), k
+
+
+MC_CASES = [("tpipe", 0), ("tpipe_trecomp", 0), ("interleave_trecomp", 0), ("tpipe", 1), ("tpipe_trecomp", 5)]
+
+
+@pytest.mark.parametrize("v", [3, 4])
+@pytest.mark.parametrize("strategy,offload", MC_CASES)
+def test_multichunk_parity(v, strategy, offload):
+    """v = 3, 4 chunks per stage (NEXT-4 / NEXT-1, DESIGN R32): fp32 gradients
+    and loss vs the oracle; after two optimizer steps (multi-chunk T-Offload
+    of chunks 2..v with the host or streamed device AdamW) the bf16
+    parameters are bit-identical to the same model at v = 2 (per-layer math
+    and per-chunk accumulation order do not depend on the chunking)."""
+    P, RT, PR = mods()
+    cfg = dict(C1_16, L=4 * v)
+    p, m = 2, 4
+    W = synth.weights(cfg["L"], cfg["h"], cfg["f"], cfg["V"], cfg["s"], seed=11, std=0.05,
+                      bias_std=0.02, ln_jitter=0.05)
+    tok, tgt = synth.tokens(cfg["V"], m, cfg["b"], cfg["s"], step=0)
+    lref, G = R.step_grads(R.to64(W), tok, tgt, cfg["a"])
+    md = P.Model(cfg["L"], cfg["h"], cfg["a"], cfg["f"], cfg["V"], cfg["s"], cfg["b"], 0)
+    plan = P.Plan(md, p, m, strategy=strategy, offload=offload, chunks=v)
+    rt = RT.Runtime(plan, stage=-1, lr=1e-3)
+    for s in range(p):
+        for c in range(1, v + 1):
+            rt.set_params(s, c, PR.pack(W, p, v, plan.partition, s, c))
+    loss = rt.step(tok, tgt, RT.STEP_NO_OPT)
+    assert abs(loss - lref) / abs(lref) < 1e-5
+    for s in range(p):
+        for c in range(1, v + 1):
+            for (k, l), g in PR.unpack(rt.get_grads(s, c), W, p, v, plan.partition, s, c).items():
+                ref = G["layers"][l][k] if l is not None else G[k]
+                assert max_rel(g, ref) <= 1e-4, (s, c, k, l)
+    st = rt.stats()
+    assert all(st["pool_high_water"][s] == plan.peak(s)["total_peak"] for s in range(p))
+    rt.close()
+    params = []
+    for vv in (v, 2):
+        md = P.Model(cfg["L"], cfg["h"], cfg["a"], cfg["f"], cfg["V"], cfg["s"], cfg["b"], 1)
+        plan = P.Plan(md, p, m, strategy=strategy, offload=offload, chunks=vv)
+        rt = RT.Runtime(plan, stage=-1, lr=1e-3)
+        for s in range(p):
+            for c in range(1, vv + 1):
+                rt.set_params(s, c, PR.pack(W, p, vv, plan.partition, s, c))
+        for k in range(2):
+            t2, g2 = synth.tokens(cfg["V"], m, cfg["b"], cfg["s"], step=k)
+            rt.step(t2, g2, 0)
+        d = {}
+        for s in range(p):
+            for c in range(1, vv + 1):
+                d.update(PR.unpack(rt.get_params(s, c), W, p, vv, plan.partition, s, c))
+        params.append(d)
+        rt.close()
+    for key in params[0]:
+        assert np.array_equal(np.asarray(params[0][key], np.float32).view(np.uint32),
+                              np.asarray(params[1][key], np.float32).view(np.uint32)), key
