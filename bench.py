@@ -228,6 +228,13 @@ def fast_init_chunk(plan, s, c, pool):
 CAP_P, CAP_BUDGET_GIB, CAP_M = 8, 20, 16
 
 
+def plan_of(md, p, m, budget, strat, off):
+    """P.Plan for a strategy name with an optional '@v<chunks>' suffix."""
+    from paper_2503_03182_b200 import plan as P
+    name, _, v = strat.partition("@v")
+    return P.Plan(md, p, m, hbm_budget=budget, strategy=name, offload=off, chunks=int(v) if v else 2)
+
+
 def capacity_plans(p=CAP_P, budget=CAP_BUDGET_GIB * 2 ** 30, m=CAP_M):
     """Largest L (multiple of p) each strategy fits under `budget` bytes per
     stage for the C5 shape (h=4096, s=8192), from the planner's byte model."""
@@ -241,14 +248,17 @@ def capacity_plans(p=CAP_P, budget=CAP_BUDGET_GIB * 2 ** 30, m=CAP_M):
                   # offload, both
                   "tpipe_offload": ("tpipe", ms), "tpipe_actoff": ("tpipe", P.OFFLOAD_ACTIVATIONS),
                   "tpipe_actoff_offload": ("tpipe", P.OFFLOAD_ACTIVATIONS | ms),
-                  "interleave": ("interleave", 0), "interleave_trecomp": ("interleave_trecomp", 0)}
+                  "interleave": ("interleave", 0), "interleave_trecomp": ("interleave_trecomp", 0),
+                  # v = 3 chunks (R32): T-Recomp of chunk 1 (a third of the stage's layers)
+                  # + T-Offload of chunks 2 and 3
+                  "tpipe_all_v3": ("tpipe_trecomp@v3", ms), "tpipe_offload_v3": ("tpipe@v3", ms)}
     best = {}
     for name, (strat, off) in strategies.items():
         for L in range(p, 400, p):
             md = P.Model(L, C5["hidden"], C5["n_heads"], C5["ffn_hidden"], C5["vocab"],
                          C5["seq_len"], C5["micro_batch"], P.BF16)
             try:
-                P.Plan(md, p, m, hbm_budget=budget, strategy=strat, offload=off)
+                plan_of(md, p, m, budget, strat, off)
                 best[name] = (L, strat, off)
             except TPipeError:
                 # odd chunk splits are invalid for v=2 at small L; a budget
@@ -274,7 +284,8 @@ def run_capacity(args):
     p, m, budget = CAP_P, CAP_M, CAP_BUDGET_GIB * 2 ** 30
     best = capacity_plans()
     names = ("1f1b", "1f1b_full_recomp", "tpipe", "tpipe_trecomp", "tpipe_all", "tpipe_offload",
-             "tpipe_actoff", "tpipe_actoff_offload", "interleave", "interleave_trecomp")
+             "tpipe_actoff", "tpipe_actoff_offload", "interleave", "interleave_trecomp", "tpipe_all_v3",
+             "tpipe_offload_v3")
     only = os.environ.get("TPIPE_CAPACITY_ONLY")
     if only:
         names = tuple(n for n in names if n in only.split(",") or n == "1f1b")
@@ -303,7 +314,7 @@ def run_capacity(args):
     for name, L, strat, off in runs:
         md = P.Model(L, C5["hidden"], C5["n_heads"], C5["ffn_hidden"], C5["vocab"],
                      C5["seq_len"], C5["micro_batch"], P.BF16)
-        plan = P.Plan(md, p, m, hbm_budget=budget, strategy=strat, offload=off)
+        plan = plan_of(md, p, m, budget, strat, off)
         t0 = time.perf_counter()
         rt = RT.Runtime(plan, stage=-1, lr=1e-5, pool_cap=budget)
         for s in range(p):
@@ -329,7 +340,8 @@ def run_capacity(args):
         res[name] = {"strategy": strat, "offload": plan.offload, "n_layers": L,
                      "plan_strategy": ["1f1b", "1f1b_full_recomp", "tpipe", "tpipe_trecomp", "interleave",
                                        "interleave_trecomp"][plan.strategy],
-                     "recomp_layers": plan.recomp_layers, "layers_chunk": list(plan.layers_chunk),
+                     "recomp_layers": plan.recomp_layers, "layers_chunk": list(plan.partition[0]),
+                     "chunks": plan.v,
                      "params_B": round(plan.params_total / 1e9, 3),
                      "plan_peak_GiB": [round(plan.peak(s)["total_peak"] / 2 ** 30, 3) for s in range(p)],
                      "pool_high_water_GiB": [round(x / 2 ** 30, 3) for x in hw],
