@@ -153,6 +153,22 @@ def cpu_baseline(c, seconds_cap=30.0):
     except Exception:
         blas = None
     cores = len(os.sched_getaffinity(0))
+    # single-thread figure: the same layer on one core, bounded
+    # to a 512-token slice of the sequence (attention cost grows with s)
+    one = None
+    try:
+        from threadpoolctl import threadpool_limits
+        s1 = min(s, 512)
+        with threadpool_limits(limits=1):
+            t3 = time.perf_counter()
+            y, cache = R.layer_fwd(x[:, :s1], L, a)
+            R.layer_bwd(dy[:, :s1], cache, L, a)
+            dt1 = time.perf_counter() - t3
+        one = {"value": round(s1 / dt1 / c["n_layers"], 3), "unit": "tokens/s", "threads": 1,
+               "sample": f"1 micro-batch fwd+bwd of 1 layer on a {s1}-token slice (h={h}), fp64, "
+                         f"{dt1:.1f}s; / L={c['n_layers']}"}
+    except Exception as e:   # reported, not fatal
+        one = {"error": str(e)[:120]}
     # SURVEY §8(d) "oracle timing beside the GPU": (i) the exact schedule simulator
     # for p = 8, m = 32, all strategies; (ii) one full fp64 training step of C1
     from oracle import schedule as S
@@ -169,9 +185,96 @@ def cpu_baseline(c, seconds_cap=30.0):
     return {"value": layer_tps / c["n_layers"], "unit": "tokens/s", "cores": cores,
             "blas_threads": blas, "kind": "oracle",
             "schedule_sim_p8_m32_all_strategies_s": round(sim_s, 3),
-            "c1_fp64_step_s": round(c1_s, 3),
+            "c1_fp64_step_s": round(c1_s, 3), "single_thread": one,
             "sample": f"{n} x (1 micro-batch fwd+bwd of 1 layer, h={h}, s={s}, fp64 NumPy) "
                       f"in {dt:.1f}s; model tokens/s = layer tokens/s / L={c['n_layers']}"}
+
+
+WORKLOADS = {  # BASELINE.json configs[2] / [3] layer shapes
+    "c3": dict(name="configs[2]: Llama-style 7B shape (L=32, h=4096, a=32, ffn=16384, V=32000, s=4096)",
+               n_layers=32, hidden=4096, n_heads=32, ffn_hidden=16384, vocab=32000, seq_len=4096),
+    "c4": dict(name="configs[3]: Llama-style 13B shape (L=40, h=5120, a=40, ffn=20480, V=32000, s=8192)",
+               n_layers=40, hidden=5120, n_heads=40, ffn_hidden=20480, vocab=32000, seq_len=8192),
+}
+
+
+def run_workload(args):
+    """The C3 / C4 model shapes through the same runtime on ONE B200 (p = 1,
+    m = 8): the planner's auto ladder (R28) under the GPU's free HBM picks the
+    strategy (C4 needs T-Recomp + T-Offload to fit). Not the 8-stage configs
+    themselves (one GPU here); a throughput line at those shapes."""
+    import torch
+    from paper_2503_03182_b200 import plan as P, runtime as RT
+    import synth
+    w = WORKLOADS[args.workload]
+    m = 8
+    md = P.Model(w["n_layers"], w["hidden"], w["n_heads"], w["ffn_hidden"], w["vocab"], w["seq_len"], 1, P.BF16)
+    free_b, _ = torch.cuda.mem_get_info()
+    budget = int(free_b * 0.93) - (1 << 30)
+    plan = P.Plan(md, 1, m, hbm_budget=budget, strategy="auto",
+                  offload=P.OFFLOAD_MODEL_STATE | P.OFFLOAD_DEVICE_OPT | P.OFFLOAD_ACTIVATIONS)
+    rt = RT.Runtime(plan, stage=-1, lr=1e-5)
+    pool = (np.random.default_rng(5).standard_normal(1 << 24, dtype=np.float32) * np.float32(0.02))
+    for ch in range(1, plan.v + 1):
+        rt.set_params(0, ch, fast_init_chunk(plan, 0, ch, pool))
+    tok, tgt = synth.tokens(w["vocab"], m, 1, w["seq_len"], step=0)
+    dtok = torch.tensor(tok, dtype=torch.int32, device="cuda")
+    dtgt = torch.tensor(tgt, dtype=torch.int32, device="cuda")
+    ext = torch.cuda.ExternalStream(rt.stream())
+    for _ in range(args.warmup):
+        rt.step_device(dtok.data_ptr(), dtgt.data_ptr())
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(0) as clk:
+        e0.record(ext)
+        for _ in range(args.steps):
+            rt.step_device(dtok.data_ptr(), dtgt.data_ptr())
+        e1.record(ext)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    tokens = m * w["seq_len"]
+    fl = model_flops_per_token(w)
+    _, _, pk, src = peaks()
+    st = rt.stats()
+    out = {"metric": METRIC, "value": round(tokens / (ms / 1e3), 1), "unit": "tokens/s", "n_gpus": 1,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 2), "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights)",
+           "config": {"workload": w["name"] + ", p=1 on one B200, m=8", "params_B": round(plan.params_total / 1e9, 2),
+                      "hbm_budget_GiB": round(budget / 2 ** 30, 1),
+                      "plan": {"strategy": ["1f1b", "1f1b_full_recomp", "tpipe", "tpipe_trecomp", "interleave",
+                                            "interleave_trecomp"][plan.strategy], "offload": plan.offload,
+                               "recomp_layers": plan.recomp_layers, "chunks": plan.v},
+                      "plan_peak_GiB": round(plan.peak(0)["total_peak"] / 2 ** 30, 2),
+                      "pool_high_water_GiB": round(st["pool_high_water"][0] / 2 ** 30, 2)},
+           "mfu": round(tokens / (ms / 1e3) * fl / (pk * 1e12), 4), "mfu_peak": f"{pk} ({src})",
+           "clocks": clk.summary()}
+    rt.close()
+    return out
+
+
+def oracle_layer_timing():
+    """fp64 oracle, one layer forward + backward of one micro-batch at the C3
+    (Llama-7B shape, s = 4096) and C4 (13B shape, s = 8192) layer shapes,
+    all host cores (SURVEY §8(d) item iii). C4's attention at s = 8192 would
+    materialise 40 x 8192^2 fp64 scores (21 GB per tensor), so C4 is timed on
+    a 2048-token sample and reported as such."""
+    from oracle import model as R
+    import synth
+    out = {}
+    for name, (h, a, f, s, s_run) in {"C3": (4096, 32, 16384, 4096, 4096),
+                                      "C4": (5120, 40, 20480, 8192, 2048)}.items():
+        W = synth.weights(1, h, f, 64, s_run, seed=1)
+        L = R.to64(W)["layers"][0]
+        rng = np.random.default_rng(0)
+        x = rng.standard_normal((1, s_run, h))
+        t0 = time.perf_counter()
+        y, cache = R.layer_fwd(x, L, a)
+        R.layer_bwd(x, cache, L, a)
+        dt = time.perf_counter() - t0
+        out[name] = {"h": h, "a": a, "ffn": f, "seq_len": s, "tokens_timed": s_run, "s": round(dt, 2),
+                     "layer_tokens_per_s": round(s_run / dt, 2), "cores": len(os.sched_getaffinity(0))}
+        del cache, y
+    return out
 
 
 def capacity(p, strategies=("1f1b", "tpipe", "tpipe_trecomp", "tpipe_all", "interleave",
@@ -229,10 +332,12 @@ CAP_P, CAP_BUDGET_GIB, CAP_M = 8, 20, 16
 
 
 def plan_of(md, p, m, budget, strat, off):
-    """P.Plan for a strategy name with an optional '@v<chunks>' suffix."""
+    """P.Plan for a strategy name with an optional '@v<chunks>' suffix ('auto':
+    the ladder also tries 3 and 4 chunks)."""
     from paper_2503_03182_b200 import plan as P
     name, _, v = strat.partition("@v")
-    return P.Plan(md, p, m, hbm_budget=budget, strategy=name, offload=off, chunks=int(v) if v else 2)
+    return P.Plan(md, p, m, hbm_budget=budget, strategy=name, offload=off,
+                  chunks=int(v) if v else (0 if name == "auto" else 2))
 
 
 def capacity_plans(p=CAP_P, budget=CAP_BUDGET_GIB * 2 ** 30, m=CAP_M):
@@ -716,7 +821,8 @@ def latest_capacity_claim():
          f"({best['plan_strategy']}, offload={best.get('offload', 0)})")
     if two:
         s += (f"; fastest >= 2x model: {two['params_vs_1f1b']}x params at {two['model_tflops_vs_1f1b']}x "
-              f"({two['plan_strategy']}, offload={two.get('offload', 0)}, r={two.get('recomp_layers', 0)})")
+              f"({two['plan_strategy']}, chunks={two.get('chunks', 2)}, offload={two.get('offload', 0)}, "
+              f"r={two.get('recomp_layers', 0)})")
     return s
 
 
@@ -1029,7 +1135,17 @@ def main():
                          "parallel (SURVEY NEXT-3)")
     ap.add_argument("--virtual-stages", type=int, default=0,
                     help="run a p-stage virtual pipeline on this one GPU (reported as n_gpus = 1)")
+    ap.add_argument("--workload", default="", choices=["", "c3", "c4"],
+                    help="throughput at the C3 / C4 model shapes on one GPU (p = 1, auto ladder)")
+    ap.add_argument("--oracle-timing", action="store_true",
+                    help="fp64 oracle per-layer timing at the C3 / C4 layer shapes (host cores)")
     args = ap.parse_args()
+    if args.workload:
+        print(json.dumps(run_workload(args)), flush=True)
+        return
+    if args.oracle_timing:
+        print(json.dumps({"oracle_layer_timing": oracle_layer_timing()}), flush=True)
+        return
     if args.capacity_run:
         print(json.dumps(run_capacity(args)), flush=True)
         return

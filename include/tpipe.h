@@ -155,7 +155,8 @@ typedef struct {
                               Per stage n / v layers per chunk, the extra ones to the
                               shallowest chunks; T-Pipe uses the period-3v slot table (D-11);
                               T-Recomp regenerates chunk 1; model-state T-Offload moves chunks
-                              2..v. layers_chunk, stage_chunk1 and balance need v = 2 */
+                              2..v. layers_chunk, stage_chunk1 and balance need v = 2.
+                              With strategy -1 (auto), 0 lets the ladder try v = 2, 3, 4 */
 } tpipe_plan_opts;
 
 enum {

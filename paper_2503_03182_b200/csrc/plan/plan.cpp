@@ -1106,20 +1106,31 @@ TP_API int tpipe_plan_create(const tpipe_model_desc* model, int32_t n_stages, in
     const bool ms_ok = o.offload < 0 || (o.offload & TPIPE_OFFLOAD_MODEL_STATE);
     const bool act_ok = o.offload < 0 || (o.offload & TPIPE_OFFLOAD_ACTIVATIONS);
     const int off_ms = TPIPE_OFFLOAD_MODEL_STATE | (o.offload > 0 ? (o.offload & TPIPE_OFFLOAD_DEVICE_OPT) : 0);
-    std::vector<std::array<int, 3>> ladder;   // {strategy, offload, r}
-    ladder.push_back({TPIPE_S_TPIPE, 0, 0});
-    if (ms_ok) ladder.push_back({TPIPE_S_TPIPE, off_ms, 0});
-    if (act_ok) ladder.push_back({TPIPE_S_TPIPE, TPIPE_OFFLOAD_ACTIVATIONS, 0});
-    if (act_ok && ms_ok) ladder.push_back({TPIPE_S_TPIPE, TPIPE_OFFLOAD_ACTIVATIONS | off_ms, 0});
-    for (int r = rmin; r <= rmax; ++r) ladder.push_back({TPIPE_S_TPIPE_TRECOMP, 0, r});
-    if (ms_ok)
-        for (int r = rmin; r <= rmax; ++r) ladder.push_back({TPIPE_S_TPIPE_TRECOMP, off_ms, r});
+    std::vector<std::array<int, 4>> ladder;   // {strategy, offload, r, chunks}
+    // chunk counts: the requested one, or (chunks = 0) 2, 3 and 4 (R32: finer
+    // chunks recompute a smaller chunk 1 and offload (v - 1)/v of the states)
+    std::vector<int> vs;
+    if (o.chunks > 0) vs.push_back(o.chunks);
+    else vs = {2, 3, 4};
+    for (int vv : vs) {
+        const int rmx = o.recomp_layers > 0 ? o.recomp_layers
+                        : (vv == 2 ? rmax : (model->n_layers / n_stages + vv - 1) / vv);
+        ladder.push_back({TPIPE_S_TPIPE, 0, 0, vv});
+        if (ms_ok) ladder.push_back({TPIPE_S_TPIPE, off_ms, 0, vv});
+        if (act_ok && vv == 2) ladder.push_back({TPIPE_S_TPIPE, TPIPE_OFFLOAD_ACTIVATIONS, 0, vv});
+        if (act_ok && ms_ok && vv == 2)
+            ladder.push_back({TPIPE_S_TPIPE, TPIPE_OFFLOAD_ACTIVATIONS | off_ms, 0, vv});
+        for (int r = rmin; r <= rmx; ++r) ladder.push_back({TPIPE_S_TPIPE_TRECOMP, 0, r, vv});
+        if (ms_ok)
+            for (int r = rmin; r <= rmx; ++r) ladder.push_back({TPIPE_S_TPIPE_TRECOMP, off_ms, r, vv});
+    }
     uint64_t best_peak = ~0ull;
     tpipe_plan* best = nullptr;
     for (auto& rung : ladder) {
         tpipe_plan* P = nullptr;
-        int rc = make_plan(model, n_stages, n_microbatches, rung[0], o.delay_rounds, W, rung[1],
-                           o.act_distance, rung[2], part, chunk1, cm, &P, dp, chunks);
+        const int Wr = o.send_window > 0 ? o.send_window : std::max(2, rung[3]);
+        int rc = make_plan(model, n_stages, n_microbatches, rung[0], o.delay_rounds, Wr, rung[1],
+                           o.act_distance, rung[2], part, chunk1, cm, &P, dp, rung[3]);
         if (rc) {
             if (rc == TPIPE_E_INCOMPAT || rc == TPIPE_E_INVALID) continue;   // rung not applicable
             delete best;
