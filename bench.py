@@ -619,21 +619,18 @@ def pipeline_replay(ps=(8,), strategies=("1f1b", "tpipe", "tpipe_trecomp", "1f1b
     tokens = m * c["micro_batch"] * c["seq_len"]
     _, _, pk_sust, _src = peaks()
     out = {}
-    head_layers = 6 * c["hidden"] * c["vocab"] / (72 * c["hidden"] ** 2 + 6 * c["seq_len"] * c["hidden"])
     for p in ps:
         res = {}
         for st in strategies:
             md = P.Model(c["n_layers"], c["hidden"], c["n_heads"], c["ffn_hidden"], c["vocab"],
                          c["seq_len"], c["micro_batch"], P.BF16)
-            base_st = st[:-4] if st.endswith("_bal") else st
+            # "_bal": the planner's duration-aware partition (R27 / R29, balance);
+            # "_v3": three chunks per stage (R32)
+            bal, v3 = st.endswith("_bal"), st.endswith("_v3")
+            base_st = st[:-4] if bal else (st[:-3] if v3 else st)
             part = None
-            if st.endswith("_bal"):
-                v = 1 if base_st.startswith("1f1b") else 2
-                part = balanced_partition(c["n_layers"], p, v, head_layers)
-                if part is None:
-                    continue
             try:
-                plan = P.Plan(md, p, m, strategy=base_st, stage_layers=part)
+                plan = P.Plan(md, p, m, strategy=base_st, balance=bal and p > 1, chunks=3 if v3 else 2)
             except Exception as e:   # e.g. an invalid chunk split
                 res[st] = {"error": str(e)[:120]}
                 continue
@@ -647,7 +644,7 @@ def pipeline_replay(ps=(8,), strategies=("1f1b", "tpipe", "tpipe_trecomp", "1f1b
             rt.close()
             mk, busy = plan.simulate_durations(op_ms)
             tps = tokens / (mk / 1e3)
-            res[st] = {"layers_chunk": list(plan.layers_chunk), "stage_layers": part,
+            res[st] = {"partition": [list(x) for x in plan.partition],
                        "ms_per_step": round(mk, 2),
                        "tokens_s": round(tps, 1),
                        "mfu": round(tps * model_flops_per_token(c) / (p * pk_sust * 1e12), 4),
@@ -666,7 +663,9 @@ def gemm_traffic():
     """Per-launch DRAM traffic of the tcgen05 GEMM class from the committed
     `ncu --set full` capture of the 12 layer GEMM shapes (scripts/
     gemm_shapes_once.py): mean dram__bytes_read.sum + dram__bytes_write.sum."""
-    path = os.path.join(ROOT, "profiles", "r1_gemm_ncu_full_v2.jsonl")
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_gemm_ncu_full_v*.jsonl")))
+    path = files[-1] if files else ""
     try:
         with open(path) as f:
             for line in f:
@@ -998,8 +997,8 @@ def run_tpipe(args):
                          "unit": "TFLOP/s",
                          "frac": round(gemm_tf / pk_sust, 4) if gemm_tf else None,
                          "traffic": traffic, "traffic_alg_bytes": alg_bytes,
-                         "traffic_src": "profiles/r1_gemm_ncu_full_v2.jsonl: mean DRAM bytes per launch "
-                                        "over the 12 layer GEMM shapes (ncu --set full)",
+                         "traffic_src": "newest profiles/r*_gemm_ncu_full_v*.jsonl: mean DRAM bytes per "
+                                        "launch over the 12 layer GEMM shapes (ncu --set full)",
                          "peak_src": f"bf16_tflops_sustained ({src})",
                          "launches_per_step": int(kcnt[0] / args.steps),
                          "share_of_step": round(kms[0] / args.steps / step_ms, 3)},
@@ -1155,7 +1154,9 @@ def main():
                                                                         "interleave",
                                                                         "interleave_trecomp",
                                                                         "1f1b_bal", "tpipe_bal",
-                                                                        "tpipe_trecomp_bal"))}),
+                                                                        "tpipe_trecomp_bal",
+                                                                        "interleave_bal", "tpipe_v3",
+                                                                        "tpipe_trecomp_v3"))}),
               flush=True)
         return
     if args.warmup < 3:

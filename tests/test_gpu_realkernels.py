@@ -264,3 +264,24 @@ def test_multichunk_parity(v, strategy, offload):
     for key in params[0]:
         assert np.array_equal(np.asarray(params[0][key], np.float32).view(np.uint32),
                               np.asarray(params[1][key], np.float32).view(np.uint32)), key
+
+
+@pytest.mark.parametrize("strategy,offload,p", [("tpipe", 0, 4), ("tpipe_trecomp", 5, 4), ("tpipe", 2, 2),
+                                                ("1f1b_full_recomp", 0, 4), ("interleave_trecomp", 0, 8)])
+def test_planned_arena_close_to_peak(strategy, offload, p):
+    """The pool lays out every buffer of the plan once (fixed lifetimes):
+    the physical arena stays within a few percent of the plan peak (the
+    ledger high-water equals the peak exactly), and steps reuse it without
+    any run-time placement."""
+    _P, RT, _PR = mods()
+    cfg = C1_16 if p == 8 else C_MID8
+    plan, rt, W = build(cfg, p, 2 * p, strategy, 1, offload)
+    tok, tgt = synth.tokens(cfg["V"], 2 * p, cfg["b"], cfg["s"], step=0)
+    for _ in range(2):
+        rt.step(tok, tgt, 0)
+    st = rt.stats()
+    peak = sum(plan.peak(s)["total_peak"] for s in range(p))
+    assert all(st["pool_high_water"][s] == plan.peak(s)["total_peak"] for s in range(p))
+    assert st["pool_overflow_bytes"] == 0
+    assert peak <= st["pool_reserved"] <= 1.12 * peak + p * (1 << 20), (st["pool_reserved"], peak)
+    rt.close()
