@@ -798,30 +798,35 @@ def quick_measure(strategy, N, m, dtok, dtgt, args, recomp_layers=0, offload=0, 
 
 
 def latest_capacity_claim():
-    """The executed-capacity headline, read from the newest committed
-    profiles/*capacity_measured*.json (so the printed claim cannot go stale)."""
+    """The executed-capacity headline, read from the newest round's committed
+    profiles/r<N>_capacity_measured*.json files (so the printed claim cannot go
+    stale): the largest executed model and the fastest one >= 2x 1F1B's size,
+    each ratio against the 1F1B run of its own file."""
     import glob
     import re
-    files = glob.glob(os.path.join(ROOT, "profiles", "*capacity_measured*.json"))
+    files = glob.glob(os.path.join(ROOT, "profiles", "r*_capacity_measured*.json"))
     if not files:
         return None
-    key = lambda f: (re.findall(r"r(\d+)_", os.path.basename(f)) or ["0"])[0].zfill(3) + \
-        (re.findall(r"_v(\d+)", f) or ["0"])[0].zfill(3)
-    f = max(files, key=key)
-    runs = json.load(open(f))["capacity_measured"]["runs"]
-    best = max((r for r in runs.values() if r.get("fits_budget")),
-               key=lambda r: r.get("params_vs_1f1b", 0), default=None)
-    if not best:
+    rnd = max(int(re.findall(r"r(\d+)_", os.path.basename(f))[0]) for f in files)
+    runs = []
+    for f in sorted(files):
+        if int(re.findall(r"r(\d+)_", os.path.basename(f))[0]) != rnd:
+            continue
+        for r in json.load(open(f))["capacity_measured"]["runs"].values():
+            if r.get("fits_budget") and "params_vs_1f1b" in r:
+                runs.append((os.path.relpath(f, ROOT), r))
+    if not runs:
         return None
-    two = max((r for r in runs.values() if r.get("fits_budget") and r.get("params_vs_1f1b", 0) >= 2),
-              key=lambda r: r.get("model_tflops_vs_1f1b", 0), default=None)
-    s = (f"{os.path.relpath(f, ROOT)}: largest executed model {best['params_B']}B params = "
-         f"{best['params_vs_1f1b']}x 1F1B's at {best['model_tflops_vs_1f1b']}x its model TFLOP/s "
-         f"({best['plan_strategy']}, offload={best.get('offload', 0)})")
+    fb, best = max(runs, key=lambda x: x[1]["params_vs_1f1b"])
+    s = (f"{fb}: largest executed model {best['params_B']}B params = {best['params_vs_1f1b']}x 1F1B's at "
+         f"{best['model_tflops_vs_1f1b']}x its model TFLOP/s ({best['plan_strategy']}, "
+         f"chunks={best.get('chunks', 2)}, offload={best.get('offload', 0)})")
+    two = [x for x in runs if x[1]["params_vs_1f1b"] >= 2]
     if two:
-        s += (f"; fastest >= 2x model: {two['params_vs_1f1b']}x params at {two['model_tflops_vs_1f1b']}x "
-              f"({two['plan_strategy']}, chunks={two.get('chunks', 2)}, offload={two.get('offload', 0)}, "
-              f"r={two.get('recomp_layers', 0)})")
+        ft, t = max(two, key=lambda x: x[1]["model_tflops_vs_1f1b"])
+        s += (f"; {ft}: fastest >= 2x model {t['params_vs_1f1b']}x params at {t['model_tflops_vs_1f1b']}x "
+              f"({t['plan_strategy']}, chunks={t.get('chunks', 2)}, offload={t.get('offload', 0)}, "
+              f"r={t.get('recomp_layers', 0)})")
     return s
 
 
