@@ -11,7 +11,10 @@ import sys
 
 
 def num(x):
-    return float(str(x).replace(",", ""))
+    try:
+        return float(str(x).replace(",", ""))
+    except ValueError:
+        return float("nan")
 
 
 rows = list(csv.reader(open(sys.argv[1])))
@@ -20,7 +23,10 @@ data = [r for r in rows[2:] if len(r) == len(hdr)]   # row 1 = units
 units = rows[1]
 shapes = [json.loads(l) for l in open(sys.argv[2]) if l.startswith("{")]
 col = {h: i for i, h in enumerate(hdr)}
-tensor_col = next((h for h in hdr if "tensor" in h and h.endswith("pct_of_peak_sustained_elapsed")), None)
+PREF = ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed")
+tensor_col = next((h for h in PREF if h in hdr), None)
 out, dram_tot, alg_tot = [], 0.0, 0.0
 for sh, r in zip(shapes, data):
     t = num(r[col["gpu__time_duration.sum"]])
