@@ -333,8 +333,12 @@ CAP_P, CAP_BUDGET_GIB, CAP_M = 8, 20, 16
 
 def plan_of(md, p, m, budget, strat, off):
     """P.Plan for a strategy name with an optional '@v<chunks>' suffix ('auto':
-    the ladder also tries 3 and 4 chunks)."""
+    the ladder also tries 3 and 4 chunks) or '@r50' (1F1B + layer-grouped
+    recompute of half of each stage's layers, the paper's 1F1B + R50)."""
     from paper_2503_03182_b200 import plan as P
+    if strat.endswith("@r50"):
+        return P.Plan(md, p, m, hbm_budget=budget, strategy=strat[:-4], offload=off,
+                      recomp_layers=max(1, md.n_layers // p // 2))
     name, _, v = strat.partition("@v")
     return P.Plan(md, p, m, hbm_budget=budget, strategy=name, offload=off,
                   chunks=int(v) if v else (0 if name == "auto" else 2))
@@ -347,6 +351,7 @@ def capacity_plans(p=CAP_P, budget=CAP_BUDGET_GIB * 2 ** 30, m=CAP_M):
     from paper_2503_03182_b200._lib import TPipeError
     ms = P.OFFLOAD_MODEL_STATE | P.OFFLOAD_DEVICE_OPT
     strategies = {"1f1b": ("1f1b", 0), "1f1b_full_recomp": ("1f1b_full_recomp", 0),
+                  "1f1b_r50": ("1f1b_full_recomp@r50", 0),
                   "tpipe": ("tpipe", 0), "tpipe_trecomp": ("tpipe_trecomp", 0),
                   "tpipe_all": ("tpipe_trecomp", ms),
                   # ladder rungs without recompute (R28): model-state T-Offload, activation
@@ -388,7 +393,7 @@ def run_capacity(args):
     import synth
     p, m, budget = CAP_P, CAP_M, CAP_BUDGET_GIB * 2 ** 30
     best = capacity_plans()
-    names = ("1f1b", "1f1b_full_recomp", "tpipe", "tpipe_trecomp", "tpipe_all", "tpipe_offload",
+    names = ("1f1b", "1f1b_full_recomp", "1f1b_r50", "tpipe", "tpipe_trecomp", "tpipe_all", "tpipe_offload",
              "tpipe_actoff", "tpipe_actoff_offload", "interleave", "interleave_trecomp", "tpipe_all_v3",
              "tpipe_offload_v3")
     only = os.environ.get("TPIPE_CAPACITY_ONLY")
@@ -1029,6 +1034,10 @@ def run_tpipe(args):
             if st in comp:
                 continue
             comp[st] = quick_measure(st, N, m, dtok, dtgt, args)
+        # the paper's 1F1B + R50 baseline (R33): half of each stage's layers
+        # recomputed layer-wise in the backward
+        comp["1f1b_r50"] = quick_measure("1f1b_full_recomp", N, m, dtok, dtgt, args,
+                                         recomp_layers=max(1, c["n_layers"] // max(N, 1) // 2))
         # partial T-Recomp (R25): half of chunk 1's layers regenerated
         r_half = max(1, plan.layers_chunk[0] // 2)
         comp[f"tpipe_trecomp_r{r_half}"] = quick_measure("tpipe_trecomp", N, m, dtok, dtgt, args,

@@ -114,7 +114,10 @@ typedef struct {
                               from F to B. 0 = all n1 layers (block-wise T-Recomp).
                               Must be <= n1. With strategy -1 (auto) and 0 here, the
                               escalation tries r = 1..n1 at each rung (DESIGN R25);
-                              with stage_layers, stage s recomputes min(r, n1(s)) layers */
+                              with stage_layers, stage s recomputes min(r, n1(s)) layers.
+                              With TPIPE_S_1F1B_FULL_RECOMP: the shallowest r layers of each
+                              stage are recomputed layer-wise in B (r = n/2 is the paper's
+                              1F1B + R50 baseline; DESIGN R33); 0 = all (full) */
     int32_t stage_layers[64]; /* cost-balanced partition (SURVEY D-12, DESIGN R27): transformer
                               layers held by stage s (chunk split ceil/floor of n(s)/2 at
                               v = 2); all zero = uniform n_layers / n_stages. When set: the

@@ -138,8 +138,11 @@ def n_partials(M: int) -> int:
     return -(-M // 16)
 
 
-def sizes(d: ModelDesc, p: int, v: int, s: int, c: int, full_recomp: bool = False):
-    """Byte model per (stage, chunk), DESIGN.md §4."""
+def sizes(d: ModelDesc, p: int, v: int, s: int, c: int, full_recomp: bool = False,
+          ckpt_layers: int = 0):
+    """Byte model per (stage, chunk), DESIGN.md §4. full_recomp: 1F1B +
+    layer-grouped recompute of the `ckpt_layers` shallowest layers (0 = all;
+    n/2 = 1F1B + R50; DESIGN R33): those keep only their input."""
     M, h, a, f, V, es = d.tokens, d.hidden, d.n_heads, d.ffn_hidden, d.vocab, d.es
     n = layers_per_chunk(d, p, v, s)[c - 1]
     act = M * h * es
@@ -149,10 +152,8 @@ def sizes(d: ModelDesc, p: int, v: int, s: int, c: int, full_recomp: bool = Fals
     LS = M * h * es + 8 * M + 3 * M * h * es + M * h * es + 4 * a * M \
         + M * h * es + 8 * M + M * f * es
     head_stash = M * h * es + 8 * M + 4 * M       # x_f, ln_f stats, CE lse
-    if full_recomp:
-        stash = n * M * h * es                   # layer inputs only
-    else:
-        stash = n * LS
+    ck = (min(ckpt_layers, n) if ckpt_layers else n) if full_recomp else 0
+    stash = ck * M * h * es + (n - ck) * LS      # checkpointed layers: their input only
     if not emb:
         stash -= act                             # layer-0 input is the IN buffer
     if head:
@@ -269,7 +270,11 @@ def build_streams(d: ModelDesc, p: int, m: int, strategy: str, k=None,
     if offload_activations and (v != 2 or trecomp):
         raise ValueError("activation offload applies to T-Pipe chunk 1 (no T-Recomp)")
     orders = S.strategy_orders(ostrat, p, m, k=k, v=v)[0]
-    sz = {(s, c): sizes(d, p, v, s, c, full_recomp=full)
+    if full and recomp_layers > max(layers_per_chunk(d, p, v, s)[0] for s in range(p)):
+        raise ValueError("recomp_layers")
+    # 1F1B + recompute: stage s recomputes min(r, n(s)) layers (0 = all)
+    sz = {(s, c): sizes(d, p, v, s, c, full_recomp=full,
+                        ckpt_layers=min(recomp_layers, layers_per_chunk(d, p, v, s)[0]) if full else 0)
           for s in range(p) for c in range(1, v + 1)}
     keep1, rec1 = {}, {}
     if trecomp:

@@ -70,8 +70,10 @@ static uint64_t layer_stash_bytes(const tpipe_model_desc& d) {
     return M * h * es + 8 * M + 3 * M * h * es + M * h * es + 4 * a * M + M * h * es + 8 * M + M * f * es;
 }
 
+// full_recomp: 1F1B + layer-grouped recompute of the ckpt (<= n, 0 = all)
+// shallowest layers of the chunk (DESIGN R33)
 static ChunkSizes chunk_sizes(const tpipe_model_desc& d, int p, int v, const int* layers, int s,
-                              int c, bool full_recomp) {
+                              int c, bool full_recomp, int ckpt = 0) {
     const uint64_t M = (uint64_t)d.micro_batch * d.seq_len, h = d.hidden, a = d.n_heads,
                    f = d.ffn_hidden, V = d.vocab, es = d.dtype == TPIPE_BF16 ? 2 : 4;
     const uint64_t n = layers[c - 1];
@@ -82,7 +84,8 @@ static ChunkSizes chunk_sizes(const tpipe_model_desc& d, int p, int v, const int
     z.has_output = !head;
     const uint64_t LS = layer_stash_bytes(d);
     const uint64_t head_stash = M * h * es + 8 * M + 4 * M;   // x_f, ln_f stats, CE lse
-    uint64_t stash = full_recomp ? n * M * h * es : n * LS;
+    const uint64_t ck = full_recomp ? (ckpt > 0 && (uint64_t)ckpt < n ? (uint64_t)ckpt : n) : 0;
+    uint64_t stash = ck * M * h * es + (n - ck) * LS;
     if (!emb) stash -= z.act;
     if (head) stash += head_stash;
     z.stash = stash;
@@ -336,7 +339,7 @@ static int build(tpipe_plan* P, bool trecomp, bool full_recomp) {
         if (s == p - 1) B.bufs.push_back({TPIPE_BUF_STATIC, TPIPE_CAT_IO, 0, 1, 4ull * m * M + 4ull * m});
 
         ChunkSizes z[5];
-        for (int c = 1; c <= v; ++c) z[c] = chunk_sizes(d, p, v, P->sl[s].data(), s, c, full_recomp);
+        for (int c = 1; c <= v; ++c) z[c] = chunk_sizes(d, p, v, P->sl[s].data(), s, c, full_recomp, P->rl_of(s));
         // partial T-Recomp (R25): layers 1..r of chunk 1 are regenerated by R (TSTASH during
         // F, RBUF from R to B); the stash of layers r+1..n1 is kept from F to B (STASH).
         // The two parts add up to the full chunk-1 stash.
@@ -688,7 +691,7 @@ static double head_fwd_s(const tpipe_model_desc& d, const CostModel& cm) {
 static double op_seconds(const tpipe_plan* P, int s, int kind, int c, double tl, double th) {
     if (kind == KR) return P->rl_of(s) * tl;
     const double f = P->sl[s][c - 1] * tl + ((s == P->p - 1 && c == P->v) ? th : 0.0);
-    if (kind == KB) return 2.0 * f + (P->strategy == TPIPE_S_1F1B_FULL_RECOMP ? P->sl[s][c - 1] * tl : 0.0);
+    if (kind == KB) return 2.0 * f + (P->strategy == TPIPE_S_1F1B_FULL_RECOMP ? P->rl_of(s) * tl : 0.0);
     return f;
 }
 
@@ -857,7 +860,14 @@ static int make_plan(const tpipe_model_desc* model, int p, int m, int strategy, 
         return set_error(TPIPE_E_INVALID, "recomp_layers %d exceeds the %d chunk-1 layers per stage",
                          recomp_layers, n1max);
     }
-    P->rl = trecomp ? (recomp_layers > 0 ? recomp_layers : n1max) : 0;
+    const bool full_rc = strategy == TPIPE_S_1F1B_FULL_RECOMP;
+    if (full_rc && recomp_layers > n1max) {
+        delete P;
+        return set_error(TPIPE_E_INVALID, "recomp_layers %d exceeds the %d layers per stage", recomp_layers, n1max);
+    }
+    // T-Recomp: chunk-1 layers R regenerates; 1F1B + recompute: layers per stage
+    // recomputed layer-wise in B, shallowest first (R33; 0 = all)
+    P->rl = (trecomp || full_rc) ? (recomp_layers > 0 ? recomp_layers : n1max) : 0;
     // App. B's delay rounds are derived for two chunks; v > 2 runs undelayed (R32)
     P->k = (trecomp && !is_il) ? (k < 0 ? (P->v == 2 ? delay_rounds_appB(p) : 0) : k) : 0;
     if (is_il) {
@@ -1233,10 +1243,12 @@ TP_API int tpipe_plan_chunk_params(const tpipe_plan* P, int32_t s, int32_t c, ui
 TP_API int tpipe_plan_simulate(const tpipe_plan* P, tpipe_sim_report* out) {
     if (!P || !out) return set_error(TPIPE_E_INVALID, "NULL argument");
     const int v = P->v;
-    auto dur = [&](int, int, int kind) -> int64_t {
-        if (v == 2) return kind == KB ? 2 : 1;
+    auto dur = [&](int s, int, int kind) -> int64_t {
+        if (v >= 2) return kind == KB ? 2 : 1;
         if (kind == KF) return 2;
-        return P->strategy == TPIPE_S_1F1B_FULL_RECOMP ? 6 : 4;
+        if (P->strategy != TPIPE_S_1F1B_FULL_RECOMP) return 4;
+        const int n = P->sl[s][0];   // + 2 units per recomputed fraction of the stage's layers (R50: 5)
+        return 4 + (2 * P->rl_of(s) + n / 2) / n;
     };
     int64_t mk = 0;
     int rc = replay_order<int64_t>(P, dur, &mk, out->busy);

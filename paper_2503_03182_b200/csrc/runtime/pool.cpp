@@ -5,6 +5,7 @@
 namespace tpipe {
 
 static constexpr size_t ALIGN = 256;
+static constexpr unsigned char CANARY_BYTE = 0xA7;
 
 int Pool::init(size_t bytes, int n_stages) {
     release();
@@ -23,6 +24,64 @@ int Pool::init(size_t bytes, int n_stages) {
     return 0;
 }
 
+int Pool::init_planned(const std::vector<PoolItem>& items, int n_stages, bool canary) {
+    release();
+    cur_.assign(n_stages, 0);
+    hw_.assign(n_stages, 0);
+    limit_.assign(n_stages, 0);
+    canary_ = canary;
+    const size_t n = items.size();
+    std::vector<size_t> size(n), order(n);
+    for (size_t i = 0; i < n; ++i) {
+        const uint64_t phys = items[i].bytes + (canary ? CANARY : 0);
+        size[i] = std::max<size_t>(ALIGN, (phys + ALIGN - 1) / ALIGN * ALIGN);
+        order[i] = i;
+    }
+    std::sort(order.begin(), order.end(), [&](size_t x, size_t y) {
+        if (size[x] != size[y]) return size[x] > size[y];
+        if (items[x].first != items[y].first) return items[x].first < items[y].first;
+        return x < y;
+    });
+    planned_off_.assign(n, 0);
+    std::vector<size_t> placed;
+    size_t top = 0;
+    for (size_t id : order) {
+        std::vector<std::pair<size_t, size_t>> busy;   // (offset, size) of lifetime-overlapping buffers
+        for (size_t q : placed)
+            if (!(items[q].last < items[id].first || items[id].last < items[q].first))
+                busy.push_back({planned_off_[q], size[q]});
+        std::sort(busy.begin(), busy.end());
+        size_t cand = 0;
+        for (auto& b : busy) {
+            if (cand + size[id] <= b.first) break;
+            cand = std::max(cand, b.first + b.second);
+        }
+        planned_off_[id] = cand;
+        top = std::max(top, cand + size[id]);
+        placed.push_back(id);
+    }
+    if (top) {
+        if (cudaMalloc(&base_, top) != cudaSuccess) {
+            base_ = nullptr;
+            return -1;
+        }
+        cap_ = top;
+    }
+    return 0;
+}
+
+void* Pool::alloc_id(int stage, int id, uint64_t bytes) {
+    if (id < 0 || (size_t)id >= planned_off_.size() || !base_) return nullptr;
+    void* p = base_ + planned_off_[id];
+    req_[p] = bytes;
+    used_[p] = {planned_off_[id], 0};
+    if (canary_) cudaMemsetAsync((char*)p + bytes, CANARY_BYTE, CANARY, canary_st_);
+    cur_[stage] += bytes;
+    hw_[stage] = std::max(hw_[stage], cur_[stage]);
+    if (limit_[stage] && cur_[stage] > limit_[stage]) over_cap_ = true;
+    return p;
+}
+
 void Pool::release() {
     if (base_) cudaFree(base_);
     for (void* p : overflow_) cudaFree(p);
@@ -30,12 +89,12 @@ void Pool::release() {
     cap_ = 0;
     overflow_.clear();
     overflow_bytes_ = 0;
+    planned_off_.clear();
     free_.clear();
     used_.clear();
     req_.clear();
 }
 
-static constexpr unsigned char CANARY_BYTE = 0xA7;
 
 void* Pool::alloc(int stage, uint64_t bytes) {
     last_fail_phys_ = false;
@@ -79,6 +138,7 @@ void Pool::free(int stage, void* p) {
     used_.erase(it);
     cur_[stage] -= req_[p];
     req_.erase(p);
+    if (!planned_off_.empty()) return;   // planned mode: addresses are fixed, nothing to merge
     if (off == SIZE_MAX) {
         cudaFree(p);
         overflow_.erase(std::find(overflow_.begin(), overflow_.end(), p));

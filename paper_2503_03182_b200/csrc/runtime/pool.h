@@ -1,10 +1,16 @@
 // HBM pool with exact live-byte accounting.
 //
-// One cudaMalloc arena carved best-fit at 256-byte granularity. The ledger
+// One cudaMalloc arena per stage. Planned mode (what the runtime uses): the
+// plan fixes every buffer's lifetime (allocating and releasing instruction),
+// so the arena layout is computed once at runtime creation — greedy by size,
+// each buffer at the lowest 256-byte-aligned offset not overlapping any
+// placed buffer whose lifetime intersects its own — and the arena is exactly
+// as large as that layout: no fragmentation at run time, deterministic
+// addresses. (Dynamic best-fit mode remains for standalone use.) The ledger
 // counts the REQUESTED bytes of every live allocation per stage, at the
 // instruction boundaries the plan prescribes, so its high-water equals the
 // plan's (and the oracle's) per-stage peak exactly; alignment padding and
-// fragmentation show up only in the physical `reserved` figure.
+// packing slack show up only in the physical `reserved` figure.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -16,10 +22,19 @@
 
 namespace tpipe {
 
+struct PoolItem {
+    uint64_t bytes;   // requested
+    int first, last;  // live from instruction `first` (start) to `last` (end), inclusive
+};
+
 class Pool {
 public:
     ~Pool() { release(); }
     int init(size_t bytes, int n_stages);
+    // planned mode: lay out `items` (indexed by buffer id) and allocate the arena
+    int init_planned(const std::vector<PoolItem>& items, int n_stages, bool canary);
+    // planned mode: the buffer `id`'s fixed address (ledger updated)
+    void* alloc_id(int stage, int id, uint64_t bytes);
     void release();
     // returns nullptr on failure; `cap` (0 = none) bounds the stage's ledger
     void* alloc(int stage, uint64_t bytes);
@@ -59,6 +74,7 @@ private:
     std::vector<void*> overflow_;
     size_t overflow_bytes_ = 0;
     std::vector<uint64_t> cur_, hw_, limit_;
+    std::vector<size_t> planned_off_;
     bool over_cap_ = false;
     size_t phys_limit_ = 0;
     bool last_fail_phys_ = false;

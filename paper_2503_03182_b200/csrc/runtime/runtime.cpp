@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <limits>
 #include <map>
 #include <memory>
 #include <new>
@@ -313,7 +314,7 @@ int exec_op(tpipe_runtime* rt, StageState& S, const tpipe_op& op, uint32_t flags
     // allocations at instruction start
     for (int e = 0; e < op.n_alloc; ++e) {
         const int id = ev[op.alloc_first + e];
-        void* ptr = pool.alloc(s, bufs[id].bytes);
+        void* ptr = pool.alloc_id(s, id, bufs[id].bytes);
         if (!ptr && pool.last_fail_physical())
             return set_error(TPIPE_E_OOM, "stage %d: pool fragmentation would place %llu bytes beyond the "
                              "HBM budget (arena %zu + overflow %zu)", s, (unsigned long long)bufs[id].bytes,
@@ -718,7 +719,7 @@ int check_layouts(const tpipe_plan& P, const std::vector<int>& owned) {
                     continue;
                 const int c = b.chunk;
                 const bool emb = (s == 0 && c == 1), head = (s == P.p - 1 && c == P.v);
-                const StashLayout SL = make_stash_layout(P.model, P.sl[s][c - 1], emb, head, full);
+                const StashLayout SL = make_stash_layout(P.model, P.sl[s][c - 1], emb, head, full, P.rl_of(s));
                 const int split = (trecomp && c == 1 && P.rl_of(s) < P.sl[s][0]) ? P.rl_of(s) : 0;
                 const uint64_t front = split ? (uint64_t)SL.layer[split].x_in : (uint64_t)SL.total;
                 uint64_t want = 0;
@@ -799,10 +800,20 @@ TP_API int tpipe_runtime_create(const tpipe_plan* plan, const tpipe_runtime_opts
         S->s = s;
         // one pool (arena) per stage: a block freed by one stage is never handed
         // to another stage's stream
-        const uint64_t need = P.peak[s].total_peak;
+        // planned arena: every buffer's lifetime is fixed by the plan, so the
+        // layout is computed once (pool.h) and nothing fragments at run time
+        std::vector<PoolItem> items(P.bufs[s].size());
+        for (size_t id = 0; id < items.size(); ++id)
+            items[id] = {P.bufs[s][id].bytes, -1, std::numeric_limits<int>::max()};
+        for (size_t j = 0; j < P.ops[s].size(); ++j) {
+            const tpipe_op& op = P.ops[s][j];
+            for (int e = 0; e < op.n_alloc; ++e) items[P.events[s][op.alloc_first + e]].first = (int)j;
+            for (int e = 0; e < op.n_free; ++e) items[P.events[s][op.free_first + e]].last = (int)j;
+        }
         S->pool.reset(new Pool);
-        if (S->pool->init((size_t)(need * 1.08) + (256ull << 20), P.p))
-            return set_error(TPIPE_E_CUDA, "pool: cudaMalloc of %llu bytes failed", (unsigned long long)need);
+        if (S->pool->init_planned(items, P.p, (o.debug_flags & TPIPE_DEBUG_POOL_CANARY) != 0))
+            return set_error(TPIPE_E_CUDA, "pool: cudaMalloc of the planned arena failed (plan peak %llu bytes)",
+                             (unsigned long long)P.peak[s].total_peak);
         if (P.hbm_budget) S->pool->set_phys_limit((size_t)P.hbm_budget);
         S->pool->set_cap(s, o.pool_cap ? o.pool_cap : P.peak[s].total_peak);
         S->pool->set_canary((o.debug_flags & TPIPE_DEBUG_POOL_CANARY) != 0, rt->stream);
@@ -816,7 +827,7 @@ TP_API int tpipe_runtime_create(const tpipe_plan* plan, const tpipe_runtime_opts
         for (size_t id = 0; id < P.bufs[s].size(); ++id) {
             const tpipe_buf& b = P.bufs[s][id];
             if (b.role != TPIPE_BUF_STATIC) continue;
-            void* ptr = S->pool->alloc(s, b.bytes);
+            void* ptr = S->pool->alloc_id(s, (int)id, b.bytes);
             if (!ptr) return set_error(TPIPE_E_CUDA, "pool: static allocation failed");
             S->bufptr[id] = ptr;
             CU(cudaMemset(ptr, 0, b.bytes));
@@ -826,7 +837,7 @@ TP_API int tpipe_runtime_create(const tpipe_plan* plan, const tpipe_runtime_opts
                 const bool emb = (s == 0 && c == 1), head = (s == P.p - 1 && c == P.v);
                 C.lay = make_param_layout(P.model, P.sl[s][c - 1], emb, head);
                 C.sl = make_stash_layout(P.model, P.sl[s][c - 1], emb, head,
-                                         P.strategy == TPIPE_S_1F1B_FULL_RECOMP);
+                                         P.strategy == TPIPE_S_1F1B_FULL_RECOMP, P.rl_of(s));
                 C.P = C.lay.total;
                 if ((uint64_t)C.P != P.chunk_params[s][c - 1])
                     return set_error(TPIPE_E_STATE, "param layout mismatch");

@@ -66,9 +66,13 @@ ParamLayout make_param_layout(const tpipe_model_desc& d, int n_layers, bool emb,
 }
 
 StashLayout make_stash_layout(const tpipe_model_desc& d, int n_layers, bool emb, bool head,
-                              bool ckpt_only) {
+                              bool ckpt_only, int ckpt_layers) {
+    // layer-grouped recompute (1F1B + recompute): layers [0, ck) keep only
+    // their input (checkpoint), the deeper ones their full stash (DESIGN R33)
+    const int ck = !ckpt_only ? 0 : (ckpt_layers > 0 && ckpt_layers < n_layers ? ckpt_layers : n_layers);
     StashLayout S;
-    S.ckpt_only = ckpt_only;
+    S.ckpt_only = ck > 0;
+    S.ckpt_layers = ck;
     const long M = (long)d.micro_batch * d.seq_len, h = d.hidden, a = d.n_heads, f = d.ffn_hidden;
     const long es = d.dtype == TPIPE_BF16 ? 2 : 4;
     long off = 0;
@@ -88,37 +92,10 @@ StashLayout make_stash_layout(const tpipe_model_desc& d, int n_layers, bool emb,
         L.ln2_rstd = take(4 * M);
         L.u = take(M * f * es);
     };
-    if (ckpt_only) {
-        for (int l = 0; l < n_layers; ++l) {
-            StashLayout::L L{};
-            L.x_in = (l == 0 && !emb) ? -1 : take(M * h * es);
-            S.layer.push_back(L);
-        }
-        if (head) {
-            S.x_f = take(M * h * es);
-            S.lnf_mean = take(4 * M);
-            S.lnf_rstd = take(4 * M);
-            S.ce_lse = take(4 * M);
-        }
-        S.total = off;
-        off = 0;
-        S.scratch.x_in = -1;
-        internals(S.scratch);
-        S.scratch_bytes = off;
-        return S;
-    }
     for (int l = 0; l < n_layers; ++l) {
-        StashLayout::L L;
+        StashLayout::L L{};
         L.x_in = (l == 0 && !emb) ? -1 : take(M * h * es);
-        L.ln1_mean = take(4 * M);
-        L.ln1_rstd = take(4 * M);
-        L.qkv = take(3 * M * h * es);
-        L.o = take(M * h * es);
-        L.lse = take(4 * a * M);
-        L.x_mid = take(M * h * es);
-        L.ln2_mean = take(4 * M);
-        L.ln2_rstd = take(4 * M);
-        L.u = take(M * f * es);
+        if (l >= ck) internals(L);
         S.layer.push_back(L);
     }
     if (head) {
@@ -128,6 +105,12 @@ StashLayout make_stash_layout(const tpipe_model_desc& d, int n_layers, bool emb,
         S.ce_lse = take(4 * M);
     }
     S.total = off;
+    if (ck > 0) {
+        off = 0;
+        S.scratch.x_in = -1;
+        internals(S.scratch);
+        S.scratch_bytes = off;
+    }
     return S;
 }
 
@@ -555,7 +538,7 @@ int chunk_forward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P,
         }
     const int n_run = a.n_run > 0 ? a.n_run : n;
     for (int l = 0; l < n_run; ++l) {
-        LayerPtrs lp = SL.ckpt_only ? scratch_ptrs(SL, l, a.stash, a.in, scratch)
+        LayerPtrs lp = l < SL.ckpt_layers ? scratch_ptrs(SL, l, a.stash, a.in, scratch)
                                     : layer_ptrs(SL.layer[l], stash_base(SL, a.stash, a.stash2, a.split, l), a.in);
         void* out;
         if (l + 1 < n_run) out = stash_base(SL, a.stash, a.stash2, a.split, l + 1) + SL.layer[l + 1].x_in;
@@ -651,7 +634,7 @@ int chunk_backward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P
     }
     for (int l = n - 1; l >= 0; --l) {
         LayerPtrs lp;
-        if (SL.ckpt_only) {
+        if (l < SL.ckpt_layers) {
             // layer-grouped just-in-time recompute (1F1B + full recompute):
             // regenerate this layer's internals from its checkpoint, output discarded
             lp = scratch_ptrs(SL, l, a.stash, a.in, w.rbuf);

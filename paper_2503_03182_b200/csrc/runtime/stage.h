@@ -38,12 +38,15 @@ struct StashLayout {
     // 1F1B + full recompute: the stash keeps only layer inputs (checkpoints);
     // one layer's internals live in a scratch (offsets relative to its base)
     bool ckpt_only = false;
+    int ckpt_layers = 0;    // layers [0, ckpt_layers) are checkpoint-only (recomputed in B)
     L scratch{};
     long scratch_bytes = 0;
 };
 
+// ckpt_only: 1F1B + layer-grouped recompute; ckpt_layers = how many of the
+// shallowest layers are checkpoint-only (0 = all of them)
 StashLayout make_stash_layout(const tpipe_model_desc& d, int n_layers, bool emb, bool head,
-                              bool ckpt_only = false);
+                              bool ckpt_only = false, int ckpt_layers = 0);
 
 struct Dims {
     int dtype, M, h, a, hd, f, V, s, b, es;

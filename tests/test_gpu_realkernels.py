@@ -285,3 +285,31 @@ def test_planned_arena_close_to_peak(strategy, offload, p):
     assert st["pool_overflow_bytes"] == 0
     assert peak <= st["pool_reserved"] <= 1.12 * peak + p * (1 << 20), (st["pool_reserved"], peak)
     rt.close()
+
+
+@pytest.mark.parametrize("r", [1, 2])
+def test_1f1b_partial_recompute_step(r):
+    """1F1B + layer-grouped recompute of r of the stage's layers (r = 2 of 4:
+    1F1B + R50; DESIGN R33): fp32 gradients vs the oracle; bf16
+    gradients and updated parameters bit-identical to plain 1F1B (the
+    recomputed layers regenerate the same values with the same kernels)."""
+    P, RT, PR = mods()
+    cfg, p, m = dict(C1_16, L=8), 2, 4
+    W = synth.weights(cfg["L"], cfg["h"], cfg["f"], cfg["V"], cfg["s"], seed=11, std=0.05,
+                      bias_std=0.02, ln_jitter=0.05)
+    tok, tgt = synth.tokens(cfg["V"], m, cfg["b"], cfg["s"], step=0)
+    lref, G = R.step_grads(R.to64(W), tok, tgt, cfg["a"])
+    md = P.Model(cfg["L"], cfg["h"], cfg["a"], cfg["f"], cfg["V"], cfg["s"], cfg["b"], 0)
+    plan = P.Plan(md, p, m, strategy="1f1b_full_recomp", recomp_layers=r)
+    rt = RT.Runtime(plan, stage=-1)
+    for s in range(p):
+        rt.set_params(s, 1, PR.pack(W, p, 1, plan.partition, s, 1))
+    rt.step(tok, tgt, RT.STEP_NO_OPT)
+    for s in range(p):
+        for (k, l), g in PR.unpack(rt.get_grads(s, 1), W, p, 1, plan.partition, s, 1).items():
+            ref = G["layers"][l][k] if l is not None else G[k]
+            assert max_rel(g, ref) <= 1e-4, (s, k, l)
+    assert all(rt.stats()["pool_high_water"][s] == plan.peak(s)["total_peak"] for s in range(p))
+    rt.close()
+    ref = _run(dict(cfg), p, m, "1f1b")
+    _assert_same(ref, _run(dict(cfg), p, m, "1f1b_full_recomp", recomp_layers=r), ("1f1b_r", r))

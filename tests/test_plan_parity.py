@@ -449,3 +449,35 @@ def test_dp_zero1_streams_match_oracle(strategy, p, dp, dtype):
     if strategy.startswith("tpipe"):
         with pytest.raises(TPipeError, match="ZeRO-1"):
             P.Plan(pd, p, m, strategy=strategy, dp=dp, offload=P.OFFLOAD_MODEL_STATE)
+
+
+@pytest.mark.parametrize("p,r", [(1, 1), (1, 2), (2, 1), (2, 2), (4, 1), (4, 2), (8, 1)])
+@pytest.mark.parametrize("dtype", [T.BF16, T.FP32])
+def test_1f1b_partial_recompute_matches_oracle(p, r, dtype):
+    """1F1B + layer-grouped recompute of the r shallowest layers per stage
+    (r = n/2: the paper's 1F1B + R50 baseline; DESIGN R33): streams
+    and bytes equal the oracle's, the stash follows r inputs + (n - r) full
+    layers, and the unit replay of R50 takes 7(m+p-1) (D-5)."""
+    P = _plan_mod()
+    L = 4 * p
+    m = 2 * p + 2
+    od = T.ModelDesc(L, 64, 4, 256, 128, 32, 2, dtype)
+    pd = P.Model(L, 64, 4, 256, 128, 32, 2, dtype)
+    plan = P.Plan(pd, p, m, strategy="1f1b_full_recomp", recomp_layers=r)
+    assert plan.recomp_layers == r
+    st, static = T.build_streams(od, p, m, "1f1b_full_recomp", recomp_layers=r)
+    for s in range(p):
+        got, bufs = plan.ops(s)
+        strip = [{k: o[k] for k in ("kind", "chunk", "mb", "peer", "channel", "msg")} for o in got]
+        assert strip == oracle_ops(st[s])
+        rep = T.replay(st[s], static[s])
+        pk = plan.peak(s)
+        for cat in ("model_state", "io", "act", "recomp_buf", "comm", "workspace"):
+            assert pk[cat] == rep.get(cat, 0), cat
+    z = T.sizes(od, p, 1, min(1, p - 1), 1, full_recomp=True, ckpt_layers=r)
+    full = T.sizes(od, p, 1, min(1, p - 1), 1)
+    es = 2 if dtype == T.BF16 else 4
+    M, h = 64, 64
+    assert z["stash"] == full["stash"] - r * (full["layer_stash"] - M * h * es)
+    if r * 2 == L // p:
+        assert plan.simulate()[0] == 7 * (m + p - 1)
