@@ -106,12 +106,6 @@ int tpipe_k_attn_bwd(int dtype, const void* qkv, const void* o, const void* dout
                      const float* lse, void* dqkv, float* ws,
                      int b, int s, int a, int d, void* stream);
 
-/* Same contracts as tpipe_k_attn_fwd / _bwd (bf16, head_dim 64/128 only), on
- * the legacy mma.sync tensor path instead of tcgen05 (A/B measurements). */
-int tpipe_k_attn_fwd_mma(const void* qkv, void* o, float* lse, int b, int s, int a, int d,
-                         void* stream);
-int tpipe_k_attn_bwd_mma(const void* qkv, const void* o, const void* dout, const float* lse,
-                         void* dqkv, float* ws, int b, int s, int a, int d, void* stream);
 
 /* Embedding: x[r] = wte[tok[r]] + wpe[r mod s]; tok int32 [rows]. */
 int tpipe_k_embed_fwd(int dtype, const int* tok, const void* wte, const void* wpe,

@@ -53,8 +53,6 @@ def _declare(L):
     L.tpipe_k_ln_bwd_rsum.argtypes = [i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp]
     L.tpipe_k_attn_fwd.argtypes = [i32, vp, vp, vp, i32, i32, i32, i32, vp]
     L.tpipe_k_attn_bwd.argtypes = [i32, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, vp]
-    L.tpipe_k_attn_fwd_mma.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp]
-    L.tpipe_k_attn_bwd_mma.argtypes = [vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, vp]
     L.tpipe_k_embed_fwd.argtypes = [i32, vp, vp, vp, vp, i32, i32, i32, vp]
     L.tpipe_k_embed_bwd.argtypes = [i32, vp, vp, vp, vp, vp, i32, i32, i32, vp]
     L.tpipe_k_ce_fwd.argtypes = [vp, vp, vp, vp, f32, i32, i32, vp]

@@ -198,12 +198,8 @@ int attn_bwd_simt(int dtype, const void* qkv, const void* o, const void* dout, c
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
-// Dispatch: tensor-core kernels (attn_tc.cu) for bf16 with head_dim 64/128,
+// Dispatch: tcgen05 kernels (attn_tc5.cu) for bf16 with head_dim 64/128,
 // SIMT otherwise.
-int attn_fwd_tc(const void* qkv, void* o, float* lse, int b, int s, int a, int d, cudaStream_t st);
-int attn_bwd_tc(const void* qkv, const void* o, const void* dout, const float* lse, void* dqkv,
-                float* ws, int b, int s, int a, int d, cudaStream_t st);
-
 int attn_fwd_tc5(const void* qkv, void* o, float* lse, int b, int s, int a, int d, cudaStream_t st);
 int attn_bwd_tc5(const void* qkv, const void* o, const void* dout, const float* lse, void* dqkv,
                  float* ws, int b, int s, int a, int d, cudaStream_t st);
@@ -224,15 +220,6 @@ int attn_bwd(int dtype, const void* qkv, const void* o, const void* dout, const 
     if (dtype == DT_BF16 && (d == 64 || d == 128))
         return attn_bwd_tc5(qkv, o, dout, lse, dqkv, ws, b, s, a, d, st);
     return attn_bwd_simt(dtype, qkv, o, dout, lse, dqkv, ws, b, s, a, d, st);
-}
-
-// legacy mma.sync path, kept callable for A/B measurements (tpipe_k_attn_*_mma)
-int attn_fwd_mma(const void* qkv, void* o, float* lse, int b, int s, int a, int d, cudaStream_t st) {
-    return attn_fwd_tc(qkv, o, lse, b, s, a, d, st);
-}
-int attn_bwd_mma(const void* qkv, const void* o, const void* dout, const float* lse, void* dqkv,
-                 float* ws, int b, int s, int a, int d, cudaStream_t st) {
-    return attn_bwd_tc(qkv, o, dout, lse, dqkv, ws, b, s, a, d, st);
 }
 
 }  // namespace tpipe

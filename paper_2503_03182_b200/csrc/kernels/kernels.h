@@ -83,10 +83,6 @@ int attn_fwd(int dtype, const void* qkv, void* o, float* lse, int b, int s, int 
 int attn_bwd(int dtype, const void* qkv, const void* o, const void* dout, const float* lse,
              void* dqkv, float* ws, int b, int s, int a, int d, cudaStream_t st);
 
-// legacy mma.sync (FA2-structure) tensor-core path, for A/B comparison
-int attn_fwd_mma(const void* qkv, void* o, float* lse, int b, int s, int a, int d, cudaStream_t st);
-int attn_bwd_mma(const void* qkv, const void* o, const void* dout, const float* lse, void* dqkv,
-                 float* ws, int b, int s, int a, int d, cudaStream_t st);
 
 // ---------------------------------------------------------------- embedding
 // x[r] = wte[tok[r]] + wpe[r % s]

@@ -99,19 +99,6 @@ TP_API int tpipe_k_attn_bwd(int dtype, const void* qkv, const void* o, const voi
                      "attn_bwd");
 }
 
-TP_API int tpipe_k_attn_fwd_mma(const void* qkv, void* o, float* lse, int b, int s, int a, int d,
-                                void* stream) {
-    if (d != 64 && d != 128) return set_error(TPIPE_E_INVALID, "head_dim must be 64 or 128");
-    return launch_rc(attn_fwd_mma(qkv, o, lse, b, s, a, d, S(stream)), "attn_fwd_mma");
-}
-
-TP_API int tpipe_k_attn_bwd_mma(const void* qkv, const void* o, const void* dout, const float* lse,
-                                void* dqkv, float* ws, int b, int s, int a, int d, void* stream) {
-    if (d != 64 && d != 128) return set_error(TPIPE_E_INVALID, "head_dim must be 64 or 128");
-    return launch_rc(attn_bwd_mma(qkv, o, dout, lse, dqkv, ws, b, s, a, d, S(stream)),
-                     "attn_bwd_mma");
-}
-
 TP_API int tpipe_k_embed_fwd(int dtype, const int* tok, const void* wte, const void* wpe, void* x,
                              int rows, int s, int h, void* stream) {
     if (int e = chk_dtype(dtype)) return e;

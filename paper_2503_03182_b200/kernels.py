@@ -54,16 +54,6 @@ def tpipe_k_attn_bwd(dtype, qkv, o, dout, lse, dqkv, ws, b, s, a, d):
                                  a, d, _stream()), "attn_bwd")
 
 
-def tpipe_k_attn_fwd_mma(qkv, o, lse, b, s, a, d):
-    check(lib().tpipe_k_attn_fwd_mma(_p(qkv), _p(o), _p(lse), b, s, a, d, _stream()),
-          "attn_fwd_mma")
-
-
-def tpipe_k_attn_bwd_mma(qkv, o, dout, lse, dqkv, ws, b, s, a, d):
-    check(lib().tpipe_k_attn_bwd_mma(_p(qkv), _p(o), _p(dout), _p(lse), _p(dqkv), _p(ws), b, s, a,
-                                     d, _stream()), "attn_bwd_mma")
-
-
 def tpipe_k_embed_fwd(dtype, tok, wte, wpe, x, rows, s, h):
     check(lib().tpipe_k_embed_fwd(dtype, _p(tok), _p(wte), _p(wpe), _p(x), rows, s, h, _stream()),
           "embed_fwd")

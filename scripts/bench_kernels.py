@@ -60,7 +60,7 @@ for ak, bk in ((1, 1), (1, 0), (0, 0), (0, 1)):
 for o in out:
     print(json.dumps(o))
 
-# attention at the C2 / C3 shape: tcgen05 (default) vs legacy mma.sync
+# attention at the C2 / C3 shape (tcgen05)
 b, a, d = 1, h // 128, 128
 qkv = (torch.randn((b * s, 3 * h), device=dev) * 0.5).to(torch.bfloat16)
 o = torch.empty((b * s, h), device=dev, dtype=torch.bfloat16)
@@ -70,9 +70,7 @@ dqkv = torch.empty_like(qkv)
 ws = torch.empty((b, a, s), device=dev)
 ffl = 4.0 * b * a * (s * (s + 1) / 2) * d
 for name, f_fwd, f_bwd in (("tcgen05", lambda: K.tpipe_k_attn_fwd(1, qkv, o, lse, b, s, a, d),
-                            lambda: K.tpipe_k_attn_bwd(1, qkv, o, dout, lse, dqkv, ws, b, s, a, d)),
-                           ("mma", lambda: K.tpipe_k_attn_fwd_mma(qkv, o, lse, b, s, a, d),
-                            lambda: K.tpipe_k_attn_bwd_mma(qkv, o, dout, lse, dqkv, ws, b, s, a, d))):
+                            lambda: K.tpipe_k_attn_bwd(1, qkv, o, dout, lse, dqkv, ws, b, s, a, d)),):
     ms = timeit(f_fwd)
     print(json.dumps(dict(kernel=f"attn_fwd_{name}", s=s, heads=a, d=d, ms=round(ms, 4),
                           tflops=round(ffl / ms / 1e9, 1))))

@@ -350,13 +350,11 @@ def test_layernorm_bwd_rsum(dtype, rows, hd):
 
 
 # ------------------------------------------------------------------ attention
-@pytest.mark.parametrize("dtype,impl", [("fp32", "default"), ("bf16", "default"), ("bf16", "mma")])
+@pytest.mark.parametrize("dtype,impl", [("fp32", "default"), ("bf16", "default")])
 @pytest.mark.parametrize("b,s,a,d", [(2, 32, 4, 16), (1, 100, 2, 64), (1, 257, 2, 128),
                                      (2, 384, 2, 128), (3, 200, 4, 64)])
 def test_attention(dtype, impl, b, s, a, d):
-    """bf16 d=64/128 'default' = tcgen05/TMEM kernels; 'mma' = legacy mma.sync."""
-    if impl == "mma" and d not in (64, 128):
-        pytest.skip("mma path is d=64/128 only")
+    """bf16 d=64/128 = tcgen05/TMEM kernels; other d and fp32 = the SIMT kernels."""
     dt = 1 if dtype == "bf16" else 0
     hdim = a * d
     rng = np.random.default_rng(s + d)
@@ -365,10 +363,7 @@ def test_attention(dtype, impl, b, s, a, d):
     o = torch.empty((b * s, hdim), device=dev, dtype=qkv.dtype)
     lse = torch.empty((b, a, s), device=dev)
     k = K()
-    if impl == "mma":
-        k.tpipe_k_attn_fwd_mma(qkv, o, lse, b, s, a, d)
-    else:
-        k.tpipe_k_attn_fwd(dt, qkv, o, lse, b, s, a, d)
+    k.tpipe_k_attn_fwd(dt, qkv, o, lse, b, s, a, d)
     Q = h(qkv).reshape(b, s, 3 * hdim)
     q = R.split_heads(Q[..., :hdim], a)
     kk = R.split_heads(Q[..., hdim:2 * hdim], a)
@@ -376,10 +371,7 @@ def test_attention(dtype, impl, b, s, a, d):
     Oref, cache, lref = R.attn_fwd(q, kk, v)
     dqkv = torch.empty_like(qkv)
     ws = torch.empty((b, a, s), device=dev)
-    if impl == "mma":
-        k.tpipe_k_attn_bwd_mma(qkv, o, dout, lse, dqkv, ws, b, s, a, d)
-    else:
-        k.tpipe_k_attn_bwd(dt, qkv, o, dout, lse, dqkv, ws, b, s, a, d)
+    k.tpipe_k_attn_bwd(dt, qkv, o, dout, lse, dqkv, ws, b, s, a, d)
     torch.cuda.synchronize()
     dQ, dK, dV = R.attn_bwd(R.split_heads(h(dout).reshape(b, s, hdim), a), cache)
     tol, metric = (2e-2, rel_l2) if dtype == "bf16" else (1e-4, max_rel)
