@@ -65,6 +65,8 @@ void tpipe_k_gemm_set_stream_k(int on);
  * computes a 256 x 256 tile with tcgen05.mma.cta_group::2, each CTA staging
  * half of the A and B operands. Used when the shape yields >= 32 such tiles. */
 void tpipe_k_gemm_set_pair(int on);
+/* CTA-pair 256 x 256 tiles once a GEMM has >= n of them (default 96; A/B knob) */
+void tpipe_k_gemm_set_pair_min_tiles(int n);
 
 /* Enable (1) or disable (0, default) 256 x 512 CTA-pair tiles (two N = 256
  * tcgen05.mma per K step sharing the A stage; one TMEM accumulator): fewer

@@ -255,6 +255,9 @@ static bool g_pair_enabled = true;
 static bool g_wide_enabled = false;
 void gemm_set_stream_k(int on) { g_stream_k_enabled = on != 0; }
 void gemm_set_pair(int on) { g_pair_enabled = on != 0; }
+// CTA-pair tiles from this many 256 x 256 tiles on (measured crossover, see gemm_tc)
+static int g_pair_min_tiles = 96;
+void gemm_set_pair_min_tiles(int n) { g_pair_min_tiles = n > 0 ? n : 96; }
 void gemm_set_wide(int on) { g_wide_enabled = on != 0; }
 
 // CG = 1: one CTA computes a 128 x BN tile. CG = 2: a CTA pair (cluster of 2
@@ -950,7 +953,7 @@ int gemm_tc(const GemmDesc& g, cudaStream_t st) {
     // loop is long (>= 4096); a 2048 x 2048 x 2048 GEMM (64 pair tiles on 74
     // pairs) is faster as 128 single-CTA tiles.
     const long pair_tiles = (long)((g.M + 255) / 256) * ((g.N + 255) / 256);
-    if (g_pair_enabled && (pair_tiles >= 96 || (pair_tiles >= 32 && g.K >= 4096))) {
+    if (g_pair_enabled && (pair_tiles >= g_pair_min_tiles || (pair_tiles >= 32 && g.K >= 4096))) {
         // 256 x 512 pair tiles when they fill the 74 pairs' waves as well as
         // 256 x 256 does (same wave efficiency, half the tiles)
         const long units = num_sms() / 2;
