@@ -826,6 +826,14 @@ def latest_capacity_claim():
     s = (f"{fb}: largest executed model {best['params_B']}B params = {best['params_vs_1f1b']}x 1F1B's at "
          f"{best['model_tflops_vs_1f1b']}x its model TFLOP/s ({best['plan_strategy']}, "
          f"chunks={best.get('chunks', 2)}, offload={best.get('offload', 0)})")
+    # against the paper's 1F1B + R50 baseline, within one capacity file
+    for f in sorted({x[0] for x in runs}):
+        r50 = next((r for ff, r in runs if ff == f and r.get("plan_strategy") == "1f1b_full_recomp"
+                    and 0 < r.get("recomp_layers", 0) < r.get("n_layers", 0) // CAP_P), None)
+        if r50:
+            big = max((r for ff, r in runs if ff == f), key=lambda r: r["params_B"])
+            s += (f"; {f}: vs 1F1B+R50 {round(big['params_B'] / r50['params_B'], 2)}x params at "
+                  f"{round(big['model_tflops'] / r50['model_tflops'], 3)}x its model TFLOP/s")
     two = [x for x in runs if x[1]["params_vs_1f1b"] >= 2]
     if two:
         ft, t = max(two, key=lambda x: x[1]["model_tflops_vs_1f1b"])
