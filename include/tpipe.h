@@ -331,6 +331,8 @@ typedef struct {
      * overflow; 0 in a healthy run, TPIPE_E_OOM if it would exceed pool_cap) */
     uint64_t pool_overflow_bytes;
     int32_t  transport;             /* -1 virtual, else TPIPE_TRANSPORT_* in use */
+    double   host_issue_ms;         /* last step: host time to issue all its work (before the
+                                       final wait); near the step time = submission-bound */
 } tpipe_runtime_stats;
 
 typedef struct tpipe_runtime tpipe_runtime;

@@ -65,7 +65,8 @@ class RuntimeStats(C.Structure):
                 ("offload_h2d_bytes", C.c_double), ("host_opt_ms", C.c_double),
                 ("kernel_ms", C.c_double * 4), ("kernel_flops", C.c_double * 4),
                 ("kernel_count", i64 * 4), ("offload_d2h_ms", C.c_double),
-                ("offload_h2d_ms", C.c_double), ("pool_overflow_bytes", u64), ("transport", i32)]
+                ("offload_h2d_ms", C.c_double), ("pool_overflow_bytes", u64), ("transport", i32),
+                ("host_issue_ms", C.c_double)]
 
 
 def declare(L):

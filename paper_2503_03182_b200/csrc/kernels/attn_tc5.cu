@@ -29,6 +29,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tmap_cache.h"
 
 namespace tpipe {
 namespace fa5 {
@@ -1119,13 +1120,9 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 static int map2d(CUtensorMap* m, const void* base, long cols, long rows, long ld, int box_rows = 128) {
     auto enc = encode_fn();
     if (!enc) return -1;
-    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
-    cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
-    cuuint32_t es[2] = {1, 1};
-    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS
+    return tmap_encode_2d_cached(enc, m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, base, (uint64_t)cols, (uint64_t)rows,
+                                 (uint64_t)(ld * 2), 64u, (uint32_t)box_rows, CU_TENSOR_MAP_SWIZZLE_128B) ==
+                   CUDA_SUCCESS
                ? 0
                : -2;
 }

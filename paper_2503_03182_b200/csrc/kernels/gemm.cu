@@ -35,6 +35,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tmap_cache.h"
 
 namespace tpipe {
 
@@ -797,13 +798,9 @@ static int make_map(CUtensorMap* map, const void* base, long cols, long rows, lo
                     CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
     auto enc = get_encode();
     if (!enc) return -1;
-    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)(ld * (f32 ? 4 : 2))};
-    cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
-    cuuint32_t es[2] = {1, 1};
-    CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
-                     const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r = tmap_encode_2d_cached(enc, map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                                       base, (uint64_t)cols, (uint64_t)rows, (uint64_t)(ld * (f32 ? 4 : 2)),
+                                       (uint32_t)box_inner, (uint32_t)box_outer, sw);
     return r == CUDA_SUCCESS ? 0 : -2;
 }
 

@@ -122,6 +122,7 @@ struct tpipe_runtime {
     std::unique_ptr<DpGroup> dpg;      // dp > 1: this stage's replica group
     int dp_rank = 0;
     int transport_kind = -1;           // -1 virtual, else TPIPE_TRANSPORT_*
+    double host_issue_ms = 0;
     int timeout_ms = 300000;
     uint32_t debug = 0;
     bool selftest_done = false;
@@ -604,6 +605,7 @@ int run_step_impl(tpipe_runtime* rt, const int32_t* tok_dev, const int32_t* tgt_
     rt->d2h_ev.clear();
     rt->h2d_ev.clear();
     rt->d2h_bytes = rt->h2d_bytes = 0;
+    const auto t_issue0 = std::chrono::steady_clock::now();
     const long l0 = launch_count();
     profiler().begin_step((flags & TPIPE_STEP_PROFILE) != 0);
     const bool op_times = (flags & TPIPE_STEP_OP_TIMES) != 0;
@@ -674,6 +676,8 @@ int run_step_impl(tpipe_runtime* rt, const int32_t* tok_dev, const int32_t* tgt_
         CU(cudaEventRecord(j, S.cs));
         CU(cudaStreamWaitEvent(cs, j, 0));
     }
+    rt->host_issue_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_issue0).count();
     float loss = 0.f;
     if (std::find(rt->owned.begin(), rt->owned.end(), P.p - 1) != rt->owned.end()) {
         std::vector<float> slots(P.m);
@@ -1122,6 +1126,7 @@ TP_API int tpipe_runtime_get_stats(const tpipe_runtime* rt, tpipe_runtime_stats*
     out->offload_d2h_ms = span_ms(rt->d2h_ev);
     out->offload_h2d_ms = span_ms(rt->h2d_ev);
     out->transport = rt->transport_kind;
+    out->host_issue_ms = rt->host_issue_ms;
     for (int c = 0; c < 4; ++c) {
         out->kernel_ms[c] = rt->kms[c];
         out->kernel_flops[c] = rt->kflops[c];

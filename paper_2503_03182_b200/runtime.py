@@ -92,7 +92,7 @@ class Runtime:
                     kernel_ms=list(s.kernel_ms), kernel_flops=list(s.kernel_flops),
                     kernel_count=list(s.kernel_count), offload_d2h_ms=s.offload_d2h_ms,
                     offload_h2d_ms=s.offload_h2d_ms, pool_overflow_bytes=s.pool_overflow_bytes,
-                    transport=s.transport)
+                    transport=s.transport, host_issue_ms=s.host_issue_ms)
 
     def op_times(self, stage):
         """Per compute op (F/B/R, plan order) GPU ms of the last STEP_OP_TIMES step."""
