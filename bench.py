@@ -391,8 +391,10 @@ def run_capacity(args):
     import torch
     from paper_2503_03182_b200 import plan as P, runtime as RT
     import synth
-    p, m, budget = CAP_P, CAP_M, CAP_BUDGET_GIB * 2 ** 30
-    best = capacity_plans()
+    p, m = args.cap_p or CAP_P, CAP_M
+    budget_gib = args.cap_budget_gib or CAP_BUDGET_GIB
+    budget = int(budget_gib * 2 ** 30)
+    best = capacity_plans(p, budget, m)
     names = ("1f1b", "1f1b_full_recomp", "1f1b_r50", "tpipe", "tpipe_trecomp", "tpipe_all", "tpipe_offload",
              "tpipe_actoff", "tpipe_actoff_offload", "interleave", "interleave_trecomp", "tpipe_all_v3",
              "tpipe_offload_v3")
@@ -424,7 +426,11 @@ def run_capacity(args):
     for name, L, strat, off in runs:
         md = P.Model(L, C5["hidden"], C5["n_heads"], C5["ffn_hidden"], C5["vocab"],
                      C5["seq_len"], C5["micro_batch"], P.BF16)
-        plan = plan_of(md, p, m, budget, strat, off)
+        try:
+            plan = plan_of(md, p, m, budget, strat, off)
+        except Exception as e:   # e.g. no rung fits the budget at this size
+            res[name] = {"n_layers": L, "strategy": strat, "error": str(e)[:160]}
+            continue
         t0 = time.perf_counter()
         rt = RT.Runtime(plan, stage=-1, lr=1e-5, pool_cap=budget)
         for s in range(p):
@@ -457,7 +463,7 @@ def run_capacity(args):
                      "pool_high_water_GiB": [round(x / 2 ** 30, 3) for x in hw],
                      "high_water_eq_plan": all(hw[s] == plan.peak(s)["total_peak"] for s in range(p)),
                      "max_stage_GiB": round(max(hw) / 2 ** 30, 3),
-                     "fits_budget": max(hw) <= budget,
+                     "fits_budget": max(hw) <= budget, "stages": p, "budget_GiB": budget_gib,
                      "device_used_GiB": round((total_b - free_b) / 2 ** 30, 1),
                      "loss_first": round(float(loss0), 4), "loss_last": round(float(loss), 4),
                      "ms_per_step": round(ms, 1), "tokens_s": round(tokens / (ms / 1e3), 1),
@@ -469,16 +475,18 @@ def run_capacity(args):
         torch.cuda.synchronize()
     out = {"capacity_measured": {
         "how": f"one B200, all p={p} stages in one process (virtual pipeline), pool ledger per stage "
-               f"capped at {CAP_BUDGET_GIB} GiB, shape h=4096 a=32 f=16384 V=32000 s=8192 b=1 m={m}, "
+               f"capped at {budget_gib} GiB, shape h=4096 a=32 f=16384 V=32000 s=8192 b=1 m={m}, "
                f"largest L (multiple of p) the planner fits, then built and stepped ({src} peak {pk_sust})",
         "runs": res}}
     b = res.get("1f1b")
     if b:
         for n, r in res.items():
+            if "error" in r:
+                continue
             r["params_vs_1f1b"] = round(r["params_B"] / b["params_B"], 3)
             r["model_tflops_vs_1f1b"] = round(r["model_tflops"] / b["model_tflops"], 3)
     fr, ta = res.get("1f1b_full_recomp"), res.get("tpipe_all@1f1b_full_recomp_size")
-    if fr and ta:
+    if fr and ta and "tokens_s" in fr and "tokens_s" in ta:
         out["capacity_measured"]["equal_size_tpipe_all_vs_1f1b_full_recomp_tokens_s"] = \
             round(ta["tokens_s"] / fr["tokens_s"], 3)
     return out
@@ -829,7 +837,8 @@ def latest_capacity_claim():
     # against the paper's 1F1B + R50 baseline, within one capacity file
     for f in sorted({x[0] for x in runs}):
         r50 = next((r for ff, r in runs if ff == f and r.get("plan_strategy") == "1f1b_full_recomp"
-                    and 0 < r.get("recomp_layers", 0) < r.get("n_layers", 0) // CAP_P), None)
+                    and 0 < r.get("recomp_layers", 0) < r.get("n_layers", 0) // r.get("stages", CAP_P)),
+                   None)
         if r50:
             big = max((r for ff, r in runs if ff == f), key=lambda r: r["params_B"])
             s += (f"; {f}: vs 1F1B+R50 {round(big['params_B'] / r50['params_B'], 2)}x params at "
@@ -1149,6 +1158,8 @@ def main():
                     help="measured-op-duration replay of p = 2, 4, 8 stage pipelines (C2)")
     ap.add_argument("--capacity-run", action="store_true",
                     help="executed capacity at a fixed per-stage HBM budget (p=8 virtual pipeline, one GPU)")
+    ap.add_argument("--cap-p", type=int, default=0, help="--capacity-run stages (default 8)")
+    ap.add_argument("--cap-budget-gib", type=float, default=0, help="--capacity-run per-stage budget (default 20)")
     ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
                     help="stage transport for N > 1 ranks (CUDA-IPC copy-engine pull, or NCCL send/recv)")
     ap.add_argument("--pp", type=int, default=0,
