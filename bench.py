@@ -912,18 +912,38 @@ def run_tpipe(args):
     # p > 1: the planner picks the cost-balanced stage partition when its cost
     # model says it pays (R27/R28)
     plan = P.Plan(md, N, m, strategy=args.strategy, balance=N > 1, dp=dp)
-    ids, ipc_name = None, None
     transport = RT.TRANSPORT_IPC if args.transport == "ipc" else RT.TRANSPORT_NCCL
-    if world > 1:
-        if transport == RT.TRANSPORT_NCCL:
-            ids = [b"".join(RT.nccl_unique_id() for _ in plan.channels)] if rank == 0 else [None]
-        else:
-            ids = [f"/tpipe_bench_{os.getpid()}_{np.random.default_rng().integers(1 << 40)}"] \
-                if rank == 0 else [None]
-        dist.broadcast_object_list(ids, src=0)
-        ids, ipc_name = (ids[0], None) if transport == RT.TRANSPORT_NCCL else (None, ids[0])
-    rt = RT.Runtime(plan, stage=stage, device=local, nccl_ids=ids, lr=1e-4,
-                    transport=transport, ipc_name=ipc_name, dp_rank=dp_rank)
+
+    def make_runtime(tr):
+        ids, ipc_name = None, None
+        if world > 1:
+            if tr == RT.TRANSPORT_NCCL:
+                ids = [b"".join(RT.nccl_unique_id() for _ in plan.channels)] if rank == 0 else [None]
+            else:
+                ids = [f"/tpipe_bench_{os.getpid()}_{np.random.default_rng().integers(1 << 40)}"] \
+                    if rank == 0 else [None]
+            dist.broadcast_object_list(ids, src=0)
+            ids, ipc_name = (ids[0], None) if tr == RT.TRANSPORT_NCCL else (None, ids[0])
+        return RT.Runtime(plan, stage=stage, device=local, nccl_ids=ids, lr=1e-4, transport=tr,
+                          ipc_name=ipc_name, dp_rank=dp_rank, timeout_ms=120000)
+
+    if world > 1 and transport == RT.TRANSPORT_IPC and dp == 1:
+        # CUDA IPC first; if any rank cannot set it up (no peer access, shm
+        # unavailable), every rank falls back to NCCL together
+        rt, err = None, ""
+        try:
+            rt = make_runtime(RT.TRANSPORT_IPC)
+        except Exception as e:   # reported in the line, not fatal
+            err = str(e)[:200]
+        ok = torch.tensor([1 if rt is not None else 0])
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok[0]) == 0:
+            if rt is not None:
+                rt.close()
+            rt = make_runtime(RT.TRANSPORT_NCCL)
+            args.transport = f"nccl (ipc setup failed: {err or 'on another rank'})"
+    else:
+        rt = make_runtime(transport)
     rng = np.random.default_rng(1234 + max(stage, 0))   # replicas of a stage start equal
     stages = [stage] if world > 1 else list(range(N))
     for s in stages:
