@@ -8,7 +8,7 @@ Writes the stage's loss, gradients (after step 1, no optimizer) and
 parameters (after `steps` optimizer steps) to an .npz file.
 
     python tests/mp_stage_worker.py OUT.npz STAGE P M STRATEGY DTYPE IPC_NAME
-        L H A F V S B [STEPS] [OFFLOAD] [TIMEOUT_MS] [SEED] [DP] [DP_RANK]
+        L H A F V S B [STEPS] [OFFLOAD] [TIMEOUT_MS] [SEED] [DP] [DP_RANK] [CHUNKS]
 
 With DP > 1 (ZeRO-1 data parallelism, DESIGN R31) replica k runs
 micro-batches [k*M, (k+1)*M) of a DP*M-micro-batch step.
@@ -33,10 +33,12 @@ def main(argv):
     seed = int(argv[17]) if len(argv) > 17 else 11
     dp = int(argv[18]) if len(argv) > 18 else 1
     dp_rank = int(argv[19]) if len(argv) > 19 else 0
+    chunks = int(argv[20]) if len(argv) > 20 else 2
     import synth
     from paper_2503_03182_b200 import params as PR, plan as P, runtime as RT
 
-    plan = P.Plan(P.Model(L, h, a, f, V, s, b, dtype), p, m, strategy=strategy, offload=offload, dp=dp)
+    plan = P.Plan(P.Model(L, h, a, f, V, s, b, dtype), p, m, strategy=strategy, offload=offload, dp=dp,
+                  chunks=chunks)
     rt = RT.Runtime(plan, stage=stage, device=0, lr=1e-3, transport=RT.TRANSPORT_IPC,
                     ipc_name=ipc, timeout_ms=timeout_ms, dp_rank=dp_rank)
 

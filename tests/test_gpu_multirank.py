@@ -32,7 +32,7 @@ C1_16 = dict(C1, L=16)     # C1 width, 16 layers: p = 8 with two chunks of one l
 
 
 def run_job(tmp_path, cfg, p, m, strategy, dtype, steps=1, offload=0, timeout_ms=120000,
-            stages=None, wall=600, dp=1, tag=""):
+            stages=None, wall=600, dp=1, tag="", chunks=2):
     """Launch one process per (replica, stage); results keyed by stage (dp = 1)
     or by (replica, stage)."""
     name = f"/tpipe_t_{os.getpid()}_{uuid.uuid4().hex[:12]}"
@@ -43,7 +43,7 @@ def run_job(tmp_path, cfg, p, m, strategy, dtype, steps=1, offload=0, timeout_ms
             out = str(tmp_path / f"{tag}r{k}_stage{s}.npz")
             args = [sys.executable, WORKER, out, str(s), str(p), str(m), strategy, str(dtype), name,
                     *(str(cfg[kk]) for kk in ("L", "h", "a", "f", "V", "s", "b")), str(steps),
-                    str(offload), str(timeout_ms), "11", str(dp), str(k)]
+                    str(offload), str(timeout_ms), "11", str(dp), str(k), str(chunks)]
             procs.append((key, out, subprocess.Popen(args, stdout=subprocess.PIPE,
                                                      stderr=subprocess.STDOUT, cwd=ROOT)))
     res, logs = {}, {}
@@ -74,10 +74,10 @@ def rel_l2(a, b):
     return float(np.linalg.norm(a - b) / (np.linalg.norm(b) + 1e-30))
 
 
-def _plan(cfg, p, m, strategy, dtype, offload=0):
+def _plan(cfg, p, m, strategy, dtype, offload=0, chunks=2):
     from paper_2503_03182_b200 import plan as P
     return P.Plan(P.Model(cfg["L"], cfg["h"], cfg["a"], cfg["f"], cfg["V"], cfg["s"], cfg["b"], dtype),
-                  p, m, strategy=strategy, offload=offload)
+                  p, m, strategy=strategy, offload=offload, chunks=chunks)
 
 
 def check_vs_oracle(cfg, p, m, strategy, dtype, res, tol, metric):
@@ -245,3 +245,25 @@ def test_dp_pp_zero1_bf16_deterministic(tmp_path):
         hi = [(x.view(np.uint32) + 0x7FFF + ((x.view(np.uint32) >> 16) & 1)) >> 16 for x in ps]
         for k in range(1, dp):
             assert np.array_equal(hi[0], hi[k]), sc
+
+
+def test_multiprocess_v3_dp2_fp32(tmp_path):
+    """Three chunks per stage (R32) with two ZeRO-1 replicas (R31), p = 2:
+    4 processes; the replicas' summed gradients equal the oracle's full-batch
+    gradients, replicas hold identical parameters after two steps."""
+    from paper_2503_03182_b200 import params as PR
+    cfg, p, dp, m, v = dict(C1, L=12), 2, 2, 4, 3
+    res, logs = run_job(tmp_path, cfg, p, m, "tpipe_trecomp", 0, steps=2, dp=dp, chunks=v)
+    assert_ok(res, logs)
+    plan = _plan(cfg, p, m, "tpipe_trecomp", 0, chunks=v)
+    W = synth.weights(cfg["L"], cfg["h"], cfg["f"], cfg["V"], cfg["s"], seed=11, std=0.05,
+                      bias_std=0.02, ln_jitter=0.05)
+    tok, tgt = synth.tokens(cfg["V"], dp * m, cfg["b"], cfg["s"], step=0)
+    lref, G = R.step_grads(R.to64(W), tok, tgt, cfg["a"])
+    for s in range(p):
+        for c in range(1, v + 1):
+            g = np.sum([res[(k, s)][f"grad{c}"] for k in range(dp)], axis=0)
+            for (kk, l), gg in PR.unpack(g, W, p, v, plan.partition, s, c).items():
+                ref = G["layers"][l][kk] if l is not None else G[kk]
+                assert max_rel(gg, ref) <= 1e-4, (s, c, kk, l)
+            assert np.array_equal(res[(0, s)][f"param{c}"], res[(1, s)][f"param{c}"])

@@ -313,3 +313,33 @@ def test_1f1b_partial_recompute_step(r):
     rt.close()
     ref = _run(dict(cfg), p, m, "1f1b")
     _assert_same(ref, _run(dict(cfg), p, m, "1f1b_full_recomp", recomp_layers=r), ("1f1b_r", r))
+
+
+def test_config_loader_end_to_end(tmp_path):
+    """JSON config -> plan -> runtime -> step gives the same loss and
+    gradients as the direct API call (config.py is marshalling only)."""
+    import json
+    P, RT, PR = mods()
+    from paper_2503_03182_b200 import config as CFG
+    cfg, p, m = C1_16, 4, 8
+    doc = {"model": {"n_layers": cfg["L"], "hidden": cfg["h"], "n_heads": cfg["a"], "ffn_hidden": cfg["f"],
+                     "vocab": cfg["V"], "seq_len": cfg["s"], "micro_batch": cfg["b"], "dtype": "bf16"},
+           "p": p, "m": m, "strategy": "tpipe_trecomp", "chunks": 2}
+    f = tmp_path / "cfg.json"
+    f.write_text(json.dumps(doc))
+    outs = []
+    md = P.Model(cfg["L"], cfg["h"], cfg["a"], cfg["f"], cfg["V"], cfg["s"], cfg["b"], P.BF16)
+    for plan in (CFG.load(str(f)), P.Plan(md, p, m, strategy="tpipe_trecomp")):
+        rt = RT.Runtime(plan, stage=-1)
+        W = synth.weights(cfg["L"], cfg["h"], cfg["f"], cfg["V"], cfg["s"], seed=11, std=0.05,
+                          bias_std=0.02, ln_jitter=0.05)
+        for s in range(p):
+            for c in (1, 2):
+                rt.set_params(s, c, PR.pack(W, p, 2, plan.partition, s, c))
+        tok, tgt = synth.tokens(cfg["V"], m, cfg["b"], cfg["s"], step=0)
+        loss = rt.step(tok, tgt, RT.STEP_NO_OPT)
+        outs.append((loss, [rt.get_grads(s, c).view(np.uint32).copy() for s in range(p) for c in (1, 2)]))
+        rt.close()
+    assert outs[0][0] == outs[1][0]
+    for a, b in zip(outs[0][1], outs[1][1]):
+        assert np.array_equal(a, b)
