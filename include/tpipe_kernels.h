@@ -53,13 +53,6 @@ int tpipe_k_gemm_simt(int dtype, int M, int N, int K,
                       const void* R, long ldr, void* C2, long ldc2,
                       const void* aux, long ldaux, void* stream);
 
-/* Enable (1) or disable (0, default) stream-K scheduling in the tcgen05 GEMM
- * (process-wide; for A/B measurement). Stream-K splits the concatenated K
- * iterations of all output tiles evenly over the SMs; split tiles are summed
- * in a fixed order, so results stay bit-reproducible for a given shape and
- * SM count. Uses a lazily allocated per-stream workspace of #SMs x 128 KB. */
-void tpipe_k_gemm_set_stream_k(int on);
-
 /* Enable (1, default) or disable (0) CTA-pair tiles in the tcgen05 GEMM
  * (process-wide; for A/B measurement): a cluster of two CTAs on one TPC
  * computes a 256 x 256 tile with tcgen05.mma.cta_group::2, each CTA staging
@@ -67,13 +60,6 @@ void tpipe_k_gemm_set_stream_k(int on);
 void tpipe_k_gemm_set_pair(int on);
 /* CTA-pair 256 x 256 tiles once a GEMM has >= n of them (default 96; A/B knob) */
 void tpipe_k_gemm_set_pair_min_tiles(int n);
-
-/* Enable (1) or disable (0, default) 256 x 512 CTA-pair tiles (two N = 256
- * tcgen05.mma per K step sharing the A stage; one TMEM accumulator): fewer
- * operand bytes per flop for the L2 -> SM bound mainloop. Chosen for pair
- * shapes whose 256 x 512 tile count fills the 74 pairs' waves as well as the
- * 256 x 256 tiling (process-wide; for A/B measurement). */
-void tpipe_k_gemm_set_wide(int on);
 
 /* LayerNorm forward over rows of length h (eps 1e-5, biased variance):
  * y = (x-mean)*rstd*gamma + beta; mean/rstd fp32 [rows]. */

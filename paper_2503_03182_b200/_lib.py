@@ -44,8 +44,6 @@ def _declare(L):
                  vp, i64, vp]
     L.tpipe_k_gemm.argtypes = gemm_args
     L.tpipe_k_gemm_simt.argtypes = gemm_args
-    L.tpipe_k_gemm_set_stream_k.argtypes = [i32]
-    L.tpipe_k_gemm_set_stream_k.restype = None
     L.tpipe_k_gemm_set_pair.argtypes = [i32]
     L.tpipe_k_gemm_set_pair.restype = None
     L.tpipe_k_gemm_set_pair_min_tiles.argtypes = [i32]

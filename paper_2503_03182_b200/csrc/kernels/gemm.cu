@@ -10,23 +10,15 @@
 // Both operands may be K-major or MN-major (fprop: K/K, dgrad: K/MN,
 // wgrad: MN/MN), so no transposes are materialised.
 //
-// Stream-K (off by default; tpipe_k_gemm_set_stream_k): when whole tiles
-// would leave SMs idle in the last wave (every 2048-multiple shape of the
-// model on 148 SMs caps at ~86%), the tiles' K iterations are laid end to end
-// and split evenly over the CTAs (or CTA pairs). Measured 20-50% SLOWER than
-// the data-parallel schedule on the model shapes (the owners' partial fix-up
-// sits on the critical path and concurrent CTAs no longer share L2 lines), so
-// it is kept for A/B runs only. A CTA whose
-// range starts inside a tile ("contributor") writes its fp32 partial to its
-// own workspace slot and publishes a flag; the CTA that holds the tile's k=0
-// part ("owner", which reaches it last) adds the partials in CTA order in its
-// epilogue. Fixed summation order => bit-reproducible results.
+// Two schedules were built, measured and removed (round 2): stream-K
+// (K iterations split over CTAs with an ordered fp32 fix-up; 20-50% slower on
+// the model shapes) and 256 x 512 pair tiles (one TMEM accumulator, exposed
+// epilogue; profiles/r1_gemm_wide_ab.jsonl). DESIGN §9b has the numbers.
 //
 // fp32: exact-fp32 SIMT tiled kernel (parity mode).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
-#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -248,39 +240,23 @@ constexpr int TC_BM = 128, TC_BK = 64;
 // critical path of the dGELU GEMM: 775 -> 1029 TFLOP/s). The light epilogues
 // (store, bias, fp32 reduce-add) keep EW = 4.
 __host__ __device__ constexpr int tc_threads(int ew) { return 128 + 32 * ew; }
-static bool g_stream_k_enabled = false;   // measured slower on the model shapes
 static bool g_pair_enabled = true;
-// 256 x 512 pair tiles measured slower on the model shapes (fc1 fprop 54 -> 70 us,
-// fc2 dgrad 58 -> 81 us: the exposed single-accumulator epilogue outweighs the
-// 25% fewer operand bytes; profiles/r1_gemm_wide_ab.jsonl): off by default
-static bool g_wide_enabled = false;
-void gemm_set_stream_k(int on) { g_stream_k_enabled = on != 0; }
 void gemm_set_pair(int on) { g_pair_enabled = on != 0; }
 // CTA-pair tiles from this many 256 x 256 tiles on (measured crossover, see gemm_tc)
 static int g_pair_min_tiles = 96;
 void gemm_set_pair_min_tiles(int n) { g_pair_min_tiles = n > 0 ? n : 96; }
-void gemm_set_wide(int on) { g_wide_enabled = on != 0; }
 
 // CG = 1: one CTA computes a 128 x BN tile. CG = 2: a CTA pair (cluster of 2
 // on one TPC) computes a 256 x BN tile with tcgen05.mma.cta_group::2; each CTA
 // stages 128 rows of A and BN/2 rows of B, so per-SM operand traffic (L2->smem
 // and smem->tensor core) is 2/3 of the CG = 1, BN = 256 tile's.
-// BN = 512 (CG = 2 only): the pair computes a 256 x 512 tile as two N = 256
-// MMAs per K step that share the A stage; per SM 48 KB of operands feed 1024
-// MMA clocks (47 B/clk vs 64 B/clk for 256 x 256: the mainloop is bound by
-// L2 -> SM operand delivery, profiles/r1_gemm_l2_analysis.txt). The 512
-// accumulator columns fill TMEM, so there is one accumulator (the epilogue of
-// a tile is not overlapped with the next tile's mainloop).
 template <int BN, int CG = 1, int EPI_WARPS = 4>
 struct TcCfg {
-    static_assert(BN <= 256 || (BN == 512 && CG == 2), "BN = 512 needs a CTA pair");
-    static constexpr int STAGES = BN == 512 ? 4 : (CG == 2 ? 6 : (BN == 256 ? 4 : 6));
+    static_assert(BN <= 256, "one tcgen05.mma covers N <= 256");
+    static constexpr int STAGES = CG == 2 ? 6 : (BN == 256 ? 4 : 6);
     static constexpr int A_BYTES = TC_BM * TC_BK * 2;
     static constexpr int B_BYTES = (BN / CG) * TC_BK * 2;
-    static constexpr int NACC = BN == 512 ? 1 : 2;          // TMEM accumulator buffers
-    static constexpr int TMEM_COLS = NACC * BN;
-    static constexpr int MMA_N = BN > 256 ? 256 : BN;       // N of one tcgen05.mma
-    static constexpr int B_LOAD_ROWS = BN == 512 ? 128 : BN / CG;   // rows per B TMA box (K-major)
+    static constexpr int TMEM_COLS = 2 * BN;                // double-buffered accumulators
     // epilogue staging: EPI_WARPS warps x 2 buffers x one 32 x 32 chunk; the
     // 8-warp epilogues (GELU, dGELU, residual) only store bf16 (2 KB chunks),
     // so both variants fit the same operand ring depth
@@ -389,65 +365,28 @@ __device__ __forceinline__ uint32_t tc_idesc() {
            | ((uint32_t)((TC_BM * CG) >> 4) << 24);  // M
 }
 
-// Work of one CTA: whole tiles strided by the grid (data-parallel) or a
-// contiguous range of the concatenated K iterations (stream-K).
+// Persistent data-parallel schedule: unit u (a CTA, or a CTA pair for CG = 2,
+// whose CTAs walk the same tiles) takes tiles u, u + G, u + 2G, ...
 struct TcSched {
-    int num_tiles, num_kb, sk, tile_dp, stride;
-    long it, it_end;
-    // CG = 2: both CTAs of a pair walk the same tiles (unit = cluster)
-    __device__ void init(int nt, int nkb, int sk_, int cg = 1) {
+    int num_tiles, tile, stride;
+    __device__ void init(int nt, int cg = 1) {
         num_tiles = nt;
-        num_kb = nkb;
-        sk = sk_;
-        tile_dp = blockIdx.x / cg;
+        tile = blockIdx.x / cg;
         stride = gridDim.x / cg;
-        const long I = (long)nt * nkb;
-        it = (long)tile_dp * I / stride;
-        it_end = (long)(tile_dp + 1) * I / stride;
     }
-    // next segment: tile, k blocks [kb0, kb1)
-    __device__ bool next(int& tile, int& kb0, int& kb1) {
-        if (!sk) {
-            if (tile_dp >= num_tiles) return false;
-            tile = tile_dp;
-            kb0 = 0;
-            kb1 = num_kb;
-            tile_dp += stride;
-            return true;
-        }
-        if (it >= it_end) return false;
-        tile = (int)(it / num_kb);
-        kb0 = (int)(it % num_kb);
-        const long left = it_end - it;
-        kb1 = left < (long)(num_kb - kb0) ? kb0 + (int)left : num_kb;
-        it += kb1 - kb0;
+    __device__ bool next(int& t) {
+        if (tile >= num_tiles) return false;
+        t = tile;
+        tile += stride;
         return true;
     }
 };
-
-// unit (CTA, or CTA pair for CG = 2) whose stream-K range holds iteration x
-__device__ __forceinline__ int sk_unit_of(long x, long I, int G) {
-    int c = (int)(x * G / I);
-    while (c + 1 < G && (long)(c + 1) * I / G <= x) ++c;
-    while (c > 0 && (long)c * I / G > x) --c;
-    return c;
-}
-
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 template <int BN, bool A_MN, bool B_MN, int CG, int EPI_WARPS>
 __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
-                   const GemmDesc g, int num_m, int num_n, int num_kb, int sk, float* __restrict__ sk_ws,
-                   unsigned* __restrict__ sk_flags, unsigned epoch) {
+                   const GemmDesc g, int num_m, int num_n, int num_kb) {
     using Cfg = TcCfg<BN, CG, EPI_WARPS>;
     constexpr int STAGES = Cfg::STAGES;
     constexpr int TM = TC_BM * CG;        // tile rows
@@ -505,15 +444,13 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
             int stage = 0;
             uint32_t phase = 0;
             TcSched sch;
-            sch.init(num_tiles, num_kb, sk, CG);
-            int tile, kb0, kb1;
-            while (sch.next(tile, kb0, kb1)) {
+            sch.init(num_tiles, CG);
+            int tile;
+            while (sch.next(tile)) {
                 const int mb = tile % num_m, nb = tile / num_m;
                 const int am = mb * TM + rank * TC_BM;     // this CTA's A rows
-                // this CTA's B rows: [bn, bn + BNC); BN = 512: [bn, +128) and [bn + 256, +128)
-                // (MMA h of the pair reads tile columns [256h, 256h + 256), 128 per CTA)
-                const int bn = BN == 512 ? nb * BN + rank * 128 : nb * BN + rank * BNC;
-                for (int kb = kb0; kb < kb1; ++kb) {
+                const int bn = nb * BN + rank * BNC;       // this CTA's B rows: [bn, bn + BNC)
+                for (int kb = 0; kb < num_kb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* a = sA + stage * Cfg::A_BYTES;
                     uint8_t* b = sB + stage * Cfg::B_BYTES;
@@ -545,16 +482,11 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
                                 tma_load_2d_pair(a + i * 64 * TC_BK * 2, &tmA, fb, am + i * 64, kb * TC_BK);
                         }
                         if (!B_MN) {
-#pragma unroll
-                            for (int hh = 0; hh < BNC / Cfg::B_LOAD_ROWS; ++hh)
-                                tma_load_2d_pair(b + hh * Cfg::B_LOAD_ROWS * TC_BK * 2, &tmB, fb, kb * TC_BK,
-                                                 bn + hh * 256);
+                            tma_load_2d_pair(b, &tmB, fb, kb * TC_BK, bn);
                         } else {
 #pragma unroll
                             for (int i = 0; i < BNC / 64; ++i)
-                                tma_load_2d_pair(b + i * 64 * TC_BK * 2, &tmB, fb,
-                                                 BN == 512 ? bn + (i >> 1) * 256 + (i & 1) * 64 : bn + i * 64,
-                                                 kb * TC_BK);
+                                tma_load_2d_pair(b + i * 64 * TC_BK * 2, &tmB, fb, bn + i * 64, kb * TC_BK);
                         }
                         if (rank != 0) mbar_arrive_cluster(fb);
                     }
@@ -566,20 +498,20 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
     } else if (warp == 1) {
         if (rank == 0) {
             // ---------------- MMA issuer (whole warp of the pair leader; the elected lane issues)
-            const uint32_t idesc = tc_idesc<Cfg::MMA_N, A_MN, B_MN, CG>();
+            const uint32_t idesc = tc_idesc<BN, A_MN, B_MN, CG>();
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
             TcSched sch;
-            sch.init(num_tiles, num_kb, sk, CG);
-            int tile, kb0, kb1;
-            for (; sch.next(tile, kb0, kb1); ++it) {
-                const int acc = Cfg::NACC == 2 ? (it & 1) : 0;
-                const uint32_t aph = Cfg::NACC == 2 ? ((it >> 1) & 1) : (it & 1);
+            sch.init(num_tiles, CG);
+            int tile;
+            for (; sch.next(tile); ++it) {
+                const int acc = it & 1;
+                const uint32_t aph = (it >> 1) & 1;
                 mbar_wait(&tempty[acc], aph ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem_base + acc * BN;
-                for (int kb = kb0; kb < kb1; ++kb) {
+                for (int kb = 0; kb < num_kb; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t a_addr = smem_u32(sA + stage * Cfg::A_BYTES);
@@ -593,14 +525,9 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
                                                  : umma_desc_sw128(a_addr + k * 32, 0, 1024);
                         const uint64_t db = B_MN ? umma_desc_sw128(b_addr + k * 2048, TC_BK * 128, 1024)
                                                  : umma_desc_sw128(b_addr + k * 32, 0, 1024);
-                        const uint32_t accum = (kb != kb0 || k != 0) ? 1u : 0u;
+                        const uint32_t accum = (kb != 0 || k != 0) ? 1u : 0u;
                         if (CG == 2) umma_bf16_pair(d, da, db, idesc, accum);
                         else umma_bf16(d, da, db, idesc, accum);
-                        if (BN == 512) {   // second N half: B rows [128, 256) of the stage (+16 KB)
-                            const uint64_t db2 = B_MN ? umma_desc_sw128(b_addr + 16384 + k * 2048, TC_BK * 128, 1024)
-                                                      : umma_desc_sw128(b_addr + 16384 + k * 32, 0, 1024);
-                            umma_bf16_pair(d + 256, da, db2, idesc, accum);
-                        }
                     }
                     if (CG == 2) umma_commit_pair(&empty[stage], 3);
                     else umma_commit(&empty[stage]);
@@ -626,58 +553,19 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
         int sb = 0;
         int it = 0;
         TcSched sch;
-        sch.init(num_tiles, num_kb, sk, CG);
-        const long I = (long)num_tiles * num_kb;
+        sch.init(num_tiles, CG);
         const uint32_t tempty_leader = CG == 2 ? mapa_shared(&tempty[0], 0) : 0;
-        const int row = ew * 32 + lane;   // row of the tile this thread owns
         constexpr int NCH = BN / 32 / (EPI_WARPS / 4);   // 32-column chunks per column group
         const int c_lo = chalf * NCH, c_hi = c_lo + NCH;
-        int tile, kb0, kb1;
-        for (; sch.next(tile, kb0, kb1); ++it) {
+        int tile;
+        for (; sch.next(tile); ++it) {
             const int mb = tile % num_m, nb = tile / num_m;
-            const int acc = Cfg::NACC == 2 ? (it & 1) : 0;
-            const uint32_t aph = Cfg::NACC == 2 ? ((it >> 1) & 1) : (it & 1);
+            const int acc = it & 1;
+            const uint32_t aph = (it >> 1) & 1;
             mbar_wait(&tfull[acc], aph);
             tc_fence_after();
             const int m0 = mb * TM + rank * TC_BM + ew * 32;
             const long m = m0 + lane;
-            if (kb0 > 0) {
-                // ---- stream-K contributor: fp32 partial -> own slot (one per CTA;
-                // for a pair each CTA holds its 128 rows), then flag
-                float* slot = sk_ws + (size_t)blockIdx.x * TC_BM * BN;
-#pragma unroll 1
-                for (int c = c_lo; c < c_hi; ++c) {
-                    uint32_t r[32];
-                    tmem_ld32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + c * 32, r);
-                    tmem_wait_ld();
-                    float4* dst = reinterpret_cast<float4*>(slot + ((size_t)c * TC_BM + row) * 32);
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        __stcg(dst + q, make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
-                                                    __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3])));
-                }
-                __threadfence();
-                named_bar_sync(1, 32 * EPI_WARPS);
-                if (ew == 0 && lane == 0) st_release_u32(sk_flags + blockIdx.x, epoch);
-                tc_fence_before();
-                if (CG == 2) {
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
-                } else {
-                    mbar_arrive(&tempty[acc]);
-                }
-                continue;
-            }
-            // owner of a split tile: contributors are the CTAs after this one up
-            // to the one holding the tile's last iteration
-            const int unit = blockIdx.x / CG, nunits = gridDim.x / CG;
-            int c_last = unit;
-            if (kb1 < num_kb) {
-                c_last = sk_unit_of((long)tile * num_kb + num_kb - 1, I, nunits);
-                for (int cc = unit + 1; cc <= c_last; ++cc)
-                    while (ld_acquire_u32(sk_flags + cc * CG + rank) != epoch) {
-                    }
-            }
             // fused LM head + CE (K8): this thread owns row m of the tile
             const bool lse_mode = g.epi == EPI_LSE_PART, ce_mode = g.epi == EPI_CE_GRAD;
             int tgt = -1;
@@ -696,18 +584,6 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
                 float v[32], v2[32];
 #pragma unroll
                 for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-                for (int cc = unit + 1; cc <= c_last; ++cc) {   // fixed order: k ascending
-                    const float4* src = reinterpret_cast<const float4*>(
-                        sk_ws + (size_t)(cc * CG + rank) * TC_BM * BN + ((size_t)c * TC_BM + row) * 32);
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const float4 p = __ldcg(src + q);
-                        v[4 * q] += p.x;
-                        v[4 * q + 1] += p.y;
-                        v[4 * q + 2] += p.z;
-                        v[4 * q + 3] += p.w;
-                    }
-                }
                 if (lse_mode) {
                     // online (max, sum exp) over the 64-column group, fp32 from
                     // the accumulators; the target logit captured in passing
@@ -814,52 +690,6 @@ static int num_sms() {
     return n;
 }
 
-// Stream-K workspace, one per (device, stream): #SMs slots of a 128 x 256 fp32
-// partial tile (19.4 MB on 148 SMs) + one flag per slot. Flags carry a
-// per-launch epoch, so they never need resetting. Launches on one stream are
-// serialised, so a slot is never shared by two live kernels.
-struct SkWs {
-    float* ws = nullptr;
-    unsigned* flags = nullptr;
-};
-static int sk_workspace(cudaStream_t st, SkWs& out) {
-    static std::mutex mu;
-    static std::vector<std::pair<std::pair<int, cudaStream_t>, SkWs>> cache;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    std::lock_guard<std::mutex> lk(mu);
-    for (auto& e : cache)
-        if (e.first.first == dev && e.first.second == st) {
-            out = e.second;
-            return 0;
-        }
-    SkWs w;
-    const size_t slots = (size_t)num_sms();
-    if (cudaMalloc(&w.ws, slots * TC_BM * 256 * sizeof(float)) != cudaSuccess) return -6;
-    if (cudaMalloc(&w.flags, slots * sizeof(unsigned)) != cudaSuccess) return -6;
-    if (cudaMemset(w.flags, 0, slots * sizeof(unsigned)) != cudaSuccess) return -6;
-    if (cudaDeviceSynchronize() != cudaSuccess) return -6;
-    cache.push_back({{dev, st}, w});
-    out = w;
-    return 0;
-}
-static unsigned next_epoch() {
-    static std::atomic<unsigned> e{0};
-    unsigned v = ++e;
-    if (v == 0) v = ++e;   // 0 is the flags' initial value
-    return v;
-}
-
-// Stream-K pays when whole tiles leave >= 8% of the SM-waves idle and each CTA
-// still gets >= 4 K blocks.
-static bool use_stream_k(int tiles, int num_kb, int G) {
-    if (tiles <= 0) return false;
-    const long waves = (tiles + G - 1) / G;
-    const double eff = (double)tiles / (double)(waves * G);
-    const long I = (long)tiles * num_kb;
-    return eff < 0.92 && I >= 4L * G;
-}
-
 template <int BN, bool A_MN, bool B_MN, int CG, int EPI_WARPS>
 static int launch_tc(const GemmDesc& g, cudaStream_t st) {
     using Cfg = TcCfg<BN, CG, EPI_WARPS>;
@@ -873,7 +703,7 @@ static int launch_tc(const GemmDesc& g, cudaStream_t st) {
         rc = make_map(&ta, g.A, g.M, g.K, g.lda, 64, TC_BK);
     if (rc) return rc;
     if (!B_MN)
-        rc = make_map(&tb, g.B, g.K, g.N, g.ldb, TC_BK, Cfg::B_LOAD_ROWS);
+        rc = make_map(&tb, g.B, g.K, g.N, g.ldb, TC_BK, BNC);
     else
         rc = make_map(&tb, g.B, g.N, g.K, g.ldb, 64, TC_BK);
     if (rc) return rc;
@@ -898,22 +728,14 @@ static int launch_tc(const GemmDesc& g, cudaStream_t st) {
     const int num_kb = (g.K + TC_BK - 1) / TC_BK;
     const int tiles = num_m * num_n;
     const int units = num_sms() / CG;
-    // (stream-K partial slots are 128 x 256: not for BN = 512)
-    const int sk = BN <= 256 && g_stream_k_enabled && use_stream_k(tiles, num_kb, units) ? 1 : 0;
-    const int grid = CG * (sk ? units : (tiles < units ? tiles : units));
-    SkWs w;
-    unsigned epoch = 0;
-    if (sk) {
-        if (int e = sk_workspace(st, w)) return e;
-        epoch = next_epoch();
-    }
+    const int grid = CG * (tiles < units ? tiles : units);
     auto kern = gemm_tc_kernel<BN, A_MN, B_MN, CG, EPI_WARPS>;
     static PerDeviceOnce attr_set;
     if (attr_set.first()) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     }
     if (launch_k(kern, dim3(grid), dim3(TC_THREADS), Cfg::SMEM, st, CG, ta, tb, tc, tc2, g, num_m, num_n,
-                 num_kb, sk, w.ws, w.flags, epoch) != cudaSuccess)
+                 num_kb) != cudaSuccess)
         return -3;
     note_launches(1);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
@@ -950,16 +772,8 @@ int gemm_tc(const GemmDesc& g, cudaStream_t st) {
     // loop is long (>= 4096); a 2048 x 2048 x 2048 GEMM (64 pair tiles on 74
     // pairs) is faster as 128 single-CTA tiles.
     const long pair_tiles = (long)((g.M + 255) / 256) * ((g.N + 255) / 256);
-    if (g_pair_enabled && (pair_tiles >= g_pair_min_tiles || (pair_tiles >= 32 && g.K >= 4096))) {
-        // 256 x 512 pair tiles when they fill the 74 pairs' waves as well as
-        // 256 x 256 does (same wave efficiency, half the tiles)
-        const long units = num_sms() / 2;
-        const long wide_tiles = (long)((g.M + 255) / 256) * ((g.N + 511) / 512);
-        auto eff = [&](long t) { return (double)t / (double)(((t + units - 1) / units) * units); };
-        if (g_wide_enabled && wide_tiles >= units && eff(wide_tiles) >= eff(pair_tiles) - 0.02)
-            return launch_majors<512, 2>(g, st);
+    if (g_pair_enabled && (pair_tiles >= g_pair_min_tiles || (pair_tiles >= 32 && g.K >= 4096)))
         return launch_majors<256, 2>(g, st);
-    }
     const int num_m = (g.M + TC_BM - 1) / TC_BM;
     // N=128 tiles read 8 KB of operands per 64-cycle MMA (128 B/cycle, the
     // shared-memory limit); N=256 tiles need 96 B/cycle. Prefer 256 whenever

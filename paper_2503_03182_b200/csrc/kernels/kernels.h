@@ -53,14 +53,10 @@ int gemm(int dtype, const GemmDesc& g, cudaStream_t st);
 int gemm_simt(int dtype, const GemmDesc& g, cudaStream_t st);
 // tcgen05 kernel (bf16 only).
 int gemm_tc(const GemmDesc& g, cudaStream_t st);
-// stream-K scheduling on/off for the tcgen05 GEMM (default on)
-void gemm_set_stream_k(int on);
 // CTA-pair (cta_group::2) 256-row tiles on/off (default on)
 void gemm_set_pair(int on);
 // pair tiles from n 256 x 256 tiles on (default 96)
 void gemm_set_pair_min_tiles(int n);
-// 256 x 512 CTA-pair tiles where they fill the waves as well as 256 x 256 (default off: measured slower)
-void gemm_set_wide(int on);
 
 // ---------------------------------------------------------------- layernorm
 // y = (x - mean) * rstd * gamma + beta over rows of length h; saves mean/rstd (fp32).

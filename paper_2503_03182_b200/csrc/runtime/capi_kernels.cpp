@@ -55,10 +55,8 @@ TP_API int tpipe_k_gemm_simt(int dtype, int M, int N, int K, const void* A, long
     return launch_rc(gemm_simt(dtype, g, S(stream)), "gemm_simt");
 }
 
-TP_API void tpipe_k_gemm_set_stream_k(int on) { gemm_set_stream_k(on); }
 TP_API void tpipe_k_gemm_set_pair(int on) { gemm_set_pair(on); }
 TP_API void tpipe_k_gemm_set_pair_min_tiles(int n) { gemm_set_pair_min_tiles(n); }
-TP_API void tpipe_k_gemm_set_wide(int on) { gemm_set_wide(on); }
 
 TP_API int tpipe_k_ln_fwd(int dtype, const void* x, const void* gamma, const void* beta, void* y,
                           float* mean, float* rstd, int rows, int h, void* stream) {

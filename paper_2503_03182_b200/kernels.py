@@ -95,13 +95,5 @@ def tpipe_host_adamw(master, m, v, grad, w_bf16, n, decay, lr, b1, b2, eps, wd, 
                            b2, eps, wd, bc1, bc2)
 
 
-def tpipe_k_gemm_set_stream_k(on):
-    lib().tpipe_k_gemm_set_stream_k(1 if on else 0)
-
-
 def tpipe_k_gemm_set_pair(on):
     lib().tpipe_k_gemm_set_pair(1 if on else 0)
-
-
-def tpipe_k_gemm_set_wide(on):
-    lib().tpipe_k_gemm_set_wide(1 if on else 0)

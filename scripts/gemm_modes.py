@@ -1,5 +1,5 @@
-"""GEMM schedule A/B on the model shapes: single-CTA vs CTA-pair tiles, data-
-parallel vs stream-K (CUDA events, warm). python scripts/gemm_modes.py [c3]"""
+"""GEMM schedule A/B on the model shapes: single-CTA vs CTA-pair tiles (CUDA
+events, warm; the stream-K arm was removed with the schedule). python scripts/gemm_modes.py [c3]"""
 import sys, os, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -42,9 +42,8 @@ for name, m, n, k, ak, bk, epi in shapes:
     bias = torch.zeros(n, device="cuda", dtype=torch.bfloat16)
     row = {"kernel": name, "M": m, "N": n, "K": k}
     for pair in (0, 1):
-        for sk in (0, 1):
+        for sk in (0,):
             K.tpipe_k_gemm_set_pair(pair)
-            K.tpipe_k_gemm_set_stream_k(sk)
             fn = lambda: K.tpipe_k_gemm(1, m, n, k, A, k if ak else m, ak, B, k if bk else n, bk, epi, C, n,
                                         bias=bias, R=Rr, ldr=n, C2=C2, ldc2=n, aux=Rr, ldaux=n)
             ms = timeit(fn)
@@ -53,5 +52,4 @@ for name, m, n, k, ak, bk, epi in shapes:
             tot[key] = tot.get(key, 0.0) + ms
     print(json.dumps(row), flush=True)
 K.tpipe_k_gemm_set_pair(1)
-K.tpipe_k_gemm_set_stream_k(0)
 print(json.dumps({"total_ms_per_layer_set": {k: round(v, 4) for k, v in tot.items()}}))

@@ -37,7 +37,6 @@ for name, m, n, k, ak, bk, epi in shapes:
                          bias=bias, R=Rr, ldr=n, C2=C2, ldc2=n, aux=Rr, ldaux=n))
     calls.append((name, m, n, k, byts, fn))
 K.tpipe_k_gemm_set_pair(1)
-K.tpipe_k_gemm_set_stream_k(0)
 for rep in range(2):
     for c in calls:
         c[5]()

@@ -83,11 +83,10 @@ def test_gemm_bf16_tcgen05(M, N, Kd, majors):
 
 @pytest.mark.parametrize("M,N,Kd", [(512, 512, 4160), (296, 320, 4200), (2048, 2048, 2048)])
 @pytest.mark.parametrize("majors", [(1, 1), (1, 0), (0, 0)])
-def test_gemm_stream_k(M, N, Kd, majors):
-    """Shapes whose whole tiles under-fill the SMs take the stream-K schedule
-    (split tiles summed from per-CTA partials in a fixed order): matches fp64,
-    matches the data-parallel schedule to fp32 rounding, and is bit-identical
-    run to run (fp32 store, fp32 accumulate, bias and dGELU epilogues)."""
+def test_gemm_underfilled(M, N, Kd, majors):
+    """Shapes whose whole tiles under-fill the SMs (a partial last wave, long
+    K): matches fp64 and is bit-identical run to run (fp32 store, fp32
+    accumulate, bias and dGELU epilogues)."""
     ak, bk = majors
     k = K()
     rng = np.random.default_rng(M * 7 + Kd)
@@ -112,14 +111,8 @@ def test_gemm_stream_k(M, N, Kd, majors):
         k.tpipe_k_gemm(1, *args, k.EPI_DGELU, Cd, N, C2=Cg, ldc2=N, aux=U, ldaux=N)
         torch.cuda.synchronize()
         return C, Acc, Cb, Cd
-    try:
-        k.tpipe_k_gemm_set_stream_k(1)
-        r1 = run()
-        r2 = run()
-        k.tpipe_k_gemm_set_stream_k(0)
-        dp = run()
-    finally:
-        k.tpipe_k_gemm_set_stream_k(0)
+    r1 = run()
+    r2 = run()
     for u, v in zip(r1, r2):
         assert torch.equal(u, v)
     C, Acc, Cb, Cd = r1
@@ -127,7 +120,6 @@ def test_gemm_stream_k(M, N, Kd, majors):
     assert max_rel(h(Acc), 1 + ref) < 1e-4
     assert rel_l2(h(Cb), ref + h(bias)) < 1e-2
     assert rel_l2(h(Cd), ref * R.gelu_grad(h(U))) < 1e-2
-    assert max_rel(h(C), h(dp[0])) < 1e-5
 
 
 @pytest.mark.parametrize("M,N,Kd", [(2048, 6144, 2048), (2000, 2080, 4200), (4096, 2816, 520)])
@@ -175,11 +167,9 @@ def test_gemm_cta_pair(M, N, Kd, majors):
 @pytest.mark.parametrize("M,N,Kd", [(2048, 8192, 2048), (8192, 2048, 1024), (2000, 8992, 320),
                                     (2048, 50304, 256)])
 @pytest.mark.parametrize("majors", [(1, 1), (1, 0), (0, 0)])
-def test_gemm_wide_pair(M, N, Kd, majors):
-    """256 x 512 CTA-pair tiles (two N = 256 MMAs per K step, one TMEM
-    accumulator) incl. ragged M / N / K edges and a last N tile whose second
-    half lies wholly beyond N: matches fp64 and is bit-identical to the
-    256 x 256 pair tiling (same per-element K order) for fp32 store, fp32
+def test_gemm_pair_ragged(M, N, Kd, majors):
+    """CTA-pair shapes incl. ragged M / N / K edges and the vocabulary-wide
+    N: matches fp64 and is bit-identical run to run for fp32 store, fp32
     accumulate, bias+GELU and dGELU epilogues."""
     ak, bk = majors
     k = K()
@@ -206,18 +196,14 @@ def test_gemm_wide_pair(M, N, Kd, majors):
         k.tpipe_k_gemm(1, *args, k.EPI_BIAS_GELU, Cu, N, bias=bias, C2=Cgl, ldc2=N)
         torch.cuda.synchronize()
         return C, Acc, Cd, Cg, Cu, Cgl
-    try:
-        k.tpipe_k_gemm_set_wide(1)
-        wide = run()
-    finally:
-        k.tpipe_k_gemm_set_wide(0)
-    narrow = run()
-    C, Acc, Cd, Cg, Cu, Cgl = wide
+    first = run()
+    again = run()
+    C, Acc, Cd, Cg, Cu, Cgl = first
     assert max_rel(h(C), ref) < 1e-4
     assert max_rel(h(Acc), 2 + ref) < 1e-4
     assert rel_l2(h(Cd), ref * R.gelu_grad(h(U))) < 1e-2
     assert rel_l2(h(Cu), ref + h(bias)) < 1e-2
-    for u, v in zip(wide, narrow):
+    for u, v in zip(first, again):
         assert torch.equal(u, v)
 
 
