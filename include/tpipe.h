@@ -278,6 +278,11 @@ int tpipe_plan_chunk_params(const tpipe_plan* plan, int32_t stage, int32_t chunk
                                     interprocess events, POSIX-shm mailbox (`ipc_name`); works
                                     across GPUs (NVLink peer access) and for several ranks on
                                     one GPU (tests) */
+#define TPIPE_TRANSPORT_NCCL_LOOPBACK 2   /* stage = -1 only: the in-process virtual pipeline
+                                    with every message moved by an ncclSend / ncclRecv pair on a
+                                    one-rank communicator (rank 0 to itself) — runs the NCCL
+                                    library path on one GPU, where NCCL refuses two ranks per
+                                    device (profiles/r2_nccl_samegpu_refused.txt); tests */
 
 /* debug_flags */
 #define TPIPE_DEBUG_POOL_CANARY 1u  /* guard bytes after every pool allocation, checked after

@@ -923,7 +923,10 @@ TP_API int tpipe_runtime_create(const tpipe_plan* plan, const tpipe_runtime_opts
         }
         ipc_pipe += "_r" + std::to_string(o.dp_rank);   // each replica's own pipeline rendezvous
     }
-    if (o.stage < 0 || P.p == 1) {
+    if ((o.stage < 0 || P.p == 1) && o.transport == TPIPE_TRANSPORT_NCCL_LOOPBACK) {
+        TRY(make_virtual_nccl_transport(P.channels, &rt->tr));
+        rt->transport_kind = TPIPE_TRANSPORT_NCCL_LOOPBACK;
+    } else if (o.stage < 0 || P.p == 1) {
         rt->tr = make_virtual_transport(P.channels);
         rt->transport_kind = -1;
     } else if (o.transport == TPIPE_TRANSPORT_IPC) {

@@ -69,8 +69,12 @@ public:
     explicit VirtualTransport(size_t n) : q_(n), popped_(n, 0), done_(n) {}
     ~VirtualTransport() override {
         for (auto e : ev_) cudaEventDestroy(e);
+        if (comm_) {
+            if (aborted_ && nccl()->CommAbort) nccl()->CommAbort(comm_);
+            else nccl()->CommDestroy(comm_);
+        }
     }
-    const char* name() const override { return "virtual"; }
+    const char* name() const override { return comm_ ? "virtual-nccl" : "virtual"; }
     void begin_step() override {
         for (auto& q : q_) q.clear();
         for (auto& n : popped_) n = 0;
@@ -97,7 +101,19 @@ public:
         q_[ch].pop_front();
         cudaEvent_t d = ev();
         cudaError_t e = cudaStreamWaitEvent(cs, mg.ready, 0);
-        if (!e) e = cudaMemcpyAsync(dst, mg.src, bytes, cudaMemcpyDeviceToDevice, cs);
+        if (!e && comm_) {
+            // loopback: the message travels as an ncclSend / ncclRecv pair on
+            // the one-rank communicator (rank 0 to itself), on the receiver's stream
+            const NcclApi* N = nccl();
+            ncclResult_t r = N->GroupStart();
+            if (r == ncclSuccess) r = N->Send(mg.src, bytes, ncclUint8, 0, comm_, cs);
+            if (r == ncclSuccess) r = N->Recv(dst, bytes, ncclUint8, 0, comm_, cs);
+            const ncclResult_t r2 = N->GroupEnd();
+            if (r == ncclSuccess) r = r2;
+            if (r != ncclSuccess) return set_error(TPIPE_E_NCCL, "loopback ncclSend/ncclRecv: %s", N->GetErrorString(r));
+        } else if (!e) {
+            e = cudaMemcpyAsync(dst, mg.src, bytes, cudaMemcpyDeviceToDevice, cs);
+        }
         if (!e) e = cudaEventRecord(d, cs);
         if (e) return set_error(TPIPE_E_CUDA, "virtual recv copy: %s", cudaGetErrorString(e));
         done_[ch].push_back(d);
@@ -110,6 +126,31 @@ public:
     }
     bool recv_ready(int ch) const override { return !q_[ch].empty(); }
     bool send_wait_ready(int ch, int msg) const override { return popped_[ch] > msg; }
+    int sync(cudaStream_t cs, int timeout_ms) override {
+        if (!comm_) return Transport::sync(cs, timeout_ms);
+        const NcclApi* N = nccl();
+        const auto t0 = Clock::now();
+        for (;;) {
+            cudaError_t e = cudaStreamQuery(cs);
+            if (e == cudaSuccess) return 0;
+            if (e != cudaErrorNotReady) return set_error(TPIPE_E_CUDA, "step stream: %s", cudaGetErrorString(e));
+            ncclResult_t ae = ncclSuccess;
+            if (N->CommGetAsyncError && N->CommGetAsyncError(comm_, &ae) == ncclSuccess && ae != ncclSuccess &&
+                ae != ncclInProgress) {
+                abort();
+                return set_error(TPIPE_E_NCCL, "NCCL asynchronous error: %s", N->GetErrorString(ae));
+            }
+            if (ms_since(t0) > timeout_ms) {
+                abort();
+                return set_error(TPIPE_E_TIMEOUT, "step did not complete within %d ms", timeout_ms);
+            }
+            std::this_thread::sleep_for(std::chrono::microseconds(50));
+        }
+    }
+    void abort() override { aborted_ = true; }
+
+    ncclComm_t comm_ = nullptr;   // NCCL loopback (TPIPE_TRANSPORT_NCCL_LOOPBACK)
+    bool aborted_ = false;
 
 private:
     std::vector<std::deque<Msg>> q_;
@@ -470,6 +511,22 @@ public:
 
 std::unique_ptr<Transport> make_virtual_transport(const ChannelList& ch) {
     return std::unique_ptr<Transport>(new VirtualTransport(ch.size()));
+}
+
+int make_virtual_nccl_transport(const ChannelList& ch, std::unique_ptr<Transport>* out) {
+    const NcclApi* N = nccl();
+    if (!N) return set_error(TPIPE_E_NCCL, "libnccl.so.2 not loadable");
+    ncclUniqueId id;
+    ncclResult_t r = N->GetUniqueId(&id);
+    if (r != ncclSuccess) return set_error(TPIPE_E_NCCL, "ncclGetUniqueId: %s", N->GetErrorString(r));
+    std::unique_ptr<VirtualTransport> T(new VirtualTransport(ch.size()));
+    r = N->CommInitRank(&T->comm_, 1, id, 0);
+    if (r != ncclSuccess) {
+        T->comm_ = nullptr;
+        return set_error(TPIPE_E_NCCL, "ncclCommInitRank (1 rank): %s", N->GetErrorString(r));
+    }
+    *out = std::move(T);
+    return 0;
 }
 
 int make_nccl_transport(const ChannelList& chl, int stage, const void* ids_, int timeout_ms,

@@ -2,7 +2,7 @@
 // [b·s, h] activation (forward) or activation-gradient (backward) message per
 // (chunk boundary, micro-batch) — the pipeline-parallel P2P of P:195 / P:210.
 //
-// One interface, three implementations; the runtime's SEND / RECV /
+// One interface, three implementations (plus an NCCL loopback of the first); the runtime's SEND / RECV /
 // SEND_WAIT instructions are the same code for all of them:
 //   * virtual — every stage in one process on one GPU (stage == -1); a
 //     message is a device-to-device copy from the sender's MSG buffer, the
@@ -62,6 +62,11 @@ public:
 using ChannelList = std::vector<std::array<int, 3>>;   // {kind, src, dst}
 
 std::unique_ptr<Transport> make_virtual_transport(const ChannelList& ch);
+// the virtual transport with every message moved by an ncclSend / ncclRecv
+// pair on a one-rank communicator (rank 0 to itself): runs the NCCL library
+// path — dlopen'd entry points, group calls, stream ordering, asynchronous
+// error polling — on one GPU, where NCCL refuses two ranks per device
+int make_virtual_nccl_transport(const ChannelList& ch, std::unique_ptr<Transport>* out);
 
 int make_nccl_transport(const ChannelList& ch, int stage, const void* ids, int timeout_ms,
                         std::unique_ptr<Transport>* out);

@@ -16,6 +16,7 @@ STEP_OP_TIMES = 4
 
 TRANSPORT_NCCL = 0
 TRANSPORT_IPC = 1
+TRANSPORT_NCCL_LOOPBACK = 2   # stage = -1: virtual pipeline, messages as ncclSend/ncclRecv to self
 DEBUG_POOL_CANARY = 1
 DEBUG_POOL_CANARY_SELFTEST = 2
 

@@ -121,10 +121,12 @@ def test_multiprocess_p8_fp32_parity(tmp_path, strategy, offload):
     check_vs_oracle(C1_16, 8, 16, strategy, 0, res, 1e-4, max_rel)
 
 
-def _virtual(cfg, p, m, strategy, dtype, steps, offload=0):
+def _virtual(cfg, p, m, strategy, dtype, steps, offload=0, transport=None):
     from paper_2503_03182_b200 import params as PR, runtime as RT
     plan = _plan(cfg, p, m, strategy, dtype, offload)
-    rt = RT.Runtime(plan, stage=-1, lr=1e-3)
+    rt = RT.Runtime(plan, stage=-1, lr=1e-3, **({} if transport is None else {"transport": transport}))
+    if transport is not None:
+        assert rt.stats()["transport"] == transport
     W = synth.weights(cfg["L"], cfg["h"], cfg["f"], cfg["V"], cfg["s"], seed=11, std=0.05,
                       bias_std=0.02, ln_jitter=0.05)
     for s in range(p):
@@ -267,3 +269,23 @@ def test_multiprocess_v3_dp2_fp32(tmp_path):
                 ref = G["layers"][l][kk] if l is not None else G[kk]
                 assert max_rel(gg, ref) <= 1e-4, (s, c, kk, l)
             assert np.array_equal(res[(0, s)][f"param{c}"], res[(1, s)][f"param{c}"])
+
+
+@pytest.mark.parametrize("p,strategy,offload,cfg,m", [
+    (4, "interleave_trecomp", 0, C1, 8),
+    (8, "tpipe_trecomp", 5, C1_16, 16),
+])
+def test_nccl_loopback_bitexact_vs_virtual(p, strategy, offload, cfg, m):
+    """NCCL refuses two ranks on one GPU (profiles/r2_nccl_samegpu_refused.txt),
+    so the NCCL library path runs here as a loopback: every stage-to-stage
+    message of the virtual pipeline is an ncclSend / ncclRecv pair on a
+    one-rank communicator (TPIPE_TRANSPORT_NCCL_LOOPBACK), with the step's
+    completion polling ncclCommGetAsyncError. bf16, 2 optimizer steps:
+    bit-identical to the device-copy virtual pipeline."""
+    from paper_2503_03182_b200 import runtime as RT
+    ref = _virtual(cfg, p, m, strategy, 1, 2, offload)
+    got = _virtual(cfg, p, m, strategy, 1, 2, offload, transport=RT.TRANSPORT_NCCL_LOOPBACK)
+    assert got[0] == ref[0] and got[2] == ref[2]
+    for part in (1, 3):
+        for k, v in ref[part].items():
+            assert np.array_equal(got[part][k].view(np.uint32), v.view(np.uint32)), k
