@@ -35,6 +35,22 @@ namespace tpipe {
 namespace fa5 {
 
 constexpr int BR = 128;          // rows per tile (queries or keys)
+
+// Timeline tracing for the probe build only (scripts/attn_trace.py compiles a
+// separate library with -DTPIPE_ATTN_TRACE): SM clock stamps of CTA 0's role
+// events, [event][index] with TR_N indices per event.
+#ifdef TPIPE_ATTN_TRACE
+constexpr int TR_N = 512;
+__device__ unsigned long long* g_trace;
+#define TR(ev, idx)                                                               \
+    do {                                                                          \
+        if (blockIdx.x == 0 && (idx) < TR_N) g_trace[(ev) * TR_N + (idx)] = clock64(); \
+    } while (0)
+#else
+#define TR(ev, idx) \
+    do {            \
+    } while (0)
+#endif
 constexpr float LOG2E = 1.4426950408889634f;
 
 __device__ __forceinline__ void fence_async_smem() {
@@ -130,6 +146,34 @@ __device__ __forceinline__ float ex2(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// 2^x for a pair of x <= 8 on the FMA pipe (the forward softmax is bound by
+// the MUFU pipe: 16 ex2 / clk / SM for 128 x 128 scores per tile; part of the
+// exponentials go here instead). x = j + f, j = round(x) via the 1.5*2^23
+// trick, f in [-0.5, 0.5]; 2^f by a degree-3 polynomial (relative-error fit,
+// max 7.5e-5 — below bf16's 2^-9 rounding of P); 2^j added to the exponent
+// bits (the magic's low 9 bits are zero, so bits(t) << 23 == j << 23).
+// x is clamped at -125 (result ~2^-125 instead of 0: negligible against the
+// row sum >= 1; only off-diagonal tiles, where no score is masked, use it).
+__device__ __forceinline__ void ex2_poly2(uint64_t x2, float& p0, float& p1) {
+    float a, b;
+    upk2(x2, a, b);
+    const uint64_t xc = pk2(fmaxf(a, -125.f), fmaxf(b, -125.f));
+    const uint64_t t = fadd2(xc, pk2(12582912.f, 12582912.f));
+    const uint64_t jf = fadd2(t, pk2(-12582912.f, -12582912.f));
+    const uint64_t f = ffma2(jf, pk2(-1.f, -1.f), xc);
+    uint64_t q = ffma2(f, pk2(0.0551716611f, 0.0551716611f), pk2(0.242611155f, 0.242611155f));
+    q = ffma2(q, f, pk2(0.693260968f, 0.693260968f));
+    q = ffma2(q, f, pk2(0.999928057f, 0.999928057f));
+    float t0, t1, q0, q1;
+    upk2(t, t0, t1);
+    upk2(q, q0, q1);
+    p0 = __uint_as_float(__float_as_uint(q0) + (__float_as_uint(t0) << 23));
+    p1 = __uint_as_float(__float_as_uint(q1) + (__float_as_uint(t1) << 23));
+}
+// pairs (of the 32 per thread per tile) whose exponentials use ex2_poly2
+#ifndef FWD_POLY_OF_16
+#define FWD_POLY_OF_16 4
+#endif
 __device__ __forceinline__ uint32_t bf2(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t*>(&v);
@@ -140,6 +184,23 @@ __device__ __forceinline__ void st_row32_pk(uint8_t* tile, int r, int col0, cons
     const uint32_t base = smem_u32(tile);
 #pragma unroll
     for (int q = 0; q < 4; ++q) sts128(base + swz(r, c0 + q), w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+}
+
+// 32 lanes x 16 columns store (thread t writes lane base+t)
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+// smem -> TMEM copy of one K-step (16 bf16 = 256 bits per row) of a 128-row
+// operand tile, described by its MMA shared-memory descriptor: row i lands in
+// lane i, 8 columns — the A-operand layout of a TS tcgen05.mma. Issued by the
+// MMA thread: tcgen05.cp and tcgen05.mma execute in issue order.
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+    asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
 }
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
@@ -163,12 +224,18 @@ __device__ __forceinline__ int sched_item(int k, int T) {
 // S double-buffered in TMEM (columns [0,128) and [128,256)); P_j is written
 // back over S_j as packed bf16 (64 columns) and consumed as the TMEM
 // A-operand of O += P_j V_j; O (D columns at 256) accumulates in TMEM and is
-// rescaled in place by the row threads when the running max moves.
+// rescaled in place by the row threads when the running max moves. The
+// item's Q is copied into TMEM (columns [384, 384 + D/2), tcgen05.cp) and is
+// the TMEM A operand of S = Q K^T: both MMAs read only K or V from shared
+// memory (an SS MMA is bound by the tensor core's ~64 B/clk shared-memory
+// operand path: profiles/r2_mma_rate.jsonl).
 // All rings (K/V stages, S buffers, P/PV handshakes) run on a global tile
 // counter g that continues across this CTA's items, so the S MMA of an item's
 // first tile overlaps the previous item's last softmax and epilogue; Q is
-// double-buffered per item.
-//   MMA  : S_0 | for g: [S_{g+1} once PV_{g-1} freed its buffer] [PV_g once P_g ready]
+// double-buffered per item in shared memory.
+//   MMA  : S_0 | for g: [S_{g+1}] [PV_g once P_g ready] — S_{g+1} overwrites
+//          P_{g-1}, read by PV_{g-1} issued before it (tcgen05.mma runs in
+//          issue order), so no wait for PV_{g-1} to finish
 //   rows : S_g -> P_g (one pass, 64 scores per thread in registers) -> wait PV_{g-1}
 //          -> O *= corr_g (skipped per warp when corr == 1) -> P_g ready
 // Item t (heaviest first): qb = nqb-1 - t/(a*nb), head = t%a, batch = (t/a)%nb.
@@ -234,7 +301,7 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t tmem = *tmem_slot;
     pdl_wait();
     pdl_trigger();
-    const uint32_t tO = tmem + 256;
+    const uint32_t tO = tmem + 256, tQ = tmem + 384;
 
     if (warp == 0) {
         {   // whole warp waits; the elected lane issues the TMA loads
@@ -255,6 +322,7 @@ __global__ void __launch_bounds__(384, 1)
                     const int st = g % STAGES;
                     const uint32_t ph = ((g / STAGES) & 1) ^ 1;
                     mbar_wait(&k_empty[st], ph);
+                    if (lane == 0) TR(0, g);
                     if (elect_one()) {
                         mbar_arrive_expect_tx(&k_full[st], TB);
                         tma_tile<D>(sK + st * TB, &tm_qkv, &k_full[st], h + head * D, b * s + j * BR);
@@ -283,19 +351,29 @@ __global__ void __launch_bounds__(384, 1)
             }
             auto issue_s = [&]() {
                 const int sl = k_s & 1;
-                if (j_s == 0) mbar_wait(&q_full[sl], (k_s >> 1) & 1);
+                if (j_s == 0) {
+                    // the item's Q -> TMEM, after the previous item's S MMAs (issue order)
+                    mbar_wait(&q_full[sl], (k_s >> 1) & 1);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint32_t aQ = smem_u32(sQ + sl * TB);
+#pragma unroll
+                        for (int kk = 0; kk < D / 16; ++kk) tmem_cp_128x256b(tQ + kk * 8, desc_k(aQ, kk));
+                        umma_commit(&q_empty[sl]);   // smem Q free once copied
+                    }
+                    __syncwarp();
+                }
                 const int st = gs % STAGES;
                 mbar_wait(&k_full[st], (gs / STAGES) & 1);
                 tc_fence_after();
-                const uint32_t aQ = smem_u32(sQ + sl * TB);
                 const uint32_t aK = smem_u32(sK + st * TB);
                 const uint32_t tS = tmem + (gs & 1) * 128;
+                if (lane == 0) TR(1, gs);
                 if (elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk) umma_bf16(tS, desc_k(aQ, kk), desc_k(aK, kk), iS, kk > 0);
+                    for (int kk = 0; kk < D / 16; ++kk) umma_bf16_ts(tS, tQ + kk * 8, desc_k(aK, kk), iS, kk > 0);
                     umma_commit(&s_full[gs & 1]);
                     umma_commit(&k_empty[st]);
-                    if (j_s == nkb_s - 1) umma_commit(&q_empty[sl]);   // Q of this item fully consumed
                 }
                 __syncwarp();
                 ++gs;
@@ -313,16 +391,14 @@ __global__ void __launch_bounds__(384, 1)
                 if (t < 0) break;
                 const int nkb = nqb - t / (a * nb);
                 for (int j = 0; j < nkb; ++j, ++g) {
-                    if (have_s) {
-                        if (g >= 1) mbar_wait(pv_done, (g - 1) & 1);   // S buffer (g+1)&1 held P_{g-1}
-                        issue_s();
-                    }
+                    if (have_s) issue_s();   // S buffer (g+1)&1 held P_{g-1}: PV_{g-1} was issued first
                     mbar_wait(p_full, g & 1);
                     const int st = g % STAGES;
                     mbar_wait(&v_full[st], (g / STAGES) & 1);
                     tc_fence_after();
                     const uint32_t aV = smem_u32(sV + st * TB);
                     const uint32_t tP = tmem + (g & 1) * 128;
+                    if (lane == 0) TR(2, g);
                     if (elect_one()) {
 #pragma unroll
                         for (int kk = 0; kk < BR / 16; ++kk)
@@ -353,6 +429,7 @@ __global__ void __launch_bounds__(384, 1)
             for (int j = 0; j < nkb; ++j, ++g) {
                 const uint32_t tS = tmem + (g & 1) * 128 + lane_off;
                 mbar_wait(&s_full[g & 1], (g >> 1) & 1);
+                if (threadIdx.x == 128) TR(3, g);
                 tc_fence_after();
                 float sv[64];
                 {
@@ -379,18 +456,42 @@ __global__ void __launch_bounds__(384, 1)
                 lmx *= sc;
                 float* mb = sMax + (g & 1) * 2 * BR;
                 mb[cg * BR + r] = lmx;
+                if (threadIdx.x == 128) TR(4, g);
                 named_bar_sync(1, 256);
-                const float mx = fmax3(m, lmx, mb[(cg ^ 1) * BR + r]);
+                // lazy rescaling: the reference max moves only when a score exceeds
+                // it by more than 2^8 (P <= 256 is exact enough in bf16 and the sums
+                // are fp32), so O is rarely rescaled; both column groups see the
+                // same values and take the same decision
+                const float mnew = fmax3(m, lmx, mb[(cg ^ 1) * BR + r]);
+                const float mx = mnew - m > 8.0f ? mnew : m;
                 const uint64_t sc2 = pk2(sc, sc), nm2 = pk2(-mx, -mx);
                 uint64_t rs2 = pk2(0.f, 0.f);
                 uint32_t pk[32];
+                if (j < nkb - 1) {   // no masked score: part of the exponentials on the FMA pipe
 #pragma unroll
-                for (int e = 0; e < 64; e += 2) {
-                    float x0, x1;
-                    upk2(ffma2(pk2(sv[e], sv[e + 1]), sc2, nm2), x0, x1);
-                    const float p0 = ex2(x0), p1 = ex2(x1);
-                    rs2 = fadd2(rs2, pk2(p0, p1));
-                    pk[e / 2] = bf2(p0, p1);
+                    for (int e = 0; e < 64; e += 2) {
+                        const uint64_t x2 = ffma2(pk2(sv[e], sv[e + 1]), sc2, nm2);
+                        float p0, p1;
+                        if (((e >> 1) & 15) < FWD_POLY_OF_16) {
+                            ex2_poly2(x2, p0, p1);
+                        } else {
+                            float x0, x1;
+                            upk2(x2, x0, x1);
+                            p0 = ex2(x0);
+                            p1 = ex2(x1);
+                        }
+                        rs2 = fadd2(rs2, pk2(p0, p1));
+                        pk[e / 2] = bf2(p0, p1);
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 64; e += 2) {
+                        float x0, x1;
+                        upk2(ffma2(pk2(sv[e], sv[e + 1]), sc2, nm2), x0, x1);
+                        const float p0 = ex2(x0), p1 = ex2(x1);
+                        rs2 = fadd2(rs2, pk2(p0, p1));
+                        pk[e / 2] = bf2(p0, p1);
+                    }
                 }
                 float rs0, rs1;
                 upk2(rs2, rs0, rs1);
@@ -399,6 +500,7 @@ __global__ void __launch_bounds__(384, 1)
                 l = l * corr + rs;        // partial (this group's columns), same m history
                 m = mx;
                 tmem_st32(tS + cg * 32, pk);   // P_g over S_g: packed cols [32cg, 32cg+32)
+                if (threadIdx.x == 128) TR(5, g);
                 if (j > 0) {
                     mbar_wait(pv_done, (g - 1) & 1);
                     tc_fence_after();
@@ -416,6 +518,8 @@ __global__ void __launch_bounds__(384, 1)
                 }
                 tmem_wait_st();
                 tc_fence_before();
+                if (threadIdx.x == 128) TR(6, g);
+                if (threadIdx.x == 383) TR(7, g);
                 mbar_arrive(p_full);
             }
             sSum[cg * BR + r] = l;
@@ -490,15 +594,19 @@ __device__ __forceinline__ void st_row32_h(uint8_t* tile, int r, int col0, const
 // (with 2 slots every half paid one L2 round trip). Sized to the 227 KB limit.
 template <int D>
 struct BwdCfg {
-    static constexpr int NQ = D == 128 ? 3 : 4;
-    static constexpr int NK = 4;
+    static constexpr int NQ = D == 128 ? 5 : 6;
+    static constexpr int NK = D == 128 ? 5 : 6;
 };
 
 // dK/dV (persistent): an item is 128 keys of one (sequence, head); it loops
 // over 64-query halves from the diagonal. Item t (heaviest first):
 // kb = t/(a*nb), head = t%a, batch = (t/a)%nb. Half rings (Q/dO halves, S/dP
-// TMEM buffers, P/dS smem) run on a global half counter across items; K/V are
-// single-buffered per item and released after the item's last S MMA.
+// TMEM buffers) run on a global half counter across items; K/V are
+// single-buffered per item and released after the item's last S MMA. P^T and
+// dS^T are written back over S^T / dP^T in TMEM (bf16, each column group
+// inside its own columns) and feed dV += P^T dO, dK += dS^T Q as TMEM A
+// operands: no shared-memory round trip (the kernel was shared-memory
+// bandwidth bound, profiles/r2_attn_trace.txt).
 template <int D>
 __global__ void __launch_bounds__(384, 1)
     dkdv2_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_qkv64,
@@ -513,9 +621,7 @@ __global__ void __launch_bounds__(384, 1)
     uint8_t* sV = sK + TB;
     uint8_t* sQ = sV + TB;                 // [NQ] half tiles
     uint8_t* sO = sQ + NQ * HB;            // [NQ] dO half tiles
-    uint8_t* sP = sO + NQ * HB;            // [2] P^T  [128 keys][64 q] (one atom, 16 KB)
-    uint8_t* sS = sP + 2 * BR * 128;       // [2] dS^T
-    float* sL = reinterpret_cast<float*>(sS + 2 * BR * 128);   // [2][64]
+    float* sL = reinterpret_cast<float*>(sO + NQ * HB);        // [2][64]
     float* sD = sL + 2 * HR;                                   // [2][64]
     uint64_t* bar = reinterpret_cast<uint64_t*>(sD + 2 * HR);
     uint64_t* kv_full = bar;
@@ -591,6 +697,7 @@ __global__ void __launch_bounds__(384, 1)
                 for (int hh = 0; hh < nh; ++hh, ++g) {
                     const int sl = g % NQ;
                     mbar_wait(&q_empty[sl], ((g / NQ) & 1) ^ 1);
+                    if (lane == 0) TR(8, g);
                     const int qrow = row0 + (2 * kb + hh) * HR;
                     if (elect_one()) {
                         mbar_arrive_expect_tx(&q_full[sl], 2 * HB);
@@ -620,6 +727,7 @@ __global__ void __launch_bounds__(384, 1)
                 tc_fence_after();
                 const uint32_t aQ = smem_u32(sQ + sl * HB), aO = smem_u32(sO + sl * HB);
                 const uint32_t tS = tmem + (gs & 1) * 128, tP = tS + 64;
+                if (lane == 0) TR(9, gs);
                 if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < D / 16; ++kk) {
@@ -651,12 +759,15 @@ __global__ void __launch_bounds__(384, 1)
                     tc_fence_after();
                     const int qs = g % NQ;
                     const uint32_t aQ = smem_u32(sQ + qs * HB), aO = smem_u32(sO + qs * HB);
-                    const uint32_t aP = smem_u32(sP + sl * BR * 128), aS = smem_u32(sS + sl * BR * 128);
+                    const uint32_t tPt = tmem + sl * 128, tSt = tPt + 64;   // P^T, dS^T (packed)
+                    if (lane == 0) TR(10, g);
                     if (elect_one()) {
+                        // queries [32c, 32c+32) of a half sit packed in columns [32c, 32c+16)
 #pragma unroll
                         for (int kk = 0; kk < HR / 16; ++kk) {
-                            umma_bf16(tdV, desc_k(aP, kk), desc_mn_h(aO, kk), iG, (hh | kk) > 0);  // dV += P^T dO
-                            umma_bf16(tdK, desc_k(aS, kk), desc_mn_h(aQ, kk), iG, (hh | kk) > 0);  // dK += dS^T Q
+                            const uint32_t ca = (kk >> 1) * 32 + (kk & 1) * 8;
+                            umma_bf16_ts(tdV, tPt + ca, desc_mn_h(aO, kk), iG, (hh | kk) > 0);  // dV += P^T dO
+                            umma_bf16_ts(tdK, tSt + ca, desc_mn_h(aQ, kk), iG, (hh | kk) > 0);  // dK += dS^T Q
                         }
                         umma_commit(&g_done[sl]);
                         umma_commit(&q_empty[qs]);
@@ -709,14 +820,14 @@ __global__ void __launch_bounds__(384, 1)
             for (int hh = 0; hh < nh; ++hh, ++g) {
                 const int sl = g & 1;
                 const int q0 = (2 * kb + hh) * HR;
-                // P/dS buffer `sl` was last read by the MMAs of half g-2
-                if (g >= 2) mbar_wait(&g_done[sl], ((g - 2) >> 1) & 1);
+                // (TMEM buffer `sl`'s P^T / dS^T of half g-2 were read by dV / dK
+                // MMAs issued before S_g: tcgen05.mma executes in issue order)
                 mbar_wait(&ld_full[sl], (g >> 1) & 1);
+                if (threadIdx.x == 128) TR(11, g);
                 mbar_wait(&s_full[sl], (g >> 1) & 1);
+                if (threadIdx.x == 128) TR(12, g);
                 tc_fence_after();
                 const uint32_t tS = tmem + sl * 128 + lane_off, tP = tS + 64;
-                uint8_t* P = sP + sl * BR * 128;
-                uint8_t* Sd = sS + sl * BR * 128;
                 const float* L = sL + sl * HR;
                 const float* Dq = sD + sl * HR;
                 {
@@ -727,6 +838,7 @@ __global__ void __launch_bounds__(384, 1)
                     tmem_wait_ld();
                     // P^T = exp2(S^T sc - L_q); every key of the block precedes every
                     // query of this column group except on the diagonal halves
+                    if (threadIdx.x == 128) TR(13, g);
                     const int qc = q0 + c * 32;
                     const bool full = qc >= kb * BR + BR - 1 && qc + 32 <= s;
                     const uint64_t sc2 = pk2(sc, sc);
@@ -760,12 +872,14 @@ __global__ void __launch_bounds__(384, 1)
                         wp[e / 2] = bf2(p[e], p[e + 1]);
                         wd[e / 2] = bf2(d0, d1);
                     }
-                    st_row32_pk(P, r, c * 32, wp);
-                    st_row32_pk(Sd, r, c * 32, wd);
+                    tmem_st16(tS + c * 32, wp);   // P^T over this group's own S^T columns
+                    tmem_st16(tP + c * 32, wd);   // dS^T over its own dP^T columns
                 }
                 mbar_arrive(&ld_empty[sl]);
-                fence_async_smem();
+                tmem_wait_st();
                 tc_fence_before();
+                if (threadIdx.x == 128) TR(14, g);
+                if (threadIdx.x == 383) TR(15, g);
                 mbar_arrive(&p_full[sl]);
             }
             mbar_wait(&g_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
@@ -812,8 +926,13 @@ __global__ void __launch_bounds__(384, 1)
 
 // dQ (persistent): an item is 128 queries of one (sequence, head); it loops
 // over 64-key halves up to the diagonal. Item t (heaviest first):
-// qb = nqb-1 - t/(a*nb). Q/dO single-buffered per item (released after the
-// item's last S MMA); K/V halves, S/dP buffers and dS smem on a global ring.
+// qb = nqb-1 - t/(a*nb). Shared memory holds only the streamed operands: the
+// item's Q / dO tiles are copied once into TMEM (tcgen05.cp, the A operands
+// of the S and dP MMAs) and dS is written back over S in TMEM (the A operand
+// of dQ += dS K), so per 64-key half the tensor core reads just the K and V
+// halves from shared memory (profiles/r2_attn_trace.txt: the smem-operand
+// version was shared-memory-bandwidth bound). TMEM: S/dP [2 buffers x 128],
+// dQ [128], Q [64], dO [64] columns.
 template <int D>
 __global__ void __launch_bounds__(384, 1)
     dq2_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
@@ -828,8 +947,7 @@ __global__ void __launch_bounds__(384, 1)
     uint8_t* sO = sQ + TB;
     uint8_t* sK = sO + TB;              // [NK] half tiles
     uint8_t* sV = sK + NK * HB;         // [NK]
-    uint8_t* sS = sV + NK * HB;         // [2] dS [128 q][64 keys] (one atom)
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sS + 2 * BR * 128);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sV + NK * HB);
     uint64_t* q_full = bar;
     uint64_t* q_empty = bar + 1;
     uint64_t* kv_full = bar + 2;          // [NK]
@@ -879,7 +997,7 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t tmem = *tmem_slot;
     pdl_wait();
     pdl_trigger();
-    const uint32_t tdQ = tmem + 256;
+    const uint32_t tdQ = tmem + 256, tQ = tmem + 384, tdO = tmem + 448;
 
     if (warp == 0) {
         {   // whole warp waits; the elected lane issues the TMA loads
@@ -901,6 +1019,7 @@ __global__ void __launch_bounds__(384, 1)
                 for (int hh = 0; hh < nh; ++hh, ++g) {
                     const int sl = g % NK;
                     mbar_wait(&kv_empty[sl], ((g / NK) & 1) ^ 1);
+                    if (lane == 0) TR(16, g);
                     if (elect_one()) {
                         mbar_arrive_expect_tx(&kv_full[sl], 2 * HB);
                         tma_half<D>(sK + sl * HB, &tm_qkv64, &kv_full[sl], h + head * D, row0 + hh * HR);
@@ -924,19 +1043,33 @@ __global__ void __launch_bounds__(384, 1)
             }
             auto issue_s = [&]() {
                 const int sl = gs % NK;
-                if (h_s == 0) mbar_wait(q_full, k_s & 1);
+                if (h_s == 0) {
+                    // the item's Q, dO -> TMEM (after the previous item's last S / dP
+                    // MMAs read the old copies: tcgen05.cp and .mma run in issue order)
+                    mbar_wait(q_full, k_s & 1);
+                    tc_fence_after();
+                    if (elect_one()) {
+#pragma unroll
+                        for (int kk = 0; kk < D / 16; ++kk) {
+                            tmem_cp_128x256b(tQ + kk * 8, desc_k(aQ, kk));
+                            tmem_cp_128x256b(tdO + kk * 8, desc_k(aO, kk));
+                        }
+                        umma_commit(q_empty);   // smem Q, dO free once copied
+                    }
+                    __syncwarp();
+                }
                 mbar_wait(&kv_full[sl], (gs / NK) & 1);
                 tc_fence_after();
                 const uint32_t aK = smem_u32(sK + sl * HB), aV = smem_u32(sV + sl * HB);
                 const uint32_t tS = tmem + (gs & 1) * 128, tP = tS + 64;
+                if (lane == 0) TR(17, gs);
                 if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < D / 16; ++kk) {
-                        umma_bf16(tS, desc_k(aQ, kk), desc_k_h(aK, kk), iS, kk > 0);   // S = Q K^T
-                        umma_bf16(tP, desc_k(aO, kk), desc_k_h(aV, kk), iS, kk > 0);   // dP = dO V^T
+                        umma_bf16_ts(tS, tQ + kk * 8, desc_k_h(aK, kk), iS, kk > 0);    // S = Q K^T
+                        umma_bf16_ts(tP, tdO + kk * 8, desc_k_h(aV, kk), iS, kk > 0);   // dP = dO V^T
                     }
                     umma_commit(&s_full[gs & 1]);
-                    if (h_s == nh_s - 1) umma_commit(q_empty);   // Q, dO of this item consumed
                 }
                 __syncwarp();
                 ++gs;
@@ -959,11 +1092,14 @@ __global__ void __launch_bounds__(384, 1)
                     mbar_wait(&p_full[g & 1], (g >> 1) & 1);
                     tc_fence_after();
                     const int ks = g % NK;
-                    const uint32_t aK = smem_u32(sK + ks * HB), aS = smem_u32(sS + sl * BR * 128);
+                    const uint32_t aK = smem_u32(sK + ks * HB), tdS = tmem + sl * 128;
+                    if (lane == 0) TR(18, g);
                     if (elect_one()) {
+                        // dS of keys [32c, 32c+32) sits packed in columns [32c, 32c+16)
 #pragma unroll
                         for (int kk = 0; kk < HR / 16; ++kk)
-                            umma_bf16(tdQ, desc_k(aS, kk), desc_mn_h(aK, kk), iG, (hh | kk) > 0);   // dQ += dS K
+                            umma_bf16_ts(tdQ, tdS + (kk >> 1) * 32 + (kk & 1) * 8, desc_mn_h(aK, kk), iG,
+                                         (hh | kk) > 0);   // dQ += dS K
                         umma_commit(&g_done[sl]);
                         umma_commit(&kv_empty[ks]);
                     }
@@ -991,17 +1127,19 @@ __global__ void __launch_bounds__(384, 1)
             const float Dq = q < s ? Db[q] : 0.f;
             for (int hh = 0; hh < nh; ++hh, ++g) {
                 const int sl = g & 1;
-                if (g >= 2) mbar_wait(&g_done[sl], ((g - 2) >> 1) & 1);   // dS buffer reuse
+                // (the S buffer's dS of half g-2 was read by dQ MMAs issued before S_g)
+                if (threadIdx.x == 128) TR(19, g);
                 mbar_wait(&s_full[sl], (g >> 1) & 1);
+                if (threadIdx.x == 128) TR(20, g);
                 tc_fence_after();
                 const uint32_t tS = tmem + sl * 128 + lane_off, tP = tS + 64;
-                uint8_t* Sd = sS + sl * BR * 128;
                 {
                     const int c = cg;
                     uint32_t sr[32], pr[32];
                     tmem_ld32(tS + c * 32, sr);
                     tmem_ld32(tP + c * 32, pr);
                     tmem_wait_ld();
+                    if (threadIdx.x == 128) TR(21, g);
                     const int kc = hh * HR + c * 32;
                     const bool full = kc + 31 <= qb * BR;   // below the diagonal for every row
                     const uint64_t sc2 = pk2(sc, sc), nl2 = pk2(-L, -L), nd2 = pk2(-Dq, -Dq);
@@ -1029,10 +1167,12 @@ __global__ void __launch_bounds__(384, 1)
                         upk2(d2, d0, d1);
                         wd[e / 2] = bf2(d0, d1);
                     }
-                    st_row32_pk(Sd, r, c * 32, wd);
+                    tmem_st16(tS + c * 32, wd);   // dS over this group's own S columns
                 }
-                fence_async_smem();
+                tmem_wait_st();
                 tc_fence_before();
+                if (threadIdx.x == 128) TR(22, g);
+                if (threadIdx.x == 383) TR(23, g);
                 mbar_arrive(&p_full[sl]);
             }
             mbar_wait(&g_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
@@ -1163,8 +1303,8 @@ static int bwd5(const void* qkv, const void* o, const void* dout, const float* l
                 float* ws, int b, int s, int a, cudaStream_t st) {
     constexpr int TB = fa5::Tile<D>::BYTES;
     constexpr int HB = (D / 64) * 64 * 128;
-    constexpr int smem_kv = 1024 + 2 * TB + 2 * fa5::BwdCfg<D>::NQ * HB + 4 * 128 * 128 + 4 * 64 * 4 + 256;
-    constexpr int smem_q = 1024 + 2 * TB + 2 * fa5::BwdCfg<D>::NK * HB + 2 * 128 * 128 + 256;
+    constexpr int smem_kv = 1024 + 2 * TB + 2 * fa5::BwdCfg<D>::NQ * HB + 4 * 64 * 4 + 256;
+    constexpr int smem_q = 1024 + 2 * TB + 2 * fa5::BwdCfg<D>::NK * HB + 256;
     static_assert(smem_kv <= 232448 && smem_q <= 232448, "backward smem over the 227 KB limit");
     static PerDeviceOnce attr;
     if (attr.first()) {
@@ -1191,6 +1331,12 @@ static int bwd5(const void* qkv, const void* o, const void* dout, const float* l
     note_launches(3);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
+
+#ifdef TPIPE_ATTN_TRACE
+extern "C" __attribute__((visibility("default"))) int tpipe_attn_trace_set(void* buf) {
+    return cudaMemcpyToSymbol(fa5::g_trace, &buf, sizeof(buf)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 int attn_fwd_tc5(const void* qkv, void* o, float* lse, int b, int s, int a, int d, cudaStream_t st) {
     return d == 64 ? fwd5<64>(qkv, o, lse, b, s, a, st) : fwd5<128>(qkv, o, lse, b, s, a, st);

@@ -1,8 +1,12 @@
 """Time the tcgen05 attention kernels over several shapes (CUDA events, warm):
-python scripts/attn_time.py [b,s,a,d ...]   e.g. 1,2048,16,128 4,4096,16,128"""
+python scripts/attn_time.py [--lib libtpipe_variant.so] [b,s,a,d ...]   e.g. 1,2048,16,128 4,4096,16,128"""
 import sys, os, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
+from paper_2503_03182_b200 import _lib
+if len(sys.argv) > 2 and sys.argv[1] == "--lib":   # time a variant build of the library
+    _lib.LIB_PATH = os.path.abspath(sys.argv[2])
+    del sys.argv[1:3]
 from paper_2503_03182_b200 import kernels as K
 
 shapes = [tuple(int(v) for v in a.split(",")) for a in sys.argv[1:]] or \
