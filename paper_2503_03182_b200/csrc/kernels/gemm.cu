@@ -233,6 +233,44 @@ int gemm_simt(int dtype, const GemmDesc& g, cudaStream_t st) {
 
 // ============================================================== tcgen05 (bf16)
 constexpr int TC_BM = 128, TC_BK = 64;
+
+// Probe build only (libtpipe_gprobe.so, `make gprobe`, scripts/gemm_probe.py;
+// never loaded by the product path): TPIPE_GEMM_PROBE bit 1 = the producer
+// skips the TMA loads (operands are whatever the smem ring holds), bit 2 = the
+// epilogue skips its math and stores -- which part of the pipeline bounds a shape.
+#ifdef TPIPE_GEMM_PROBE
+__constant__ int c_gemm_probe;
+#define GEMM_PROBE c_gemm_probe
+// SM-clock stamps of CTA 0's roles, [event][index] (scripts/gemm_probe.py --trace):
+// 0 MMA: first MMA of k-block i issued, 1 MMA: full[] wait of k-block i done,
+// 2 epilogue warp 4: tile i accumulator ready, 3 epilogue warp 4: tile i done,
+// 4 producer: empty[] wait of k-block i done
+constexpr int GTR_N = 1024;
+__device__ unsigned long long* g_gtrace;
+#define GTR(ev, idx)                                                                          \
+    do {                                                                                      \
+        if (g_gtrace && blockIdx.x == 0 && (idx) < GTR_N) g_gtrace[(ev) * GTR_N + (idx)] = clock64(); \
+    } while (0)
+// per-CTA stamps (index = blockIdx.x): 5 entry / 6 exit globaltimer (ns),
+// 7 entry / 8 exit clock64, 9 first MMA issued (ns), 10 last tile epilogue done (ns)
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define GTRB(ev, val)                                                      \
+    do {                                                                   \
+        if (g_gtrace && blockIdx.x < GTR_N) g_gtrace[(ev) * GTR_N + blockIdx.x] = (val); \
+    } while (0)
+#else
+#define GTRB(ev, val) \
+    do {              \
+    } while (0)
+#define GEMM_PROBE 0
+#define GTR(ev, idx) \
+    do {             \
+    } while (0)
+#endif
 // EW = 8 epilogue warps (two warpgroups, warps 4..11) for the math-heavy
 // epilogues (GELU, dGELU, residual): warp w reads TMEM lane quarter w % 4 and
 // column half (w - 4) / 4 of every tile, so the fused math runs on 2 warps per
@@ -265,20 +303,57 @@ struct TcCfg {
     static constexpr int SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + STAGING + 256;
 };
 
-// epilogue math on 32 columns n0.. of row m (no stores); out2 for GELU/dGELU.
-// Rows m >= M (TMA clips their stores) skip the residual / aux loads.
-__device__ __forceinline__ void epi_math(const GemmDesc& g, long m, long n0, bool row_ok,
-                                         float (&v)[32], float (&v2)[32]) {
+// Global operands of one 32-column epilogue chunk (bias, residual / dGELU's
+// u), loaded one chunk ahead so their latency hides under the previous
+// chunk's math and stores (and, for the first chunk, under the wait for the
+// accumulator): a chunk's loads issued on demand cost ~1-2K cycles
+// (profiles/r2_gemm_trace_*.jsonl).
+struct EpiPre {
+    uint4 b[4];   // bias[n0 .. n0+31], bf16
+    uint4 x[4];   // residual / aux row m, columns n0 .. n0+31, bf16
+};
+
+__device__ __forceinline__ void epi_prefetch(const GemmDesc& g, long m, long n0, bool row_ok, EpiPre& p) {
+    const int epi = g.epi;
+    if (epi == EPI_BIAS || epi == EPI_BIAS_RES || epi == EPI_BIAS_GELU) {
+        const uint4* q = reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(g.bias) + n0);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) p.b[i] = __ldg(q + i);
+    }
+    if (epi == EPI_BIAS_RES || epi == EPI_DGELU) {
+        const bf16* src = epi == EPI_BIAS_RES ? reinterpret_cast<const bf16*>(g.res) + m * g.ldr
+                                              : reinterpret_cast<const bf16*>(g.aux) + m * g.ldaux;
+        const uint4* q = reinterpret_cast<const uint4*>(src + n0);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) p.x[i] = row_ok ? q[i] : make_uint4(0, 0, 0, 0);
+    }
+}
+
+__device__ __forceinline__ void unpack8(const uint4& u, float* o) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h[j]);
+        o[2 * j] = f.x;
+        o[2 * j + 1] = f.y;
+    }
+}
+
+// epilogue math on 32 columns (no stores); out2 for GELU/dGELU. Rows m >= M
+// (TMA clips their stores) prefetched zeros.
+__device__ __forceinline__ void epi_math(const GemmDesc& g, const EpiPre& p, float (&v)[32], float (&v2)[32]) {
     const int epi = g.epi;
     if (epi == EPI_BIAS || epi == EPI_BIAS_RES || epi == EPI_BIAS_GELU) {
         float b[32];
-        load32<bf16>(reinterpret_cast<const bf16*>(g.bias) + n0, b);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) unpack8(p.b[i], b + 8 * i);
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = v[j] + b[j];
     }
-    if (epi == EPI_BIAS_RES && row_ok) {
+    if (epi == EPI_BIAS_RES) {
         float r[32];
-        load32<bf16>(reinterpret_cast<const bf16*>(g.res) + m * g.ldr + n0, r);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) unpack8(p.x[i], r + 8 * i);
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = v[j] + r[j];
     }
@@ -288,12 +363,8 @@ __device__ __forceinline__ void epi_math(const GemmDesc& g, long m, long n0, boo
     }
     if (epi == EPI_DGELU) {
         float u[32];
-        if (row_ok) {
-            load32<bf16>(reinterpret_cast<const bf16*>(g.aux) + m * g.ldaux + n0, u);
-        } else {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) u[j] = 0.f;
-        }
+        for (int i = 0; i < 4; ++i) unpack8(p.x[i], u + 8 * i);
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
             float gd;
@@ -405,6 +476,10 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int num_tiles = num_m * num_n;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;   // 0 = pair leader (issues the MMAs)
+    if (threadIdx.x == 0) {
+        GTRB(5, gtimer());
+        GTRB(7, clock64());
+    }
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
@@ -446,15 +521,22 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
             TcSched sch;
             sch.init(num_tiles, CG);
             int tile;
+            int gkb = 0;
+            (void)gkb;
             while (sch.next(tile)) {
                 const int mb = tile % num_m, nb = tile / num_m;
                 const int am = mb * TM + rank * TC_BM;     // this CTA's A rows
                 const int bn = nb * BN + rank * BNC;       // this CTA's B rows: [bn, bn + BNC)
                 for (int kb = 0; kb < num_kb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
+                    GTR(4, gkb++);
                     uint8_t* a = sA + stage * Cfg::A_BYTES;
                     uint8_t* b = sB + stage * Cfg::B_BYTES;
                     if (!elect_one()) {
+                    } else if (GEMM_PROBE & 1) {
+                        if (CG == 1) mbar_arrive(&full[stage]);
+                        else if (rank == 0) mbar_arrive(&full[stage]);
+                        else mbar_arrive_cluster(mapa_shared(&full[stage], 0));
                     } else if (CG == 1) {
                         if (!A_MN) {
                             tma_load_2d(a, &tmA, &full[stage], kb * TC_BK, am);
@@ -499,48 +581,70 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
         if (rank == 0) {
             // ---------------- MMA issuer (whole warp of the pair leader; the elected lane issues)
             const uint32_t idesc = tc_idesc<BN, A_MN, B_MN, CG>();
-            int stage = 0;
-            uint32_t phase = 0;
-            int it = 0;
-            TcSched sch;
-            sch.init(num_tiles, CG);
-            int tile;
-            for (; sch.next(tile); ++it) {
-                const int acc = it & 1;
-                const uint32_t aph = (it >> 1) & 1;
-                mbar_wait(&tempty[acc], aph ^ 1);
-                tc_fence_after();
-                const uint32_t d = tmem_base + acc * BN;
-                for (int kb = 0; kb < num_kb; ++kb) {
+            // descriptors of stage 0, k = 0; stage s / K-slice k are 64-bit adds
+            // on the start-address field (addr >> 4; smem < 256 KB, no carry),
+            // so the issuing loop between MMAs stays a few instructions long
+            const uint64_t da0 = A_MN ? umma_desc_sw128(smem_u32(sA), TC_BK * 128, 1024)
+                                      : umma_desc_sw128(smem_u32(sA), 0, 1024);
+            const uint64_t db0 = B_MN ? umma_desc_sw128(smem_u32(sB), TC_BK * 128, 1024)
+                                      : umma_desc_sw128(smem_u32(sB), 0, 1024);
+            constexpr uint64_t DK_A = A_MN ? (2048 >> 4) : (32 >> 4), DK_B = B_MN ? (2048 >> 4) : (32 >> 4);
+            // The elected lane runs the whole issue loop alone, and waits for
+            // the next stage's operands between the last two MMAs of a k-block
+            // (under the in-flight MMAs): UTCHMMA issue stalls while the tensor
+            // pipe's short queue is full, so any instruction latency between
+            // the last MMA of one k-block and the first of the next is a bubble
+            // (scripts/microbench/mma_loop.cu, profiles/r2_gemm_probe_*.jsonl).
+            if (elect_one()) {
+                int stage = 0;
+                uint32_t phase = 0;
+                int it = 0;
+                int gkb = 0;
+                (void)gkb;
+                TcSched sch;
+                sch.init(num_tiles, CG);
+                int tile;
+                for (; sch.next(tile); ++it) {
+                    const int acc = it & 1;
+                    const uint32_t aph = (it >> 1) & 1;
+                    mbar_wait(&tempty[acc], aph ^ 1);
                     mbar_wait(&full[stage], phase);
+                    GTR(1, gkb);
                     tc_fence_after();
-                    const uint32_t a_addr = smem_u32(sA + stage * Cfg::A_BYTES);
-                    const uint32_t b_addr = smem_u32(sB + stage * Cfg::B_BYTES);
-                    if (elect_one()) {
+                    const uint32_t d = tmem_base + acc * BN;
+                    for (int kb = 0; kb < num_kb; ++kb) {
+                        const uint64_t das = da0 + (uint64_t)(stage * (Cfg::A_BYTES >> 4));
+                        const uint64_t dbs = db0 + (uint64_t)(stage * (Cfg::B_BYTES >> 4));
+                        const int nstage = stage + 1 == STAGES ? 0 : stage + 1;
+                        const uint32_t nphase = stage + 1 == STAGES ? phase ^ 1 : phase;
 #pragma unroll
-                    for (int k = 0; k < TC_BK / 16; ++k) {
-                        // K-major: 16 elements = 32 bytes inside the 128B swizzle atom row;
-                        // MN-major: 16 K-rows of 128 B = 2048 bytes; MN atoms 8192 B apart.
-                        const uint64_t da = A_MN ? umma_desc_sw128(a_addr + k * 2048, TC_BK * 128, 1024)
-                                                 : umma_desc_sw128(a_addr + k * 32, 0, 1024);
-                        const uint64_t db = B_MN ? umma_desc_sw128(b_addr + k * 2048, TC_BK * 128, 1024)
-                                                 : umma_desc_sw128(b_addr + k * 32, 0, 1024);
-                        const uint32_t accum = (kb != 0 || k != 0) ? 1u : 0u;
-                        if (CG == 2) umma_bf16_pair(d, da, db, idesc, accum);
-                        else umma_bf16(d, da, db, idesc, accum);
+                        for (int k = 0; k < TC_BK / 16; ++k) {
+                            // K-major: 16 elements = 32 bytes inside the 128B swizzle atom row;
+                            // MN-major: 16 K-rows of 128 B = 2048 bytes; MN atoms 8192 B apart.
+                            if (k == TC_BK / 16 - 1 && kb + 1 < num_kb) {
+                                mbar_wait(&full[nstage], nphase);
+                                GTR(1, gkb + 1);
+                                tc_fence_after();
+                            }
+                            const uint64_t da = das + k * DK_A;
+                            const uint64_t db = dbs + k * DK_B;
+                            const uint32_t accum = (kb != 0 || k != 0) ? 1u : 0u;
+                            if (CG == 2) umma_bf16_pair(d, da, db, idesc, accum);
+                            else umma_bf16(d, da, db, idesc, accum);
+                            if (k == 0) GTR(0, gkb);
+                            if (k == 0 && gkb == 0) GTRB(9, gtimer());
+                        }
+                        if (CG == 2) umma_commit_pair(&empty[stage], 3);
+                        else umma_commit(&empty[stage]);
+                        stage = nstage;
+                        phase = nphase;
+                        ++gkb;
                     }
-                    if (CG == 2) umma_commit_pair(&empty[stage], 3);
-                    else umma_commit(&empty[stage]);
-                    }
-                    __syncwarp();
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
-                }
-                if (elect_one()) {
                     if (CG == 2) umma_commit_pair(&tfull[acc], 3);
                     else umma_commit(&tfull[acc]);
                 }
-                __syncwarp();
             }
+            __syncwarp();
         }
     } else if (warp >= 4) {
         // ---------------- epilogue: TMEM -> registers -> fused math -> swizzled smem -> TMA
@@ -562,25 +666,47 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
             const int mb = tile % num_m, nb = tile / num_m;
             const int acc = it & 1;
             const uint32_t aph = (it >> 1) & 1;
-            mbar_wait(&tfull[acc], aph);
-            tc_fence_after();
             const int m0 = mb * TM + rank * TC_BM + ew * 32;
             const long m = m0 + lane;
+            const bool row_ok = m < g.M;
             // fused LM head + CE (K8): this thread owns row m of the tile
             const bool lse_mode = g.epi == EPI_LSE_PART, ce_mode = g.epi == EPI_CE_GRAD;
+            const bool pre = !lse_mode && !ce_mode && g.epi != EPI_STORE && g.epi != EPI_STORE_F32 &&
+                             g.epi != EPI_ACC_F32 && !(GEMM_PROBE & 8);
+            EpiPre cur;
+            if (GEMM_PROBE & 8) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) cur.b[i] = cur.x[i] = make_uint4(0, 0, 0, 0);
+            }
+            if (pre && nb * BN + c_lo * 32 < g.N) epi_prefetch(g, m, nb * BN + c_lo * 32, row_ok, cur);
             int tgt = -1;
             float lse_m = 0.f, gmax = -INFINITY, gsum = 0.f;
-            if ((lse_mode || ce_mode) && m < g.M) {
+            if ((lse_mode || ce_mode) && row_ok) {
                 tgt = g.targets[m];
                 if (ce_mode) lse_m = g.lse[m];
             }
+            mbar_wait(&tfull[acc], aph);
+            if (warp == 4) GTR(2, it);
+            tc_fence_after();
 #pragma unroll 1
             for (int c = c_lo; c < c_hi; ++c) {
                 uint32_t r[32];
                 tmem_ld32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + c * 32, r);
-                tmem_wait_ld();
                 const int n0 = nb * BN + c * 32;
-                if (n0 >= g.N) continue;      // warp-uniform; TMA clips partial rows
+                tmem_wait_ld();
+                if (c + 1 == c_hi) {
+                    // the tile's accumulator is in registers: release it to the MMA
+                    // warp now, before the last chunk's math and stores
+                    tc_fence_before();
+                    if (CG == 2) {
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
+                    } else {
+                        mbar_arrive(&tempty[acc]);
+                    }
+                }
+                if (warp == 4) GTR(11, it * 8 + (c - c_lo));
+                if (n0 >= g.N || (GEMM_PROBE & 2)) continue;      // warp-uniform; TMA clips partial rows
                 float v[32], v2[32];
 #pragma unroll
                 for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
@@ -606,7 +732,7 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
                     }
                     if (hit) g.zt[m] = zt;
                     if ((((n0 + 32) & 63) == 0 || n0 + 32 >= g.N)) {
-                        if (m < g.M)
+                        if (row_ok)
                             reinterpret_cast<float2*>(g.part)[(size_t)m * ((g.N + 63) >> 6) + (n0 >> 6)] =
                                 make_float2(gmax, gsum);
                         gmax = -INFINITY;
@@ -622,29 +748,40 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
                         v[j] = pj * g.scale;
                     }
                 } else {
-                    epi_math(g, m, n0, m < g.M, v, v2);
+                    epi_math(g, cur, v, v2);
+                    // next chunk's operands: in flight during this chunk's stores
+                    // and the next TMEM load
+                    if (pre && c + 1 < c_hi && n0 + 32 < g.N) epi_prefetch(g, m, n0 + 32, row_ok, cur);
+                }
+                if (GEMM_PROBE & 4) {   // probe: math only, keep the result live
+                    float x = 0.f;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) x += v[j] + v2[j];
+                    if (x == 12345.f) g.zt[0] = x;
+                    continue;
                 }
                 stage_store(mystg + sb * Cfg::STG_BUF, v, f32out, reduce, &tmC, n0, m0, lane);
                 sb ^= 1;
+                if (warp == 4) GTR(12, it * 8 + (c - c_lo));
                 if (two) {
                     stage_store(mystg + sb * Cfg::STG_BUF, v2, false, false, &tmC2, n0, m0, lane);
                     sb ^= 1;
                 }
+                if (warp == 4) GTR(13, it * 8 + (c - c_lo));
             }
-            tc_fence_before();
-            if (CG == 2) {
-                __syncwarp();
-                if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
-            } else {
-                mbar_arrive(&tempty[acc]);
-            }
+            if (warp == 4) GTR(3, it);
         }
         if (lane == 0) bulk_wait_all();
         __syncwarp();
     }
+    if (warp == 4 && lane == 0) GTRB(10, gtimer());
     tc_fence_before();
     if (CG == 2) cluster_sync_all();
     else __syncthreads();
+    if (threadIdx.x == 0) {
+        GTRB(6, gtimer());
+        GTRB(8, clock64());
+    }
     if (warp == 2) {
         tc_fence_after();
         if (CG == 2) tmem_dealloc_pair(tmem_base, Cfg::TMEM_COLS);
@@ -734,6 +871,15 @@ static int launch_tc(const GemmDesc& g, cudaStream_t st) {
     if (attr_set.first()) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     }
+#ifdef TPIPE_GEMM_PROBE
+    static int probe_set = 0;   // once per process (one switch setting per run)
+    if (!probe_set) {
+        const char* e = getenv("TPIPE_GEMM_PROBE");
+        const int v = e ? atoi(e) : 0;
+        cudaMemcpyToSymbol(c_gemm_probe, &v, sizeof(int));
+        probe_set = 1;
+    }
+#endif
     if (launch_k(kern, dim3(grid), dim3(TC_THREADS), Cfg::SMEM, st, CG, ta, tb, tc, tc2, g, num_m, num_n,
                  num_kb) != cudaSuccess)
         return -3;
@@ -756,6 +902,12 @@ static int launch_majors(const GemmDesc& g, cudaStream_t st) {
                        g.epi == EPI_LSE_PART || g.epi == EPI_CE_GRAD;
     return heavy ? launch_majors_ew<BN, CG, 8>(g, st) : launch_majors_ew<BN, CG, 4>(g, st);
 }
+
+#ifdef TPIPE_GEMM_PROBE
+extern "C" __attribute__((visibility("default"))) int tpipe_gemm_trace_set(void* buf) {
+    return cudaMemcpyToSymbol(g_gtrace, &buf, sizeof(buf)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 int gemm_tc(const GemmDesc& g, cudaStream_t st) {
     if (g.M <= 0 || g.N <= 0) return 0;

@@ -44,30 +44,35 @@ def timed(fn, iters=20):
     return e0.elapsed_time(e1) / iters
 
 
-tot = [0.0, 0.0]
-for name, m, n, k, ak, bk, epi in shapes:
-    A = torch.randn((m, k) if ak else (k, m), device="cuda").to(torch.bfloat16)
-    B = torch.randn((n, k) if bk else (k, n), device="cuda").to(torch.bfloat16)
-    f32 = epi in (E.EPI_ACC_F32, E.EPI_STORE_F32)
-    C = torch.zeros((m, n), device="cuda", dtype=torch.float32 if f32 else torch.bfloat16)
-    C2 = torch.empty((m, n), device="cuda", dtype=torch.bfloat16)
-    Rr = torch.zeros((m, n), device="cuda", dtype=torch.bfloat16)
-    bias = torch.zeros(n, device="cuda", dtype=torch.bfloat16)
-    ours = lambda: K.tpipe_k_gemm(1, m, n, k, A, k if ak else m, ak, B, k if bk else n, bk, epi, C, n,
-                                  bias=bias, R=Rr, ldr=n, C2=C2, ldc2=n, aux=Rr, ldaux=n)
-    Am = A if ak else A.t()          # logical [m, k]
-    Bm = B.t() if bk else B          # logical [k, n]
-    Cb = torch.empty((m, n), device="cuda", dtype=torch.bfloat16)
-    cub = lambda: torch.matmul(Am, Bm, out=Cb)
-    t0, t1 = timed(ours), timed(cub)
-    if name != "sq8192":
-        tot[0] += t0
-        tot[1] += t1
-    fl = 2 * m * n * k
-    print(json.dumps({"kernel": name, "M": m, "N": n, "K": k, "ours_us": round(t0 * 1e3, 2),
-                      "ours_tflops": round(fl / t0 / 1e9, 1), "cublas_us": round(t1 * 1e3, 2),
-                      "cublas_tflops": round(fl / t1 / 1e9, 1), "ours_over_cublas": round(t1 / t0, 3)}),
-          flush=True)
-    del A, B, C, C2, Rr, Cb
-print(json.dumps({"layer_plus_head_total_ms": {"ours": round(tot[0], 4), "cublas": round(tot[1], 4),
-                                               "ours_speed_vs_cublas": round(tot[1] / tot[0], 3)}}))
+def main():
+    tot = [0.0, 0.0]
+    for name, m, n, k, ak, bk, epi in shapes:
+        A = torch.randn((m, k) if ak else (k, m), device="cuda").to(torch.bfloat16)
+        B = torch.randn((n, k) if bk else (k, n), device="cuda").to(torch.bfloat16)
+        f32 = epi in (E.EPI_ACC_F32, E.EPI_STORE_F32)
+        C = torch.zeros((m, n), device="cuda", dtype=torch.float32 if f32 else torch.bfloat16)
+        C2 = torch.empty((m, n), device="cuda", dtype=torch.bfloat16)
+        Rr = torch.zeros((m, n), device="cuda", dtype=torch.bfloat16)
+        bias = torch.zeros(n, device="cuda", dtype=torch.bfloat16)
+        ours = lambda: K.tpipe_k_gemm(1, m, n, k, A, k if ak else m, ak, B, k if bk else n, bk, epi, C, n,
+                                      bias=bias, R=Rr, ldr=n, C2=C2, ldc2=n, aux=Rr, ldaux=n)
+        Am = A if ak else A.t()          # logical [m, k]
+        Bm = B.t() if bk else B          # logical [k, n]
+        Cb = torch.empty((m, n), device="cuda", dtype=torch.bfloat16)
+        cub = lambda: torch.matmul(Am, Bm, out=Cb)
+        t0, t1 = timed(ours), timed(cub)
+        if name != "sq8192":
+            tot[0] += t0
+            tot[1] += t1
+        fl = 2 * m * n * k
+        print(json.dumps({"kernel": name, "M": m, "N": n, "K": k, "ours_us": round(t0 * 1e3, 2),
+                          "ours_tflops": round(fl / t0 / 1e9, 1), "cublas_us": round(t1 * 1e3, 2),
+                          "cublas_tflops": round(fl / t1 / 1e9, 1), "ours_over_cublas": round(t1 / t0, 3)}),
+              flush=True)
+        del A, B, C, C2, Rr, Cb
+    print(json.dumps({"layer_plus_head_total_ms": {"ours": round(tot[0], 4), "cublas": round(tot[1], 4),
+                                                   "ours_speed_vs_cublas": round(tot[1] / tot[0], 3)}}))
+
+
+if __name__ == "__main__":
+    main()
