@@ -114,33 +114,10 @@ __device__ __forceinline__ void tma_tile(uint8_t* sm, const CUtensorMap* map, ui
 }
 
 
-// ---- packed fp32x2 arithmetic (FFMA2 / FADD2 / FMUL2 on sm_100) and the
-// single-instruction ex2 (MUFU.EX2; the .ftz flush only touches results below
-// 2^-126). The elementwise warps of the backward kernels were issue-bound
+// ---- the single-instruction ex2 (MUFU.EX2; the .ftz flush only touches
+// results below 2^-126); packed fp32x2 helpers (pk2, ffma2, ...) are in
+// common.cuh. The elementwise warps of the backward kernels were issue-bound
 // (~21 instructions per score); these cut it to ~4.
-__device__ __forceinline__ uint64_t pk2(float a, float b) {
-    uint64_t r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-    return r;
-}
-__device__ __forceinline__ void upk2(uint64_t r, float& a, float& b) {
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
-}
-__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
-    uint64_t d;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-    return d;
-}
-__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
-    uint64_t d;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
-__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
-    uint64_t d;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
 __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

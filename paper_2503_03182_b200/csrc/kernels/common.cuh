@@ -128,6 +128,56 @@ __device__ __forceinline__ void gelu_fast_and_grad(float u, float& g, float& dg)
     dg = __fadd_rn(__fmul_rn(0.5f, __fadd_rn(1.0f, t)), __fmul_rn(__fmul_rn(0.5f, u), dt));
 }
 
+// ---- packed fp32x2 arithmetic (FFMA2 / FADD2 / FMUL2 on sm_100): one
+// instruction per pair, each lane rounded exactly as the scalar .rn op
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void upk2(uint64_t r, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+// gelu_fast / gelu_fast_and_grad on a pair: the same .rn op sequence per
+// lane (bit-identical to the scalar versions), half the FP instructions
+__device__ __forceinline__ uint64_t gelu_fast2(uint64_t u) {
+    const uint64_t C = pk2(0.7978845608028654f, 0.7978845608028654f), A = pk2(0.044715f, 0.044715f);
+    const uint64_t inner = fmul2(C, fadd2(u, fmul2(A, fmul2(fmul2(u, u), u))));
+    float i0, i1;
+    upk2(inner, i0, i1);
+    const uint64_t t = pk2(tanh_fast(i0), tanh_fast(i1));
+    return fmul2(fmul2(pk2(0.5f, 0.5f), u), fadd2(pk2(1.f, 1.f), t));
+}
+__device__ __forceinline__ void gelu_fast_and_grad2(uint64_t u, uint64_t& g, uint64_t& dg) {
+    const uint64_t C = pk2(0.7978845608028654f, 0.7978845608028654f), A = pk2(0.044715f, 0.044715f);
+    const uint64_t H = pk2(0.5f, 0.5f), ONE = pk2(1.f, 1.f);
+    const uint64_t u2 = fmul2(u, u);
+    const uint64_t inner = fmul2(C, fadd2(u, fmul2(A, fmul2(u2, u))));
+    float i0, i1;
+    upk2(inner, i0, i1);
+    const uint64_t t = pk2(tanh_fast(i0), tanh_fast(i1));
+    const uint64_t hu = fmul2(H, u), opt = fadd2(ONE, t);
+    g = fmul2(hu, opt);
+    const uint64_t tt = fmul2(t, t ^ 0x8000000080000000ull);   // -(t*t), exactly
+    const uint64_t dt = fmul2(fmul2(fadd2(ONE, tt), C), fadd2(ONE, fmul2(pk2(0.134145f, 0.134145f), u2)));
+    dg = fadd2(fmul2(H, opt), fmul2(hu, dt));
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

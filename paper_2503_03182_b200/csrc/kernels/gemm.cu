@@ -291,7 +291,12 @@ void gemm_set_pair_min_tiles(int n) { g_pair_min_tiles = n > 0 ? n : 96; }
 template <int BN, int CG = 1, int EPI_WARPS = 4>
 struct TcCfg {
     static_assert(BN <= 256, "one tcgen05.mma covers N <= 256");
-    static constexpr int STAGES = CG == 2 ? 6 : (BN == 256 ? 4 : 6);
+    // pair tiles with the 8-warp (two-output) epilogues: 5 operand stages and a
+    // 4-deep staging ring per warp, so a chunk's TMA stores never wait for the
+    // previous chunk's (the wait for a store to finish reading its buffer was
+    // ~1/3 of a chunk's time); the others: 2-deep staging
+    static constexpr int NSTG = (CG == 2 && EPI_WARPS == 8) ? 4 : 2;
+    static constexpr int STAGES = CG == 2 ? (EPI_WARPS == 8 ? 5 : 6) : (BN == 256 ? 4 : 6);
     static constexpr int A_BYTES = TC_BM * TC_BK * 2;
     static constexpr int B_BYTES = (BN / CG) * TC_BK * 2;
     static constexpr int TMEM_COLS = 2 * BN;                // double-buffered accumulators
@@ -299,7 +304,7 @@ struct TcCfg {
     // 8-warp epilogues (GELU, dGELU, residual) only store bf16 (2 KB chunks),
     // so both variants fit the same operand ring depth
     static constexpr int STG_BUF = EPI_WARPS == 8 ? 2048 : 4096;
-    static constexpr int STAGING = EPI_WARPS * 2 * STG_BUF;
+    static constexpr int STAGING = EPI_WARPS * NSTG * STG_BUF;
     static constexpr int SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + STAGING + 256;
 };
 
@@ -313,8 +318,9 @@ struct EpiPre {
     uint4 x[4];   // residual / aux row m, columns n0 .. n0+31, bf16
 };
 
+template <int EPI>
 __device__ __forceinline__ void epi_prefetch(const GemmDesc& g, long m, long n0, bool row_ok, EpiPre& p) {
-    const int epi = g.epi;
+    constexpr int epi = EPI;
     if (epi == EPI_BIAS || epi == EPI_BIAS_RES || epi == EPI_BIAS_GELU) {
         const uint4* q = reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(g.bias) + n0);
 #pragma unroll
@@ -329,48 +335,40 @@ __device__ __forceinline__ void epi_prefetch(const GemmDesc& g, long m, long n0,
     }
 }
 
-__device__ __forceinline__ void unpack8(const uint4& u, float* o) {
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const float2 f = __bfloat1622float2(h[j]);
-        o[2 * j] = f.x;
-        o[2 * j + 1] = f.y;
-    }
+// a bf16x2 word as an fp32 pair (exact)
+__device__ __forceinline__ uint64_t bf2_to_f2(uint32_t w) {
+    return pk2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
 }
 
 // epilogue math on 32 columns (no stores); out2 for GELU/dGELU. Rows m >= M
-// (TMA clips their stores) prefetched zeros.
-__device__ __forceinline__ void epi_math(const GemmDesc& g, const EpiPre& p, float (&v)[32], float (&v2)[32]) {
-    const int epi = g.epi;
-    if (epi == EPI_BIAS || epi == EPI_BIAS_RES || epi == EPI_BIAS_GELU) {
-        float b[32];
+// (TMA clips their stores) prefetched zeros. Packed fp32x2 ops throughout
+// (the same .rn rounding per element as scalar code; the epilogue's FP issue
+// was the larger part of its per-chunk time, profiles/r2_gemm_trace_*.jsonl).
+template <int EPI>
+__device__ __forceinline__ void epi_math(const EpiPre& p, float (&v)[32], float (&v2)[32]) {
+    constexpr int epi = EPI;
+    const uint32_t* bw = reinterpret_cast<const uint32_t*>(p.b);
+    const uint32_t* xw = reinterpret_cast<const uint32_t*>(p.x);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) unpack8(p.b[i], b + 8 * i);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = v[j] + b[j];
-    }
-    if (epi == EPI_BIAS_RES) {
-        float r[32];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) unpack8(p.x[i], r + 8 * i);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = v[j] + r[j];
-    }
-    if (epi == EPI_BIAS_GELU) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v2[j] = gelu_fast(rnd<bf16>(v[j]));
-    }
-    if (epi == EPI_DGELU) {
-        float u[32];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) unpack8(p.x[i], u + 8 * i);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            float gd;
-            gelu_fast_and_grad(u[j], v2[j], gd);
-            v[j] = v[j] * gd;
+    for (int q = 0; q < 16; ++q) {
+        uint64_t x = pk2(v[2 * q], v[2 * q + 1]);
+        if (epi == EPI_BIAS || epi == EPI_BIAS_RES || epi == EPI_BIAS_GELU) x = fadd2(x, bf2_to_f2(bw[q]));
+        if (epi == EPI_BIAS_RES) x = fadd2(x, bf2_to_f2(xw[q]));
+        if (epi == EPI_BIAS_GELU) {
+            // GELU of the stored (bf16-rounded) pre-activation u
+            float x0, x1;
+            upk2(x, x0, x1);
+            const __nv_bfloat162 u = __floats2bfloat162_rn(x0, x1);
+            const uint64_t gg = gelu_fast2(bf2_to_f2(*reinterpret_cast<const uint32_t*>(&u)));
+            upk2(gg, v2[2 * q], v2[2 * q + 1]);
         }
+        if (epi == EPI_DGELU) {
+            uint64_t gg, gd;
+            gelu_fast_and_grad2(bf2_to_f2(xw[q]), gg, gd);
+            upk2(gg, v2[2 * q], v2[2 * q + 1]);
+            x = fmul2(x, gd);
+        }
+        upk2(x, v[2 * q], v[2 * q + 1]);
     }
 }
 
@@ -386,16 +384,19 @@ __device__ __forceinline__ void tma_reduce_add_2d(const void* map, const void* s
                  : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read1() {
-    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // Stage one warp's 32 x 32 chunk (row = lane) in swizzled smem and issue one
-// TMA store (or fp32 reduce-add) of the box at (n0, m0).
+// TMA store (or fp32 reduce-add) of the box at (n0, m0). NSTG: the warp's
+// staging ring depth (the store that last used `buf` was NSTG stores ago).
+template <int NSTG>
 __device__ __forceinline__ void stage_store(uint8_t* buf, const float (&v)[32], bool f32, bool reduce,
                                             const CUtensorMap* map, int n0, int m0, int lane) {
-    if (lane == 0) bulk_wait_read1();   // the store that last used `buf` has read it
+    if (lane == 0) bulk_wait_read<NSTG - 1>();   // the store that last used `buf` has read it
     __syncwarp();
     const uint32_t sb = smem_u32(buf);
     if (f32) {   // 128 B rows, 128B swizzle: chunk q of row r at (q ^ (r & 7))
@@ -453,7 +454,10 @@ struct TcSched {
     }
 };
 
-template <int BN, bool A_MN, bool B_MN, int CG, int EPI_WARPS>
+// One kernel per epilogue kind (EPI): a kernel that carried every epilogue
+// variant was 39-48 KB of SASS, over the 32 KB instruction cache, with the
+// producer, MMA and epilogue loops far apart in it.
+template <int BN, bool A_MN, bool B_MN, int CG, int EPI_WARPS, int EPI>
 __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
@@ -650,10 +654,10 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
         // ---------------- epilogue: TMEM -> registers -> fused math -> swizzled smem -> TMA
         const int ew = warp & 3;             // TMEM lane quarter = tile rows [32ew, 32ew+32)
         const int chalf = (warp - 4) >> 2;   // column half of the tile
-        uint8_t* mystg = stg + (warp - 4) * 2 * Cfg::STG_BUF;
-        const bool f32out = (g.epi == EPI_ACC_F32 || g.epi == EPI_STORE_F32);
-        const bool reduce = (g.epi == EPI_ACC_F32);
-        const bool two = (g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU);
+        uint8_t* mystg = stg + (warp - 4) * Cfg::NSTG * Cfg::STG_BUF;
+        constexpr bool f32out = (EPI == EPI_ACC_F32 || EPI == EPI_STORE_F32);
+        constexpr bool reduce = (EPI == EPI_ACC_F32);
+        constexpr bool two = (EPI == EPI_BIAS_GELU || EPI == EPI_DGELU);
         int sb = 0;
         int it = 0;
         TcSched sch;
@@ -670,15 +674,15 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
             const long m = m0 + lane;
             const bool row_ok = m < g.M;
             // fused LM head + CE (K8): this thread owns row m of the tile
-            const bool lse_mode = g.epi == EPI_LSE_PART, ce_mode = g.epi == EPI_CE_GRAD;
-            const bool pre = !lse_mode && !ce_mode && g.epi != EPI_STORE && g.epi != EPI_STORE_F32 &&
-                             g.epi != EPI_ACC_F32 && !(GEMM_PROBE & 8);
+            constexpr bool lse_mode = EPI == EPI_LSE_PART, ce_mode = EPI == EPI_CE_GRAD;
+            const bool pre = !lse_mode && !ce_mode && EPI != EPI_STORE && EPI != EPI_STORE_F32 &&
+                             EPI != EPI_ACC_F32 && !(GEMM_PROBE & 8);
             EpiPre cur;
             if (GEMM_PROBE & 8) {
 #pragma unroll
                 for (int i = 0; i < 4; ++i) cur.b[i] = cur.x[i] = make_uint4(0, 0, 0, 0);
             }
-            if (pre && nb * BN + c_lo * 32 < g.N) epi_prefetch(g, m, nb * BN + c_lo * 32, row_ok, cur);
+            if (pre && nb * BN + c_lo * 32 < g.N) epi_prefetch<EPI>(g, m, nb * BN + c_lo * 32, row_ok, cur);
             int tgt = -1;
             float lse_m = 0.f, gmax = -INFINITY, gsum = 0.f;
             if ((lse_mode || ce_mode) && row_ok) {
@@ -748,10 +752,10 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
                         v[j] = pj * g.scale;
                     }
                 } else {
-                    epi_math(g, cur, v, v2);
+                    epi_math<EPI>(cur, v, v2);
                     // next chunk's operands: in flight during this chunk's stores
                     // and the next TMEM load
-                    if (pre && c + 1 < c_hi && n0 + 32 < g.N) epi_prefetch(g, m, n0 + 32, row_ok, cur);
+                    if (pre && c + 1 < c_hi && n0 + 32 < g.N) epi_prefetch<EPI>(g, m, n0 + 32, row_ok, cur);
                 }
                 if (GEMM_PROBE & 4) {   // probe: math only, keep the result live
                     float x = 0.f;
@@ -760,12 +764,12 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
                     if (x == 12345.f) g.zt[0] = x;
                     continue;
                 }
-                stage_store(mystg + sb * Cfg::STG_BUF, v, f32out, reduce, &tmC, n0, m0, lane);
-                sb ^= 1;
+                stage_store<Cfg::NSTG>(mystg + sb * Cfg::STG_BUF, v, f32out, reduce, &tmC, n0, m0, lane);
+                sb = (sb + 1) & (Cfg::NSTG - 1);
                 if (warp == 4) GTR(12, it * 8 + (c - c_lo));
                 if (two) {
-                    stage_store(mystg + sb * Cfg::STG_BUF, v2, false, false, &tmC2, n0, m0, lane);
-                    sb ^= 1;
+                    stage_store<Cfg::NSTG>(mystg + sb * Cfg::STG_BUF, v2, false, false, &tmC2, n0, m0, lane);
+                    sb = (sb + 1) & (Cfg::NSTG - 1);
                 }
                 if (warp == 4) GTR(13, it * 8 + (c - c_lo));
             }
@@ -827,7 +831,7 @@ static int num_sms() {
     return n;
 }
 
-template <int BN, bool A_MN, bool B_MN, int CG, int EPI_WARPS>
+template <int BN, bool A_MN, bool B_MN, int CG, int EPI_WARPS, int EPI>
 static int launch_tc(const GemmDesc& g, cudaStream_t st) {
     using Cfg = TcCfg<BN, CG, EPI_WARPS>;
     constexpr int TC_THREADS = tc_threads(EPI_WARPS);
@@ -866,7 +870,7 @@ static int launch_tc(const GemmDesc& g, cudaStream_t st) {
     const int tiles = num_m * num_n;
     const int units = num_sms() / CG;
     const int grid = CG * (tiles < units ? tiles : units);
-    auto kern = gemm_tc_kernel<BN, A_MN, B_MN, CG, EPI_WARPS>;
+    auto kern = gemm_tc_kernel<BN, A_MN, B_MN, CG, EPI_WARPS, EPI>;
     static PerDeviceOnce attr_set;
     if (attr_set.first()) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -887,20 +891,35 @@ static int launch_tc(const GemmDesc& g, cudaStream_t st) {
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
-template <int BN, int CG, int EW>
-static int launch_majors_ew(const GemmDesc& g, cudaStream_t st) {
+// 8 epilogue warps for the math-heavy epilogues (all store bf16 only: the
+// 8-warp variant stages 2 KB chunks), 4 for the light ones
+__host__ __device__ constexpr int epi_warps(int epi) {
+    return (epi == EPI_BIAS_GELU || epi == EPI_DGELU || epi == EPI_BIAS_RES || epi == EPI_LSE_PART ||
+            epi == EPI_CE_GRAD) ? 8 : 4;
+}
+template <int BN, int CG, int EPI>
+static int launch_majors_epi(const GemmDesc& g, cudaStream_t st) {
+    constexpr int EW = epi_warps(EPI);
     const bool amn = !g.a_kmajor, bmn = !g.b_kmajor;
-    if (!amn && !bmn) return launch_tc<BN, false, false, CG, EW>(g, st);
-    if (!amn && bmn) return launch_tc<BN, false, true, CG, EW>(g, st);
-    if (amn && bmn) return launch_tc<BN, true, true, CG, EW>(g, st);
-    return launch_tc<BN, true, false, CG, EW>(g, st);
+    if (!amn && !bmn) return launch_tc<BN, false, false, CG, EW, EPI>(g, st);
+    if (!amn && bmn) return launch_tc<BN, false, true, CG, EW, EPI>(g, st);
+    if (amn && bmn) return launch_tc<BN, true, true, CG, EW, EPI>(g, st);
+    return launch_tc<BN, true, false, CG, EW, EPI>(g, st);
 }
 template <int BN, int CG>
 static int launch_majors(const GemmDesc& g, cudaStream_t st) {
-    // (all three store bf16 only: the 8-warp variant stages 2 KB chunks)
-    const bool heavy = g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU || g.epi == EPI_BIAS_RES ||
-                       g.epi == EPI_LSE_PART || g.epi == EPI_CE_GRAD;
-    return heavy ? launch_majors_ew<BN, CG, 8>(g, st) : launch_majors_ew<BN, CG, 4>(g, st);
+    switch (g.epi) {
+        case EPI_STORE: return launch_majors_epi<BN, CG, EPI_STORE>(g, st);
+        case EPI_BIAS: return launch_majors_epi<BN, CG, EPI_BIAS>(g, st);
+        case EPI_BIAS_RES: return launch_majors_epi<BN, CG, EPI_BIAS_RES>(g, st);
+        case EPI_BIAS_GELU: return launch_majors_epi<BN, CG, EPI_BIAS_GELU>(g, st);
+        case EPI_DGELU: return launch_majors_epi<BN, CG, EPI_DGELU>(g, st);
+        case EPI_ACC_F32: return launch_majors_epi<BN, CG, EPI_ACC_F32>(g, st);
+        case EPI_STORE_F32: return launch_majors_epi<BN, CG, EPI_STORE_F32>(g, st);
+        case EPI_LSE_PART: return launch_majors_epi<BN, CG, EPI_LSE_PART>(g, st);
+        case EPI_CE_GRAD: return launch_majors_epi<BN, CG, EPI_CE_GRAD>(g, st);
+        default: return -4;
+    }
 }
 
 #ifdef TPIPE_GEMM_PROBE
