@@ -60,6 +60,11 @@ int tpipe_k_gemm_simt(int dtype, int M, int N, int K,
 void tpipe_k_gemm_set_pair(int on);
 /* CTA-pair 256 x 256 tiles once a GEMM has >= n of them (default 96; A/B knob) */
 void tpipe_k_gemm_set_pair_min_tiles(int n);
+/* Enable (1, default) or disable (0) the 240 / 224-column tile widths: for a
+ * K-major B operand the GEMM picks, per shape, the width in {256, 240, 224}
+ * with the fewest waves x width over the 148 SMs (74 CTA pairs); 0 = always
+ * 256 (A/B knob). */
+void tpipe_k_gemm_set_wide_choice(int on);
 
 /* LayerNorm forward over rows of length h (eps 1e-5, biased variance):
  * y = (x-mean)*rstd*gamma + beta; mean/rstd fp32 [rows]. */

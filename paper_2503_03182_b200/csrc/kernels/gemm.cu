@@ -283,23 +283,39 @@ void gemm_set_pair(int on) { g_pair_enabled = on != 0; }
 // CTA-pair tiles from this many 256 x 256 tiles on (measured crossover, see gemm_tc)
 static int g_pair_min_tiles = 96;
 void gemm_set_pair_min_tiles(int n) { g_pair_min_tiles = n > 0 ? n : 96; }
+// 240 / 224-wide tiles where they fill the waves better (on by default; off =
+// 256 only, for A/B runs)
+static bool g_wide_choice = true;
+void gemm_set_wide_choice(int on) { g_wide_choice = on != 0; }
 
 // CG = 1: one CTA computes a 128 x BN tile. CG = 2: a CTA pair (cluster of 2
 // on one TPC) computes a 256 x BN tile with tcgen05.mma.cta_group::2; each CTA
 // stages 128 rows of A and BN/2 rows of B, so per-SM operand traffic (L2->smem
 // and smem->tensor core) is 2/3 of the CG = 1, BN = 256 tile's.
+// BN = 256, 240, 224 (or 128): 240 / 224-wide tiles make the tile count of
+// the model's 2048 / 6144 / 8192-wide outputs fill the 74 CTA pairs (148 SMs)
+// where 256-wide tiles leave 14% of every wave idle (gemm_tc's choice); their
+// last 16 columns (BN = 240) are a half chunk stored without TMA.
 template <int BN, int CG = 1, int EPI_WARPS = 4>
 struct TcCfg {
-    static_assert(BN <= 256, "one tcgen05.mma covers N <= 256");
+    static_assert(BN <= 256 && BN % 16 == 0, "one tcgen05.mma covers N <= 256");
+    static constexpr int BNC = BN / CG;                      // B rows (N) staged per CTA
+    static constexpr int BNC64 = (BNC + 63) / 64 * 64;       // MN-major B: whole 64-column boxes
     // pair tiles with the 8-warp (two-output) epilogues: 5 operand stages and a
     // 4-deep staging ring per warp, so a chunk's TMA stores never wait for the
     // previous chunk's (the wait for a store to finish reading its buffer was
     // ~1/3 of a chunk's time); the others: 2-deep staging
     static constexpr int NSTG = (CG == 2 && EPI_WARPS == 8) ? 4 : 2;
-    static constexpr int STAGES = CG == 2 ? (EPI_WARPS == 8 ? 5 : 6) : (BN == 256 ? 4 : 6);
+    static constexpr int STAGES = CG == 2 ? (EPI_WARPS == 8 ? 5 : 6) : (BN > 128 ? 4 : 6);
+    static_assert(1024 + STAGES * (TC_BM * TC_BK * 2 + ((BN / CG + 63) / 64 * 64) * TC_BK * 2) +
+                          EPI_WARPS * NSTG * (EPI_WARPS == 8 ? 2048 : 4096) + 256 <= 232448,
+                  "shared memory over the 227 KB per-CTA limit");
     static constexpr int A_BYTES = TC_BM * TC_BK * 2;
-    static constexpr int B_BYTES = (BN / CG) * TC_BK * 2;
-    static constexpr int TMEM_COLS = 2 * BN;                // double-buffered accumulators
+    static constexpr int B_BYTES = BNC64 * TC_BK * 2;         // smem per stage
+    static constexpr int B_LOAD_K = BNC * TC_BK * 2;          // bytes one stage's TMA loads (K-major B)
+    static constexpr int B_LOAD_MN = BNC64 * TC_BK * 2;       // (MN-major B)
+    static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;   // double-buffered accumulators (pow2)
+    static constexpr int NCHUNK = (BN + 31) / 32;             // 32-column epilogue chunks (last may be 16)
     // epilogue staging: EPI_WARPS warps x 2 buffers x one 32 x 32 chunk; the
     // 8-warp epilogues (GELU, dGELU, residual) only store bf16 (2 KB chunks),
     // so both variants fit the same operand ring depth
@@ -319,19 +335,53 @@ struct EpiPre {
 };
 
 template <int EPI>
-__device__ __forceinline__ void epi_prefetch(const GemmDesc& g, long m, long n0, bool row_ok, EpiPre& p) {
+__device__ __forceinline__ void epi_prefetch(const GemmDesc& g, long m, long n0, bool row_ok, EpiPre& p,
+                                             bool half) {
     constexpr int epi = EPI;
     if (epi == EPI_BIAS || epi == EPI_BIAS_RES || epi == EPI_BIAS_GELU) {
         const uint4* q = reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(g.bias) + n0);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) p.b[i] = __ldg(q + i);
+        for (int i = 0; i < 4; ++i) p.b[i] = (i < 2 || !half) ? __ldg(q + i) : make_uint4(0, 0, 0, 0);
     }
     if (epi == EPI_BIAS_RES || epi == EPI_DGELU) {
         const bf16* src = epi == EPI_BIAS_RES ? reinterpret_cast<const bf16*>(g.res) + m * g.ldr
                                               : reinterpret_cast<const bf16*>(g.aux) + m * g.ldaux;
         const uint4* q = reinterpret_cast<const uint4*>(src + n0);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) p.x[i] = row_ok ? q[i] : make_uint4(0, 0, 0, 0);
+        for (int i = 0; i < 4; ++i) p.x[i] = (row_ok && (i < 2 || !half)) ? q[i] : make_uint4(0, 0, 0, 0);
+    }
+}
+
+// Direct stores of NC columns n0 .. n0+NC-1 of row m by the thread that owns
+// the row (no shared-memory staging): the 16-column half chunk of a BN = 240
+// tile (in range: N and n0 are multiples of 16), and every chunk when the
+// staging path is off. REDUCE: fp32 C += v with red.global.add (one add per
+// element per launch, by its only owner: deterministic).
+template <int NC, bool F32, bool REDUCE>
+__device__ __forceinline__ void row_store(void* C, long ldc, long m, long n0, const float (&v)[32]) {
+    if (F32) {
+        float* q = reinterpret_cast<float*>(C) + m * ldc + n0;
+#pragma unroll
+        for (int i = 0; i < NC / 4; ++i) {
+            if (REDUCE)
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(q + 4 * i), "f"(v[4 * i]),
+                             "f"(v[4 * i + 1]), "f"(v[4 * i + 2]), "f"(v[4 * i + 3])
+                             : "memory");
+            else
+                reinterpret_cast<float4*>(q)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+    } else {
+        uint4* q = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(C) + m * ldc + n0);
+#pragma unroll
+        for (int i = 0; i < NC / 8; ++i) {
+            uint32_t w[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * i + 2 * j], v[8 * i + 2 * j + 1]);
+                w[j] = *reinterpret_cast<uint32_t*>(&h2);
+            }
+            q[i] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
     }
 }
 
@@ -553,13 +603,15 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
                             tma_load_2d(b, &tmB, &full[stage], kb * TC_BK, bn);
                         } else {
 #pragma unroll
-                            for (int i = 0; i < BNC / 64; ++i)
+                            for (int i = 0; i < Cfg::BNC64 / 64; ++i)
                                 tma_load_2d(b + i * 64 * TC_BK * 2, &tmB, &full[stage], bn + i * 64, kb * TC_BK);
                         }
-                        mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
+                        mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES + (B_MN ? Cfg::B_LOAD_MN : Cfg::B_LOAD_K));
                     } else {
                         const uint32_t fb = mapa_shared(&full[stage], 0);   // leader's barrier
-                        if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (Cfg::A_BYTES + Cfg::B_BYTES));
+                        if (rank == 0)
+                            mbar_arrive_expect_tx(&full[stage],
+                                                  2 * (Cfg::A_BYTES + (B_MN ? Cfg::B_LOAD_MN : Cfg::B_LOAD_K)));
                         if (!A_MN) {
                             tma_load_2d_pair(a, &tmA, fb, kb * TC_BK, am);
                         } else {
@@ -571,7 +623,7 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
                             tma_load_2d_pair(b, &tmB, fb, kb * TC_BK, bn);
                         } else {
 #pragma unroll
-                            for (int i = 0; i < BNC / 64; ++i)
+                            for (int i = 0; i < Cfg::BNC64 / 64; ++i)
                                 tma_load_2d_pair(b + i * 64 * TC_BK * 2, &tmB, fb, bn + i * 64, kb * TC_BK);
                         }
                         if (rank != 0) mbar_arrive_cluster(fb);
@@ -663,8 +715,11 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
         TcSched sch;
         sch.init(num_tiles, CG);
         const uint32_t tempty_leader = CG == 2 ? mapa_shared(&tempty[0], 0) : 0;
-        constexpr int NCH = BN / 32 / (EPI_WARPS / 4);   // 32-column chunks per column group
-        const int c_lo = chalf * NCH, c_hi = c_lo + NCH;
+        // 32-column chunks per column group (two groups with 8 warps; BN = 224 / 240
+        // split 4 + 3 / 4 + 3.5)
+        constexpr int NCH0 = EPI_WARPS == 8 ? (Cfg::NCHUNK + 1) / 2 : Cfg::NCHUNK;
+        const int c_lo = chalf * NCH0, c_hi = chalf ? Cfg::NCHUNK : NCH0;
+        constexpr bool HAS_HALF = BN % 32 != 0;   // chunk NCHUNK - 1 is 16 columns wide
         int tile;
         for (; sch.next(tile); ++it) {
             const int mb = tile % num_m, nb = tile / num_m;
@@ -682,7 +737,8 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
 #pragma unroll
                 for (int i = 0; i < 4; ++i) cur.b[i] = cur.x[i] = make_uint4(0, 0, 0, 0);
             }
-            if (pre && nb * BN + c_lo * 32 < g.N) epi_prefetch<EPI>(g, m, nb * BN + c_lo * 32, row_ok, cur);
+            if (pre && nb * BN + c_lo * 32 < g.N)
+                epi_prefetch<EPI>(g, m, nb * BN + c_lo * 32, row_ok, cur, HAS_HALF && c_lo == Cfg::NCHUNK - 1);
             int tgt = -1;
             float lse_m = 0.f, gmax = -INFINITY, gsum = 0.f;
             if ((lse_mode || ce_mode) && row_ok) {
@@ -755,13 +811,29 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
                     epi_math<EPI>(cur, v, v2);
                     // next chunk's operands: in flight during this chunk's stores
                     // and the next TMEM load
-                    if (pre && c + 1 < c_hi && n0 + 32 < g.N) epi_prefetch<EPI>(g, m, n0 + 32, row_ok, cur);
+                    if (pre && c + 1 < c_hi && n0 + 32 < g.N)
+                        epi_prefetch<EPI>(g, m, n0 + 32, row_ok, cur, HAS_HALF && c + 1 == Cfg::NCHUNK - 1);
                 }
                 if (GEMM_PROBE & 4) {   // probe: math only, keep the result live
                     float x = 0.f;
 #pragma unroll
                     for (int j = 0; j < 32; ++j) x += v[j] + v2[j];
                     if (x == 12345.f) g.zt[0] = x;
+                    continue;
+                }
+                if (HAS_HALF && c == Cfg::NCHUNK - 1) {
+                    // 16-column half chunk: direct stores of this thread's row
+                    if (row_ok) {
+                        row_store<16, f32out, reduce>(g.C, g.ldc, m, n0, v);
+                        if (two) row_store<16, false, false>(g.C2, g.ldc2, m, n0, v2);
+                    }
+                    continue;
+                }
+                if (GEMM_PROBE & 16) {   // probe: direct row stores instead of smem staging + TMA
+                    if (row_ok) {
+                        row_store<32, f32out, reduce>(g.C, g.ldc, m, n0, v);
+                        if (two) row_store<32, false, false>(g.C2, g.ldc2, m, n0, v2);
+                    }
                     continue;
                 }
                 stage_store<Cfg::NSTG>(mystg + sb * Cfg::STG_BUF, v, f32out, reduce, &tmC, n0, m0, lane);
@@ -916,8 +988,12 @@ static int launch_majors(const GemmDesc& g, cudaStream_t st) {
         case EPI_DGELU: return launch_majors_epi<BN, CG, EPI_DGELU>(g, st);
         case EPI_ACC_F32: return launch_majors_epi<BN, CG, EPI_ACC_F32>(g, st);
         case EPI_STORE_F32: return launch_majors_epi<BN, CG, EPI_STORE_F32>(g, st);
-        case EPI_LSE_PART: return launch_majors_epi<BN, CG, EPI_LSE_PART>(g, st);
-        case EPI_CE_GRAD: return launch_majors_epi<BN, CG, EPI_CE_GRAD>(g, st);
+        // the fused head's 64-column LSE groups need each column group to be a
+        // multiple of 64 wide (BN = 128 or 256; gemm_tc never picks 224 / 240)
+        case EPI_LSE_PART:
+            return BN % 128 == 0 ? launch_majors_epi<(BN % 128 == 0 ? BN : 256), CG, EPI_LSE_PART>(g, st) : -4;
+        case EPI_CE_GRAD:
+            return BN % 128 == 0 ? launch_majors_epi<(BN % 128 == 0 ? BN : 256), CG, EPI_CE_GRAD>(g, st) : -4;
         default: return -4;
     }
 }
@@ -943,15 +1019,43 @@ int gemm_tc(const GemmDesc& g, cudaStream_t st) {
     // loop is long (>= 4096); a 2048 x 2048 x 2048 GEMM (64 pair tiles on 74
     // pairs) is faster as 128 single-CTA tiles.
     const long pair_tiles = (long)((g.M + 255) / 256) * ((g.N + 255) / 256);
-    if (g_pair_enabled && (pair_tiles >= g_pair_min_tiles || (pair_tiles >= 32 && g.K >= 4096)))
+    // tile width: the MMA time of a wave is ~ BN (tcgen05.mma runs at its N/2
+    // cycles per K=16 step when fed, profiles/r2_mma_loop.jsonl), so pick the
+    // width with the fewest waves x BN: e.g. N = 8192 on 74 pairs: 256-wide =
+    // 4 waves of 256 (3.46 full), 224-wide = 296 tiles = 4 full waves of 224
+    const bool head = g.epi == EPI_LSE_PART || g.epi == EPI_CE_GRAD;
+    auto width = [&](int rows, int units, int allow224) {
+        const long mt = (g.M + rows - 1) / rows;
+        int best = 256;
+        long bestc = (mt * ((g.N + 255) / 256) + units - 1) / units * 256;
+        // K-major B only (the forward GEMMs): an MN-major B tile of 112 / 120
+        // columns per CTA starts off the 128-byte swizzle atoms and is loaded as
+        // two 64-column boxes; measured 13-15% slower than 256-wide
+        // (profiles/r2_gemm_ab_wide.jsonl), while the K-major widths gain 2-4%
+        if (head || !g_wide_choice || !g.b_kmajor) return best;
+        for (int bn : {240, 224}) {
+            if (bn == 224 && !allow224) continue;
+            const long c = (mt * ((g.N + bn - 1) / bn) + units - 1) / units * bn;
+            if (c < bestc) {
+                bestc = c;
+                best = bn;
+            }
+        }
+        return best;
+    };
+    if (g_pair_enabled && (pair_tiles >= g_pair_min_tiles || (pair_tiles >= 32 && g.K >= 4096))) {
+        const int bn = width(256, num_sms() / 2, 1);
+        if (bn == 224) return launch_majors<224, 2>(g, st);
+        if (bn == 240) return launch_majors<240, 2>(g, st);
         return launch_majors<256, 2>(g, st);
+    }
     const int num_m = (g.M + TC_BM - 1) / TC_BM;
     // N=128 tiles read 8 KB of operands per 64-cycle MMA (128 B/cycle, the
     // shared-memory limit); N=256 tiles need 96 B/cycle. Prefer 256 whenever
     // it still occupies >= ~65% of the SMs.
     // (a ragged last N tile is fine: TMA zero-fills, the epilogue masks n >= N)
     const bool wide = (long)num_m * ((g.N + 255) / 256) * 3 >= 2L * num_sms();
-    if (wide) return launch_majors<256, 1>(g, st);
+    if (wide) return width(128, num_sms(), 0) == 240 ? launch_majors<240, 1>(g, st) : launch_majors<256, 1>(g, st);
     return launch_majors<128, 1>(g, st);
 }
 

@@ -97,3 +97,7 @@ def tpipe_host_adamw(master, m, v, grad, w_bf16, n, decay, lr, b1, b2, eps, wd, 
 
 def tpipe_k_gemm_set_pair(on):
     lib().tpipe_k_gemm_set_pair(1 if on else 0)
+
+
+def tpipe_k_gemm_set_wide_choice(on):
+    lib().tpipe_k_gemm_set_wide_choice(1 if on else 0)

@@ -12,11 +12,13 @@ for r in rows:
 tot = defaultdict(float)
 for k, v in t.items():
     best = {lib: min(xs) for lib, xs in v.items()}
-    print(f"{k:11s}", best, f"ratio {best.get('libtpipe_v0.so', 0) / best.get('libtpipe.so', 1):.3f}")
+    libs = sorted(best)
+    print(f"{k:11s}", best, f"ratio {libs[0]}/{libs[-1]} = {best[libs[0]] / best[libs[-1]]:.3f}")
     if k != "sq8192":
         for lib, x in best.items():
             tot[lib] += x
-print(dict(tot), "speedup", round(tot["libtpipe_v0.so"] / tot["libtpipe.so"], 4))
+libs = sorted(tot)
+print(dict(tot), f"speedup {libs[0]}/{libs[-1]}", round(tot[libs[0]] / tot[libs[-1]], 4))
 try:
     for l in open("gpurun_out/gemm_trace_ab.jsonl"):
         d = json.loads(l)

@@ -21,6 +21,9 @@ sys.path.insert(0, os.path.join(ROOT, "scripts"))
 from gemm_vs_cublas import shapes, timed  # noqa: E402
 
 probe = int(os.environ.get("TPIPE_GEMM_PROBE", "0"))
+wide = os.environ.get("GEMM_WIDE")
+if wide is not None:
+    K.tpipe_k_gemm_set_wide_choice(int(wide))
 only = os.environ.get("GEMM_PROBE_SHAPES")
 for name, m, n, k, ak, bk, epi in shapes:
     if only and name not in only.split(","):
@@ -36,6 +39,6 @@ for name, m, n, k, ak, bk, epi in shapes:
                                   bias=bias, R=Rr, ldr=n, C2=C2, ldc2=n, aux=Rr, ldaux=n)
     t = timed(ours)
     fl = 2 * m * n * k
-    print(json.dumps({"lib": os.path.basename(_lib.LIB_PATH), "probe": probe, "kernel": name, "M": m, "N": n, "K": k, "us": round(t * 1e3, 2),
+    print(json.dumps({"lib": os.path.basename(_lib.LIB_PATH) + ("" if wide is None else f":wide{wide}") + f":p{probe}", "probe": probe, "kernel": name, "M": m, "N": n, "K": k, "us": round(t * 1e3, 2),
                       "tflops": round(fl / t / 1e9, 1)}), flush=True)
     del A, B, C, C2, Rr

@@ -20,6 +20,8 @@ from paper_2503_03182_b200 import kernels as K  # noqa: E402
 from gemm_vs_cublas import shapes  # noqa: E402
 
 N_TR = 1024
+if os.environ.get("GEMM_WIDE") is not None:
+    K.tpipe_k_gemm_set_wide_choice(int(os.environ["GEMM_WIDE"]))
 want = sys.argv[1] if len(sys.argv) > 1 else "fc1_fprop"
 for name, m, n, k, ak, bk, epi in shapes:
     if name != want:

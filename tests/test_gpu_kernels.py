@@ -502,3 +502,66 @@ def test_head_ce_fused_vs_fp64(rows, V, h):
     assert abs(float(loss) - loss_ref) / abs(loss_ref) < 1e-5
     err = float(torch.linalg.norm(dl.double() - dref) / torch.linalg.norm(dref))
     assert err < 1e-2, err
+
+
+@pytest.mark.parametrize("M,N,Kd,width", [(2048, 8192, 512, 224), (2048, 6144, 320, 240),
+                                          (2048, 2048, 4160, 240), (2048, 2048, 512, 240),
+                                          (1904, 2080, 200, 240), (6144, 2048, 256, 240)])
+@pytest.mark.parametrize("majors", [(1, 1), (1, 0), (0, 0)])
+def test_gemm_wide_choice(M, N, Kd, width, majors):
+    """240 / 224-column tiles (chosen where they fill the 148 SMs better;
+    `width` is the cost model's pick for the shape: CTA pairs for all but
+    (2048, 2048, 512) and (1904, 2080, 200)) incl. the 16-column half chunk
+    stored without TMA and ragged M / N / K: every epilogue matches fp64 and
+    the 256-wide kernel (wide choice off) to fp32 accumulation-order tolerance.
+    The widths apply to K-major B (majors (1, 1)); the others stay 256 wide."""
+    ak, bk = majors
+    k = K()
+    rng = np.random.default_rng(M + 7 * N + Kd + width)
+    A = rng.standard_normal((M, Kd)).astype(np.float32)
+    B = rng.standard_normal((N, Kd)).astype(np.float32)
+    At = t(A if ak else A.T.copy(), "bf16")
+    Bt = t(B if bk else B.T.copy(), "bf16")
+    ref = h(At if ak else At.T) @ h(Bt if bk else Bt.T).T
+    U = t(rng.standard_normal((M, N)), "bf16")
+    Rr = t(rng.standard_normal((M, N)), "bf16")
+    bias = t(rng.standard_normal(N), "bf16")
+    args = (M, N, Kd, At, Kd if ak else M, ak, Bt, Kd if bk else N, bk)
+
+    def run():
+        C = torch.zeros((M, N), device=dev, dtype=torch.float32)
+        k.tpipe_k_gemm(1, *args, k.EPI_STORE_F32, C, N)
+        Acc = torch.full((M, N), 2.0, device=dev, dtype=torch.float32)
+        k.tpipe_k_gemm(1, *args, k.EPI_ACC_F32, Acc, N)
+        Cs = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
+        k.tpipe_k_gemm(1, *args, k.EPI_STORE, Cs, N)
+        Cr = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
+        k.tpipe_k_gemm(1, *args, k.EPI_BIAS_RES, Cr, N, bias=bias, R=Rr, ldr=N)
+        Cd = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
+        Cg = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
+        k.tpipe_k_gemm(1, *args, k.EPI_DGELU, Cd, N, C2=Cg, ldc2=N, aux=U, ldaux=N)
+        Cu = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
+        Cgl = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
+        k.tpipe_k_gemm(1, *args, k.EPI_BIAS_GELU, Cu, N, bias=bias, C2=Cgl, ldc2=N)
+        torch.cuda.synchronize()
+        return C, Acc, Cs, Cr, Cd, Cg, Cu, Cgl
+    wide = run()
+    try:
+        k.tpipe_k_gemm_set_wide_choice(0)
+        narrow = run()
+    finally:
+        k.tpipe_k_gemm_set_wide_choice(1)
+    C, Acc, Cs, Cr, Cd, Cg, Cu, Cgl = wide
+    assert max_rel(h(C), ref) < 1e-4
+    assert max_rel(h(Acc), 2 + ref) < 1e-4
+    assert rel_l2(h(Cs), ref) < 1e-2
+    assert rel_l2(h(Cr), ref + h(bias) + h(Rr)) < 1e-2
+    assert rel_l2(h(Cd), ref * R.gelu_grad(h(U))) < 1e-2
+    assert rel_l2(h(Cg), R.gelu(h(U))) < 1e-2
+    assert rel_l2(h(Cu), ref + h(bias)) < 1e-2
+    assert rel_l2(h(Cgl), R.gelu(h(Cu))) < 1e-2
+    # same math, different tile grouping: fp32 results agree to accumulation order
+    assert max_rel(h(C), h(narrow[0])) < 1e-5
+    assert max_rel(h(Acc), h(narrow[1])) < 1e-5
+    for a, b in zip(wide[2:], narrow[2:]):
+        assert rel_l2(h(a), h(b)) < 1e-2
