@@ -65,6 +65,9 @@ void tpipe_k_gemm_set_pair_min_tiles(int n);
  * with the fewest waves x width over the 148 SMs (74 CTA pairs); 0 = always
  * 256 (A/B knob). */
 void tpipe_k_gemm_set_wide_choice(int on);
+/* Enable (1, default) or disable (0) the row-parallel LayerNorm backward
+ * kernel for bf16 h <= 2048 (0 = the staged kernel; process-wide A/B knob). */
+void tpipe_k_ln_set_rows_bwd(int on);
 
 /* LayerNorm forward over rows of length h (eps 1e-5, biased variance):
  * y = (x-mean)*rstd*gamma + beta; mean/rstd fp32 [rows]. */

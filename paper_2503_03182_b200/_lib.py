@@ -48,9 +48,10 @@ def _declare(L):
     L.tpipe_k_gemm_set_pair.restype = None
     L.tpipe_k_gemm_set_pair_min_tiles.argtypes = [i32]
     L.tpipe_k_gemm_set_pair_min_tiles.restype = None
-    if hasattr(L, "tpipe_k_gemm_set_wide_choice"):   # (absent from older builds used in A/B runs)
-        L.tpipe_k_gemm_set_wide_choice.argtypes = [i32]
-        L.tpipe_k_gemm_set_wide_choice.restype = None
+    for knob in ("tpipe_k_gemm_set_wide_choice", "tpipe_k_ln_set_rows_bwd"):
+        if hasattr(L, knob):   # (absent from older builds used in A/B runs)
+            getattr(L, knob).argtypes = [i32]
+            getattr(L, knob).restype = None
     L.tpipe_k_ln_fwd.argtypes = [i32, vp, vp, vp, vp, vp, vp, i32, i32, vp]
     L.tpipe_k_ln_bwd.argtypes = [i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp]
     L.tpipe_k_ln_bwd_rsum.argtypes = [i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp]

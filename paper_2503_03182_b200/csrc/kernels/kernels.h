@@ -58,6 +58,7 @@ void gemm_set_pair(int on);
 // pair tiles from n 256 x 256 tiles on (default 96)
 void gemm_set_pair_min_tiles(int n);
 void gemm_set_wide_choice(int on);
+void ln_set_rows_bwd(int on);
 
 // ---------------------------------------------------------------- layernorm
 // y = (x - mean) * rstd * gamma + beta over rows of length h; saves mean/rstd (fp32).

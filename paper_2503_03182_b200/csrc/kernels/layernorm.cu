@@ -110,6 +110,10 @@ __global__ void ln_fwd_kernel(const T* __restrict__ x, const T* __restrict__ gam
 // (deterministic). Partial-block layout: RB rows per CTA.
 constexpr int RB = 16;        // rows per CTA in the backward / column-sum kernels
 constexpr int WIDE_THREADS = 512;
+// row-parallel LN backward (ln_bwd_rows_kernel) for h <= 2048 (on by default;
+// off = the staged kernel, for A/B runs)
+static bool g_ln_rows = true;
+void ln_set_rows_bwd(int on) { g_ln_rows = on != 0; }
 
 // Sum of (a, b) over the tpr threads of row group `grp` (named barrier 1+grp).
 // In-warp butterfly, then the per-warp values in warp order: same order for
@@ -545,6 +549,185 @@ ln_bwd_stage_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
     }
 }
 
+// ---------------------------------------------------------------- row-parallel backward
+// LN backward for h = 256 * NSEG <= 2048 (the C2 width), one CTA of 8 warps per
+// 16-row block. All of the block's dy / x / resid rows are fetched at once
+// with 16-byte cp.async into shared memory (warp w fetches, lane-sliced, the
+// two rows w and w + 8 it computes, one commit group per row), then:
+//  1. dx: a warp per row, the two row means (of dxhat and dxhat * xhat) by
+//     warp shuffles only -- no CTA barrier per row (the staged kernel above
+//     serialised the rows behind a 256-thread named barrier each and ran at
+//     0.36 of the HBM peak, bench hbm_kernels);
+//  2. after one __syncthreads, the dgamma / dbeta / dresid column partials: a
+//     thread owns 8 columns and accumulates them over the 16 rows in row order,
+//     from shared memory.
+// Deterministic: fixed shuffle trees, fixed row order. Same partial layout as
+// ln_bwd_stage_kernel ([3][nblk][h]).
+template <int NSEG>
+__global__ void __launch_bounds__(256, 1)
+ln_bwd_rows_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x, const bf16* __restrict__ gamma,
+                   const float* __restrict__ mean, const float* __restrict__ rstd,
+                   const bf16* __restrict__ resid, bf16* __restrict__ dx, float* __restrict__ ws, int rows,
+                   int nblk, int with_rsum) {
+    constexpr int h = NSEG * 256;
+    pdl_wait();
+    pdl_trigger();
+    __shared__ float smu[RB], srs[RB];
+    extern __shared__ __align__(128) uint8_t smraw[];
+    bf16* sdy = reinterpret_cast<bf16*>(smraw);   // [RB][h]
+    bf16* sx = sdy + RB * h;                      // [RB][h]
+    bf16* sr = sx + RB * h;                       // [RB][h]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r0 = blockIdx.x * RB, nr = min(RB, rows - r0);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const int k = warp + 8 * q;
+        if (k < nr) {
+            const long base = (long)(r0 + k) * h;
+#pragma unroll
+            for (int i = 0; i < NSEG; ++i) {
+                const int c = (i * 32 + lane) * 8;
+                cp_async16(sdy + k * h + c, dy + base + c);
+                cp_async16(sx + k * h + c, x + base + c);
+                if (resid) cp_async16(sr + k * h + c, resid + base + c);
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    if (threadIdx.x < nr) {
+        smu[threadIdx.x] = mean[r0 + threadIdx.x];
+        srs[threadIdx.x] = rstd[r0 + threadIdx.x];
+    }
+    uint4 gu[NSEG];
+#pragma unroll
+    for (int i = 0; i < NSEG; ++i) gu[i] = __ldg(reinterpret_cast<const uint4*>(gamma + (i * 32 + lane) * 8));
+    __syncthreads();   // smu / srs
+    // ---- phase 1: dx, rows warp and warp + 8
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const int k = warp + 8 * q;
+        if (q == 0) asm volatile("cp.async.wait_group 1;" ::: "memory");
+        else asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+        if (k >= nr) continue;
+        const float mu = smu[k], rs = srs[k];
+        const uint64_t rs2 = fpair(rs, rs), nm2 = fpair(-mu, -mu);
+        uint64_t s1_2 = 0ull, s2_2 = 0ull;
+#pragma unroll
+        for (int i = 0; i < NSEG; ++i) {
+            const int c = (i * 32 + lane) * 8;
+            const uint4 du = *reinterpret_cast<const uint4*>(sdy + k * h + c);
+            const uint4 xu = *reinterpret_cast<const uint4*>(sx + k * h + c);
+            const uint32_t dw[4] = {du.x, du.y, du.z, du.w}, xw[4] = {xu.x, xu.y, xu.z, xu.w},
+                           gw[4] = {gu[i].x, gu[i].y, gu[i].z, gu[i].w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint64_t xh2 = fmul2x(fadd2x(bfpair(xw[j]), nm2), rs2);   // (x - mu) * rstd
+                const uint64_t dxh2 = fmul2x(bfpair(dw[j]), bfpair(gw[j]));
+                s1_2 = fadd2x(s1_2, dxh2);
+                s2_2 = ffma2x(dxh2, xh2, s2_2);
+            }
+        }
+        float s1a, s1b, s2a, s2b;
+        funpair(s1_2, s1a, s1b);
+        funpair(s2_2, s2a, s2b);
+        const float s1 = warp_sum(s1a + s1b), s2 = warp_sum(s2a + s2b);
+        const float c1 = s1 / (float)h, c2 = s2 / (float)h;
+        const uint64_t nc1 = fpair(-c1, -c1), nc2 = fpair(-c2, -c2);
+        const long base = (long)(r0 + k) * h;
+#pragma unroll
+        for (int i = 0; i < NSEG; ++i) {
+            const int c = (i * 32 + lane) * 8;
+            const uint4 du = *reinterpret_cast<const uint4*>(sdy + k * h + c);
+            const uint4 xu = *reinterpret_cast<const uint4*>(sx + k * h + c);
+            uint4 ru = make_uint4(0, 0, 0, 0);
+            if (resid) ru = *reinterpret_cast<const uint4*>(sr + k * h + c);
+            const uint32_t dw[4] = {du.x, du.y, du.z, du.w}, xw[4] = {xu.x, xu.y, xu.z, xu.w},
+                           gw[4] = {gu[i].x, gu[i].y, gu[i].z, gu[i].w}, rw[4] = {ru.x, ru.y, ru.z, ru.w};
+            uint32_t ow[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint64_t xh2 = fmul2x(fadd2x(bfpair(xw[j]), nm2), rs2);
+                const uint64_t dxh2 = fmul2x(bfpair(dw[j]), bfpair(gw[j]));
+                // rstd * (dxh - c1 - xh * c2) + resid
+                const uint64_t t = ffma2x(xh2, nc2, fadd2x(dxh2, nc1));
+                float o0, o1;
+                funpair(ffma2x(t, rs2, bfpair(rw[j])), o0, o1);
+                __nv_bfloat162 hv = __floats2bfloat162_rn(o0, o1);
+                ow[j] = *reinterpret_cast<uint32_t*>(&hv);
+            }
+            *reinterpret_cast<uint4*>(dx + base + c) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+        }
+    }
+    __syncthreads();   // every row of the block is in shared memory
+    // ---- phase 2: column partials over the block's rows (row order)
+    const int c = threadIdx.x * 8;
+    if (c >= h) return;
+    uint64_t pg2[4] = {0ull, 0ull, 0ull, 0ull}, pb2[4] = {0ull, 0ull, 0ull, 0ull},
+             pr2[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll 4
+    for (int k = 0; k < nr; ++k) {
+        const uint4 du = *reinterpret_cast<const uint4*>(sdy + k * h + c);
+        const uint4 xu = *reinterpret_cast<const uint4*>(sx + k * h + c);
+        const uint64_t rs2 = fpair(srs[k], srs[k]), nm2 = fpair(-smu[k], -smu[k]);
+        const uint32_t dw[4] = {du.x, du.y, du.z, du.w}, xw[4] = {xu.x, xu.y, xu.z, xu.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint64_t d2 = bfpair(dw[j]);
+            const uint64_t xh2 = fmul2x(fadd2x(bfpair(xw[j]), nm2), rs2);
+            pg2[j] = ffma2x(d2, xh2, pg2[j]);
+            pb2[j] = fadd2x(pb2[j], d2);
+        }
+        if (with_rsum) {
+            const uint4 ru = *reinterpret_cast<const uint4*>(sr + k * h + c);
+            const uint32_t rw[4] = {ru.x, ru.y, ru.z, ru.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) pr2[j] = fadd2x(pr2[j], bfpair(rw[j]));
+        }
+    }
+    float pg[8], pb[8], pr[8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        funpair(pg2[j], pg[2 * j], pg[2 * j + 1]);
+        funpair(pb2[j], pb[2 * j], pb[2 * j + 1]);
+        funpair(pr2[j], pr[2 * j], pr[2 * j + 1]);
+    }
+    float* wg = ws + (long)blockIdx.x * h + c;
+    float* wb = ws + (long)(nblk + blockIdx.x) * h + c;
+    *reinterpret_cast<float4*>(wg) = make_float4(pg[0], pg[1], pg[2], pg[3]);
+    *reinterpret_cast<float4*>(wg + 4) = make_float4(pg[4], pg[5], pg[6], pg[7]);
+    *reinterpret_cast<float4*>(wb) = make_float4(pb[0], pb[1], pb[2], pb[3]);
+    *reinterpret_cast<float4*>(wb + 4) = make_float4(pb[4], pb[5], pb[6], pb[7]);
+    if (with_rsum) {
+        float* wr = ws + (long)(2 * nblk + blockIdx.x) * h + c;
+        *reinterpret_cast<float4*>(wr) = make_float4(pr[0], pr[1], pr[2], pr[3]);
+        *reinterpret_cast<float4*>(wr + 4) = make_float4(pr[4], pr[5], pr[6], pr[7]);
+    }
+}
+
+// row-parallel backward for h in {256, 512, ..., 2048}; false = not handled
+static bool launch_ln_bwd_rows(const void* dy, const void* x, const void* gamma, const float* mean,
+                               const float* rstd, const void* resid, void* dx, float* ws, int rows, int h,
+                               int nb, int with_rsum, cudaStream_t st) {
+    if (!g_ln_rows || h % 256 || h > 2048) return false;
+    switch (h / 256) {
+#define TP_LNR(S)                                                                                         \
+    case S: {                                                                                             \
+        static PerDeviceOnce attr;                                                                        \
+        if (attr.first())                                                                                 \
+            cudaFuncSetAttribute(ln_bwd_rows_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                                 3 * RB * 256 * S * 2);                                                   \
+        launch_k(ln_bwd_rows_kernel<S>, dim3(nb), dim3(256), (size_t)3 * RB * h * 2, st, 1,               \
+                 (const bf16*)dy, (const bf16*)x, (const bf16*)gamma, mean, rstd, (const bf16*)resid,     \
+                 (bf16*)dx, ws, rows, nb, with_rsum);                                                     \
+        return true;                                                                                      \
+    }
+        TP_LNR(1) TP_LNR(2) TP_LNR(3) TP_LNR(4) TP_LNR(5) TP_LNR(6) TP_LNR(7) TP_LNR(8)
+#undef TP_LNR
+        default: return false;
+    }
+}
+
 static int wide_groups(int h) {
     const int tpr = h / 8;
     int G = WIDE_THREADS / tpr;
@@ -687,14 +870,16 @@ int ln_bwd(int dtype, const void* dy, const void* x, const void* gamma, const fl
         int RC = LNB_SMEM_ROWS_BYTES / (3 * h * 2);
         if (RC > RB) RC = RB;
         const size_t smem = (size_t)RC * 3 * h * 2;
-        static PerDeviceOnce attr;
-        if (attr.first()) {
-            cudaFuncSetAttribute(ln_bwd_stage_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 LNB_SMEM_ROWS_BYTES);
+        if (!launch_ln_bwd_rows(dy, x, gamma, mean, rstd, resid, dx, ws, rows, h, nb, rs, st)) {
+            static PerDeviceOnce attr;
+            if (attr.first()) {
+                cudaFuncSetAttribute(ln_bwd_stage_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     LNB_SMEM_ROWS_BYTES);
+            }
+            launch_k(ln_bwd_stage_kernel, dim3(nb), dim3(G * (h / 8)), smem, st, 1, (const bf16*)dy,
+                     (const bf16*)x, (const bf16*)gamma, (const float*)mean, (const float*)rstd,
+                     (const bf16*)resid, (bf16*)dx, ws, rows, h, nb, rs, RC);
         }
-        launch_k(ln_bwd_stage_kernel, dim3(nb), dim3(G * (h / 8)), smem, st, 1, (const bf16*)dy,
-                 (const bf16*)x, (const bf16*)gamma, (const float*)mean, (const float*)rstd, (const bf16*)resid,
-                 (bf16*)dx, ws, rows, h, nb, rs, RC);
         launch_k(reduce_parts_kernel, dim3((h + 31) / 32, 2 + rs), dim3(256), 0, st, 1, (const float*)ws, dgamma,
                  dbeta, dresid_sum, h, nb);
         note_launches(2);
@@ -783,13 +968,16 @@ int ln_bwd_partials(int dtype, const void* dy, const void* x, const void* gamma,
     int RC = LNB_SMEM_ROWS_BYTES / (3 * h * 2);
     if (RC > RB) RC = RB;
     const size_t smem = (size_t)RC * 3 * h * 2;
-    static PerDeviceOnce attr;
-    if (attr.first()) {
-        cudaFuncSetAttribute(ln_bwd_stage_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, LNB_SMEM_ROWS_BYTES);
+    if (!launch_ln_bwd_rows(dy, x, gamma, mean, rstd, resid, dx, ws, rows, h, nb, with_rsum ? 1 : 0, st)) {
+        static PerDeviceOnce attr;
+        if (attr.first()) {
+            cudaFuncSetAttribute(ln_bwd_stage_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 LNB_SMEM_ROWS_BYTES);
+        }
+        launch_k(ln_bwd_stage_kernel, dim3(nb), dim3(G * (h / 8)), smem, st, 1, (const bf16*)dy, (const bf16*)x,
+                 (const bf16*)gamma, (const float*)mean, (const float*)rstd, (const bf16*)resid, (bf16*)dx, ws,
+                 rows, h, nb, with_rsum ? 1 : 0, RC);
     }
-    launch_k(ln_bwd_stage_kernel, dim3(nb), dim3(G * (h / 8)), smem, st, 1, (const bf16*)dy, (const bf16*)x,
-             (const bf16*)gamma, (const float*)mean, (const float*)rstd, (const bf16*)resid, (bf16*)dx, ws, rows,
-             h, nb, with_rsum ? 1 : 0, RC);
     note_launches(1);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }

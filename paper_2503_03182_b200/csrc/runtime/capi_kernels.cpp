@@ -58,6 +58,7 @@ TP_API int tpipe_k_gemm_simt(int dtype, int M, int N, int K, const void* A, long
 TP_API void tpipe_k_gemm_set_pair(int on) { gemm_set_pair(on); }
 TP_API void tpipe_k_gemm_set_pair_min_tiles(int n) { gemm_set_pair_min_tiles(n); }
 TP_API void tpipe_k_gemm_set_wide_choice(int on) { gemm_set_wide_choice(on); }
+TP_API void tpipe_k_ln_set_rows_bwd(int on) { ln_set_rows_bwd(on); }
 
 TP_API int tpipe_k_ln_fwd(int dtype, const void* x, const void* gamma, const void* beta, void* y,
                           float* mean, float* rstd, int rows, int h, void* stream) {

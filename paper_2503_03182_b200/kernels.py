@@ -101,3 +101,7 @@ def tpipe_k_gemm_set_pair(on):
 
 def tpipe_k_gemm_set_wide_choice(on):
     lib().tpipe_k_gemm_set_wide_choice(1 if on else 0)
+
+
+def tpipe_k_ln_set_rows_bwd(on):
+    lib().tpipe_k_ln_set_rows_bwd(1 if on else 0)
