@@ -7,6 +7,7 @@
 //   0 gemm-like   1 no barrier wait   2 no commit   3 descriptors precomputed
 //   (64-bit adds on a base descriptor)   4 = 3 + 2 k-blocks per iteration
 //   5 tight (no wait / commit, precomputed descriptors; the floor reference)
+//   6 tight TS (A from TMEM), B K-major   7 tight TS, B MN-major   8 tight SS, B MN-major
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2503_03182_b200/csrc \
 //        scripts/microbench/mma_loop.cu -o /tmp/mma_loop && /tmp/mma_loop
 #include <cstdio>
@@ -50,13 +51,17 @@ __global__ void __launch_bounds__(128, 1) loop_rate(long long* out) {
         if (warp == 0) {
             __syncwarp();
             t0 = clock64();
-            if (V == 5) {
+            if (V >= 5) {
                 if (elect_one()) {
                     const uint64_t da0 = umma_desc_sw128(smem_u32(sA), 0, 1024);
-                    const uint64_t db0 = umma_desc_sw128(smem_u32(sB), 0, 1024);
+                    const uint64_t db0 = (V == 7 || V == 8) ? umma_desc_sw128(smem_u32(sB), 64 * 128, 1024)
+                                                            : umma_desc_sw128(smem_u32(sB), 0, 1024);
+                    const uint64_t dbk = (V == 7 || V == 8) ? 128 : 2;   // per K=16 step
+                    const uint32_t idb = idesc | ((V == 7 || V == 8) ? (1u << 16) : 0u);
                     for (int i = 0; i < KB * 4; ++i) {
                         const int k = i & 3;
-                        umma_bf16(tmem, da0 + 2 * k, db0 + 2 * k, idesc, i > 0);
+                        if (V == 6 || V == 7) umma_bf16_ts(tmem, tmem + 256 + 8 * k, db0 + dbk * k, idb, i > 0);
+                        else umma_bf16(tmem, da0 + 2 * k, db0 + dbk * k, idb, i > 0);
                     }
                 }
             } else {
@@ -115,7 +120,7 @@ __global__ void __launch_bounds__(128, 1) loop_rate(long long* out) {
 template <int V, int N>
 static void run(int grid, long long* d) {
     static const char* names[] = {"gemm_like", "no_wait", "no_commit", "precomputed_desc", "precomputed_x2",
-                                  "tight"};
+                                  "tight",     "tight_ts_bK", "tight_ts_bMN", "tight_ss_bMN"};
     auto k = loop_rate<V, N>;
     constexpr int STAGES = N > 128 ? 4 : 6;
     const int smem = 1024 + STAGES * (128 * 64 * 2 + N * 64 * 2);
@@ -140,11 +145,12 @@ static void run(int grid, long long* d) {
 template <int N>
 static void all(int grid, long long* d) {
     run<0, N>(grid, d);
-    run<1, N>(grid, d);
-    run<2, N>(grid, d);
-    run<3, N>(grid, d);
-    run<4, N>(grid, d);
     run<5, N>(grid, d);
+    run<8, N>(grid, d);
+    if (N <= 256 - 32) {   // A in TMEM columns [256, 288): accumulator N <= 224 (N = 256: SS only)
+        run<6, N>(grid, d);
+        run<7, N>(grid, d);
+    }
 }
 
 int main() {
@@ -154,8 +160,9 @@ int main() {
     cudaMalloc(&d, 160 * sizeof(long long));
     for (int grid : {1, sms}) {
         all<256>(grid, d);
-        all<224>(grid, d);
         all<128>(grid, d);
+        all<64>(grid, d);
+        all<32>(grid, d);
     }
     return 0;
 }
