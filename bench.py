@@ -976,15 +976,18 @@ def run_tpipe(args):
             ms = float(t[0])
         return ms
 
+    # CUDA-graph steps (TPIPE_STEP_GRAPH: captured in the first warm-up step,
+    # replayed after) where the plan allows it: one process, no T-Offload, no DP
+    gf = RT.STEP_GRAPH if (args.graph and world == 1 and dp == 1 and not plan.offload) else 0
     for _ in range(args.warmup):
-        rt.step_device(dtok.data_ptr(), dtgt.data_ptr())
+        rt.step_device(dtok.data_ptr(), dtgt.data_ptr(), gf)
     with Clocks(local) as clk:
-        ms = timed(lambda: rt.step_device(dtok.data_ptr(), dtgt.data_ptr()), args.steps)
+        ms = timed(lambda: rt.step_device(dtok.data_ptr(), dtgt.data_ptr(), gf), args.steps)
     launches = rt.stats()["kernel_launches"]
     # e2e: host tokens (pinned) -> tpipe_step (H2D inside) -> loss D2H
     htok = torch.from_numpy(tok).pin_memory().numpy()
     htgt = torch.from_numpy(tgt).pin_memory().numpy()
-    ms_e2e = timed(lambda: rt.step(htok, htgt), args.steps)
+    ms_e2e = timed(lambda: rt.step(htok, htgt, gf), args.steps)
     # profiled pass of the same K steps: per-kernel-class CUDA-event timing
     kms = np.zeros(4)
     kfl = np.zeros(4)
@@ -1026,6 +1029,8 @@ def run_tpipe(args):
                        "parallelism": (f"pp{N}" if dp == 1 else f"dp{dp}xpp{N} (ZeRO-1)") if world > 1 else
                        (f"virtual pp{N} on 1 GPU" if N > 1 else "pp1"),
                        "transport": (args.transport if world > 1 else "in-process"),
+                       "step_issue": ("CUDA graph replay (TPIPE_STEP_GRAPH; captured in warm-up)" if gf
+                                      else "instruction stream issued per step"),
                        **({"same_gpu_test": "all ranks on GPU 0 (TPIPE_BENCH_SAME_GPU): "
                                             "not an N-GPU measurement"} if same_gpu else {}),
                        "layers_per_chunk": list(plan.layers_chunk),
@@ -1174,6 +1179,8 @@ def main():
     ap.add_argument("--impl", default="tpipe", choices=["tpipe", "reference"])
     ap.add_argument("--strategy", default="tpipe", choices=["tpipe", "tpipe_trecomp", "1f1b"])
     ap.add_argument("--no-extras", action="store_true", help="skip capacity sweep and CPU oracle")
+    ap.add_argument("--graph", type=int, default=1,
+                    help="1: time steps as CUDA-graph replays (TPIPE_STEP_GRAPH) where the plan allows it")
     ap.add_argument("--pipeline-replay", action="store_true",
                     help="measured-op-duration replay of p = 2, 4, 8 stage pipelines (C2)")
     ap.add_argument("--capacity-run", action="store_true",

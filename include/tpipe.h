@@ -346,6 +346,14 @@ typedef struct tpipe_runtime tpipe_runtime;
 #define TPIPE_STEP_PROFILE 2u       /* bracket GEMM / attention launches with CUDA events */
 #define TPIPE_STEP_OP_TIMES 4u      /* record each compute op's (F / B / R) duration with CUDA
                                        events on the stage stream (tpipe_runtime_op_times) */
+#define TPIPE_STEP_GRAPH 8u         /* run the step's device work as one CUDA graph: the first
+                                       step with this flag (and a given NO_OPT setting) captures
+                                       the instruction stream's launches, events and copies,
+                                       later steps replay it; AdamW reads its per-step
+                                       hyper-parameters from device memory. Same kernels, same
+                                       order, same results. Needs an in-process (virtual)
+                                       transport, no T-Offload, no DP, no debug pool canaries
+                                       (else TPIPE_E_INVALID); ignored with PROFILE / OP_TIMES */
 
 int tpipe_runtime_create(const tpipe_plan* plan, const tpipe_runtime_opts* opts,
                          tpipe_runtime** out);

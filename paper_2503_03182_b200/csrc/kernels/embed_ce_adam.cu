@@ -346,9 +346,10 @@ int ce_bwd(int dtype, const float* logits, const int* tgt, const float* lse, voi
 template <typename T>
 __global__ void adamw_kernel(float* __restrict__ master, float* __restrict__ m,
                              float* __restrict__ v, float* __restrict__ grad, T* __restrict__ w,
-                             long n, int decay, AdamHyper hp) {
+                             long n, int decay, AdamHyper hp, const AdamHyper* __restrict__ hp_dev) {
     const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    if (hp_dev) hp = *hp_dev;
     AdamOut o = adam_elem(master[i], m[i], v[i], grad[i], decay, hp);
     master[i] = o.w;
     m[i] = o.m;
@@ -358,14 +359,14 @@ __global__ void adamw_kernel(float* __restrict__ master, float* __restrict__ m,
 }
 
 int adamw(int dtype, float* master, float* m, float* v, float* grad, void* w, long n, int decay,
-          const AdamHyper& hp, cudaStream_t st) {
+          const AdamHyper& hp, cudaStream_t st, const AdamHyper* hp_dev) {
     if (n <= 0) return 0;
     const int blocks = (int)((n + 255) / 256);
     if (dtype == DT_BF16)
-        adamw_kernel<bf16><<<blocks, 256, 0, st>>>(master, m, v, grad, (bf16*)w, n, decay, hp);
+        adamw_kernel<bf16><<<blocks, 256, 0, st>>>(master, m, v, grad, (bf16*)w, n, decay, hp, hp_dev);
     else  // fp32: the weight IS the master
         adamw_kernel<float><<<blocks, 256, 0, st>>>(master, m, v, grad,
-                                                    (float*)(w == master ? nullptr : w), n, decay, hp);
+                                                    (float*)(w == master ? nullptr : w), n, decay, hp, hp_dev);
     note_launches(1);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }

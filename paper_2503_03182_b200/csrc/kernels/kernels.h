@@ -141,8 +141,11 @@ struct DpPtrs {
 // arrays, element i <-> lo + i), the new weight written into every replica's w.
 int dp_adamw(int dtype, const DpPtrs& p, int dp, float* master, float* m, float* v, long lo, long n,
              int decay, const AdamHyper& hp, cudaStream_t st);
+// hp_dev (optional): read the hyper-parameters from device memory instead of
+// the by-value hp (a CUDA-graph step replays the launch with its captured
+// arguments; the runtime updates *hp_dev before each replay)
 int adamw(int dtype, float* master, float* m, float* v, float* grad, void* w, long n, int decay,
-          const AdamHyper& hp, cudaStream_t st);
+          const AdamHyper& hp, cudaStream_t st, const AdamHyper* hp_dev = nullptr);
 // host reference of the same arithmetic, bit-identical (T-Offload host optimizer)
 void adamw_host(float* master, float* m, float* v, const float* grad, uint16_t* w_bf16, long n,
                 int decay, const AdamHyper& hp);

@@ -132,6 +132,12 @@ struct tpipe_runtime {
     float lr = 3e-4f, b1 = 0.9f, b2 = 0.95f, eps = 1e-8f, wd = 0.1f;
     long t = 0;
     long launches_last = 0;
+    // TPIPE_STEP_GRAPH: the captured step (one per NO_OPT setting), its launch
+    // count, and the device copy of the AdamW hyper-parameters it reads
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    long glaunches[2] = {0, 0};
+    AdamHyper* hp_dev = nullptr;
+    bool capturing = false;
     double d2h_bytes = 0, h2d_bytes = 0;
     // timing-enabled event pairs bracketing each offload copy of the last step
     std::vector<cudaEvent_t> tevpool;
@@ -221,7 +227,8 @@ int adam_chunk(tpipe_runtime* rt, ChunkState& C, const AdamHyper& hp, cudaStream
     for (auto& sg : C.lay.segments) {
         const long off = sg[0], n = sg[1];
         void* w = dt == DT_BF16 ? (void*)((uint16_t*)C.w + off) : (void*)(C.master + off);
-        if (adamw(dt, C.master + off, C.m + off, C.v + off, C.grad + off, w, n, (int)sg[2], hp, st))
+        if (adamw(dt, C.master + off, C.m + off, C.v + off, C.grad + off, w, n, (int)sg[2], hp, st,
+                  rt->capturing ? rt->hp_dev : nullptr))
             return set_error(TPIPE_E_CUDA, "adamw launch failed");
     }
     return 0;
@@ -594,34 +601,13 @@ int run_step(tpipe_runtime* rt, const int32_t* tok_dev, const int32_t* tgt_dev, 
     return rc;
 }
 
-int run_step_impl(tpipe_runtime* rt, const int32_t* tok_dev, const int32_t* tgt_dev, uint32_t flags,
-             float* loss_out) {
+// The instruction streams of one step: every op of every owned stage, issued
+// on the stage streams in plan order (the host only orders the issue; all
+// waiting is on the device), joined back into rt->stream.
+static int issue_ops(tpipe_runtime* rt, uint32_t flags, bool op_times) {
     const auto& P = rt->plan;
-    const Dims& D = rt->D;
     cudaStream_t cs = rt->stream;
-    const size_t io_bytes = (size_t)P.m * D.M * 4;
-    rt->evnext = 0;
-    rt->tevnext = 0;
-    rt->d2h_ev.clear();
-    rt->h2d_ev.clear();
-    rt->d2h_bytes = rt->h2d_bytes = 0;
-    const auto t_issue0 = std::chrono::steady_clock::now();
-    const long l0 = launch_count();
-    profiler().begin_step((flags & TPIPE_STEP_PROFILE) != 0);
-    const bool op_times = (flags & TPIPE_STEP_OP_TIMES) != 0;
-    // stage streams: separate per stage in the virtual pipeline, except while
-    // timing ops or kernel classes (OP_TIMES / PROFILE: serial, each op's or
-    // kernel's own GPU time)
-    for (int s : rt->owned) {
-        StageState& S = *rt->st[s];
-        S.pc = 0;
-        if (s == 0 && tok_dev) CU(cudaMemcpyAsync(S.tokens, tok_dev, io_bytes, cudaMemcpyDeviceToDevice, cs));
-        if (s == P.p - 1) {
-            if (tgt_dev) CU(cudaMemcpyAsync(S.targets, tgt_dev, io_bytes, cudaMemcpyDeviceToDevice, cs));
-            CU(cudaMemsetAsync(S.loss_slots, 0, (size_t)P.m * 4, cs));
-        }
-    }
-    // (after the token / target copies above, so every stage sees them)
+    // (after the token / target copies, so every stage sees them)
     cudaEvent_t fork = next_event(rt);
     CU(cudaEventRecord(fork, cs));
     for (int s : rt->owned) {
@@ -676,6 +662,79 @@ int run_step_impl(tpipe_runtime* rt, const int32_t* tok_dev, const int32_t* tgt_
         CU(cudaEventRecord(j, S.cs));
         CU(cudaStreamWaitEvent(cs, j, 0));
     }
+    return 0;
+}
+
+int run_step_impl(tpipe_runtime* rt, const int32_t* tok_dev, const int32_t* tgt_dev, uint32_t flags,
+             float* loss_out) {
+    const auto& P = rt->plan;
+    const Dims& D = rt->D;
+    cudaStream_t cs = rt->stream;
+    const size_t io_bytes = (size_t)P.m * D.M * 4;
+    rt->evnext = 0;
+    rt->tevnext = 0;
+    rt->d2h_ev.clear();
+    rt->h2d_ev.clear();
+    rt->d2h_bytes = rt->h2d_bytes = 0;
+    const auto t_issue0 = std::chrono::steady_clock::now();
+    const long l0 = launch_count();
+    profiler().begin_step((flags & TPIPE_STEP_PROFILE) != 0);
+    const bool op_times = (flags & TPIPE_STEP_OP_TIMES) != 0;
+    const bool graph = (flags & TPIPE_STEP_GRAPH) && !op_times && !(flags & TPIPE_STEP_PROFILE);
+    if (graph && (rt->transport_kind != -1 || std::strcmp(rt->tr->name(), "virtual") != 0 || rt->dpg ||
+                  P.offload != 0 || rt->debug != 0))
+        return set_error(TPIPE_E_INVALID,
+                         "TPIPE_STEP_GRAPH needs an in-process transport, no T-Offload, no DP, no debug canaries");
+    // stage streams: separate per stage in the virtual pipeline, except while
+    // timing ops or kernel classes (OP_TIMES / PROFILE: serial, each op's or
+    // kernel's own GPU time)
+    for (int s : rt->owned) {
+        StageState& S = *rt->st[s];
+        S.pc = 0;
+        if (s == 0 && tok_dev) CU(cudaMemcpyAsync(S.tokens, tok_dev, io_bytes, cudaMemcpyDeviceToDevice, cs));
+        if (s == P.p - 1) {
+            if (tgt_dev) CU(cudaMemcpyAsync(S.targets, tgt_dev, io_bytes, cudaMemcpyDeviceToDevice, cs));
+            CU(cudaMemsetAsync(S.loss_slots, 0, (size_t)P.m * 4, cs));
+        }
+    }
+    const int gi = (flags & TPIPE_STEP_NO_OPT) ? 1 : 0;
+    bool replayed = false;
+    if (graph) {
+        // this step's AdamW hyper-parameters, read by the graph's AdamW launches
+        if (!rt->hp_dev) CU(cudaMalloc(&rt->hp_dev, sizeof(AdamHyper)));
+        const AdamHyper hp = hyper(rt, rt->t + 1);
+        CU(cudaMemcpyAsync(rt->hp_dev, &hp, sizeof(hp), cudaMemcpyHostToDevice, cs));
+        if (rt->gexec[gi]) {
+            CU(cudaGraphLaunch(rt->gexec[gi], cs));
+            replayed = true;
+        } else {
+            CU(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+            rt->capturing = true;
+        }
+    }
+    if (!replayed) {
+        const int rc = issue_ops(rt, flags, op_times);
+        if (rt->capturing) {
+            rt->capturing = false;
+            cudaGraph_t gr = nullptr;
+            const cudaError_t e = cudaStreamEndCapture(cs, &gr);
+            if (rc) {
+                if (gr) cudaGraphDestroy(gr);
+                return rc;
+            }
+            if (e != cudaSuccess || !gr) return set_error(TPIPE_E_CUDA, "step graph capture failed");
+            const cudaError_t ei = cudaGraphInstantiate(&rt->gexec[gi], gr, 0);
+            cudaGraphDestroy(gr);
+            if (ei != cudaSuccess) {
+                rt->gexec[gi] = nullptr;
+                return set_error(TPIPE_E_CUDA, "step graph instantiate failed");
+            }
+            rt->glaunches[gi] = launch_count() - l0;
+            CU(cudaGraphLaunch(rt->gexec[gi], cs));
+        } else if (rc) {
+            return rc;
+        }
+    }
     rt->host_issue_ms =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_issue0).count();
     float loss = 0.f;
@@ -702,7 +761,7 @@ int run_step_impl(tpipe_runtime* rt, const int32_t* tok_dev, const int32_t* tgt_
             }
     }
     if (!(flags & TPIPE_STEP_NO_OPT)) rt->t += 1;
-    rt->launches_last = launch_count() - l0;
+    rt->launches_last = replayed ? rt->glaunches[gi] : launch_count() - l0;
     return 0;
 }
 
@@ -967,6 +1026,9 @@ TP_API void tpipe_runtime_destroy(tpipe_runtime* rt) {
     }
     rt->tr.reset();
     rt->dpg.reset();
+    for (auto& g : rt->gexec)
+        if (g) cudaGraphExecDestroy(g);
+    if (rt->hp_dev) cudaFree(rt->hp_dev);
     for (auto e : rt->evpool) cudaEventDestroy(e);
     for (auto e : rt->tevpool) cudaEventDestroy(e);
     if (rt->h_tok_stage) cudaFreeHost(rt->h_tok_stage);

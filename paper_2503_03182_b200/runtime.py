@@ -13,6 +13,7 @@ from ._lib import check, lib
 STEP_NO_OPT = 1
 STEP_PROFILE = 2
 STEP_OP_TIMES = 4
+STEP_GRAPH = 8
 
 TRANSPORT_NCCL = 0
 TRANSPORT_IPC = 1

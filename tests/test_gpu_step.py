@@ -181,6 +181,35 @@ def test_side_stream_bitexact(cfg, dtype):
         assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
 
 
+@pytest.mark.parametrize("cfg,dtype,strategy,p", [("C_MID", 1, "tpipe", 1), ("C_MID", 1, "tpipe_trecomp", 2),
+                                                   ("C1", 0, "tpipe_trecomp", 4), ("C1", 1, "1f1b", 2)])
+def test_graph_step_bitexact(cfg, dtype, strategy, p):
+    """TPIPE_STEP_GRAPH (the step's device work captured once as a CUDA graph,
+    replayed afterwards; AdamW's per-step hyper-parameters from device memory)
+    vs the issued step: losses, gradients (a NO_OPT graph) and parameters after
+    3 optimizer steps bit-identical."""
+    _P, RT, _PR = mods()
+    c = C1 if cfg == "C1" else C_MID
+    m = 4
+    res = []
+    for flags in (0, RT.STEP_GRAPH):
+        plan, rt, _W = build(c, p, m, strategy, dtype)
+        tok, tgt = synth.tokens(c["vocab"], m, c["micro_batch"], c["seq_len"], step=1)
+        l0 = rt.step(tok, tgt, RT.STEP_NO_OPT | flags)
+        chunks = [(s, ch) for s in range(p) for ch in range(1, plan.v + 1)]
+        grads = [rt.get_grads(s, ch) for s, ch in chunks]
+        losses = [l0]
+        for step in range(3):
+            tok, tgt = synth.tokens(c["vocab"], m, c["micro_batch"], c["seq_len"], step=step + 2)
+            losses.append(rt.step(tok, tgt, flags))
+        assert rt.stats()["kernel_launches"] > 0
+        res.append((losses, grads, [rt.get_params(s, ch) for s, ch in chunks]))
+        rt.close()
+    assert res[0][0] == res[1][0]
+    for a, b in zip(res[0][1] + res[0][2], res[1][1] + res[1][2]):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
 @pytest.mark.parametrize("dtype", [0, 1])
 def test_offload_bitexact(dtype):
     """T-Offload (host AdamW for chunk 2) vs device AdamW: parameters
