@@ -298,23 +298,35 @@ ln_fwd_warp_kernel(const bf16* __restrict__ x, const bf16* __restrict__ gamma,
     constexpr int h = NV * 256;
     const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    if (row >= rows) return;
+    // gamma / beta staged once per CTA in shared memory, loaded with the rows
+    // (their latency off the tail; no registers held)
+    __shared__ __align__(16) bf16 sg[h], sbt[h];
+    for (int c = threadIdx.x * 8; c < h; c += 256 * 8) {
+        *reinterpret_cast<uint4*>(sg + c) = __ldg(reinterpret_cast<const uint4*>(gamma + c));
+        *reinterpret_cast<uint4*>(sbt + c) = __ldg(reinterpret_cast<const uint4*>(beta + c));
+    }
     const bf16* xr = x + (long)row * h;
     uint4 u[NV];
+    if (row < rows) {
 #pragma unroll
-    for (int i = 0; i < NV; ++i) ld8(xr + (i * 32 + lane) * 8, u[i]);
+        for (int i = 0; i < NV; ++i) ld8(xr + (i * 32 + lane) * 8, u[i]);
+    }
+    __syncthreads();
+    if (row >= rows) return;
     float mu, rs;
     if (!apply_only) {
-        float s = 0.f;
+        // eight independent partial sums per lane (short dependency chains),
+        // added in a fixed order
+        float s8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
             float v[8];
             unpack8(u[i], v);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) s += v[j];
+            for (int j = 0; j < 8; ++j) s8[j] += v[j];
         }
-        mu = warp_sum(s) / (float)h;
-        float q = 0.f;
+        mu = warp_sum(((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]))) / (float)h;
+        float q8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
             float v[8];
@@ -322,9 +334,10 @@ ln_fwd_warp_kernel(const bf16* __restrict__ x, const bf16* __restrict__ gamma,
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const float d = v[j] - mu;
-                q += d * d;
+                q8[j] += d * d;
             }
         }
+        const float q = ((q8[0] + q8[1]) + (q8[2] + q8[3])) + ((q8[4] + q8[5]) + (q8[6] + q8[7]));
         rs = 1.0f / sqrtf(warp_sum(q) / (float)h + LN_EPS);
         if (lane == 0) {
             mean[row] = mu;
@@ -340,8 +353,8 @@ ln_fwd_warp_kernel(const bf16* __restrict__ x, const bf16* __restrict__ gamma,
         const int c = (i * 32 + lane) * 8;
         float v[8], g[8], b[8], o[8];
         unpack8(u[i], v);
-        Vec<bf16>::load(gamma + c, g);
-        Vec<bf16>::load(beta + c, b);
+        unpack8(*reinterpret_cast<const uint4*>(sg + c), g);
+        unpack8(*reinterpret_cast<const uint4*>(sbt + c), b);
 #pragma unroll
         for (int j = 0; j < 8; ++j) o[j] = ln_y(v[j], mu, rs, g[j], b[j]);
         Vec<bf16>::store(yr + c, o);
