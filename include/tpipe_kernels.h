@@ -45,6 +45,17 @@ int tpipe_k_gemm(int dtype, int M, int N, int K,
                  const void* R, long ldr, void* C2, long ldc2,
                  const void* aux, long ldaux, void* stream);
 
+/* bf16 GEMM with the attention-backward row statistic fused into its
+ * epilogue (the out-projection data gradient): C = dO = A * B^T (bf16, ldc);
+ * Dout[(b*a + head)*s + q] = sum_{e < hd} C[m, head*hd + e] * O[m, head*hd + e]
+ * (fp32, the stored bf16 C times O, in column order) for m = b*s + q,
+ * a = N / hd heads. hd in {64, 128}, N % hd == 0, M % s == 0, ldo % 8 == 0.
+ * Dout is the D = rowsum(dO o O) of the attention backward (P:461,
+ * FlashAttention), so tpipe_k_attn_bwd's D pass can be skipped. */
+int tpipe_k_gemm_dot(int M, int N, int K, const void* A, long lda, int a_kmajor,
+                     const void* B, long ldb, int b_kmajor, void* C, long ldc,
+                     const void* O, long ldo, float* Dout, int s, int hd, void* stream);
+
 /* Same contract, always the SIMT kernel (used as the fp32-mode path). */
 int tpipe_k_gemm_simt(int dtype, int M, int N, int K,
                       const void* A, long lda, int a_kmajor,

@@ -44,6 +44,7 @@ def _declare(L):
                  vp, i64, vp]
     L.tpipe_k_gemm.argtypes = gemm_args
     L.tpipe_k_gemm_simt.argtypes = gemm_args
+    L.tpipe_k_gemm_dot.argtypes = [i32, i32, i32, vp, i64, i32, vp, i64, i32, vp, i64, vp, i64, vp, i32, i32, vp]
     L.tpipe_k_gemm_set_pair.argtypes = [i32]
     L.tpipe_k_gemm_set_pair.restype = None
     L.tpipe_k_gemm_set_pair_min_tiles.argtypes = [i32]

@@ -202,7 +202,7 @@ int attn_bwd_simt(int dtype, const void* qkv, const void* o, const void* dout, c
 // SIMT otherwise.
 int attn_fwd_tc5(const void* qkv, void* o, float* lse, int b, int s, int a, int d, cudaStream_t st);
 int attn_bwd_tc5(const void* qkv, const void* o, const void* dout, const float* lse, void* dqkv,
-                 float* ws, int b, int s, int a, int d, cudaStream_t st);
+                 float* ws, int b, int s, int a, int d, cudaStream_t st, bool have_d);
 
 // bf16 with head_dim 64/128: tcgen05 kernels (attn_tc5.cu); fp32 (parity
 // mode) and other head dims: SIMT.
@@ -215,10 +215,10 @@ int attn_fwd(int dtype, const void* qkv, void* o, float* lse, int b, int s, int 
 }
 
 int attn_bwd(int dtype, const void* qkv, const void* o, const void* dout, const float* lse,
-             void* dqkv, float* ws, int b, int s, int a, int d, cudaStream_t st) {
+             void* dqkv, float* ws, int b, int s, int a, int d, cudaStream_t st, bool have_d) {
     if (d > 32 * MAXE) return -1;
     if (dtype == DT_BF16 && (d == 64 || d == 128))
-        return attn_bwd_tc5(qkv, o, dout, lse, dqkv, ws, b, s, a, d, st);
+        return attn_bwd_tc5(qkv, o, dout, lse, dqkv, ws, b, s, a, d, st, have_d);
     return attn_bwd_simt(dtype, qkv, o, dout, lse, dqkv, ws, b, s, a, d, st);
 }
 

@@ -1277,7 +1277,7 @@ static int fwd5(const void* qkv, void* o, float* lse, int b, int s, int a, cudaS
 
 template <int D>
 static int bwd5(const void* qkv, const void* o, const void* dout, const float* lse, void* dqkv,
-                float* ws, int b, int s, int a, cudaStream_t st) {
+                float* ws, int b, int s, int a, cudaStream_t st, bool have_d) {
     constexpr int TB = fa5::Tile<D>::BYTES;
     constexpr int HB = (D / 64) * 64 * 128;
     constexpr int smem_kv = 1024 + 2 * TB + 2 * fa5::BwdCfg<D>::NQ * HB + 4 * 64 * 4 + 256;
@@ -1295,8 +1295,8 @@ static int bwd5(const void* qkv, const void* o, const void* dout, const float* l
     if (map2d(&md64, dout, (long)a * D, (long)b * s, (long)a * D, 64)) return -2;
     const long drows = (long)b * s * a;
     const unsigned dblocks = (unsigned)((drows * (D / 8) + 255) / 256);
-    if (launch_k(fa5::d_kernel<D / 8>, dim3(dblocks), dim3(256), 0, st, 1, (const bf16*)o, (const bf16*)dout, ws, s,
-                 a, drows) != cudaSuccess)
+    if (!have_d && launch_k(fa5::d_kernel<D / 8>, dim3(dblocks), dim3(256), 0, st, 1, (const bf16*)o,
+                            (const bf16*)dout, ws, s, a, drows) != cudaSuccess)
         return -3;
     const int grid = persistent_grid(((s + 127) / 128) * a * b);
     if (launch_k(fa5::dkdv2_kernel<D>, dim3(grid), dim3(384), smem_kv, st, 1, mq, mq64, md64, lse,
@@ -1305,7 +1305,7 @@ static int bwd5(const void* qkv, const void* o, const void* dout, const float* l
     if (launch_k(fa5::dq2_kernel<D>, dim3(grid), dim3(384), smem_q, st, 1, mq, md, mq64, lse, (const float*)ws,
                  (bf16*)dqkv, s, a, b) != cudaSuccess)
         return -3;
-    note_launches(3);
+    note_launches(have_d ? 2 : 3);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 
@@ -1320,9 +1320,9 @@ int attn_fwd_tc5(const void* qkv, void* o, float* lse, int b, int s, int a, int 
 }
 
 int attn_bwd_tc5(const void* qkv, const void* o, const void* dout, const float* lse, void* dqkv,
-                 float* ws, int b, int s, int a, int d, cudaStream_t st) {
-    return d == 64 ? bwd5<64>(qkv, o, dout, lse, dqkv, ws, b, s, a, st)
-                   : bwd5<128>(qkv, o, dout, lse, dqkv, ws, b, s, a, st);
+                 float* ws, int b, int s, int a, int d, cudaStream_t st, bool have_d) {
+    return d == 64 ? bwd5<64>(qkv, o, dout, lse, dqkv, ws, b, s, a, st, have_d)
+                   : bwd5<128>(qkv, o, dout, lse, dqkv, ws, b, s, a, st, have_d);
 }
 
 }  // namespace tpipe

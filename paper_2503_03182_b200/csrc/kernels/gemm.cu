@@ -343,7 +343,7 @@ __device__ __forceinline__ void epi_prefetch(const GemmDesc& g, long m, long n0,
 #pragma unroll
         for (int i = 0; i < 4; ++i) p.b[i] = (i < 2 || !half) ? __ldg(q + i) : make_uint4(0, 0, 0, 0);
     }
-    if (epi == EPI_BIAS_RES || epi == EPI_DGELU) {
+    if (epi == EPI_BIAS_RES || epi == EPI_DGELU || epi == EPI_STORE_DOT) {
         const bf16* src = epi == EPI_BIAS_RES ? reinterpret_cast<const bf16*>(g.res) + m * g.ldr
                                               : reinterpret_cast<const bf16*>(g.aux) + m * g.ldaux;
         const uint4* q = reinterpret_cast<const uint4*>(src + n0);
@@ -741,6 +741,7 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
                 epi_prefetch<EPI>(g, m, nb * BN + c_lo * 32, row_ok, cur, HAS_HALF && c_lo == Cfg::NCHUNK - 1);
             int tgt = -1;
             float lse_m = 0.f, gmax = -INFINITY, gsum = 0.f;
+            float dacc = 0.f;   // EPI_STORE_DOT
             if ((lse_mode || ce_mode) && row_ok) {
                 tgt = g.targets[m];
                 if (ce_mode) lse_m = g.lse[m];
@@ -809,6 +810,26 @@ __global__ void __launch_bounds__(tc_threads(EPI_WARPS), 1)
                     }
                 } else {
                     epi_math<EPI>(cur, v, v2);
+                    if (EPI == EPI_STORE_DOT) {
+                        // D of (row m, head): the stored (bf16-rounded) dO times O, in
+                        // column order; written when the head's last chunk is done
+                        const uint32_t* xw = reinterpret_cast<const uint32_t*>(cur.x);
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) {
+                            const __nv_bfloat162 d2 = __floats2bfloat162_rn(v[2 * q], v[2 * q + 1]);
+                            const float2 df = __bfloat1622float2(d2);
+                            dacc = fmaf(df.x, __uint_as_float(xw[q] << 16), dacc);
+                            dacc = fmaf(df.y, __uint_as_float(xw[q] & 0xffff0000u), dacc);
+                        }
+                        if ((n0 + 32) % g.dot_hd == 0) {
+                            if (row_ok) {
+                                const long bb = m / g.dot_s, qq = m % g.dot_s;
+                                const int heads = g.N / g.dot_hd, head = (n0 + 32) / g.dot_hd - 1;
+                                g.part[(bb * heads + head) * g.dot_s + qq] = dacc;
+                            }
+                            dacc = 0.f;
+                        }
+                    }
                     // next chunk's operands: in flight during this chunk's stores
                     // and the next TMEM load
                     if (pre && c + 1 < c_hi && n0 + 32 < g.N)
@@ -994,6 +1015,9 @@ static int launch_majors(const GemmDesc& g, cudaStream_t st) {
             return BN % 128 == 0 ? launch_majors_epi<(BN % 128 == 0 ? BN : 256), CG, EPI_LSE_PART>(g, st) : -4;
         case EPI_CE_GRAD:
             return BN % 128 == 0 ? launch_majors_epi<(BN % 128 == 0 ? BN : 256), CG, EPI_CE_GRAD>(g, st) : -4;
+        // a column group must hold whole heads (dot_hd <= 128)
+        case EPI_STORE_DOT:
+            return BN % 128 == 0 ? launch_majors_epi<(BN % 128 == 0 ? BN : 256), CG, EPI_STORE_DOT>(g, st) : -4;
         default: return -4;
     }
 }
@@ -1010,6 +1034,9 @@ int gemm_tc(const GemmDesc& g, cudaStream_t st) {
     // TMA: 16-byte aligned bases and row strides; 32-column epilogue chunks
     if ((g.epi == EPI_LSE_PART || g.epi == EPI_CE_GRAD) && (!g.targets || (g.epi == EPI_LSE_PART ? !g.part || !g.zt : !g.lse)))
         return -4;
+    if (g.epi == EPI_STORE_DOT && (!g.aux || !g.part || g.dot_s <= 0 || (g.dot_hd != 64 && g.dot_hd != 128) ||
+                                   g.N % g.dot_hd || g.M % g.dot_s || (g.ldaux % 8)))
+        return -4;
     if ((g.N % 32) || (g.lda % 8) || (g.ldb % 8) || (g.epi != EPI_LSE_PART && (g.ldc % 8)) ||
         ((g.epi == EPI_BIAS_GELU || g.epi == EPI_DGELU) && (g.ldc2 % 8)))
         return -5;
@@ -1023,7 +1050,7 @@ int gemm_tc(const GemmDesc& g, cudaStream_t st) {
     // cycles per K=16 step when fed, profiles/r2_mma_loop.jsonl), so pick the
     // width with the fewest waves x BN: e.g. N = 8192 on 74 pairs: 256-wide =
     // 4 waves of 256 (3.46 full), 224-wide = 296 tiles = 4 full waves of 224
-    const bool head = g.epi == EPI_LSE_PART || g.epi == EPI_CE_GRAD;
+    const bool head = g.epi == EPI_LSE_PART || g.epi == EPI_CE_GRAD || g.epi == EPI_STORE_DOT;
     auto width = [&](int rows, int units, int allow224) {
         const long mt = (g.M + rows - 1) / rows;
         int best = 256;
@@ -1061,6 +1088,7 @@ int gemm_tc(const GemmDesc& g, cudaStream_t st) {
 
 int gemm(int dtype, const GemmDesc& g, cudaStream_t st) {
     if (dtype == DT_BF16) return gemm_tc(g, st);
+    if (g.epi == EPI_STORE_DOT) return -4;   // tcgen05 path only
     return gemm_simt(DT_FP32, g, st);
 }
 

@@ -23,6 +23,11 @@ enum Epi : int {
     EPI_LSE_PART = 7,   // part[m][n/64] = (max, sum exp(z - max)) over each 64-column
                         // group; zt[m] = z[m, targets[m]]; no C store
     EPI_CE_GRAD = 8,    // C(bf16) = (exp(z - lse[m]) - [n == targets[m]]) * scale
+    // attention-output gradient with the backward's row statistic (tcgen05 path
+    // only): C(bf16) = dO = acc; part[(b*a + head)*s + q] = sum over the head's
+    // dot_hd columns of dO[m, .] * aux[m, .] (= O), fp32, column order, for
+    // m = b*s + q (the attention backward's D = rowsum(dO o O))
+    EPI_STORE_DOT = 9,
 };
 
 struct GemmDesc {
@@ -41,6 +46,8 @@ struct GemmDesc {
     float* part = nullptr;     // [M][ceil(N/64)][2]
     float* zt = nullptr;       // [M]
     float scale = 0.f;
+    // EPI_STORE_DOT: sequence length and head dim (N = heads * dot_hd)
+    int dot_s = 0, dot_hd = 0;
 };
 
 // 64-column groups of the fused head's LSE partials (the narrowest column span
@@ -80,8 +87,10 @@ int ln_bwd(int dtype, const void* dy, const void* x, const void* gamma, const fl
 int attn_fwd(int dtype, const void* qkv, void* o, float* lse, int b, int s, int a, int d,
              cudaStream_t st);
 // dqkv: [b*s, 3h]; ws: fp32 [b, a, s] for D = rowsum(dO * O).
+// have_d: ws already holds D (written by the out-projection dgrad GEMM's
+// EPI_STORE_DOT epilogue); the tcgen05 path then skips its D kernel.
 int attn_bwd(int dtype, const void* qkv, const void* o, const void* dout, const float* lse,
-             void* dqkv, float* ws, int b, int s, int a, int d, cudaStream_t st);
+             void* dqkv, float* ws, int b, int s, int a, int d, cudaStream_t st, bool have_d = false);
 
 
 // ---------------------------------------------------------------- embedding

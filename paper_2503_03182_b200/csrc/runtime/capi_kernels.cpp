@@ -45,6 +45,17 @@ TP_API int tpipe_k_gemm(int dtype, int M, int N, int K, const void* A, long lda,
     return launch_rc(gemm(dtype, g, S(stream)), "gemm");
 }
 
+TP_API int tpipe_k_gemm_dot(int M, int N, int K, const void* A, long lda, int a_kmajor, const void* B,
+                            long ldb, int b_kmajor, void* C, long ldc, const void* O, long ldo, float* Dout,
+                            int s, int hd, void* stream) {
+    GemmDesc g = mk(M, N, K, A, lda, a_kmajor, B, ldb, b_kmajor, EPI_STORE_DOT, C, ldc, nullptr, nullptr, 0,
+                    nullptr, 0, O, ldo);
+    g.part = Dout;
+    g.dot_s = s;
+    g.dot_hd = hd;
+    return launch_rc(gemm(DT_BF16, g, S(stream)), "gemm_dot");
+}
+
 TP_API int tpipe_k_gemm_simt(int dtype, int M, int N, int K, const void* A, long lda,
                              int a_kmajor, const void* B, long ldb, int b_kmajor, int epi, void* C,
                              long ldc, const void* bias, const void* R, long ldr, void* C2,

@@ -472,13 +472,27 @@ static int layer_backward(const Dims& D, const LW& W, const LayerPtrs& lp, const
     if (ss) TRY(stream_dep(st, ax, ev[2]));
     TRY(mm(D, h, h, M, w.G1, h, 0, lp.o, h, 0, EPI_ACC_F32, W.g[W_O], h, nullptr, nullptr, 0,
            nullptr, 0, nullptr, 0, ax));
-    // main: out-proj dgrad, attention backward (P recomputed from LSE)
-    TRY(mm(D, M, h, h, w.G1, h, 1, W.w[W_O], h, 0, EPI_STORE, w.dout, h, nullptr, nullptr, 0,
-           nullptr, 0, nullptr, 0, st));
+    // main: out-proj dgrad, attention backward (P recomputed from LSE). On the
+    // tcgen05 path the dgrad GEMM's epilogue also produces the backward's
+    // D = rowsum(dO o O) per (token, head) (EPI_STORE_DOT): no separate pass
+    const bool fuse_d = dt == DT_BF16 && (D.hd == 64 || D.hd == 128);
+    if (fuse_d) {
+        GemmDesc g;
+        g.M = M; g.N = h; g.K = h;
+        g.A = w.G1; g.lda = h; g.a_kmajor = 1;
+        g.B = W.w[W_O]; g.ldb = h; g.b_kmajor = 0;
+        g.epi = EPI_STORE_DOT; g.C = w.dout; g.ldc = h;
+        g.aux = lp.o; g.ldaux = h; g.part = w.Dv; g.dot_s = D.s; g.dot_hd = D.hd;
+        ProfScope ps(0, 2.0 * M * h * h, st);
+        if (gemm(dt, g, st)) return -7;
+    } else {
+        TRY(mm(D, M, h, h, w.G1, h, 1, W.w[W_O], h, 0, EPI_STORE, w.dout, h, nullptr, nullptr, 0,
+               nullptr, 0, nullptr, 0, st));
+    }
     {
         // algorithmic: P recompute + dV, dP, dQ, dK = 5 GEMMs over the causal triangle
         ProfScope ps(2, 10.0 * D.b * D.a * (0.5 * D.s * (D.s + 1)) * D.hd, st);
-        TRY(attn_bwd(dt, lp.qkv, lp.o, w.dout, lp.lse, w.dqkv, w.Dv, D.b, D.s, D.a, D.hd, st));
+        TRY(attn_bwd(dt, lp.qkv, lp.o, w.dout, lp.lse, w.dqkv, w.Dv, D.b, D.s, D.a, D.hd, st, fuse_d));
     }
     if (ss) TRY(stream_dep(st, ax, ev[3]));
     // aux: QKV weight gradient

@@ -29,6 +29,11 @@ def tpipe_k_gemm(dtype, M, N, K, A, lda, a_kmajor, B, ldb, b_kmajor, epi, C, ldc
              _p(R), ldr, _p(C2), ldc2, _p(aux), ldaux, _stream()), "tpipe_k_gemm")
 
 
+def tpipe_k_gemm_dot(M, N, K, A, lda, a_kmajor, B, ldb, b_kmajor, C, ldc, O, ldo, Dout, s, hd):
+    check(lib().tpipe_k_gemm_dot(M, N, K, _p(A), lda, a_kmajor, _p(B), ldb, b_kmajor, _p(C), ldc, _p(O), ldo,
+                                 _p(Dout), s, hd, _stream()), "tpipe_k_gemm_dot")
+
+
 def tpipe_k_ln_fwd(dtype, x, g, b, y, mean, rstd, rows, h):
     check(lib().tpipe_k_ln_fwd(dtype, _p(x), _p(g), _p(b), _p(y), _p(mean), _p(rstd), rows, h,
                                _stream()), "ln_fwd")

@@ -611,3 +611,34 @@ def test_layernorm_bwd_rows_vs_staged(rows, hd):
     assert rel_l2(h(dx), h(old[0])) < 1e-2
     for u, v in zip(new[1:], old[1:]):
         assert max_rel(h(u), h(v)) < 1e-5
+
+
+@pytest.mark.parametrize("M,N,Kd,s,hd,bk", [(2048, 2048, 2048, 2048, 128, 0), (512, 256, 320, 256, 64, 0),
+                                             (4096, 4096, 512, 1024, 128, 0), (1024, 2048, 256, 512, 128, 1)])
+def test_gemm_dot_epilogue(M, N, Kd, s, hd, bk):
+    """EPI_STORE_DOT (the out-projection data gradient with the attention
+    backward's D = rowsum(dO o O) fused into its epilogue): C matches fp64 and
+    D equals the fp64 dot of the stored bf16 C with O per (token, head) in the
+    [b, a, s] layout the attention backward reads; bit-reproducible."""
+    k = K()
+    rng = np.random.default_rng(M + N + Kd + hd)
+    A = rng.standard_normal((M, Kd)).astype(np.float32)
+    B = rng.standard_normal((N, Kd)).astype(np.float32)
+    At = t(A, "bf16")
+    Bt = t(B if bk else B.T.copy(), "bf16")
+    O = t(rng.standard_normal((M, N)), "bf16")
+    ref = h(At) @ h(Bt if bk else Bt.T).T
+
+    def run():
+        C = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
+        Dv = torch.full((M // s, N // hd, s), 7.0, device=dev)
+        k.tpipe_k_gemm_dot(M, N, Kd, At, Kd, 1, Bt, Kd if bk else N, bk, C, N, O, N, Dv, s, hd)
+        torch.cuda.synchronize()
+        return C, Dv
+    (C, Dv), (C2, Dv2) = run(), run()
+    assert torch.equal(C, C2) and torch.equal(Dv, Dv2)
+    assert rel_l2(h(C), ref) < 1e-2
+    a = N // hd
+    prod = (h(C) * h(O)).reshape(M // s, s, a, hd).sum(-1)          # [b, s, a]
+    Dref = prod.transpose(0, 2, 1)                                    # [b, a, s]
+    assert max_rel(h(Dv), Dref) < 1e-4
