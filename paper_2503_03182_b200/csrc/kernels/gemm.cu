@@ -301,12 +301,11 @@ struct TcCfg {
     static_assert(BN <= 256 && BN % 16 == 0, "one tcgen05.mma covers N <= 256");
     static constexpr int BNC = BN / CG;                      // B rows (N) staged per CTA
     static constexpr int BNC64 = (BNC + 63) / 64 * 64;       // MN-major B: whole 64-column boxes
-    // pair tiles with the 8-warp (two-output) epilogues: 5 operand stages and a
-    // 4-deep staging ring per warp, so a chunk's TMA stores never wait for the
-    // previous chunk's (the wait for a store to finish reading its buffer was
-    // ~1/3 of a chunk's time); the others: 2-deep staging
-    static constexpr int NSTG = (CG == 2 && EPI_WARPS == 8) ? 4 : 2;
-    static constexpr int STAGES = CG == 2 ? (EPI_WARPS == 8 ? 5 : 6) : (BN > 128 ? 4 : 6);
+    // 2-deep staging ring per epilogue warp; pair tiles keep 6 operand stages
+    // (a 4-deep ring for the two-output epilogues at the cost of a 6th stage
+    // measured 1-2% slower on FC1 / FC2-dgrad, profiles/r2_gemm_ab_ring4.jsonl)
+    static constexpr int NSTG = 2;
+    static constexpr int STAGES = CG == 2 ? 6 : (BN > 128 ? 4 : 6);
     static_assert(1024 + STAGES * (TC_BM * TC_BK * 2 + ((BN / CG + 63) / 64 * 64) * TC_BK * 2) +
                           EPI_WARPS * NSTG * (EPI_WARPS == 8 ? 2048 : 4096) + 256 <= 232448,
                   "shared memory over the 227 KB per-CTA limit");
