@@ -153,8 +153,11 @@ __device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
     return d;
 }
-// gelu_fast / gelu_fast_and_grad on a pair: the same .rn op sequence per
-// lane (bit-identical to the scalar versions), half the FP instructions
+// gelu_fast / gelu_fast_and_grad on a pair: the same op sequence per lane,
+// half the FP instructions. ptxas contracts the packed u + 0.044715 u^3 into
+// an FFMA2 (so these are not bit-identical to the scalar versions), the same
+// way in both: the forward's stored GELU and the backward's recomputed one
+// stay bit-identical (tests/test_gpu_kernels.py::test_gelu_recompute_bitexact)
 __device__ __forceinline__ uint64_t gelu_fast2(uint64_t u) {
     const uint64_t C = pk2(0.7978845608028654f, 0.7978845608028654f), A = pk2(0.044715f, 0.044715f);
     const uint64_t inner = fmul2(C, fadd2(u, fmul2(A, fmul2(fmul2(u, u), u))));

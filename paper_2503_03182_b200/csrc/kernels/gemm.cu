@@ -391,8 +391,8 @@ __device__ __forceinline__ uint64_t bf2_to_f2(uint32_t w) {
 
 // epilogue math on 32 columns (no stores); out2 for GELU/dGELU. Rows m >= M
 // (TMA clips their stores) prefetched zeros. Packed fp32x2 ops throughout
-// (the same .rn rounding per element as scalar code; the epilogue's FP issue
-// was the larger part of its per-chunk time, profiles/r2_gemm_trace_*.jsonl).
+// (the epilogue's FP issue was the larger part of its per-chunk time,
+// profiles/r2_gemm_trace_*.jsonl; see gelu_fast2 on contraction).
 template <int EPI>
 __device__ __forceinline__ void epi_math(const EpiPre& p, float (&v)[32], float (&v2)[32]) {
     constexpr int epi = EPI;

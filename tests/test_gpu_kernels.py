@@ -642,3 +642,25 @@ def test_gemm_dot_epilogue(M, N, Kd, s, hd, bk):
     prod = (h(C) * h(O)).reshape(M // s, s, a, hd).sum(-1)          # [b, s, a]
     Dref = prod.transpose(0, 2, 1)                                    # [b, a, s]
     assert max_rel(h(Dv), Dref) < 1e-4
+
+
+@pytest.mark.parametrize("M,N,Kd,majors", [(2048, 8192, 256, (1, 1)), (512, 1024, 128, (1, 0))])
+def test_gelu_recompute_bitexact(M, N, Kd, majors):
+    """The GELU the backward recomputes (EPI_DGELU's C2 = gelu(U)) is
+    bit-identical to the activation the forward stored (EPI_BIAS_GELU's C2 =
+    gelu(u)) for the same stored pre-activation u: the FC2 weight gradient sees
+    exactly the forward's operand."""
+    ak, bk = majors
+    k = K()
+    rng = np.random.default_rng(M + N)
+    A = t(rng.standard_normal((M, Kd)), "bf16")
+    B = t(rng.standard_normal((N, Kd)) if bk else rng.standard_normal((Kd, N)), "bf16")
+    bias = t(0.5 * rng.standard_normal(N), "bf16")
+    U = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
+    Gf = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
+    k.tpipe_k_gemm(1, M, N, Kd, A, Kd, ak, B, Kd if bk else N, bk, k.EPI_BIAS_GELU, U, N, bias=bias, C2=Gf, ldc2=N)
+    Dd = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
+    Gb = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
+    k.tpipe_k_gemm(1, M, N, Kd, A, Kd, ak, B, Kd if bk else N, bk, k.EPI_DGELU, Dd, N, C2=Gb, ldc2=N, aux=U, ldaux=N)
+    torch.cuda.synchronize()
+    assert torch.equal(Gf, Gb)
