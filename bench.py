@@ -552,6 +552,10 @@ def hbm_kernels(c, hbm_peak):
         ("ln_fwd", lambda: K.tpipe_k_ln_fwd(1, x, g, b, y, mean, rstd, M, h), 2 * 2 * M * h + 8 * M),
         ("ln_bwd_rsum", lambda: K.tpipe_k_ln_bwd_rsum(1, dy, x, g, mean, rstd, res, dx, dg, db, drs, ws, M, h),
          4 * 2 * M * h + 8 * M),
+        # the layer backward's form: the same kernel, column partials left for the
+        # layer's one shared reduce launch (bytes: the partials written, too)
+        ("ln_bwd_partials", lambda: K.tpipe_k_ln_bwd_partials(dy, x, g, mean, rstd, res, dx, ws, M, h, 1),
+         4 * 2 * M * h + 8 * M + 3 * 4 * ((M + 15) // 16) * h),
         ("colsum_ffn", lambda: K.tpipe_k_colsum(1, du, dbias, ws, M, f), 2 * M * f),
         ("adamw_64M", lambda: K.tpipe_k_adamw(1, master, mm_, vv, grad, w, n_p, 1, 1e-4, 0.9, 0.95, 1e-8,
                                                 0.1, 0.1, 0.05), 30 * n_p),

@@ -102,6 +102,15 @@ int tpipe_k_ln_bwd_rsum(int dtype, const void* dy, const void* x, const void* ga
                         float* dgamma, float* dbeta, float* dresid_sum, float* ws, int rows,
                         int h, void* stream);
 
+/* The layer backward's form of the LN backward (bf16, h % 256 == 0): dx as
+ * in tpipe_k_ln_bwd (+ resid) and, instead of reduced dgamma / dbeta /
+ * dresid_sum, the per-16-row-block column partials ws[3][ceil(rows/16)][h]
+ * (fp32; the layer backward reduces them together with its bias-gradient
+ * partials in one launch). with_rsum: the third partial. */
+int tpipe_k_ln_bwd_partials(const void* dy, const void* x, const void* gamma, const float* mean,
+                            const float* rstd, const void* resid, void* dx, float* ws, int rows, int h,
+                            int with_rsum, void* stream);
+
 /* Causal attention forward. qkv [b*s, 3h] (q|k|v, head j at columns j*d),
  * o [b*s, h], lse fp32 [b, a, s]; h = a*d, scale 1/sqrt(d). */
 int tpipe_k_attn_fwd(int dtype, const void* qkv, void* o, float* lse,

@@ -56,6 +56,7 @@ def _declare(L):
     L.tpipe_k_ln_fwd.argtypes = [i32, vp, vp, vp, vp, vp, vp, i32, i32, vp]
     L.tpipe_k_ln_bwd.argtypes = [i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp]
     L.tpipe_k_ln_bwd_rsum.argtypes = [i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp]
+    L.tpipe_k_ln_bwd_partials.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, i32, vp]
     L.tpipe_k_attn_fwd.argtypes = [i32, vp, vp, vp, i32, i32, i32, i32, vp]
     L.tpipe_k_attn_bwd.argtypes = [i32, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, vp]
     L.tpipe_k_embed_fwd.argtypes = [i32, vp, vp, vp, vp, i32, i32, i32, vp]

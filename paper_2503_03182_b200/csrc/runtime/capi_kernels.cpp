@@ -86,6 +86,14 @@ TP_API int tpipe_k_ln_bwd(int dtype, const void* dy, const void* x, const void* 
                      "ln_bwd");
 }
 
+TP_API int tpipe_k_ln_bwd_partials(const void* dy, const void* x, const void* gamma, const float* mean,
+                                   const float* rstd, const void* resid, void* dx, float* ws, int rows, int h,
+                                   int with_rsum, void* stream) {
+    return launch_rc(ln_bwd_partials(DT_BF16, dy, x, gamma, mean, rstd, resid, dx, ws, rows, h, with_rsum,
+                                     S(stream)),
+                     "ln_bwd_partials");
+}
+
 TP_API int tpipe_k_ln_bwd_rsum(int dtype, const void* dy, const void* x, const void* gamma,
                                const float* mean, const float* rstd, const void* resid, void* dx,
                                float* dgamma, float* dbeta, float* dresid_sum, float* ws, int rows,

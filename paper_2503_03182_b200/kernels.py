@@ -44,6 +44,11 @@ def tpipe_k_ln_bwd(dtype, dy, x, g, mean, rstd, resid, dx, dg, db, ws, rows, h):
                                _p(dg), _p(db), _p(ws), rows, h, _stream()), "ln_bwd")
 
 
+def tpipe_k_ln_bwd_partials(dy, x, g, mean, rstd, resid, dx, ws, rows, h, with_rsum=1):
+    check(lib().tpipe_k_ln_bwd_partials(_p(dy), _p(x), _p(g), _p(mean), _p(rstd), _p(resid), _p(dx), _p(ws),
+                                        rows, h, 1 if with_rsum else 0, _stream()), "ln_bwd_partials")
+
+
 def tpipe_k_ln_bwd_rsum(dtype, dy, x, g, mean, rstd, resid, dx, dg, db, drs, ws, rows, h):
     check(lib().tpipe_k_ln_bwd_rsum(dtype, _p(dy), _p(x), _p(g), _p(mean), _p(rstd), _p(resid),
                                     _p(dx), _p(dg), _p(db), _p(drs), _p(ws), rows, h, _stream()),

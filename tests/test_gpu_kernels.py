@@ -664,3 +664,34 @@ def test_gelu_recompute_bitexact(M, N, Kd, majors):
     k.tpipe_k_gemm(1, M, N, Kd, A, Kd, ak, B, Kd if bk else N, bk, k.EPI_DGELU, Dd, N, C2=Gb, ldc2=N, aux=U, ldaux=N)
     torch.cuda.synchronize()
     assert torch.equal(Gf, Gb)
+
+
+def test_ln_bwd_partials_capi():
+    """tpipe_k_ln_bwd_partials (the layer backward's LN backward): dx equals
+    the reduced form's and the column partials sum to its dgamma / dbeta /
+    residual column sum in block order."""
+    rows, hd = 300, 2048
+    rng = np.random.default_rng(5)
+    x = t(rng.standard_normal((rows, hd)), "bf16")
+    g = t(1 + 0.1 * rng.standard_normal(hd), "bf16")
+    b = t(0.1 * rng.standard_normal(hd), "bf16")
+    dy = t(rng.standard_normal((rows, hd)), "bf16")
+    res = t(rng.standard_normal((rows, hd)), "bf16")
+    y = torch.empty_like(x)
+    mean = torch.empty(rows, device=dev)
+    rstd = torch.empty(rows, device=dev)
+    k = K()
+    k.tpipe_k_ln_fwd(1, x, g, b, y, mean, rstd, rows, hd)
+    nb = (rows + 15) // 16
+    ws = torch.empty(3 * nb * hd, device=dev)
+    dx = torch.empty_like(x)
+    k.tpipe_k_ln_bwd_partials(dy, x, g, mean, rstd, res, dx, ws, rows, hd, 1)
+    dx2 = torch.empty_like(x)
+    dg, db, drs = torch.zeros(hd, device=dev), torch.zeros(hd, device=dev), torch.zeros(hd, device=dev)
+    ws2 = torch.empty(3 * nb * hd, device=dev)
+    k.tpipe_k_ln_bwd_rsum(1, dy, x, g, mean, rstd, res, dx2, dg, db, drs, ws2, rows, hd)
+    torch.cuda.synchronize()
+    assert torch.equal(dx, dx2)
+    parts = h(ws).reshape(3, nb, hd).sum(1)
+    for got, ref in zip(parts, (h(dg), h(db), h(drs))):
+        assert max_rel(got, ref) < 1e-5
