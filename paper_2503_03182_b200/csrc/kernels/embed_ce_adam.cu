@@ -358,9 +358,61 @@ __global__ void adamw_kernel(float* __restrict__ master, float* __restrict__ m,
     if (w) w[i] = from_f<T>(o.w);
 }
 
+// Four consecutive parameters per thread with 16-byte loads / stores (the
+// fp32 states are ~29 of the 30 bytes per parameter; scalar loads left the
+// kernel at ~0.79 of the HBM peak). Same adam_elem arithmetic per element.
+template <typename T>
+__global__ void adamw4_kernel(float* __restrict__ master, float* __restrict__ m, float* __restrict__ v,
+                              float* __restrict__ grad, T* __restrict__ w, long n, int decay, AdamHyper hp,
+                              const AdamHyper* __restrict__ hp_dev) {
+    const long i = ((long)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (i >= n) return;
+    if (hp_dev) hp = *hp_dev;
+    if (i + 4 <= n) {
+        const float4 w4 = *reinterpret_cast<const float4*>(master + i);
+        const float4 m4 = *reinterpret_cast<const float4*>(m + i);
+        const float4 v4 = *reinterpret_cast<const float4*>(v + i);
+        const float4 g4 = *reinterpret_cast<const float4*>(grad + i);
+        const AdamOut a = adam_elem(w4.x, m4.x, v4.x, g4.x, decay, hp);
+        const AdamOut b = adam_elem(w4.y, m4.y, v4.y, g4.y, decay, hp);
+        const AdamOut c = adam_elem(w4.z, m4.z, v4.z, g4.z, decay, hp);
+        const AdamOut d = adam_elem(w4.w, m4.w, v4.w, g4.w, decay, hp);
+        *reinterpret_cast<float4*>(master + i) = make_float4(a.w, b.w, c.w, d.w);
+        *reinterpret_cast<float4*>(m + i) = make_float4(a.m, b.m, c.m, d.m);
+        *reinterpret_cast<float4*>(v + i) = make_float4(a.v, b.v, c.v, d.v);
+        *reinterpret_cast<float4*>(grad + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (w) {
+            w[i] = from_f<T>(a.w);
+            w[i + 1] = from_f<T>(b.w);
+            w[i + 2] = from_f<T>(c.w);
+            w[i + 3] = from_f<T>(d.w);
+        }
+        return;
+    }
+    for (long j = i; j < n; ++j) {   // ragged tail (< 4 elements)
+        const AdamOut o = adam_elem(master[j], m[j], v[j], grad[j], decay, hp);
+        master[j] = o.w;
+        m[j] = o.m;
+        v[j] = o.v;
+        grad[j] = 0.f;
+        if (w) w[j] = from_f<T>(o.w);
+    }
+}
+
 int adamw(int dtype, float* master, float* m, float* v, float* grad, void* w, long n, int decay,
           const AdamHyper& hp, cudaStream_t st, const AdamHyper* hp_dev) {
     if (n <= 0) return 0;
+    if (((reinterpret_cast<uintptr_t>(master) | reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(v) |
+          reinterpret_cast<uintptr_t>(grad)) & 15) == 0) {
+        const int blocks4 = (int)((n + 1023) / 1024);
+        if (dtype == DT_BF16)
+            adamw4_kernel<bf16><<<blocks4, 256, 0, st>>>(master, m, v, grad, (bf16*)w, n, decay, hp, hp_dev);
+        else
+            adamw4_kernel<float><<<blocks4, 256, 0, st>>>(master, m, v, grad, (float*)(w == master ? nullptr : w),
+                                                         n, decay, hp, hp_dev);
+        note_launches(1);
+        return cudaGetLastError() == cudaSuccess ? 0 : -3;
+    }
     const int blocks = (int)((n + 255) / 256);
     if (dtype == DT_BF16)
         adamw_kernel<bf16><<<blocks, 256, 0, st>>>(master, m, v, grad, (bf16*)w, n, decay, hp, hp_dev);

@@ -442,10 +442,13 @@ def test_colsum(rows, n):
 
 
 # ------------------------------------------------------------------ AdamW
+@pytest.mark.parametrize("off", [0, 1])
 @pytest.mark.parametrize("decay", [0, 1])
-def test_adamw_device_host_bitexact(decay):
+def test_adamw_device_host_bitexact(decay, off):
     """Device AdamW == host AdamW bit for bit (T-Offload on/off),
-    and both match the fp64 oracle step."""
+    and both match the fp64 oracle step. off = 1: fp32 states one element past
+    a 16-byte boundary (the scalar kernel; off = 0 the 4-wide one with a
+    ragged tail)."""
     n = 100_003
     rng = np.random.default_rng(9)
     w0 = rng.standard_normal(n).astype(np.float32)
@@ -455,7 +458,8 @@ def test_adamw_device_host_bitexact(decay):
     hp = dict(lr=3e-3, b1=0.9, b2=0.95, eps=1e-8, wd=0.1)
     step = 3
     bc1, bc2 = 1 - 0.9 ** step, 1 - 0.95 ** step
-    Wm, Mm, Vm, Gm = (torch.tensor(x, device=dev) for x in (w0, m0, v0, g0))
+    Wm, Mm, Vm, Gm = (torch.tensor(np.concatenate([np.zeros(off, np.float32), x]), device=dev)[off:]
+                      for x in (w0, m0, v0, g0))
     wb = torch.empty(n, dtype=torch.bfloat16, device=dev)
     K().tpipe_k_adamw(1, Wm, Mm, Vm, Gm, wb, n, decay, hp["lr"], hp["b1"], hp["b2"], hp["eps"],
                       hp["wd"], bc1, bc2)
