@@ -216,10 +216,13 @@ __device__ __forceinline__ int sched_item(int k, int T) {
 //   rows : S_g -> P_g (one pass, 64 scores per thread in registers) -> wait PV_{g-1}
 //          -> O *= corr_g (skipped per warp when corr == 1) -> P_g ready
 // Item t (heaviest first): qb = nqb-1 - t/(a*nb), head = t%a, batch = (t/a)%nb.
-template <int D>
-__global__ void __launch_bounds__(384, 1)
+// NG column groups of 4 softmax warps each (row r = TMEM lane; fwd5 uses 2).
+template <int D, int NG>
+__global__ void __launch_bounds__(128 + 128 * NG, 1)
     fwd2_kernel(const __grid_constant__ CUtensorMap tm_qkv, bf16* __restrict__ o,
                 float* __restrict__ lse, int s, int a, int nb) {
+    constexpr int SC = BR / NG;          // scores per softmax thread per tile
+    constexpr int OC = D / NG / 32;      // 32-column O chunks per group
     constexpr int TB = Tile<D>::BYTES;
     constexpr int STAGES = 2;
     extern __shared__ uint8_t smraw[];
@@ -227,9 +230,9 @@ __global__ void __launch_bounds__(384, 1)
     uint8_t* sQ = sm;                        // [2]
     uint8_t* sK = sQ + 2 * TB;               // [STAGES]
     uint8_t* sV = sK + STAGES * TB;          // [STAGES]
-    float* sMax = reinterpret_cast<float*>(sV + STAGES * TB);   // [2 iters][2 groups][128]
-    float* sSum = sMax + 4 * BR;                                  // [2 groups][128]
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sSum + 2 * BR);
+    float* sMax = reinterpret_cast<float*>(sV + STAGES * TB);   // [2 iters][NG groups][128]
+    float* sSum = sMax + 2 * NG * BR;                             // [NG groups][128]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sSum + NG * BR);
     uint64_t* q_full = bar;                  // [2]
     uint64_t* q_empty = bar + 2;             // [2]
     // K and V stages have their own barriers: K_{g+2} is fetched once S_g has
@@ -267,7 +270,7 @@ __global__ void __launch_bounds__(384, 1)
             mbar_init(&v_full[i], 1);
             mbar_init(&v_empty[i], 1);
         }
-        mbar_init(p_full, 256);
+        mbar_init(p_full, 128 * NG);
         mbar_init(pv_done, 1);
         fence_mbar_init();
     }
@@ -388,8 +391,8 @@ __global__ void __launch_bounds__(384, 1)
             }
         }
     } else if (warp >= 4) {
-        // 8 softmax warps: row r = TMEM lane (warp % 4 = lane quarter); column
-        // group cg owns scores [64cg, 64cg+64) and O columns [cg D/2, (cg+1) D/2)
+        // 4 NG softmax warps: row r = TMEM lane (warp % 4 = lane quarter); column
+        // group cg owns scores [SC cg, SC (cg+1)) and O columns [cg D/NG, (cg+1) D/NG)
         const int et = threadIdx.x - 128;
         const int r = et & 127, cg = et >> 7;
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
@@ -408,45 +411,44 @@ __global__ void __launch_bounds__(384, 1)
                 mbar_wait(&s_full[g & 1], (g >> 1) & 1);
                 if (threadIdx.x == 128) TR(3, g);
                 tc_fence_after();
-                float sv[64];
-                {
-                    uint32_t ra[32], rb[32];
-                    tmem_ld32(tS + cg * 64, ra);
-                    tmem_ld32(tS + cg * 64 + 32, rb);
+                float sv[SC];
+#pragma unroll
+                for (int hh = 0; hh < SC / 32; ++hh) {
+                    uint32_t ra[32];
+                    tmem_ld32(tS + cg * SC + hh * 32, ra);
                     tmem_wait_ld();
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        sv[e] = __uint_as_float(ra[e]);
-                        sv[32 + e] = __uint_as_float(rb[e]);
-                    }
+                    for (int e = 0; e < 32; ++e) sv[hh * 32 + e] = __uint_as_float(ra[e]);
                 }
                 if (j == nkb - 1) {   // diagonal tile: keys after the query are masked
-                    const int k0 = j * BR + cg * 64;
+                    const int k0 = j * BR + cg * SC;
 #pragma unroll
-                    for (int e = 0; e < 64; ++e)
+                    for (int e = 0; e < SC; ++e)
                         if (k0 + e > q) sv[e] = -INFINITY;
                 }
                 // running max in scaled units: max(s) * sc == max(s * sc) (sc > 0)
                 float lmx = -INFINITY;
 #pragma unroll
-                for (int e = 0; e < 64; e += 2) lmx = fmax3(lmx, sv[e], sv[e + 1]);
+                for (int e = 0; e < SC; e += 2) lmx = fmax3(lmx, sv[e], sv[e + 1]);
                 lmx *= sc;
-                float* mb = sMax + (g & 1) * 2 * BR;
+                float* mb = sMax + (g & 1) * NG * BR;
                 mb[cg * BR + r] = lmx;
                 if (threadIdx.x == 128) TR(4, g);
-                named_bar_sync(1, 256);
+                named_bar_sync(1, 128 * NG);
                 // lazy rescaling: the reference max moves only when a score exceeds
                 // it by more than 2^8 (P <= 256 is exact enough in bf16 and the sums
-                // are fp32), so O is rarely rescaled; both column groups see the
-                // same values and take the same decision
-                const float mnew = fmax3(m, lmx, mb[(cg ^ 1) * BR + r]);
+                // are fp32), so O is rarely rescaled; every column group sees the
+                // same values and takes the same decision
+                float mnew = m;
+#pragma unroll
+                for (int c2 = 0; c2 < NG; ++c2) mnew = fmaxf(mnew, mb[c2 * BR + r]);
                 const float mx = mnew - m > 8.0f ? mnew : m;
                 const uint64_t sc2 = pk2(sc, sc), nm2 = pk2(-mx, -mx);
                 uint64_t rs2 = pk2(0.f, 0.f);
-                uint32_t pk[32];
+                uint32_t pk[SC / 2];
                 if (j < nkb - 1) {   // no masked score: part of the exponentials on the FMA pipe
 #pragma unroll
-                    for (int e = 0; e < 64; e += 2) {
+                    for (int e = 0; e < SC; e += 2) {
                         const uint64_t x2 = ffma2(pk2(sv[e], sv[e + 1]), sc2, nm2);
                         float p0, p1;
                         if (((e >> 1) & 15) < FWD_POLY_OF_16) {
@@ -462,7 +464,7 @@ __global__ void __launch_bounds__(384, 1)
                     }
                 } else {
 #pragma unroll
-                    for (int e = 0; e < 64; e += 2) {
+                    for (int e = 0; e < SC; e += 2) {
                         float x0, x1;
                         upk2(ffma2(pk2(sv[e], sv[e + 1]), sc2, nm2), x0, x1);
                         const float p0 = ex2(x0), p1 = ex2(x1);
@@ -476,14 +478,17 @@ __global__ void __launch_bounds__(384, 1)
                 const float corr = ex2(m - mx);
                 l = l * corr + rs;        // partial (this group's columns), same m history
                 m = mx;
-                tmem_st32(tS + cg * 32, pk);   // P_g over S_g: packed cols [32cg, 32cg+32)
+                // P_g over S_g: packed cols [SC/2 cg, SC/2 (cg+1)) (every group's S
+                // was loaded before the barrier above)
+                if constexpr (SC == 64) tmem_st32(tS + cg * 32, pk);
+                else tmem_st16(tS + cg * 16, pk);
                 if (threadIdx.x == 128) TR(5, g);
                 if (j > 0) {
                     mbar_wait(pv_done, (g - 1) & 1);
                     tc_fence_after();
                     if (__any_sync(0xffffffffu, corr != 1.0f)) {
 #pragma unroll
-                        for (int c = cg * (D / 64); c < (cg + 1) * (D / 64); ++c) {
+                        for (int c = cg * OC; c < (cg + 1) * OC; ++c) {
                             uint32_t ov[32];
                             tmem_ld32(tO + lane_off + c * 32, ov);
                             tmem_wait_ld();
@@ -496,19 +501,21 @@ __global__ void __launch_bounds__(384, 1)
                 tmem_wait_st();
                 tc_fence_before();
                 if (threadIdx.x == 128) TR(6, g);
-                if (threadIdx.x == 383) TR(7, g);
+                if (threadIdx.x == 127 + 128 * NG) TR(7, g);
                 mbar_arrive(p_full);
             }
             sSum[cg * BR + r] = l;
-            named_bar_sync(1, 256);
-            l += sSum[(cg ^ 1) * BR + r];
+            named_bar_sync(1, 128 * NG);
+            l = 0.f;   // every group adds the NG partial sums in the same order
+#pragma unroll
+            for (int c2 = 0; c2 < NG; ++c2) l += sSum[c2 * BR + r];
             mbar_wait(pv_done, (g - 1) & 1);
             tc_fence_after();
             // tcgen05.ld is .sync.aligned: every lane loads; only valid rows store
             const float inv = 1.0f / l;
             bf16* orow = o + ((long)b * s + q) * h + head * D;
 #pragma unroll
-            for (int c = cg * (D / 64); c < (cg + 1) * (D / 64); ++c) {
+            for (int c = cg * OC; c < (cg + 1) * OC; ++c) {
                 float v[32];
                 tmem_ld32f(tO + lane_off + c * 32, v);
                 if (q < s) {
@@ -524,7 +531,7 @@ __global__ void __launch_bounds__(384, 1)
                 }
             }
             if (q < s && cg == 0) lse[((long)b * a + head) * s + q] = (m + log2f(l)) / LOG2E;
-            // the next item's sSum write is ordered after the other group's read
+            // the next item's sSum write is ordered after the other groups' reads
             // above by the named barrier of its first tile
         }
     }
@@ -1259,17 +1266,21 @@ static int persistent_grid(int items) { return items < num_sms() ? items : num_s
 
 template <int D>
 static int fwd5(const void* qkv, void* o, float* lse, int b, int s, int a, cudaStream_t st) {
+    // softmax column groups: 4 (16 softmax warps, 32 scores per thread) measured
+    // 3% slower than 2 at D = 128 (profiles/r2_attn_fwd_ng.jsonl)
+    constexpr int NG = 2;
     constexpr int TB = fa5::Tile<D>::BYTES;
-    constexpr int smem = 1024 + TB * 6 + 6 * 128 * 4 + 256;
+    constexpr int smem = 1024 + TB * 6 + 3 * NG * 128 * 4 + 256;
+    static_assert(smem <= 232448, "forward smem over the 227 KB limit");
     static PerDeviceOnce attr;
     if (attr.first()) {
-        cudaFuncSetAttribute(fa5::fwd2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(fa5::fwd2_kernel<D, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     }
     CUtensorMap m;
     if (map2d(&m, qkv, 3L * a * D, (long)b * s, 3L * a * D)) return -2;
     const int grid = persistent_grid(((s + 127) / 128) * a * b);
-    if (launch_k(fa5::fwd2_kernel<D>, dim3(grid), dim3(384), smem, st, 1, m, (bf16*)o, lse, s, a, b) !=
-        cudaSuccess)
+    if (launch_k(fa5::fwd2_kernel<D, NG>, dim3(grid), dim3(128 + 128 * NG), smem, st, 1, m, (bf16*)o, lse, s, a,
+                 b) != cudaSuccess)
         return -3;
     note_launches(1);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
