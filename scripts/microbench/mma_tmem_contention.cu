@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(384, 1) contention(int N, int mode, long long*
         long long t0 = clock64();
         if (elect_one()) {
             const uint64_t db0 = umma_desc_sw128(smem_u32(sm), 0, 1024);
-            if (mode < 3) {
+            if (mode < 3 || mode >= 5) {
                 for (int i = 0; i < ITER; ++i) {
                     const int k = i & 3;
                     umma_bf16_ts(tmem, tmem + 384 + 8 * k, db0 + 2 * k, id, i > 0);
@@ -82,6 +82,19 @@ __global__ void __launch_bounds__(384, 1) contention(int N, int mode, long long*
             out[blockIdx.x] = t1 - t0;
             done = 1;
         }
+    } else if (warp >= 4 && (mode == 5 || (mode == 6 && (warp & 3) != 0))) {
+        // ALU-heavy warps (softmax-like: packed FMAs + MUFU.EX2), mode 6 only on
+        // the three sub-partitions the MMA-issuing warp 0 does not use
+        float x0 = threadIdx.x * 1e-3f, x1 = x0 + 0.5f, acc = 0.f;
+        while (!done) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(x1) : "f"(x0));
+                x0 = fmaf(x1, 0.999f, -0.25f);
+                acc += x1;
+            }
+        }
+        if (acc == 1234.5f) out[gridDim.x] = 1;
     } else if (warp >= 4 && (mode == 1 || mode == 2 || mode == 4)) {
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
         const int cg = (warp - 4) >> 2;   // two column groups
@@ -116,10 +129,11 @@ int main() {
     cudaMalloc(&d, (sms + 1) * sizeof(long long));
     cudaFuncSetAttribute(contention, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
     static const char* names[] = {"mma_alone", "with_tmem_ld", "with_tmem_ld_st", "dq_pattern_alone",
-                                  "dq_pattern_with_tmem_ld_st"};
+                                  "dq_pattern_with_tmem_ld_st", "with_alu_warps_all_sps",
+                                  "with_alu_warps_other_sps"};
     for (int N : {64, 128})
-        for (int mode = 0; mode < 5; ++mode) {
-            if (mode >= 3 && N != 64) continue;
+        for (int mode = 0; mode < 7; ++mode) {
+            if ((mode == 3 || mode == 4) && N != 64) continue;
             contention<<<sms, 384, 66 * 1024>>>(N, mode, d);
             cudaError_t e = cudaDeviceSynchronize();
             if (e != cudaSuccess) {
