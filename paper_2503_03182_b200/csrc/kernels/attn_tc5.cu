@@ -390,6 +390,26 @@ __global__ void __launch_bounds__(128 + 128 * NG, 1)
                 }
             }
         }
+#ifdef TPIPE_ATTN_TRACE
+    } else if (warp == 3 || warp == 2) {
+        // trace build only: observers stamping when S_g (warp 3) / PV_g (warp 2)
+        // complete on the tensor pipe, independent of the softmax warps
+        int g = 0;
+        for (int k = 0;; ++k) {
+            const int t = sched_item(k, T);
+            if (t < 0) break;
+            const int nkb = nqb - t / (a * nb);
+            for (int j = 0; j < nkb; ++j, ++g) {
+                if (warp == 3) {
+                    mbar_wait(&s_full[g & 1], (g >> 1) & 1);
+                    if (lane == 0) TR(24, g);
+                } else {
+                    mbar_wait(pv_done, g & 1);
+                    if (lane == 0) TR(25, g);
+                }
+            }
+        }
+#endif
     } else if (warp >= 4) {
         // 4 NG softmax warps: row r = TMEM lane (warp % 4 = lane quarter); column
         // group cg owns scores [SC cg, SC (cg+1)) and O columns [cg D/NG, (cg+1) D/NG)

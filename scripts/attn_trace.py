@@ -18,7 +18,7 @@ _lib.LIB_PATH = os.path.join(ROOT, "paper_2503_03182_b200", "libtpipe_trace.so")
 from paper_2503_03182_b200 import kernels as K  # noqa: E402
 
 b, s, a, d = (int(x) for x in sys.argv[1:5]) if len(sys.argv) > 4 else (1, 2048, 16, 128)
-TR_N, NEV = 512, 24
+TR_N, NEV = 512, 26
 h = a * d
 torch.manual_seed(0)
 qkv = torch.randn((b * s, 3 * h), device="cuda").to(torch.bfloat16)
@@ -67,8 +67,9 @@ def report(name, evs, labels):
 
 
 res = {}
-fw = report("fwd2", [0, 1, 3, 4, 5, 6, 7, 2],
-            {0: "Kload", 1: "S_iss", 3: "S_seen", 4: "max_st", 5: "P_st", 6: "pfull0", 7: "pfull7", 2: "PV_iss"})
+fw = report("fwd2", [0, 1, 24, 3, 4, 5, 6, 7, 2, 25],
+            {0: "Kload", 1: "S_iss", 24: "S_done", 3: "S_seen", 4: "max_st", 5: "P_st", 6: "pfull0", 7: "pfull7",
+             2: "PV_iss", 25: "PV_done"})
 kv = report("dkdv2", [8, 9, 11, 12, 13, 14, 15, 10],
             {8: "Qload", 9: "S_iss", 11: "ld_seen", 12: "S_seen", 13: "ld_done", 14: "pfull0", 15: "pfull7",
              10: "G_iss"})

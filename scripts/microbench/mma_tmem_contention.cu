@@ -14,7 +14,7 @@
 
 using namespace tpipe;
 
-constexpr int ITER = 4096;
+constexpr int ITER = 65536;   // long enough (~2 ms per CTA) for the power state to settle
 
 __device__ __forceinline__ void tld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile(
@@ -29,17 +29,19 @@ __device__ __forceinline__ void tld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-__global__ void __launch_bounds__(384, 1) contention(int N, int mode, long long* out) {
+__global__ void __launch_bounds__(384, 1) contention(int N, int mode, long long* out, const uint8_t* gsrc) {
     extern __shared__ uint8_t smraw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t bar;
+    __shared__ uint64_t bar, bar2, bar3;
     __shared__ uint32_t slot;
     __shared__ volatile int done;
-    for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x)
+    for (int i = threadIdx.x; i < 96 * 1024 / 4; i += blockDim.x)
         reinterpret_cast<uint32_t*>(sm)[i] = 0x3c003c00u ^ (i * 2654435761u & 0x00ff00ffu);
     const int warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
+        mbar_init(&bar2, 1);
+        mbar_init(&bar3, 1);
         fence_mbar_init();
         done = 0;
     }
@@ -54,7 +56,33 @@ __global__ void __launch_bounds__(384, 1) contention(int N, int mode, long long*
         long long t0 = clock64();
         if (elect_one()) {
             const uint64_t db0 = umma_desc_sw128(smem_u32(sm), 0, 1024);
-            if (mode < 3 || mode >= 5) {
+            if (mode == 7 || mode == 8 || mode == 9 || mode == 10) {
+                // the forward kernel's pattern (D = 128): per tile, S = Q K^T (8 TS
+                // MMAs, A = Q in TMEM [384, 448), B = K K-major in 2 swizzle atoms of
+                // 64 d x 128 keys) into S buffer (tile & 1) * 128, then O += P V (8
+                // TS MMAs, A = P packed in the other S buffer, B = V MN-major), a
+                // commit after each group (mode 8: + a second commit, as the kernel)
+                const uint32_t idS = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+                const uint32_t idO = idS | (1u << 16);   // B MN-major
+                const uint32_t aK = smem_u32(sm), aV = smem_u32(sm + 32768);
+                for (int tile = 0; tile < ITER / 16; ++tile) {
+                    const uint32_t tS = tmem + (tile & 1) * 128;
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk)
+                        umma_bf16_ts(tS, tmem + 384 + kk * 8,
+                                     umma_desc_sw128(aK + (kk >> 2) * (128 * 128) + (kk & 3) * 32, 0, 1024), idS,
+                                     kk > 0);
+                    umma_commit(&bar2);
+                    if (mode == 8) umma_commit(&bar3);
+                    const uint32_t tP = tmem + ((tile + 1) & 1) * 128;
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk)
+                        umma_bf16_ts(tmem + 256, tP + kk * 8, umma_desc_sw128(aV + kk * 2048, 128 * 128, 1024), idO,
+                                     (tile | kk) > 0);
+                    umma_commit(&bar2);
+                    if (mode == 8) umma_commit(&bar3);
+                }
+            } else if (mode < 3 || mode >= 5) {
                 for (int i = 0; i < ITER; ++i) {
                     const int k = i & 3;
                     umma_bf16_ts(tmem, tmem + 384 + 8 * k, db0 + 2 * k, id, i > 0);
@@ -82,7 +110,32 @@ __global__ void __launch_bounds__(384, 1) contention(int N, int mode, long long*
             out[blockIdx.x] = t1 - t0;
             done = 1;
         }
-    } else if (warp >= 4 && (mode == 5 || (mode == 6 && (warp & 3) != 0))) {
+    } else if (warp == 3 && (mode == 9 || mode == 10)) {
+        // a TMA-like producer: 32 KB bulk copies global -> shared (the
+        // forward's K / V tile loads, ~64 KB per 2000 cycles), back to back
+        __shared__ uint64_t cbar;
+        if (threadIdx.x == 96) {
+            mbar_init(&cbar, 1);
+            fence_mbar_init();
+        }
+        __syncwarp();
+        uint32_t ph = 0;
+        long off = (long)blockIdx.x * 65536;
+        while (!done) {
+            if (threadIdx.x == 96) {
+                mbar_arrive_expect_tx(&cbar, 32768);
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 32768, [%2];" ::"r"(
+                        smem_u32(sm + 65536)),
+                    "l"(gsrc + off), "r"(smem_u32(&cbar))
+                    : "memory");
+            }
+            __syncwarp();
+            mbar_wait(&cbar, ph);
+            ph ^= 1;
+            off = (off + 32768) % (64L << 20);
+        }
+    } else if (warp >= 4 && (mode == 5 || mode == 10 || (mode == 6 && (warp & 3) != 0))) {
         // ALU-heavy warps (softmax-like: packed FMAs + MUFU.EX2), mode 6 only on
         // the three sub-partitions the MMA-issuing warp 0 does not use
         float x0 = threadIdx.x * 1e-3f, x1 = x0 + 0.5f, acc = 0.f;
@@ -127,14 +180,18 @@ int main() {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     long long* d;
     cudaMalloc(&d, (sms + 1) * sizeof(long long));
-    cudaFuncSetAttribute(contention, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
+    uint8_t* gsrc;
+    cudaMalloc(&gsrc, (64L << 20) + 65536L * 160);
+    cudaFuncSetAttribute(contention, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
     static const char* names[] = {"mma_alone", "with_tmem_ld", "with_tmem_ld_st", "dq_pattern_alone",
                                   "dq_pattern_with_tmem_ld_st", "with_alu_warps_all_sps",
-                                  "with_alu_warps_other_sps"};
+                                  "with_alu_warps_other_sps", "fwd_pattern", "fwd_pattern_2commits",
+                                  "fwd_pattern_with_bulk_copies", "fwd_pattern_bulk_copies_alu_warps"};
     for (int N : {64, 128})
-        for (int mode = 0; mode < 7; ++mode) {
+        for (int mode = 0; mode < 11; ++mode) {
             if ((mode == 3 || mode == 4) && N != 64) continue;
-            contention<<<sms, 384, 66 * 1024>>>(N, mode, d);
+            if (mode >= 7 && N != 128) continue;
+            contention<<<sms, 384, 100 * 1024>>>(N, mode, d, gsrc);
             cudaError_t e = cudaDeviceSynchronize();
             if (e != cudaSuccess) {
                 printf("error %s\n", cudaGetErrorString(e));
