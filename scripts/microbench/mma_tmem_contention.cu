@@ -8,6 +8,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2503_03182_b200/csrc \
 //        scripts/microbench/mma_tmem_contention.cu -o /tmp/mtc && /tmp/mtc
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "kernels/common.cuh"
@@ -175,7 +176,7 @@ __global__ void __launch_bounds__(384, 1) contention(int N, int mode, long long*
     }
 }
 
-int main() {
+int main(int argc, char** argv) {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     long long* d;
@@ -183,6 +184,34 @@ int main() {
     uint8_t* gsrc;
     cudaMalloc(&gsrc, (64L << 20) + 65536L * 160);
     cudaFuncSetAttribute(contention, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    if (argc > 1) {   // soak: mode argv[1] (N = 128) back to back for argv[2] seconds, report each launch
+        const int mode = atoi(argv[1]);
+        const double secs = argc > 2 ? atof(argv[2]) : 5.0;
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        double el = 0;
+        int it = 0;
+        while (el < secs * 1e3) {
+            cudaEventRecord(e0);
+            contention<<<sms, 384, 100 * 1024>>>(128, mode, d, gsrc);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            el += ms;
+            long long h[160];
+            cudaMemcpy(h, d, sms * sizeof(long long), cudaMemcpyDeviceToHost);
+            double avg = 0;
+            for (int i = 0; i < sms; ++i) avg += h[i];
+            avg /= sms;
+            if (it % 50 == 0)
+                printf("{\"mode\": %d, \"t_ms\": %.0f, \"cycles_per_mma\": %.1f, \"launch_ms\": %.3f}\n", mode, el,
+                       avg / ITER, ms);
+            ++it;
+        }
+        return 0;
+    }
     static const char* names[] = {"mma_alone", "with_tmem_ld", "with_tmem_ld_st", "dq_pattern_alone",
                                   "dq_pattern_with_tmem_ld_st", "with_alu_warps_all_sps",
                                   "with_alu_warps_other_sps", "fwd_pattern", "fwd_pattern_2commits",
