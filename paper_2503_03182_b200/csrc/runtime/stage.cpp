@@ -352,7 +352,10 @@ uint64_t fwd_ws_bytes(const Dims& D, const StashLayout& SL, bool head) {
 struct SideStream {
     int dev = 0;
     cudaStream_t main = nullptr, aux = nullptr;
-    cudaEvent_t ev[5] = {};
+    // ev[0..4]: within a layer; ev[5..7]: the aux stream's FC1 wgrad, out-proj
+    // wgrad and QKV wgrad of a layer, waited on by the next layer's main-stream
+    // writers of the buffers they read (deferred join, layer_backward)
+    cudaEvent_t ev[8] = {};
 };
 static std::mutex g_side_mu;
 static std::vector<SideStream*> g_side;
@@ -413,12 +416,20 @@ static int stream_dep(cudaStream_t a, cudaStream_t b, cudaEvent_t e) {
 // Every buffer is written and read on one stream or ordered by an event
 // (the partial-sum workspace is used on main only; dy is read by fc2 wgrad on
 // aux before LN1 bwd overwrites it on main: ev[2]).
+// wait_prev: the previous layer's backward deferred its join (its aux-stream
+// weight gradients may still run): wait for the ones that read a buffer this
+// layer's main stream is about to overwrite (w.du / w.g, w.G1, w.dqkv).
+// defer_join: leave this layer's aux work running into the next layer's
+// backward (the next layer must be called with wait_prev) instead of joining.
 static int layer_backward(const Dims& D, const LW& W, const LayerPtrs& lp, const void* dy, void* dx,
-                          const BwdWs& w, cudaStream_t st) {
+                          const BwdWs& w, cudaStream_t st, bool wait_prev = false, bool defer_join = false) {
     const int M = D.M, h = D.h, f = D.f, dt = D.dtype;
     SideStream* ss = (g_side_stream_enabled && !profiler().on) ? side_stream(st) : nullptr;
     const cudaStream_t ax = ss ? ss->aux : st;
     cudaEvent_t* ev = ss ? ss->ev : nullptr;
+    if (!ss) wait_prev = defer_join = false;
+    // (previous layer's FC2 / FC1 wgrads read w.g / w.du, written next)
+    if (wait_prev && cudaStreamWaitEvent(st, ev[5], 0) != cudaSuccess) return -3;
     // FC2: dg = dy W2 (dGELU fused: du = dg * gelu'(u), g = gelu(u) recomputed)
     TRY(mm(D, M, f, h, dy, h, 1, W.w[W_2], f, 0, EPI_DGELU, w.du, f, nullptr, nullptr, 0, w.g, f,
            lp.u, f, st));
@@ -433,6 +444,7 @@ static int layer_backward(const Dims& D, const LW& W, const LayerPtrs& lp, const
     }
     TRY(mm(D, f, h, M, w.du, f, 0, w.ln, h, 0, EPI_ACC_F32, W.g[W_1], h, nullptr, nullptr, 0,
            nullptr, 0, nullptr, 0, ax));
+    if (defer_join && cudaEventRecord(ev[5], ax) != cudaSuccess) return -3;
     // ---- main: data-gradient chain. bf16: the b1 column partials and LN2's
     // (gamma, beta, b2) partials sit side by side in w.part and are reduced by
     // one launch after the LN2 backward (same per-column order)
@@ -448,6 +460,8 @@ static int layer_backward(const Dims& D, const LW& W, const LayerPtrs& lp, const
     }
     TRY(mm(D, M, h, f, w.du, f, 1, W.w[W_1], h, 0, EPI_STORE, w.dln, h, nullptr, nullptr, 0,
            nullptr, 0, nullptr, 0, st));
+    // (previous layer's out-proj wgrad reads w.G1, written next)
+    if (wait_prev && cudaStreamWaitEvent(st, ev[6], 0) != cudaSuccess) return -3;
     {
         ProfScope _ps(3, 0.0, st);
         // + dB2 = colsum(dy), fused (dy is LN2's residual-branch gradient)
@@ -472,6 +486,7 @@ static int layer_backward(const Dims& D, const LW& W, const LayerPtrs& lp, const
     if (ss) TRY(stream_dep(st, ax, ev[2]));
     TRY(mm(D, h, h, M, w.G1, h, 0, lp.o, h, 0, EPI_ACC_F32, W.g[W_O], h, nullptr, nullptr, 0,
            nullptr, 0, nullptr, 0, ax));
+    if (defer_join && cudaEventRecord(ev[6], ax) != cudaSuccess) return -3;
     // main: out-proj dgrad, attention backward (P recomputed from LSE). On the
     // tcgen05 path the dgrad GEMM's epilogue also produces the backward's
     // D = rowsum(dO o O) per (token, head) (EPI_STORE_DOT): no separate pass
@@ -489,6 +504,8 @@ static int layer_backward(const Dims& D, const LW& W, const LayerPtrs& lp, const
         TRY(mm(D, M, h, h, w.G1, h, 1, W.w[W_O], h, 0, EPI_STORE, w.dout, h, nullptr, nullptr, 0,
                nullptr, 0, nullptr, 0, st));
     }
+    // (previous layer's QKV wgrad reads w.dqkv, written next)
+    if (wait_prev && cudaStreamWaitEvent(st, ev[7], 0) != cudaSuccess) return -3;
     {
         // algorithmic: P recompute + dV, dP, dQ, dK = 5 GEMMs over the causal triangle
         ProfScope ps(2, 10.0 * D.b * D.a * (0.5 * D.s * (D.s + 1)) * D.hd, st);
@@ -498,6 +515,7 @@ static int layer_backward(const Dims& D, const LW& W, const LayerPtrs& lp, const
     // aux: QKV weight gradient
     TRY(mm(D, 3 * h, h, M, w.dqkv, 3 * h, 0, w.ln, h, 0, EPI_ACC_F32, W.g[W_QKV], h, nullptr,
            nullptr, 0, nullptr, 0, nullptr, 0, ax));
+    if (defer_join && cudaEventRecord(ev[7], ax) != cudaSuccess) return -3;
     // main: QKV bias / dgrad, LN1 backward (bqkv and LN1's (gamma, beta, bo)
     // partials reduced together, as above)
     float* part_q = w.part + nb16 * 3 * h;
@@ -530,7 +548,8 @@ static int layer_backward(const Dims& D, const LW& W, const LayerPtrs& lp, const
         }
     }
     // join: the layer's gradients are complete and w.* free for the next layer
-    if (ss) TRY(stream_dep(ax, st, ev[4]));
+    // (deferred: the next layer waits on ev[5..7] where it needs to)
+    if (ss && !defer_join) TRY(stream_dep(ax, st, ev[4]));
     return 0;
 }
 
@@ -646,6 +665,7 @@ int chunk_backward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P
         }
         dy = w.G0;
     }
+    bool prev_deferred = false;
     for (int l = n - 1; l >= 0; --l) {
         LayerPtrs lp;
         if (l < SL.ckpt_layers) {
@@ -657,7 +677,13 @@ int chunk_backward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P
             lp = layer_ptrs(SL.layer[l], stash_base(SL, a.stash, a.stash2, a.split, l), a.in);
         }
         void* dx = (l > 0 || lay.emb) ? w.G0 : a.gout;
-        TRY(layer_backward(D, layer_w(D, P, l), lp, dy, dx, w, st));
+        // the join of a layer's aux-stream weight gradients is deferred into the
+        // next layer's backward unless that layer recomputes its internals first
+        // (the recompute forward writes w.ln / w.g, which they read) or this is
+        // the chunk's last layer
+        const bool defer = l > 0 && l - 1 >= SL.ckpt_layers;
+        TRY(layer_backward(D, layer_w(D, P, l), lp, dy, dx, w, st, prev_deferred, defer));
+        prev_deferred = defer;
         dy = w.G0;
     }
     if (lay.emb)
