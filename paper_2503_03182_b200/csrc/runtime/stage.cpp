@@ -354,8 +354,9 @@ struct SideStream {
     cudaStream_t main = nullptr, aux = nullptr;
     // ev[0..4]: within a layer; ev[5..7]: the aux stream's FC1 wgrad, out-proj
     // wgrad and QKV wgrad of a layer, waited on by the next layer's main-stream
-    // writers of the buffers they read (deferred join, layer_backward)
-    cudaEvent_t ev[8] = {};
+    // writers of the buffers they read (deferred join, layer_backward); ev[8]:
+    // dlogits ready for the LM-head weight gradient on aux (chunk_backward)
+    cudaEvent_t ev[9] = {};
 };
 static std::mutex g_side_mu;
 static std::vector<SideStream*> g_side;
@@ -603,6 +604,7 @@ int chunk_backward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P
     BwdWs w = carve_bwd(D, a.ws, lay.head, lay.emb, part_elems(D), SL.ckpt_only ? SL.scratch_bytes : 0);
     const uint8_t* wb = reinterpret_cast<const uint8_t*>(P.w);
     const void* dy = a.gin;
+    bool head_on_aux = false;
     if (lay.head) {
         const void* ln_g = wb + lay.lnf_g * D.es;
         {
@@ -653,8 +655,16 @@ int chunk_backward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P
             TRY(ce_fwd(w.logits, a.targets, lse, a.loss_slot, a.loss_scale, M, D.V, st));
             TRY(ce_bwd(D.dtype, w.logits, a.targets, lse, w.dlogits, a.loss_scale, M, D.V, st));
         }
+        // LM-head weight gradient on the side stream, concurrent with the head's
+        // data gradient (a single wave of 64 CTA-pair tiles with a 50K-deep K
+        // loop leaves 10 of 74 pairs idle); dlogits / lnf are head-only
+        // workspace, untouched until the chunk's final join
+        SideStream* hs = (g_side_stream_enabled && !profiler().on) ? side_stream(st) : nullptr;
+        const cudaStream_t hax = hs ? hs->aux : st;
+        if (hs) TRY(stream_dep(st, hax, hs->ev[8]));
         TRY(mm(D, D.V, h, M, w.dlogits, D.V, 0, w.lnf, h, 0, EPI_ACC_F32, P.grad + lay.w_head, h,
-               nullptr, nullptr, 0, nullptr, 0, nullptr, 0, st));
+               nullptr, nullptr, 0, nullptr, 0, nullptr, 0, hax));
+        head_on_aux = hs != nullptr;
         TRY(mm(D, M, h, D.V, w.dlogits, D.V, 1, wh, h, 0, EPI_STORE, w.dlnf, h, nullptr, nullptr, 0,
                nullptr, 0, nullptr, 0, st));
         {
@@ -685,6 +695,11 @@ int chunk_backward(const Dims& D, const StashLayout& SL, const ChunkParamsDev& P
         TRY(layer_backward(D, layer_w(D, P, l), lp, dy, dx, w, st, prev_deferred, defer));
         prev_deferred = defer;
         dy = w.G0;
+    }
+    if (head_on_aux && n == 0) {   // no layer backward joined the side stream
+        SideStream* hs = side_stream(st);
+        if (!hs) return -3;
+        TRY(stream_dep(hs->aux, st, hs->ev[4]));
     }
     if (lay.emb)
         {
