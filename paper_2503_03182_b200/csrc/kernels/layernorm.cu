@@ -236,18 +236,24 @@ struct ReduceSegs {
     const float* src[4];
     float* out[4];
     int n[4];
+    int cb[5];   // first 32-column block of each segment in the flat grid (cb[nseg] = grid size)
 };
 __global__ void __launch_bounds__(256) reduce_segs_kernel(const ReduceSegs segs, int nblk) {
     pdl_wait();
     pdl_trigger();
     __shared__ float4 red[32][8];
-    const int t = blockIdx.y;
+    // flat grid over every segment's 32-column blocks (no idle CTAs for the
+    // narrower segments)
+    int t = 0;
+#pragma unroll
+    for (int i = 1; i < 4; ++i)
+        if ((int)blockIdx.x >= segs.cb[i] && segs.cb[i] < segs.cb[4]) t = i;
+    const int bx = blockIdx.x - segs.cb[t];
     const int n = segs.n[t];
-    if (blockIdx.x * 32 >= n) return;   // CTA-uniform
     const float* src = segs.src[t];
     float* out = segs.out[t];
     const int cg = threadIdx.x & 7, g = threadIdx.x >> 3;
-    const int col = blockIdx.x * 32 + cg * 4;
+    const int col = bx * 32 + cg * 4;
     float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
     if (col < n) {
 #pragma unroll 4
@@ -999,16 +1005,16 @@ int reduce_segments(const float* const* src, float* const* out, const int* n, in
                     cudaStream_t st) {
     if (nseg <= 0 || nseg > 4 || rows <= 0) return nseg == 0 ? 0 : -1;
     ReduceSegs sg{};
-    int maxn = 0;
     for (int i = 0; i < nseg; ++i) {
         if (n[i] % 4) return -1;
         sg.src[i] = src[i];
         sg.out[i] = out[i];
         sg.n[i] = n[i];
-        maxn = n[i] > maxn ? n[i] : maxn;
     }
     const int nb = (rows + RB - 1) / RB;
-    launch_k(reduce_segs_kernel, dim3((maxn + 31) / 32, nseg), dim3(256), 0, st, 1, sg, nb);
+    sg.cb[0] = 0;
+    for (int i = 0; i < 4; ++i) sg.cb[i + 1] = sg.cb[i] + (i < nseg ? (sg.n[i] + 31) / 32 : 0);
+    launch_k(reduce_segs_kernel, dim3(sg.cb[4]), dim3(256), 0, st, 1, sg, nb);
     note_launches(1);
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
